@@ -1,0 +1,426 @@
+#!/usr/bin/env python
+"""Dion2 optimizer-step benchmark (BASELINE.json metric).
+
+    python bench.py [--gpus N] [--steps K] [--warmup W] [--impl ours|reference]
+
+Workload (N = 1): BASELINE configs[1], the 1B-class transformer matrix set
+(24 layers of Wq, Wk, Wv, Wo 2048x2048, W_up 8192x2048, W_down 2048x8192;
+144 matrices, 1.208 B parameters), fp32 W / M / G, alpha = 0.25, auto axis,
+5 Newton-Schulz steps on the bf16 tcgen05 path.  One "step" = one Dion2
+update of every matrix (Alg. 1 over the whole model).  Synthetic data:
+W0 ~ N(0, 1/n), G ~ N(0, 1) from a seeded generator, M0 = 0.  The inputs
+(14.5 GB touched per step) are far larger than L2 (126 MB), so no flush is
+needed between steps.  The same library at alpha = 1 (full Muon) is timed
+beside it, as is the fp64 oracle on the host cores (cpu_baseline).
+
+Prints ONE JSON line (rank 0).
+"""
+from __future__ import annotations
+
+import argparse
+import json
+import math
+import os
+import subprocess
+import sys
+import threading
+import time
+
+ROOT = os.path.dirname(os.path.abspath(__file__))
+sys.path.insert(0, ROOT)
+
+import numpy as np  # noqa: E402
+
+PEAKS_FALLBACK = {"hbm_gbs": 6650.0, "bf16_tflops": 1590.0, "bf16_tflops_sustained": 1400.0}
+
+
+def load_peaks():
+    p = os.path.join(ROOT, "MEASURED_PEAKS.json")
+    if os.path.exists(p):
+        with open(p) as f:
+            d = json.load(f)
+        return d, "measured"
+    return PEAKS_FALLBACK, "fallback"
+
+
+def model_shapes(name: str):
+    from synth import layer_set_1b, layer_set_8b
+    if name == "1b":
+        return layer_set_1b(24)
+    if name == "1b16":
+        return layer_set_1b(16)
+    if name == "8b":
+        return layer_set_8b(32)
+    raise ValueError(name)
+
+
+def work_model(shapes, alpha, steps=5):
+    """Algorithmic work per Dion2 step: NS FLOPs T(4p^2 q + 2p^3) and
+    per-phase algorithmic HBM bytes."""
+    ns_flops = {"ns_gram": 0.0, "ns_poly": 0.0, "ns_apply": 0.0}
+    byts = {"momentum_score": 0.0, "gather": 0.0, "scatter": 0.0}
+    for (m, n) in shapes:
+        rows = m <= n
+        d, o = (m, n) if rows else (n, m)
+        k = max(1, min(d, int(math.floor(alpha * d + 0.5))))
+        p, q = min(k, o), max(k, o)
+        ns_flops["ns_gram"] += steps * 2.0 * p * p * q
+        ns_flops["ns_poly"] += steps * 2.0 * p ** 3
+        ns_flops["ns_apply"] += steps * 2.0 * p * p * q
+        byts["momentum_score"] += m * n * 12.0 + d * 4.0       # read G, read M, write M, write scores
+        byts["gather"] += k * o * (4.0 + 4.0 + 2.0)           # read M[K], write mu*M[K], write bf16 X
+        byts["scatter"] += k * o * (2.0 + 4.0 + 4.0)          # read bf16 O, read+write W[K]
+    return ns_flops, byts
+
+
+class ClockSampler:
+    """nvidia-smi clocks / throttle reasons sampled DURING the timed region."""
+
+    FIELDS = "clocks.sm,clocks.max.sm,power.draw,clocks_event_reasons.active,clocks_event_reasons.hw_slowdown," \
+             "clocks_event_reasons.hw_thermal_slowdown,clocks_event_reasons.sw_thermal_slowdown," \
+             "clocks_event_reasons.sw_power_cap"
+
+    def __init__(self, index: int):
+        self.index = index
+        self.proc = None
+        self.lines = []
+
+    def __enter__(self):
+        try:
+            self.proc = subprocess.Popen(["nvidia-smi", "-i", str(self.index), f"--query-gpu={self.FIELDS}",
+                                          "--format=csv,noheader,nounits", "-lms", "100"],
+                                         stdout=subprocess.PIPE, stderr=subprocess.DEVNULL, text=True)
+            self.t = threading.Thread(target=self._read, daemon=True)
+            self.t.start()
+        except OSError:
+            self.proc = None
+        time.sleep(0.25)
+        return self
+
+    def _read(self):
+        for line in self.proc.stdout:
+            self.lines.append(line.strip())
+
+    def __exit__(self, *a):
+        if self.proc is not None:
+            time.sleep(0.15)
+            self.proc.terminate()
+            try:
+                self.proc.wait(timeout=5)
+            except subprocess.TimeoutExpired:
+                self.proc.kill()
+
+    def summary(self):
+        sm, mx, reasons = [], [], set()
+        names = ["hw_slowdown", "hw_thermal_slowdown", "sw_thermal_slowdown", "sw_power_cap"]
+        for ln in self.lines:
+            parts = [x.strip() for x in ln.split(",")]
+            if len(parts) < 8:
+                continue
+            try:
+                sm.append(float(parts[0]))
+                mx.append(float(parts[1]))
+            except ValueError:
+                continue
+            for nm, v in zip(names, parts[4:8]):
+                if v.lower().startswith("active"):
+                    reasons.add(nm)
+        if not sm:
+            return {"sm_mhz": None, "sm_max_mhz": None, "reasons": ["unsampled"]}
+        return {"sm_mhz": float(np.median(sm)), "sm_max_mhz": max(mx), "reasons": sorted(reasons), "samples": len(sm)}
+
+
+# ---------------------------------------------------------------------------------- our arm
+
+def build_state(shapes, device, seed=0):
+    """Flat fp32 W / M / G buffers with one row-major view per matrix."""
+    import torch
+    total = sum(m * n for m, n in shapes)
+    gen = torch.Generator(device=device)
+    gen.manual_seed(seed)
+    W = torch.empty(total, dtype=torch.float32, device=device)
+    G = torch.empty(total, dtype=torch.float32, device=device)
+    M = torch.zeros(total, dtype=torch.float32, device=device)
+    W.normal_(0.0, 1.0, generator=gen)
+    G.normal_(0.0, 1.0, generator=gen)
+    Ws, Ms, Gs, off = [], [], [], 0
+    for (m, n) in shapes:
+        Ws.append(W[off:off + m * n].view(m, n).mul_(1.0 / math.sqrt(n)))
+        Ms.append(M[off:off + m * n].view(m, n))
+        Gs.append(G[off:off + m * n].view(m, n))
+        off += m * n
+    return (W, M, G), Ws, Ms, Gs
+
+
+def time_steps(opt, Ws, Ms, Gs, steps, warmup, dist_barrier=None):
+    import torch
+    for _ in range(warmup):
+        opt.step(Ws, Ms, Gs)
+    torch.cuda.synchronize()
+    if dist_barrier:
+        dist_barrier()
+    torch.cuda.synchronize()
+    s = torch.cuda.current_stream()
+    e0, e1 = torch.cuda.Event(enable_timing=True), torch.cuda.Event(enable_timing=True)
+    e0.record(s)
+    for _ in range(steps):
+        opt.step(Ws, Ms, Gs)
+    e1.record(s)
+    torch.cuda.synchronize()
+    if dist_barrier:
+        dist_barrier()
+    return e0.elapsed_time(e1) / steps
+
+
+def cpu_oracle_baseline(shapes, alpha, budget_s=20.0):
+    """Time the fp64 oracle (as it stands) on a bounded sample of the workload:
+    whole layers (6 matrices each) until ~budget_s; scaled to ms per model step."""
+    import oracle as O
+    from synth import gen_grad, gen_w0
+    per_layer = 6
+    layers = len(shapes) // per_layer
+    cfg = O.OracleConfig(alpha=alpha)
+    t_used, done = 0.0, 0
+    for L in range(layers):
+        mats = shapes[L * per_layer:(L + 1) * per_layer]
+        data = [(gen_w0(m, n, 0, L * per_layer + i).astype(np.float64), np.zeros((m, n)),
+                 gen_grad(m, n, 0, L * per_layer + i, 0).astype(np.float64)) for i, (m, n) in enumerate(mats)]
+        t0 = time.perf_counter()
+        for (W, M, G) in data:
+            O.dion2_step(W, M, G, cfg)
+        t_used += time.perf_counter() - t0
+        done += 1
+        if t_used >= budget_s:
+            break
+    ms_model = t_used / done * layers * 1e3
+    cores = len(os.sched_getaffinity(0))
+    return {"value": ms_model, "unit": "ms/step", "cores": cores, "kind": "oracle",
+            "sample": f"{done} of {layers} layers ({done * per_layer} matrices) at alpha={alpha}, one step, "
+                      f"fp64 NumPy; scaled x{layers / done:.1f} to the whole model"}
+
+
+def e2e_run(opt, Ws, Ms, Gs, G_flat, steps):
+    """End to end through the public API: pinned host G -> device, the step, and the
+    selected index sets + status word read back, every step, inside the timed region."""
+    import torch
+    from paper_2512_16928_b200 import dion2 as D
+    host_G = torch.empty(G_flat.numel(), dtype=torch.float32, pin_memory=True)
+    host_G.copy_(G_flat.cpu())
+    ks = []
+    for W in Ws:
+        m, n = W.shape
+        d = m if m <= n else n
+        ks.append(max(1, min(d, int(math.floor(float(np.float32(opt.cfg_kw.get("alpha", 0.25))) * d + 0.5)))))
+    sel_dev = torch.empty(sum(ks), dtype=torch.int32, device=G_flat.device)
+    sel_views, off = [], 0
+    for k in ks:
+        sel_views.append(sel_dev[off:off + k])
+        off += k
+    sel_host = torch.empty(sum(ks), dtype=torch.int32, pin_memory=True)
+    torch.cuda.synchronize()
+    s = torch.cuda.current_stream()
+    e0, e1 = torch.cuda.Event(enable_timing=True), torch.cuda.Event(enable_timing=True)
+    e0.record(s)
+    for _ in range(steps):
+        G_flat.copy_(host_G, non_blocking=True)
+        opt.step(Ws, Ms, Gs, sel_out=sel_views)
+        sel_host.copy_(sel_dev, non_blocking=True)
+    e1.record(s)
+    torch.cuda.synchronize()
+    rc, _ = opt.status()
+    return e0.elapsed_time(e1) / steps, G_flat.numel() * 4, sum(ks) * 4, rc
+
+
+def run_ours(args):
+    import torch
+    import torch.distributed as dist
+    from paper_2512_16928_b200 import Dion2, get_phase_times, last_launch_count, set_phase_timing
+
+    world = int(os.environ.get("WORLD_SIZE", "1"))
+    rank = int(os.environ.get("RANK", "0"))
+    local = int(os.environ.get("LOCAL_RANK", "0"))
+    if world > 1:
+        dist.init_process_group("nccl")
+    torch.cuda.set_device(local)
+    dev = torch.device("cuda", local)
+    barrier = (lambda: dist.barrier()) if world > 1 else None
+
+    shapes = model_shapes(args.config)
+    n_params = sum(m * n for m, n in shapes)
+    bufs, Ws, Ms, Gs = build_state(shapes, dev, seed=rank)
+    opt = Dion2(alpha=args.alpha, axis="auto", precision="bf16")
+
+    with ClockSampler(local) as clk:
+        ms = time_steps(opt, Ws, Ms, Gs, args.steps, args.warmup, barrier)
+    launches = last_launch_count() * args.steps
+    rc, bad = opt.status()
+    if rc != 0:
+        raise RuntimeError(f"status {rc} (matrix {bad})")
+
+    # per-phase device time (CUDA events on the launching stream around every launch)
+    set_phase_timing(True)
+    ms_timed = time_steps(opt, Ws, Ms, Gs, args.steps, 0, None)
+    phases = get_phase_times()
+    set_phase_timing(False)
+
+    peaks, peak_src = load_peaks()
+    ns_flops, byts = work_model(shapes, args.alpha)
+    per_phase = {}
+    for name, (t_ms, cnt) in phases.items():
+        if cnt == 0:
+            continue
+        t = t_ms / args.steps
+        ent = {"ms_per_step": t, "launches_per_step": cnt / args.steps}
+        if name in ns_flops:
+            ent["tflops"] = ns_flops[name] / (t * 1e-3) / 1e12
+            ent["frac_bf16_burst"] = ent["tflops"] / peaks["bf16_tflops"]
+        if name in byts:
+            ent["gbs"] = byts[name] / (t * 1e-3) / 1e9
+            ent["frac_hbm"] = ent["gbs"] / peaks["hbm_gbs"]
+        per_phase[name] = ent
+    ns_ms = sum(per_phase[p]["ms_per_step"] for p in ns_flops if p in per_phase)
+    ns_total = sum(ns_flops.values())
+    ns_tflops = ns_total / (ns_ms * 1e-3) / 1e12 if ns_ms > 0 else 0.0
+    # dominant kernel (largest per-step device time)
+    dom = max(per_phase, key=lambda p: per_phase[p]["ms_per_step"])
+    de = per_phase[dom]
+    if dom in ns_flops:
+        roof = {"kernel": dom, "bound": "tensor", "achieved": de["tflops"], "peak": peaks["bf16_tflops"],
+                "unit": "TFLOP/s", "frac": de["frac_bf16_burst"], "traffic": None,
+                "per_launch": f"{ns_flops[dom] / de['launches_per_step'] / 1e12:.4f} TFLOP"}
+    else:
+        roof = {"kernel": dom, "bound": "hbm", "achieved": de["gbs"], "peak": peaks["hbm_gbs"], "unit": "GB/s",
+                "frac": de["frac_hbm"], "traffic": None,
+                "per_launch": f"{byts[dom] / de['launches_per_step'] / 1e9:.3f} GB"}
+    roof["peak_source"] = f"MEASURED_PEAKS.json ({peak_src}, burst)"
+    roof["timing"] = "CUDA events around each launch on the launching stream, separate K-step pass"
+    trafp = os.path.join(ROOT, "profiles", "traffic.json")
+    if os.path.exists(trafp):
+        with open(trafp) as f:
+            tr = json.load(f)
+        if dom in tr:
+            roof["traffic"] = tr[dom]
+
+    # alpha = 1 (full Muon, same library)
+    ms_a1 = None
+    if not args.no_alpha1 and args.alpha != 1.0:
+        del opt
+        torch.cuda.empty_cache()
+        opt1 = Dion2(alpha=1.0, axis="auto", precision="bf16")
+        ms_a1 = time_steps(opt1, Ws, Ms, Gs, max(2, min(args.steps, 5)), max(1, min(args.warmup, 2)), barrier)
+        del opt1
+        torch.cuda.empty_cache()
+        opt = Dion2(alpha=args.alpha, axis="auto", precision="bf16")
+        opt.step(Ws, Ms, Gs)
+
+    # end to end through the public API (host G)
+    e2e_ms, h2d, d2h, rc2 = e2e_run(opt, Ws, Ms, Gs, bufs[2], max(2, min(args.steps, 5)))
+
+    # max over ranks
+    if world > 1:
+        t = torch.tensor([ms, e2e_ms], device=dev)
+        dist.all_reduce(t, op=dist.ReduceOp.MAX)
+        ms, e2e_ms = t.tolist()
+
+    cpu = None
+    if rank == 0 and world == 1 and not args.no_cpu:
+        cpu = cpu_oracle_baseline(shapes, args.alpha, budget_s=args.cpu_budget)
+
+    if rank == 0:
+        out = {
+            "metric": "Dion2 optimizer-step ms per model at alpha=0.25 vs alpha=1; NS tensor-peak fraction",
+            "value": ms if world == 1 else ms / world,
+            "unit": "ms/step",
+            "n_gpus": world,
+            "steps": args.steps,
+            "warmup": args.warmup,
+            "ms_per_step": ms,
+            "higher_is_better": False,
+            "scaling": "weak",
+            "vs_baseline": None,
+            "dtype": "f32 state / bf16 NS",
+            "data": "synthetic (W0~N(0,1/n), G~N(0,1), M0=0; seeded device RNG)",
+            "config": {"workload": f"{args.config}-set Dion2 step (configs[1])", "matrices": len(shapes),
+                       "params": n_params, "alpha": args.alpha, "axis": "auto", "ns_steps": 5,
+                       "l2_flush": "not needed: 14.5 GB touched per step >> 126 MB L2",
+                       "parallelism": "single GPU" if world == 1 else f"{world} independent replicas"},
+            "alpha1_ms_per_step": ms_a1,
+            "speedup_vs_alpha1": (ms_a1 / ms) if ms_a1 else None,
+            "ns_tflops": ns_tflops,
+            "ns_frac_bf16_burst": ns_tflops / peaks["bf16_tflops"],
+            "ns_frac_bf16_sustained": ns_tflops / peaks["bf16_tflops_sustained"],
+            "ms_per_step_with_phase_events": ms_timed,
+            "phases": per_phase,
+            "roofline": roof,
+            "cpu_baseline": cpu,
+            "e2e": {"value": e2e_ms, "unit": "ms/step", "h2d_bytes_per_step": h2d, "d2h_bytes_per_step": d2h,
+                    "what": "pinned host G -> device, dion2_step_batched, selected indices -> host, every step"},
+            "gpu_launches": launches,
+            "clocks": clk.summary(),
+        }
+        print(json.dumps(out))
+    if world > 1:
+        dist.destroy_process_group()
+
+
+# ---------------------------------------------------------------------------------- reference arm
+
+def run_reference(args):
+    """The reference arm for this tier is the fp64 oracle on the host cores, on our
+    arm's config/metric: each step is a bounded sample (one transformer layer of the
+    set), reported scaled to ms per whole-model step."""
+    rank = int(os.environ.get("RANK", "0"))
+    world = int(os.environ.get("WORLD_SIZE", "1"))
+    if rank != 0:
+        return
+    import oracle as O
+    from synth import gen_grad, gen_w0
+    shapes = model_shapes(args.config)
+    layer = shapes[:6]
+    layers = len(shapes) // 6
+    cfg = O.OracleConfig(alpha=args.alpha)
+    data = [(gen_w0(m, n, 0, i).astype(np.float64), np.zeros((m, n)), gen_grad(m, n, 0, i, 0).astype(np.float64))
+            for i, (m, n) in enumerate(layer)]
+    for _ in range(args.warmup):
+        for (W, M, G) in data:
+            O.dion2_step(W, M, G, cfg)
+    t0 = time.perf_counter()
+    for _ in range(args.steps):
+        for (W, M, G) in data:
+            O.dion2_step(W, M, G, cfg)
+    dt = (time.perf_counter() - t0) / args.steps
+    ms = dt * layers * 1e3
+    cores = len(os.sched_getaffinity(0))
+    out = {"impl": "reference",
+           "metric": "Dion2 optimizer-step ms per model at alpha=0.25 vs alpha=1; NS tensor-peak fraction",
+           "value": ms, "unit": "ms/step", "n_gpus": world, "steps": args.steps, "warmup": args.warmup,
+           "ms_per_step": ms, "higher_is_better": False, "scaling": "weak", "vs_baseline": None, "dtype": "f64",
+           "data": "synthetic (W0~N(0,1/n), G~N(0,1), M0=0; seeded host RNG)",
+           "config": {"workload": f"{args.config}-set Dion2 step (configs[1])", "alpha": args.alpha, "axis": "auto",
+                      "ns_steps": 5},
+           "cpu_baseline": {"value": ms, "unit": "ms/step", "cores": cores, "kind": "oracle",
+                            "sample": f"1 of {layers} layers (6 matrices) per step, fp64 NumPy, scaled x{layers}"},
+           "e2e": {"value": ms, "unit": "ms/step", "h2d_bytes_per_step": 0, "d2h_bytes_per_step": 0}}
+    print(json.dumps(out))
+
+
+def main():
+    ap = argparse.ArgumentParser()
+    ap.add_argument("--gpus", type=int, default=1)
+    ap.add_argument("--steps", type=int, default=10)
+    ap.add_argument("--warmup", type=int, default=3)
+    ap.add_argument("--impl", choices=["ours", "reference"], default="ours")
+    ap.add_argument("--alpha", type=float, default=0.25)
+    ap.add_argument("--config", default="1b")
+    ap.add_argument("--no-alpha1", action="store_true")
+    ap.add_argument("--no-cpu", action="store_true")
+    ap.add_argument("--cpu-budget", type=float, default=20.0)
+    args = ap.parse_args()
+    if args.impl == "reference":
+        run_reference(args)
+    else:
+        run_ours(args)
+
+
+if __name__ == "__main__":
+    main()

@@ -1,0 +1,140 @@
+/*
+ * dion2.h -- C ABI of the B200-native Dion2 optimizer step (arXiv 2512.16928).
+ *
+ * The library implements Algorithm 1 of the paper ("alpha-Dion2(G, M)",
+ * PAPER.md P:177-191) for a batch of weight matrices on one GPU:
+ *
+ *   l.2  M <- M + G
+ *   l.3  K <- Select_alpha(M)  (top l1 rows or columns)
+ *   l.4  O <- NewtonSchulz(M[K, :])
+ *   l.5  M[K, :] <- mu * M[K, :]   Eq. (error-feedback)
+ *   l.6  W[K, :] <- W[K, :] - eta*sqrt(fan-out/fan-in)*O  Eq. (orth-update)
+ *
+ * "Column-selection is analogous"; auto mode selects along the
+ * shorter dimension.  The readings taken where the paper is silent
+ * (NS coefficients/steps/normalisation, k rounding, tie-break, orientation)
+ * are listed in DESIGN.md "Readings".
+ *
+ * Conventions
+ *  - Every pointer is a DEVICE pointer unless marked HOST.
+ *  - Matrices are row-major: element (i, j) of W is W[i*ld + j]; rows =
+ *    fan-out, cols = fan-in (y = W x).
+ *  - The caller owns every buffer (W, M, G, workspace, optional outputs).
+ *    The library never allocates device memory inside a step; size the
+ *    workspace with dion2_workspace_size() and pass it to every step.
+ *  - All work is enqueued asynchronously on `stream` (a cudaStream_t passed
+ *    as void*; NULL = legacy default stream).  No host synchronisation
+ *    happens inside a step.  Calls that touch the same matrices must not
+ *    overlap.  The workspace may not be shared by concurrent calls.
+ *  - Return value: a dion2_status code.  Codes 1-4 are detected on the host
+ *    before anything is enqueued.  Non-finite scores are detected on the
+ *    device: that matrix's W and M[K] writes are skipped and
+ *    dion2_get_status() reports it (ENONFINITE).
+ */
+#ifndef DION2_H_
+#define DION2_H_
+
+#include <stddef.h>
+#include <stdint.h>
+
+#ifdef __cplusplus
+extern "C" {
+#endif
+
+#define DION2_ABI_VERSION 1
+#define DION2_MAX_NS_STEPS 16
+
+typedef enum {
+  DION2_OK = 0,
+  DION2_EINVAL_CONFIG = 1, /* alpha not in (0,1], mu not in [0,1), lr < 0, ns_steps not in [1,16], eps <= 0, bad enum */
+  DION2_EINVAL_SHAPE = 2,  /* rows/cols < 1, ld < cols, NULL W/M/G, d > DION2_MAX_SELECT_DIM */
+  DION2_EWORKSPACE = 3,    /* workspace NULL or smaller than dion2_workspace_size() */
+  DION2_EUNSUPPORTED = 4,  /* a configuration this build does not implement */
+  DION2_ECUDA = 5,         /* a CUDA runtime / launch error */
+  DION2_ENCCL = 6,         /* reserved for the multi-GPU entry point */
+  DION2_ENONFINITE = 7     /* (device-side) a matrix's scores were NaN/Inf */
+} dion2_status;
+
+/* Longest selection axis supported by the single-CTA top-k kernel. */
+#define DION2_MAX_SELECT_DIM 49152
+
+typedef enum { DION2_AXIS_ROWS = 0, DION2_AXIS_COLS = 1, DION2_AXIS_AUTO = 2 } dion2_axis;
+typedef enum { DION2_SELECT_L1 = 0, DION2_SELECT_RANDOM = 1 } dion2_select;
+typedef enum { DION2_NS_BF16 = 0, DION2_NS_FP32 = 1 } dion2_precision;
+typedef enum { DION2_DT_F32 = 0, DION2_DT_BF16 = 1 } dion2_dtype;
+
+/* One weight matrix and its optimizer state. */
+typedef struct {
+  int64_t rows;        /* m = fan-out, >= 1 */
+  int64_t cols;        /* n = fan-in,  >= 1 */
+  int64_t ld;          /* row stride in elements of W, M and G; >= cols */
+  float* W;            /* [rows x ld] fp32, updated in place (selected rows/cols only) */
+  float* M;            /* [rows x ld] fp32 momentum, updated in place */
+  const void* G;       /* [rows x ld] gradient, dtype cfg.grad_dtype, read only */
+  int32_t* sel_out;    /* optional [k] int32: the selected indices, ascending (NULL = not written) */
+  float* O_out;        /* optional fp32 copy of O in natural orientation: [k x cols] (rows mode) or
+                          [rows x k] (cols mode), dense row-major (NULL = not written) */
+} dion2_matrix;
+
+/* Hyper-parameters of Alg. 1.  Fill with dion2_config_init() first. */
+typedef struct {
+  float alpha;        /* selection fraction in (0, 1]; k = max(1, floor(alpha*d + 1/2)) (reading R7) */
+  float mu;           /* momentum decay in [0, 1), default 0.95 (Alg. 1 header) */
+  float lr;           /* eta >= 0, default 0.02 */
+  int32_t ns_steps;   /* Newton-Schulz iterations T in [1, 16], default 5 (reading R2) */
+  float ns_coeffs[DION2_MAX_NS_STEPS][3]; /* (a, b, c) per iteration, default (3.4445, -4.7750, 2.0315) (reading R1) */
+  float ns_eps;       /* X0 = X / (||X||_F + eps), default 1e-7 (reading R3) */
+  int32_t axis;       /* dion2_axis, default AUTO (shorter dimension) */
+  int32_t select;     /* dion2_select, default L1 (only L1 is implemented; RANDOM -> EUNSUPPORTED) */
+  int32_t precision;  /* dion2_precision: BF16 = tcgen05 tensor-core NS (hot path); FP32 = SIMT fp32 NS (validation) */
+  int32_t grad_dtype; /* dion2_dtype of G, default F32 */
+  int32_t decay_mode; /* 0 = selective decay Eq. (error-feedback) (paper); 1 = full decay M <- mu*M (ablation) */
+  int32_t scale_mode; /* 0 = eta*sqrt(rows/cols) of the full W (Alg. 1 l.6); 1 = sqrt of the submatrix dims (SPEC S:360 flag) */
+  uint64_t seed;      /* random selection keying (unused for L1) */
+  uint64_t step;      /* random selection keying (unused for L1) */
+} dion2_config;
+
+/* Fill *cfg with the defaults above.  Always returns DION2_OK. */
+int dion2_config_init(dion2_config* cfg);
+
+/* Bytes of device workspace a step over mats[0..n) with *cfg needs (HOST
+ * mats/cfg; the W/M/G pointers are not read).  Returns EINVAL_* on a bad
+ * configuration or shape. */
+int dion2_workspace_size(const dion2_matrix* mats, int32_t n, const dion2_config* cfg, size_t* bytes_out);
+
+/* One Dion2 step on one matrix (== dion2_step_batched with n = 1). */
+int dion2_step(const dion2_matrix* mat, const dion2_config* cfg, void* workspace, size_t ws_bytes, void* stream);
+
+/* One Dion2 step on every matrix of mats[0..n) (HOST array of descriptors).
+ * Matrices are independent (Alg. 1 is per matrix parameter); the
+ * library batches each phase over all of them. */
+int dion2_step_batched(const dion2_matrix* mats, int32_t n, const dion2_config* cfg,
+                       void* workspace, size_t ws_bytes, void* stream);
+
+/* Synchronises the device, then reads the workspace's status word.
+ * Returns DION2_OK or DION2_ENONFINITE (and the index of the first matrix
+ * whose scores were non-finite in *first_bad_matrix, -1 if none).  The status
+ * word is cleared at the start of every step. */
+int dion2_get_status(const void* workspace, int32_t* first_bad_matrix);
+
+/* Human-readable name of a status code (static storage). */
+const char* dion2_strerror(int code);
+
+/* Per-phase device timing (CUDA events recorded on the step's stream around
+ * every kernel launch).  Off by default; enabling it adds event records only. */
+int dion2_set_phase_timing(int32_t enable);
+/* Synchronises; writes the accumulated milliseconds and launch counts per
+ * phase since the last reset (HOST arrays of cap entries), then resets. */
+int dion2_get_phase_times(float* ms_out, int32_t* launches_out, int32_t cap, int32_t* n_phases_out);
+/* Name of phase i ("momentum_score", "select", "gather", "ns_gram", "ns_poly", "ns_apply", "scatter", ...). */
+const char* dion2_phase_name(int32_t i);
+
+/* Number of kernel launches the last step enqueued. */
+int32_t dion2_last_launch_count(void);
+
+int32_t dion2_abi_version(void);
+
+#ifdef __cplusplus
+}
+#endif
+#endif /* DION2_H_ */

@@ -1,0 +1,709 @@
+// dion2_api.cu -- host runtime of the Dion2 step: config validation, the
+// per-(shapes, config, workspace) plan (axis/k resolution, wide orientation,
+// NS shape groups, workspace carve-up, TMA tensor maps, launch list), and the
+// C ABI declared in include/dion2.h.
+#include <cudaTypedefs.h>
+
+#include <algorithm>
+#include <cmath>
+#include <cstring>
+#include <map>
+#include <memory>
+#include <mutex>
+#include <string>
+#include <vector>
+
+#include "../../include/dion2.h"
+#include "kernels.cuh"
+
+using namespace dion2;
+
+namespace {
+
+constexpr int kNumPhases = 9;
+const char* kPhaseNames[kNumPhases] = {"momentum_score", "select", "gather", "norm", "ns_gram",
+                                       "ns_poly",        "ns_apply", "scatter", "full_decay"};
+enum Phase { PH_K1 = 0, PH_SELECT, PH_GATHER, PH_NORM, PH_GRAM, PH_POLY, PH_APPLY, PH_SCATTER, PH_FULLDECAY };
+
+std::mutex g_mu;
+int g_sm_count = 0;
+bool g_attr_done = false;
+int32_t g_last_launches = 0;
+
+// ------------------------------------------------------------------ phase timing
+bool g_timing = false;
+struct TimedLaunch {
+  int phase;
+  cudaEvent_t a, b;
+};
+std::vector<TimedLaunch> g_timed;
+std::vector<cudaEvent_t> g_event_pool;
+cudaEvent_t take_event() {
+  if (!g_event_pool.empty()) {
+    cudaEvent_t e = g_event_pool.back();
+    g_event_pool.pop_back();
+    return e;
+  }
+  cudaEvent_t e;
+  cudaEventCreate(&e);
+  return e;
+}
+
+// ------------------------------------------------------------------ helpers
+inline size_t align_up(size_t x, size_t a) { return (x + a - 1) / a * a; }
+inline int64_t ceil_div(int64_t a, int64_t b) { return (a + b - 1) / b; }
+
+PFN_cuTensorMapEncodeTiled_v12000 get_encode_fn() {
+  static PFN_cuTensorMapEncodeTiled_v12000 fn = nullptr;
+  if (!fn) {
+    void* p = nullptr;
+    cudaDriverEntryPointQueryResult q;
+    if (cudaGetDriverEntryPoint("cuTensorMapEncodeTiled", &p, cudaEnableDefault, &q) == cudaSuccess &&
+        q == cudaDriverEntryPointSuccess)
+      fn = reinterpret_cast<PFN_cuTensorMapEncodeTiled_v12000>(p);
+  }
+  return fn;
+}
+
+// 3-D bf16 tensor map over [count][rows][cols] (row-major), SWIZZLE_128B, box {64, box_rows, 1}.
+bool make_map(CUtensorMap* m, const void* base, int64_t cols, int64_t rows, int64_t count, int box_cols, int box_rows) {
+  auto enc = get_encode_fn();
+  if (!enc) return false;
+  cuuint64_t dims[3] = {(cuuint64_t)cols, (cuuint64_t)rows, (cuuint64_t)count};
+  cuuint64_t strides[2] = {(cuuint64_t)(cols * 2), (cuuint64_t)(cols * rows * 2)};
+  cuuint32_t box[3] = {(cuuint32_t)box_cols, (cuuint32_t)box_rows, 1};
+  cuuint32_t estr[3] = {1, 1, 1};
+  CUresult r = enc(m, CU_TENSOR_MAP_DATA_TYPE_BFLOAT16, 3, const_cast<void*>(base), dims, strides, box, estr,
+                   CU_TENSOR_MAP_INTERLEAVE_NONE, CU_TENSOR_MAP_SWIZZLE_128B, CU_TENSOR_MAP_L2_PROMOTION_L2_256B,
+                   CU_TENSOR_MAP_FLOAT_OOB_FILL_NONE);
+  return r == CUDA_SUCCESS;
+}
+
+int validate_config(const dion2_config* c) {
+  if (!c) return DION2_EINVAL_CONFIG;
+  if (!(c->alpha > 0.f && c->alpha <= 1.f)) return DION2_EINVAL_CONFIG;
+  if (!(c->mu >= 0.f && c->mu < 1.f)) return DION2_EINVAL_CONFIG;
+  if (!(c->lr >= 0.f) || !std::isfinite(c->lr)) return DION2_EINVAL_CONFIG;
+  if (c->ns_steps < 1 || c->ns_steps > DION2_MAX_NS_STEPS) return DION2_EINVAL_CONFIG;
+  if (!(c->ns_eps > 0.f)) return DION2_EINVAL_CONFIG;
+  for (int t = 0; t < c->ns_steps; ++t)
+    for (int j = 0; j < 3; ++j)
+      if (!std::isfinite(c->ns_coeffs[t][j])) return DION2_EINVAL_CONFIG;
+  if (c->axis < 0 || c->axis > 2) return DION2_EINVAL_CONFIG;
+  if (c->select != DION2_SELECT_L1 && c->select != DION2_SELECT_RANDOM) return DION2_EINVAL_CONFIG;
+  if (c->precision != DION2_NS_BF16 && c->precision != DION2_NS_FP32) return DION2_EINVAL_CONFIG;
+  if (c->grad_dtype != DION2_DT_F32 && c->grad_dtype != DION2_DT_BF16) return DION2_EINVAL_CONFIG;
+  if (c->decay_mode < 0 || c->decay_mode > 1) return DION2_EINVAL_CONFIG;
+  if (c->scale_mode < 0 || c->scale_mode > 1) return DION2_EINVAL_CONFIG;
+  if (c->select == DION2_SELECT_RANDOM) return DION2_EUNSUPPORTED;
+  return DION2_OK;
+}
+
+int validate_shape(const dion2_matrix& m, bool need_ptrs) {
+  if (m.rows < 1 || m.cols < 1 || m.ld < m.cols) return DION2_EINVAL_SHAPE;
+  if (m.rows > (1ll << 31) - 1 || m.cols > (1ll << 31) - 1) return DION2_EINVAL_SHAPE;
+  if (need_ptrs && (!m.W || !m.M || !m.G)) return DION2_EINVAL_SHAPE;
+  return DION2_OK;
+}
+
+// ------------------------------------------------------------------ plan
+struct MatPlan {
+  int axis, d, o, k, sr, sc, transposed, p, q, p_pad, q_pad, group, zi, rowblocks, ga, gb;
+  float fan_sqrt;
+  size_t off_scores, off_partials, off_sel, off_sumsq;
+};
+
+struct Group {
+  int p_pad, q_pad, count;
+  std::vector<int> mats;  // global matrix indices
+  size_t off_X0, off_X1, off_A, off_B, off_gmats;
+};
+
+struct Launch {
+  int phase;
+  int bn;
+  int kind;  // 0 = tc BN128, 1 = tc BN256, 2 = simt
+  NsTcParams tc;
+  int simt_group;
+};
+
+struct Plan {
+  int n;
+  bool bf16_ns;
+  int ns_steps;
+  std::vector<MatPlan> mp;
+  std::vector<Group> groups;
+  size_t off_status, off_bad, off_desc, off_rowmats, off_rowprefix, off_colmats, off_colprefix, off_gprefix,
+      off_nsscale, off_ns_begin, off_ns_end, total;
+  int64_t total_rows = 0, total_col_tiles = 0;
+  int n_row_mats = 0, n_col_mats = 0, total_gather_tiles = 0, max_d = 0;
+  std::vector<uint8_t> host_tables;  // [off_desc, off_ns_begin) image (descriptors + aux)
+  std::vector<Launch> ns_launches;
+  void* ws = nullptr;
+  uint64_t id = 0;
+  std::vector<const void*> last_ptrs;  // W, M, G, sel_out, O_out per matrix as last uploaded
+};
+
+std::map<std::string, std::unique_ptr<Plan>> g_plans;
+std::map<void*, uint64_t> g_ws_last_plan;  // workspace -> id of the plan whose tables it holds
+uint64_t g_next_plan_id = 1;
+
+std::string plan_key(const dion2_matrix* mats, int n, const dion2_config* c, void* ws) {
+  std::string k;
+  auto put = [&](const void* p, size_t s) { k.append(reinterpret_cast<const char*>(p), s); };
+  put(&n, sizeof n);
+  put(&ws, sizeof ws);
+  for (int i = 0; i < n; ++i) {
+    put(&mats[i].rows, 8);
+    put(&mats[i].cols, 8);
+    put(&mats[i].ld, 8);
+  }
+  put(&c->alpha, 4);
+  put(&c->ns_steps, 4);
+  put(c->ns_coeffs, sizeof(float) * 3 * c->ns_steps);
+  put(&c->axis, 4);
+  put(&c->select, 4);
+  put(&c->precision, 4);
+  put(&c->grad_dtype, 4);
+  put(&c->decay_mode, 4);
+  put(&c->scale_mode, 4);
+  return k;
+}
+
+// Build the plan layout (no device work).  ws may be null (size query).
+int build_layout(Plan& P, const dion2_matrix* mats, int n, const dion2_config* c) {
+  P.n = n;
+  P.bf16_ns = c->precision == DION2_NS_BF16;
+  P.ns_steps = c->ns_steps;
+  P.mp.resize(n);
+  const size_t xel = P.bf16_ns ? 2 : 4;
+  std::map<std::pair<int, int>, int> gidx;
+  for (int i = 0; i < n; ++i) {
+    const dion2_matrix& m = mats[i];
+    MatPlan& q = P.mp[i];
+    const int64_t rows = m.rows, cols = m.cols;
+    int axis = c->axis == DION2_AXIS_AUTO ? (rows <= cols ? DION2_AXIS_ROWS : DION2_AXIS_COLS) : c->axis;
+    q.axis = axis;
+    q.d = (int)(axis == DION2_AXIS_ROWS ? rows : cols);
+    q.o = (int)(axis == DION2_AXIS_ROWS ? cols : rows);
+    if (q.d > DION2_MAX_SELECT_DIM) return DION2_EINVAL_SHAPE;
+    int64_t k = (int64_t)std::floor((double)c->alpha * (double)q.d + 0.5);  // reading R7
+    k = std::max<int64_t>(1, std::min<int64_t>(k, q.d));
+    q.k = (int)k;
+    q.sr = axis == DION2_AXIS_ROWS ? q.k : (int)rows;
+    q.sc = axis == DION2_AXIS_ROWS ? (int)cols : q.k;
+    q.transposed = q.sr > q.sc;  // wide orientation (reading R4)
+    q.p = std::min(q.sr, q.sc);
+    q.q = std::max(q.sr, q.sc);
+    q.p_pad = (int)align_up(q.p, 128);
+    q.q_pad = (int)align_up(q.q, 256);
+    if (c->scale_mode == 0) q.fan_sqrt = (float)std::sqrt((double)rows / (double)cols);  // Alg. 1 l.6
+    else q.fan_sqrt = (float)std::sqrt((double)q.sr / (double)q.sc);
+    q.rowblocks = (int)ceil_div(rows, 64);
+    q.ga = (int)ceil_div(q.sr, kTileA);
+    q.gb = (int)ceil_div(q.sc, kTileB);
+    auto key = std::make_pair(q.p_pad, q.q_pad);
+    auto it = gidx.find(key);
+    if (it == gidx.end()) {
+      Group g{};
+      g.p_pad = q.p_pad;
+      g.q_pad = q.q_pad;
+      g.count = 0;
+      gidx[key] = (int)P.groups.size();
+      P.groups.push_back(g);
+      it = gidx.find(key);
+    }
+    q.group = it->second;
+    q.zi = P.groups[q.group].count++;
+    P.groups[q.group].mats.push_back(i);
+    P.max_d = std::max(P.max_d, q.d);
+  }
+  // ---- workspace carve-up
+  size_t off = 0;
+  auto take = [&](size_t bytes) {
+    size_t o = off;
+    off = align_up(off + std::max<size_t>(bytes, 1), 256);
+    return o;
+  };
+  P.off_status = take(16);
+  P.off_bad = take(4 * (size_t)n);
+  P.off_desc = take(sizeof(MatDesc) * n);
+  P.off_rowmats = take(4 * (size_t)n);
+  P.off_rowprefix = take(8 * (size_t)n);
+  P.off_colmats = take(4 * (size_t)n);
+  P.off_colprefix = take(8 * (size_t)n);
+  P.off_gprefix = take(4 * (size_t)n);
+  for (auto& g : P.groups) g.off_gmats = take(4 * (size_t)g.count);
+  P.off_nsscale = take(8 * (size_t)n);
+  for (int i = 0; i < n; ++i) {
+    MatPlan& q = P.mp[i];
+    q.off_scores = take(4 * (size_t)q.d);
+    q.off_partials = q.axis == DION2_AXIS_COLS ? take(4 * (size_t)q.rowblocks * (size_t)mats[i].cols) : 0;
+    q.off_sel = take(4 * (size_t)q.k);
+    q.off_sumsq = take(4 * (size_t)q.ga * q.gb);
+  }
+  off = align_up(off, 4096);
+  P.off_ns_begin = off;
+  for (auto& g : P.groups) {
+    const size_t xb = (size_t)g.count * g.p_pad * g.q_pad * xel;
+    const size_t ab = (size_t)g.count * g.p_pad * g.p_pad * xel;
+    g.off_X0 = off; off = align_up(off + xb, 4096);
+    g.off_X1 = off; off = align_up(off + xb, 4096);
+    g.off_A = off;  off = align_up(off + ab, 4096);
+    g.off_B = off;  off = align_up(off + ab, 4096);
+  }
+  P.off_ns_end = off;
+  P.total = off + 4096;  // slack for base alignment
+  return DION2_OK;
+}
+
+inline void* at(void* ws, size_t off) { return static_cast<uint8_t*>(ws) + off; }
+
+// Fill host tables and NS launches for a concrete workspace.
+int build_device_plan(Plan& P, const dion2_matrix* mats, const dion2_config* c, void* ws) {
+  P.ws = ws;
+  const int n = P.n;
+  P.host_tables.assign(P.off_nsscale - P.off_desc, 0);
+  auto H = [&](size_t off) { return P.host_tables.data() + (off - P.off_desc); };
+  MatDesc* D = reinterpret_cast<MatDesc*>(H(P.off_desc));
+  std::vector<int32_t> rowmats, colmats;
+  std::vector<int64_t> rowprefix, colprefix;
+  std::vector<int32_t> gprefix(n);
+  int64_t rows_acc = 0, ctiles_acc = 0;
+  int gt_acc = 0;
+  for (int i = 0; i < n; ++i) {
+    const MatPlan& q = P.mp[i];
+    const Group& g = P.groups[q.group];
+    MatDesc& d = D[i];
+    d.rows = mats[i].rows;
+    d.cols = mats[i].cols;
+    d.ld = mats[i].ld;
+    d.axis = q.axis;
+    d.d = q.d; d.o = q.o; d.k = q.k; d.sr = q.sr; d.sc = q.sc; d.transposed = q.transposed;
+    d.p = q.p; d.q = q.q; d.p_pad = q.p_pad; d.q_pad = q.q_pad;
+    d.grad_bf16 = c->grad_dtype == DION2_DT_BF16;
+    d.update_scale = q.fan_sqrt;
+    d.scores = (float*)at(ws, q.off_scores);
+    d.col_partials = q.axis == DION2_AXIS_COLS ? (float*)at(ws, q.off_partials) : nullptr;
+    d.sel = (int32_t*)at(ws, q.off_sel);
+    d.sumsq_partials = (float*)at(ws, q.off_sumsq);
+    d.ns_scale = (float*)at(ws, P.off_nsscale) + 2 * i;
+    const size_t xel = P.bf16_ns ? 2 : 4;
+    d.X0 = at(ws, g.off_X0 + (size_t)q.zi * g.p_pad * g.q_pad * xel);
+    d.X1 = at(ws, g.off_X1 + (size_t)q.zi * g.p_pad * g.q_pad * xel);
+    d.final_in_x1 = (P.ns_steps & 1);
+    d.gather_tile_base = gt_acc;
+    d.gather_tiles_a = q.ga;
+    d.gather_tiles_b = q.gb;
+    d.rowblocks = q.rowblocks;
+    gprefix[i] = gt_acc;
+    gt_acc += q.ga * q.gb;
+    if (q.axis == DION2_AXIS_ROWS) {
+      rowmats.push_back(i);
+      rowprefix.push_back(rows_acc);
+      rows_acc += mats[i].rows;
+    } else {
+      colmats.push_back(i);
+      colprefix.push_back(ctiles_acc);
+      ctiles_acc += (int64_t)q.rowblocks * ceil_div(mats[i].cols, 256);
+    }
+  }
+  P.total_rows = rows_acc;
+  P.total_col_tiles = ctiles_acc;
+  P.n_row_mats = (int)rowmats.size();
+  P.n_col_mats = (int)colmats.size();
+  P.total_gather_tiles = gt_acc;
+  if (!rowmats.empty()) {
+    memcpy(H(P.off_rowmats), rowmats.data(), 4 * rowmats.size());
+    memcpy(H(P.off_rowprefix), rowprefix.data(), 8 * rowprefix.size());
+  }
+  if (!colmats.empty()) {
+    memcpy(H(P.off_colmats), colmats.data(), 4 * colmats.size());
+    memcpy(H(P.off_colprefix), colprefix.data(), 8 * colprefix.size());
+  }
+  memcpy(H(P.off_gprefix), gprefix.data(), 4 * n);
+  for (auto& g : P.groups) memcpy(H(g.off_gmats), g.mats.data(), 4 * g.mats.size());
+
+  // ---- Newton-Schulz launch list: per iteration t: gram, poly, apply; per phase the
+  // groups are batched (<= kMaxGroups per launch, one BN class per launch).
+  P.ns_launches.clear();
+  const float* scale_all = (const float*)at(ws, P.off_nsscale);
+  for (int t = 0; t < P.ns_steps; ++t) {
+    const float a = c->ns_coeffs[t][0], b = c->ns_coeffs[t][1], cc = c->ns_coeffs[t][2];
+    for (int ph = PH_GRAM; ph <= PH_APPLY; ++ph) {
+      // bucket groups by BN class
+      std::vector<int> by_bn[2];
+      for (int gi = 0; gi < (int)P.groups.size(); ++gi) {
+        const Group& g = P.groups[gi];
+        int bn256 = ph == PH_APPLY ? 1 : (g.p_pad % 256 == 0);
+        by_bn[bn256].push_back(gi);
+      }
+      for (int cls = 0; cls < 2; ++cls) {
+        const int BN = cls ? 256 : 128;
+        auto& gl = by_bn[cls];
+        for (size_t s0 = 0; s0 < gl.size(); s0 += kMaxGroups) {
+          Launch L{};
+          L.phase = ph;
+          L.bn = BN;
+          L.kind = P.bf16_ns ? cls : 2;
+          NsParams& np = L.tc.p;
+          np.ngroups = (int)std::min<size_t>(kMaxGroups, gl.size() - s0);
+          np.ns_scale_all = scale_all;
+          if (ph == PH_GRAM) { np.cacc = 1.f; np.cC = 0.f; np.scale_sel = t == 0 ? 2 : 0; np.b_kmajor = 1; }
+          if (ph == PH_POLY) { np.cacc = cc; np.cC = b; np.scale_sel = 0; np.b_kmajor = 1; }
+          if (ph == PH_APPLY) { np.cacc = 1.f; np.cC = a; np.scale_sel = t == 0 ? 1 : 0; np.b_kmajor = 0; }
+          int tiles = 0;
+          for (int j = 0; j < np.ngroups; ++j) {
+            const Group& g = P.groups[gl[s0 + j]];
+            const size_t xel = P.bf16_ns ? 2 : 4;
+            void* Xc = at(ws, (t & 1) ? g.off_X1 : g.off_X0);
+            void* Xn = at(ws, (t & 1) ? g.off_X0 : g.off_X1);
+            void* A = at(ws, g.off_A);
+            void* Bm = at(ws, g.off_B);
+            NsGroup& G = np.g[j];
+            G.count = g.count;
+            G.gmats = (const int32_t*)at(ws, g.off_gmats);
+            const long long xs = (long long)g.p_pad * g.q_pad, as = (long long)g.p_pad * g.p_pad;
+            if (ph == PH_GRAM) {
+              G.m_tiles = g.p_pad / 128; G.n_tiles = g.p_pad / BN; G.k_blocks = g.q_pad / 64;
+              G.a = Xc; G.a_mstride = xs; G.lda = g.q_pad;
+              G.b = Xc; G.b_mstride = xs; G.ldb = g.q_pad;
+              G.out = A; G.out_mstride = as; G.out_ld = g.p_pad;
+              G.cin = nullptr; G.cin_mstride = 0; G.cin_ld = 0;
+              if (P.bf16_ns) {
+                if (!make_map(&L.tc.mapA[j], Xc, g.q_pad, g.p_pad, g.count, 64, 128)) return DION2_ECUDA;
+                if (!make_map(&L.tc.mapB[j], Xc, g.q_pad, g.p_pad, g.count, 64, BN)) return DION2_ECUDA;
+              }
+            } else if (ph == PH_POLY) {
+              G.m_tiles = g.p_pad / 128; G.n_tiles = g.p_pad / BN; G.k_blocks = g.p_pad / 64;
+              G.a = A; G.a_mstride = as; G.lda = g.p_pad;
+              G.b = A; G.b_mstride = as; G.ldb = g.p_pad;
+              G.out = Bm; G.out_mstride = as; G.out_ld = g.p_pad;
+              G.cin = A; G.cin_mstride = as; G.cin_ld = g.p_pad;
+              if (P.bf16_ns) {
+                if (!make_map(&L.tc.mapA[j], A, g.p_pad, g.p_pad, g.count, 64, 128)) return DION2_ECUDA;
+                if (!make_map(&L.tc.mapB[j], A, g.p_pad, g.p_pad, g.count, 64, BN)) return DION2_ECUDA;
+              }
+            } else {
+              G.m_tiles = g.p_pad / 128; G.n_tiles = g.q_pad / BN; G.k_blocks = g.p_pad / 64;
+              G.a = Bm; G.a_mstride = as; G.lda = g.p_pad;
+              G.b = Xc; G.b_mstride = xs; G.ldb = g.q_pad;
+              G.out = Xn; G.out_mstride = xs; G.out_ld = g.q_pad;
+              G.cin = Xc; G.cin_mstride = xs; G.cin_ld = g.q_pad;
+              if (P.bf16_ns) {
+                if (!make_map(&L.tc.mapA[j], Bm, g.p_pad, g.p_pad, g.count, 64, 128)) return DION2_ECUDA;
+                // MN-major B operand: box = 64 columns of X (N) x 64 rows of X (K)
+                if (!make_map(&L.tc.mapB[j], Xc, g.q_pad, g.p_pad, g.count, 64, 64)) return DION2_ECUDA;
+              }
+            }
+            (void)xel;
+            G.tile_base = tiles;
+            tiles += G.count * G.m_tiles * G.n_tiles;
+          }
+          np.total_tiles = tiles;
+          if (P.bf16_ns) {
+            P.ns_launches.push_back(L);
+          } else {
+            // SIMT path: one launch per group
+            for (int j = 0; j < np.ngroups; ++j) {
+              Launch L2 = L;
+              L2.simt_group = j;
+              P.ns_launches.push_back(L2);
+            }
+          }
+        }
+      }
+    }
+  }
+  return DION2_OK;
+}
+
+void ensure_device_attrs() {
+  if (g_attr_done) return;
+  int dev = 0;
+  cudaGetDevice(&dev);
+  cudaDeviceGetAttribute(&g_sm_count, cudaDevAttrMultiProcessorCount, dev);
+  ns_tc_set_attrs();
+  cudaFuncSetAttribute(k_topk_select, cudaFuncAttributeMaxDynamicSharedMemorySize, 4 * DION2_MAX_SELECT_DIM);
+  cudaFuncSetAttribute(k_full_decay, cudaFuncAttributeMaxDynamicSharedMemorySize, DION2_MAX_SELECT_DIM);
+  g_attr_done = true;
+}
+
+struct Launcher {
+  cudaStream_t s;
+  int count = 0;
+  int err = DION2_OK;
+  int cur_phase = -1;
+  cudaEvent_t ev_a = nullptr;
+  void begin(int phase) {
+    cur_phase = phase;
+    if (g_timing) {
+      ev_a = take_event();
+      cudaEventRecord(ev_a, s);
+    }
+  }
+  void end() {
+    ++count;
+    if (cudaPeekAtLastError() != cudaSuccess) {
+      cudaGetLastError();
+      err = DION2_ECUDA;
+    }
+    if (g_timing) {
+      cudaEvent_t b = take_event();
+      cudaEventRecord(b, s);
+      g_timed.push_back({cur_phase, ev_a, b});
+    }
+  }
+};
+
+int run_step(Plan& P, const dion2_matrix* mats, const dion2_config* c, void* ws, cudaStream_t s) {
+  const int n = P.n;
+  // (re)upload descriptor tables when pointers or the workspace's owner plan changed
+  bool upload = g_ws_last_plan[ws] != P.id;
+  bool zero_ns = upload;
+  if ((int)P.last_ptrs.size() != 5 * n) {
+    P.last_ptrs.assign(5 * n, nullptr);
+    upload = true;
+  }
+  MatDesc* D = reinterpret_cast<MatDesc*>(P.host_tables.data());
+  for (int i = 0; i < n; ++i) {
+    const void* ptrs[5] = {mats[i].W, mats[i].M, mats[i].G, mats[i].sel_out, mats[i].O_out};
+    for (int j = 0; j < 5; ++j)
+      if (P.last_ptrs[5 * i + j] != ptrs[j]) { upload = true; P.last_ptrs[5 * i + j] = ptrs[j]; }
+    D[i].W = mats[i].W;
+    D[i].M = mats[i].M;
+    D[i].G = mats[i].G;
+    D[i].sel_out = mats[i].sel_out;
+    D[i].O_out = mats[i].O_out;
+    const size_t gel = c->grad_dtype == DION2_DT_BF16 ? 2 : 4;
+    const bool al = ((uintptr_t)mats[i].W % 16 == 0) && ((uintptr_t)mats[i].M % 16 == 0) &&
+                    ((uintptr_t)mats[i].G % (gel == 4 ? 16 : 8) == 0) && (mats[i].ld % 4 == 0);
+    D[i].vec4 = al ? 1 : 0;
+  }
+  if (upload) {
+    if (cudaMemcpyAsync(at(ws, P.off_desc), P.host_tables.data(), P.host_tables.size(), cudaMemcpyHostToDevice, s) !=
+        cudaSuccess)
+      return DION2_ECUDA;
+    g_ws_last_plan[ws] = P.id;
+  }
+  if (zero_ns) {
+    // NS buffers must hold zeros in their padding (zero rows/cols are exact no-ops for NS)
+    if (cudaMemsetAsync(at(ws, P.off_ns_begin), 0, P.off_ns_end - P.off_ns_begin, s) != cudaSuccess)
+      return DION2_ECUDA;
+  }
+  // status[0] = flags (0), status[1] = first bad matrix (atomicMin from 0x7f7f7f7f)
+  if (cudaMemsetAsync(at(ws, P.off_status), 0, 4, s) != cudaSuccess) return DION2_ECUDA;
+  if (cudaMemsetAsync(at(ws, P.off_status + 4), 0x7f, 4, s) != cudaSuccess) return DION2_ECUDA;
+
+  const MatDesc* dmats = (const MatDesc*)at(ws, P.off_desc);
+  int32_t* bad = (int32_t*)at(ws, P.off_bad);
+  int32_t* status = (int32_t*)at(ws, P.off_status);
+  Launcher L{s};
+  const int sms = g_sm_count > 0 ? g_sm_count : 148;
+
+  // K1 momentum + score (Alg. 1 l.2-3)
+  if (P.n_row_mats) {
+    L.begin(PH_K1);
+    int64_t blocks = std::min<int64_t>(ceil_div(P.total_rows, 8), (int64_t)sms * 8);
+    k_momentum_score_rows<<<(unsigned)blocks, 256, 0, s>>>(dmats, (const int32_t*)at(ws, P.off_rowmats),
+                                                           (const int64_t*)at(ws, P.off_rowprefix), P.n_row_mats,
+                                                           P.total_rows);
+    L.end();
+  }
+  if (P.n_col_mats) {
+    L.begin(PH_K1);
+    int64_t blocks = std::min<int64_t>(P.total_col_tiles, (int64_t)sms * 8);
+    k_momentum_score_cols<<<(unsigned)blocks, 256, 0, s>>>(dmats, (const int32_t*)at(ws, P.off_colmats),
+                                                           (const int64_t*)at(ws, P.off_colprefix), P.n_col_mats,
+                                                           P.total_col_tiles);
+    L.end();
+  }
+  // K2 select (Alg. 1 l.3)
+  L.begin(PH_SELECT);
+  k_topk_select<<<n, kSelectThreads, 4 * P.max_d, s>>>(dmats, bad, status);
+  L.end();
+  // K3 gather + decay (Alg. 1 l.4-5)
+  {
+    L.begin(PH_GATHER);
+    int blocks = std::min(P.total_gather_tiles, sms * 8);
+    const int decay = 1;
+    launch_gather_decay(P.bf16_ns, blocks, s, dmats, (const int32_t*)at(ws, P.off_gprefix), n, P.total_gather_tiles,
+                        bad, decay, c->mu);
+    L.end();
+    L.begin(PH_NORM);
+    k_norm_finalize<<<(unsigned)ceil_div(n, 8), 256, 0, s>>>(dmats, n, c->ns_eps);
+    L.end();
+  }
+  // K4-K6 Newton-Schulz (Alg. 1 l.4)
+  for (const Launch& ln : P.ns_launches) {
+    L.begin(ln.phase);
+    if (ln.kind == 0 || ln.kind == 1) {
+      launch_ns_tc(ln.bn, std::min(ln.tc.p.total_tiles, sms), s, ln.tc);
+    } else {
+      const NsGroup& G = ln.tc.p.g[ln.simt_group];
+      const int Mdim = G.m_tiles * 128;
+      const int Ndim = G.n_tiles * ln.bn;
+      dim3 grid(Ndim / 64, Mdim / 64, G.count);
+      k_ns_gemm_simt_f32<<<grid, 256, 0, s>>>(ln.tc.p, ln.simt_group);
+    }
+    L.end();
+  }
+  // K7 scatter (Alg. 1 l.6)
+  {
+    L.begin(PH_SCATTER);
+    int blocks = std::min(P.total_gather_tiles, sms * 8);
+    launch_scatter_update(P.bf16_ns, blocks, s, dmats, (const int32_t*)at(ws, P.off_gprefix), n, P.total_gather_tiles,
+                          bad, c->lr);
+    L.end();
+  }
+  if (c->decay_mode == 1) {
+    L.begin(PH_FULLDECAY);
+    int64_t maxrows = 0;
+    for (int i = 0; i < n; ++i) maxrows = std::max<int64_t>(maxrows, mats[i].rows);
+    dim3 grid((unsigned)ceil_div(maxrows, 64), n);
+    k_full_decay<<<grid, 256, P.max_d, s>>>(dmats, n, bad, c->mu);
+    L.end();
+  }
+  g_last_launches = L.count;
+  return L.err;
+}
+
+}  // namespace
+
+// ============================================================================ C ABI
+
+extern "C" {
+
+int dion2_config_init(dion2_config* cfg) {
+  if (!cfg) return DION2_EINVAL_CONFIG;
+  memset(cfg, 0, sizeof(*cfg));
+  cfg->alpha = 0.25f;
+  cfg->mu = 0.95f;
+  cfg->lr = 0.02f;
+  cfg->ns_steps = 5;
+  for (int t = 0; t < DION2_MAX_NS_STEPS; ++t) {
+    cfg->ns_coeffs[t][0] = 3.4445f;
+    cfg->ns_coeffs[t][1] = -4.7750f;
+    cfg->ns_coeffs[t][2] = 2.0315f;
+  }
+  cfg->ns_eps = 1e-7f;
+  cfg->axis = DION2_AXIS_AUTO;
+  cfg->select = DION2_SELECT_L1;
+  cfg->precision = DION2_NS_BF16;
+  cfg->grad_dtype = DION2_DT_F32;
+  cfg->decay_mode = 0;
+  cfg->scale_mode = 0;
+  return DION2_OK;
+}
+
+int dion2_workspace_size(const dion2_matrix* mats, int32_t n, const dion2_config* cfg, size_t* bytes_out) {
+  if (!bytes_out) return DION2_EINVAL_CONFIG;
+  int rc = validate_config(cfg);
+  if (rc) return rc;
+  if (n < 1 || !mats) return DION2_EINVAL_SHAPE;
+  for (int i = 0; i < n; ++i)
+    if ((rc = validate_shape(mats[i], false))) return rc;
+  Plan P;
+  rc = build_layout(P, mats, n, cfg);
+  if (rc) return rc;
+  *bytes_out = P.total;
+  return DION2_OK;
+}
+
+int dion2_step_batched(const dion2_matrix* mats, int32_t n, const dion2_config* cfg, void* workspace,
+                       size_t ws_bytes, void* stream) {
+  int rc = validate_config(cfg);
+  if (rc) return rc;
+  if (n < 1 || !mats) return DION2_EINVAL_SHAPE;
+  for (int i = 0; i < n; ++i)
+    if ((rc = validate_shape(mats[i], true))) return rc;
+  if (!workspace) return DION2_EWORKSPACE;
+  std::lock_guard<std::mutex> lock(g_mu);
+  ensure_device_attrs();
+  // align the usable workspace base to 4 KiB (TMA / swizzle alignment)
+  void* ws = reinterpret_cast<void*>(align_up(reinterpret_cast<uintptr_t>(workspace), 4096));
+  const size_t slack = (uintptr_t)ws - (uintptr_t)workspace;
+  std::string key = plan_key(mats, n, cfg, ws);
+  auto it = g_plans.find(key);
+  Plan* P;
+  if (it == g_plans.end()) {
+    auto np = std::make_unique<Plan>();
+    rc = build_layout(*np, mats, n, cfg);
+    if (rc) return rc;
+    if (np->total - 4096 + slack > ws_bytes) return DION2_EWORKSPACE;
+    rc = build_device_plan(*np, mats, cfg, ws);
+    if (rc) return rc;
+    np->id = g_next_plan_id++;
+    P = np.get();
+    g_plans[key] = std::move(np);
+  } else {
+    P = it->second.get();
+    if (P->total - 4096 + slack > ws_bytes) return DION2_EWORKSPACE;
+  }
+  return run_step(*P, mats, cfg, ws, reinterpret_cast<cudaStream_t>(stream));
+}
+
+int dion2_step(const dion2_matrix* mat, const dion2_config* cfg, void* workspace, size_t ws_bytes, void* stream) {
+  return dion2_step_batched(mat, 1, cfg, workspace, ws_bytes, stream);
+}
+
+int dion2_get_status(const void* workspace, int32_t* first_bad_matrix) {
+  if (!workspace) return DION2_EWORKSPACE;
+  if (cudaDeviceSynchronize() != cudaSuccess) return DION2_ECUDA;
+  const void* ws = reinterpret_cast<const void*>(align_up(reinterpret_cast<uintptr_t>(workspace), 4096));
+  int32_t st[2] = {0, 0};
+  if (cudaMemcpy(st, ws, 8, cudaMemcpyDeviceToHost) != cudaSuccess) return DION2_ECUDA;
+  if (first_bad_matrix) *first_bad_matrix = st[0] ? st[1] : -1;
+  return st[0] ? DION2_ENONFINITE : DION2_OK;
+}
+
+const char* dion2_strerror(int code) {
+  switch (code) {
+    case DION2_OK: return "ok";
+    case DION2_EINVAL_CONFIG: return "invalid configuration";
+    case DION2_EINVAL_SHAPE: return "invalid matrix shape or pointer";
+    case DION2_EWORKSPACE: return "workspace missing or too small";
+    case DION2_EUNSUPPORTED: return "unsupported configuration";
+    case DION2_ECUDA: return "CUDA error";
+    case DION2_ENCCL: return "NCCL error";
+    case DION2_ENONFINITE: return "non-finite scores (matrix skipped)";
+    default: return "unknown status";
+  }
+}
+
+int dion2_set_phase_timing(int32_t enable) {
+  std::lock_guard<std::mutex> lock(g_mu);
+  g_timing = enable != 0;
+  return DION2_OK;
+}
+
+int dion2_get_phase_times(float* ms_out, int32_t* launches_out, int32_t cap, int32_t* n_phases_out) {
+  std::lock_guard<std::mutex> lock(g_mu);
+  std::vector<float> ms(kNumPhases, 0.f);
+  std::vector<int32_t> cnt(kNumPhases, 0);
+  int rc = DION2_OK;
+  for (auto& t : g_timed) {
+    if (cudaEventSynchronize(t.b) != cudaSuccess) rc = DION2_ECUDA;
+    float e = 0.f;
+    cudaEventElapsedTime(&e, t.a, t.b);
+    ms[t.phase] += e;
+    cnt[t.phase] += 1;
+    g_event_pool.push_back(t.a);
+    g_event_pool.push_back(t.b);
+  }
+  g_timed.clear();
+  for (int i = 0; i < std::min<int>(cap, kNumPhases); ++i) {
+    if (ms_out) ms_out[i] = ms[i];
+    if (launches_out) launches_out[i] = cnt[i];
+  }
+  if (n_phases_out) *n_phases_out = kNumPhases;
+  return rc;
+}
+
+const char* dion2_phase_name(int32_t i) { return (i >= 0 && i < kNumPhases) ? kPhaseNames[i] : "?"; }
+
+int32_t dion2_last_launch_count(void) { return g_last_launches; }
+
+int32_t dion2_abi_version(void) { return DION2_ABI_VERSION; }
+
+}  // extern "C"

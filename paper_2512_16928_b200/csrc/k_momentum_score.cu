@@ -1,0 +1,186 @@
+// K1: fused momentum accumulation + l1 scoring.
+//   Alg. 1 l.2  M <- M + G
+//   Alg. 1 l.3  score = l1 norm of every row / column of the updated M
+// HBM-bound single pass: read G, read M, write M (12 B per fp32 parameter).
+#include "kernels.cuh"
+
+namespace dion2 {
+
+// ------------------------------------------------------------------ rows mode
+// One warp per row; a persistent grid strides over the flattened rows of all
+// row-mode matrices.  Score = per-lane sequential sum, then a fixed xor-tree:
+// deterministic run to run.
+template <bool kBf16G>
+__device__ __forceinline__ float row_pass(const MatDesc& md, int64_t r, int lane) {
+  float* __restrict__ Mrow = md.M + r * md.ld;
+  const int64_t n = md.cols;
+  float acc = 0.f;
+  if (md.vec4) {
+    const int64_t n4 = n >> 2;
+    float4* M4 = reinterpret_cast<float4*>(Mrow);
+    constexpr int U = 4;
+    int64_t j = lane;
+    for (; j + 32 * (U - 1) < n4; j += 32 * U) {
+      float4 m[U], g[U];
+#pragma unroll
+      for (int u = 0; u < U; ++u) m[u] = M4[j + 32 * u];
+#pragma unroll
+      for (int u = 0; u < U; ++u) {
+        if constexpr (kBf16G) {
+          const uint2 raw = __ldg(reinterpret_cast<const uint2*>(
+                                      reinterpret_cast<const __nv_bfloat16*>(md.G) + r * md.ld) +
+                                  (j + 32 * u));
+          const __nv_bfloat162 lo = *reinterpret_cast<const __nv_bfloat162*>(&raw.x);
+          const __nv_bfloat162 hi = *reinterpret_cast<const __nv_bfloat162*>(&raw.y);
+          g[u] = make_float4(__low2float(lo), __high2float(lo), __low2float(hi), __high2float(hi));
+        } else {
+          g[u] = __ldg(reinterpret_cast<const float4*>(reinterpret_cast<const float*>(md.G) + r * md.ld) + (j + 32 * u));
+        }
+      }
+#pragma unroll
+      for (int u = 0; u < U; ++u) {
+        m[u].x += g[u].x; m[u].y += g[u].y; m[u].z += g[u].z; m[u].w += g[u].w;
+        M4[j + 32 * u] = m[u];
+        acc += fabsf(m[u].x) + fabsf(m[u].y) + fabsf(m[u].z) + fabsf(m[u].w);
+      }
+    }
+    for (; j < n4; j += 32) {
+      float4 m = M4[j];
+      float4 g;
+      if constexpr (kBf16G) {
+        const __nv_bfloat16* gr = reinterpret_cast<const __nv_bfloat16*>(md.G) + r * md.ld + 4 * j;
+        g = make_float4(bf16_to_f(gr[0]), bf16_to_f(gr[1]), bf16_to_f(gr[2]), bf16_to_f(gr[3]));
+      } else {
+        g = __ldg(reinterpret_cast<const float4*>(reinterpret_cast<const float*>(md.G) + r * md.ld) + j);
+      }
+      m.x += g.x; m.y += g.y; m.z += g.z; m.w += g.w;
+      M4[j] = m;
+      acc += fabsf(m.x) + fabsf(m.y) + fabsf(m.z) + fabsf(m.w);
+    }
+    for (int64_t t = 4 * n4 + lane; t < n; t += 32) {
+      float g = kBf16G ? bf16_to_f(reinterpret_cast<const __nv_bfloat16*>(md.G)[r * md.ld + t])
+                       : reinterpret_cast<const float*>(md.G)[r * md.ld + t];
+      float m = Mrow[t] + g;
+      Mrow[t] = m;
+      acc += fabsf(m);
+    }
+  } else {
+    for (int64_t t = lane; t < n; t += 32) {
+      float g = kBf16G ? bf16_to_f(reinterpret_cast<const __nv_bfloat16*>(md.G)[r * md.ld + t])
+                       : reinterpret_cast<const float*>(md.G)[r * md.ld + t];
+      float m = Mrow[t] + g;
+      Mrow[t] = m;
+      acc += fabsf(m);
+    }
+  }
+  return warp_sum(acc);
+}
+
+__global__ void __launch_bounds__(256) k_momentum_score_rows(const MatDesc* __restrict__ mats,
+                                                             const int32_t* __restrict__ row_mats,
+                                                             const int64_t* __restrict__ row_prefix, int n_row_mats,
+                                                             int64_t total_rows) {
+  const int lane = threadIdx.x & 31;
+  const int64_t warp = (int64_t)blockIdx.x * (blockDim.x >> 5) + (threadIdx.x >> 5);
+  const int64_t nwarps = (int64_t)gridDim.x * (blockDim.x >> 5);
+  for (int64_t gr = warp; gr < total_rows; gr += nwarps) {
+    // locate the matrix: largest i with row_prefix[i] <= gr
+    int lo = 0, hi = n_row_mats - 1;
+    while (lo < hi) {
+      int mid = (lo + hi + 1) >> 1;
+      if (row_prefix[mid] <= gr) lo = mid; else hi = mid - 1;
+    }
+    const MatDesc& md = mats[row_mats[lo]];
+    const int64_t r = gr - row_prefix[lo];
+    float s = md.grad_bf16 ? row_pass<true>(md, r, lane) : row_pass<false>(md, r, lane);
+    if (lane == 0) md.scores[r] = s;
+  }
+}
+
+// ------------------------------------------------------------------ cols mode
+// Block = 64 rows x 256 columns; thread (ty in [0,4), tx in [0,64)) owns 4
+// column slots and rows ty, ty+4, ...; a fixed-order smem reduce over ty gives
+// one partial per (row block, column).  K2 sums the partials in row-block
+// order: no float atomics anywhere.
+constexpr int kColRB = 64;
+constexpr int kColCB = 256;
+
+template <bool kBf16G>
+__device__ __forceinline__ void col_tile(const MatDesc& md, int rb, int cb, float (*red)[kColCB]) {
+  const int tx = threadIdx.x & 63, ty = threadIdx.x >> 6;
+  const int64_t r0 = (int64_t)rb * kColRB;
+  const int64_t c0 = (int64_t)cb * kColCB;
+  const int64_t rend = md.rows < r0 + kColRB ? md.rows : r0 + kColRB;
+  float acc[4] = {0.f, 0.f, 0.f, 0.f};
+  const bool full4 = md.vec4 && (c0 + tx * 4 + 3 < md.cols);
+  if (full4) {
+    const int64_t c = c0 + tx * 4;
+#pragma unroll 4
+    for (int64_t r = r0 + ty; r < rend; r += 4) {
+      float4* mp = reinterpret_cast<float4*>(md.M + r * md.ld + c);
+      float4 m = *mp, g;
+      if constexpr (kBf16G) {
+        const uint2 raw = __ldg(reinterpret_cast<const uint2*>(reinterpret_cast<const __nv_bfloat16*>(md.G) + r * md.ld + c));
+        const __nv_bfloat162 lo = *reinterpret_cast<const __nv_bfloat162*>(&raw.x);
+        const __nv_bfloat162 hi = *reinterpret_cast<const __nv_bfloat162*>(&raw.y);
+        g = make_float4(__low2float(lo), __high2float(lo), __low2float(hi), __high2float(hi));
+      } else {
+        g = __ldg(reinterpret_cast<const float4*>(reinterpret_cast<const float*>(md.G) + r * md.ld + c));
+      }
+      m.x += g.x; m.y += g.y; m.z += g.z; m.w += g.w;
+      *mp = m;
+      acc[0] += fabsf(m.x); acc[1] += fabsf(m.y); acc[2] += fabsf(m.z); acc[3] += fabsf(m.w);
+    }
+#pragma unroll
+    for (int s = 0; s < 4; ++s) red[ty][tx * 4 + s] = acc[s];
+  } else {
+    // scalar slots: column c0 + tx*4 + s (same slot map as above)
+    for (int64_t r = r0 + ty; r < rend; r += 4) {
+#pragma unroll
+      for (int s = 0; s < 4; ++s) {
+        const int64_t c = c0 + tx * 4 + s;
+        if (c < md.cols) {
+          float g = kBf16G ? bf16_to_f(reinterpret_cast<const __nv_bfloat16*>(md.G)[r * md.ld + c])
+                           : reinterpret_cast<const float*>(md.G)[r * md.ld + c];
+          float m = md.M[r * md.ld + c] + g;
+          md.M[r * md.ld + c] = m;
+          acc[s] += fabsf(m);
+        }
+      }
+    }
+#pragma unroll
+    for (int s = 0; s < 4; ++s) red[ty][tx * 4 + s] = acc[s];
+  }
+  __syncthreads();
+  {
+    const int c = threadIdx.x;  // 256 threads cover the 256 columns of the tile
+    const int64_t col = c0 + c;
+    if (col < md.cols) {
+      float v = ((red[0][c] + red[1][c]) + red[2][c]) + red[3][c];
+      md.col_partials[(int64_t)rb * md.cols + col] = v;
+    }
+  }
+  __syncthreads();
+}
+
+__global__ void __launch_bounds__(256) k_momentum_score_cols(const MatDesc* __restrict__ mats,
+                                                             const int32_t* __restrict__ col_mats,
+                                                             const int64_t* __restrict__ tile_prefix, int n_col_mats,
+                                                             int64_t total_tiles) {
+  __shared__ float red[4][kColCB];
+  for (int64_t t = blockIdx.x; t < total_tiles; t += gridDim.x) {
+    int lo = 0, hi = n_col_mats - 1;
+    while (lo < hi) {
+      int mid = (lo + hi + 1) >> 1;
+      if (tile_prefix[mid] <= t) lo = mid; else hi = mid - 1;
+    }
+    const MatDesc& md = mats[col_mats[lo]];
+    const int64_t local = t - tile_prefix[lo];
+    const int cbs = (int)((md.cols + kColCB - 1) / kColCB);
+    const int rb = (int)(local / cbs), cb = (int)(local % cbs);
+    if (md.grad_bf16) col_tile<true>(md, rb, cb, red);
+    else col_tile<false>(md, rb, cb, red);
+  }
+}
+
+}  // namespace dion2

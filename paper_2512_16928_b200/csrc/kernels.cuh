@@ -1,0 +1,71 @@
+// kernels.cuh -- kernel entry points of the Dion2 step (launched by dion2_api.cu).
+#pragma once
+#include "common.cuh"
+
+namespace dion2 {
+
+// ---------------- K1 momentum + l1 score (k_momentum_score.cu)
+__global__ void k_momentum_score_rows(const MatDesc* __restrict__ mats, const int32_t* __restrict__ row_mats,
+                                      const int64_t* __restrict__ row_prefix, int n_row_mats, int64_t total_rows);
+__global__ void k_momentum_score_cols(const MatDesc* __restrict__ mats, const int32_t* __restrict__ col_mats,
+                                      const int64_t* __restrict__ tile_prefix, int n_col_mats, int64_t total_tiles);
+
+// ---------------- K2 top-k select (k_select.cu)
+constexpr int kSelectThreads = 1024;
+__global__ void k_topk_select(const MatDesc* __restrict__ mats, int32_t* __restrict__ bad, int32_t* __restrict__ status);
+
+// ---------------- K3 gather + decay + sum of squares, norm finalize; K7 scatter (k_gather_scatter.cu)
+constexpr int kTileA = 32;   // S rows per gather/scatter tile
+constexpr int kTileB = 64;   // S cols per gather/scatter tile
+// host launchers (the templates are instantiated in their own translation unit)
+void launch_gather_decay(bool bf16, int blocks, cudaStream_t s, const MatDesc* mats, const int32_t* tile_prefix_mats,
+                         int n_mats, int total_tiles, const int32_t* bad, int decay, float mu);
+void launch_scatter_update(bool bf16, int blocks, cudaStream_t s, const MatDesc* mats, const int32_t* tile_prefix_mats,
+                           int n_mats, int total_tiles, const int32_t* bad, float lr);
+__global__ void k_norm_finalize(const MatDesc* __restrict__ mats, int n_mats, float eps);
+__global__ void k_full_decay(const MatDesc* __restrict__ mats, int n_mats, const int32_t* __restrict__ bad, float mu);
+
+// ---------------- K4-K6 Newton-Schulz GEMMs
+// D = oscale * (cacc * Aop . Bop + cC * C), written as OutT.
+//   Aop: [M x K] row-major (K-major); Bop(k, n) = B[n][k] (b_kmajor) or B[k][n].
+constexpr int kMaxGroups = 4;
+
+struct NsGroup {
+  int count;                 // matrices in the group
+  int m_tiles, n_tiles, k_blocks;
+  int tile_base;             // first global tile of the group
+  const int32_t* gmats;      // [count] global matrix index (for the per-matrix scale)
+  const void* a;  long long a_mstride; int lda;
+  const void* b;  long long b_mstride; int ldb;
+  void* out;      long long out_mstride; int out_ld;
+  const void* cin; long long cin_mstride; int cin_ld;
+};
+
+struct NsParams {
+  NsGroup g[kMaxGroups];
+  int ngroups, total_tiles;
+  float cacc, cC;
+  int scale_sel;             // 0: oscale = 1; 1: s; 2: s^2
+  const float* ns_scale_all; // [n_mats][2]
+  int b_kmajor;
+};
+
+// tcgen05 path (k_ns_tcgen05.cu): tensor maps for the TMA operand loads.
+struct NsTcParams {
+  CUtensorMap mapA[kMaxGroups];
+  CUtensorMap mapB[kMaxGroups];
+  NsParams p;
+};
+void ns_tc_set_attrs();
+void launch_ns_tc(int bn, int grid, cudaStream_t s, const NsTcParams& P);
+template <int BN>
+constexpr int ns_tc_stages() { return BN == 256 ? 4 : 6; }
+template <int BN>
+constexpr int ns_tc_smem_bytes() {
+  return 1024 /*align slack*/ + ns_tc_stages<BN>() * (128 * 64 * 2 + BN * 64 * 2) + 256 /*barriers*/;
+}
+
+// fp32 SIMT validation path (k_ns_simt.cu): grid (n_tiles, m_tiles, count) per group.
+__global__ void k_ns_gemm_simt_f32(const NsParams P, int group);
+
+}  // namespace dion2

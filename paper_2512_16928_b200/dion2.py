@@ -1,0 +1,200 @@
+"""Thin ctypes binding over libdion2.so (include/dion2.h).
+
+Argument marshalling only: every step of the Dion2 update runs in the CUDA
+kernels behind the C ABI.  PyTorch supplies device memory and the current
+stream.  There is no CPU fallback: if the extension is missing or a tensor is
+not on a CUDA device, these functions raise.
+"""
+from __future__ import annotations
+
+import ctypes
+import os
+from typing import Dict, List, Optional, Sequence, Tuple
+
+import torch
+
+_PKG = os.path.dirname(os.path.abspath(__file__))
+LIB_PATH = os.path.join(_PKG, "lib", "libdion2.so")
+
+MAX_NS_STEPS = 16
+AXIS = {"rows": 0, "cols": 1, "auto": 2}
+PRECISION = {"bf16": 0, "fp32": 1}
+STATUS = {0: "OK", 1: "EINVAL_CONFIG", 2: "EINVAL_SHAPE", 3: "EWORKSPACE", 4: "EUNSUPPORTED",
+          5: "ECUDA", 6: "ENCCL", 7: "ENONFINITE"}
+EXPORTED = ["dion2_config_init", "dion2_workspace_size", "dion2_step", "dion2_step_batched", "dion2_get_status",
+            "dion2_strerror", "dion2_set_phase_timing", "dion2_get_phase_times", "dion2_phase_name",
+            "dion2_last_launch_count", "dion2_abi_version"]
+
+
+class Dion2Matrix(ctypes.Structure):
+    _fields_ = [("rows", ctypes.c_int64), ("cols", ctypes.c_int64), ("ld", ctypes.c_int64),
+                ("W", ctypes.c_void_p), ("M", ctypes.c_void_p), ("G", ctypes.c_void_p),
+                ("sel_out", ctypes.c_void_p), ("O_out", ctypes.c_void_p)]
+
+
+class Dion2Config(ctypes.Structure):
+    _fields_ = [("alpha", ctypes.c_float), ("mu", ctypes.c_float), ("lr", ctypes.c_float),
+                ("ns_steps", ctypes.c_int32), ("ns_coeffs", (ctypes.c_float * 3) * MAX_NS_STEPS),
+                ("ns_eps", ctypes.c_float), ("axis", ctypes.c_int32), ("select", ctypes.c_int32),
+                ("precision", ctypes.c_int32), ("grad_dtype", ctypes.c_int32), ("decay_mode", ctypes.c_int32),
+                ("scale_mode", ctypes.c_int32), ("seed", ctypes.c_uint64), ("step", ctypes.c_uint64)]
+
+
+class Dion2Error(RuntimeError):
+    def __init__(self, code: int, where: str):
+        self.code = code
+        super().__init__(f"{where}: {STATUS.get(code, code)} ({_lib().dion2_strerror(code).decode()})")
+
+
+_LIB = None
+
+
+def _lib():
+    global _LIB
+    if _LIB is None:
+        if not os.path.exists(LIB_PATH):
+            raise RuntimeError(f"libdion2.so not built ({LIB_PATH}); run python -m paper_2512_16928_b200._build")
+        lib = ctypes.CDLL(LIB_PATH)
+        P = ctypes.POINTER
+        lib.dion2_config_init.argtypes = [P(Dion2Config)]
+        lib.dion2_workspace_size.argtypes = [P(Dion2Matrix), ctypes.c_int32, P(Dion2Config), P(ctypes.c_size_t)]
+        lib.dion2_step.argtypes = [P(Dion2Matrix), P(Dion2Config), ctypes.c_void_p, ctypes.c_size_t, ctypes.c_void_p]
+        lib.dion2_step_batched.argtypes = [P(Dion2Matrix), ctypes.c_int32, P(Dion2Config), ctypes.c_void_p,
+                                           ctypes.c_size_t, ctypes.c_void_p]
+        lib.dion2_get_status.argtypes = [ctypes.c_void_p, P(ctypes.c_int32)]
+        lib.dion2_strerror.argtypes = [ctypes.c_int]
+        lib.dion2_strerror.restype = ctypes.c_char_p
+        lib.dion2_set_phase_timing.argtypes = [ctypes.c_int32]
+        lib.dion2_get_phase_times.argtypes = [P(ctypes.c_float), P(ctypes.c_int32), ctypes.c_int32, P(ctypes.c_int32)]
+        lib.dion2_phase_name.argtypes = [ctypes.c_int32]
+        lib.dion2_phase_name.restype = ctypes.c_char_p
+        lib.dion2_last_launch_count.restype = ctypes.c_int32
+        lib.dion2_abi_version.restype = ctypes.c_int32
+        _LIB = lib
+    return _LIB
+
+
+def make_config(alpha: float = 0.25, mu: float = 0.95, lr: float = 0.02, ns_steps: int = 5,
+                ns_coeffs: Optional[Sequence[Tuple[float, float, float]]] = None, ns_eps: float = 1e-7,
+                axis: str = "auto", precision: str = "bf16", grad_dtype: Optional[torch.dtype] = None,
+                decay_mode: int = 0, scale_mode: int = 0) -> Dion2Config:
+    cfg = Dion2Config()
+    _lib().dion2_config_init(ctypes.byref(cfg))
+    cfg.alpha, cfg.mu, cfg.lr, cfg.ns_steps, cfg.ns_eps = alpha, mu, lr, ns_steps, ns_eps
+    if ns_coeffs is not None:
+        if len(ns_coeffs) != ns_steps:
+            raise ValueError("ns_coeffs must have ns_steps rows")
+        for t, (a, b, c) in enumerate(ns_coeffs):
+            cfg.ns_coeffs[t][0], cfg.ns_coeffs[t][1], cfg.ns_coeffs[t][2] = a, b, c
+    cfg.axis = AXIS[axis]
+    cfg.precision = PRECISION[precision]
+    cfg.grad_dtype = 1 if grad_dtype == torch.bfloat16 else 0
+    cfg.decay_mode, cfg.scale_mode = decay_mode, scale_mode
+    return cfg
+
+
+def _check_tensor(t: torch.Tensor, name: str, dtype: torch.dtype, like: Optional[torch.Tensor] = None):
+    if not t.is_cuda:
+        raise ValueError(f"{name} must be a CUDA tensor (no CPU path exists)")
+    if t.dtype != dtype:
+        raise ValueError(f"{name} must be {dtype}, got {t.dtype}")
+    if t.dim() != 2 or t.stride(1) != 1:
+        raise ValueError(f"{name} must be 2-D with unit column stride")
+    if like is not None and (t.shape != like.shape or t.stride(0) != like.stride(0)):
+        raise ValueError(f"{name} must match W's shape and row stride")
+
+
+def describe(Ws: Sequence[torch.Tensor], Ms: Sequence[torch.Tensor], Gs: Sequence[torch.Tensor],
+             sel_out: Optional[Sequence[Optional[torch.Tensor]]] = None,
+             O_out: Optional[Sequence[Optional[torch.Tensor]]] = None):
+    n = len(Ws)
+    if not (len(Ms) == n and len(Gs) == n) or n == 0:
+        raise ValueError("Ws, Ms, Gs must be non-empty and equally long")
+    arr = (Dion2Matrix * n)()
+    gdt = Gs[0].dtype
+    for i, (W, M, G) in enumerate(zip(Ws, Ms, Gs)):
+        _check_tensor(W, "W", torch.float32)
+        _check_tensor(M, "M", torch.float32, W)
+        _check_tensor(G, "G", gdt, W)
+        arr[i].rows, arr[i].cols, arr[i].ld = W.shape[0], W.shape[1], W.stride(0)
+        arr[i].W, arr[i].M, arr[i].G = W.data_ptr(), M.data_ptr(), G.data_ptr()
+        s = sel_out[i] if sel_out is not None else None
+        o = O_out[i] if O_out is not None else None
+        arr[i].sel_out = s.data_ptr() if s is not None else None
+        arr[i].O_out = o.data_ptr() if o is not None else None
+    return arr, gdt
+
+
+def workspace_bytes(shapes: Sequence[Tuple[int, int]], **cfg_kw) -> int:
+    n = len(shapes)
+    arr = (Dion2Matrix * n)()
+    for i, (m, nn) in enumerate(shapes):
+        arr[i].rows, arr[i].cols, arr[i].ld = m, nn, nn
+    cfg = make_config(**cfg_kw)
+    out = ctypes.c_size_t(0)
+    rc = _lib().dion2_workspace_size(arr, n, ctypes.byref(cfg), ctypes.byref(out))
+    if rc:
+        raise Dion2Error(rc, "dion2_workspace_size")
+    return out.value
+
+
+class Dion2:
+    """Stateful convenience wrapper: caches the config and a workspace tensor.
+
+    opt = Dion2(alpha=0.25); opt.step(Ws, Ms, Gs)   # all on one CUDA device
+    """
+
+    def __init__(self, **cfg_kw):
+        self.cfg_kw = dict(cfg_kw)
+        self._ws: Optional[torch.Tensor] = None
+
+    def workspace(self, arr, n, cfg, device) -> torch.Tensor:
+        need = ctypes.c_size_t(0)
+        rc = _lib().dion2_workspace_size(arr, n, ctypes.byref(cfg), ctypes.byref(need))
+        if rc:
+            raise Dion2Error(rc, "dion2_workspace_size")
+        if self._ws is None or self._ws.numel() < need.value or self._ws.device != device:
+            self._ws = torch.empty(need.value, dtype=torch.uint8, device=device)
+        return self._ws
+
+    def step(self, Ws, Ms, Gs, sel_out=None, O_out=None, stream: Optional[torch.cuda.Stream] = None, **override):
+        kw = dict(self.cfg_kw)
+        kw.update(override)
+        arr, gdt = describe(Ws, Ms, Gs, sel_out, O_out)
+        kw.setdefault("grad_dtype", gdt)
+        cfg = make_config(**kw)
+        dev = Ws[0].device
+        ws = self.workspace(arr, len(Ws), cfg, dev)
+        st = stream if stream is not None else torch.cuda.current_stream(dev)
+        rc = _lib().dion2_step_batched(arr, len(Ws), ctypes.byref(cfg), ws.data_ptr(), ws.numel(), st.cuda_stream)
+        if rc:
+            raise Dion2Error(rc, "dion2_step_batched")
+
+    def status(self) -> Tuple[int, int]:
+        bad = ctypes.c_int32(-1)
+        rc = _lib().dion2_get_status(self._ws.data_ptr() if self._ws is not None else None, ctypes.byref(bad))
+        return rc, bad.value
+
+
+def step(W, M, G, **kw):
+    """One Dion2 step on one matrix (dion2_step)."""
+    Dion2(**kw).step([W], [M], [G])
+
+
+def set_phase_timing(enable: bool) -> None:
+    _lib().dion2_set_phase_timing(1 if enable else 0)
+
+
+def get_phase_times() -> Dict[str, Tuple[float, int]]:
+    cap = 16
+    ms = (ctypes.c_float * cap)()
+    cnt = (ctypes.c_int32 * cap)()
+    n = ctypes.c_int32(0)
+    rc = _lib().dion2_get_phase_times(ms, cnt, cap, ctypes.byref(n))
+    if rc:
+        raise Dion2Error(rc, "dion2_get_phase_times")
+    return {_lib().dion2_phase_name(i).decode(): (ms[i], cnt[i]) for i in range(n.value)}
+
+
+def last_launch_count() -> int:
+    return int(_lib().dion2_last_launch_count())

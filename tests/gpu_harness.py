@@ -1,0 +1,121 @@
+"""Shared GPU-vs-oracle parity harness (used by the -m gpu tests, smoke() and bench).
+
+Protocol: identical fp32 inputs on both sides (host
+NumPy generation, copied to the device; the oracle converts the same fp32
+values to fp64 exactly).  Both sides run T steps; index sets must agree
+exactly except at legitimate near-ties (|s_i - s_(k)| <= 1e-6 s_(k) with the
+oracle's fp64 scores), where the oracle adopts the GPU's set (force_K) so the
+trajectories stay aligned.  Weights are compared on the cumulative update
+dW = W_T - W_0 (relative Frobenius).
+"""
+from __future__ import annotations
+
+import math
+from dataclasses import dataclass, field
+from typing import List, Optional, Sequence, Tuple
+
+import numpy as np
+import torch
+
+import oracle as O
+from synth import gen_grad, gen_w0
+from paper_2512_16928_b200 import Dion2
+
+TIE_REL = 1e-6
+
+
+@dataclass
+class ParityResult:
+    dW_rel: List[float] = field(default_factory=list)      # per matrix
+    W_rel: List[float] = field(default_factory=list)
+    M_rel: List[float] = field(default_factory=list)        # max|dM| / max|M|
+    O_rel: List[float] = field(default_factory=list)        # last-step O, relative Frobenius
+    ties: int = 0
+    index_mismatch: int = 0
+    unselected_w_bitwise: bool = True
+    unselected_m_bitwise: bool = True
+
+
+def oracle_cfg(alpha, axis, mu=0.95, lr=0.02, decay_mode=0, scale_mode=0):
+    ax = {"rows": O.AXIS_ROWS, "cols": O.AXIS_COLS, "auto": O.AXIS_AUTO}[axis]
+    # the library takes alpha/mu/lr as fp32: give the oracle the same values
+    return O.OracleConfig(alpha=float(np.float32(alpha)), mu=float(np.float32(mu)), lr=float(np.float32(lr)),
+                          axis=ax, decay_mode=decay_mode, scale_mode=scale_mode)
+
+
+def _tie_equivalent(K_gpu, K_ref, scores):
+    if np.array_equal(K_gpu, K_ref):
+        return True
+    k = len(K_ref)
+    skth = np.sort(scores)[::-1][k - 1]
+    diff = np.setxor1d(K_gpu, K_ref)
+    return bool(np.all(np.abs(scores[diff] - skth) <= TIE_REL * max(skth, 1e-300)))
+
+
+def run_parity(shapes: Sequence[Tuple[int, int]], alpha: float, axis: str = "auto", precision: str = "bf16",
+               steps: int = 10, seed: int = 0, mu: float = 0.95, lr: float = 0.02, row_scaled: bool = False,
+               decay_mode: int = 0, check_bitwise: bool = True, device: str = "cuda") -> ParityResult:
+    res = ParityResult()
+    cfg_o = oracle_cfg(alpha, axis, mu, lr, decay_mode)
+    W0 = [gen_w0(m, n, seed, i) for i, (m, n) in enumerate(shapes)]
+    Wg = [torch.from_numpy(w).to(device) for w in W0]
+    Mg = [torch.zeros(m, n, device=device) for (m, n) in shapes]
+    Wr = [w.astype(np.float64) for w in W0]
+    Mr = [np.zeros((m, n)) for (m, n) in shapes]
+    opt = Dion2(alpha=alpha, mu=mu, lr=lr, axis=axis, precision=precision, decay_mode=decay_mode)
+    ks = []
+    for (m, n) in shapes:
+        ax = O.resolve_axis(m, n, cfg_o.axis)
+        ks.append(O.select_count(cfg_o.alpha, m if ax == O.AXIS_ROWS else n))
+    for t in range(steps):
+        G = [gen_grad(m, n, seed, i, t, row_scaled=row_scaled) for i, (m, n) in enumerate(shapes)]
+        Gg = [torch.from_numpy(g).to(device) for g in G]
+        sel = [torch.empty(k, dtype=torch.int32, device=device) for k in ks]
+        Oo = []
+        for i, (m, n) in enumerate(shapes):
+            ax = O.resolve_axis(m, n, cfg_o.axis)
+            Oo.append(torch.empty((ks[i], n) if ax == O.AXIS_ROWS else (m, ks[i]), device=device))
+        if check_bitwise:
+            Wb = [w.clone() for w in Wg]
+            Mb = [mm.clone() for mm in Mg]
+        opt.step(Wg, Mg, Gg, sel_out=sel, O_out=Oo)
+        torch.cuda.synchronize()
+        for i, (m, n) in enumerate(shapes):
+            Kg = sel[i].cpu().numpy().astype(np.int64)
+            g64 = G[i].astype(np.float64)
+            Wsave, Msave = Wr[i].copy(), Mr[i].copy()
+            K, Oref, ax = O.dion2_step(Wr[i], Mr[i], g64, cfg_o)
+            if not np.array_equal(K, Kg):
+                scores = O.l1_scores(Msave + g64, ax)
+                if _tie_equivalent(Kg, K, scores):
+                    res.ties += 1
+                    Wr[i], Mr[i] = Wsave, Msave
+                    K, Oref, ax = O.dion2_step(Wr[i], Mr[i], g64, cfg_o, force_K=Kg)
+                else:
+                    res.index_mismatch += 1
+            if t == steps - 1:
+                og = Oo[i].cpu().numpy().astype(np.float64)
+                res.O_rel.append(float(np.linalg.norm(og - Oref) / max(np.linalg.norm(Oref), 1e-300)))
+            if check_bitwise:
+                # unselected rows/cols: W bit-identical, M == fp32(M_prev + G) bit-identical
+                unsel = np.ones(m if ax == O.AXIS_ROWS else n, bool)
+                unsel[Kg] = False
+                wb, wa = Wb[i].cpu().numpy(), Wg[i].cpu().numpy()
+                mb, ma = Mb[i].cpu().numpy(), Mg[i].cpu().numpy()
+                expect_m = (mb + G[i]).astype(np.float32)
+                if decay_mode == 0:
+                    if ax == O.AXIS_ROWS:
+                        res.unselected_w_bitwise &= bool(np.array_equal(wb[unsel], wa[unsel]))
+                        res.unselected_m_bitwise &= bool(np.array_equal(expect_m[unsel], ma[unsel]))
+                    else:
+                        res.unselected_w_bitwise &= bool(np.array_equal(wb[:, unsel], wa[:, unsel]))
+                        res.unselected_m_bitwise &= bool(np.array_equal(expect_m[:, unsel], ma[:, unsel]))
+    for i in range(len(shapes)):
+        wg = Wg[i].cpu().numpy().astype(np.float64)
+        dref = Wr[i] - W0[i].astype(np.float64)
+        dgpu = wg - W0[i].astype(np.float64)
+        res.dW_rel.append(float(np.linalg.norm(dgpu - dref) / max(np.linalg.norm(dref), 1e-300)))
+        res.W_rel.append(float(np.linalg.norm(wg - Wr[i]) / np.linalg.norm(Wr[i])))
+        mg = Mg[i].cpu().numpy().astype(np.float64)
+        res.M_rel.append(float(np.abs(mg - Mr[i]).max() / max(np.abs(Mr[i]).max(), 1e-300)))
+    return res

@@ -1,0 +1,121 @@
+"""C-ABI library checks that need no GPU (-m "not gpu").
+
+The library loads, exports every function include/dion2.h declares, and its
+host-side logic (config defaults, validation, workspace sizing) behaves as
+the header documents.  No compute call is made here.
+"""
+import ctypes
+import os
+import re
+
+import pytest
+
+from paper_2512_16928_b200 import _build
+from paper_2512_16928_b200 import dion2 as D
+
+ROOT = os.path.dirname(os.path.dirname(os.path.abspath(__file__)))
+
+
+@pytest.fixture(scope="module")
+def lib():
+    _build.build()
+    return D._lib()
+
+
+def _declared_functions():
+    src = open(os.path.join(ROOT, "include", "dion2.h")).read()
+    src = re.sub(r"/\*.*?\*/", "", src, flags=re.S)
+    return sorted(set(re.findall(r"\b(dion2_[a-z_]+)\s*\(", src)))
+
+
+def test_exports_every_declared_symbol(lib):
+    names = _declared_functions()
+    assert len(names) >= 10
+    for name in names:
+        assert hasattr(lib, name), name
+    assert set(names) == set(D.EXPORTED)
+
+
+def test_abi_version(lib):
+    assert lib.dion2_abi_version() == 1
+
+
+def test_config_defaults(lib):
+    cfg = D.Dion2Config()
+    assert lib.dion2_config_init(ctypes.byref(cfg)) == 0
+    assert abs(cfg.alpha - 0.25) < 1e-7 and abs(cfg.mu - 0.95) < 1e-7 and abs(cfg.lr - 0.02) < 1e-7
+    assert cfg.ns_steps == 5 and abs(cfg.ns_eps - 1e-7) < 1e-12
+    assert [round(x, 4) for x in cfg.ns_coeffs[0]] == [3.4445, -4.775, 2.0315]
+    assert cfg.axis == 2 and cfg.precision == 0 and cfg.decay_mode == 0
+
+
+def _mats(shapes):
+    arr = (D.Dion2Matrix * len(shapes))()
+    for i, (m, n) in enumerate(shapes):
+        arr[i].rows, arr[i].cols, arr[i].ld = m, n, n
+    return arr
+
+
+def _size(lib, shapes, **kw):
+    cfg = D.make_config(**kw)
+    out = ctypes.c_size_t(0)
+    rc = lib.dion2_workspace_size(_mats(shapes), len(shapes), ctypes.byref(cfg), ctypes.byref(out))
+    return rc, out.value
+
+
+def test_workspace_size_scales_with_alpha(lib):
+    shapes = [(2048, 2048), (8192, 2048), (2048, 8192)]
+    rc1, b1 = _size(lib, shapes, alpha=1.0)
+    rc2, b2 = _size(lib, shapes, alpha=0.25)
+    assert rc1 == 0 and rc2 == 0 and b1 > b2 > 0
+    # the bf16 NS buffers dominate: X ping/pong (2 x p x q) + A, B (2 x p x p), 2 bytes each
+    assert b2 >= 2 * 2 * (512 * 2048 * 3) + 2 * 2 * (512 * 512 * 3)
+
+
+@pytest.mark.parametrize("kw,code", [
+    (dict(alpha=0.0), 1), (dict(alpha=1.5), 1), (dict(mu=1.0), 1), (dict(mu=-0.1), 1), (dict(lr=-1.0), 1),
+    (dict(ns_steps=0), 1), (dict(ns_steps=17), 1), (dict(ns_eps=0.0), 1),
+])
+def test_config_validation(lib, kw, code):
+    rc, _ = _size(lib, [(64, 64)], **kw)
+    assert rc == code
+
+
+def test_random_select_unsupported(lib):
+    cfg = D.make_config()
+    cfg.select = 1
+    out = ctypes.c_size_t(0)
+    assert lib.dion2_workspace_size(_mats([(8, 8)]), 1, ctypes.byref(cfg), ctypes.byref(out)) == 4
+
+
+def test_shape_validation(lib):
+    arr = _mats([(64, 64)])
+    arr[0].ld = 32  # ld < cols
+    cfg = D.make_config()
+    out = ctypes.c_size_t(0)
+    assert lib.dion2_workspace_size(arr, 1, ctypes.byref(cfg), ctypes.byref(out)) == 2
+    assert _size(lib, [(0, 5)])[0] == 2
+    assert _size(lib, [(10, 60000)], axis="cols")[0] == 2  # selection axis longer than DION2_MAX_SELECT_DIM
+
+
+def test_step_rejects_before_touching_the_device(lib):
+    cfg = D.make_config()
+    arr = _mats([(64, 64)])  # NULL W/M/G
+    assert lib.dion2_step_batched(arr, 1, ctypes.byref(cfg), None, 0, None) == 2
+    arr[0].W = arr[0].M = arr[0].G = 16
+    assert lib.dion2_step_batched(arr, 1, ctypes.byref(cfg), None, 0, None) == 3  # no workspace
+    cfg.alpha = 2.0
+    assert lib.dion2_step_batched(arr, 1, ctypes.byref(cfg), None, 0, None) == 1
+
+
+def test_strerror(lib):
+    for c in range(8):
+        assert lib.dion2_strerror(c)
+    assert lib.dion2_phase_name(0) == b"momentum_score"
+
+
+def test_binding_refuses_cpu_tensors():
+    import torch
+    W = torch.zeros(4, 4)
+    with pytest.raises(ValueError, match="CUDA"):
+        D.describe([W], [W.clone()], [W.clone()])

@@ -1,0 +1,187 @@
+"""GPU parity: the CUDA path (through the C ABI) against the fp64 oracle (-m gpu).
+
+Gates (BASELINE.json north star):
+  * index sets exact (ties within 1e-6 relative resolved by the harness);
+  * cumulative dW within 1e-5 relative Frobenius on the fp32 validation path,
+    within 2e-2 on the bf16 tensor-core path;
+  * unselected rows/cols of W bit-identical, unselected M == fp32(M + G) bitwise.
+"""
+import numpy as np
+import pytest
+import torch
+
+import oracle as O
+from synth import gen_grad, gen_w0, layer_set_1b
+from paper_2512_16928_b200 import Dion2, get_phase_times, last_launch_count, set_phase_timing
+
+from gpu_harness import run_parity
+
+pytestmark = pytest.mark.gpu
+
+BF16_TOL = 2e-2
+FP32_TOL = 1e-5
+
+
+def _assert(res, tol):
+    assert res.index_mismatch == 0, res
+    assert max(res.dW_rel) <= tol, res
+    assert res.unselected_w_bitwise and res.unselected_m_bitwise, res
+    assert max(res.M_rel) <= 1e-5, res
+
+
+# ---------------------------------------------------------------- configs[0]: 256x128, alpha=0.25, 10 steps
+@pytest.mark.parametrize("axis", ["auto", "rows"])
+def test_config1_fp32_validation_path(axis):
+    _assert(run_parity([(256, 128)], 0.25, axis, "fp32", steps=10), FP32_TOL)
+
+
+@pytest.mark.parametrize("axis", ["auto", "rows", "cols"])
+def test_config1_bf16_tensor_core_path(axis):
+    _assert(run_parity([(256, 128)], 0.25, axis, "bf16", steps=10), BF16_TOL)
+
+
+# ---------------------------------------------------------------- ragged, multi-tile batches, every orientation
+BATCH_AUTO = [(300, 520), (520, 300), (384, 384), (130, 1030), (7, 33)]
+
+
+@pytest.mark.parametrize("precision,tol", [("fp32", FP32_TOL), ("bf16", BF16_TOL)])
+@pytest.mark.parametrize("axis,shapes", [
+    ("auto", BATCH_AUTO),
+    ("rows", [(1000, 200), (300, 520)]),      # (1000,200): k=300 > n -> X = S^T
+    ("cols", [(200, 1000), (520, 300)]),      # (200,1000): k=300 > m -> X = S
+])
+def test_ragged_batches(precision, tol, axis, shapes):
+    _assert(run_parity(shapes, 0.3, axis, precision, steps=4, row_scaled=True), tol)
+
+
+@pytest.mark.parametrize("alpha", [1.0, 0.5, 0.125])
+def test_alpha_sweep_bf16(alpha):
+    _assert(run_parity([(256, 512), (512, 256)], alpha, "auto", "bf16", steps=3), BF16_TOL)
+
+
+def test_alpha1_is_full_muon_fp32():
+    _assert(run_parity([(128, 384)], 1.0, "auto", "fp32", steps=5), FP32_TOL)
+
+
+def test_one_layer_of_the_1b_set_bf16():
+    """One transformer layer of BASELINE configs[1] at full size, alpha=0.25."""
+    _assert(run_parity(layer_set_1b(layers=1), 0.25, "auto", "bf16", steps=2, check_bitwise=True), BF16_TOL)
+
+
+def test_full_decay_ablation_fp32():
+    _assert(run_parity([(96, 160)], 0.25, "auto", "fp32", steps=3, decay_mode=1), FP32_TOL)
+
+
+# ---------------------------------------------------------------- exact selection (ties, tie-break)
+def test_select_exact_ties_lowest_index():
+    """Integer-valued G: every l1 score is exact in fp32, with many exact ties;
+    K must equal the brute-force (score desc, index asc) set bit for bit."""
+    rng = np.random.default_rng(0)
+    m, n = 700, 40
+    G = rng.integers(0, 3, size=(m, n)).astype(np.float32)
+    G[100:200] = G[0]          # exact duplicates of row 0's l1 score
+    W = torch.zeros(m, n, device="cuda")
+    M = torch.zeros(m, n, device="cuda")
+    sel = torch.empty(O.select_count(np.float32(0.25), m), dtype=torch.int32, device="cuda")
+    Dion2(alpha=0.25, axis="rows").step([W], [M], [torch.from_numpy(G).cuda()], sel_out=[sel])
+    s = np.abs(G.astype(np.float64)).sum(1)
+    want = sorted(sorted(range(m), key=lambda i: (-s[i], i))[:len(sel)])
+    assert sel.cpu().numpy().tolist() == want
+
+
+@pytest.mark.parametrize("d", [1, 2, 5, 1024, 1025, 4097, 32768])
+def test_select_sizes(d):
+    m, n = (d, 8)
+    G = gen_grad(m, n, 3, 0, 0, row_scaled=True)
+    W = torch.zeros(m, n, device="cuda")
+    M = torch.zeros(m, n, device="cuda")
+    k = O.select_count(np.float32(0.25), m)
+    sel = torch.empty(k, dtype=torch.int32, device="cuda")
+    Dion2(alpha=0.25, axis="rows").step([W], [M], [torch.from_numpy(G).cuda()], sel_out=[sel])
+    s = O.l1_scores(G.astype(np.float64), O.AXIS_ROWS)
+    ref = O.select_l1(s, k)
+    got = sel.cpu().numpy()
+    if not np.array_equal(got, ref):  # allow fp32-vs-fp64 near-ties only
+        kth = np.sort(s)[::-1][k - 1]
+        assert np.all(np.abs(s[np.setxor1d(got, ref)] - kth) <= 1e-6 * kth)
+
+
+# ---------------------------------------------------------------- edge cases
+def test_lr_zero_leaves_w_bitwise():
+    W = torch.from_numpy(gen_w0(128, 256)).cuda()
+    W0 = W.clone()
+    M = torch.zeros_like(W)
+    Dion2(alpha=0.25, lr=0.0).step([W], [M], [torch.from_numpy(gen_grad(128, 256)).cuda()])
+    assert torch.equal(W, W0)
+
+
+def test_zero_input_leaves_w_unchanged_and_selects_lowest():
+    W = torch.from_numpy(gen_w0(64, 96)).cuda()
+    W0 = W.clone()
+    M = torch.zeros_like(W)
+    sel = torch.empty(16, dtype=torch.int32, device="cuda")
+    Dion2(alpha=0.25).step([W], [M], [torch.zeros_like(W)], sel_out=[sel])
+    assert torch.equal(W, W0)
+    assert sel.cpu().tolist() == list(range(16))
+
+
+def test_nonfinite_matrix_is_skipped_and_reported():
+    Ws = [torch.from_numpy(gen_w0(64, 128, 0, i)).cuda() for i in range(3)]
+    W0 = [w.clone() for w in Ws]
+    Ms = [torch.zeros_like(w) for w in Ws]
+    Gs = [torch.from_numpy(gen_grad(64, 128, 0, i)).cuda() for i in range(3)]
+    Gs[1][5, 7] = float("nan")
+    opt = Dion2(alpha=0.25)
+    opt.step(Ws, Ms, Gs)
+    rc, bad = opt.status()
+    assert rc == 7 and bad == 1
+    assert torch.equal(Ws[1], W0[1])
+    assert not torch.equal(Ws[0], W0[0]) and not torch.equal(Ws[2], W0[2])
+    # the next clean step clears the status
+    Gs[1].zero_()
+    opt.step(Ws, Ms, [torch.zeros_like(g) for g in Gs])
+    assert opt.status() == (0, -1)
+
+
+def test_bitwise_determinism():
+    shapes = [(512, 1024), (1024, 512)]
+    outs = []
+    for _ in range(2):
+        Ws = [torch.from_numpy(gen_w0(m, n, 1, i)).cuda() for i, (m, n) in enumerate(shapes)]
+        Ms = [torch.zeros_like(w) for w in Ws]
+        opt = Dion2(alpha=0.25)
+        for t in range(3):
+            opt.step(Ws, Ms, [torch.from_numpy(gen_grad(m, n, 1, i, t)).cuda() for i, (m, n) in enumerate(shapes)])
+        outs.append([w.clone() for w in Ws] + [mm.clone() for mm in Ms])
+    for a, b in zip(*outs):
+        assert torch.equal(a, b)
+
+
+def test_bf16_gradient_input():
+    _m, _n = 256, 512
+    W = torch.from_numpy(gen_w0(_m, _n)).cuda()
+    W0 = W.clone()
+    M = torch.zeros_like(W)
+    G = torch.from_numpy(gen_grad(_m, _n)).cuda()
+    Gb = G.to(torch.bfloat16)
+    Dion2(alpha=0.25).step([W], [M], [Gb])
+    # momentum accumulated exactly the bf16 values
+    Wr, Mr = W0.cpu().double().numpy(), np.zeros((_m, _n))
+    O.dion2_step(Wr, Mr, Gb.float().cpu().double().numpy(), O.OracleConfig(alpha=0.25))
+    dref = Wr - W0.cpu().double().numpy()
+    dgpu = W.cpu().double().numpy() - W0.cpu().double().numpy()
+    assert np.linalg.norm(dgpu - dref) / np.linalg.norm(dref) <= BF16_TOL
+
+
+def test_phase_timing_and_launch_count():
+    Ws = [torch.from_numpy(gen_w0(256, 512)).cuda()]
+    Ms = [torch.zeros_like(Ws[0])]
+    set_phase_timing(True)
+    try:
+        Dion2(alpha=0.25).step(Ws, Ms, [torch.ones_like(Ws[0])])
+        times = get_phase_times()
+    finally:
+        set_phase_timing(False)
+    assert last_launch_count() >= 7
+    for ph in ("momentum_score", "select", "gather", "ns_gram", "ns_poly", "ns_apply", "scatter"):
+        assert times[ph][1] >= 1 and times[ph][0] > 0
