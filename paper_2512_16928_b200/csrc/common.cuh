@@ -42,6 +42,7 @@ struct MatDesc {
   void* X1;               // pong
   int32_t final_in_x1;    // X_T lives in X1 (T odd)
   int32_t gather_tile_base, gather_tiles_a, gather_tiles_b;
+  int32_t sa_pad, sb_pad;  // padded extents of S such that wide(S_pad) = X_pad (p_pad x q_pad)
   int32_t rowblocks;      // ceil(rows/64) (cols mode partials)
 };
 

@@ -6,6 +6,8 @@
 
 #include <algorithm>
 #include <cmath>
+#include <cstdio>
+#include <cstdlib>
 #include <cstring>
 #include <map>
 #include <memory>
@@ -108,7 +110,7 @@ int validate_shape(const dion2_matrix& m, bool need_ptrs) {
 
 // ------------------------------------------------------------------ plan
 struct MatPlan {
-  int axis, d, o, k, sr, sc, transposed, p, q, p_pad, q_pad, group, zi, rowblocks, ga, gb;
+  int axis, d, o, k, sr, sc, transposed, p, q, p_pad, q_pad, group, zi, rowblocks, ga, gb, sa_pad, sb_pad;
   float fan_sqrt;
   size_t off_scores, off_partials, off_sel, off_sumsq;
 };
@@ -142,10 +144,14 @@ struct Plan {
   void* ws = nullptr;
   uint64_t id = 0;
   std::vector<const void*> last_ptrs;  // W, M, G, sel_out, O_out per matrix as last uploaded
+  void* dtab = nullptr;                // plan-owned device copy of host_tables
 };
 
+// device address of a table offset (tables are carved with workspace-style offsets
+// starting at off_desc but live in the plan-owned buffer)
+inline void* tab(Plan& P, size_t off) { return static_cast<uint8_t*>(P.dtab) + (off - P.off_desc); }
+
 std::map<std::string, std::unique_ptr<Plan>> g_plans;
-std::map<void*, uint64_t> g_ws_last_plan;  // workspace -> id of the plan whose tables it holds
 uint64_t g_next_plan_id = 1;
 
 std::string plan_key(const dion2_matrix* mats, int n, const dion2_config* c, void* ws) {
@@ -200,8 +206,12 @@ int build_layout(Plan& P, const dion2_matrix* mats, int n, const dion2_config* c
     if (c->scale_mode == 0) q.fan_sqrt = (float)std::sqrt((double)rows / (double)cols);  // Alg. 1 l.6
     else q.fan_sqrt = (float)std::sqrt((double)q.sr / (double)q.sc);
     q.rowblocks = (int)ceil_div(rows, 64);
-    q.ga = (int)ceil_div(q.sr, kTileA);
-    q.gb = (int)ceil_div(q.sc, kTileB);
+    // gather tiles cover the padded extent of S (wide(S_pad) = X_pad) so K3 also
+    // rewrites X's zero padding every step
+    q.sa_pad = q.transposed ? q.q_pad : q.p_pad;
+    q.sb_pad = q.transposed ? q.p_pad : q.q_pad;
+    q.ga = (int)ceil_div(q.sa_pad, kTileA);
+    q.gb = (int)ceil_div(q.sb_pad, kTileB);
     auto key = std::make_pair(q.p_pad, q.q_pad);
     auto it = gidx.find(key);
     if (it == gidx.end()) {
@@ -264,6 +274,7 @@ int build_device_plan(Plan& P, const dion2_matrix* mats, const dion2_config* c, 
   P.ws = ws;
   const int n = P.n;
   P.host_tables.assign(P.off_nsscale - P.off_desc, 0);
+  if (!P.dtab && cudaMalloc(&P.dtab, P.host_tables.size()) != cudaSuccess) return DION2_ECUDA;
   auto H = [&](size_t off) { return P.host_tables.data() + (off - P.off_desc); };
   MatDesc* D = reinterpret_cast<MatDesc*>(H(P.off_desc));
   std::vector<int32_t> rowmats, colmats;
@@ -295,6 +306,8 @@ int build_device_plan(Plan& P, const dion2_matrix* mats, const dion2_config* c, 
     d.gather_tile_base = gt_acc;
     d.gather_tiles_a = q.ga;
     d.gather_tiles_b = q.gb;
+    d.sa_pad = q.sa_pad;
+    d.sb_pad = q.sb_pad;
     d.rowblocks = q.rowblocks;
     gprefix[i] = gt_acc;
     gt_acc += q.ga * q.gb;
@@ -362,7 +375,7 @@ int build_device_plan(Plan& P, const dion2_matrix* mats, const dion2_config* c, 
             void* Bm = at(ws, g.off_B);
             NsGroup& G = np.g[j];
             G.count = g.count;
-            G.gmats = (const int32_t*)at(ws, g.off_gmats);
+            G.gmats = (const int32_t*)tab(P, g.off_gmats);
             const long long xs = (long long)g.p_pad * g.q_pad, as = (long long)g.p_pad * g.p_pad;
             if (ph == PH_GRAM) {
               G.m_tiles = g.p_pad / 128; G.n_tiles = g.p_pad / BN; G.k_blocks = g.q_pad / 64;
@@ -448,6 +461,15 @@ struct Launcher {
       cudaGetLastError();
       err = DION2_ECUDA;
     }
+    static const bool debug_sync = getenv("DION2_DEBUG_SYNC") != nullptr;
+    if (debug_sync) {
+      cudaError_t e = cudaStreamSynchronize(s);
+      if (e != cudaSuccess) {
+        fprintf(stderr, "[dion2] launch %d (phase %s) failed: %s\n", count, kPhaseNames[cur_phase],
+                cudaGetErrorString(e));
+        err = DION2_ECUDA;
+      }
+    }
     if (g_timing) {
       cudaEvent_t b = take_event();
       cudaEventRecord(b, s);
@@ -458,9 +480,9 @@ struct Launcher {
 
 int run_step(Plan& P, const dion2_matrix* mats, const dion2_config* c, void* ws, cudaStream_t s) {
   const int n = P.n;
-  // (re)upload descriptor tables when pointers or the workspace's owner plan changed
-  bool upload = g_ws_last_plan[ws] != P.id;
-  bool zero_ns = upload;
+  // The descriptor tables live in plan-owned device memory (the workspace is pure
+  // scratch); re-upload only when the caller's W/M/G/sel_out/O_out pointers change.
+  bool upload = false;
   if ((int)P.last_ptrs.size() != 5 * n) {
     P.last_ptrs.assign(5 * n, nullptr);
     upload = true;
@@ -481,21 +503,14 @@ int run_step(Plan& P, const dion2_matrix* mats, const dion2_config* c, void* ws,
     D[i].vec4 = al ? 1 : 0;
   }
   if (upload) {
-    if (cudaMemcpyAsync(at(ws, P.off_desc), P.host_tables.data(), P.host_tables.size(), cudaMemcpyHostToDevice, s) !=
-        cudaSuccess)
-      return DION2_ECUDA;
-    g_ws_last_plan[ws] = P.id;
-  }
-  if (zero_ns) {
-    // NS buffers must hold zeros in their padding (zero rows/cols are exact no-ops for NS)
-    if (cudaMemsetAsync(at(ws, P.off_ns_begin), 0, P.off_ns_end - P.off_ns_begin, s) != cudaSuccess)
+    if (cudaMemcpyAsync(P.dtab, P.host_tables.data(), P.host_tables.size(), cudaMemcpyHostToDevice, s) != cudaSuccess)
       return DION2_ECUDA;
   }
   // status[0] = flags (0), status[1] = first bad matrix (atomicMin from 0x7f7f7f7f)
   if (cudaMemsetAsync(at(ws, P.off_status), 0, 4, s) != cudaSuccess) return DION2_ECUDA;
   if (cudaMemsetAsync(at(ws, P.off_status + 4), 0x7f, 4, s) != cudaSuccess) return DION2_ECUDA;
 
-  const MatDesc* dmats = (const MatDesc*)at(ws, P.off_desc);
+  const MatDesc* dmats = (const MatDesc*)tab(P, P.off_desc);
   int32_t* bad = (int32_t*)at(ws, P.off_bad);
   int32_t* status = (int32_t*)at(ws, P.off_status);
   Launcher L{s};
@@ -505,16 +520,16 @@ int run_step(Plan& P, const dion2_matrix* mats, const dion2_config* c, void* ws,
   if (P.n_row_mats) {
     L.begin(PH_K1);
     int64_t blocks = std::min<int64_t>(ceil_div(P.total_rows, 8), (int64_t)sms * 8);
-    k_momentum_score_rows<<<(unsigned)blocks, 256, 0, s>>>(dmats, (const int32_t*)at(ws, P.off_rowmats),
-                                                           (const int64_t*)at(ws, P.off_rowprefix), P.n_row_mats,
+    k_momentum_score_rows<<<(unsigned)blocks, 256, 0, s>>>(dmats, (const int32_t*)tab(P, P.off_rowmats),
+                                                           (const int64_t*)tab(P, P.off_rowprefix), P.n_row_mats,
                                                            P.total_rows);
     L.end();
   }
   if (P.n_col_mats) {
     L.begin(PH_K1);
     int64_t blocks = std::min<int64_t>(P.total_col_tiles, (int64_t)sms * 8);
-    k_momentum_score_cols<<<(unsigned)blocks, 256, 0, s>>>(dmats, (const int32_t*)at(ws, P.off_colmats),
-                                                           (const int64_t*)at(ws, P.off_colprefix), P.n_col_mats,
+    k_momentum_score_cols<<<(unsigned)blocks, 256, 0, s>>>(dmats, (const int32_t*)tab(P, P.off_colmats),
+                                                           (const int64_t*)tab(P, P.off_colprefix), P.n_col_mats,
                                                            P.total_col_tiles);
     L.end();
   }
@@ -527,7 +542,7 @@ int run_step(Plan& P, const dion2_matrix* mats, const dion2_config* c, void* ws,
     L.begin(PH_GATHER);
     int blocks = std::min(P.total_gather_tiles, sms * 8);
     const int decay = 1;
-    launch_gather_decay(P.bf16_ns, blocks, s, dmats, (const int32_t*)at(ws, P.off_gprefix), n, P.total_gather_tiles,
+    launch_gather_decay(P.bf16_ns, blocks, s, dmats, (const int32_t*)tab(P, P.off_gprefix), n, P.total_gather_tiles,
                         bad, decay, c->mu);
     L.end();
     L.begin(PH_NORM);
@@ -552,7 +567,7 @@ int run_step(Plan& P, const dion2_matrix* mats, const dion2_config* c, void* ws,
   {
     L.begin(PH_SCATTER);
     int blocks = std::min(P.total_gather_tiles, sms * 8);
-    launch_scatter_update(P.bf16_ns, blocks, s, dmats, (const int32_t*)at(ws, P.off_gprefix), n, P.total_gather_tiles,
+    launch_scatter_update(P.bf16_ns, blocks, s, dmats, (const int32_t*)tab(P, P.off_gprefix), n, P.total_gather_tiles,
                           bad, c->lr);
     L.end();
   }

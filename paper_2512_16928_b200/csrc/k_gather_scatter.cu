@@ -88,17 +88,20 @@ __global__ void __launch_bounds__(256) k_gather_decay(const MatDesc* __restrict_
       for (int w = 0; w < 8; ++w) s += wsum[w];
       md.sumsq_partials[local] = s;
     }
+    // The tile grid covers the padded extent of X, so every step also rewrites
+    // X's zero padding (zero rows / columns are exact no-ops for NS) and the
+    // workspace needs no state between calls.
     XT* X = reinterpret_cast<XT*>(md.X0);
     if (!md.transposed) {
       // X[a][b] = S[a][b]
 #pragma unroll
       for (int rr = 0; rr < 2; ++rr) {
         const int al = ty + 16 * rr, a = a0 + al;
-        if (a < md.sr) {
+        if (a < md.sa_pad) {
 #pragma unroll
           for (int c = 0; c < 4; ++c) {
             const int b = b0 + tx * 4 + c;
-            if (b < md.sc) X[(int64_t)a * md.q_pad + b] = to_x<XT>(tile[al][tx * 4 + c]);
+            if (b < md.sb_pad) X[(int64_t)a * md.q_pad + b] = to_x<XT>(tile[al][tx * 4 + c]);
           }
         }
       }
@@ -106,11 +109,11 @@ __global__ void __launch_bounds__(256) k_gather_decay(const MatDesc* __restrict_
       // X[b][a] = S[a][b]: thread -> (b_local = tid/4, 8 consecutive a)
       const int bl = threadIdx.x >> 2, ac = (threadIdx.x & 3) * 8;
       const int b = b0 + bl;
-      if (b < md.sc) {
+      if (b < md.sb_pad) {
 #pragma unroll
         for (int i = 0; i < 8; ++i) {
           const int a = a0 + ac + i;
-          if (a < md.sr) X[(int64_t)b * md.q_pad + a] = to_x<XT>(tile[ac + i][bl]);
+          if (a < md.sa_pad) X[(int64_t)b * md.q_pad + a] = to_x<XT>(tile[ac + i][bl]);
         }
       }
     }
@@ -131,7 +134,7 @@ __global__ void k_norm_finalize(const MatDesc* __restrict__ mats, int n_mats, fl
   const int mi = blockIdx.x * (blockDim.x >> 5) + (threadIdx.x >> 5);
   if (mi >= n_mats) return;
   const MatDesc& md = mats[mi];
-  const int nt = ((md.sr + kTileA - 1) / kTileA) * md.gather_tiles_b;
+  const int nt = md.gather_tiles_a * md.gather_tiles_b;
   float s = 0.f;
   for (int i = lane; i < nt; i += 32) s += md.sumsq_partials[i];
   s = warp_sum(s);
@@ -155,6 +158,7 @@ __global__ void __launch_bounds__(256) k_scatter_update(const MatDesc* __restric
     const int local = t - md.gather_tile_base;
     const int ta = local / md.gather_tiles_b, tb = local % md.gather_tiles_b;
     const int a0 = ta * kTileA, b0 = tb * kTileB;
+    if (a0 >= md.sr || b0 >= md.sc) continue;  // padding-only tile (block-uniform)
     const XT* X = reinterpret_cast<const XT*>(md.final_in_x1 ? md.X1 : md.X0);
     if (md.transposed) {
       // O_S[a][b] = X[b][a]: coalesced read along a, stage in smem
