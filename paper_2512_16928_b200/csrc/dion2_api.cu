@@ -110,7 +110,8 @@ int validate_shape(const dion2_matrix& m, bool need_ptrs) {
 
 // ------------------------------------------------------------------ plan
 struct MatPlan {
-  int axis, d, o, k, sr, sc, transposed, p, q, p_pad, q_pad, group, zi, rowblocks, ga, gb, sa_pad, sb_pad;
+  int axis, d, o, k, sr, sc, transposed, p, q, p_pad, q_pad, group, zi, rowblocks, ga, gb, sa_pad, sb_pad, path,
+      n_sumsq;
   float fan_sqrt;
   size_t off_scores, off_partials, off_sel, off_sumsq;
 };
@@ -139,6 +140,10 @@ struct Plan {
       off_nsscale, off_ns_begin, off_ns_end, total;
   int64_t total_rows = 0, total_col_tiles = 0;
   int n_row_mats = 0, n_col_mats = 0, total_gather_tiles = 0, max_d = 0;
+  // streaming fast paths: list 0 = rows (units: X rows p_pad / selected rows k),
+  // list 1 = cols with X = S^T (units: 32-row slabs of X's columns, q_pad / 32)
+  size_t off_fl_mats[2], off_fl_gprefix[2], off_fl_sprefix[2];
+  int fl_n[2] = {0, 0}, fl_gunits[2] = {0, 0}, fl_sunits[2] = {0, 0}, fl_maxk = 0;
   std::vector<uint8_t> host_tables;  // [off_desc, off_ns_begin) image (descriptors + aux)
   std::vector<Launch> ns_launches;
   void* ws = nullptr;
@@ -210,8 +215,13 @@ int build_layout(Plan& P, const dion2_matrix* mats, int n, const dion2_config* c
     // rewrites X's zero padding every step
     q.sa_pad = q.transposed ? q.q_pad : q.p_pad;
     q.sb_pad = q.transposed ? q.p_pad : q.q_pad;
-    q.ga = (int)ceil_div(q.sa_pad, kTileA);
-    q.gb = (int)ceil_div(q.sb_pad, kTileB);
+    // gather/scatter path: streaming kernels for the two orientations auto mode produces
+    if (axis == DION2_AXIS_ROWS && !q.transposed && P.bf16_ns) q.path = 1;
+    else if (axis == DION2_AXIS_COLS && q.transposed && P.bf16_ns && q.k <= kMaxColKFast) q.path = 2;
+    else q.path = 0;
+    q.ga = q.path == 0 ? (int)ceil_div(q.sa_pad, kTileA) : 0;
+    q.gb = q.path == 0 ? (int)ceil_div(q.sb_pad, kTileB) : 0;
+    q.n_sumsq = q.path == 0 ? q.ga * q.gb : (q.path == 1 ? q.p_pad : q.q_pad / 32);
     auto key = std::make_pair(q.p_pad, q.q_pad);
     auto it = gidx.find(key);
     if (it == gidx.end()) {
@@ -243,6 +253,11 @@ int build_layout(Plan& P, const dion2_matrix* mats, int n, const dion2_config* c
   P.off_colmats = take(4 * (size_t)n);
   P.off_colprefix = take(8 * (size_t)n);
   P.off_gprefix = take(4 * (size_t)n);
+  for (int l = 0; l < 2; ++l) {
+    P.off_fl_mats[l] = take(4 * (size_t)n);
+    P.off_fl_gprefix[l] = take(4 * (size_t)n);
+    P.off_fl_sprefix[l] = take(4 * (size_t)n);
+  }
   for (auto& g : P.groups) g.off_gmats = take(4 * (size_t)g.count);
   P.off_nsscale = take(8 * (size_t)n);
   for (int i = 0; i < n; ++i) {
@@ -250,7 +265,7 @@ int build_layout(Plan& P, const dion2_matrix* mats, int n, const dion2_config* c
     q.off_scores = take(4 * (size_t)q.d);
     q.off_partials = q.axis == DION2_AXIS_COLS ? take(4 * (size_t)q.rowblocks * (size_t)mats[i].cols) : 0;
     q.off_sel = take(4 * (size_t)q.k);
-    q.off_sumsq = take(4 * (size_t)q.ga * q.gb);
+    q.off_sumsq = take(4 * (size_t)q.n_sumsq);
   }
   off = align_up(off, 4096);
   P.off_ns_begin = off;
@@ -280,6 +295,9 @@ int build_device_plan(Plan& P, const dion2_matrix* mats, const dion2_config* c, 
   std::vector<int32_t> rowmats, colmats;
   std::vector<int64_t> rowprefix, colprefix;
   std::vector<int32_t> gprefix(n);
+  std::vector<int32_t> fl_mats[2], fl_gp[2], fl_sp[2];
+  P.fl_gunits[0] = P.fl_gunits[1] = P.fl_sunits[0] = P.fl_sunits[1] = 0;
+  P.fl_maxk = 0;
   int64_t rows_acc = 0, ctiles_acc = 0;
   int gt_acc = 0;
   for (int i = 0; i < n; ++i) {
@@ -309,8 +327,21 @@ int build_device_plan(Plan& P, const dion2_matrix* mats, const dion2_config* c, 
     d.sa_pad = q.sa_pad;
     d.sb_pad = q.sb_pad;
     d.rowblocks = q.rowblocks;
+    d.path = q.path;
+    d.n_sumsq = q.n_sumsq;
     gprefix[i] = gt_acc;
     gt_acc += q.ga * q.gb;
+    if (q.path > 0) {
+      const int l = q.path - 1;
+      const int gu = l == 0 ? q.p_pad : q.q_pad / 32;
+      const int su = l == 0 ? q.k : q.q_pad / 32;
+      fl_mats[l].push_back(i);
+      fl_gp[l].push_back(P.fl_gunits[l]);
+      fl_sp[l].push_back(P.fl_sunits[l]);
+      P.fl_gunits[l] += gu;
+      P.fl_sunits[l] += su;
+      if (l == 1) P.fl_maxk = std::max(P.fl_maxk, q.k);
+    }
     if (q.axis == DION2_AXIS_ROWS) {
       rowmats.push_back(i);
       rowprefix.push_back(rows_acc);
@@ -326,6 +357,14 @@ int build_device_plan(Plan& P, const dion2_matrix* mats, const dion2_config* c, 
   P.n_row_mats = (int)rowmats.size();
   P.n_col_mats = (int)colmats.size();
   P.total_gather_tiles = gt_acc;
+  for (int l = 0; l < 2; ++l) {
+    P.fl_n[l] = (int)fl_mats[l].size();
+    if (P.fl_n[l]) {
+      memcpy(H(P.off_fl_mats[l]), fl_mats[l].data(), 4 * fl_mats[l].size());
+      memcpy(H(P.off_fl_gprefix[l]), fl_gp[l].data(), 4 * fl_gp[l].size());
+      memcpy(H(P.off_fl_sprefix[l]), fl_sp[l].data(), 4 * fl_sp[l].size());
+    }
+  }
   if (!rowmats.empty()) {
     memcpy(H(P.off_rowmats), rowmats.data(), 4 * rowmats.size());
     memcpy(H(P.off_rowprefix), rowprefix.data(), 8 * rowprefix.size());
@@ -362,9 +401,12 @@ int build_device_plan(Plan& P, const dion2_matrix* mats, const dion2_config* c, 
           NsParams& np = L.tc.p;
           np.ngroups = (int)std::min<size_t>(kMaxGroups, gl.size() - s0);
           np.ns_scale_all = scale_all;
+          // gram: A = s^2 X X^T; poly: C = a I + b A + c A A^T (consistent bf16 A);
+          // apply: X' = s C X (the linear term a X is folded into C: no epilogue read)
+          np.diag = 0.f;
           if (ph == PH_GRAM) { np.cacc = 1.f; np.cC = 0.f; np.scale_sel = t == 0 ? 2 : 0; np.b_kmajor = 1; }
-          if (ph == PH_POLY) { np.cacc = cc; np.cC = b; np.scale_sel = 0; np.b_kmajor = 1; }
-          if (ph == PH_APPLY) { np.cacc = 1.f; np.cC = a; np.scale_sel = t == 0 ? 1 : 0; np.b_kmajor = 0; }
+          if (ph == PH_POLY) { np.cacc = cc; np.cC = b; np.diag = a; np.scale_sel = 0; np.b_kmajor = 1; }
+          if (ph == PH_APPLY) { np.cacc = 1.f; np.cC = 0.f; np.scale_sel = t == 0 ? 1 : 0; np.b_kmajor = 0; }
           int tiles = 0;
           for (int j = 0; j < np.ngroups; ++j) {
             const Group& g = P.groups[gl[s0 + j]];
@@ -402,7 +444,7 @@ int build_device_plan(Plan& P, const dion2_matrix* mats, const dion2_config* c, 
               G.a = Bm; G.a_mstride = as; G.lda = g.p_pad;
               G.b = Xc; G.b_mstride = xs; G.ldb = g.q_pad;
               G.out = Xn; G.out_mstride = xs; G.out_ld = g.q_pad;
-              G.cin = Xc; G.cin_mstride = xs; G.cin_ld = g.q_pad;
+              G.cin = nullptr; G.cin_mstride = 0; G.cin_ld = 0;
               if (P.bf16_ns) {
                 if (!make_map(&L.tc.mapA[j], Bm, g.p_pad, g.p_pad, g.count, 64, 128)) return DION2_ECUDA;
                 // MN-major B operand: box = 64 columns of X (N) x 64 rows of X (K)
@@ -437,6 +479,7 @@ void ensure_device_attrs() {
   cudaGetDevice(&dev);
   cudaDeviceGetAttribute(&g_sm_count, cudaDevAttrMultiProcessorCount, dev);
   ns_tc_set_attrs();
+  launch_fast_paths_attrs();
   cudaFuncSetAttribute(k_topk_select, cudaFuncAttributeMaxDynamicSharedMemorySize, 4 * DION2_MAX_SELECT_DIM);
   cudaFuncSetAttribute(k_full_decay, cudaFuncAttributeMaxDynamicSharedMemorySize, DION2_MAX_SELECT_DIM);
   g_attr_done = true;
@@ -539,12 +582,28 @@ int run_step(Plan& P, const dion2_matrix* mats, const dion2_config* c, void* ws,
   L.end();
   // K3 gather + decay (Alg. 1 l.4-5)
   {
-    L.begin(PH_GATHER);
-    int blocks = std::min(P.total_gather_tiles, sms * 8);
     const int decay = 1;
-    launch_gather_decay(P.bf16_ns, blocks, s, dmats, (const int32_t*)tab(P, P.off_gprefix), n, P.total_gather_tiles,
-                        bad, decay, c->mu);
-    L.end();
+    if (P.total_gather_tiles > 0) {
+      L.begin(PH_GATHER);
+      int blocks = std::min(P.total_gather_tiles, sms * 8);
+      launch_gather_decay(P.bf16_ns, blocks, s, dmats, (const int32_t*)tab(P, P.off_gprefix), n,
+                          P.total_gather_tiles, bad, decay, c->mu);
+      L.end();
+    }
+    if (P.fl_n[0]) {
+      L.begin(PH_GATHER);
+      const int blocks = (int)std::min<int64_t>(ceil_div(P.fl_gunits[0], 8), (int64_t)sms * 8);
+      launch_gather_rows(blocks, s, dmats, (const int32_t*)tab(P, P.off_fl_mats[0]),
+                         (const int32_t*)tab(P, P.off_fl_gprefix[0]), P.fl_n[0], P.fl_gunits[0], bad, c->mu);
+      L.end();
+    }
+    if (P.fl_n[1]) {
+      L.begin(PH_GATHER);
+      const int blocks = std::min(P.fl_gunits[1], sms * 4);
+      launch_gather_cols_t(blocks, P.fl_maxk, s, dmats, (const int32_t*)tab(P, P.off_fl_mats[1]),
+                           (const int32_t*)tab(P, P.off_fl_gprefix[1]), P.fl_n[1], P.fl_gunits[1], bad, c->mu);
+      L.end();
+    }
     L.begin(PH_NORM);
     k_norm_finalize<<<(unsigned)ceil_div(n, 8), 256, 0, s>>>(dmats, n, c->ns_eps);
     L.end();
@@ -565,11 +624,27 @@ int run_step(Plan& P, const dion2_matrix* mats, const dion2_config* c, void* ws,
   }
   // K7 scatter (Alg. 1 l.6)
   {
-    L.begin(PH_SCATTER);
-    int blocks = std::min(P.total_gather_tiles, sms * 8);
-    launch_scatter_update(P.bf16_ns, blocks, s, dmats, (const int32_t*)tab(P, P.off_gprefix), n, P.total_gather_tiles,
-                          bad, c->lr);
-    L.end();
+    if (P.total_gather_tiles > 0) {
+      L.begin(PH_SCATTER);
+      int blocks = std::min(P.total_gather_tiles, sms * 8);
+      launch_scatter_update(P.bf16_ns, blocks, s, dmats, (const int32_t*)tab(P, P.off_gprefix), n,
+                            P.total_gather_tiles, bad, c->lr);
+      L.end();
+    }
+    if (P.fl_n[0]) {
+      L.begin(PH_SCATTER);
+      const int blocks = (int)std::min<int64_t>(ceil_div(P.fl_sunits[0], 8), (int64_t)sms * 8);
+      launch_scatter_rows(blocks, s, dmats, (const int32_t*)tab(P, P.off_fl_mats[0]),
+                          (const int32_t*)tab(P, P.off_fl_sprefix[0]), P.fl_n[0], P.fl_sunits[0], bad, c->lr);
+      L.end();
+    }
+    if (P.fl_n[1]) {
+      L.begin(PH_SCATTER);
+      const int blocks = std::min(P.fl_sunits[1], sms * 4);
+      launch_scatter_cols_t(blocks, P.fl_maxk, s, dmats, (const int32_t*)tab(P, P.off_fl_mats[1]),
+                            (const int32_t*)tab(P, P.off_fl_sprefix[1]), P.fl_n[1], P.fl_sunits[1], bad, c->lr);
+      L.end();
+    }
   }
   if (c->decay_mode == 1) {
     L.begin(PH_FULLDECAY);

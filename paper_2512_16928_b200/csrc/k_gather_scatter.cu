@@ -134,7 +134,7 @@ __global__ void k_norm_finalize(const MatDesc* __restrict__ mats, int n_mats, fl
   const int mi = blockIdx.x * (blockDim.x >> 5) + (threadIdx.x >> 5);
   if (mi >= n_mats) return;
   const MatDesc& md = mats[mi];
-  const int nt = md.gather_tiles_a * md.gather_tiles_b;
+  const int nt = md.n_sumsq;
   float s = 0.f;
   for (int i = lane; i < nt; i += 32) s += md.sumsq_partials[i];
   s = warp_sum(s);

@@ -1,0 +1,428 @@
+// Streaming fast paths of K3 (gather + selective decay + sum of squares) and
+// K7 (sparse update) for the two orientations auto mode produces:
+//
+//  rows mode, X = S = M[K, :] (k <= n)       one warp per X row, float4 streams
+//  cols mode, X = S^T, S = M[:, K] (k <= m)  one CTA per 32-row slab of M; every
+//      row is streamed whole (coalesced float4) and the selected columns are
+//      picked with a shared-memory bitmask: at alpha = 0.25 a 32-byte sector
+//      holds a selected column with probability 1 - 0.75^8 = 0.90, so reading
+//      whole rows costs no more DRAM traffic than per-element gathers and
+//      keeps every access coalesced (SURVEY finding 8).
+//
+// Semantics are those of k_gather_decay / k_scatter_update (Alg. 1 l.4-6,
+// PAPER.md P:186-189): X = wide(M[K]) pre-decay, M[K] <- mu M[K], per-unit
+// sum of squares for ||X||_F, W[K] <- W[K] - lr*sqrt(m/n)*O; unselected
+// entries are never written (a float4 containing no selected column is not
+// stored; a float4 containing one is stored with its other lanes unchanged
+// bit for bit).  Padding of X (rows >= k, columns >= the other dim) is
+// rewritten with zeros every step.
+#include "kernels.cuh"
+
+namespace dion2 {
+
+__device__ __forceinline__ int find_unit(const int32_t* __restrict__ prefix, int n, int t) {
+  int lo = 0, hi = n - 1;
+  while (lo < hi) {
+    int mid = (lo + hi + 1) >> 1;
+    if (prefix[mid] <= t) lo = mid; else hi = mid - 1;
+  }
+  return lo;
+}
+
+__device__ __forceinline__ uint2 pack4_bf16(float a, float b, float c, float d) {
+  __nv_bfloat162 lo = __floats2bfloat162_rn(a, b), hi = __floats2bfloat162_rn(c, d);
+  uint2 u;
+  u.x = *reinterpret_cast<uint32_t*>(&lo);
+  u.y = *reinterpret_cast<uint32_t*>(&hi);
+  return u;
+}
+
+// ------------------------------------------------------------------ rows mode
+// unit = one X row r in [0, p_pad) of one matrix
+__global__ void __launch_bounds__(256) k_gather_rows(const MatDesc* __restrict__ mats,
+                                                     const int32_t* __restrict__ list_mats,
+                                                     const int32_t* __restrict__ list_prefix, int n_list,
+                                                     int total_units, const int32_t* __restrict__ bad, float mu) {
+  const int lane = threadIdx.x & 31;
+  const int warp = blockIdx.x * (blockDim.x >> 5) + (threadIdx.x >> 5);
+  const int nwarps = gridDim.x * (blockDim.x >> 5);
+  for (int u = warp; u < total_units; u += nwarps) {
+    const int li = find_unit(list_prefix, n_list, u);
+    const int mi = list_mats[li];
+    const MatDesc& md = mats[mi];
+    const int r = u - list_prefix[li];
+    __nv_bfloat16* xrow = reinterpret_cast<__nv_bfloat16*>(md.X0) + (int64_t)r * md.q_pad;
+    float ss = 0.f;
+    if (r < md.k) {
+      float* mrow = md.M + (int64_t)md.sel[r] * md.ld;
+      const float f = bad[mi] ? 1.f : mu;
+      const int n = (int)md.cols;
+      if (md.vec4) {
+        const int n4 = n >> 2;
+        float4* m4 = reinterpret_cast<float4*>(mrow);
+        uint2* x4 = reinterpret_cast<uint2*>(xrow);
+        int j = lane;
+        for (; j + 96 < n4; j += 128) {
+          float4 v[4];
+#pragma unroll
+          for (int q = 0; q < 4; ++q) v[q] = m4[j + 32 * q];
+#pragma unroll
+          for (int q = 0; q < 4; ++q) {
+            ss += v[q].x * v[q].x + v[q].y * v[q].y + v[q].z * v[q].z + v[q].w * v[q].w;
+            x4[j + 32 * q] = pack4_bf16(v[q].x, v[q].y, v[q].z, v[q].w);
+            m4[j + 32 * q] = make_float4(f * v[q].x, f * v[q].y, f * v[q].z, f * v[q].w);
+          }
+        }
+        for (; j < n4; j += 32) {
+          float4 v = m4[j];
+          ss += v.x * v.x + v.y * v.y + v.z * v.z + v.w * v.w;
+          x4[j] = pack4_bf16(v.x, v.y, v.z, v.w);
+          m4[j] = make_float4(f * v.x, f * v.y, f * v.z, f * v.w);
+        }
+        for (int c = 4 * n4 + lane; c < n; c += 32) {
+          float v = mrow[c];
+          ss += v * v;
+          xrow[c] = __float2bfloat16_rn(v);
+          mrow[c] = f * v;
+        }
+      } else {
+        for (int c = lane; c < n; c += 32) {
+          float v = mrow[c];
+          ss += v * v;
+          xrow[c] = __float2bfloat16_rn(v);
+          mrow[c] = f * v;
+        }
+      }
+      for (int c = n + lane; c < md.q_pad; c += 32) xrow[c] = __float2bfloat16_rn(0.f);
+    } else {
+      uint4* x16 = reinterpret_cast<uint4*>(xrow);  // q_pad % 256 == 0: whole 16-B chunks
+      for (int c = lane; c < md.q_pad / 8; c += 32) x16[c] = make_uint4(0, 0, 0, 0);
+    }
+    ss = warp_sum(ss);
+    if (lane == 0) md.sumsq_partials[r] = ss;
+  }
+}
+
+// unit = one selected row r in [0, k)
+__global__ void __launch_bounds__(256) k_scatter_rows(const MatDesc* __restrict__ mats,
+                                                      const int32_t* __restrict__ list_mats,
+                                                      const int32_t* __restrict__ list_prefix, int n_list,
+                                                      int total_units, const int32_t* __restrict__ bad, float lr) {
+  const int lane = threadIdx.x & 31;
+  const int warp = blockIdx.x * (blockDim.x >> 5) + (threadIdx.x >> 5);
+  const int nwarps = gridDim.x * (blockDim.x >> 5);
+  for (int u = warp; u < total_units; u += nwarps) {
+    const int li = find_unit(list_prefix, n_list, u);
+    const int mi = list_mats[li];
+    const MatDesc& md = mats[mi];
+    if (bad[mi]) continue;
+    const int r = u - list_prefix[li];
+    const __nv_bfloat16* xrow =
+        reinterpret_cast<const __nv_bfloat16*>(md.final_in_x1 ? md.X1 : md.X0) + (int64_t)r * md.q_pad;
+    float* wrow = md.W + (int64_t)md.sel[r] * md.ld;
+    float* orow = md.O_out ? md.O_out + (int64_t)r * md.cols : nullptr;
+    const float sc = lr * md.update_scale;
+    const int n = (int)md.cols;
+    if (md.vec4) {
+      const int n4 = n >> 2;
+      float4* w4 = reinterpret_cast<float4*>(wrow);
+      const uint2* x4 = reinterpret_cast<const uint2*>(xrow);
+      int j = lane;
+      for (; j + 96 < n4; j += 128) {
+        float4 w[4];
+        uint2 o[4];
+#pragma unroll
+        for (int q = 0; q < 4; ++q) {
+          w[q] = w4[j + 32 * q];
+          o[q] = x4[j + 32 * q];
+        }
+#pragma unroll
+        for (int q = 0; q < 4; ++q) {
+          const __nv_bfloat162 lo = *reinterpret_cast<const __nv_bfloat162*>(&o[q].x);
+          const __nv_bfloat162 hi = *reinterpret_cast<const __nv_bfloat162*>(&o[q].y);
+          const float o0 = __low2float(lo), o1 = __high2float(lo), o2 = __low2float(hi), o3 = __high2float(hi);
+          w[q].x -= sc * o0; w[q].y -= sc * o1; w[q].z -= sc * o2; w[q].w -= sc * o3;
+          w4[j + 32 * q] = w[q];
+          if (orow) {
+            const int c = 4 * (j + 32 * q);
+            orow[c] = o0; orow[c + 1] = o1; orow[c + 2] = o2; orow[c + 3] = o3;
+          }
+        }
+      }
+      for (; j < n4; j += 32) {
+        float4 w = w4[j];
+        const uint2 o = x4[j];
+        const __nv_bfloat162 lo = *reinterpret_cast<const __nv_bfloat162*>(&o.x);
+        const __nv_bfloat162 hi = *reinterpret_cast<const __nv_bfloat162*>(&o.y);
+        const float o0 = __low2float(lo), o1 = __high2float(lo), o2 = __low2float(hi), o3 = __high2float(hi);
+        w.x -= sc * o0; w.y -= sc * o1; w.z -= sc * o2; w.w -= sc * o3;
+        w4[j] = w;
+        if (orow) {
+          orow[4 * j] = o0; orow[4 * j + 1] = o1; orow[4 * j + 2] = o2; orow[4 * j + 3] = o3;
+        }
+      }
+      for (int c = 4 * n4 + lane; c < n; c += 32) {
+        const float o = __bfloat162float(xrow[c]);
+        wrow[c] -= sc * o;
+        if (orow) orow[c] = o;
+      }
+    } else {
+      for (int c = lane; c < n; c += 32) {
+        const float o = __bfloat162float(xrow[c]);
+        wrow[c] -= sc * o;
+        if (orow) orow[c] = o;
+      }
+    }
+  }
+}
+
+// ------------------------------------------------------------------ cols mode, X = S^T
+// unit = one 32-row slab of X's column range [0, q_pad) (i.e. rows i0..i0+31 of M)
+constexpr int kSlab = 32;
+
+struct ColMask {
+  uint32_t* mask;  // [n/32 + 1]
+  int32_t* rank;   // [n/32 + 1] exclusive popcount prefix
+};
+
+__device__ __forceinline__ void build_mask(const MatDesc& md, uint32_t* mask, int32_t* rank) {
+  const int nw = (int)((md.cols + 31) >> 5);
+  for (int w = threadIdx.x; w < nw; w += blockDim.x) mask[w] = 0u;
+  __syncthreads();
+  for (int r = threadIdx.x; r < md.k; r += blockDim.x) {
+    const int c = md.sel[r];
+    atomicOr(&mask[c >> 5], 1u << (c & 31));
+  }
+  __syncthreads();
+  if (threadIdx.x < 32) {
+    int carry = 0;
+    for (int w0 = 0; w0 < nw; w0 += 32) {
+      const int w = w0 + threadIdx.x;
+      const int pc = w < nw ? __popc(mask[w]) : 0;
+      int x = pc;
+#pragma unroll
+      for (int o = 1; o < 32; o <<= 1) {
+        const int y = __shfl_up_sync(0xffffffffu, x, o);
+        if ((int)threadIdx.x >= o) x += y;
+      }
+      if (w < nw) rank[w] = carry + x - pc;
+      carry += __shfl_sync(0xffffffffu, x, 31);
+    }
+  }
+  __syncthreads();
+}
+
+__device__ __forceinline__ int col_rank(const uint32_t* mask, const int32_t* rank, int c) {
+  return rank[c >> 5] + __popc(mask[c >> 5] & ((1u << (c & 31)) - 1u));
+}
+
+// smem: mask [1536] u32, rank [1536] i32, tile [kSlab][kMaxColK + 8] bf16
+constexpr int kMaxColK = kMaxColKFast;
+constexpr int kMaskWords = DION2_MAX_SELECT_DIM_WORDS;
+
+__global__ void __launch_bounds__(256) k_gather_cols_t(const MatDesc* __restrict__ mats,
+                                                       const int32_t* __restrict__ list_mats,
+                                                       const int32_t* __restrict__ list_prefix, int n_list,
+                                                       int total_units, const int32_t* __restrict__ bad, float mu) {
+  extern __shared__ __align__(16) uint8_t sm[];
+  uint32_t* mask = reinterpret_cast<uint32_t*>(sm);
+  int32_t* rank = reinterpret_cast<int32_t*>(sm + 4 * kMaskWords);
+  __nv_bfloat16* tile = reinterpret_cast<__nv_bfloat16*>(sm + 8 * kMaskWords);  // [kSlab][ldt]
+  __shared__ float wsum[8];
+  int cur_mat = -1;
+  const int lane = threadIdx.x & 31, wid = threadIdx.x >> 5;
+  for (int u = blockIdx.x; u < total_units; u += gridDim.x) {
+    const int li = find_unit(list_prefix, n_list, u);
+    const int mi = list_mats[li];
+    const MatDesc& md = mats[mi];
+    if (mi != cur_mat) {
+      build_mask(md, mask, rank);
+      cur_mat = mi;
+    }
+    const int slab = u - list_prefix[li];
+    const int i0 = slab * kSlab;
+    const int k = md.k;
+    const int ldt = k + 8;  // bf16 elements per tile row (padding breaks bank conflicts)
+    const float f = bad[mi] ? 1.f : mu;
+    const int n = (int)md.cols;
+    float ss = 0.f;
+    // each warp streams rows i0 + wid + 8*j (4 rows per warp)
+    for (int il = wid; il < kSlab; il += 8) {
+      const int64_t i = (int64_t)i0 + il;
+      __nv_bfloat16* trow = tile + il * ldt;
+      if (i >= md.rows) {
+        for (int r = lane; r < k; r += 32) trow[r] = __float2bfloat16_rn(0.f);
+        continue;
+      }
+      float* mrow = md.M + i * md.ld;
+      if (md.vec4) {
+        float4* m4 = reinterpret_cast<float4*>(mrow);
+        const int n4 = n >> 2;
+        for (int j = lane; j < n4; j += 32) {
+          const int c = 4 * j;
+          const uint32_t bits = (mask[c >> 5] >> (c & 31)) & 0xFu;
+          if (bits == 0u) continue;
+          float4 v = m4[j];
+          int rk = col_rank(mask, rank, c);
+          float e[4] = {v.x, v.y, v.z, v.w};
+#pragma unroll
+          for (int q = 0; q < 4; ++q) {
+            if (bits & (1u << q)) {
+              trow[rk++] = __float2bfloat16_rn(e[q]);
+              ss += e[q] * e[q];
+              e[q] *= f;
+            }
+          }
+          m4[j] = make_float4(e[0], e[1], e[2], e[3]);
+        }
+        for (int c = 4 * n4 + lane; c < n; c += 32) {
+          if (!((mask[c >> 5] >> (c & 31)) & 1u)) continue;
+          const float v = mrow[c];
+          trow[col_rank(mask, rank, c)] = __float2bfloat16_rn(v);
+          ss += v * v;
+          mrow[c] = f * v;
+        }
+      } else {
+        for (int c = lane; c < n; c += 32) {
+          if (!((mask[c >> 5] >> (c & 31)) & 1u)) continue;
+          const float v = mrow[c];
+          trow[col_rank(mask, rank, c)] = __float2bfloat16_rn(v);
+          ss += v * v;
+          mrow[c] = f * v;
+        }
+      }
+    }
+    ss = warp_sum(ss);
+    if (lane == 0) wsum[wid] = ss;
+    __syncthreads();
+    if (threadIdx.x == 0) {
+      float s = 0.f;
+      for (int w = 0; w < 8; ++w) s += wsum[w];
+      md.sumsq_partials[slab] = s;
+    }
+    // X[r][i0 .. i0+31] = tile[0..31][r]  (64 contiguous bytes per X row), rows r >= k are zero
+    __nv_bfloat16* X = reinterpret_cast<__nv_bfloat16*>(md.X0);
+    for (int t = threadIdx.x; t < md.p_pad * 4; t += blockDim.x) {
+      const int r = t >> 2, part = (t & 3) * 8;
+      uint4 out = make_uint4(0, 0, 0, 0);
+      if (r < k) {
+        __nv_bfloat16 h[8];
+#pragma unroll
+        for (int e = 0; e < 8; ++e) h[e] = tile[(part + e) * ldt + r];
+        out = *reinterpret_cast<uint4*>(h);
+      }
+      *reinterpret_cast<uint4*>(X + (int64_t)r * md.q_pad + i0 + part) = out;
+    }
+    __syncthreads();
+  }
+}
+
+__global__ void __launch_bounds__(256) k_scatter_cols_t(const MatDesc* __restrict__ mats,
+                                                        const int32_t* __restrict__ list_mats,
+                                                        const int32_t* __restrict__ list_prefix, int n_list,
+                                                        int total_units, const int32_t* __restrict__ bad, float lr) {
+  extern __shared__ __align__(16) uint8_t sm[];
+  uint32_t* mask = reinterpret_cast<uint32_t*>(sm);
+  int32_t* rank = reinterpret_cast<int32_t*>(sm + 4 * kMaskWords);
+  __nv_bfloat16* tile = reinterpret_cast<__nv_bfloat16*>(sm + 8 * kMaskWords);  // [kSlab][ldt]
+  int cur_mat = -1;
+  const int lane = threadIdx.x & 31, wid = threadIdx.x >> 5;
+  for (int u = blockIdx.x; u < total_units; u += gridDim.x) {
+    const int li = find_unit(list_prefix, n_list, u);
+    const int mi = list_mats[li];
+    const MatDesc& md = mats[mi];
+    const int slab = u - list_prefix[li];
+    const int i0 = slab * kSlab;
+    if (bad[mi] || i0 >= md.rows) continue;  // block-uniform
+    if (mi != cur_mat) {
+      build_mask(md, mask, rank);
+      cur_mat = mi;
+    }
+    const int k = md.k;
+    const int ldt = k + 8;
+    // O tile: tile[il][r] = X_T[r][i0 + il]
+    const __nv_bfloat16* X = reinterpret_cast<const __nv_bfloat16*>(md.final_in_x1 ? md.X1 : md.X0);
+    for (int t = threadIdx.x; t < k * 4; t += blockDim.x) {
+      const int r = t >> 2, part = (t & 3) * 8;
+      const uint4 in = *reinterpret_cast<const uint4*>(X + (int64_t)r * md.q_pad + i0 + part);
+      const __nv_bfloat16* h = reinterpret_cast<const __nv_bfloat16*>(&in);
+#pragma unroll
+      for (int e = 0; e < 8; ++e) tile[(part + e) * ldt + r] = h[e];
+    }
+    __syncthreads();
+    const float sc = lr * md.update_scale;
+    const int n = (int)md.cols;
+    for (int il = wid; il < kSlab; il += 8) {
+      const int64_t i = (int64_t)i0 + il;
+      if (i >= md.rows) break;
+      const __nv_bfloat16* trow = tile + il * ldt;
+      float* wrow = md.W + i * md.ld;
+      float* orow = md.O_out ? md.O_out + i * k : nullptr;
+      if (md.vec4) {
+        float4* w4 = reinterpret_cast<float4*>(wrow);
+        const int n4 = n >> 2;
+        for (int j = lane; j < n4; j += 32) {
+          const int c = 4 * j;
+          const uint32_t bits = (mask[c >> 5] >> (c & 31)) & 0xFu;
+          if (bits == 0u) continue;
+          float4 w = w4[j];
+          int rk = col_rank(mask, rank, c);
+          float e[4] = {w.x, w.y, w.z, w.w};
+#pragma unroll
+          for (int q = 0; q < 4; ++q) {
+            if (bits & (1u << q)) {
+              const float o = __bfloat162float(trow[rk]);
+              e[q] -= sc * o;
+              if (orow) orow[rk] = o;
+              ++rk;
+            }
+          }
+          w4[j] = make_float4(e[0], e[1], e[2], e[3]);
+        }
+        for (int c = 4 * n4 + lane; c < n; c += 32) {
+          if (!((mask[c >> 5] >> (c & 31)) & 1u)) continue;
+          const int rk = col_rank(mask, rank, c);
+          const float o = __bfloat162float(trow[rk]);
+          wrow[c] -= sc * o;
+          if (orow) orow[rk] = o;
+        }
+      } else {
+        for (int c = lane; c < n; c += 32) {
+          if (!((mask[c >> 5] >> (c & 31)) & 1u)) continue;
+          const int rk = col_rank(mask, rank, c);
+          const float o = __bfloat162float(trow[rk]);
+          wrow[c] -= sc * o;
+          if (orow) orow[rk] = o;
+        }
+      }
+    }
+    __syncthreads();
+  }
+}
+
+size_t cols_t_smem_bytes(int k) { return 8 * (size_t)kMaskWords + (size_t)kSlab * (k + 8) * 2; }
+
+void launch_fast_paths_attrs() {
+  const int mx = (int)cols_t_smem_bytes(kMaxColK);
+  cudaFuncSetAttribute(k_gather_cols_t, cudaFuncAttributeMaxDynamicSharedMemorySize, mx);
+  cudaFuncSetAttribute(k_scatter_cols_t, cudaFuncAttributeMaxDynamicSharedMemorySize, mx);
+}
+
+void launch_gather_rows(int blocks, cudaStream_t s, const MatDesc* mats, const int32_t* lm, const int32_t* lp, int nl,
+                        int units, const int32_t* bad, float mu) {
+  k_gather_rows<<<blocks, 256, 0, s>>>(mats, lm, lp, nl, units, bad, mu);
+}
+void launch_scatter_rows(int blocks, cudaStream_t s, const MatDesc* mats, const int32_t* lm, const int32_t* lp, int nl,
+                         int units, const int32_t* bad, float lr) {
+  k_scatter_rows<<<blocks, 256, 0, s>>>(mats, lm, lp, nl, units, bad, lr);
+}
+void launch_gather_cols_t(int blocks, int max_k, cudaStream_t s, const MatDesc* mats, const int32_t* lm,
+                          const int32_t* lp, int nl, int units, const int32_t* bad, float mu) {
+  k_gather_cols_t<<<blocks, 256, cols_t_smem_bytes(max_k), s>>>(mats, lm, lp, nl, units, bad, mu);
+}
+void launch_scatter_cols_t(int blocks, int max_k, cudaStream_t s, const MatDesc* mats, const int32_t* lm,
+                           const int32_t* lp, int nl, int units, const int32_t* bad, float lr) {
+  k_scatter_cols_t<<<blocks, 256, cols_t_smem_bytes(max_k), s>>>(mats, lm, lp, nl, units, bad, lr);
+}
+
+}  // namespace dion2

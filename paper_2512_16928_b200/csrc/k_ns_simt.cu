@@ -62,6 +62,7 @@ __global__ void __launch_bounds__(256) k_ns_gemm_simt_f32(const NsParams P, int 
       const int c = n0 + tx * 4 + j;
       float v = P.cacc * acc[i][j];
       if (C) v += P.cC * C[(int64_t)r * g.cin_ld + c];
+      if (r == c) v += P.diag;
       D[(int64_t)r * g.out_ld + c] = osc * v;
     }
   }

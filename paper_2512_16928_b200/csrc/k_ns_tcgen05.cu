@@ -162,7 +162,7 @@ __global__ void __launch_bounds__(192, 1) k_ns_gemm_tc(const __grid_constant__ N
       const uint32_t acc_phase = (it >> 1) & 1;
       float osc = 1.f;
       if (p.scale_sel) osc = p.ns_scale_all[2 * G.gmats[c.z] + (p.scale_sel - 1)];
-      const float ca = p.cacc * osc, cc = p.cC * osc;
+      const float ca = p.cacc * osc, cc = p.cC * osc, dterm = p.diag * osc;
       const int64_t row = (int64_t)c.tm * kBM + row_in_tile;
       __nv_bfloat16* out = reinterpret_cast<__nv_bfloat16*>(G.out) + (int64_t)c.z * G.out_mstride + row * G.out_ld +
                            (int64_t)c.tn * BN;
@@ -193,14 +193,20 @@ __global__ void __launch_bounds__(192, 1) k_ns_gemm_tc(const __grid_constant__ N
 #pragma unroll
           for (int e = 0; e < 32; ++e) cv[e] = 0.f;
         }
+        // diagonal term (poly phase: C = a*I + b*A + c*A*A): element e sits on the
+        // global diagonal iff row == col0 + e
+        const int dcol = (int)(row - ((int64_t)c.tn * BN + cc32 * 32));
+        float o[32];
+#pragma unroll
+        for (int e = 0; e < 32; ++e) o[e] = ca * v[e] + cc * cv[e] + (e == dcol ? dterm : 0.f);
         uint4* dst = reinterpret_cast<uint4*>(out + cc32 * 32);
 #pragma unroll
         for (int q = 0; q < 4; ++q) {
           uint4 u;
-          u.x = pack_bf16x2(ca * v[q * 8 + 0] + cc * cv[q * 8 + 0], ca * v[q * 8 + 1] + cc * cv[q * 8 + 1]);
-          u.y = pack_bf16x2(ca * v[q * 8 + 2] + cc * cv[q * 8 + 2], ca * v[q * 8 + 3] + cc * cv[q * 8 + 3]);
-          u.z = pack_bf16x2(ca * v[q * 8 + 4] + cc * cv[q * 8 + 4], ca * v[q * 8 + 5] + cc * cv[q * 8 + 5]);
-          u.w = pack_bf16x2(ca * v[q * 8 + 6] + cc * cv[q * 8 + 6], ca * v[q * 8 + 7] + cc * cv[q * 8 + 7]);
+          u.x = pack_bf16x2(o[q * 8 + 0], o[q * 8 + 1]);
+          u.y = pack_bf16x2(o[q * 8 + 2], o[q * 8 + 3]);
+          u.z = pack_bf16x2(o[q * 8 + 4], o[q * 8 + 5]);
+          u.w = pack_bf16x2(o[q * 8 + 6], o[q * 8 + 7]);
           dst[q] = u;
         }
       }

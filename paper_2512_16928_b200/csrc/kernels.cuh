@@ -23,6 +23,20 @@ void launch_gather_decay(bool bf16, int blocks, cudaStream_t s, const MatDesc* m
 void launch_scatter_update(bool bf16, int blocks, cudaStream_t s, const MatDesc* mats, const int32_t* tile_prefix_mats,
                            int n_mats, int total_tiles, const int32_t* bad, float lr);
 __global__ void k_norm_finalize(const MatDesc* __restrict__ mats, int n_mats, float eps);
+
+// streaming fast paths (k_gather_scatter_fast.cu): rows mode X = S, cols mode X = S^T
+#define DION2_MAX_SELECT_DIM_WORDS 1536  // DION2_MAX_SELECT_DIM / 32
+constexpr int kMaxColKFast = 1024;          // largest k of the cols streaming path (smem tile)
+size_t cols_t_smem_bytes(int k);
+void launch_fast_paths_attrs();
+void launch_gather_rows(int blocks, cudaStream_t s, const MatDesc* mats, const int32_t* lm, const int32_t* lp, int nl,
+                        int units, const int32_t* bad, float mu);
+void launch_scatter_rows(int blocks, cudaStream_t s, const MatDesc* mats, const int32_t* lm, const int32_t* lp, int nl,
+                         int units, const int32_t* bad, float lr);
+void launch_gather_cols_t(int blocks, int max_k, cudaStream_t s, const MatDesc* mats, const int32_t* lm,
+                          const int32_t* lp, int nl, int units, const int32_t* bad, float mu);
+void launch_scatter_cols_t(int blocks, int max_k, cudaStream_t s, const MatDesc* mats, const int32_t* lm,
+                           const int32_t* lp, int nl, int units, const int32_t* bad, float lr);
 __global__ void k_full_decay(const MatDesc* __restrict__ mats, int n_mats, const int32_t* __restrict__ bad, float mu);
 
 // ---------------- K4-K6 Newton-Schulz GEMMs
@@ -45,6 +59,7 @@ struct NsParams {
   NsGroup g[kMaxGroups];
   int ngroups, total_tiles;
   float cacc, cC;
+  float diag;                // added on the global diagonal (poly: C = a*I + b*A + c*A^2)
   int scale_sel;             // 0: oscale = 1; 1: s; 2: s^2
   const float* ns_scale_all; // [n_mats][2]
   int b_kmajor;
