@@ -58,7 +58,9 @@ def work_model(shapes, alpha, steps=5):
     """Algorithmic work per Dion2 step: NS FLOPs T(4p^2 q + 2p^3) and
     per-phase algorithmic HBM bytes."""
     ns_flops = {"ns_gram": 0.0, "ns_poly": 0.0, "ns_apply": 0.0}
-    byts = {"momentum_score": 0.0, "gather": 0.0, "scatter": 0.0}
+    byts = {"momentum_score": 0.0}
+    for ph in ("gather", "gather_rows", "gather_cols", "scatter", "scatter_rows", "scatter_cols"):
+        byts[ph] = 0.0
     for (m, n) in shapes:
         rows = m <= n
         d, o = (m, n) if rows else (n, m)
@@ -68,8 +70,15 @@ def work_model(shapes, alpha, steps=5):
         ns_flops["ns_poly"] += steps * 2.0 * p ** 3
         ns_flops["ns_apply"] += steps * 2.0 * p * p * q
         byts["momentum_score"] += m * n * 12.0 + d * 4.0       # read G, read M, write M, write scores
-        byts["gather"] += k * o * (4.0 + 4.0 + 2.0)           # read M[K], write mu*M[K], write bf16 X
-        byts["scatter"] += k * o * (2.0 + 4.0 + 4.0)          # read bf16 O, read+write W[K]
+        # the library's path choice (dion2_api.cu build_layout)
+        if rows and k <= n:
+            sfx = "_rows"
+        elif (not rows) and k <= m and k <= 1024:
+            sfx = "_cols"
+        else:
+            sfx = ""
+        byts["gather" + sfx] += k * o * (4.0 + 4.0 + 2.0)     # read M[K], write mu*M[K], write bf16 X
+        byts["scatter" + sfx] += k * o * (2.0 + 4.0 + 4.0)    # read bf16 O, read+write W[K]
     return ns_flops, byts
 
 

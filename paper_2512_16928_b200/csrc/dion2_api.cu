@@ -22,10 +22,15 @@ using namespace dion2;
 
 namespace {
 
-constexpr int kNumPhases = 9;
-const char* kPhaseNames[kNumPhases] = {"momentum_score", "select", "gather", "norm", "ns_gram",
-                                       "ns_poly",        "ns_apply", "scatter", "full_decay"};
-enum Phase { PH_K1 = 0, PH_SELECT, PH_GATHER, PH_NORM, PH_GRAM, PH_POLY, PH_APPLY, PH_SCATTER, PH_FULLDECAY };
+constexpr int kNumPhases = 13;
+const char* kPhaseNames[kNumPhases] = {"momentum_score", "select",       "gather",       "norm",
+                                       "ns_gram",        "ns_poly",      "ns_apply",     "scatter",
+                                       "full_decay",     "gather_rows",  "gather_cols",  "scatter_rows",
+                                       "scatter_cols"};
+enum Phase {
+  PH_K1 = 0, PH_SELECT, PH_GATHER, PH_NORM, PH_GRAM, PH_POLY, PH_APPLY, PH_SCATTER, PH_FULLDECAY,
+  PH_GATHER_ROWS, PH_GATHER_COLS, PH_SCATTER_ROWS, PH_SCATTER_COLS
+};
 
 std::mutex g_mu;
 int g_sm_count = 0;
@@ -68,7 +73,8 @@ PFN_cuTensorMapEncodeTiled_v12000 get_encode_fn() {
 }
 
 // 3-D bf16 tensor map over [count][rows][cols] (row-major), SWIZZLE_128B, box {64, box_rows, 1}.
-bool make_map(CUtensorMap* m, const void* base, int64_t cols, int64_t rows, int64_t count, int box_cols, int box_rows) {
+bool make_map(CUtensorMap* m, const void* base, int64_t cols, int64_t rows, int64_t count, int box_cols, int box_rows,
+              CUtensorMapSwizzle swz = CU_TENSOR_MAP_SWIZZLE_128B) {
   auto enc = get_encode_fn();
   if (!enc) return false;
   cuuint64_t dims[3] = {(cuuint64_t)cols, (cuuint64_t)rows, (cuuint64_t)count};
@@ -76,7 +82,7 @@ bool make_map(CUtensorMap* m, const void* base, int64_t cols, int64_t rows, int6
   cuuint32_t box[3] = {(cuuint32_t)box_cols, (cuuint32_t)box_rows, 1};
   cuuint32_t estr[3] = {1, 1, 1};
   CUresult r = enc(m, CU_TENSOR_MAP_DATA_TYPE_BFLOAT16, 3, const_cast<void*>(base), dims, strides, box, estr,
-                   CU_TENSOR_MAP_INTERLEAVE_NONE, CU_TENSOR_MAP_SWIZZLE_128B, CU_TENSOR_MAP_L2_PROMOTION_L2_256B,
+                   CU_TENSOR_MAP_INTERLEAVE_NONE, swz, CU_TENSOR_MAP_L2_PROMOTION_L2_256B,
                    CU_TENSOR_MAP_FLOAT_OOB_FILL_NONE);
   return r == CUDA_SUCCESS;
 }
@@ -452,6 +458,9 @@ int build_device_plan(Plan& P, const dion2_matrix* mats, const dion2_config* c, 
               }
             }
             (void)xel;
+            if (P.bf16_ns &&
+                !make_map(&L.tc.mapD[j], G.out, G.out_ld, g.p_pad, g.count, 32, 32, CU_TENSOR_MAP_SWIZZLE_64B))
+              return DION2_ECUDA;
             G.tile_base = tiles;
             tiles += G.count * G.m_tiles * G.n_tiles;
           }
@@ -591,14 +600,14 @@ int run_step(Plan& P, const dion2_matrix* mats, const dion2_config* c, void* ws,
       L.end();
     }
     if (P.fl_n[0]) {
-      L.begin(PH_GATHER);
+      L.begin(PH_GATHER_ROWS);
       const int blocks = (int)std::min<int64_t>(ceil_div(P.fl_gunits[0], 8), (int64_t)sms * 8);
       launch_gather_rows(blocks, s, dmats, (const int32_t*)tab(P, P.off_fl_mats[0]),
                          (const int32_t*)tab(P, P.off_fl_gprefix[0]), P.fl_n[0], P.fl_gunits[0], bad, c->mu);
       L.end();
     }
     if (P.fl_n[1]) {
-      L.begin(PH_GATHER);
+      L.begin(PH_GATHER_COLS);
       const int blocks = std::min(P.fl_gunits[1], sms * 4);
       launch_gather_cols_t(blocks, P.fl_maxk, s, dmats, (const int32_t*)tab(P, P.off_fl_mats[1]),
                            (const int32_t*)tab(P, P.off_fl_gprefix[1]), P.fl_n[1], P.fl_gunits[1], bad, c->mu);
@@ -632,14 +641,14 @@ int run_step(Plan& P, const dion2_matrix* mats, const dion2_config* c, void* ws,
       L.end();
     }
     if (P.fl_n[0]) {
-      L.begin(PH_SCATTER);
+      L.begin(PH_SCATTER_ROWS);
       const int blocks = (int)std::min<int64_t>(ceil_div(P.fl_sunits[0], 8), (int64_t)sms * 8);
       launch_scatter_rows(blocks, s, dmats, (const int32_t*)tab(P, P.off_fl_mats[0]),
                           (const int32_t*)tab(P, P.off_fl_sprefix[0]), P.fl_n[0], P.fl_sunits[0], bad, c->lr);
       L.end();
     }
     if (P.fl_n[1]) {
-      L.begin(PH_SCATTER);
+      L.begin(PH_SCATTER_COLS);
       const int blocks = std::min(P.fl_sunits[1], sms * 4);
       launch_scatter_cols_t(blocks, P.fl_maxk, s, dmats, (const int32_t*)tab(P, P.off_fl_mats[1]),
                             (const int32_t*)tab(P, P.off_fl_sprefix[1]), P.fl_n[1], P.fl_sunits[1], bad, c->lr);

@@ -84,6 +84,7 @@ __global__ void __launch_bounds__(192, 1) k_ns_gemm_tc(const __grid_constant__ N
     for (int gi = 0; gi < p.ngroups; ++gi) {
       tma_prefetch_desc(&P.mapA[gi]);
       tma_prefetch_desc(&P.mapB[gi]);
+      tma_prefetch_desc(&P.mapD[gi]);
     }
   }
   if (warp == 1) tmem_alloc(tmem_base_slot, kTmemCols);
@@ -154,6 +155,8 @@ __global__ void __launch_bounds__(192, 1) k_ns_gemm_tc(const __grid_constant__ N
     // ---------------- epilogue (warps 2..5 -> TMEM lane groups 2,3,0,1)
     const int lg = warp & 3;
     const int row_in_tile = lg * 32 + lane;
+    uint8_t* stage_base = smem + S * kStageBytes + 1024;  // 1024-B aligned, after the barriers
+    int sbuf = 0;
     int it = 0;
     for (int t = blockIdx.x; t < p.total_tiles; t += gridDim.x, ++it) {
       const TileCoord c = decode_tile(p, t);
@@ -164,12 +167,17 @@ __global__ void __launch_bounds__(192, 1) k_ns_gemm_tc(const __grid_constant__ N
       if (p.scale_sel) osc = p.ns_scale_all[2 * G.gmats[c.z] + (p.scale_sel - 1)];
       const float ca = p.cacc * osc, cc = p.cC * osc, dterm = p.diag * osc;
       const int64_t row = (int64_t)c.tm * kBM + row_in_tile;
-      __nv_bfloat16* out = reinterpret_cast<__nv_bfloat16*>(G.out) + (int64_t)c.z * G.out_mstride + row * G.out_ld +
-                           (int64_t)c.tn * BN;
       const __nv_bfloat16* cin =
           G.cin ? reinterpret_cast<const __nv_bfloat16*>(G.cin) + (int64_t)c.z * G.cin_mstride + row * G.cin_ld +
                       (int64_t)c.tn * BN
                 : nullptr;
+      // C-term (poly: b*A) for chunk 0 is fetched before the accumulator is ready,
+      // then one chunk ahead: its latency hides under the MMA / the previous chunk.
+      uint4 craw[4] = {};
+      if (cin) {
+#pragma unroll
+        for (int q = 0; q < 4; ++q) craw[q] = reinterpret_cast<const uint4*>(cin)[q];
+      }
       mbar_wait(&tfull_bar[acc], acc_phase);
       tc_fence_after();
 #pragma unroll 1
@@ -177,21 +185,18 @@ __global__ void __launch_bounds__(192, 1) k_ns_gemm_tc(const __grid_constant__ N
         float v[32];
         tmem_ld_32x32b_x32(tmem_base + acc * BN + cc32 * 32 + ((uint32_t)(lg * 32) << 16), v);
         float cv[32];
-        if (cin) {
-          const uint4* src = reinterpret_cast<const uint4*>(cin + cc32 * 32);
 #pragma unroll
-          for (int q = 0; q < 4; ++q) {
-            uint4 u = src[q];
-            const __nv_bfloat162* h = reinterpret_cast<const __nv_bfloat162*>(&u);
+        for (int q = 0; q < 4; ++q) {
+          const __nv_bfloat162* h = reinterpret_cast<const __nv_bfloat162*>(&craw[q]);
 #pragma unroll
-            for (int e = 0; e < 4; ++e) {
-              cv[q * 8 + 2 * e] = __low2float(h[e]);
-              cv[q * 8 + 2 * e + 1] = __high2float(h[e]);
-            }
+          for (int e = 0; e < 4; ++e) {
+            cv[q * 8 + 2 * e] = __low2float(h[e]);
+            cv[q * 8 + 2 * e + 1] = __high2float(h[e]);
           }
-        } else {
+        }
+        if (cin && cc32 + 1 < BN / 32) {
 #pragma unroll
-          for (int e = 0; e < 32; ++e) cv[e] = 0.f;
+          for (int q = 0; q < 4; ++q) craw[q] = reinterpret_cast<const uint4*>(cin + (cc32 + 1) * 32)[q];
         }
         // diagonal term (poly phase: C = a*I + b*A + c*A*A): element e sits on the
         // global diagonal iff row == col0 + e
@@ -199,7 +204,11 @@ __global__ void __launch_bounds__(192, 1) k_ns_gemm_tc(const __grid_constant__ N
         float o[32];
 #pragma unroll
         for (int e = 0; e < 32; ++e) o[e] = ca * v[e] + cc * cv[e] + (e == dcol ? dterm : 0.f);
-        uint4* dst = reinterpret_cast<uint4*>(out + cc32 * 32);
+        // stage the 32x32 bf16 chunk in SWIZZLE_64B layout (row = lane, 16-B chunk
+        // q stored at q ^ ((row >> 1) & 3): conflict-free) and TMA-store it
+        uint8_t* buf = stage_base + (lg * 2 + sbuf) * 2048;
+        if (lane == 0) bulk_wait_read<1>();  // the store that used this buffer two chunks ago is done reading
+        __syncwarp();
 #pragma unroll
         for (int q = 0; q < 4; ++q) {
           uint4 u;
@@ -207,12 +216,20 @@ __global__ void __launch_bounds__(192, 1) k_ns_gemm_tc(const __grid_constant__ N
           u.y = pack_bf16x2(o[q * 8 + 2], o[q * 8 + 3]);
           u.z = pack_bf16x2(o[q * 8 + 4], o[q * 8 + 5]);
           u.w = pack_bf16x2(o[q * 8 + 6], o[q * 8 + 7]);
-          dst[q] = u;
+          *reinterpret_cast<uint4*>(buf + lane * 64 + ((q ^ ((lane >> 1) & 3)) << 4)) = u;
         }
+        fence_proxy_async_smem();
+        __syncwarp();
+        if (lane == 0) {
+          tma_store_3d(&P.mapD[c.group], buf, c.tn * BN + cc32 * 32, c.tm * kBM + lg * 32, c.z);
+          bulk_commit();
+        }
+        sbuf ^= 1;
       }
       tc_fence_before();
       mbar_arrive(&tempty_bar[acc]);
     }
+    if (lane == 0) bulk_wait_all();
   }
   tc_fence_before();
   __syncthreads();

@@ -69,6 +69,7 @@ struct NsParams {
 struct NsTcParams {
   CUtensorMap mapA[kMaxGroups];
   CUtensorMap mapB[kMaxGroups];
+  CUtensorMap mapD[kMaxGroups];  // output (TMA store): box {32 cols, 32 rows, 1}, SWIZZLE_64B
   NsParams p;
 };
 void ns_tc_set_attrs();
@@ -77,7 +78,8 @@ template <int BN>
 constexpr int ns_tc_stages() { return BN == 256 ? 4 : 6; }
 template <int BN>
 constexpr int ns_tc_smem_bytes() {
-  return 1024 /*align slack*/ + ns_tc_stages<BN>() * (128 * 64 * 2 + BN * 64 * 2) + 256 /*barriers*/;
+  return 1024 /*align slack*/ + ns_tc_stages<BN>() * (128 * 64 * 2 + BN * 64 * 2) + 1024 /*barriers*/ +
+         4 * 2 * 2048 /*epilogue staging: 4 warps x 2 buffers x (32 x 32 bf16)*/;
 }
 
 // fp32 SIMT validation path (k_ns_simt.cu): grid (n_tiles, m_tiles, count) per group.

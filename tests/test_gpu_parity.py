@@ -192,5 +192,5 @@ def test_phase_timing_and_launch_count():
     finally:
         set_phase_timing(False)
     assert last_launch_count() >= 7
-    for ph in ("momentum_score", "select", "gather", "ns_gram", "ns_poly", "ns_apply", "scatter"):
+    for ph in ("momentum_score", "select", "gather_rows", "ns_gram", "ns_poly", "ns_apply", "scatter_rows"):
         assert times[ph][1] >= 1 and times[ph][0] > 0
