@@ -43,10 +43,10 @@ def load_peaks():
     return PEAKS_FALLBACK, "fallback"
 
 
-def model_shapes(name: str):
+def model_shapes(name: str, layers: int = 0):
     from synth import layer_set_1b, layer_set_8b
     if name == "1b":
-        return layer_set_1b(24)
+        return layer_set_1b(layers or 24)
     if name == "1b16":
         return layer_set_1b(16)
     if name == "8b":
@@ -254,7 +254,7 @@ def run_ours(args):
     dev = torch.device("cuda", local)
     barrier = (lambda: dist.barrier()) if world > 1 else None
 
-    shapes = model_shapes(args.config)
+    shapes = model_shapes(args.config, args.layers)
     n_params = sum(m * n for m, n in shapes)
     bufs, Ws, Ms, Gs = build_state(shapes, dev, seed=rank)
     opt = Dion2(alpha=args.alpha, axis="auto", precision="bf16")
@@ -323,11 +323,13 @@ def run_ours(args):
         opt.step(Ws, Ms, Gs)
 
     # end to end through the public API (host G)
-    e2e_ms, h2d, d2h, rc2 = e2e_run(opt, Ws, Ms, Gs, bufs[2], max(2, min(args.steps, 5)))
+    e2e_ms, h2d, d2h = None, None, None
+    if not args.no_e2e:
+        e2e_ms, h2d, d2h, _ = e2e_run(opt, Ws, Ms, Gs, bufs[2], max(2, min(args.steps, 5)))
 
     # max over ranks
     if world > 1:
-        t = torch.tensor([ms, e2e_ms], device=dev)
+        t = torch.tensor([ms, e2e_ms or 0.0], device=dev)
         dist.all_reduce(t, op=dist.ReduceOp.MAX)
         ms, e2e_ms = t.tolist()
 
@@ -424,6 +426,8 @@ def main():
     ap.add_argument("--no-alpha1", action="store_true")
     ap.add_argument("--no-cpu", action="store_true")
     ap.add_argument("--cpu-budget", type=float, default=20.0)
+    ap.add_argument("--layers", type=int, default=0, help="override the layer count (profiling only)")
+    ap.add_argument("--no-e2e", action="store_true")
     args = ap.parse_args()
     if args.impl == "reference":
         run_reference(args)
