@@ -212,7 +212,7 @@ int build_layout(Plan& P, const dion2_matrix* mats, int n, const dion2_config* c
     q.transposed = q.sr > q.sc;  // wide orientation (reading R4)
     q.p = std::min(q.sr, q.sc);
     q.q = std::max(q.sr, q.sc);
-    q.p_pad = (int)align_up(q.p, 128);
+    q.p_pad = (int)align_up(q.p, 256);  // 256-row CTA-pair tiles
     q.q_pad = (int)align_up(q.q, 256);
     if (c->scale_mode == 0) q.fan_sqrt = (float)std::sqrt((double)rows / (double)cols);  // Alg. 1 l.6
     else q.fan_sqrt = (float)std::sqrt((double)q.sr / (double)q.sc);
@@ -386,6 +386,9 @@ int build_device_plan(Plan& P, const dion2_matrix* mats, const dion2_config* c, 
   // groups are batched (<= kMaxGroups per launch, one BN class per launch).
   P.ns_launches.clear();
   const float* scale_all = (const float*)at(ws, P.off_nsscale);
+  // bf16 path: 2-SM (cta_group::2) 256 x 256 tiles; DION2_NS_1SM=1 selects the 1-SM 128 x 256 kernel
+  const bool pair = P.bf16_ns && !getenv("DION2_NS_1SM");
+  const int MT = pair ? 256 : 128;
   for (int t = 0; t < P.ns_steps; ++t) {
     const float a = c->ns_coeffs[t][0], b = c->ns_coeffs[t][1], cc = c->ns_coeffs[t][2];
     for (int ph = PH_GRAM; ph <= PH_APPLY; ++ph) {
@@ -403,7 +406,7 @@ int build_device_plan(Plan& P, const dion2_matrix* mats, const dion2_config* c, 
           Launch L{};
           L.phase = ph;
           L.bn = BN;
-          L.kind = P.bf16_ns ? cls : 2;
+          L.kind = P.bf16_ns ? (pair ? 3 : cls) : 2;
           NsParams& np = L.tc.p;
           np.ngroups = (int)std::min<size_t>(kMaxGroups, gl.size() - s0);
           np.ns_scale_all = scale_all;
@@ -426,27 +429,27 @@ int build_device_plan(Plan& P, const dion2_matrix* mats, const dion2_config* c, 
             G.gmats = (const int32_t*)tab(P, g.off_gmats);
             const long long xs = (long long)g.p_pad * g.q_pad, as = (long long)g.p_pad * g.p_pad;
             if (ph == PH_GRAM) {
-              G.m_tiles = g.p_pad / 128; G.n_tiles = g.p_pad / BN; G.k_blocks = g.q_pad / 64;
+              G.m_tiles = g.p_pad / MT; G.n_tiles = g.p_pad / BN; G.k_blocks = g.q_pad / 64;
               G.a = Xc; G.a_mstride = xs; G.lda = g.q_pad;
               G.b = Xc; G.b_mstride = xs; G.ldb = g.q_pad;
               G.out = A; G.out_mstride = as; G.out_ld = g.p_pad;
               G.cin = nullptr; G.cin_mstride = 0; G.cin_ld = 0;
               if (P.bf16_ns) {
                 if (!make_map(&L.tc.mapA[j], Xc, g.q_pad, g.p_pad, g.count, 64, 128)) return DION2_ECUDA;
-                if (!make_map(&L.tc.mapB[j], Xc, g.q_pad, g.p_pad, g.count, 64, BN)) return DION2_ECUDA;
+                if (!make_map(&L.tc.mapB[j], Xc, g.q_pad, g.p_pad, g.count, 64, pair ? 128 : BN)) return DION2_ECUDA;
               }
             } else if (ph == PH_POLY) {
-              G.m_tiles = g.p_pad / 128; G.n_tiles = g.p_pad / BN; G.k_blocks = g.p_pad / 64;
+              G.m_tiles = g.p_pad / MT; G.n_tiles = g.p_pad / BN; G.k_blocks = g.p_pad / 64;
               G.a = A; G.a_mstride = as; G.lda = g.p_pad;
               G.b = A; G.b_mstride = as; G.ldb = g.p_pad;
               G.out = Bm; G.out_mstride = as; G.out_ld = g.p_pad;
               G.cin = A; G.cin_mstride = as; G.cin_ld = g.p_pad;
               if (P.bf16_ns) {
                 if (!make_map(&L.tc.mapA[j], A, g.p_pad, g.p_pad, g.count, 64, 128)) return DION2_ECUDA;
-                if (!make_map(&L.tc.mapB[j], A, g.p_pad, g.p_pad, g.count, 64, BN)) return DION2_ECUDA;
+                if (!make_map(&L.tc.mapB[j], A, g.p_pad, g.p_pad, g.count, 64, pair ? 128 : BN)) return DION2_ECUDA;
               }
             } else {
-              G.m_tiles = g.p_pad / 128; G.n_tiles = g.q_pad / BN; G.k_blocks = g.p_pad / 64;
+              G.m_tiles = g.p_pad / MT; G.n_tiles = g.q_pad / BN; G.k_blocks = g.p_pad / 64;
               G.a = Bm; G.a_mstride = as; G.lda = g.p_pad;
               G.b = Xc; G.b_mstride = xs; G.ldb = g.q_pad;
               G.out = Xn; G.out_mstride = xs; G.out_ld = g.q_pad;
@@ -489,6 +492,7 @@ void ensure_device_attrs() {
   cudaDeviceGetAttribute(&g_sm_count, cudaDevAttrMultiProcessorCount, dev);
   ns_tc_set_attrs();
   launch_fast_paths_attrs();
+  ns_pair_set_attrs();
   cudaFuncSetAttribute(k_topk_select, cudaFuncAttributeMaxDynamicSharedMemorySize, 4 * DION2_MAX_SELECT_DIM);
   cudaFuncSetAttribute(k_full_decay, cudaFuncAttributeMaxDynamicSharedMemorySize, DION2_MAX_SELECT_DIM);
   g_attr_done = true;
@@ -620,7 +624,9 @@ int run_step(Plan& P, const dion2_matrix* mats, const dion2_config* c, void* ws,
   // K4-K6 Newton-Schulz (Alg. 1 l.4)
   for (const Launch& ln : P.ns_launches) {
     L.begin(ln.phase);
-    if (ln.kind == 0 || ln.kind == 1) {
+    if (ln.kind == 3) {
+      launch_ns_pair(std::min(2 * ln.tc.p.total_tiles, sms & ~1), s, ln.tc);
+    } else if (ln.kind == 0 || ln.kind == 1) {
       launch_ns_tc(ln.bn, std::min(ln.tc.p.total_tiles, sms), s, ln.tc);
     } else {
       const NsGroup& G = ln.tc.p.g[ln.simt_group];

@@ -1,0 +1,254 @@
+// K4-K6 on a CTA pair: tcgen05.mma.cta_group::2, 256 x 256 x 16 per instruction.
+//
+// Same three Newton-Schulz phases and epilogue algebra as k_ns_tcgen05.cu
+// (gram A = s^2 X X^T; poly C = a I + b A + c A A^T; apply X' = s C X; PAPER.md
+// P:65, Alg. 1 l.4, readings R1-R6), but each tile is computed by a cluster
+// of two CTAs on one TPC: CTA r stages rows [128 r, 128 r + 128) of the A
+// operand and half of the B operand, the leader CTA issues one 256 x 256 MMA
+// that reads both CTAs' shared memory, and each CTA's TMEM receives its 128
+// accumulator rows.  Per SM this halves the B-operand shared-memory traffic
+// (TMA write + MMA read), which caps the 1-CTA 128 x 256 tile near 65-70% of
+// peak (ncu: profiles/).
+//
+// Roles per CTA (192 threads): warp 0 TMA producer (both CTAs; completion is
+// counted on the leader's full barrier), warp 1 TMEM allocator (both) + MMA
+// issuer (leader only), warps 2-5 epilogue (both; TMEM -> bf16 -> swizzled
+// smem -> TMA store).  TMEM: two 256-column fp32 accumulators.
+#include "kernels.cuh"
+
+namespace dion2 {
+
+namespace {
+
+constexpr int kBK = 64;
+constexpr int kStagesPair = 6;
+constexpr uint32_t kAB = 128 * kBK * 2;      // A half-tile per CTA (128 rows x 64 k)
+constexpr uint32_t kBB = 128 * kBK * 2;      // B half-tile per CTA (128 n x 64 k)
+constexpr uint32_t kStage = kAB + kBB;       // 32 KiB
+constexpr uint32_t kTmemCols = 512;
+constexpr uint32_t kIdescK = umma_idesc_bf16(256, 256, 0);
+constexpr uint32_t kIdescMN = umma_idesc_bf16(256, 256, 1);
+
+struct TileCoord {
+  int group, z, tm, tn;
+};
+
+__device__ __forceinline__ TileCoord decode_tile(const NsParams& p, int t) {
+  int g = 0;
+#pragma unroll
+  for (int i = 1; i < kMaxGroups; ++i)
+    if (i < p.ngroups && t >= p.g[i].tile_base) g = i;
+  const NsGroup& G = p.g[g];
+  const int local = t - G.tile_base;
+  const int per = G.m_tiles * G.n_tiles;
+  TileCoord c;
+  c.group = g;
+  c.z = local / per;
+  const int r = local % per;
+  c.tm = r / G.n_tiles;
+  c.tn = r % G.n_tiles;
+  return c;
+}
+
+__device__ __forceinline__ uint32_t pack_bf16x2(float lo, float hi) {
+  __nv_bfloat162 v = __floats2bfloat162_rn(lo, hi);
+  return *reinterpret_cast<uint32_t*>(&v);
+}
+
+}  // namespace
+
+constexpr int ns_pair_smem_bytes() { return 1024 + kStagesPair * (int)kStage + 1024 + 4 * 2 * 2048; }
+
+__global__ void __cluster_dims__(2, 1, 1) __launch_bounds__(192, 1)
+    k_ns_gemm_tc_pair(const __grid_constant__ NsTcParams P) {
+  constexpr int S = kStagesPair;
+  extern __shared__ uint8_t smem_raw[];
+  uint8_t* smem = reinterpret_cast<uint8_t*>((reinterpret_cast<uintptr_t>(smem_raw) + 1023) & ~uintptr_t(1023));
+  uint64_t* full_bar = reinterpret_cast<uint64_t*>(smem + S * kStage);
+  uint64_t* empty_bar = full_bar + S;
+  uint64_t* tfull_bar = empty_bar + S;
+  uint64_t* tempty_bar = tfull_bar + 2;
+  uint32_t* tmem_base_slot = reinterpret_cast<uint32_t*>(tempty_bar + 2);
+  uint8_t* stage_base = smem + S * kStage + 1024;
+
+  const NsParams& p = P.p;
+  const int warp = threadIdx.x >> 5, lane = threadIdx.x & 31;
+  const uint32_t rank = cluster_ctarank();
+  const int cid = (int)cluster_id_x(), ncl = (int)nclusters_x();
+
+  if (warp == 0 && lane == 0) {
+    for (int i = 0; i < S; ++i) {
+      mbar_init(&full_bar[i], 1);
+      mbar_init(&empty_bar[i], 1);
+    }
+    for (int i = 0; i < 2; ++i) {
+      mbar_init(&tfull_bar[i], 1);
+      mbar_init(&tempty_bar[i], 8);  // one arrival per epilogue warp of both CTAs
+    }
+    fence_mbar_init();
+    for (int gi = 0; gi < p.ngroups; ++gi) {
+      tma_prefetch_desc(&P.mapA[gi]);
+      tma_prefetch_desc(&P.mapB[gi]);
+      tma_prefetch_desc(&P.mapD[gi]);
+    }
+  }
+  if (warp == 1) tmem_alloc_pair(tmem_base_slot, kTmemCols);
+  tc_fence_before();
+  cluster_sync();
+  tc_fence_after();
+  const uint32_t tmem_base = *tmem_base_slot;
+
+  if (warp == 0) {
+    if (lane == 0) {
+      // ---------------- TMA producer (both CTAs)
+      int stage = 0;
+      uint32_t phase = 0;
+      for (int t = cid; t < p.total_tiles; t += ncl) {
+        const TileCoord c = decode_tile(p, t);
+        const NsGroup& G = p.g[c.group];
+        for (int kb = 0; kb < G.k_blocks; ++kb) {
+          mbar_wait(&empty_bar[stage], phase ^ 1);
+          uint8_t* sa = smem + stage * kStage;
+          uint8_t* sb = sa + kAB;
+          const uint32_t leader_full = mapa_shared(smem_u32(&full_bar[stage]), 0);
+          if (rank == 0) mbar_arrive_expect_tx(&full_bar[stage], 2 * kStage);
+          tma_load_3d_pair(sa, &P.mapA[c.group], leader_full, kb * kBK, c.tm * 256 + (int)rank * 128, c.z);
+          if (p.b_kmajor) {
+            tma_load_3d_pair(sb, &P.mapB[c.group], leader_full, kb * kBK, c.tn * 256 + (int)rank * 128, c.z);
+          } else {
+#pragma unroll
+            for (int j = 0; j < 2; ++j)
+              tma_load_3d_pair(sb + j * 64 * kBK * 2, &P.mapB[c.group], leader_full,
+                               c.tn * 256 + (int)rank * 128 + j * 64, kb * kBK, c.z);
+          }
+          if (++stage == S) { stage = 0; phase ^= 1; }
+        }
+      }
+    }
+  } else if (warp == 1) {
+    if (lane == 0 && rank == 0) {
+      // ---------------- MMA issuer (leader CTA)
+      const uint32_t idesc = p.b_kmajor ? kIdescK : kIdescMN;
+      int stage = 0;
+      uint32_t phase = 0;
+      int it = 0;
+      for (int t = cid; t < p.total_tiles; t += ncl, ++it) {
+        const TileCoord c = decode_tile(p, t);
+        const NsGroup& G = p.g[c.group];
+        const int acc = it & 1;
+        const uint32_t acc_phase = (it >> 1) & 1;
+        mbar_wait(&tempty_bar[acc], acc_phase ^ 1);
+        tc_fence_after();
+        const uint32_t tmem_d = tmem_base + acc * 256;
+        for (int kb = 0; kb < G.k_blocks; ++kb) {
+          mbar_wait(&full_bar[stage], phase);
+          tc_fence_after();
+          const uint32_t a_addr = smem_u32(smem + stage * kStage);
+          const uint32_t b_addr = a_addr + kAB;
+#pragma unroll
+          for (int k = 0; k < kBK / 16; ++k) {
+            const uint64_t adesc = umma_desc_sw128(a_addr + k * 32, 16, 1024);
+            const uint64_t bdesc = p.b_kmajor ? umma_desc_sw128(b_addr + k * 32, 16, 1024)
+                                              : umma_desc_sw128(b_addr + k * 2048, 64 * kBK * 2, 1024);
+            umma_bf16_ss_pair(tmem_d, adesc, bdesc, idesc, (kb | k) != 0);
+          }
+          umma_commit_pair(&empty_bar[stage]);
+          if (++stage == S) { stage = 0; phase ^= 1; }
+        }
+        umma_commit_pair(&tfull_bar[acc]);
+      }
+    }
+  } else {
+    // ---------------- epilogue (both CTAs; warps 2..5 -> TMEM lane groups 2,3,0,1)
+    const int lg = warp & 3;
+    const int row_in_tile = (int)rank * 128 + lg * 32 + lane;
+    const uint32_t leader_tempty[2] = {mapa_shared(smem_u32(&tempty_bar[0]), 0),
+                                       mapa_shared(smem_u32(&tempty_bar[1]), 0)};
+    int sbuf = 0;
+    int it = 0;
+    for (int t = cid; t < p.total_tiles; t += ncl, ++it) {
+      const TileCoord c = decode_tile(p, t);
+      const NsGroup& G = p.g[c.group];
+      const int acc = it & 1;
+      const uint32_t acc_phase = (it >> 1) & 1;
+      float osc = 1.f;
+      if (p.scale_sel) osc = p.ns_scale_all[2 * G.gmats[c.z] + (p.scale_sel - 1)];
+      const float ca = p.cacc * osc, cc = p.cC * osc, dterm = p.diag * osc;
+      const int64_t row = (int64_t)c.tm * 256 + row_in_tile;
+      const __nv_bfloat16* cin =
+          G.cin ? reinterpret_cast<const __nv_bfloat16*>(G.cin) + (int64_t)c.z * G.cin_mstride + row * G.cin_ld +
+                      (int64_t)c.tn * 256
+                : nullptr;
+      uint4 craw[4] = {};
+      if (cin) {
+#pragma unroll
+        for (int q = 0; q < 4; ++q) craw[q] = reinterpret_cast<const uint4*>(cin)[q];
+      }
+      mbar_wait(&tfull_bar[acc], acc_phase);
+      tc_fence_after();
+#pragma unroll 1
+      for (int cc32 = 0; cc32 < 8; ++cc32) {
+        float v[32];
+        tmem_ld_32x32b_x32(tmem_base + acc * 256 + cc32 * 32 + ((uint32_t)(lg * 32) << 16), v);
+        float cv[32];
+#pragma unroll
+        for (int q = 0; q < 4; ++q) {
+          const __nv_bfloat162* h = reinterpret_cast<const __nv_bfloat162*>(&craw[q]);
+#pragma unroll
+          for (int e = 0; e < 4; ++e) {
+            cv[q * 8 + 2 * e] = __low2float(h[e]);
+            cv[q * 8 + 2 * e + 1] = __high2float(h[e]);
+          }
+        }
+        if (cin && cc32 + 1 < 8) {
+#pragma unroll
+          for (int q = 0; q < 4; ++q) craw[q] = reinterpret_cast<const uint4*>(cin + (cc32 + 1) * 32)[q];
+        }
+        const int dcol = (int)(row - ((int64_t)c.tn * 256 + cc32 * 32));
+        float o[32];
+#pragma unroll
+        for (int e = 0; e < 32; ++e) o[e] = ca * v[e] + cc * cv[e] + (e == dcol ? dterm : 0.f);
+        uint8_t* buf = stage_base + (lg * 2 + sbuf) * 2048;
+        if (lane == 0) bulk_wait_read<1>();
+        __syncwarp();
+#pragma unroll
+        for (int q = 0; q < 4; ++q) {
+          uint4 u;
+          u.x = pack_bf16x2(o[q * 8 + 0], o[q * 8 + 1]);
+          u.y = pack_bf16x2(o[q * 8 + 2], o[q * 8 + 3]);
+          u.z = pack_bf16x2(o[q * 8 + 4], o[q * 8 + 5]);
+          u.w = pack_bf16x2(o[q * 8 + 6], o[q * 8 + 7]);
+          *reinterpret_cast<uint4*>(buf + lane * 64 + ((q ^ ((lane >> 1) & 3)) << 4)) = u;
+        }
+        fence_proxy_async_smem();
+        __syncwarp();
+        if (lane == 0) {
+          tma_store_3d(&P.mapD[c.group], buf, c.tn * 256 + cc32 * 32, c.tm * 256 + (int)rank * 128 + lg * 32, c.z);
+          bulk_commit();
+        }
+        sbuf ^= 1;
+      }
+      tc_fence_before();
+      __syncwarp();
+      if (lane == 0) mbar_arrive_cluster(leader_tempty[acc]);
+    }
+    if (lane == 0) bulk_wait_all();
+  }
+  tc_fence_before();
+  __syncthreads();
+  cluster_sync();
+  if (warp == 1) {
+    tc_fence_after();
+    tmem_dealloc_pair(tmem_base, kTmemCols);
+  }
+}
+
+void ns_pair_set_attrs() {
+  cudaFuncSetAttribute(k_ns_gemm_tc_pair, cudaFuncAttributeMaxDynamicSharedMemorySize, ns_pair_smem_bytes());
+}
+
+void launch_ns_pair(int grid, cudaStream_t s, const NsTcParams& P) {
+  k_ns_gemm_tc_pair<<<grid, 192, ns_pair_smem_bytes(), s>>>(P);
+}
+
+}  // namespace dion2

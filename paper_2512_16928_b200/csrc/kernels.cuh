@@ -74,6 +74,8 @@ struct NsTcParams {
 };
 void ns_tc_set_attrs();
 void launch_ns_tc(int bn, int grid, cudaStream_t s, const NsTcParams& P);
+void ns_pair_set_attrs();
+void launch_ns_pair(int grid, cudaStream_t s, const NsTcParams& P);
 template <int BN>
 constexpr int ns_tc_stages() { return BN == 256 ? 4 : 6; }
 template <int BN>
