@@ -387,11 +387,15 @@ int build_device_plan(Plan& P, const dion2_matrix* mats, const dion2_config* c, 
   P.ns_launches.clear();
   const float* scale_all = (const float*)at(ws, P.off_nsscale);
   // bf16 path: 2-SM (cta_group::2) 256 x 256 tiles; DION2_NS_1SM=1 selects the 1-SM 128 x 256 kernel
-  const bool pair = P.bf16_ns && !getenv("DION2_NS_1SM");
-  const int MT = pair ? 256 : 128;
+  // (measured: the pair kernel wins on the long-K gram, the 1-SM kernel on the
+  // short-K poly and the MN-major apply; DION2_NS_PAIR=all|none overrides)
+  const char* pair_env = getenv("DION2_NS_PAIR");
+  const int pair_mode = !pair_env ? 1 : (strcmp(pair_env, "all") == 0 ? 2 : (strcmp(pair_env, "none") == 0 ? 0 : 1));
   for (int t = 0; t < P.ns_steps; ++t) {
     const float a = c->ns_coeffs[t][0], b = c->ns_coeffs[t][1], cc = c->ns_coeffs[t][2];
     for (int ph = PH_GRAM; ph <= PH_APPLY; ++ph) {
+      const bool pair = P.bf16_ns && (pair_mode == 2 || (pair_mode == 1 && ph == PH_GRAM));
+      const int MT = pair ? 256 : 128;
       // bucket groups by BN class
       std::vector<int> by_bn[2];
       for (int gi = 0; gi < (int)P.groups.size(); ++gi) {
