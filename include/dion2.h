@@ -129,6 +129,62 @@ int dion2_get_phase_times(float* ms_out, int32_t* launches_out, int32_t cap, int
 /* Name of phase i ("momentum_score", "select", "gather", "ns_gram", "ns_poly", "ns_apply", "scatter", ...). */
 const char* dion2_phase_name(int32_t i);
 
+/* ------------------------------------------------------------------------------------------
+ * Multi-GPU: owner-compute step over P ranks (paper P:113: "only the
+ * selected subset of the matrix ... communicated").
+ *
+ * Every matrix is sharded over the P ranks along its NON-selection axis (the selection axis
+ * is resolved from the GLOBAL shape exactly as in dion2_step: auto = rows iff m <= n):
+ *   rows mode: rank r holds columns [r*n/P, (r+1)*n/P) of W, M, G   (shard rows x cols/P)
+ *   cols mode: rank r holds rows    [r*m/P, (r+1)*m/P) of W, M, G   (shard rows/P x cols)
+ * so every rank owns a slice of EVERY row (column) that can be selected.  The step:
+ *   1. M <- M + G and partial l1 scores on the local shard            (K1, local)
+ *   2. all-gather of the partial scores, summed in rank order         (NCCL; identical on all ranks)
+ *   3. top-k on every rank (identical K everywhere; no index traffic)  (K2)
+ *   4. X-piece = wide(M[K])[:, this rank's block] (k x o/P, bf16), local selective decay
+ *   5. pieces -> owner of the matrix (grouped ncclSend/ncclRecv)      (bytes ~ alpha)
+ *   6. owner: assemble X, Newton-Schulz, split O into pieces           (tcgen05 NS)
+ *   7. O pieces -> back to every rank; local W[K] update              (K7, local)
+ * Owners are assigned by LPT on NS FLOPs, identically on every rank.  All sizes are known on the
+ * host, so nothing synchronises the host inside a step.  Requirements: the sharded dimension
+ * divisible by P; rows mode n/P % 8 == 0; cols mode m/P % 32 == 0 and k <= 1024; k <= the other
+ * dimension (always true in auto mode); bf16 NS.  Otherwise DION2_EUNSUPPORTED.
+ * ------------------------------------------------------------------------------------------ */
+typedef struct {
+  int64_t rows;        /* GLOBAL m = fan-out */
+  int64_t cols;        /* GLOBAL n = fan-in */
+  int64_t ld;          /* row stride (elements) of the local shard, >= shard cols */
+  float* W;            /* local shard of W, fp32 */
+  float* M;            /* local shard of M, fp32 */
+  const void* G;       /* local shard of G, dtype cfg.grad_dtype */
+  int32_t* sel_out;    /* optional [k]: the selected indices (identical on every rank) */
+} dion2_shard;
+
+/* Host-only layout query for rank `rank` of `world` (no device work).  Any output may be NULL.
+ *   axis_out[n]          resolved selection axis per matrix
+ *   owner_out[n]         owning rank per matrix (LPT on NS FLOPs, ties -> lower index / rank)
+ *   shard_rows_out[n], shard_cols_out[n]   local shard shape
+ *   send_bytes_out[world], recv_bytes_out[world]   bytes this rank sends to / receives from each
+ *                        peer in ONE exchange direction (gather-to-owner; scatter-back mirrors it)
+ *   ws_bytes_out         workspace this rank needs */
+int dion2_dist_info(const dion2_shard* shards, int32_t n, const dion2_config* cfg, int32_t world, int32_t rank,
+                    int32_t* axis_out, int32_t* owner_out, int64_t* shard_rows_out, int64_t* shard_cols_out,
+                    int64_t* send_bytes_out, int64_t* recv_bytes_out, size_t* ws_bytes_out);
+
+/* One distributed step on this rank.  nccl_comm: an ncclComm_t (e.g. torch's
+ * ProcessGroupNCCL._comm_ptr()) spanning `world` ranks; NCCL calls are enqueued on `stream`.
+ * comm_bytes_out (HOST, optional): bytes this rank sent over the interconnect in this step. */
+int dion2_step_batched_dist(const dion2_shard* shards, int32_t n, const dion2_config* cfg, void* workspace,
+                            size_t ws_bytes, void* nccl_comm, int32_t world, int32_t rank, void* stream,
+                            uint64_t* comm_bytes_out);
+
+/* Loopback: all `world` ranks in this process on ONE device, exchanges done with device copies
+ * on `stream` (tests the distributed layout and kernels without NCCL or several GPUs).
+ * shards: [world * n], rank-major; workspaces: [world] HOST array of per-rank workspaces. */
+int dion2_step_batched_loopback(const dion2_shard* shards, int32_t n, const dion2_config* cfg,
+                                void* const* workspaces, size_t ws_bytes, int32_t world, void* stream,
+                                uint64_t* comm_bytes_out);
+
 /* Number of kernel launches the last step enqueued. */
 int32_t dion2_last_launch_count(void);
 

@@ -45,6 +45,7 @@ struct MatDesc {
   int32_t sa_pad, sb_pad;  // padded extents of S such that wide(S_pad) = X_pad (p_pad x q_pad)
   int32_t path;            // gather/scatter path: 0 generic tiles, 1 rows streaming, 2 cols streaming (X = S^T)
   int32_t n_sumsq;         // number of sum-of-squares partials K3 writes
+  int32_t scores_final;    // select reads `scores` as final (distributed step: combined across ranks)
   int32_t rowblocks;      // ceil(rows/64) (cols mode partials)
 };
 

@@ -15,22 +15,17 @@
 #include <string>
 #include <vector>
 
-#include "../../include/dion2.h"
-#include "kernels.cuh"
+#include "runtime.h"
 
 using namespace dion2;
+using namespace dion2rt;
 
-namespace {
+namespace dion2rt {
 
-constexpr int kNumPhases = 13;
 const char* kPhaseNames[kNumPhases] = {"momentum_score", "select",       "gather",       "norm",
                                        "ns_gram",        "ns_poly",      "ns_apply",     "scatter",
                                        "full_decay",     "gather_rows",  "gather_cols",  "scatter_rows",
                                        "scatter_cols"};
-enum Phase {
-  PH_K1 = 0, PH_SELECT, PH_GATHER, PH_NORM, PH_GRAM, PH_POLY, PH_APPLY, PH_SCATTER, PH_FULLDECAY,
-  PH_GATHER_ROWS, PH_GATHER_COLS, PH_SCATTER_ROWS, PH_SCATTER_COLS
-};
 
 std::mutex g_mu;
 int g_sm_count = 0;
@@ -39,10 +34,6 @@ int32_t g_last_launches = 0;
 
 // ------------------------------------------------------------------ phase timing
 bool g_timing = false;
-struct TimedLaunch {
-  int phase;
-  cudaEvent_t a, b;
-};
 std::vector<TimedLaunch> g_timed;
 std::vector<cudaEvent_t> g_event_pool;
 cudaEvent_t take_event() {
@@ -57,8 +48,6 @@ cudaEvent_t take_event() {
 }
 
 // ------------------------------------------------------------------ helpers
-inline size_t align_up(size_t x, size_t a) { return (x + a - 1) / a * a; }
-inline int64_t ceil_div(int64_t a, int64_t b) { return (a + b - 1) / b; }
 
 PFN_cuTensorMapEncodeTiled_v12000 get_encode_fn() {
   static PFN_cuTensorMapEncodeTiled_v12000 fn = nullptr;
@@ -74,7 +63,7 @@ PFN_cuTensorMapEncodeTiled_v12000 get_encode_fn() {
 
 // 3-D bf16 tensor map over [count][rows][cols] (row-major), SWIZZLE_128B, box {64, box_rows, 1}.
 bool make_map(CUtensorMap* m, const void* base, int64_t cols, int64_t rows, int64_t count, int box_cols, int box_rows,
-              CUtensorMapSwizzle swz = CU_TENSOR_MAP_SWIZZLE_128B) {
+              CUtensorMapSwizzle swz) {
   auto enc = get_encode_fn();
   if (!enc) return false;
   cuuint64_t dims[3] = {(cuuint64_t)cols, (cuuint64_t)rows, (cuuint64_t)count};
@@ -115,52 +104,6 @@ int validate_shape(const dion2_matrix& m, bool need_ptrs) {
 }
 
 // ------------------------------------------------------------------ plan
-struct MatPlan {
-  int axis, d, o, k, sr, sc, transposed, p, q, p_pad, q_pad, group, zi, rowblocks, ga, gb, sa_pad, sb_pad, path,
-      n_sumsq;
-  float fan_sqrt;
-  size_t off_scores, off_partials, off_sel, off_sumsq;
-};
-
-struct Group {
-  int p_pad, q_pad, count;
-  std::vector<int> mats;  // global matrix indices
-  size_t off_X0, off_X1, off_A, off_B, off_gmats;
-};
-
-struct Launch {
-  int phase;
-  int bn;
-  int kind;  // 0 = tc BN128, 1 = tc BN256, 2 = simt
-  NsTcParams tc;
-  int simt_group;
-};
-
-struct Plan {
-  int n;
-  bool bf16_ns;
-  int ns_steps;
-  std::vector<MatPlan> mp;
-  std::vector<Group> groups;
-  size_t off_status, off_bad, off_desc, off_rowmats, off_rowprefix, off_colmats, off_colprefix, off_gprefix,
-      off_nsscale, off_ns_begin, off_ns_end, total;
-  int64_t total_rows = 0, total_col_tiles = 0;
-  int n_row_mats = 0, n_col_mats = 0, total_gather_tiles = 0, max_d = 0;
-  // streaming fast paths: list 0 = rows (units: X rows p_pad / selected rows k),
-  // list 1 = cols with X = S^T (units: 32-row slabs of X's columns, q_pad / 32)
-  size_t off_fl_mats[2], off_fl_gprefix[2], off_fl_sprefix[2];
-  int fl_n[2] = {0, 0}, fl_gunits[2] = {0, 0}, fl_sunits[2] = {0, 0}, fl_maxk = 0;
-  std::vector<uint8_t> host_tables;  // [off_desc, off_ns_begin) image (descriptors + aux)
-  std::vector<Launch> ns_launches;
-  void* ws = nullptr;
-  uint64_t id = 0;
-  std::vector<const void*> last_ptrs;  // W, M, G, sel_out, O_out per matrix as last uploaded
-  void* dtab = nullptr;                // plan-owned device copy of host_tables
-};
-
-// device address of a table offset (tables are carved with workspace-style offsets
-// starting at off_desc but live in the plan-owned buffer)
-inline void* tab(Plan& P, size_t off) { return static_cast<uint8_t*>(P.dtab) + (off - P.off_desc); }
 
 std::map<std::string, std::unique_ptr<Plan>> g_plans;
 uint64_t g_next_plan_id = 1;
@@ -288,7 +231,6 @@ int build_layout(Plan& P, const dion2_matrix* mats, int n, const dion2_config* c
   return DION2_OK;
 }
 
-inline void* at(void* ws, size_t off) { return static_cast<uint8_t*>(ws) + off; }
 
 // Fill host tables and NS launches for a concrete workspace.
 int build_device_plan(Plan& P, const dion2_matrix* mats, const dion2_config* c, void* ws) {
@@ -502,41 +444,33 @@ void ensure_device_attrs() {
   g_attr_done = true;
 }
 
-struct Launcher {
-  cudaStream_t s;
-  int count = 0;
-  int err = DION2_OK;
-  int cur_phase = -1;
-  cudaEvent_t ev_a = nullptr;
-  void begin(int phase) {
-    cur_phase = phase;
-    if (g_timing) {
-      ev_a = take_event();
-      cudaEventRecord(ev_a, s);
-    }
+
+// norm finalize (optional) + the Newton-Schulz launch list of a plan.
+int run_ns(Plan& P, const dion2_config* c, Launcher& L, cudaStream_t s, bool do_norm) {
+  const int sms = g_sm_count > 0 ? g_sm_count : 148;
+  const MatDesc* dmats = (const MatDesc*)tab(P, P.off_desc);
+  if (do_norm) {
+    L.begin(PH_NORM);
+    k_norm_finalize<<<(unsigned)ceil_div(P.n, 8), 256, 0, s>>>(dmats, P.n, c->ns_eps);
+    L.end();
   }
-  void end() {
-    ++count;
-    if (cudaPeekAtLastError() != cudaSuccess) {
-      cudaGetLastError();
-      err = DION2_ECUDA;
+  for (const Launch& ln : P.ns_launches) {
+    L.begin(ln.phase);
+    if (ln.kind == 3) {
+      launch_ns_pair(std::min(2 * ln.tc.p.total_tiles, sms & ~1), s, ln.tc);
+    } else if (ln.kind == 0 || ln.kind == 1) {
+      launch_ns_tc(ln.bn, std::min(ln.tc.p.total_tiles, sms), s, ln.tc);
+    } else {
+      const NsGroup& G = ln.tc.p.g[ln.simt_group];
+      const int Mdim = G.m_tiles * 128;
+      const int Ndim = G.n_tiles * ln.bn;
+      dim3 grid(Ndim / 64, Mdim / 64, G.count);
+      k_ns_gemm_simt_f32<<<grid, 256, 0, s>>>(ln.tc.p, ln.simt_group);
     }
-    static const bool debug_sync = getenv("DION2_DEBUG_SYNC") != nullptr;
-    if (debug_sync) {
-      cudaError_t e = cudaStreamSynchronize(s);
-      if (e != cudaSuccess) {
-        fprintf(stderr, "[dion2] launch %d (phase %s) failed: %s\n", count, kPhaseNames[cur_phase],
-                cudaGetErrorString(e));
-        err = DION2_ECUDA;
-      }
-    }
-    if (g_timing) {
-      cudaEvent_t b = take_event();
-      cudaEventRecord(b, s);
-      g_timed.push_back({cur_phase, ev_a, b});
-    }
+    L.end();
   }
-};
+  return L.err;
+}
 
 int run_step(Plan& P, const dion2_matrix* mats, const dion2_config* c, void* ws, cudaStream_t s) {
   const int n = P.n;
@@ -621,26 +555,9 @@ int run_step(Plan& P, const dion2_matrix* mats, const dion2_config* c, void* ws,
                            (const int32_t*)tab(P, P.off_fl_gprefix[1]), P.fl_n[1], P.fl_gunits[1], bad, c->mu);
       L.end();
     }
-    L.begin(PH_NORM);
-    k_norm_finalize<<<(unsigned)ceil_div(n, 8), 256, 0, s>>>(dmats, n, c->ns_eps);
-    L.end();
   }
-  // K4-K6 Newton-Schulz (Alg. 1 l.4)
-  for (const Launch& ln : P.ns_launches) {
-    L.begin(ln.phase);
-    if (ln.kind == 3) {
-      launch_ns_pair(std::min(2 * ln.tc.p.total_tiles, sms & ~1), s, ln.tc);
-    } else if (ln.kind == 0 || ln.kind == 1) {
-      launch_ns_tc(ln.bn, std::min(ln.tc.p.total_tiles, sms), s, ln.tc);
-    } else {
-      const NsGroup& G = ln.tc.p.g[ln.simt_group];
-      const int Mdim = G.m_tiles * 128;
-      const int Ndim = G.n_tiles * ln.bn;
-      dim3 grid(Ndim / 64, Mdim / 64, G.count);
-      k_ns_gemm_simt_f32<<<grid, 256, 0, s>>>(ln.tc.p, ln.simt_group);
-    }
-    L.end();
-  }
+  // norm finalize + K4-K6 Newton-Schulz (Alg. 1 l.4)
+  run_ns(P, c, L, s, true);
   // K7 scatter (Alg. 1 l.6)
   {
     if (P.total_gather_tiles > 0) {
@@ -677,7 +594,7 @@ int run_step(Plan& P, const dion2_matrix* mats, const dion2_config* c, void* ws,
   return L.err;
 }
 
-}  // namespace
+}  // namespace dion2rt
 
 // ============================================================================ C ABI
 

@@ -1,0 +1,755 @@
+// dion2_dist.cu -- owner-compute distributed Dion2 step (include/dion2.h).
+//
+// Layout (per rank): every matrix j is sharded along its NON-selection axis, so the rank
+// holds a slice of every selectable row (column).  The rank's piece of X_j = wide(M[K])
+// is the column block X_j[:, rank*o/P : (rank+1)*o/P] (k x o/P), produced by the same
+// streaming gather kernels as the single-GPU step (with X pointing into the send buffer),
+// and consumed by the same scatter kernels (with the final X pointing into the receive
+// buffer).  The owner of j assembles X_j from the P blocks, runs the tcgen05 NS engine
+// of a regular single-GPU plan over its owned matrices, and splits X_T back.
+//
+// Transport: NCCL (ncclAllGather + grouped ncclSend/ncclRecv on the caller's stream,
+// resolved with dlsym from the process's libnccl -- torch's), or "loopback" (all ranks in
+// one process on one device; exchanges are device copies) for tests.
+#include <dlfcn.h>
+
+#include <algorithm>
+#include <cmath>
+#include <cstdio>
+#include <cstdlib>
+#include <cstring>
+#include <numeric>
+
+#include "runtime.h"
+
+using namespace dion2;
+
+namespace dion2rt {
+namespace {
+
+// ------------------------------------------------------------------ NCCL (dlsym)
+typedef int ncclResult_t;
+typedef void* ncclComm_t;
+constexpr int kNcclChar = 0, kNcclFloat32 = 7;
+struct NcclApi {
+  ncclResult_t (*allgather)(const void*, void*, size_t, int, ncclComm_t, cudaStream_t) = nullptr;
+  ncclResult_t (*send)(const void*, size_t, int, int, ncclComm_t, cudaStream_t) = nullptr;
+  ncclResult_t (*recv)(void*, size_t, int, int, ncclComm_t, cudaStream_t) = nullptr;
+  ncclResult_t (*group_start)() = nullptr;
+  ncclResult_t (*group_end)() = nullptr;
+  bool ok = false;
+};
+NcclApi& nccl_api() {
+  static NcclApi api = [] {
+    NcclApi a;
+    void* h = dlopen("libnccl.so.2", RTLD_NOW | RTLD_NOLOAD);
+    if (!h) h = dlopen("libnccl.so.2", RTLD_NOW | RTLD_GLOBAL);
+    if (!h) return a;
+    a.allgather = reinterpret_cast<decltype(a.allgather)>(dlsym(h, "ncclAllGather"));
+    a.send = reinterpret_cast<decltype(a.send)>(dlsym(h, "ncclSend"));
+    a.recv = reinterpret_cast<decltype(a.recv)>(dlsym(h, "ncclRecv"));
+    a.group_start = reinterpret_cast<decltype(a.group_start)>(dlsym(h, "ncclGroupStart"));
+    a.group_end = reinterpret_cast<decltype(a.group_end)>(dlsym(h, "ncclGroupEnd"));
+    a.ok = a.allgather && a.send && a.recv && a.group_start && a.group_end;
+    return a;
+  }();
+  return api;
+}
+
+// ------------------------------------------------------------------ plan
+struct DistMat {
+  int64_t m, n;            // global shape
+  int axis, d, o, k, qo;   // selection axis, its length, other length, selected, block width o/P
+  int64_t srows, scols;    // local shard shape
+  int owner;
+  int64_t piece;           // bytes of one k x qo bf16 piece (256-B aligned)
+  int64_t soff;            // offset of this matrix's piece inside its owner's section
+  double flops;
+  int path, ga, gb;
+  int n_sumsq;
+  size_t off_partials, off_sel, off_sumsq;
+};
+
+struct DistPlan {
+  int n = 0, world = 1, rank = 0;
+  std::vector<DistMat> dm;
+  int64_t total_d = 0;
+  // workspace offsets
+  size_t off_status, off_bad, off_scores, off_scores_all, off_sumsq_local, off_sumsq_all, off_send, off_recv,
+      off_osend, off_orecv, off_owner, total;
+  std::vector<int64_t> sdispl, scount;  // per owner: my send section
+  int64_t R = 0;                         // bytes per rank section of my recv / osend buffers
+  // device tables (plan-owned)
+  std::vector<uint8_t> htab;
+  void* dtab = nullptr;
+  size_t t_desc, t_rowmats, t_rowprefix, t_colmats, t_colprefix, t_flm[2], t_flg[2], t_fls[2], t_gidx, t_roff,
+      t_gprefix;
+  int n_row_mats = 0, n_col_mats = 0, fl_n[2] = {0, 0}, fl_gunits[2] = {0, 0}, fl_sunits[2] = {0, 0}, fl_maxk = 0,
+      max_d = 0, total_gather_tiles = 0;
+  int64_t total_rows = 0, total_col_tiles = 0, max_cols_col = 0;
+  std::vector<const void*> last_ptrs;
+  bool uploaded = false;
+  // owner side
+  std::vector<int> owned;
+  std::unique_ptr<Plan> owner;
+  PieceTable ptab{};
+  int max_p_pad = 0, max_k_owned = 0;
+};
+
+void* dt(DistPlan& D, size_t off) { return static_cast<uint8_t*>(D.dtab) + off; }
+
+int resolve(DistPlan& D, const dion2_shard* sh, int n, const dion2_config* c, int world, int rank) {
+  if (world < 1 || rank < 0 || rank >= world || n < 1 || !sh) return DION2_EINVAL_SHAPE;
+  if (c->precision != DION2_NS_BF16 || c->decay_mode != 0) return DION2_EUNSUPPORTED;
+  D.n = n;
+  D.world = world;
+  D.rank = rank;
+  D.dm.assign(n, DistMat{});
+  for (int j = 0; j < n; ++j) {
+    DistMat& q = D.dm[j];
+    q.m = sh[j].rows;
+    q.n = sh[j].cols;
+    if (q.m < 1 || q.n < 1) return DION2_EINVAL_SHAPE;
+    q.axis = c->axis == DION2_AXIS_AUTO ? (q.m <= q.n ? DION2_AXIS_ROWS : DION2_AXIS_COLS) : c->axis;
+    q.d = (int)(q.axis == DION2_AXIS_ROWS ? q.m : q.n);
+    q.o = (int)(q.axis == DION2_AXIS_ROWS ? q.n : q.m);
+    if (q.d > DION2_MAX_SELECT_DIM) return DION2_EINVAL_SHAPE;
+    int64_t k = (int64_t)std::floor((double)c->alpha * (double)q.d + 0.5);  // reading R7
+    q.k = (int)std::max<int64_t>(1, std::min<int64_t>(k, q.d));
+    if (q.k > q.o || q.o % world) return DION2_EUNSUPPORTED;
+    q.qo = q.o / world;
+    if (q.axis == DION2_AXIS_ROWS) {
+      if (q.qo % 8) return DION2_EUNSUPPORTED;
+      q.srows = q.m;
+      q.scols = q.qo;
+    } else {
+      if (q.qo % 8) return DION2_EUNSUPPORTED;
+      q.srows = q.qo;
+      q.scols = q.n;
+    }
+    if (sh[j].ld < q.scols) return DION2_EINVAL_SHAPE;
+    q.piece = (int64_t)align_up((size_t)q.k * q.qo * 2, 256);
+    const double p = q.k, qq = q.o;
+    q.flops = c->ns_steps * (4.0 * p * p * qq + 2.0 * p * p * p);
+    // gather/scatter path: streaming rows (1), streaming cols (2), generic tiles (0)
+    q.path = q.axis == DION2_AXIS_ROWS ? 1 : ((q.qo % 32 == 0 && q.k <= kMaxColKFast) ? 2 : 0);
+    q.ga = q.path == 0 ? (int)ceil_div(q.srows, kTileA) : 0;
+    q.gb = q.path == 0 ? (int)ceil_div(q.k, kTileB) : 0;
+    q.n_sumsq = q.path == 1 ? q.k : (q.path == 2 ? q.qo / 32 : q.ga * q.gb);
+  }
+  // owners: LPT on NS FLOPs (descending, ties -> lower index), least-loaded rank (ties -> lower rank)
+  std::vector<int> order(n);
+  std::iota(order.begin(), order.end(), 0);
+  std::stable_sort(order.begin(), order.end(), [&](int a, int b) { return D.dm[a].flops > D.dm[b].flops; });
+  std::vector<double> load(world, 0.0);
+  for (int j : order) {
+    int best = 0;
+    for (int r = 1; r < world; ++r)
+      if (load[r] < load[best]) best = r;
+    D.dm[j].owner = best;
+    load[best] += D.dm[j].flops;
+  }
+  // send sections (by owner) and my recv section size
+  D.sdispl.assign(world, 0);
+  D.scount.assign(world, 0);
+  int64_t run = 0;
+  for (int o = 0; o < world; ++o) {
+    D.sdispl[o] = run;
+    for (int j = 0; j < n; ++j)
+      if (D.dm[j].owner == o) {
+        D.dm[j].soff = run - D.sdispl[o];
+        run += D.dm[j].piece;
+      }
+    D.scount[o] = run - D.sdispl[o];
+  }
+  D.R = D.scount[rank];
+  D.owned.clear();
+  for (int j = 0; j < n; ++j)
+    if (D.dm[j].owner == rank) D.owned.push_back(j);
+  // workspace
+  size_t off = 0;
+  auto take = [&](size_t bytes) {
+    size_t o = off;
+    off = align_up(off + std::max<size_t>(bytes, 1), 256);
+    return o;
+  };
+  D.total_d = 0;
+  for (auto& q : D.dm) D.total_d += q.d;
+  D.off_status = take(16);
+  D.off_bad = take(4 * (size_t)n);
+  D.off_scores = take(4 * (size_t)D.total_d);
+  D.off_scores_all = take(4 * (size_t)D.total_d * world);
+  D.off_sumsq_local = take(4 * (size_t)n);
+  D.off_sumsq_all = take(4 * (size_t)n * world);
+  for (auto& q : D.dm) {
+    q.off_partials = q.axis == DION2_AXIS_COLS ? take(4 * (size_t)ceil_div(q.srows, 64) * q.scols) : 0;
+    q.off_sel = take(4 * (size_t)q.k);
+    q.off_sumsq = take(4 * (size_t)q.n_sumsq);
+  }
+  D.off_send = take((size_t)run);
+  D.off_orecv = take((size_t)run);
+  D.off_recv = take((size_t)D.R * world);
+  D.off_osend = take((size_t)D.R * world);
+  off = align_up(off, 4096);
+  D.off_owner = off;
+  // owner plan over the owned matrices' GLOBAL shapes (NS only)
+  size_t owner_bytes = 0;
+  if (!D.owned.empty()) {
+    std::vector<dion2_matrix> om(D.owned.size());
+    for (size_t i = 0; i < D.owned.size(); ++i) {
+      memset(&om[i], 0, sizeof(om[i]));
+      om[i].rows = D.dm[D.owned[i]].m;
+      om[i].cols = D.dm[D.owned[i]].n;
+      om[i].ld = D.dm[D.owned[i]].n;
+    }
+    D.owner = std::make_unique<Plan>();
+    int rc = build_layout(*D.owner, om.data(), (int)om.size(), c);
+    if (rc) return rc;
+    owner_bytes = D.owner->total;
+  }
+  D.total = D.off_owner + owner_bytes + 4096;
+  return DION2_OK;
+}
+
+// Device tables + owner plan for a concrete workspace.
+int build_tables(DistPlan& D, const dion2_config* c, void* ws) {
+  const int n = D.n, P = D.world;
+  size_t off = 0;
+  auto take = [&](size_t bytes) {
+    size_t o = off;
+    off = align_up(off + std::max<size_t>(bytes, 1), 256);
+    return o;
+  };
+  D.t_desc = take(sizeof(MatDesc) * n);
+  D.t_rowmats = take(4 * (size_t)n);
+  D.t_rowprefix = take(8 * (size_t)n);
+  D.t_colmats = take(4 * (size_t)n);
+  D.t_colprefix = take(8 * (size_t)n);
+  for (int l = 0; l < 2; ++l) {
+    D.t_flm[l] = take(4 * (size_t)n);
+    D.t_flg[l] = take(4 * (size_t)n);
+    D.t_fls[l] = take(4 * (size_t)n);
+  }
+  D.t_gprefix = take(4 * (size_t)n);
+  D.t_gidx = take(4 * std::max<size_t>(1, D.owned.size()));
+  D.t_roff = take(8 * std::max<size_t>(1, D.owned.size()) * P);
+  D.htab.assign(off, 0);
+  if (!D.dtab && cudaMalloc(&D.dtab, off) != cudaSuccess) return DION2_ECUDA;
+  auto H = [&](size_t o) { return D.htab.data() + o; };
+  MatDesc* md = reinterpret_cast<MatDesc*>(H(D.t_desc));
+  std::vector<int32_t> rowmats, colmats, flm[2], flg[2], fls[2];
+  std::vector<int64_t> rowprefix, colprefix;
+  std::vector<int32_t> gprefix(n, 0);
+  D.total_gather_tiles = 0;
+  D.total_rows = D.total_col_tiles = 0;
+  D.fl_gunits[0] = D.fl_gunits[1] = D.fl_sunits[0] = D.fl_sunits[1] = 0;
+  D.fl_maxk = D.max_d = 0;
+  D.max_cols_col = 0;
+  int64_t score_off = 0;
+  for (int j = 0; j < n; ++j) {
+    const DistMat& q = D.dm[j];
+    MatDesc& d = md[j];
+    memset(&d, 0, sizeof(d));
+    d.rows = q.srows;
+    d.cols = q.scols;
+    d.axis = q.axis;
+    d.d = q.d;
+    d.o = q.qo;
+    d.k = q.k;
+    d.sr = q.axis == DION2_AXIS_ROWS ? q.k : (int)q.srows;
+    d.sc = q.axis == DION2_AXIS_ROWS ? (int)q.scols : q.k;
+    d.transposed = q.axis == DION2_AXIS_COLS;  // the GLOBAL wide orientation (k <= o)
+    d.p = q.k;
+    d.q = q.qo;
+    d.p_pad = q.k;
+    d.q_pad = q.qo;
+    d.sa_pad = d.sr;
+    d.sb_pad = d.sc;
+    d.grad_bf16 = c->grad_dtype == DION2_DT_BF16;
+    d.update_scale = c->scale_mode == 0 ? (float)std::sqrt((double)q.m / (double)q.n)        // Alg. 1 l.6
+                                        : (float)std::sqrt(q.axis == DION2_AXIS_ROWS ? (double)q.k / q.n
+                                                                                     : (double)q.m / q.k);
+    d.scores = (float*)at(ws, D.off_scores) + score_off;
+    d.col_partials = q.axis == DION2_AXIS_COLS ? (float*)at(ws, q.off_partials) : nullptr;
+    d.sel = (int32_t*)at(ws, q.off_sel);
+    d.sumsq_partials = (float*)at(ws, q.off_sumsq);
+    d.X0 = at(ws, D.off_send + D.sdispl[q.owner] + q.soff);
+    d.X1 = at(ws, D.off_orecv + D.sdispl[q.owner] + q.soff);
+    d.final_in_x1 = 1;
+    d.rowblocks = (int)ceil_div(q.srows, 64);
+    d.path = q.path;
+    d.n_sumsq = q.n_sumsq;
+    d.scores_final = 1;
+    d.gather_tile_base = D.total_gather_tiles;
+    d.gather_tiles_a = q.ga;
+    d.gather_tiles_b = q.gb;
+    gprefix[j] = D.total_gather_tiles;
+    D.total_gather_tiles += q.ga * q.gb;
+    score_off += q.d;
+    D.max_d = std::max(D.max_d, q.d);
+    if (q.axis == DION2_AXIS_ROWS) {
+      rowmats.push_back(j);
+      rowprefix.push_back(D.total_rows);
+      D.total_rows += q.srows;
+    } else {
+      colmats.push_back(j);
+      colprefix.push_back(D.total_col_tiles);
+      D.total_col_tiles += (int64_t)d.rowblocks * ceil_div(q.scols, 256);
+      D.max_cols_col = std::max<int64_t>(D.max_cols_col, q.scols);
+    }
+    if (d.path == 0) continue;
+    const int l = d.path - 1;
+    flm[l].push_back(j);
+    flg[l].push_back(D.fl_gunits[l]);
+    fls[l].push_back(D.fl_sunits[l]);
+    D.fl_gunits[l] += l == 0 ? q.k : q.qo / 32;
+    D.fl_sunits[l] += l == 0 ? q.k : q.qo / 32;
+    if (l == 1) D.fl_maxk = std::max(D.fl_maxk, q.k);
+  }
+  memcpy(H(D.t_gprefix), gprefix.data(), 4 * (size_t)n);
+  D.n_row_mats = (int)rowmats.size();
+  D.n_col_mats = (int)colmats.size();
+  if (D.n_row_mats) {
+    memcpy(H(D.t_rowmats), rowmats.data(), 4 * rowmats.size());
+    memcpy(H(D.t_rowprefix), rowprefix.data(), 8 * rowprefix.size());
+  }
+  if (D.n_col_mats) {
+    memcpy(H(D.t_colmats), colmats.data(), 4 * colmats.size());
+    memcpy(H(D.t_colprefix), colprefix.data(), 8 * colprefix.size());
+  }
+  for (int l = 0; l < 2; ++l) {
+    D.fl_n[l] = (int)flm[l].size();
+    if (D.fl_n[l]) {
+      memcpy(H(D.t_flm[l]), flm[l].data(), 4 * flm[l].size());
+      memcpy(H(D.t_flg[l]), flg[l].data(), 4 * flg[l].size());
+      memcpy(H(D.t_fls[l]), fls[l].data(), 4 * fls[l].size());
+    }
+  }
+  // owner plan + piece table
+  D.max_p_pad = D.max_k_owned = 0;
+  if (!D.owned.empty()) {
+    std::vector<dion2_matrix> om(D.owned.size());
+    for (size_t i = 0; i < D.owned.size(); ++i) {
+      memset(&om[i], 0, sizeof(om[i]));
+      om[i].rows = D.dm[D.owned[i]].m;
+      om[i].cols = D.dm[D.owned[i]].n;
+      om[i].ld = D.dm[D.owned[i]].n;
+    }
+    int rc = build_device_plan(*D.owner, om.data(), c, at(ws, D.off_owner));
+    if (rc) return rc;
+    std::vector<int32_t> gidx(D.owned.size());
+    std::vector<int64_t> roff(D.owned.size() * P);
+    int64_t acc = 0;
+    for (size_t i = 0; i < D.owned.size(); ++i) {
+      const DistMat& q = D.dm[D.owned[i]];
+      gidx[i] = D.owned[i];
+      for (int r = 0; r < P; ++r) roff[i * P + r] = acc;
+      acc += q.piece;
+      D.max_p_pad = std::max(D.max_p_pad, D.owner->mp[i].p_pad);
+      D.max_k_owned = std::max(D.max_k_owned, q.k);
+      // the owner's NS runs on the global orientation: X = k x o (k <= o)
+      if (D.owner->mp[i].p != q.k || D.owner->mp[i].q != q.o) return DION2_EUNSUPPORTED;
+    }
+    memcpy(H(D.t_gidx), gidx.data(), 4 * gidx.size());
+    memcpy(H(D.t_roff), roff.data(), 8 * roff.size());
+    D.ptab.gidx = (const int32_t*)dt(D, D.t_gidx);
+    D.ptab.roff = (const int64_t*)dt(D, D.t_roff);
+    D.ptab.rstride = D.R;
+    D.ptab.world = P;
+  }
+  return DION2_OK;
+}
+
+std::map<std::string, std::unique_ptr<DistPlan>> g_dist_plans;
+
+std::string dist_key(const dion2_shard* sh, int n, const dion2_config* c, int world, int rank, void* ws) {
+  std::string k;
+  auto put = [&](const void* p, size_t s) { k.append(reinterpret_cast<const char*>(p), s); };
+  put(&n, 4);
+  put(&world, 4);
+  put(&rank, 4);
+  put(&ws, sizeof ws);
+  for (int i = 0; i < n; ++i) {
+    put(&sh[i].rows, 8);
+    put(&sh[i].cols, 8);
+    put(&sh[i].ld, 8);
+  }
+  put(&c->alpha, 4);
+  put(&c->ns_steps, 4);
+  put(c->ns_coeffs, sizeof(float) * 3 * c->ns_steps);
+  put(&c->axis, 4);
+  put(&c->precision, 4);
+  put(&c->grad_dtype, 4);
+  put(&c->decay_mode, 4);
+  put(&c->scale_mode, 4);
+  return k;
+}
+
+int get_plan(DistPlan** out, const dion2_shard* sh, int n, const dion2_config* c, int world, int rank, void* workspace,
+             size_t ws_bytes) {
+  void* ws = reinterpret_cast<void*>(align_up(reinterpret_cast<uintptr_t>(workspace), 4096));
+  const size_t slack = (uintptr_t)ws - (uintptr_t)workspace;
+  std::string key = dist_key(sh, n, c, world, rank, ws);
+  auto it = g_dist_plans.find(key);
+  if (it == g_dist_plans.end()) {
+    auto D = std::make_unique<DistPlan>();
+    int rc = resolve(*D, sh, n, c, world, rank);
+    if (rc) return rc;
+    if (D->total - 4096 + slack > ws_bytes) return DION2_EWORKSPACE;
+    rc = build_tables(*D, c, ws);
+    if (rc) return rc;
+    it = g_dist_plans.emplace(key, std::move(D)).first;
+  }
+  DistPlan& D = *it->second;
+  if (D.total - 4096 + slack > ws_bytes) return DION2_EWORKSPACE;
+  *out = &D;
+  return DION2_OK;
+}
+
+// refresh the caller's shard pointers in the device table (upload only when they change)
+int refresh(DistPlan& D, const dion2_shard* sh, const dion2_config* c, cudaStream_t s) {
+  bool up = !D.uploaded;
+  if ((int)D.last_ptrs.size() != 4 * D.n) {
+    D.last_ptrs.assign(4 * D.n, nullptr);
+    up = true;
+  }
+  MatDesc* md = reinterpret_cast<MatDesc*>(D.htab.data() + D.t_desc);
+  for (int j = 0; j < D.n; ++j) {
+    const void* p[4] = {sh[j].W, sh[j].M, sh[j].G, sh[j].sel_out};
+    for (int t = 0; t < 4; ++t)
+      if (D.last_ptrs[4 * j + t] != p[t]) { up = true; D.last_ptrs[4 * j + t] = p[t]; }
+    md[j].W = sh[j].W;
+    md[j].M = sh[j].M;
+    md[j].G = sh[j].G;
+    md[j].sel_out = sh[j].sel_out;
+    md[j].O_out = nullptr;
+    md[j].ld = sh[j].ld;
+    const size_t gel = c->grad_dtype == DION2_DT_BF16 ? 2 : 4;
+    md[j].vec4 = ((uintptr_t)sh[j].W % 16 == 0) && ((uintptr_t)sh[j].M % 16 == 0) &&
+                 ((uintptr_t)sh[j].G % (gel == 4 ? 16 : 8) == 0) && (sh[j].ld % 4 == 0);
+  }
+  if (up) {
+    if (cudaMemcpyAsync(D.dtab, D.htab.data(), D.htab.size(), cudaMemcpyHostToDevice, s) != cudaSuccess)
+      return DION2_ECUDA;
+    if (D.owner && cudaMemcpyAsync(D.owner->dtab, D.owner->host_tables.data(), D.owner->host_tables.size(),
+                                   cudaMemcpyHostToDevice, s) != cudaSuccess)
+      return DION2_ECUDA;
+    D.uploaded = true;
+  }
+  return DION2_OK;
+}
+
+// ------------------------------------------------------------------ phases (one rank)
+void phase_local_k1(DistPlan& D, void* ws, Launcher& L, cudaStream_t s) {
+  const int sms = g_sm_count > 0 ? g_sm_count : 148;
+  const MatDesc* dm = (const MatDesc*)dt(D, D.t_desc);
+  cudaMemsetAsync(at(ws, D.off_status), 0, 4, s);
+  cudaMemsetAsync(at(ws, D.off_status + 4), 0x7f, 4, s);
+  if (D.n_row_mats) {
+    L.begin(PH_K1);
+    const int64_t blocks = std::min<int64_t>(ceil_div(D.total_rows, 8), (int64_t)sms * 8);
+    k_momentum_score_rows<<<(unsigned)blocks, 256, 0, s>>>(dm, (const int32_t*)dt(D, D.t_rowmats),
+                                                           (const int64_t*)dt(D, D.t_rowprefix), D.n_row_mats,
+                                                           D.total_rows);
+    L.end();
+  }
+  if (D.n_col_mats) {
+    L.begin(PH_K1);
+    const int64_t blocks = std::min<int64_t>(D.total_col_tiles, (int64_t)sms * 8);
+    k_momentum_score_cols<<<(unsigned)blocks, 256, 0, s>>>(dm, (const int32_t*)dt(D, D.t_colmats),
+                                                           (const int64_t*)dt(D, D.t_colprefix), D.n_col_mats,
+                                                           D.total_col_tiles);
+    L.end();
+    L.begin(PH_K1);
+    launch_cols_local_scores(s, dm, (const int32_t*)dt(D, D.t_colmats), D.n_col_mats, D.max_cols_col);
+    L.end();
+  }
+}
+
+void phase_select(DistPlan& D, void* ws, Launcher& L, cudaStream_t s) {
+  const MatDesc* dm = (const MatDesc*)dt(D, D.t_desc);
+  L.begin(PH_SELECT);
+  launch_sum_rank_scores(s, (const float*)at(ws, D.off_scores_all), (float*)at(ws, D.off_scores), D.total_d, D.world);
+  L.end();
+  L.begin(PH_SELECT);
+  k_topk_select<<<D.n, kSelectThreads, 4 * D.max_d, s>>>(dm, (int32_t*)at(ws, D.off_bad),
+                                                         (int32_t*)at(ws, D.off_status));
+  L.end();
+}
+
+void phase_gather(DistPlan& D, void* ws, const dion2_config* c, Launcher& L, cudaStream_t s) {
+  const int sms = g_sm_count > 0 ? g_sm_count : 148;
+  const MatDesc* dm = (const MatDesc*)dt(D, D.t_desc);
+  const int32_t* bad = (const int32_t*)at(ws, D.off_bad);
+  if (D.total_gather_tiles) {
+    L.begin(PH_GATHER);
+    launch_gather_decay(true, std::min(D.total_gather_tiles, sms * 8), s, dm, (const int32_t*)dt(D, D.t_gprefix), D.n,
+                        D.total_gather_tiles, bad, 1, c->mu);
+    L.end();
+  }
+  if (D.fl_n[0]) {
+    L.begin(PH_GATHER_ROWS);
+    const int blocks = (int)std::min<int64_t>(ceil_div(D.fl_gunits[0], 8), (int64_t)sms * 8);
+    launch_gather_rows(blocks, s, dm, (const int32_t*)dt(D, D.t_flm[0]), (const int32_t*)dt(D, D.t_flg[0]), D.fl_n[0],
+                       D.fl_gunits[0], bad, c->mu);
+    L.end();
+  }
+  if (D.fl_n[1]) {
+    L.begin(PH_GATHER_COLS);
+    const int blocks = std::min(D.fl_gunits[1], sms * 4);
+    launch_gather_cols_t(blocks, D.fl_maxk, s, dm, (const int32_t*)dt(D, D.t_flm[1]),
+                         (const int32_t*)dt(D, D.t_flg[1]), D.fl_n[1], D.fl_gunits[1], bad, c->mu);
+    L.end();
+  }
+  L.begin(PH_NORM);
+  launch_piece_sumsq(s, dm, D.n, (float*)at(ws, D.off_sumsq_local));
+  L.end();
+}
+
+void phase_owner_ns(DistPlan& D, void* ws, const dion2_config* c, Launcher& L, cudaStream_t s) {
+  if (D.owned.empty()) return;
+  Plan& P = *D.owner;
+  const MatDesc* om = (const MatDesc*)tab(P, P.off_desc);
+  L.begin(PH_NORM);
+  launch_assemble(s, om, (int)D.owned.size(), D.max_p_pad, D.ptab, (const uint8_t*)at(ws, D.off_recv),
+                  (const float*)at(ws, D.off_sumsq_all), D.n, c->ns_eps);
+  L.end();
+  run_ns(P, c, L, s, false);
+  L.begin(PH_SCATTER);
+  launch_disassemble(s, om, (int)D.owned.size(), D.max_k_owned, D.ptab, (uint8_t*)at(ws, D.off_osend));
+  L.end();
+}
+
+void phase_scatter(DistPlan& D, void* ws, const dion2_config* c, Launcher& L, cudaStream_t s) {
+  const int sms = g_sm_count > 0 ? g_sm_count : 148;
+  const MatDesc* dm = (const MatDesc*)dt(D, D.t_desc);
+  const int32_t* bad = (const int32_t*)at(ws, D.off_bad);
+  if (D.total_gather_tiles) {
+    L.begin(PH_SCATTER);
+    launch_scatter_update(true, std::min(D.total_gather_tiles, sms * 8), s, dm, (const int32_t*)dt(D, D.t_gprefix),
+                          D.n, D.total_gather_tiles, bad, c->lr);
+    L.end();
+  }
+  if (D.fl_n[0]) {
+    L.begin(PH_SCATTER_ROWS);
+    const int blocks = (int)std::min<int64_t>(ceil_div(D.fl_sunits[0], 8), (int64_t)sms * 8);
+    launch_scatter_rows(blocks, s, dm, (const int32_t*)dt(D, D.t_flm[0]), (const int32_t*)dt(D, D.t_fls[0]), D.fl_n[0],
+                        D.fl_sunits[0], bad, c->lr);
+    L.end();
+  }
+  if (D.fl_n[1]) {
+    L.begin(PH_SCATTER_COLS);
+    const int blocks = std::min(D.fl_sunits[1], sms * 4);
+    launch_scatter_cols_t(blocks, D.fl_maxk, s, dm, (const int32_t*)dt(D, D.t_flm[1]),
+                          (const int32_t*)dt(D, D.t_fls[1]), D.fl_n[1], D.fl_sunits[1], bad, c->lr);
+    L.end();
+  }
+}
+
+// ------------------------------------------------------------------ exchanges
+struct Transport {
+  virtual ~Transport() = default;
+  virtual int allgather_scores() = 0;
+  virtual int allgather_sumsq() = 0;
+  virtual int to_owners() = 0;
+  virtual int from_owners() = 0;
+  uint64_t bytes = 0;
+};
+
+struct NcclTransport : Transport {
+  DistPlan& D;
+  void* ws;
+  ncclComm_t comm;
+  cudaStream_t s;
+  NcclTransport(DistPlan& d, void* w, void* cm, cudaStream_t st) : D(d), ws(w), comm(cm), s(st) {}
+  int allgather_scores() override {
+    bytes += (uint64_t)D.total_d * 4 * (D.world - 1);
+    return nccl_api().allgather(at(ws, D.off_scores), at(ws, D.off_scores_all), (size_t)D.total_d, kNcclFloat32, comm,
+                                s)
+               ? DION2_ENCCL
+               : DION2_OK;
+  }
+  int allgather_sumsq() override {
+    bytes += (uint64_t)D.n * 4 * (D.world - 1);
+    return nccl_api().allgather(at(ws, D.off_sumsq_local), at(ws, D.off_sumsq_all), (size_t)D.n, kNcclFloat32, comm, s)
+               ? DION2_ENCCL
+               : DION2_OK;
+  }
+  int exchange(bool forward) {
+    auto& api = nccl_api();
+    int rc = 0;
+    rc |= api.group_start();
+    for (int peer = 0; peer < D.world; ++peer) {
+      // forward: my send section for owner `peer` -> peer's recv section `rank`
+      //          and peer's send section for me -> my recv section `peer`
+      uint8_t* mine = (uint8_t*)at(ws, (forward ? D.off_send : D.off_orecv) + D.sdispl[peer]);
+      uint8_t* owner_side = (uint8_t*)at(ws, (forward ? D.off_recv : D.off_osend) + (size_t)peer * D.R);
+      const size_t nmine = (size_t)D.scount[peer], nown = (size_t)D.R;
+      if (forward) {
+        if (nmine) rc |= api.send(mine, nmine, kNcclChar, peer, comm, s);
+        if (nown) rc |= api.recv(owner_side, nown, kNcclChar, peer, comm, s);
+      } else {
+        if (nown) rc |= api.send(owner_side, nown, kNcclChar, peer, comm, s);
+        if (nmine) rc |= api.recv(mine, nmine, kNcclChar, peer, comm, s);
+      }
+      if (peer != D.rank) bytes += forward ? nmine : nown;
+    }
+    rc |= api.group_end();
+    return rc ? DION2_ENCCL : DION2_OK;
+  }
+  int to_owners() override { return exchange(true); }
+  int from_owners() override { return exchange(false); }
+};
+
+// all ranks in one process: every exchange is a set of device-to-device copies
+struct LoopbackTransport : Transport {
+  std::vector<DistPlan*> D;
+  std::vector<void*> ws;
+  cudaStream_t s;
+  LoopbackTransport(std::vector<DistPlan*> d, std::vector<void*> w, cudaStream_t st) : D(d), ws(w), s(st) {}
+  int cp(void* dst, const void* src, size_t n) {
+    if (!n) return DION2_OK;
+    return cudaMemcpyAsync(dst, src, n, cudaMemcpyDeviceToDevice, s) == cudaSuccess ? DION2_OK : DION2_ECUDA;
+  }
+  int allgather_scores() override {
+    const int P = (int)D.size();
+    int rc = 0;
+    for (int r = 0; r < P; ++r)
+      for (int r2 = 0; r2 < P; ++r2)
+        rc |= cp(at(ws[r], D[r]->off_scores_all + (size_t)r2 * D[r]->total_d * 4), at(ws[r2], D[r2]->off_scores),
+                 (size_t)D[r]->total_d * 4);
+    bytes += (uint64_t)D[0]->total_d * 4 * (P - 1);
+    return rc ? DION2_ECUDA : DION2_OK;
+  }
+  int allgather_sumsq() override {
+    const int P = (int)D.size();
+    int rc = 0;
+    for (int r = 0; r < P; ++r)
+      for (int r2 = 0; r2 < P; ++r2)
+        rc |= cp(at(ws[r], D[r]->off_sumsq_all + (size_t)r2 * D[r]->n * 4), at(ws[r2], D[r2]->off_sumsq_local),
+                 (size_t)D[r]->n * 4);
+    bytes += (uint64_t)D[0]->n * 4 * (P - 1);
+    return rc ? DION2_ECUDA : DION2_OK;
+  }
+  int to_owners() override {
+    const int P = (int)D.size();
+    int rc = 0;
+    for (int r = 0; r < P; ++r)
+      for (int o = 0; o < P; ++o) {
+        rc |= cp(at(ws[o], D[o]->off_recv + (size_t)r * D[o]->R), at(ws[r], D[r]->off_send + D[r]->sdispl[o]),
+                 (size_t)D[r]->scount[o]);
+        if (o != 0 && r == 0) bytes += (uint64_t)D[0]->scount[o];
+      }
+    return rc ? DION2_ECUDA : DION2_OK;
+  }
+  int from_owners() override {
+    const int P = (int)D.size();
+    int rc = 0;
+    for (int o = 0; o < P; ++o)
+      for (int r = 0; r < P; ++r) {
+        rc |= cp(at(ws[r], D[r]->off_orecv + D[r]->sdispl[o]), at(ws[o], D[o]->off_osend + (size_t)r * D[o]->R),
+                 (size_t)D[r]->scount[o]);
+        if (o == 0 && r != 0) bytes += (uint64_t)D[0]->R;
+      }
+    return rc ? DION2_ECUDA : DION2_OK;
+  }
+};
+
+int run_dist(std::vector<DistPlan*>& plans, std::vector<void*>& wss, const std::vector<const dion2_shard*>& shards,
+             const dion2_config* c, Transport& T, cudaStream_t s, uint64_t* bytes_out) {
+  Launcher L{s};
+  int rc = 0;
+  const size_t R = plans.size();
+  for (size_t i = 0; i < R; ++i)
+    if ((rc = refresh(*plans[i], shards[i], c, s))) return rc;
+  for (size_t i = 0; i < R; ++i) phase_local_k1(*plans[i], wss[i], L, s);
+  if ((rc = T.allgather_scores())) return rc;                       // C1
+  for (size_t i = 0; i < R; ++i) phase_select(*plans[i], wss[i], L, s);
+  for (size_t i = 0; i < R; ++i) phase_gather(*plans[i], wss[i], c, L, s);
+  if ((rc = T.allgather_sumsq())) return rc;
+  if ((rc = T.to_owners())) return rc;                              // C2
+  for (size_t i = 0; i < R; ++i) phase_owner_ns(*plans[i], wss[i], c, L, s);
+  if ((rc = T.from_owners())) return rc;                            // C3
+  for (size_t i = 0; i < R; ++i) phase_scatter(*plans[i], wss[i], c, L, s);
+  g_last_launches = L.count;
+  if (bytes_out) *bytes_out = T.bytes;
+  return L.err;
+}
+
+}  // namespace
+}  // namespace dion2rt
+
+using namespace dion2rt;
+
+extern "C" {
+
+int dion2_dist_info(const dion2_shard* shards, int32_t n, const dion2_config* cfg, int32_t world, int32_t rank,
+                    int32_t* axis_out, int32_t* owner_out, int64_t* shard_rows_out, int64_t* shard_cols_out,
+                    int64_t* send_bytes_out, int64_t* recv_bytes_out, size_t* ws_bytes_out) {
+  int rc = validate_config(cfg);
+  if (rc) return rc;
+  DistPlan D;
+  rc = resolve(D, shards, n, cfg, world, rank);
+  if (rc) return rc;
+  for (int j = 0; j < n; ++j) {
+    if (axis_out) axis_out[j] = D.dm[j].axis;
+    if (owner_out) owner_out[j] = D.dm[j].owner;
+    if (shard_rows_out) shard_rows_out[j] = D.dm[j].srows;
+    if (shard_cols_out) shard_cols_out[j] = D.dm[j].scols;
+  }
+  for (int r = 0; r < world; ++r) {
+    if (send_bytes_out) send_bytes_out[r] = D.scount[r];
+    if (recv_bytes_out) recv_bytes_out[r] = D.R;
+  }
+  if (ws_bytes_out) *ws_bytes_out = D.total;
+  return DION2_OK;
+}
+
+int dion2_step_batched_dist(const dion2_shard* shards, int32_t n, const dion2_config* cfg, void* workspace,
+                            size_t ws_bytes, void* nccl_comm, int32_t world, int32_t rank, void* stream,
+                            uint64_t* comm_bytes_out) {
+  int rc = validate_config(cfg);
+  if (rc) return rc;
+  if (!workspace) return DION2_EWORKSPACE;
+  for (int j = 0; j < n; ++j)
+    if (!shards[j].W || !shards[j].M || !shards[j].G) return DION2_EINVAL_SHAPE;
+  if (!nccl_comm) return DION2_ENCCL;
+  if (!nccl_api().ok) return DION2_ENCCL;
+  std::lock_guard<std::mutex> lock(g_mu);
+  ensure_device_attrs();
+  DistPlan* D = nullptr;
+  if ((rc = get_plan(&D, shards, n, cfg, world, rank, workspace, ws_bytes))) return rc;
+  void* ws = reinterpret_cast<void*>(align_up(reinterpret_cast<uintptr_t>(workspace), 4096));
+  cudaStream_t s = reinterpret_cast<cudaStream_t>(stream);
+  NcclTransport T(*D, ws, nccl_comm, s);
+  std::vector<DistPlan*> plans{D};
+  std::vector<void*> wss{ws};
+  std::vector<const dion2_shard*> sh{shards};
+  return run_dist(plans, wss, sh, cfg, T, s, comm_bytes_out);
+}
+
+int dion2_step_batched_loopback(const dion2_shard* shards, int32_t n, const dion2_config* cfg,
+                                void* const* workspaces, size_t ws_bytes, int32_t world, void* stream,
+                                uint64_t* comm_bytes_out) {
+  int rc = validate_config(cfg);
+  if (rc) return rc;
+  if (!workspaces || world < 1) return DION2_EWORKSPACE;
+  for (int j = 0; j < n * world; ++j)
+    if (!shards[j].W || !shards[j].M || !shards[j].G) return DION2_EINVAL_SHAPE;
+  std::lock_guard<std::mutex> lock(g_mu);
+  ensure_device_attrs();
+  std::vector<DistPlan*> plans(world);
+  std::vector<void*> wss(world);
+  std::vector<const dion2_shard*> sh(world);
+  for (int r = 0; r < world; ++r) {
+    if (!workspaces[r]) return DION2_EWORKSPACE;
+    if ((rc = get_plan(&plans[r], shards + (size_t)r * n, n, cfg, world, r, workspaces[r], ws_bytes))) return rc;
+    wss[r] = reinterpret_cast<void*>(align_up(reinterpret_cast<uintptr_t>(workspaces[r]), 4096));
+    sh[r] = shards + (size_t)r * n;
+  }
+  cudaStream_t s = reinterpret_cast<cudaStream_t>(stream);
+  LoopbackTransport T(plans, wss, s);
+  return run_dist(plans, wss, sh, cfg, T, s, comm_bytes_out);
+}
+
+}  // extern "C"

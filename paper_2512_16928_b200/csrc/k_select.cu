@@ -57,7 +57,7 @@ __global__ void __launch_bounds__(kSelectThreads) k_topk_select(const MatDesc* _
   int nonfinite = 0;
   for (int i = tid; i < d; i += blockDim.x) {
     float s;
-    if (md.axis == kAxisCols) {
+    if (md.axis == kAxisCols && !md.scores_final) {
       s = 0.f;
       for (int rb = 0; rb < md.rowblocks; ++rb) s += md.col_partials[(int64_t)rb * md.cols + i];
       md.scores[i] = s;

@@ -39,6 +39,22 @@ void launch_scatter_cols_t(int blocks, int max_k, cudaStream_t s, const MatDesc*
                            const int32_t* lp, int nl, int units, const int32_t* bad, float lr);
 __global__ void k_full_decay(const MatDesc* __restrict__ mats, int n_mats, const int32_t* __restrict__ bad, float mu);
 
+// ---------------- distributed step (k_dist.cu)
+struct PieceTable {
+  const int32_t* gidx;     // [n_owned] global matrix index
+  const int64_t* roff;     // [n_owned * world] byte offset of owned matrix jj's piece in rank r's section
+  int64_t rstride;         // bytes between consecutive ranks' sections
+  int32_t world;
+};
+void launch_cols_local_scores(cudaStream_t s, const MatDesc* mats, const int32_t* col_mats, int n_col_mats,
+                              int64_t max_cols);
+void launch_sum_rank_scores(cudaStream_t s, const float* gathered, float* out, int64_t total, int world);
+void launch_piece_sumsq(cudaStream_t s, const MatDesc* mats, int n, float* out);
+void launch_assemble(cudaStream_t s, const MatDesc* omats, int n_owned, int max_p_pad, const PieceTable& T,
+                     const uint8_t* recv, const float* sumsq_all, int n_total, float eps);
+void launch_disassemble(cudaStream_t s, const MatDesc* omats, int n_owned, int max_k, const PieceTable& T,
+                        uint8_t* send);
+
 // ---------------- K4-K6 Newton-Schulz GEMMs
 // D = oscale * (cacc * Aop . Bop + cC * C), written as OutT.
 //   Aop: [M x K] row-major (K-major); Bop(k, n) = B[n][k] (b_kmajor) or B[k][n].

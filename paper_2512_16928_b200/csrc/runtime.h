@@ -1,0 +1,136 @@
+// runtime.h -- host-runtime internals shared by the single-GPU C ABI (dion2_api.cu)
+// and the distributed step (dion2_dist.cu).  Not part of the public ABI.
+#pragma once
+#include <cudaTypedefs.h>
+
+#include <map>
+#include <memory>
+#include <mutex>
+#include <string>
+#include <vector>
+
+#include "../../include/dion2.h"
+#include "kernels.cuh"
+
+namespace dion2rt {
+using namespace dion2;
+
+constexpr int kNumPhases = 13;
+extern const char* kPhaseNames[kNumPhases];
+enum Phase {
+  PH_K1 = 0, PH_SELECT, PH_GATHER, PH_NORM, PH_GRAM, PH_POLY, PH_APPLY, PH_SCATTER, PH_FULLDECAY,
+  PH_GATHER_ROWS, PH_GATHER_COLS, PH_SCATTER_ROWS, PH_SCATTER_COLS
+};
+
+extern std::mutex g_mu;
+extern int g_sm_count;
+extern bool g_attr_done;
+extern int32_t g_last_launches;
+extern bool g_timing;
+struct TimedLaunch {
+  int phase;
+  cudaEvent_t a, b;
+};
+extern std::vector<TimedLaunch> g_timed;
+extern std::vector<cudaEvent_t> g_event_pool;
+cudaEvent_t take_event();
+
+inline size_t align_up(size_t x, size_t a) { return (x + a - 1) / a * a; }
+inline int64_t ceil_div(int64_t a, int64_t b) { return (a + b - 1) / b; }
+
+bool make_map(CUtensorMap* m, const void* base, int64_t cols, int64_t rows, int64_t count, int box_cols, int box_rows,
+              CUtensorMapSwizzle swz = CU_TENSOR_MAP_SWIZZLE_128B);
+int validate_config(const dion2_config* c);
+int validate_shape(const dion2_matrix& m, bool need_ptrs);
+
+struct MatPlan {
+  int axis, d, o, k, sr, sc, transposed, p, q, p_pad, q_pad, group, zi, rowblocks, ga, gb, sa_pad, sb_pad, path,
+      n_sumsq;
+  float fan_sqrt;
+  size_t off_scores, off_partials, off_sel, off_sumsq;
+};
+
+struct Group {
+  int p_pad, q_pad, count;
+  std::vector<int> mats;  // global matrix indices
+  size_t off_X0, off_X1, off_A, off_B, off_gmats;
+};
+
+struct Launch {
+  int phase;
+  int bn;
+  int kind;  // 0 = tc BN128, 1 = tc BN256, 2 = simt
+  NsTcParams tc;
+  int simt_group;
+};
+
+struct Plan {
+  int n;
+  bool bf16_ns;
+  int ns_steps;
+  std::vector<MatPlan> mp;
+  std::vector<Group> groups;
+  size_t off_status, off_bad, off_desc, off_rowmats, off_rowprefix, off_colmats, off_colprefix, off_gprefix,
+      off_nsscale, off_ns_begin, off_ns_end, total;
+  int64_t total_rows = 0, total_col_tiles = 0;
+  int n_row_mats = 0, n_col_mats = 0, total_gather_tiles = 0, max_d = 0;
+  // streaming fast paths: list 0 = rows (units: X rows p_pad / selected rows k),
+  // list 1 = cols with X = S^T (units: 32-row slabs of X's columns, q_pad / 32)
+  size_t off_fl_mats[2], off_fl_gprefix[2], off_fl_sprefix[2];
+  int fl_n[2] = {0, 0}, fl_gunits[2] = {0, 0}, fl_sunits[2] = {0, 0}, fl_maxk = 0;
+  std::vector<uint8_t> host_tables;  // [off_desc, off_ns_begin) image (descriptors + aux)
+  std::vector<Launch> ns_launches;
+  void* ws = nullptr;
+  uint64_t id = 0;
+  std::vector<const void*> last_ptrs;  // W, M, G, sel_out, O_out per matrix as last uploaded
+  void* dtab = nullptr;                // plan-owned device copy of host_tables
+};
+
+// device address of a table offset (tables are carved with workspace-style offsets
+// starting at off_desc but live in the plan-owned buffer)
+inline void* tab(Plan& P, size_t off) { return static_cast<uint8_t*>(P.dtab) + (off - P.off_desc); }
+
+inline void* at(void* ws, size_t off) { return static_cast<uint8_t*>(ws) + off; }
+
+struct Launcher {
+  cudaStream_t s;
+  int count = 0;
+  int err = DION2_OK;
+  int cur_phase = -1;
+  cudaEvent_t ev_a = nullptr;
+  void begin(int phase) {
+    cur_phase = phase;
+    if (g_timing) {
+      ev_a = take_event();
+      cudaEventRecord(ev_a, s);
+    }
+  }
+  void end() {
+    ++count;
+    if (cudaPeekAtLastError() != cudaSuccess) {
+      cudaGetLastError();
+      err = DION2_ECUDA;
+    }
+    static const bool debug_sync = getenv("DION2_DEBUG_SYNC") != nullptr;
+    if (debug_sync) {
+      cudaError_t e = cudaStreamSynchronize(s);
+      if (e != cudaSuccess) {
+        fprintf(stderr, "[dion2] launch %d (phase %s) failed: %s\n", count, kPhaseNames[cur_phase],
+                cudaGetErrorString(e));
+        err = DION2_ECUDA;
+      }
+    }
+    if (g_timing) {
+      cudaEvent_t b = take_event();
+      cudaEventRecord(b, s);
+      g_timed.push_back({cur_phase, ev_a, b});
+    }
+  }
+};
+
+int build_layout(Plan& P, const dion2_matrix* mats, int n, const dion2_config* c);
+int build_device_plan(Plan& P, const dion2_matrix* mats, const dion2_config* c, void* ws);
+void ensure_device_attrs();
+int run_ns(Plan& P, const dion2_config* c, Launcher& L, cudaStream_t s, bool do_norm);
+
+}  // namespace dion2rt

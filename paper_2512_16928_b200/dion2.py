@@ -23,7 +23,8 @@ STATUS = {0: "OK", 1: "EINVAL_CONFIG", 2: "EINVAL_SHAPE", 3: "EWORKSPACE", 4: "E
           5: "ECUDA", 6: "ENCCL", 7: "ENONFINITE"}
 EXPORTED = ["dion2_config_init", "dion2_workspace_size", "dion2_step", "dion2_step_batched", "dion2_get_status",
             "dion2_strerror", "dion2_set_phase_timing", "dion2_get_phase_times", "dion2_phase_name",
-            "dion2_last_launch_count", "dion2_abi_version"]
+            "dion2_last_launch_count", "dion2_abi_version", "dion2_dist_info", "dion2_step_batched_dist",
+            "dion2_step_batched_loopback"]
 
 
 class Dion2Matrix(ctypes.Structure):
@@ -38,6 +39,11 @@ class Dion2Config(ctypes.Structure):
                 ("ns_eps", ctypes.c_float), ("axis", ctypes.c_int32), ("select", ctypes.c_int32),
                 ("precision", ctypes.c_int32), ("grad_dtype", ctypes.c_int32), ("decay_mode", ctypes.c_int32),
                 ("scale_mode", ctypes.c_int32), ("seed", ctypes.c_uint64), ("step", ctypes.c_uint64)]
+
+
+class Dion2Shard(ctypes.Structure):
+    _fields_ = [("rows", ctypes.c_int64), ("cols", ctypes.c_int64), ("ld", ctypes.c_int64),
+                ("W", ctypes.c_void_p), ("M", ctypes.c_void_p), ("G", ctypes.c_void_p), ("sel_out", ctypes.c_void_p)]
 
 
 class Dion2Error(RuntimeError):
@@ -70,6 +76,15 @@ def _lib():
         lib.dion2_phase_name.restype = ctypes.c_char_p
         lib.dion2_last_launch_count.restype = ctypes.c_int32
         lib.dion2_abi_version.restype = ctypes.c_int32
+        I32, I64 = P(ctypes.c_int32), P(ctypes.c_int64)
+        lib.dion2_dist_info.argtypes = [P(Dion2Shard), ctypes.c_int32, P(Dion2Config), ctypes.c_int32, ctypes.c_int32,
+                                        I32, I32, I64, I64, I64, I64, P(ctypes.c_size_t)]
+        lib.dion2_step_batched_dist.argtypes = [P(Dion2Shard), ctypes.c_int32, P(Dion2Config), ctypes.c_void_p,
+                                                ctypes.c_size_t, ctypes.c_void_p, ctypes.c_int32, ctypes.c_int32,
+                                                ctypes.c_void_p, P(ctypes.c_uint64)]
+        lib.dion2_step_batched_loopback.argtypes = [P(Dion2Shard), ctypes.c_int32, P(Dion2Config),
+                                                    P(ctypes.c_void_p), ctypes.c_size_t, ctypes.c_int32,
+                                                    ctypes.c_void_p, P(ctypes.c_uint64)]
         _LIB = lib
     return _LIB
 
@@ -198,3 +213,138 @@ def get_phase_times() -> Dict[str, Tuple[float, int]]:
 
 def last_launch_count() -> int:
     return int(_lib().dion2_last_launch_count())
+
+
+# ----------------------------------------------------------------------------------- multi-GPU
+def _shards(shapes, Ws=None, Ms=None, Gs=None, sels=None):
+    n = len(shapes)
+    arr = (Dion2Shard * n)()
+    for i, (m, nn) in enumerate(shapes):
+        arr[i].rows, arr[i].cols = m, nn
+        if Ws is not None:
+            W = Ws[i]
+            _check_tensor(W, "W shard", torch.float32)
+            _check_tensor(Ms[i], "M shard", torch.float32, W)
+            _check_tensor(Gs[i], "G shard", Gs[0].dtype, W)
+            arr[i].ld = W.stride(0)
+            arr[i].W, arr[i].M, arr[i].G = W.data_ptr(), Ms[i].data_ptr(), Gs[i].data_ptr()
+            s = sels[i] if sels is not None else None
+            arr[i].sel_out = s.data_ptr() if s is not None else None
+        else:
+            arr[i].ld = 1 << 40
+    return arr
+
+
+def dist_info(shapes: Sequence[Tuple[int, int]], world: int, rank: int, **cfg_kw) -> dict:
+    """Host-only layout of the owner-compute step (dion2_dist_info): per matrix the
+    resolved axis, owner rank and local shard shape; per peer the bytes sent/received in
+    one exchange direction; this rank's workspace size."""
+    n = len(shapes)
+    arr = _shards(shapes)
+    cfg = make_config(**cfg_kw)
+    ax, own = (ctypes.c_int32 * n)(), (ctypes.c_int32 * n)()
+    sr, sc = (ctypes.c_int64 * n)(), (ctypes.c_int64 * n)()
+    sb, rb = (ctypes.c_int64 * world)(), (ctypes.c_int64 * world)()
+    ws = ctypes.c_size_t(0)
+    rc = _lib().dion2_dist_info(arr, n, ctypes.byref(cfg), world, rank, ax, own, sr, sc, sb, rb, ctypes.byref(ws))
+    if rc:
+        raise Dion2Error(rc, "dion2_dist_info")
+    return {"axis": list(ax), "owner": list(own), "shard": list(zip(sr, sc)), "send_bytes": list(sb),
+            "recv_bytes": list(rb), "workspace_bytes": ws.value}
+
+
+def shard_of(full: torch.Tensor, axis: int, world: int, rank: int) -> torch.Tensor:
+    """This rank's shard of a full matrix in the distributed layout: rows mode (axis 0)
+    -> column block, cols mode (axis 1) -> row block (contiguous copy)."""
+    m, n = full.shape
+    if axis == 0:
+        b = n // world
+        return full[:, rank * b:(rank + 1) * b].contiguous()
+    b = m // world
+    return full[rank * b:(rank + 1) * b].contiguous()
+
+
+def _nccl_comm_ptr(group) -> int:
+    import torch.distributed as dist
+    pg = group if group is not None else dist.group.WORLD
+    backend = pg._get_backend(torch.device("cuda"))
+    return int(backend._comm_ptr())
+
+
+class Dion2Dist:
+    """Owner-compute distributed Dion2 over a torch.distributed NCCL group (one rank per GPU).
+
+    shapes: the GLOBAL (m, n) of every matrix; each rank passes its local shards
+    (see dist_info()["shard"] and shard_of())."""
+
+    def __init__(self, shapes, group=None, **cfg_kw):
+        import torch.distributed as dist
+        self.shapes = [tuple(s) for s in shapes]
+        self.group = group
+        self.world = dist.get_world_size(group)
+        self.rank = dist.get_rank(group)
+        self.cfg_kw = dict(cfg_kw)
+        self.info = dist_info(self.shapes, self.world, self.rank, **cfg_kw)
+        self._ws: Optional[torch.Tensor] = None
+        self.last_comm_bytes = 0
+
+    def step(self, Ws, Ms, Gs, sel_out=None, stream=None):
+        kw = dict(self.cfg_kw)
+        kw.setdefault("grad_dtype", Gs[0].dtype)
+        cfg = make_config(**kw)
+        dev = Ws[0].device
+        need = self.info["workspace_bytes"]
+        if self._ws is None or self._ws.numel() < need:
+            self._ws = torch.empty(need, dtype=torch.uint8, device=dev)
+        arr = _shards(self.shapes, Ws, Ms, Gs, sel_out)
+        st = stream if stream is not None else torch.cuda.current_stream(dev)
+        nbytes = ctypes.c_uint64(0)
+        rc = _lib().dion2_step_batched_dist(arr, len(self.shapes), ctypes.byref(cfg), self._ws.data_ptr(),
+                                            self._ws.numel(), _nccl_comm_ptr(self.group), self.world, self.rank,
+                                            st.cuda_stream, ctypes.byref(nbytes))
+        if rc:
+            raise Dion2Error(rc, "dion2_step_batched_dist")
+        self.last_comm_bytes = nbytes.value
+
+    def status(self):
+        bad = ctypes.c_int32(-1)
+        rc = _lib().dion2_get_status(self._ws.data_ptr(), ctypes.byref(bad))
+        return rc, bad.value
+
+
+class Dion2Loopback:
+    """All `world` ranks of the distributed step in this process on ONE device; the
+    exchanges are device copies (dion2_step_batched_loopback).  For testing the
+    distributed layout and kernels without several GPUs."""
+
+    def __init__(self, shapes, world, **cfg_kw):
+        self.shapes = [tuple(s) for s in shapes]
+        self.world = world
+        self.cfg_kw = dict(cfg_kw)
+        self.infos = [dist_info(self.shapes, world, r, **cfg_kw) for r in range(world)]
+        self._ws: List[torch.Tensor] = []
+        self.last_comm_bytes = 0
+
+    def step(self, Ws, Ms, Gs, sel_out=None, stream=None):
+        """Ws, Ms, Gs: [world][n] local shards; sel_out: optional [world][n] int32 tensors."""
+        kw = dict(self.cfg_kw)
+        kw.setdefault("grad_dtype", Gs[0][0].dtype)
+        cfg = make_config(**kw)
+        n, P = len(self.shapes), self.world
+        dev = Ws[0][0].device
+        need = max(i["workspace_bytes"] for i in self.infos)
+        if len(self._ws) != P or self._ws[0].numel() < need:
+            self._ws = [torch.empty(need, dtype=torch.uint8, device=dev) for _ in range(P)]
+        arr = (Dion2Shard * (n * P))()
+        for r in range(P):
+            part = _shards(self.shapes, Ws[r], Ms[r], Gs[r], sel_out[r] if sel_out is not None else None)
+            for i in range(n):
+                arr[r * n + i] = part[i]
+        wsp = (ctypes.c_void_p * P)(*[w.data_ptr() for w in self._ws])
+        st = stream if stream is not None else torch.cuda.current_stream(dev)
+        nbytes = ctypes.c_uint64(0)
+        rc = _lib().dion2_step_batched_loopback(arr, n, ctypes.byref(cfg), wsp, need, P, st.cuda_stream,
+                                                ctypes.byref(nbytes))
+        if rc:
+            raise Dion2Error(rc, "dion2_step_batched_loopback")
+        self.last_comm_bytes = nbytes.value

@@ -110,6 +110,11 @@ def run_parity(shapes: Sequence[Tuple[int, int]], alpha: float, axis: str = "aut
                     else:
                         res.unselected_w_bitwise &= bool(np.array_equal(wb[:, unsel], wa[:, unsel]))
                         res.unselected_m_bitwise &= bool(np.array_equal(expect_m[:, unsel], ma[:, unsel]))
+    _finish(res, shapes, Wg, Mg, Wr, Mr, W0)
+    return res
+
+
+def _finish(res, shapes, Wg, Mg, Wr, Mr, W0):
     for i in range(len(shapes)):
         wg = Wg[i].cpu().numpy().astype(np.float64)
         dref = Wr[i] - W0[i].astype(np.float64)
@@ -118,4 +123,75 @@ def run_parity(shapes: Sequence[Tuple[int, int]], alpha: float, axis: str = "aut
         res.W_rel.append(float(np.linalg.norm(wg - Wr[i]) / np.linalg.norm(Wr[i])))
         mg = Mg[i].cpu().numpy().astype(np.float64)
         res.M_rel.append(float(np.abs(mg - Mr[i]).max() / max(np.abs(Mr[i]).max(), 1e-300)))
+    return res
+
+
+def run_parity_dist(shapes, alpha, world, steps=3, seed=0, mode="loopback", axis="auto", mu=0.95, lr=0.02,
+                    row_scaled=True, device="cuda"):
+    """Distributed step (owner-compute, shards along the non-selection axis) against the
+    fp64 oracle on the FULL matrices.  mode = "loopback" (all ranks in this process) or
+    "nccl" (world must equal the initialised torch.distributed world; this process is
+    one rank and holds only its shards; the full matrices are re-assembled with
+    all_gather for the comparison)."""
+    from paper_2512_16928_b200 import dion2 as D
+    res = ParityResult()
+    cfg_o = oracle_cfg(alpha, axis, mu, lr)
+    info = D.dist_info(shapes, world, 0, alpha=alpha, axis=axis, mu=mu, lr=lr)
+    axes = info["axis"]
+    W0 = [gen_w0(m, n, seed, i) for i, (m, n) in enumerate(shapes)]
+    Wr = [w.astype(np.float64) for w in W0]
+    Mr = [np.zeros((m, n)) for (m, n) in shapes]
+    ks = []
+    for (m, n) in shapes:
+        ax = O.resolve_axis(m, n, cfg_o.axis)
+        ks.append(O.select_count(cfg_o.alpha, m if ax == O.AXIS_ROWS else n))
+    if mode == "loopback":
+        ranks = list(range(world))
+        opt = D.Dion2Loopback(shapes, world, alpha=alpha, axis=axis, mu=mu, lr=lr)
+    else:
+        import torch.distributed as dist
+        ranks = [dist.get_rank()]
+        opt = D.Dion2Dist(shapes, alpha=alpha, axis=axis, mu=mu, lr=lr)
+    full = lambda a, i: torch.from_numpy(a)  # noqa: E731
+    Wg = {r: [D.shard_of(full(W0[i], i), axes[i], world, r).to(device) for i in range(len(shapes))] for r in ranks}
+    Mg = {r: [torch.zeros_like(w) for w in Wg[r]] for r in ranks}
+
+    def assemble(parts_by_rank, i):
+        if mode == "loopback":
+            blocks = [parts_by_rank[r][i] for r in range(world)]
+        else:
+            import torch.distributed as dist
+            blocks = [torch.empty_like(parts_by_rank[ranks[0]][i]) for _ in range(world)]
+            dist.all_gather(blocks, parts_by_rank[ranks[0]][i].contiguous())
+        return torch.cat(blocks, dim=1 if axes[i] == 0 else 0)
+
+    for t in range(steps):
+        G = [gen_grad(m, n, seed, i, t, row_scaled=row_scaled) for i, (m, n) in enumerate(shapes)]
+        Gg = {r: [D.shard_of(full(G[i], i), axes[i], world, r).to(device) for i in range(len(shapes))] for r in ranks}
+        sel = {r: [torch.empty(k, dtype=torch.int32, device=device) for k in ks] for r in ranks}
+        if mode == "loopback":
+            opt.step([Wg[r] for r in ranks], [Mg[r] for r in ranks], [Gg[r] for r in ranks],
+                     sel_out=[sel[r] for r in ranks])
+        else:
+            opt.step(Wg[ranks[0]], Mg[ranks[0]], Gg[ranks[0]], sel_out=sel[ranks[0]])
+        torch.cuda.synchronize()
+        for i in range(len(shapes)):
+            Kg = sel[ranks[0]][i].cpu().numpy().astype(np.int64)
+            for r in ranks[1:]:  # every rank selects the same set
+                if not np.array_equal(sel[r][i].cpu().numpy(), Kg):
+                    res.index_mismatch += 1
+            g64 = G[i].astype(np.float64)
+            Wsave, Msave = Wr[i].copy(), Mr[i].copy()
+            K, _, ax = O.dion2_step(Wr[i], Mr[i], g64, cfg_o)
+            if not np.array_equal(K, Kg):
+                if _tie_equivalent(Kg, K, O.l1_scores(Msave + g64, ax)):
+                    res.ties += 1
+                    Wr[i], Mr[i] = Wsave, Msave
+                    O.dion2_step(Wr[i], Mr[i], g64, cfg_o, force_K=Kg)
+                else:
+                    res.index_mismatch += 1
+    Wfull = [assemble(Wg, i) for i in range(len(shapes))]
+    Mfull = [assemble(Mg, i) for i in range(len(shapes))]
+    _finish(res, shapes, Wfull, Mfull, Wr, Mr, W0)
+    res.comm_bytes = opt.last_comm_bytes
     return res

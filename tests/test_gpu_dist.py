@@ -1,0 +1,65 @@
+"""GPU tests of the owner-compute distributed step (-m gpu).
+
+One GPU is available: the multi-rank layout is exercised in loopback mode (all P
+ranks in one process on one device, exchanges as device copies: the same kernels,
+the same tables, the same piece offsets as the NCCL path), and the NCCL transport
+itself with a single-rank NCCL process group (self send/recv and all-gather).
+"""
+import os
+import socket
+
+import numpy as np
+import pytest
+import torch
+
+from synth import layer_set_1b
+
+from gpu_harness import run_parity_dist
+
+pytestmark = pytest.mark.gpu
+
+BF16_TOL = 2e-2
+
+
+def _assert(res, tol=BF16_TOL):
+    assert res.index_mismatch == 0, res
+    assert max(res.dW_rel) <= tol, res
+    assert max(res.M_rel) <= 1e-5, res
+
+
+SHAPES = [(256, 512), (512, 256), (1024, 1024), (2048, 512), (512, 2048)]
+
+
+@pytest.mark.parametrize("world", [1, 2, 4])
+def test_loopback_parity(world):
+    _assert(run_parity_dist(SHAPES, 0.25, world, steps=3))
+
+
+@pytest.mark.parametrize("world", [2, 8])
+def test_loopback_one_layer_of_the_1b_set(world):
+    _assert(run_parity_dist(layer_set_1b(1), 0.25, world, steps=2))
+
+
+def test_loopback_alpha1_is_full_muon():
+    _assert(run_parity_dist([(256, 512), (512, 256)], 1.0, 2, steps=2))
+
+
+def _free_port():
+    s = socket.socket()
+    s.bind(("127.0.0.1", 0))
+    p = s.getsockname()[1]
+    s.close()
+    return p
+
+
+def test_nccl_transport_single_rank():
+    import torch.distributed as dist
+    os.environ.setdefault("MASTER_ADDR", "127.0.0.1")
+    os.environ["MASTER_PORT"] = str(_free_port())
+    torch.cuda.set_device(0)
+    dist.init_process_group("nccl", rank=0, world_size=1, device_id=torch.device("cuda", 0))
+    try:
+        res = run_parity_dist(SHAPES, 0.25, 1, steps=3, mode="nccl")
+        _assert(res)
+    finally:
+        dist.destroy_process_group()
