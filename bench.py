@@ -141,8 +141,8 @@ class ClockSampler:
 
 # ---------------------------------------------------------------------------------- our arm
 
-def build_state(shapes, device, seed=0):
-    """Flat fp32 W / M / G buffers with one row-major view per matrix."""
+def build_state(shapes, device, seed=0, fan_in=None):
+    """Flat fp32 W / M / G buffers with one row-major view per matrix (W0 ~ N(0, 1/fan-in))."""
     import torch
     total = sum(m * n for m, n in shapes)
     gen = torch.Generator(device=device)
@@ -153,8 +153,8 @@ def build_state(shapes, device, seed=0):
     W.normal_(0.0, 1.0, generator=gen)
     G.normal_(0.0, 1.0, generator=gen)
     Ws, Ms, Gs, off = [], [], [], 0
-    for (m, n) in shapes:
-        Ws.append(W[off:off + m * n].view(m, n).mul_(1.0 / math.sqrt(n)))
+    for i, (m, n) in enumerate(shapes):
+        Ws.append(W[off:off + m * n].view(m, n).mul_(1.0 / math.sqrt(fan_in[i] if fan_in else n)))
         Ms.append(M[off:off + m * n].view(m, n))
         Gs.append(G[off:off + m * n].view(m, n))
         off += m * n
@@ -208,18 +208,20 @@ def cpu_oracle_baseline(shapes, alpha, budget_s=20.0):
                       f"fp64 NumPy; scaled x{layers / done:.1f} to the whole model"}
 
 
-def e2e_run(opt, Ws, Ms, Gs, G_flat, steps):
+def select_counts(shapes, alpha):
+    ks = []
+    for (m, n) in shapes:
+        d = m if m <= n else n
+        ks.append(max(1, min(d, int(math.floor(float(np.float32(alpha)) * d + 0.5)))))
+    return ks
+
+
+def e2e_run(opt, Ws, Ms, Gs, G_flat, steps, ks):
     """End to end through the public API: pinned host G -> device, the step, and the
     selected index sets + status word read back, every step, inside the timed region."""
     import torch
-    from paper_2512_16928_b200 import dion2 as D
     host_G = torch.empty(G_flat.numel(), dtype=torch.float32, pin_memory=True)
     host_G.copy_(G_flat.cpu())
-    ks = []
-    for W in Ws:
-        m, n = W.shape
-        d = m if m <= n else n
-        ks.append(max(1, min(d, int(math.floor(float(np.float32(opt.cfg_kw.get("alpha", 0.25))) * d + 0.5)))))
     sel_dev = torch.empty(sum(ks), dtype=torch.int32, device=G_flat.device)
     sel_views, off = [], 0
     for k in ks:
@@ -244,20 +246,31 @@ def run_ours(args):
     import torch
     import torch.distributed as dist
     from paper_2512_16928_b200 import Dion2, get_phase_times, last_launch_count, set_phase_timing
+    from paper_2512_16928_b200 import dion2 as D
 
     world = int(os.environ.get("WORLD_SIZE", "1"))
     rank = int(os.environ.get("RANK", "0"))
     local = int(os.environ.get("LOCAL_RANK", "0"))
-    if world > 1:
-        dist.init_process_group("nccl")
+    # DION2_BENCH_DIST=1 runs the owner-compute path even at N = 1 (single-rank NCCL group)
+    use_dist = world > 1 or os.environ.get("DION2_BENCH_DIST") == "1"
     torch.cuda.set_device(local)
+    if use_dist:
+        dist.init_process_group("nccl", device_id=torch.device("cuda", local))
     dev = torch.device("cuda", local)
     barrier = (lambda: dist.barrier()) if world > 1 else None
 
     shapes = model_shapes(args.config, args.layers)
     n_params = sum(m * n for m, n in shapes)
-    bufs, Ws, Ms, Gs = build_state(shapes, dev, seed=rank)
-    opt = Dion2(alpha=args.alpha, axis="auto", precision="bf16")
+    if use_dist:
+        # owner-compute over all ranks: every matrix sharded along its non-selection axis
+        info = D.dist_info(shapes, world, rank, alpha=args.alpha)
+        bufs, Ws, Ms, Gs = build_state(info["shard"], dev, seed=rank, fan_in=[n for (_, n) in shapes])
+        make_opt = lambda a: D.Dion2Dist(shapes, alpha=a, axis="auto", precision="bf16")  # noqa: E731
+    else:
+        info = None
+        bufs, Ws, Ms, Gs = build_state(shapes, dev, seed=rank)
+        make_opt = lambda a: Dion2(alpha=a, axis="auto", precision="bf16")  # noqa: E731
+    opt = make_opt(args.alpha)
 
     with ClockSampler(local) as clk:
         ms = time_steps(opt, Ws, Ms, Gs, args.steps, args.warmup, barrier)
@@ -274,6 +287,10 @@ def run_ours(args):
 
     peaks, peak_src = load_peaks()
     ns_flops, byts = work_model(shapes, args.alpha)
+    if use_dist:  # this rank's share: 1/world of every streaming pass, NS of its owned matrices
+        owned = [s for s, o in zip(shapes, info["owner"]) if o == rank]
+        ns_flops = work_model(owned, args.alpha)[0] if owned else {k: 0.0 for k in ns_flops}
+        byts = {k: v / world for k, v in byts.items()}
     per_phase = {}
     for name, (t_ms, cnt) in phases.items():
         if cnt == 0:
@@ -315,17 +332,24 @@ def run_ours(args):
     if not args.no_alpha1 and args.alpha != 1.0:
         del opt
         torch.cuda.empty_cache()
-        opt1 = Dion2(alpha=1.0, axis="auto", precision="bf16")
+        opt1 = make_opt(1.0)
         ms_a1 = time_steps(opt1, Ws, Ms, Gs, max(2, min(args.steps, 5)), max(1, min(args.warmup, 2)), barrier)
         del opt1
         torch.cuda.empty_cache()
-        opt = Dion2(alpha=args.alpha, axis="auto", precision="bf16")
+        opt = make_opt(args.alpha)
         opt.step(Ws, Ms, Gs)
 
     # end to end through the public API (host G)
     e2e_ms, h2d, d2h = None, None, None
     if not args.no_e2e:
-        e2e_ms, h2d, d2h, _ = e2e_run(opt, Ws, Ms, Gs, bufs[2], max(2, min(args.steps, 5)))
+        e2e_ms, h2d, d2h, _ = e2e_run(opt, Ws, Ms, Gs, bufs[2], max(2, min(args.steps, 5)),
+                                      select_counts(shapes, args.alpha))
+    comm = None
+    if use_dist:
+        opt.step(Ws, Ms, Gs)
+        comm = {"sent_bytes_per_step_rank": opt.last_comm_bytes,
+                "analytic_piece_bytes_per_step_rank": 2 * sum(info["send_bytes"][o] for o in range(world) if o != rank),
+                "note": "gather-to-owner + scatter-back of k x (o/P) bf16 pieces, plus the score all-gather"}
 
     # max over ranks
     if world > 1:
@@ -340,21 +364,22 @@ def run_ours(args):
     if rank == 0:
         out = {
             "metric": "Dion2 optimizer-step ms per model at alpha=0.25 vs alpha=1; NS tensor-peak fraction",
-            "value": ms if world == 1 else ms / world,
+            "value": ms,
             "unit": "ms/step",
             "n_gpus": world,
             "steps": args.steps,
             "warmup": args.warmup,
             "ms_per_step": ms,
             "higher_is_better": False,
-            "scaling": "weak",
+            "scaling": "weak" if world == 1 else "strong",
             "vs_baseline": None,
             "dtype": "f32 state / bf16 NS",
             "data": "synthetic (W0~N(0,1/n), G~N(0,1), M0=0; seeded device RNG)",
             "config": {"workload": f"{args.config}-set Dion2 step (configs[1])", "matrices": len(shapes),
                        "params": n_params, "alpha": args.alpha, "axis": "auto", "ns_steps": 5,
                        "l2_flush": "not needed: 14.5 GB touched per step >> 126 MB L2",
-                       "parallelism": "single GPU" if world == 1 else f"{world} independent replicas"},
+                       "parallelism": "single GPU" if not use_dist else
+                       f"owner-compute over {world} GPUs (NCCL; shards along the non-selection axis)"},
             "alpha1_ms_per_step": ms_a1,
             "speedup_vs_alpha1": (ms_a1 / ms) if ms_a1 else None,
             "ns_tflops": ns_tflops,
@@ -367,10 +392,11 @@ def run_ours(args):
             "e2e": {"value": e2e_ms, "unit": "ms/step", "h2d_bytes_per_step": h2d, "d2h_bytes_per_step": d2h,
                     "what": "pinned host G -> device, dion2_step_batched, selected indices -> host, every step"},
             "gpu_launches": launches,
+            "comm": comm,
             "clocks": clk.summary(),
         }
         print(json.dumps(out))
-    if world > 1:
+    if use_dist:
         dist.destroy_process_group()
 
 

@@ -246,6 +246,7 @@ int build_device_plan(Plan& P, const dion2_matrix* mats, const dion2_config* c, 
   std::vector<int32_t> fl_mats[2], fl_gp[2], fl_sp[2];
   P.fl_gunits[0] = P.fl_gunits[1] = P.fl_sunits[0] = P.fl_sunits[1] = 0;
   P.fl_maxk = 0;
+  P.fl_maxn = 0;
   int64_t rows_acc = 0, ctiles_acc = 0;
   int gt_acc = 0;
   for (int i = 0; i < n; ++i) {
@@ -288,7 +289,10 @@ int build_device_plan(Plan& P, const dion2_matrix* mats, const dion2_config* c, 
       fl_sp[l].push_back(P.fl_sunits[l]);
       P.fl_gunits[l] += gu;
       P.fl_sunits[l] += su;
-      if (l == 1) P.fl_maxk = std::max(P.fl_maxk, q.k);
+      if (l == 1) {
+        P.fl_maxk = std::max(P.fl_maxk, q.k);
+        P.fl_maxn = std::max<int64_t>(P.fl_maxn, mats[i].cols);
+      }
     }
     if (q.axis == DION2_AXIS_ROWS) {
       rowmats.push_back(i);
@@ -550,8 +554,8 @@ int run_step(Plan& P, const dion2_matrix* mats, const dion2_config* c, void* ws,
     }
     if (P.fl_n[1]) {
       L.begin(PH_GATHER_COLS);
-      const int blocks = std::min(P.fl_gunits[1], sms * 4);
-      launch_gather_cols_t(blocks, P.fl_maxk, s, dmats, (const int32_t*)tab(P, P.off_fl_mats[1]),
+      const int blocks = std::min(P.fl_gunits[1], sms * 6);
+      launch_gather_cols_t(blocks, P.fl_maxk, P.fl_maxn, s, dmats, (const int32_t*)tab(P, P.off_fl_mats[1]),
                            (const int32_t*)tab(P, P.off_fl_gprefix[1]), P.fl_n[1], P.fl_gunits[1], bad, c->mu);
       L.end();
     }
@@ -576,8 +580,8 @@ int run_step(Plan& P, const dion2_matrix* mats, const dion2_config* c, void* ws,
     }
     if (P.fl_n[1]) {
       L.begin(PH_SCATTER_COLS);
-      const int blocks = std::min(P.fl_sunits[1], sms * 4);
-      launch_scatter_cols_t(blocks, P.fl_maxk, s, dmats, (const int32_t*)tab(P, P.off_fl_mats[1]),
+      const int blocks = std::min(P.fl_sunits[1], sms * 6);
+      launch_scatter_cols_t(blocks, P.fl_maxk, P.fl_maxn, s, dmats, (const int32_t*)tab(P, P.off_fl_mats[1]),
                             (const int32_t*)tab(P, P.off_fl_sprefix[1]), P.fl_n[1], P.fl_sunits[1], bad, c->lr);
       L.end();
     }

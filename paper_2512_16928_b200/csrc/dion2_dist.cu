@@ -497,7 +497,7 @@ void phase_gather(DistPlan& D, void* ws, const dion2_config* c, Launcher& L, cud
   if (D.fl_n[1]) {
     L.begin(PH_GATHER_COLS);
     const int blocks = std::min(D.fl_gunits[1], sms * 4);
-    launch_gather_cols_t(blocks, D.fl_maxk, s, dm, (const int32_t*)dt(D, D.t_flm[1]),
+    launch_gather_cols_t(blocks, D.fl_maxk, D.max_cols_col, s, dm, (const int32_t*)dt(D, D.t_flm[1]),
                          (const int32_t*)dt(D, D.t_flg[1]), D.fl_n[1], D.fl_gunits[1], bad, c->mu);
     L.end();
   }
@@ -540,7 +540,7 @@ void phase_scatter(DistPlan& D, void* ws, const dion2_config* c, Launcher& L, cu
   if (D.fl_n[1]) {
     L.begin(PH_SCATTER_COLS);
     const int blocks = std::min(D.fl_sunits[1], sms * 4);
-    launch_scatter_cols_t(blocks, D.fl_maxk, s, dm, (const int32_t*)dt(D, D.t_flm[1]),
+    launch_scatter_cols_t(blocks, D.fl_maxk, D.max_cols_col, s, dm, (const int32_t*)dt(D, D.t_flm[1]),
                           (const int32_t*)dt(D, D.t_fls[1]), D.fl_n[1], D.fl_sunits[1], bad, c->lr);
     L.end();
   }

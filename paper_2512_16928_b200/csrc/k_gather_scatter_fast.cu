@@ -223,11 +223,12 @@ constexpr int kMaskWords = DION2_MAX_SELECT_DIM_WORDS;
 __global__ void __launch_bounds__(256) k_gather_cols_t(const MatDesc* __restrict__ mats,
                                                        const int32_t* __restrict__ list_mats,
                                                        const int32_t* __restrict__ list_prefix, int n_list,
-                                                       int total_units, const int32_t* __restrict__ bad, float mu) {
+                                                       int total_units, const int32_t* __restrict__ bad, float mu,
+                                                       int mask_words) {
   extern __shared__ __align__(16) uint8_t sm[];
   uint32_t* mask = reinterpret_cast<uint32_t*>(sm);
-  int32_t* rank = reinterpret_cast<int32_t*>(sm + 4 * kMaskWords);
-  __nv_bfloat16* tile = reinterpret_cast<__nv_bfloat16*>(sm + 8 * kMaskWords);  // [kSlab][ldt]
+  int32_t* rank = reinterpret_cast<int32_t*>(sm + 4 * mask_words);
+  __nv_bfloat16* tile = reinterpret_cast<__nv_bfloat16*>(sm + 8 * mask_words);  // [kSlab][ldt]
   __shared__ float wsum[8];
   int cur_mat = -1;
   const int lane = threadIdx.x & 31, wid = threadIdx.x >> 5;
@@ -258,22 +259,32 @@ __global__ void __launch_bounds__(256) k_gather_cols_t(const MatDesc* __restrict
       if (md.vec4) {
         float4* m4 = reinterpret_cast<float4*>(mrow);
         const int n4 = n >> 2;
-        for (int j = lane; j < n4; j += 32) {
-          const int c = 4 * j;
-          const uint32_t bits = (mask[c >> 5] >> (c & 31)) & 0xFu;
-          if (bits == 0u) continue;
-          float4 v = m4[j];
-          int rk = col_rank(mask, rank, c);
-          float e[4] = {v.x, v.y, v.z, v.w};
+        // 4 float4 loads in flight per lane (only float4s holding a selected column)
+        for (int j0 = lane; j0 < n4; j0 += 128) {
+          float4 v[4];
+          uint32_t bits[4];
 #pragma unroll
-          for (int q = 0; q < 4; ++q) {
-            if (bits & (1u << q)) {
-              trow[rk++] = __float2bfloat16_rn(e[q]);
-              ss += e[q] * e[q];
-              e[q] *= f;
-            }
+          for (int u = 0; u < 4; ++u) {
+            const int j = j0 + 32 * u, c = 4 * j;
+            bits[u] = j < n4 ? (mask[c >> 5] >> (c & 31)) & 0xFu : 0u;
+            if (bits[u]) v[u] = m4[j];
           }
-          m4[j] = make_float4(e[0], e[1], e[2], e[3]);
+#pragma unroll
+          for (int u = 0; u < 4; ++u) {
+            if (!bits[u]) continue;
+            const int j = j0 + 32 * u, c = 4 * j;
+            int rk = col_rank(mask, rank, c);
+            float e[4] = {v[u].x, v[u].y, v[u].z, v[u].w};
+#pragma unroll
+            for (int q = 0; q < 4; ++q) {
+              if (bits[u] & (1u << q)) {
+                trow[rk++] = __float2bfloat16_rn(e[q]);
+                ss += e[q] * e[q];
+                e[q] *= f;
+              }
+            }
+            m4[j] = make_float4(e[0], e[1], e[2], e[3]);
+          }
         }
         for (int c = 4 * n4 + lane; c < n; c += 32) {
           if (!((mask[c >> 5] >> (c & 31)) & 1u)) continue;
@@ -320,11 +331,12 @@ __global__ void __launch_bounds__(256) k_gather_cols_t(const MatDesc* __restrict
 __global__ void __launch_bounds__(256) k_scatter_cols_t(const MatDesc* __restrict__ mats,
                                                         const int32_t* __restrict__ list_mats,
                                                         const int32_t* __restrict__ list_prefix, int n_list,
-                                                        int total_units, const int32_t* __restrict__ bad, float lr) {
+                                                        int total_units, const int32_t* __restrict__ bad, float lr,
+                                                        int mask_words) {
   extern __shared__ __align__(16) uint8_t sm[];
   uint32_t* mask = reinterpret_cast<uint32_t*>(sm);
-  int32_t* rank = reinterpret_cast<int32_t*>(sm + 4 * kMaskWords);
-  __nv_bfloat16* tile = reinterpret_cast<__nv_bfloat16*>(sm + 8 * kMaskWords);  // [kSlab][ldt]
+  int32_t* rank = reinterpret_cast<int32_t*>(sm + 4 * mask_words);
+  __nv_bfloat16* tile = reinterpret_cast<__nv_bfloat16*>(sm + 8 * mask_words);  // [kSlab][ldt]
   int cur_mat = -1;
   const int lane = threadIdx.x & 31, wid = threadIdx.x >> 5;
   for (int u = blockIdx.x; u < total_units; u += gridDim.x) {
@@ -361,23 +373,32 @@ __global__ void __launch_bounds__(256) k_scatter_cols_t(const MatDesc* __restric
       if (md.vec4) {
         float4* w4 = reinterpret_cast<float4*>(wrow);
         const int n4 = n >> 2;
-        for (int j = lane; j < n4; j += 32) {
-          const int c = 4 * j;
-          const uint32_t bits = (mask[c >> 5] >> (c & 31)) & 0xFu;
-          if (bits == 0u) continue;
-          float4 w = w4[j];
-          int rk = col_rank(mask, rank, c);
-          float e[4] = {w.x, w.y, w.z, w.w};
+        for (int j0 = lane; j0 < n4; j0 += 128) {
+          float4 w[4];
+          uint32_t bits[4];
 #pragma unroll
-          for (int q = 0; q < 4; ++q) {
-            if (bits & (1u << q)) {
-              const float o = __bfloat162float(trow[rk]);
-              e[q] -= sc * o;
-              if (orow) orow[rk] = o;
-              ++rk;
-            }
+          for (int u = 0; u < 4; ++u) {
+            const int j = j0 + 32 * u, c = 4 * j;
+            bits[u] = j < n4 ? (mask[c >> 5] >> (c & 31)) & 0xFu : 0u;
+            if (bits[u]) w[u] = w4[j];
           }
-          w4[j] = make_float4(e[0], e[1], e[2], e[3]);
+#pragma unroll
+          for (int u = 0; u < 4; ++u) {
+            if (!bits[u]) continue;
+            const int j = j0 + 32 * u, c = 4 * j;
+            int rk = col_rank(mask, rank, c);
+            float e[4] = {w[u].x, w[u].y, w[u].z, w[u].w};
+#pragma unroll
+            for (int q = 0; q < 4; ++q) {
+              if (bits[u] & (1u << q)) {
+                const float o = __bfloat162float(trow[rk]);
+                e[q] -= sc * o;
+                if (orow) orow[rk] = o;
+                ++rk;
+              }
+            }
+            w4[j] = make_float4(e[0], e[1], e[2], e[3]);
+          }
         }
         for (int c = 4 * n4 + lane; c < n; c += 32) {
           if (!((mask[c >> 5] >> (c & 31)) & 1u)) continue;
@@ -400,10 +421,12 @@ __global__ void __launch_bounds__(256) k_scatter_cols_t(const MatDesc* __restric
   }
 }
 
-size_t cols_t_smem_bytes(int k) { return 8 * (size_t)kMaskWords + (size_t)kSlab * (k + 8) * 2; }
+// smem: column bitmask + popcount prefix (mask_words each) + the [kSlab][k + 8] bf16 tile
+size_t cols_t_smem_bytes(int k, int mask_words) { return 8 * (size_t)mask_words + (size_t)kSlab * (k + 8) * 2; }
+static int mask_words_for(int64_t max_n) { return (int)((((max_n + 31) / 32) + 3) / 4 * 4); }
 
 void launch_fast_paths_attrs() {
-  const int mx = (int)cols_t_smem_bytes(kMaxColK);
+  const int mx = (int)cols_t_smem_bytes(kMaxColK, kMaskWords);
   cudaFuncSetAttribute(k_gather_cols_t, cudaFuncAttributeMaxDynamicSharedMemorySize, mx);
   cudaFuncSetAttribute(k_scatter_cols_t, cudaFuncAttributeMaxDynamicSharedMemorySize, mx);
 }
@@ -416,13 +439,15 @@ void launch_scatter_rows(int blocks, cudaStream_t s, const MatDesc* mats, const 
                          int units, const int32_t* bad, float lr) {
   k_scatter_rows<<<blocks, 256, 0, s>>>(mats, lm, lp, nl, units, bad, lr);
 }
-void launch_gather_cols_t(int blocks, int max_k, cudaStream_t s, const MatDesc* mats, const int32_t* lm,
+void launch_gather_cols_t(int blocks, int max_k, int64_t max_n, cudaStream_t s, const MatDesc* mats, const int32_t* lm,
                           const int32_t* lp, int nl, int units, const int32_t* bad, float mu) {
-  k_gather_cols_t<<<blocks, 256, cols_t_smem_bytes(max_k), s>>>(mats, lm, lp, nl, units, bad, mu);
+  const int mw = mask_words_for(max_n);
+  k_gather_cols_t<<<blocks, 256, cols_t_smem_bytes(max_k, mw), s>>>(mats, lm, lp, nl, units, bad, mu, mw);
 }
-void launch_scatter_cols_t(int blocks, int max_k, cudaStream_t s, const MatDesc* mats, const int32_t* lm,
-                           const int32_t* lp, int nl, int units, const int32_t* bad, float lr) {
-  k_scatter_cols_t<<<blocks, 256, cols_t_smem_bytes(max_k), s>>>(mats, lm, lp, nl, units, bad, lr);
+void launch_scatter_cols_t(int blocks, int max_k, int64_t max_n, cudaStream_t s, const MatDesc* mats,
+                           const int32_t* lm, const int32_t* lp, int nl, int units, const int32_t* bad, float lr) {
+  const int mw = mask_words_for(max_n);
+  k_scatter_cols_t<<<blocks, 256, cols_t_smem_bytes(max_k, mw), s>>>(mats, lm, lp, nl, units, bad, lr, mw);
 }
 
 }  // namespace dion2

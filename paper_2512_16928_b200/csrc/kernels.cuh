@@ -27,16 +27,17 @@ __global__ void k_norm_finalize(const MatDesc* __restrict__ mats, int n_mats, fl
 // streaming fast paths (k_gather_scatter_fast.cu): rows mode X = S, cols mode X = S^T
 #define DION2_MAX_SELECT_DIM_WORDS 1536  // DION2_MAX_SELECT_DIM / 32
 constexpr int kMaxColKFast = 1024;          // largest k of the cols streaming path (smem tile)
-size_t cols_t_smem_bytes(int k);
+size_t cols_t_smem_bytes(int k, int mask_words);
 void launch_fast_paths_attrs();
 void launch_gather_rows(int blocks, cudaStream_t s, const MatDesc* mats, const int32_t* lm, const int32_t* lp, int nl,
                         int units, const int32_t* bad, float mu);
 void launch_scatter_rows(int blocks, cudaStream_t s, const MatDesc* mats, const int32_t* lm, const int32_t* lp, int nl,
                          int units, const int32_t* bad, float lr);
-void launch_gather_cols_t(int blocks, int max_k, cudaStream_t s, const MatDesc* mats, const int32_t* lm,
+// max_k / max_n: largest k and column count over the matrices of the list (sizes the smem)
+void launch_gather_cols_t(int blocks, int max_k, int64_t max_n, cudaStream_t s, const MatDesc* mats, const int32_t* lm,
                           const int32_t* lp, int nl, int units, const int32_t* bad, float mu);
-void launch_scatter_cols_t(int blocks, int max_k, cudaStream_t s, const MatDesc* mats, const int32_t* lm,
-                           const int32_t* lp, int nl, int units, const int32_t* bad, float lr);
+void launch_scatter_cols_t(int blocks, int max_k, int64_t max_n, cudaStream_t s, const MatDesc* mats,
+                           const int32_t* lm, const int32_t* lp, int nl, int units, const int32_t* bad, float lr);
 __global__ void k_full_decay(const MatDesc* __restrict__ mats, int n_mats, const int32_t* __restrict__ bad, float mu);
 
 // ---------------- distributed step (k_dist.cu)

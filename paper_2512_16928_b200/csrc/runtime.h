@@ -78,6 +78,7 @@ struct Plan {
   // list 1 = cols with X = S^T (units: 32-row slabs of X's columns, q_pad / 32)
   size_t off_fl_mats[2], off_fl_gprefix[2], off_fl_sprefix[2];
   int fl_n[2] = {0, 0}, fl_gunits[2] = {0, 0}, fl_sunits[2] = {0, 0}, fl_maxk = 0;
+  int64_t fl_maxn = 0;
   std::vector<uint8_t> host_tables;  // [off_desc, off_ns_begin) image (descriptors + aux)
   std::vector<Launch> ns_launches;
   void* ws = nullptr;
