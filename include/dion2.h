@@ -85,13 +85,15 @@ typedef struct {
   float ns_coeffs[DION2_MAX_NS_STEPS][3]; /* (a, b, c) per iteration, default (3.4445, -4.7750, 2.0315) (reading R1) */
   float ns_eps;       /* X0 = X / (||X||_F + eps), default 1e-7 (reading R3) */
   int32_t axis;       /* dion2_axis, default AUTO (shorter dimension) */
-  int32_t select;     /* dion2_select, default L1 (only L1 is implemented; RANDOM -> EUNSUPPORTED) */
+  int32_t select;     /* dion2_select, default L1 (largest l1 norm).  RANDOM: the k indices
+                         with the smallest keys Philox4x32-10(ctr = (index, step_lo, step_hi, matrix id in
+                         the batch), key = (seed_lo, seed_hi)) word 0, lower index on ties (reading R22) */
   int32_t precision;  /* dion2_precision: BF16 = tcgen05 tensor-core NS (hot path); FP32 = SIMT fp32 NS (validation) */
   int32_t grad_dtype; /* dion2_dtype of G, default F32 */
   int32_t decay_mode; /* 0 = selective decay Eq. (error-feedback) (paper); 1 = full decay M <- mu*M (ablation) */
   int32_t scale_mode; /* 0 = eta*sqrt(rows/cols) of the full W (Alg. 1 l.6); 1 = sqrt of the submatrix dims (SPEC S:360 flag) */
-  uint64_t seed;      /* random selection keying (unused for L1) */
-  uint64_t step;      /* random selection keying (unused for L1) */
+  uint64_t seed;      /* random selection key (unused for L1) */
+  uint64_t step;      /* random selection counter: the caller's step index (unused for L1) */
 } dion2_config;
 
 /* Fill *cfg with the defaults above.  Always returns DION2_OK. */

@@ -56,6 +56,9 @@ class OracleConfig:
     ns_eps: float = DEFAULT_NS_EPS
     decay_mode: int = 0
     scale_mode: int = 0
+    select: str = "l1"      # "l1" (Default) or "random"
+    seed: int = 0           # random selection keying (reading R22)
+    step: int = 0
 
 
 def select_count(alpha: float, d: int) -> int:
@@ -96,6 +99,47 @@ def select_l1(scores: np.ndarray, k: int) -> np.ndarray:
     return np.sort(order[:k]).astype(np.int64)
 
 
+_PHILOX_M0, _PHILOX_M1 = 0xD2511F53, 0xCD9E8D57
+_PHILOX_W0, _PHILOX_W1 = 0x9E3779B9, 0xBB67AE85
+_U32 = 0xFFFFFFFF
+
+
+def philox4x32_10(ctr, key):
+    """Philox-4x32 with 10 rounds (Salmon et al., SC'11, "Parallel random numbers: as easy as
+    1, 2, 3"), element-wise over uint64 arrays holding 32-bit lanes.  ctr: 4 arrays, key: 2."""
+    c0, c1, c2, c3 = (np.asarray(x, dtype=np.uint64) & _U32 for x in ctr)
+    k0, k1 = (np.asarray(x, dtype=np.uint64) & _U32 for x in key)
+    for r in range(10):
+        if r:
+            k0 = (k0 + _PHILOX_W0) & _U32
+            k1 = (k1 + _PHILOX_W1) & _U32
+        p0 = c0 * np.uint64(_PHILOX_M0)   # exact: both factors < 2^32
+        p1 = c2 * np.uint64(_PHILOX_M1)
+        hi0, lo0 = p0 >> np.uint64(32), p0 & _U32
+        hi1, lo1 = p1 >> np.uint64(32), p1 & _U32
+        c0, c1, c2, c3 = hi1 ^ c1 ^ k0, lo1, hi0 ^ c3 ^ k1, lo0
+    return c0, c1, c2, c3
+
+
+def random_keys(d: int, seed: int, matrix_id: int, step: int) -> np.ndarray:
+    """One 32-bit key per index i of the selection axis: word 0 of
+    Philox4x32-10(counter = (i, step_lo, step_hi, matrix_id), key = (seed_lo, seed_hi))
+    (reading R22; keyed by (seed, matrix, step) like SPEC S:232)."""
+    i = np.arange(d, dtype=np.uint64)
+    z = np.zeros(d, dtype=np.uint64)
+    out = philox4x32_10((i, z + (step & _U32), z + ((step >> 32) & _U32), z + (matrix_id & _U32)),
+                        (z + (seed & _U32), z + ((seed >> 32) & _U32)))
+    return out[0]
+
+
+def select_random(d: int, k: int, seed: int, matrix_id: int, step: int) -> np.ndarray:
+    """Random Select_alpha ("selecting uniformly at random"): the k indices
+    with the smallest keys, lowest index on (probability ~2^-32) ties; ascending."""
+    keys = random_keys(d, seed, matrix_id, step)
+    order = np.lexsort((np.arange(d), keys))
+    return np.sort(order[:k]).astype(np.int64)
+
+
 def newton_schulz(X: np.ndarray, coeffs=DEFAULT_NS_COEFFS, eps: float = DEFAULT_NS_EPS) -> np.ndarray:
     """Quintic Newton-Schulz on a wide (rows <= cols) matrix.
 
@@ -121,7 +165,7 @@ def newton_schulz_auto(X: np.ndarray, coeffs=DEFAULT_NS_COEFFS, eps: float = DEF
 
 
 def dion2_step(W: np.ndarray, M: np.ndarray, G: np.ndarray, cfg: OracleConfig,
-               force_K: Optional[np.ndarray] = None):
+               force_K: Optional[np.ndarray] = None, matrix_id: int = 0):
     """One step of Alg. 1 ("alpha-Dion2(G, M)") on one matrix.
 
     W, M: float64 [m x n], updated in place.  G: float64 [m x n].
@@ -138,7 +182,12 @@ def dion2_step(W: np.ndarray, M: np.ndarray, G: np.ndarray, cfg: OracleConfig,
     s = l1_scores(M, axis)
     d = s.shape[0]
     k = select_count(cfg.alpha, d)
-    K = select_l1(s, k) if force_K is None else np.asarray(force_K, dtype=np.int64)
+    if force_K is not None:
+        K = np.asarray(force_K, dtype=np.int64)
+    elif cfg.select == "random":
+        K = select_random(d, k, cfg.seed, matrix_id, cfg.step)
+    else:
+        K = select_l1(s, k)
     # l.4  O <- NewtonSchulz(M[K, :])   (pre-decay: l.4 precedes l.5)
     X = M[K, :] if axis == AXIS_ROWS else M[:, K]
     O = newton_schulz_auto(X, cfg.ns_coeffs, cfg.ns_eps)

@@ -46,6 +46,7 @@ struct MatDesc {
   int32_t path;            // gather/scatter path: 0 generic tiles, 1 rows streaming, 2 cols streaming (X = S^T)
   int32_t n_sumsq;         // number of sum-of-squares partials K3 writes
   int32_t scores_final;    // select reads `scores` as final (distributed step: combined across ranks)
+  int32_t mid;             // matrix id in the batch (random-selection key)
   int32_t rowblocks;      // ceil(rows/64) (cols mode partials)
 };
 
@@ -61,6 +62,27 @@ __device__ __forceinline__ float bf16_to_f(__nv_bfloat16 x) { return __bfloat162
 
 __device__ __forceinline__ uint32_t smem_u32(const void* p) {
   return static_cast<uint32_t>(__cvta_generic_to_shared(p));
+}
+
+// Philox-4x32-10 (Salmon et al., SC'11), word 0 of the output block: the key of
+// index i for random selection (counter = (i, step_lo, step_hi, matrix), key = seed).
+__device__ __forceinline__ uint32_t philox_word0(uint32_t c0, uint32_t c1, uint32_t c2, uint32_t c3, uint32_t k0,
+                                                 uint32_t k1) {
+#pragma unroll
+  for (int r = 0; r < 10; ++r) {
+    if (r) {
+      k0 += 0x9E3779B9u;
+      k1 += 0xBB67AE85u;
+    }
+    const uint32_t hi0 = __umulhi(0xD2511F53u, c0), lo0 = 0xD2511F53u * c0;
+    const uint32_t hi1 = __umulhi(0xCD9E8D57u, c2), lo1 = 0xCD9E8D57u * c2;
+    const uint32_t n0 = hi1 ^ c1 ^ k0, n2 = hi0 ^ c3 ^ k1;
+    c0 = n0;
+    c1 = lo1;
+    c2 = n2;
+    c3 = lo0;
+  }
+  return c0;
 }
 
 __device__ __forceinline__ void set_status_bad(int32_t* status, int mat) {

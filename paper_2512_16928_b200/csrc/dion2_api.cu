@@ -92,7 +92,6 @@ int validate_config(const dion2_config* c) {
   if (c->grad_dtype != DION2_DT_F32 && c->grad_dtype != DION2_DT_BF16) return DION2_EINVAL_CONFIG;
   if (c->decay_mode < 0 || c->decay_mode > 1) return DION2_EINVAL_CONFIG;
   if (c->scale_mode < 0 || c->scale_mode > 1) return DION2_EINVAL_CONFIG;
-  if (c->select == DION2_SELECT_RANDOM) return DION2_EUNSUPPORTED;
   return DION2_OK;
 }
 
@@ -276,6 +275,7 @@ int build_device_plan(Plan& P, const dion2_matrix* mats, const dion2_config* c, 
     d.sa_pad = q.sa_pad;
     d.sb_pad = q.sb_pad;
     d.rowblocks = q.rowblocks;
+    d.mid = i;
     d.path = q.path;
     d.n_sumsq = q.n_sumsq;
     gprefix[i] = gt_acc;
@@ -533,7 +533,8 @@ int run_step(Plan& P, const dion2_matrix* mats, const dion2_config* c, void* ws,
   }
   // K2 select (Alg. 1 l.3)
   L.begin(PH_SELECT);
-  k_topk_select<<<n, kSelectThreads, 4 * P.max_d, s>>>(dmats, bad, status);
+  k_topk_select<<<n, kSelectThreads, 4 * P.max_d, s>>>(dmats, bad, status, c->select == DION2_SELECT_RANDOM,
+                                                       c->seed, c->step);
   L.end();
   // K3 gather + decay (Alg. 1 l.4-5)
   {

@@ -277,6 +277,7 @@ int build_tables(DistPlan& D, const dion2_config* c, void* ws) {
     d.X1 = at(ws, D.off_orecv + D.sdispl[q.owner] + q.soff);
     d.final_in_x1 = 1;
     d.rowblocks = (int)ceil_div(q.srows, 64);
+    d.mid = j;
     d.path = q.path;
     d.n_sumsq = q.n_sumsq;
     d.scores_final = 1;
@@ -466,14 +467,15 @@ void phase_local_k1(DistPlan& D, void* ws, Launcher& L, cudaStream_t s) {
   }
 }
 
-void phase_select(DistPlan& D, void* ws, Launcher& L, cudaStream_t s) {
+void phase_select(DistPlan& D, void* ws, const dion2_config* c, Launcher& L, cudaStream_t s) {
   const MatDesc* dm = (const MatDesc*)dt(D, D.t_desc);
   L.begin(PH_SELECT);
   launch_sum_rank_scores(s, (const float*)at(ws, D.off_scores_all), (float*)at(ws, D.off_scores), D.total_d, D.world);
   L.end();
   L.begin(PH_SELECT);
   k_topk_select<<<D.n, kSelectThreads, 4 * D.max_d, s>>>(dm, (int32_t*)at(ws, D.off_bad),
-                                                         (int32_t*)at(ws, D.off_status));
+                                                         (int32_t*)at(ws, D.off_status),
+                                                         c->select == DION2_SELECT_RANDOM, c->seed, c->step);
   L.end();
 }
 
@@ -664,7 +666,7 @@ int run_dist(std::vector<DistPlan*>& plans, std::vector<void*>& wss, const std::
     if ((rc = refresh(*plans[i], shards[i], c, s))) return rc;
   for (size_t i = 0; i < R; ++i) phase_local_k1(*plans[i], wss[i], L, s);
   if ((rc = T.allgather_scores())) return rc;                       // C1
-  for (size_t i = 0; i < R; ++i) phase_select(*plans[i], wss[i], L, s);
+  for (size_t i = 0; i < R; ++i) phase_select(*plans[i], wss[i], c, L, s);
   for (size_t i = 0; i < R; ++i) phase_gather(*plans[i], wss[i], c, L, s);
   if ((rc = T.allgather_sumsq())) return rc;
   if ((rc = T.to_owners())) return rc;                              // C2

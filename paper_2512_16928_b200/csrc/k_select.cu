@@ -42,7 +42,8 @@ __device__ __forceinline__ int block_exclusive_scan(int v, int* warp_tot, int* t
 
 __global__ void __launch_bounds__(kSelectThreads) k_topk_select(const MatDesc* __restrict__ mats,
                                                                 int32_t* __restrict__ bad,
-                                                                int32_t* __restrict__ status) {
+                                                                int32_t* __restrict__ status, int random_sel,
+                                                                uint64_t seed, uint64_t step) {
   extern __shared__ uint32_t keys[];  // [d]
   __shared__ uint32_t hist[256];
   __shared__ int warp_tot[33];
@@ -65,7 +66,11 @@ __global__ void __launch_bounds__(kSelectThreads) k_topk_select(const MatDesc* _
       s = md.scores[i];
     }
     if (!(s <= 3.402823466e38f)) nonfinite = 1;  // NaN or +Inf
-    keys[i] = __float_as_uint(s);
+    // Random rule: the k SMALLEST Philox keys = the k largest complemented keys;
+    // ties (p ~ 2^-32) go to the lower index exactly as for the l1 rule.
+    keys[i] = random_sel ? ~philox_word0((uint32_t)i, (uint32_t)step, (uint32_t)(step >> 32), (uint32_t)md.mid,
+                                         (uint32_t)seed, (uint32_t)(seed >> 32))
+                         : __float_as_uint(s);
   }
   nonfinite = __syncthreads_or(nonfinite);
   if (nonfinite) {

@@ -12,7 +12,9 @@ __global__ void k_momentum_score_cols(const MatDesc* __restrict__ mats, const in
 
 // ---------------- K2 top-k select (k_select.cu)
 constexpr int kSelectThreads = 1024;
-__global__ void k_topk_select(const MatDesc* __restrict__ mats, int32_t* __restrict__ bad, int32_t* __restrict__ status);
+// random_sel = 1: Random rule with Philox keys (seed, step, md.mid); else the l1 rule
+__global__ void k_topk_select(const MatDesc* __restrict__ mats, int32_t* __restrict__ bad, int32_t* __restrict__ status,
+                              int random_sel, uint64_t seed, uint64_t step);
 
 // ---------------- K3 gather + decay + sum of squares, norm finalize; K7 scatter (k_gather_scatter.cu)
 constexpr int kTileA = 32;   // S rows per gather/scatter tile

@@ -19,6 +19,7 @@ LIB_PATH = os.path.join(_PKG, "lib", "libdion2.so")
 MAX_NS_STEPS = 16
 AXIS = {"rows": 0, "cols": 1, "auto": 2}
 PRECISION = {"bf16": 0, "fp32": 1}
+SELECT = {"l1": 0, "random": 1}
 STATUS = {0: "OK", 1: "EINVAL_CONFIG", 2: "EINVAL_SHAPE", 3: "EWORKSPACE", 4: "EUNSUPPORTED",
           5: "ECUDA", 6: "ENCCL", 7: "ENONFINITE"}
 EXPORTED = ["dion2_config_init", "dion2_workspace_size", "dion2_step", "dion2_step_batched", "dion2_get_status",
@@ -92,7 +93,8 @@ def _lib():
 def make_config(alpha: float = 0.25, mu: float = 0.95, lr: float = 0.02, ns_steps: int = 5,
                 ns_coeffs: Optional[Sequence[Tuple[float, float, float]]] = None, ns_eps: float = 1e-7,
                 axis: str = "auto", precision: str = "bf16", grad_dtype: Optional[torch.dtype] = None,
-                decay_mode: int = 0, scale_mode: int = 0) -> Dion2Config:
+                decay_mode: int = 0, scale_mode: int = 0, select: str = "l1", seed: int = 0,
+                step: int = 0) -> Dion2Config:
     cfg = Dion2Config()
     _lib().dion2_config_init(ctypes.byref(cfg))
     cfg.alpha, cfg.mu, cfg.lr, cfg.ns_steps, cfg.ns_eps = alpha, mu, lr, ns_steps, ns_eps
@@ -105,6 +107,8 @@ def make_config(alpha: float = 0.25, mu: float = 0.95, lr: float = 0.02, ns_step
     cfg.precision = PRECISION[precision]
     cfg.grad_dtype = 1 if grad_dtype == torch.bfloat16 else 0
     cfg.decay_mode, cfg.scale_mode = decay_mode, scale_mode
+    cfg.select = SELECT[select]
+    cfg.seed, cfg.step = seed, step
     return cfg
 
 
@@ -288,8 +292,9 @@ class Dion2Dist:
         self._ws: Optional[torch.Tensor] = None
         self.last_comm_bytes = 0
 
-    def step(self, Ws, Ms, Gs, sel_out=None, stream=None):
+    def step(self, Ws, Ms, Gs, sel_out=None, stream=None, **override):
         kw = dict(self.cfg_kw)
+        kw.update(override)
         kw.setdefault("grad_dtype", Gs[0].dtype)
         cfg = make_config(**kw)
         dev = Ws[0].device
@@ -325,9 +330,10 @@ class Dion2Loopback:
         self._ws: List[torch.Tensor] = []
         self.last_comm_bytes = 0
 
-    def step(self, Ws, Ms, Gs, sel_out=None, stream=None):
+    def step(self, Ws, Ms, Gs, sel_out=None, stream=None, **override):
         """Ws, Ms, Gs: [world][n] local shards; sel_out: optional [world][n] int32 tensors."""
         kw = dict(self.cfg_kw)
+        kw.update(override)
         kw.setdefault("grad_dtype", Gs[0][0].dtype)
         cfg = make_config(**kw)
         n, P = len(self.shapes), self.world

@@ -54,15 +54,18 @@ def _tie_equivalent(K_gpu, K_ref, scores):
 
 def run_parity(shapes: Sequence[Tuple[int, int]], alpha: float, axis: str = "auto", precision: str = "bf16",
                steps: int = 10, seed: int = 0, mu: float = 0.95, lr: float = 0.02, row_scaled: bool = False,
-               decay_mode: int = 0, check_bitwise: bool = True, device: str = "cuda") -> ParityResult:
+               decay_mode: int = 0, check_bitwise: bool = True, device: str = "cuda", select: str = "l1",
+               sel_seed: int = 0) -> ParityResult:
     res = ParityResult()
     cfg_o = oracle_cfg(alpha, axis, mu, lr, decay_mode)
+    cfg_o.select, cfg_o.seed = select, sel_seed
     W0 = [gen_w0(m, n, seed, i) for i, (m, n) in enumerate(shapes)]
     Wg = [torch.from_numpy(w).to(device) for w in W0]
     Mg = [torch.zeros(m, n, device=device) for (m, n) in shapes]
     Wr = [w.astype(np.float64) for w in W0]
     Mr = [np.zeros((m, n)) for (m, n) in shapes]
-    opt = Dion2(alpha=alpha, mu=mu, lr=lr, axis=axis, precision=precision, decay_mode=decay_mode)
+    opt = Dion2(alpha=alpha, mu=mu, lr=lr, axis=axis, precision=precision, decay_mode=decay_mode, select=select,
+                seed=sel_seed)
     ks = []
     for (m, n) in shapes:
         ax = O.resolve_axis(m, n, cfg_o.axis)
@@ -78,14 +81,15 @@ def run_parity(shapes: Sequence[Tuple[int, int]], alpha: float, axis: str = "aut
         if check_bitwise:
             Wb = [w.clone() for w in Wg]
             Mb = [mm.clone() for mm in Mg]
-        opt.step(Wg, Mg, Gg, sel_out=sel, O_out=Oo)
+        opt.step(Wg, Mg, Gg, sel_out=sel, O_out=Oo, step=t)
+        cfg_o.step = t
         torch.cuda.synchronize()
         for i, (m, n) in enumerate(shapes):
             Kg = sel[i].cpu().numpy().astype(np.int64)
             g64 = G[i].astype(np.float64)
             Wsave, Msave = Wr[i].copy(), Mr[i].copy()
-            K, Oref, ax = O.dion2_step(Wr[i], Mr[i], g64, cfg_o)
-            if not np.array_equal(K, Kg):
+            K, Oref, ax = O.dion2_step(Wr[i], Mr[i], g64, cfg_o, matrix_id=i)
+            if not np.array_equal(K, Kg) and select == "l1":
                 scores = O.l1_scores(Msave + g64, ax)
                 if _tie_equivalent(Kg, K, scores):
                     res.ties += 1
@@ -93,6 +97,8 @@ def run_parity(shapes: Sequence[Tuple[int, int]], alpha: float, axis: str = "aut
                     K, Oref, ax = O.dion2_step(Wr[i], Mr[i], g64, cfg_o, force_K=Kg)
                 else:
                     res.index_mismatch += 1
+            elif not np.array_equal(K, Kg):
+                res.index_mismatch += 1  # random rule: integer-exact, no tie allowance
             if t == steps - 1:
                 og = Oo[i].cpu().numpy().astype(np.float64)
                 res.O_rel.append(float(np.linalg.norm(og - Oref) / max(np.linalg.norm(Oref), 1e-300)))
@@ -127,7 +133,7 @@ def _finish(res, shapes, Wg, Mg, Wr, Mr, W0):
 
 
 def run_parity_dist(shapes, alpha, world, steps=3, seed=0, mode="loopback", axis="auto", mu=0.95, lr=0.02,
-                    row_scaled=True, device="cuda"):
+                    row_scaled=True, device="cuda", select="l1", sel_seed=0):
     """Distributed step (owner-compute, shards along the non-selection axis) against the
     fp64 oracle on the FULL matrices.  mode = "loopback" (all ranks in this process) or
     "nccl" (world must equal the initialised torch.distributed world; this process is
@@ -136,6 +142,7 @@ def run_parity_dist(shapes, alpha, world, steps=3, seed=0, mode="loopback", axis
     from paper_2512_16928_b200 import dion2 as D
     res = ParityResult()
     cfg_o = oracle_cfg(alpha, axis, mu, lr)
+    cfg_o.select, cfg_o.seed = select, sel_seed
     info = D.dist_info(shapes, world, 0, alpha=alpha, axis=axis, mu=mu, lr=lr)
     axes = info["axis"]
     W0 = [gen_w0(m, n, seed, i) for i, (m, n) in enumerate(shapes)]
@@ -147,11 +154,11 @@ def run_parity_dist(shapes, alpha, world, steps=3, seed=0, mode="loopback", axis
         ks.append(O.select_count(cfg_o.alpha, m if ax == O.AXIS_ROWS else n))
     if mode == "loopback":
         ranks = list(range(world))
-        opt = D.Dion2Loopback(shapes, world, alpha=alpha, axis=axis, mu=mu, lr=lr)
+        opt = D.Dion2Loopback(shapes, world, alpha=alpha, axis=axis, mu=mu, lr=lr, select=select, seed=sel_seed)
     else:
         import torch.distributed as dist
         ranks = [dist.get_rank()]
-        opt = D.Dion2Dist(shapes, alpha=alpha, axis=axis, mu=mu, lr=lr)
+        opt = D.Dion2Dist(shapes, alpha=alpha, axis=axis, mu=mu, lr=lr, select=select, seed=sel_seed)
     full = lambda a, i: torch.from_numpy(a)  # noqa: E731
     Wg = {r: [D.shard_of(full(W0[i], i), axes[i], world, r).to(device) for i in range(len(shapes))] for r in ranks}
     Mg = {r: [torch.zeros_like(w) for w in Wg[r]] for r in ranks}
@@ -171,9 +178,10 @@ def run_parity_dist(shapes, alpha, world, steps=3, seed=0, mode="loopback", axis
         sel = {r: [torch.empty(k, dtype=torch.int32, device=device) for k in ks] for r in ranks}
         if mode == "loopback":
             opt.step([Wg[r] for r in ranks], [Mg[r] for r in ranks], [Gg[r] for r in ranks],
-                     sel_out=[sel[r] for r in ranks])
+                     sel_out=[sel[r] for r in ranks], step=t)
         else:
-            opt.step(Wg[ranks[0]], Mg[ranks[0]], Gg[ranks[0]], sel_out=sel[ranks[0]])
+            opt.step(Wg[ranks[0]], Mg[ranks[0]], Gg[ranks[0]], sel_out=sel[ranks[0]], step=t)
+        cfg_o.step = t
         torch.cuda.synchronize()
         for i in range(len(shapes)):
             Kg = sel[ranks[0]][i].cpu().numpy().astype(np.int64)
@@ -182,8 +190,10 @@ def run_parity_dist(shapes, alpha, world, steps=3, seed=0, mode="loopback", axis
                     res.index_mismatch += 1
             g64 = G[i].astype(np.float64)
             Wsave, Msave = Wr[i].copy(), Mr[i].copy()
-            K, _, ax = O.dion2_step(Wr[i], Mr[i], g64, cfg_o)
-            if not np.array_equal(K, Kg):
+            K, _, ax = O.dion2_step(Wr[i], Mr[i], g64, cfg_o, matrix_id=i)
+            if not np.array_equal(K, Kg) and select != "l1":
+                res.index_mismatch += 1
+            elif not np.array_equal(K, Kg):
                 if _tie_equivalent(Kg, K, O.l1_scores(Msave + g64, ax)):
                     res.ties += 1
                     Wr[i], Mr[i] = Wsave, Msave

@@ -81,11 +81,12 @@ def test_config_validation(lib, kw, code):
     assert rc == code
 
 
-def test_random_select_unsupported(lib):
-    cfg = D.make_config()
-    cfg.select = 1
+def test_select_rule_validation(lib):
+    cfg = D.make_config(select="random", seed=5, step=7)
     out = ctypes.c_size_t(0)
-    assert lib.dion2_workspace_size(_mats([(8, 8)]), 1, ctypes.byref(cfg), ctypes.byref(out)) == 4
+    assert lib.dion2_workspace_size(_mats([(8, 8)]), 1, ctypes.byref(cfg), ctypes.byref(out)) == 0
+    cfg.select = 2
+    assert lib.dion2_workspace_size(_mats([(8, 8)]), 1, ctypes.byref(cfg), ctypes.byref(out)) == 1
 
 
 def test_shape_validation(lib):

@@ -40,6 +40,21 @@ def test_loopback_one_layer_of_the_1b_set(world):
     _assert(run_parity_dist(layer_set_1b(1), 0.25, world, steps=2))
 
 
+def test_loopback_8_ranks_one_layer_of_the_8b_set():
+    """BASELINE configs[3] shapes on 8 (loopback) ranks."""
+    from synth import layer_set_8b
+    _assert(run_parity_dist(layer_set_8b(1), 0.25, 8, steps=1))
+
+
+def test_loopback_8_ranks_stress_shapes():
+    """BASELINE configs[4]: 4096 x 32768 and 28672 x 8192 at alpha = 0.0625 on 8 (loopback) ranks."""
+    _assert(run_parity_dist([(4096, 32768), (28672, 8192)], 0.0625, 8, steps=1))
+
+
+def test_loopback_random_selection():
+    _assert(run_parity_dist(SHAPES, 0.25, 4, steps=3, select="random", sel_seed=99))
+
+
 def test_loopback_alpha1_is_full_muon():
     _assert(run_parity_dist([(256, 512), (512, 256)], 1.0, 2, steps=2))
 

@@ -74,6 +74,25 @@ def test_one_layer_of_the_1b_set_bf16():
     _assert(run_parity(layer_set_1b(layers=1), 0.25, "auto", "bf16", steps=2, check_bitwise=True), BF16_TOL)
 
 
+def test_one_layer_of_the_8b_set_bf16():
+    """One layer of BASELINE configs[3] (Llama-3-8B-like shapes), alpha = 0.25, full size."""
+    from synth import layer_set_8b
+    _assert(run_parity(layer_set_8b(1), 0.25, "auto", "bf16", steps=1, check_bitwise=True), BF16_TOL)
+
+
+def test_stress_shapes_alpha_1_16():
+    """BASELINE configs[4]: 4096 x 32768 (rows, k = 256) and 28672 x 8192 (cols, k = 512) at alpha = 0.0625."""
+    _assert(run_parity([(4096, 32768), (28672, 8192)], 0.0625, "auto", "bf16", steps=1, check_bitwise=True),
+            BF16_TOL)
+
+
+@pytest.mark.parametrize("precision,tol", [("fp32", FP32_TOL), ("bf16", BF16_TOL)])
+def test_random_selection(precision, tol):
+    """Random rule: GPU Philox keys must select exactly the oracle's subset."""
+    _assert(run_parity([(256, 128), (300, 520), (1024, 2048)], 0.25, "auto", precision, steps=4,
+                       select="random", sel_seed=1234), tol)
+
+
 def test_full_decay_ablation_fp32():
     _assert(run_parity([(96, 160)], 0.25, "auto", "fp32", steps=3, decay_mode=1), FP32_TOL)
 

@@ -307,3 +307,51 @@ def test_comm_volume_golden():
         assert O.selected_bytes(r, c, 1.0, O.AXIS_AUTO, b) == int(full)
     # owner exchange (gather + scatter back) at alpha=1 is Muon's 2*m*n*b*(P-1)/P
     assert O.comm_volume(2048, 8192, 1.0, O.AXIS_AUTO, 8, 2) == 2 * 2048 * 8192 * 2 * 7 // 8
+
+
+# ----------------------------------------------------------------------------- random selection
+
+def test_philox_known_answer_vectors():
+    for row in _read_rows("philox4x32_10_kat.txt"):
+        v = [int(x, 16) for x in row]
+        out = O.philox4x32_10(v[0:4], v[4:6])
+        assert [int(x) for x in out] == v[6:10]
+
+
+def test_select_random_is_a_valid_subset_and_deterministic():
+    for d in (1, 7, 64, 1000):
+        for alpha in (0.125, 0.25, 1.0):
+            k = O.select_count(alpha, d)
+            K = O.select_random(d, k, seed=3, matrix_id=5, step=11)
+            assert len(K) == k and len(set(K.tolist())) == k and list(K) == sorted(K)
+            assert K.min() >= 0 and K.max() < d
+            assert np.array_equal(K, O.select_random(d, k, 3, 5, 11))
+    assert list(O.select_random(9, 9, 1, 2, 3)) == list(range(9))          # alpha = 1 -> all
+    assert not np.array_equal(O.select_random(512, 64, 0, 0, 1), O.select_random(512, 64, 0, 0, 2))
+    assert not np.array_equal(O.select_random(512, 64, 0, 0, 1), O.select_random(512, 64, 0, 1, 1))
+    assert not np.array_equal(O.select_random(512, 64, 0, 0, 1), O.select_random(512, 64, 1, 0, 1))
+
+
+def test_select_random_is_uniform_chi_square():
+    """Every index is selected with probability k/d: chi-square over 4000 keyed draws
+    (d = 64, k = 16) at significance 0.001."""
+    from scipy.stats import chisquare
+    d, k, n = 64, 16, 4000
+    counts = np.zeros(d)
+    for step in range(n):
+        counts[O.select_random(d, k, seed=7, matrix_id=0, step=step)] += 1
+    assert chisquare(counts).pvalue > 1e-3
+    # joint uniformity of pairs: a fixed pair is co-selected with p = k(k-1)/(d(d-1))
+    both = sum(1 for step in range(n) if {0, 1} <= set(O.select_random(d, k, 7, 0, step).tolist()))
+    p = k * (k - 1) / (d * (d - 1))
+    assert abs(both - n * p) < 4 * math.sqrt(n * p * (1 - p))
+
+
+def test_dion2_step_random_uses_the_keyed_subset():
+    m, n = 48, 96
+    W, M, _ = _state(m, n)
+    G = gen_grad(m, n).astype(np.float64)
+    cfg = O.OracleConfig(alpha=0.25, select="random", seed=9, step=4)
+    K, Omat, ax = O.dion2_step(W, M, G, cfg, matrix_id=3)
+    assert ax == O.AXIS_ROWS and np.array_equal(K, O.select_random(m, 12, 9, 3, 4))
+    np.testing.assert_allclose(Omat, O.newton_schulz_auto(G[K]), atol=1e-14)
