@@ -476,10 +476,10 @@ int run_ns(Plan& P, const dion2_config* c, Launcher& L, cudaStream_t s, bool do_
   return L.err;
 }
 
-int run_step(Plan& P, const dion2_matrix* mats, const dion2_config* c, void* ws, cudaStream_t s) {
+// Upload the caller's W/M/G/sel_out/O_out pointers into the plan-owned descriptor
+// table when they changed (the workspace itself is pure scratch).
+int refresh_tables(Plan& P, const dion2_matrix* mats, const dion2_config* c, cudaStream_t s) {
   const int n = P.n;
-  // The descriptor tables live in plan-owned device memory (the workspace is pure
-  // scratch); re-upload only when the caller's W/M/G/sel_out/O_out pointers change.
   bool upload = false;
   if ((int)P.last_ptrs.size() != 5 * n) {
     P.last_ptrs.assign(5 * n, nullptr);
@@ -500,92 +500,100 @@ int run_step(Plan& P, const dion2_matrix* mats, const dion2_config* c, void* ws,
                     ((uintptr_t)mats[i].G % (gel == 4 ? 16 : 8) == 0) && (mats[i].ld % 4 == 0);
     D[i].vec4 = al ? 1 : 0;
   }
-  if (upload) {
-    if (cudaMemcpyAsync(P.dtab, P.host_tables.data(), P.host_tables.size(), cudaMemcpyHostToDevice, s) != cudaSuccess)
-      return DION2_ECUDA;
-  }
-  // status[0] = flags (0), status[1] = first bad matrix (atomicMin from 0x7f7f7f7f)
-  if (cudaMemsetAsync(at(ws, P.off_status), 0, 4, s) != cudaSuccess) return DION2_ECUDA;
-  if (cudaMemsetAsync(at(ws, P.off_status + 4), 0x7f, 4, s) != cudaSuccess) return DION2_ECUDA;
+  if (upload &&
+      cudaMemcpyAsync(P.dtab, P.host_tables.data(), P.host_tables.size(), cudaMemcpyHostToDevice, s) != cudaSuccess)
+    return DION2_ECUDA;
+  return DION2_OK;
+}
 
+int reset_status(int32_t* status, cudaStream_t s) {
+  // status[0] = flags (0), status[1] = first bad matrix (atomicMin from 0x7f7f7f7f)
+  if (cudaMemsetAsync(status, 0, 4, s) != cudaSuccess) return DION2_ECUDA;
+  if (cudaMemsetAsync(status + 1, 0x7f, 4, s) != cudaSuccess) return DION2_ECUDA;
+  return DION2_OK;
+}
+
+// grid of a streaming kernel: `persistent` caps it at a few CTAs per SM (grid-stride
+// loops); otherwise one CTA per work chunk, so CTAs retire quickly and a concurrently
+// launched (higher-priority) NS kernel can take SM slots as they free up.
+inline int stream_grid(int64_t units, int per_sm, bool persistent) {
+  const int sms = g_sm_count > 0 ? g_sm_count : 148;
+  const int64_t cap = persistent ? (int64_t)sms * per_sm : (int64_t)1 << 30;
+  return (int)std::max<int64_t>(1, std::min<int64_t>(units, cap));
+}
+
+// K1 momentum + score, K2 select, K3 gather + decay (Alg. 1 l.2-5)
+void stage_pre(Plan& P, const dion2_config* c, void* ws, int32_t* status, Launcher& L, cudaStream_t s,
+               bool persistent) {
+  const int n = P.n;
   const MatDesc* dmats = (const MatDesc*)tab(P, P.off_desc);
   int32_t* bad = (int32_t*)at(ws, P.off_bad);
-  int32_t* status = (int32_t*)at(ws, P.off_status);
-  Launcher L{s};
-  const int sms = g_sm_count > 0 ? g_sm_count : 148;
-
-  // K1 momentum + score (Alg. 1 l.2-3)
   if (P.n_row_mats) {
     L.begin(PH_K1);
-    int64_t blocks = std::min<int64_t>(ceil_div(P.total_rows, 8), (int64_t)sms * 8);
-    k_momentum_score_rows<<<(unsigned)blocks, 256, 0, s>>>(dmats, (const int32_t*)tab(P, P.off_rowmats),
-                                                           (const int64_t*)tab(P, P.off_rowprefix), P.n_row_mats,
-                                                           P.total_rows);
+    const int blocks = stream_grid(ceil_div(P.total_rows, 8), 8, persistent);
+    k_momentum_score_rows<<<blocks, 256, 0, s>>>(dmats, (const int32_t*)tab(P, P.off_rowmats),
+                                                 (const int64_t*)tab(P, P.off_rowprefix), P.n_row_mats, P.total_rows);
     L.end();
   }
   if (P.n_col_mats) {
     L.begin(PH_K1);
-    int64_t blocks = std::min<int64_t>(P.total_col_tiles, (int64_t)sms * 8);
-    k_momentum_score_cols<<<(unsigned)blocks, 256, 0, s>>>(dmats, (const int32_t*)tab(P, P.off_colmats),
-                                                           (const int64_t*)tab(P, P.off_colprefix), P.n_col_mats,
-                                                           P.total_col_tiles);
+    const int blocks = stream_grid(P.total_col_tiles, 8, persistent);
+    k_momentum_score_cols<<<blocks, 256, 0, s>>>(dmats, (const int32_t*)tab(P, P.off_colmats),
+                                                 (const int64_t*)tab(P, P.off_colprefix), P.n_col_mats,
+                                                 P.total_col_tiles);
     L.end();
   }
-  // K2 select (Alg. 1 l.3)
   L.begin(PH_SELECT);
-  k_topk_select<<<n, kSelectThreads, 4 * P.max_d, s>>>(dmats, bad, status, c->select == DION2_SELECT_RANDOM,
-                                                       c->seed, c->step);
+  k_topk_select<<<n, kSelectThreads, 4 * P.max_d, s>>>(dmats, bad, status, c->select == DION2_SELECT_RANDOM, c->seed,
+                                                       c->step);
   L.end();
-  // K3 gather + decay (Alg. 1 l.4-5)
-  {
-    const int decay = 1;
-    if (P.total_gather_tiles > 0) {
-      L.begin(PH_GATHER);
-      int blocks = std::min(P.total_gather_tiles, sms * 8);
-      launch_gather_decay(P.bf16_ns, blocks, s, dmats, (const int32_t*)tab(P, P.off_gprefix), n,
-                          P.total_gather_tiles, bad, decay, c->mu);
-      L.end();
-    }
-    if (P.fl_n[0]) {
-      L.begin(PH_GATHER_ROWS);
-      const int blocks = (int)std::min<int64_t>(ceil_div(P.fl_gunits[0], 8), (int64_t)sms * 8);
-      launch_gather_rows(blocks, s, dmats, (const int32_t*)tab(P, P.off_fl_mats[0]),
-                         (const int32_t*)tab(P, P.off_fl_gprefix[0]), P.fl_n[0], P.fl_gunits[0], bad, c->mu);
-      L.end();
-    }
-    if (P.fl_n[1]) {
-      L.begin(PH_GATHER_COLS);
-      const int blocks = std::min(P.fl_gunits[1], sms * 6);
-      launch_gather_cols_t(blocks, P.fl_maxk, P.fl_maxn, s, dmats, (const int32_t*)tab(P, P.off_fl_mats[1]),
-                           (const int32_t*)tab(P, P.off_fl_gprefix[1]), P.fl_n[1], P.fl_gunits[1], bad, c->mu);
-      L.end();
-    }
+  if (P.total_gather_tiles > 0) {
+    L.begin(PH_GATHER);
+    launch_gather_decay(P.bf16_ns, stream_grid(P.total_gather_tiles, 8, persistent), s, dmats,
+                        (const int32_t*)tab(P, P.off_gprefix), n, P.total_gather_tiles, bad, 1, c->mu);
+    L.end();
   }
-  // norm finalize + K4-K6 Newton-Schulz (Alg. 1 l.4)
-  run_ns(P, c, L, s, true);
-  // K7 scatter (Alg. 1 l.6)
-  {
-    if (P.total_gather_tiles > 0) {
-      L.begin(PH_SCATTER);
-      int blocks = std::min(P.total_gather_tiles, sms * 8);
-      launch_scatter_update(P.bf16_ns, blocks, s, dmats, (const int32_t*)tab(P, P.off_gprefix), n,
-                            P.total_gather_tiles, bad, c->lr);
-      L.end();
-    }
-    if (P.fl_n[0]) {
-      L.begin(PH_SCATTER_ROWS);
-      const int blocks = (int)std::min<int64_t>(ceil_div(P.fl_sunits[0], 8), (int64_t)sms * 8);
-      launch_scatter_rows(blocks, s, dmats, (const int32_t*)tab(P, P.off_fl_mats[0]),
-                          (const int32_t*)tab(P, P.off_fl_sprefix[0]), P.fl_n[0], P.fl_sunits[0], bad, c->lr);
-      L.end();
-    }
-    if (P.fl_n[1]) {
-      L.begin(PH_SCATTER_COLS);
-      const int blocks = std::min(P.fl_sunits[1], sms * 6);
-      launch_scatter_cols_t(blocks, P.fl_maxk, P.fl_maxn, s, dmats, (const int32_t*)tab(P, P.off_fl_mats[1]),
-                            (const int32_t*)tab(P, P.off_fl_sprefix[1]), P.fl_n[1], P.fl_sunits[1], bad, c->lr);
-      L.end();
-    }
+  if (P.fl_n[0]) {
+    L.begin(PH_GATHER_ROWS);
+    launch_gather_rows(stream_grid(ceil_div(P.fl_gunits[0], 8), 8, persistent), s, dmats,
+                       (const int32_t*)tab(P, P.off_fl_mats[0]), (const int32_t*)tab(P, P.off_fl_gprefix[0]),
+                       P.fl_n[0], P.fl_gunits[0], bad, c->mu);
+    L.end();
+  }
+  if (P.fl_n[1]) {
+    L.begin(PH_GATHER_COLS);
+    launch_gather_cols_t(stream_grid(P.fl_gunits[1], 6, persistent), P.fl_maxk, P.fl_maxn, s, dmats,
+                         (const int32_t*)tab(P, P.off_fl_mats[1]), (const int32_t*)tab(P, P.off_fl_gprefix[1]),
+                         P.fl_n[1], P.fl_gunits[1], bad, c->mu);
+    L.end();
+  }
+}
+
+// K7 scatter (Alg. 1 l.6) and the full-decay ablation
+void stage_post(Plan& P, const dion2_matrix* mats, const dion2_config* c, void* ws, Launcher& L, cudaStream_t s,
+                bool persistent) {
+  const int n = P.n;
+  const MatDesc* dmats = (const MatDesc*)tab(P, P.off_desc);
+  int32_t* bad = (int32_t*)at(ws, P.off_bad);
+  if (P.total_gather_tiles > 0) {
+    L.begin(PH_SCATTER);
+    launch_scatter_update(P.bf16_ns, stream_grid(P.total_gather_tiles, 8, persistent), s, dmats,
+                          (const int32_t*)tab(P, P.off_gprefix), n, P.total_gather_tiles, bad, c->lr);
+    L.end();
+  }
+  if (P.fl_n[0]) {
+    L.begin(PH_SCATTER_ROWS);
+    launch_scatter_rows(stream_grid(ceil_div(P.fl_sunits[0], 8), 8, persistent), s, dmats,
+                        (const int32_t*)tab(P, P.off_fl_mats[0]), (const int32_t*)tab(P, P.off_fl_sprefix[0]),
+                        P.fl_n[0], P.fl_sunits[0], bad, c->lr);
+    L.end();
+  }
+  if (P.fl_n[1]) {
+    L.begin(PH_SCATTER_COLS);
+    launch_scatter_cols_t(stream_grid(P.fl_sunits[1], 6, persistent), P.fl_maxk, P.fl_maxn, s, dmats,
+                          (const int32_t*)tab(P, P.off_fl_mats[1]), (const int32_t*)tab(P, P.off_fl_sprefix[1]),
+                          P.fl_n[1], P.fl_sunits[1], bad, c->lr);
+    L.end();
   }
   if (c->decay_mode == 1) {
     L.begin(PH_FULLDECAY);
@@ -595,6 +603,114 @@ int run_step(Plan& P, const dion2_matrix* mats, const dion2_config* c, void* ws,
     k_full_decay<<<grid, 256, P.max_d, s>>>(dmats, n, bad, c->mu);
     L.end();
   }
+}
+
+// ------------------------------------------------------------------ chunked pipeline
+// The matrices are split into C contiguous chunks (equal parameter counts), each with its
+// own sub-plan and workspace region.  Chunk c's Newton-Schulz runs on a library-owned
+// high-priority stream while the caller's stream runs chunk c+1's momentum/score/select/
+// gather and chunk c-1's scatter: the tensor-bound NS and the HBM-bound passes overlap.
+// (Matrices are independent; every matrix still sees Alg. 1 in order.)
+struct ChunkedPlan {
+  std::vector<std::unique_ptr<Plan>> subs;
+  std::vector<int> first, count;
+  std::vector<size_t> off;        // sub-plan workspace offsets from the aligned base
+  size_t total = 0;
+  std::vector<cudaEvent_t> ev;    // fork + pre/ns done per chunk
+};
+std::map<std::string, std::unique_ptr<ChunkedPlan>> g_cplans;
+
+cudaStream_t ns_stream() {
+  static cudaStream_t st = nullptr;
+  if (!st) {
+    int least = 0, greatest = 0;
+    cudaDeviceGetStreamPriorityRange(&least, &greatest);
+    cudaStreamCreateWithPriority(&st, cudaStreamNonBlocking, greatest);
+  }
+  return st;
+}
+
+// DION2_CHUNKS overrides; default: pipeline in 2 chunks when the set is large enough to
+// keep both the NS and the streaming kernels busy (>= 12 matrices, >= 128 M parameters).
+int chunk_count(const dion2_matrix* mats, int n) {
+  if (const char* e = getenv("DION2_CHUNKS")) return std::max(1, std::min(n, atoi(e)));
+  int64_t params = 0;
+  for (int i = 0; i < n; ++i) params += mats[i].rows * mats[i].cols;
+  return (n >= 12 && params >= (int64_t)128 << 20) ? 2 : 1;
+}
+
+int build_chunked_layout(ChunkedPlan& C, const dion2_matrix* mats, int n, const dion2_config* c, int chunks) {
+  int64_t total = 0;
+  for (int i = 0; i < n; ++i) total += mats[i].rows * mats[i].cols;
+  int64_t acc = 0;
+  int start = 0;
+  for (int i = 0; i < n; ++i) {
+    acc += mats[i].rows * mats[i].cols;
+    const int j = (int)C.first.size();
+    if (j < chunks - 1 && acc * chunks >= total * (j + 1) && i + 1 < n) {
+      C.first.push_back(start);
+      C.count.push_back(i + 1 - start);
+      start = i + 1;
+    }
+  }
+  C.first.push_back(start);
+  C.count.push_back(n - start);
+  size_t off = 0;
+  for (size_t j = 0; j < C.first.size(); ++j) {
+    auto P = std::make_unique<Plan>();
+    int rc = build_layout(*P, mats + C.first[j], C.count[j], c);
+    if (rc) return rc;
+    C.off.push_back(off);
+    off = align_up(off + P->total, 4096);
+    C.subs.push_back(std::move(P));
+  }
+  C.total = off + 4096;
+  return DION2_OK;
+}
+
+int run_chunked(ChunkedPlan& C, const dion2_matrix* mats, const dion2_config* c, void* ws, cudaStream_t s0) {
+  const int nc = (int)C.subs.size();
+  cudaStream_t s1 = ns_stream();
+  if (C.ev.empty()) {
+    C.ev.resize(2 * nc + 1);
+    for (auto& e : C.ev) cudaEventCreateWithFlags(&e, cudaEventDisableTiming);
+  }
+  int rc = 0;
+  for (int j = 0; j < nc; ++j)
+    if ((rc = refresh_tables(*C.subs[j], mats + C.first[j], c, s0))) return rc;
+  int32_t* status = (int32_t*)at(ws, C.off[0] + C.subs[0]->off_status);  // the workspace's status word
+  if ((rc = reset_status(status, s0))) return rc;
+  Launcher L0{s0}, L1{s1};
+  cudaEventRecord(C.ev[0], s0);  // fork: s1 follows everything enqueued on s0 so far
+  cudaStreamWaitEvent(s1, C.ev[0], 0);
+  for (int j = 0; j < nc; ++j) {
+    Plan& P = *C.subs[j];
+    void* wsj = at(ws, C.off[j]);
+    stage_pre(P, c, wsj, status, L0, s0, false);
+    cudaEventRecord(C.ev[1 + 2 * j], s0);
+    cudaStreamWaitEvent(s1, C.ev[1 + 2 * j], 0);
+    run_ns(P, c, L1, s1, true);
+    cudaEventRecord(C.ev[2 + 2 * j], s1);
+    if (j > 0) {
+      cudaStreamWaitEvent(s0, C.ev[2 + 2 * (j - 1)], 0);
+      stage_post(*C.subs[j - 1], mats + C.first[j - 1], c, at(ws, C.off[j - 1]), L0, s0, false);
+    }
+  }
+  cudaStreamWaitEvent(s0, C.ev[2 + 2 * (nc - 1)], 0);  // join
+  stage_post(*C.subs[nc - 1], mats + C.first[nc - 1], c, at(ws, C.off[nc - 1]), L0, s0, false);
+  g_last_launches = L0.count + L1.count;
+  return L0.err ? L0.err : L1.err;
+}
+
+int run_step(Plan& P, const dion2_matrix* mats, const dion2_config* c, void* ws, cudaStream_t s) {
+  int rc = refresh_tables(P, mats, c, s);
+  if (rc) return rc;
+  int32_t* status = (int32_t*)at(ws, P.off_status);
+  if ((rc = reset_status(status, s))) return rc;
+  Launcher L{s};
+  stage_pre(P, c, ws, status, L, s, true);
+  run_ns(P, c, L, s, true);  // norm finalize + K4-K6 Newton-Schulz (Alg. 1 l.4)
+  stage_post(P, mats, c, ws, L, s, true);
   g_last_launches = L.count;
   return L.err;
 }
@@ -634,6 +750,14 @@ int dion2_workspace_size(const dion2_matrix* mats, int32_t n, const dion2_config
   if (n < 1 || !mats) return DION2_EINVAL_SHAPE;
   for (int i = 0; i < n; ++i)
     if ((rc = validate_shape(mats[i], false))) return rc;
+  const int chunks = chunk_count(mats, n);
+  if (chunks > 1) {
+    ChunkedPlan C;
+    rc = build_chunked_layout(C, mats, n, cfg, chunks);
+    if (rc) return rc;
+    *bytes_out = C.total;
+    return DION2_OK;
+  }
   Plan P;
   rc = build_layout(P, mats, n, cfg);
   if (rc) return rc;
@@ -655,6 +779,31 @@ int dion2_step_batched(const dion2_matrix* mats, int32_t n, const dion2_config* 
   void* ws = reinterpret_cast<void*>(align_up(reinterpret_cast<uintptr_t>(workspace), 4096));
   const size_t slack = (uintptr_t)ws - (uintptr_t)workspace;
   std::string key = plan_key(mats, n, cfg, ws);
+  const int chunks = chunk_count(mats, n);
+  if (chunks > 1) {
+    key.append(reinterpret_cast<const char*>(&chunks), sizeof chunks);
+    auto ct = g_cplans.find(key);
+    ChunkedPlan* C;
+    if (ct == g_cplans.end()) {
+      auto nc = std::make_unique<ChunkedPlan>();
+      rc = build_chunked_layout(*nc, mats, n, cfg, chunks);
+      if (rc) return rc;
+      if (nc->total - 4096 + slack > ws_bytes) return DION2_EWORKSPACE;
+      for (size_t j = 0; j < nc->subs.size(); ++j) {
+        Plan& S = *nc->subs[j];
+        if ((rc = build_device_plan(S, mats + nc->first[j], cfg, at(ws, nc->off[j])))) return rc;
+        MatDesc* D = reinterpret_cast<MatDesc*>(S.host_tables.data());
+        for (int i = 0; i < S.n; ++i) D[i].mid = nc->first[j] + i;  // global matrix id (status, random keys)
+        S.id = g_next_plan_id++;
+      }
+      C = nc.get();
+      g_cplans[key] = std::move(nc);
+    } else {
+      C = ct->second.get();
+      if (C->total - 4096 + slack > ws_bytes) return DION2_EWORKSPACE;
+    }
+    return run_chunked(*C, mats, cfg, ws, reinterpret_cast<cudaStream_t>(stream));
+  }
   auto it = g_plans.find(key);
   Plan* P;
   if (it == g_plans.end()) {

@@ -76,7 +76,7 @@ __global__ void __launch_bounds__(kSelectThreads) k_topk_select(const MatDesc* _
   if (nonfinite) {
     if (tid == 0) {
       bad[mi] = 1;
-      set_status_bad(status, mi);
+      set_status_bad(status, md.mid);
     }
     for (int i = tid; i < k; i += blockDim.x) {
       md.sel[i] = i;

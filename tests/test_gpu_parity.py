@@ -93,6 +93,29 @@ def test_random_selection(precision, tol):
                        select="random", sel_seed=1234), tol)
 
 
+@pytest.mark.parametrize("chunks", ["2", "3"])
+def test_chunked_pipeline(chunks, monkeypatch):
+    """The two-stream chunked pipeline (NS of chunk c overlapping the streaming passes of
+    its neighbours) computes the same step; random keys use the global matrix id."""
+    monkeypatch.setenv("DION2_CHUNKS", chunks)
+    shapes = [(256, 512), (512, 256), (384, 640), (1024, 512), (256, 256), (640, 384), (512, 1024)]
+    _assert(run_parity(shapes, 0.25, "auto", "bf16", steps=3), BF16_TOL)
+    _assert(run_parity(shapes, 0.25, "auto", "bf16", steps=2, select="random", sel_seed=5), BF16_TOL)
+
+
+def test_chunked_nonfinite_reports_global_index(monkeypatch):
+    monkeypatch.setenv("DION2_CHUNKS", "3")
+    Ws = [torch.from_numpy(gen_w0(64, 128, 0, i)).cuda() for i in range(6)]
+    W0 = [w.clone() for w in Ws]
+    Ms = [torch.zeros_like(w) for w in Ws]
+    Gs = [torch.from_numpy(gen_grad(64, 128, 0, i)).cuda() for i in range(6)]
+    Gs[4][1, 2] = float("inf")
+    opt = Dion2(alpha=0.25)
+    opt.step(Ws, Ms, Gs)
+    assert opt.status() == (7, 4)
+    assert torch.equal(Ws[4], W0[4]) and not torch.equal(Ws[5], W0[5])
+
+
 def test_full_decay_ablation_fp32():
     _assert(run_parity([(96, 160)], 0.25, "auto", "fp32", steps=3, decay_mode=1), FP32_TOL)
 
