@@ -187,6 +187,29 @@ int dion2_step_batched_loopback(const dion2_shard* shards, int32_t n, const dion
                                 void* const* workspaces, size_t ws_bytes, int32_t world, void* stream,
                                 uint64_t* comm_bytes_out);
 
+/* ------------------------------------------------------------------------------------------
+ * Compressed DP-sync (paper 3.2): `world` data-parallel replicas, each holding the
+ * FULL W and M and its OWN local gradient G (no gradient all-reduce).  With the random rule
+ * (cfg.select = DION2_SELECT_RANDOM, identical seed/step on every replica) the selection needs
+ * no global state, so each replica accumulates M <- M + G locally, draws the same K, and only
+ * the selected fp32 submatrix M[K, :] (or M[:, K]) is averaged across replicas (one
+ * ncclAllReduce of sum_j k_j*o_j floats instead of sum_j m_j*n_j).  Every replica then runs the
+ * rest of Alg. 1 on identical rows, so W stays identical while unselected momentum rows diverge;
+ * by linearity the mean momentum equals the full-sync momentum and the W trajectory equals
+ * full gradient sync ("the information that is synchronized suffices to compute the correct
+ * parameter update").  cfg.select must be RANDOM (EUNSUPPORTED otherwise).
+ * ------------------------------------------------------------------------------------------ */
+int dion2_dpsync_workspace_size(const dion2_matrix* mats, int32_t n, const dion2_config* cfg, int32_t world,
+                                size_t* bytes_out);
+int dion2_step_batched_dpsync(const dion2_matrix* mats, int32_t n, const dion2_config* cfg, void* workspace,
+                              size_t ws_bytes, void* nccl_comm, int32_t world, int32_t rank, void* stream,
+                              uint64_t* comm_bytes_out);
+/* All replicas in one process on one device (mats: [world * n], replica-major; the all-reduce is
+ * emulated with device copies and a fixed-order sum). */
+int dion2_step_batched_dpsync_loopback(const dion2_matrix* mats, int32_t n, const dion2_config* cfg,
+                                       void* const* workspaces, size_t ws_bytes, int32_t world, void* stream,
+                                       uint64_t* comm_bytes_out);
+
 /* Number of kernel launches the last step enqueued. */
 int32_t dion2_last_launch_count(void);
 

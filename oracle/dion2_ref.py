@@ -212,6 +212,36 @@ def dion2_step(W: np.ndarray, M: np.ndarray, G: np.ndarray, cfg: OracleConfig,
     return K, O, axis
 
 
+def dion2_step_dpsync(Ws, Ms, Gs, cfg: OracleConfig, matrix_id: int = 0):
+    """Compressed DP-sync: P data-parallel replicas, each with its own local
+    gradient G_r and its own (diverging) momentum M_r.  With a selection rule that needs no
+    global state (random, "with uniform random selection, only the selected submatrix
+    M[K,:] needs to be synchronized"), each replica accumulates M_r <- M_r + G_r, the shared
+    K is drawn, only M_r[K,:] is averaged across replicas, and every replica then runs the
+    rest of Alg. 1 on the synchronised rows (identical W updates everywhere).
+    Ws, Ms: lists of per-replica float64 arrays (updated in place).  Returns K."""
+    assert cfg.select == "random", "compressed DP-sync needs a selection rule without global state"
+    P = len(Ws)
+    m, n = Ws[0].shape
+    for r in range(P):
+        Ms[r] += Gs[r]
+    axis = resolve_axis(m, n, cfg.axis)
+    d = m if axis == AXIS_ROWS else n
+    K = select_random(d, select_count(cfg.alpha, d), cfg.seed, matrix_id, cfg.step)
+    if axis == AXIS_ROWS:
+        avg = sum(Mr[K, :] for Mr in Ms) / P
+        for Mr in Ms:
+            Mr[K, :] = avg
+    else:
+        avg = sum(Mr[:, K] for Mr in Ms) / P
+        for Mr in Ms:
+            Mr[:, K] = avg
+    # the rest of Alg. 1 on the synchronised rows: M += 0 (already accumulated), same K
+    for r in range(P):
+        dion2_step(Ws[r], Ms[r], np.zeros_like(Gs[r]), cfg, force_K=K, matrix_id=matrix_id)
+    return K
+
+
 def muon_step(W: np.ndarray, M: np.ndarray, G: np.ndarray, cfg: OracleConfig) -> np.ndarray:
     """Heavy-ball Muon ("O_Muon = Newton-Schulz(M)"):
     M <- mu*M + G; O = NS(M); W <- W - eta*sqrt(m/n)*O.  No Nesterov (reading R12)."""

@@ -525,6 +525,13 @@ inline int stream_grid(int64_t units, int per_sm, bool persistent) {
 // K1 momentum + score, K2 select, K3 gather + decay (Alg. 1 l.2-5)
 void stage_pre(Plan& P, const dion2_config* c, void* ws, int32_t* status, Launcher& L, cudaStream_t s,
                bool persistent) {
+  stage_k1_select(P, c, ws, status, L, s, persistent);
+  stage_gather(P, c, ws, L, s, persistent);
+}
+
+// K1 momentum + score, K2 select (Alg. 1 l.2-3)
+void stage_k1_select(Plan& P, const dion2_config* c, void* ws, int32_t* status, Launcher& L, cudaStream_t s,
+                     bool persistent) {
   const int n = P.n;
   const MatDesc* dmats = (const MatDesc*)tab(P, P.off_desc);
   int32_t* bad = (int32_t*)at(ws, P.off_bad);
@@ -547,6 +554,13 @@ void stage_pre(Plan& P, const dion2_config* c, void* ws, int32_t* status, Launch
   k_topk_select<<<n, kSelectThreads, 4 * P.max_d, s>>>(dmats, bad, status, c->select == DION2_SELECT_RANDOM, c->seed,
                                                        c->step);
   L.end();
+}
+
+// K3 gather + selective decay (Alg. 1 l.4-5)
+void stage_gather(Plan& P, const dion2_config* c, void* ws, Launcher& L, cudaStream_t s, bool persistent) {
+  const int n = P.n;
+  const MatDesc* dmats = (const MatDesc*)tab(P, P.off_desc);
+  int32_t* bad = (int32_t*)at(ws, P.off_bad);
   if (P.total_gather_tiles > 0) {
     L.begin(PH_GATHER);
     launch_gather_decay(P.bf16_ns, stream_grid(P.total_gather_tiles, 8, persistent), s, dmats,

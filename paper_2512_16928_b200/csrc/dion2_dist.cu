@@ -37,6 +37,7 @@ struct NcclApi {
   ncclResult_t (*recv)(void*, size_t, int, int, ncclComm_t, cudaStream_t) = nullptr;
   ncclResult_t (*group_start)() = nullptr;
   ncclResult_t (*group_end)() = nullptr;
+  ncclResult_t (*allreduce)(const void*, void*, size_t, int, int, ncclComm_t, cudaStream_t) = nullptr;
   bool ok = false;
 };
 NcclApi& nccl_api() {
@@ -50,7 +51,8 @@ NcclApi& nccl_api() {
     a.recv = reinterpret_cast<decltype(a.recv)>(dlsym(h, "ncclRecv"));
     a.group_start = reinterpret_cast<decltype(a.group_start)>(dlsym(h, "ncclGroupStart"));
     a.group_end = reinterpret_cast<decltype(a.group_end)>(dlsym(h, "ncclGroupEnd"));
-    a.ok = a.allgather && a.send && a.recv && a.group_start && a.group_end;
+    a.allreduce = reinterpret_cast<decltype(a.allreduce)>(dlsym(h, "ncclAllReduce"));
+    a.ok = a.allgather && a.send && a.recv && a.group_start && a.group_end && a.allreduce;
     return a;
   }();
   return api;
@@ -678,6 +680,124 @@ int run_dist(std::vector<DistPlan*>& plans, std::vector<void*>& wss, const std::
   return L.err;
 }
 
+// ------------------------------------------------------------------ compressed DP-sync
+// Replicas (one per rank) hold full W, M and their own local G.  With the random rule the
+// selection needs no global state, so only the selected fp32 rows M[K] are all-reduced
+// (averaged); every replica then runs the rest of the step on identical rows.
+struct DpPlan {
+  Plan P;
+  int world = 1;
+  size_t off_buf = 0, off_gather = 0, total = 0;
+  int64_t buf_floats = 0;
+  int total_rows = 0;
+  void* dtab = nullptr;  // [n] int32 row prefix, then [n] int64 buffer offsets
+  size_t t_prefix = 0, t_off = 0;
+  bool uploaded = false;
+  std::vector<uint8_t> htab;
+};
+std::map<std::string, std::unique_ptr<DpPlan>> g_dp_plans;
+
+int dp_layout(DpPlan& D, const dion2_matrix* mats, int n, const dion2_config* c, int world) {
+  if (c->select != DION2_SELECT_RANDOM) return DION2_EUNSUPPORTED;  // l1 scores need the full momentum
+  if (world < 1) return DION2_EINVAL_SHAPE;
+  D.world = world;
+  int rc = build_layout(D.P, mats, n, c);
+  if (rc) return rc;
+  D.buf_floats = 0;
+  D.total_rows = 0;
+  for (auto& q : D.P.mp) {
+    D.buf_floats += (int64_t)q.sr * q.sc;
+    D.total_rows += q.sr;
+  }
+  D.off_buf = align_up(D.P.total, 4096);
+  D.off_gather = align_up(D.off_buf + 4 * (size_t)D.buf_floats, 4096);
+  D.total = D.off_gather + 4 * (size_t)D.buf_floats * world + 4096;
+  return DION2_OK;
+}
+
+int dp_get_plan(DpPlan** out, const dion2_matrix* mats, int n, const dion2_config* c, int world, void* workspace,
+                size_t ws_bytes, void** ws_out) {
+  void* ws = reinterpret_cast<void*>(align_up(reinterpret_cast<uintptr_t>(workspace), 4096));
+  const size_t slack = (uintptr_t)ws - (uintptr_t)workspace;
+  std::string key;
+  auto put = [&](const void* p, size_t s) { key.append(reinterpret_cast<const char*>(p), s); };
+  put(&n, 4);
+  put(&world, 4);
+  put(&ws, sizeof ws);
+  for (int i = 0; i < n; ++i) {
+    put(&mats[i].rows, 8);
+    put(&mats[i].cols, 8);
+    put(&mats[i].ld, 8);
+  }
+  put(&c->alpha, 4);
+  put(&c->ns_steps, 4);
+  put(c->ns_coeffs, sizeof(float) * 3 * c->ns_steps);
+  put(&c->axis, 4);
+  put(&c->precision, 4);
+  put(&c->grad_dtype, 4);
+  put(&c->decay_mode, 4);
+  put(&c->scale_mode, 4);
+  auto it = g_dp_plans.find(key);
+  if (it == g_dp_plans.end()) {
+    auto D = std::make_unique<DpPlan>();
+    int rc = dp_layout(*D, mats, n, c, world);
+    if (rc) return rc;
+    if (D->total - 4096 + slack > ws_bytes) return DION2_EWORKSPACE;
+    if ((rc = build_device_plan(D->P, mats, c, ws))) return rc;
+    D->t_prefix = 0;
+    D->t_off = align_up(4 * (size_t)n, 256);
+    D->htab.assign(D->t_off + 8 * (size_t)n, 0);
+    int32_t* pre = reinterpret_cast<int32_t*>(D->htab.data());
+    int64_t* off = reinterpret_cast<int64_t*>(D->htab.data() + D->t_off);
+    int rows = 0;
+    int64_t fo = 0;
+    for (int i = 0; i < n; ++i) {
+      pre[i] = rows;
+      off[i] = fo;
+      rows += D->P.mp[i].sr;
+      fo += (int64_t)D->P.mp[i].sr * D->P.mp[i].sc;
+    }
+    if (cudaMalloc(&D->dtab, D->htab.size()) != cudaSuccess) return DION2_ECUDA;
+    it = g_dp_plans.emplace(key, std::move(D)).first;
+  }
+  DpPlan& D = *it->second;
+  if (D.total - 4096 + slack > ws_bytes) return DION2_EWORKSPACE;
+  *out = &D;
+  *ws_out = ws;
+  return DION2_OK;
+}
+
+void dp_pack(DpPlan& D, void* ws, bool unpack, float scale, cudaStream_t s, Launcher& L) {
+  L.begin(unpack ? PH_GATHER : PH_SELECT);
+  launch_dp_pack(unpack, s, (const MatDesc*)tab(D.P, D.P.off_desc),
+                 (const int32_t*)((uint8_t*)D.dtab + D.t_prefix), (const int64_t*)((uint8_t*)D.dtab + D.t_off),
+                 D.P.n, D.total_rows, (float*)at(ws, D.off_buf), scale, (const int32_t*)at(ws, D.P.off_bad));
+  L.end();
+}
+
+// phases 1: refresh + K1 + select + pack; 2: unpack + gather + NS + scatter
+int dp_phase1(DpPlan& D, const dion2_matrix* mats, const dion2_config* c, void* ws, cudaStream_t s, Launcher& L) {
+  int rc = refresh_tables(D.P, mats, c, s);
+  if (rc) return rc;
+  if (!D.uploaded) {
+    if (cudaMemcpyAsync(D.dtab, D.htab.data(), D.htab.size(), cudaMemcpyHostToDevice, s) != cudaSuccess)
+      return DION2_ECUDA;
+    D.uploaded = true;
+  }
+  int32_t* status = (int32_t*)at(ws, D.P.off_status);
+  if ((rc = reset_status(status, s))) return rc;
+  stage_k1_select(D.P, c, ws, status, L, s, true);
+  dp_pack(D, ws, false, 1.f, s, L);
+  return DION2_OK;
+}
+
+void dp_phase2(DpPlan& D, const dion2_matrix* mats, const dion2_config* c, void* ws, cudaStream_t s, Launcher& L) {
+  dp_pack(D, ws, true, 1.f / (float)D.world, s, L);  // M[K] <- mean over replicas
+  stage_gather(D.P, c, ws, L, s, true);
+  run_ns(D.P, c, L, s, true);
+  stage_post(D.P, mats, c, ws, L, s, true);
+}
+
 }  // namespace
 }  // namespace dion2rt
 
@@ -752,6 +872,86 @@ int dion2_step_batched_loopback(const dion2_shard* shards, int32_t n, const dion
   cudaStream_t s = reinterpret_cast<cudaStream_t>(stream);
   LoopbackTransport T(plans, wss, s);
   return run_dist(plans, wss, sh, cfg, T, s, comm_bytes_out);
+}
+
+}  // extern "C"
+
+// ------------------------------------------------------------------ compressed DP-sync ABI
+extern "C" {
+
+int dion2_dpsync_workspace_size(const dion2_matrix* mats, int32_t n, const dion2_config* cfg, int32_t world,
+                                size_t* bytes_out) {
+  int rc = validate_config(cfg);
+  if (rc) return rc;
+  if (!bytes_out) return DION2_EINVAL_CONFIG;
+  if (n < 1 || !mats) return DION2_EINVAL_SHAPE;
+  for (int i = 0; i < n; ++i)
+    if ((rc = validate_shape(mats[i], false))) return rc;
+  DpPlan D;
+  if ((rc = dp_layout(D, mats, n, cfg, world))) return rc;
+  *bytes_out = D.total;
+  return DION2_OK;
+}
+
+int dion2_step_batched_dpsync(const dion2_matrix* mats, int32_t n, const dion2_config* cfg, void* workspace,
+                              size_t ws_bytes, void* nccl_comm, int32_t world, int32_t rank, void* stream,
+                              uint64_t* comm_bytes_out) {
+  int rc = validate_config(cfg);
+  if (rc) return rc;
+  if (n < 1 || !mats) return DION2_EINVAL_SHAPE;
+  for (int i = 0; i < n; ++i)
+    if ((rc = validate_shape(mats[i], true))) return rc;
+  if (!workspace) return DION2_EWORKSPACE;
+  if (!nccl_comm || !nccl_api().ok) return DION2_ENCCL;
+  if (rank < 0 || rank >= world) return DION2_EINVAL_SHAPE;
+  std::lock_guard<std::mutex> lock(g_mu);
+  ensure_device_attrs();
+  DpPlan* D = nullptr;
+  void* ws = nullptr;
+  if ((rc = dp_get_plan(&D, mats, n, cfg, world, workspace, ws_bytes, &ws))) return rc;
+  cudaStream_t s = reinterpret_cast<cudaStream_t>(stream);
+  Launcher L{s};
+  if ((rc = dp_phase1(*D, mats, cfg, ws, s, L))) return rc;
+  float* buf = (float*)at(ws, D->off_buf);
+  if (nccl_api().allreduce(buf, buf, (size_t)D->buf_floats, kNcclFloat32, /*ncclSum*/ 0, nccl_comm, s))
+    return DION2_ENCCL;
+  dp_phase2(*D, mats, cfg, ws, s, L);
+  g_last_launches = L.count;
+  if (comm_bytes_out) *comm_bytes_out = (uint64_t)(2.0 * (world - 1) / world * 4.0 * (double)D->buf_floats);
+  return L.err;
+}
+
+int dion2_step_batched_dpsync_loopback(const dion2_matrix* mats, int32_t n, const dion2_config* cfg,
+                                       void* const* workspaces, size_t ws_bytes, int32_t world, void* stream,
+                                       uint64_t* comm_bytes_out) {
+  int rc = validate_config(cfg);
+  if (rc) return rc;
+  if (n < 1 || !mats || world < 1 || !workspaces) return DION2_EINVAL_SHAPE;
+  for (int i = 0; i < n * world; ++i)
+    if ((rc = validate_shape(mats[i], true))) return rc;
+  std::lock_guard<std::mutex> lock(g_mu);
+  ensure_device_attrs();
+  std::vector<DpPlan*> D(world);
+  std::vector<void*> ws(world);
+  for (int r = 0; r < world; ++r)
+    if ((rc = dp_get_plan(&D[r], mats + (size_t)r * n, n, cfg, world, workspaces[r], ws_bytes, &ws[r]))) return rc;
+  cudaStream_t s = reinterpret_cast<cudaStream_t>(stream);
+  Launcher L{s};
+  for (int r = 0; r < world; ++r)
+    if ((rc = dp_phase1(*D[r], mats + (size_t)r * n, cfg, ws[r], s, L))) return rc;
+  // all-reduce (sum) emulated: gather every replica's buffer at replica 0, sum in rank order, broadcast
+  const size_t bytes = 4 * (size_t)D[0]->buf_floats;
+  for (int r = 0; r < world; ++r)
+    cudaMemcpyAsync(at(ws[0], D[0]->off_gather + r * bytes), at(ws[r], D[r]->off_buf), bytes,
+                    cudaMemcpyDeviceToDevice, s);
+  launch_sum_rank_scores(s, (const float*)at(ws[0], D[0]->off_gather), (float*)at(ws[0], D[0]->off_buf),
+                         D[0]->buf_floats, world);
+  for (int r = 1; r < world; ++r)
+    cudaMemcpyAsync(at(ws[r], D[r]->off_buf), at(ws[0], D[0]->off_buf), bytes, cudaMemcpyDeviceToDevice, s);
+  for (int r = 0; r < world; ++r) dp_phase2(*D[r], mats + (size_t)r * n, cfg, ws[r], s, L);
+  g_last_launches = L.count;
+  if (comm_bytes_out) *comm_bytes_out = (uint64_t)(2.0 * (world - 1) / world * (double)bytes);
+  return L.err;
 }
 
 }  // extern "C"

@@ -1,0 +1,58 @@
+// Compressed DP-sync: pack the selected fp32 submatrix
+// S = M[K, :] (or M[:, K]) of every matrix into one contiguous buffer for the
+// all-reduce, and write the averaged rows back.  One warp per row of S; rows
+// mode streams contiguous rows of M, cols mode gathers the selected columns.
+#include "kernels.cuh"
+
+namespace dion2 {
+
+__device__ __forceinline__ int find_row(const int32_t* __restrict__ prefix, int n, int t) {
+  int lo = 0, hi = n - 1;
+  while (lo < hi) {
+    int mid = (lo + hi + 1) >> 1;
+    if (prefix[mid] <= t) lo = mid; else hi = mid - 1;
+  }
+  return lo;
+}
+
+// unit = one row a of S of one matrix; row_prefix[mi] = first unit of matrix mi
+template <bool kUnpack>
+__global__ void __launch_bounds__(256) k_dp_pack(const MatDesc* __restrict__ mats, const int32_t* __restrict__ row_prefix,
+                                                 const int64_t* __restrict__ buf_off, int n_mats, int total_rows,
+                                                 float* __restrict__ buf, float scale, const int32_t* __restrict__ bad) {
+  const int lane = threadIdx.x & 31;
+  const int warp = blockIdx.x * (blockDim.x >> 5) + (threadIdx.x >> 5);
+  const int nwarps = gridDim.x * (blockDim.x >> 5);
+  for (int u = warp; u < total_rows; u += nwarps) {
+    const int mi = find_row(row_prefix, n_mats, u);
+    const MatDesc& md = mats[mi];
+    if (kUnpack && bad[mi]) continue;
+    const int a = u - row_prefix[mi];
+    float* b = buf + buf_off[mi] + (int64_t)a * md.sc;
+    if (md.axis == kAxisRows) {
+      float* mrow = md.M + (int64_t)md.sel[a] * md.ld;
+      for (int c = lane; c < md.sc; c += 32) {
+        if (kUnpack) mrow[c] = scale * b[c];
+        else b[c] = mrow[c];
+      }
+    } else {
+      float* mrow = md.M + (int64_t)a * md.ld;
+      for (int c = lane; c < md.sc; c += 32) {
+        float* p = mrow + md.sel[c];
+        if (kUnpack) *p = scale * b[c];
+        else b[c] = *p;
+      }
+    }
+  }
+}
+
+void launch_dp_pack(bool unpack, cudaStream_t s, const MatDesc* mats, const int32_t* row_prefix, const int64_t* buf_off,
+                    int n_mats, int total_rows, float* buf, float scale, const int32_t* bad) {
+  const int blocks = (total_rows + 7) / 8;
+  if (unpack)
+    k_dp_pack<true><<<blocks, 256, 0, s>>>(mats, row_prefix, buf_off, n_mats, total_rows, buf, scale, bad);
+  else
+    k_dp_pack<false><<<blocks, 256, 0, s>>>(mats, row_prefix, buf_off, n_mats, total_rows, buf, scale, bad);
+}
+
+}  // namespace dion2

@@ -58,6 +58,10 @@ void launch_assemble(cudaStream_t s, const MatDesc* omats, int n_owned, int max_
 void launch_disassemble(cudaStream_t s, const MatDesc* omats, int n_owned, int max_k, const PieceTable& T,
                         uint8_t* send);
 
+// ---------------- compressed DP-sync (k_dpsync.cu): M[K] <-> contiguous fp32 buffer
+void launch_dp_pack(bool unpack, cudaStream_t s, const MatDesc* mats, const int32_t* row_prefix, const int64_t* buf_off,
+                    int n_mats, int total_rows, float* buf, float scale, const int32_t* bad);
+
 // ---------------- K4-K6 Newton-Schulz GEMMs
 // D = oscale * (cacc * Aop . Bop + cC * C), written as OutT.
 //   Aop: [M x K] row-major (K-major); Bop(k, n) = B[n][k] (b_kmajor) or B[k][n].

@@ -133,5 +133,14 @@ int build_layout(Plan& P, const dion2_matrix* mats, int n, const dion2_config* c
 int build_device_plan(Plan& P, const dion2_matrix* mats, const dion2_config* c, void* ws);
 void ensure_device_attrs();
 int run_ns(Plan& P, const dion2_config* c, Launcher& L, cudaStream_t s, bool do_norm);
+int refresh_tables(Plan& P, const dion2_matrix* mats, const dion2_config* c, cudaStream_t s);
+int reset_status(int32_t* status, cudaStream_t s);
+void stage_pre(Plan& P, const dion2_config* c, void* ws, int32_t* status, Launcher& L, cudaStream_t s,
+               bool persistent);
+void stage_k1_select(Plan& P, const dion2_config* c, void* ws, int32_t* status, Launcher& L, cudaStream_t s,
+                     bool persistent);
+void stage_gather(Plan& P, const dion2_config* c, void* ws, Launcher& L, cudaStream_t s, bool persistent);
+void stage_post(Plan& P, const dion2_matrix* mats, const dion2_config* c, void* ws, Launcher& L, cudaStream_t s,
+                bool persistent);
 
 }  // namespace dion2rt

@@ -25,7 +25,8 @@ STATUS = {0: "OK", 1: "EINVAL_CONFIG", 2: "EINVAL_SHAPE", 3: "EWORKSPACE", 4: "E
 EXPORTED = ["dion2_config_init", "dion2_workspace_size", "dion2_step", "dion2_step_batched", "dion2_get_status",
             "dion2_strerror", "dion2_set_phase_timing", "dion2_get_phase_times", "dion2_phase_name",
             "dion2_last_launch_count", "dion2_abi_version", "dion2_dist_info", "dion2_step_batched_dist",
-            "dion2_step_batched_loopback"]
+            "dion2_step_batched_loopback", "dion2_dpsync_workspace_size", "dion2_step_batched_dpsync",
+            "dion2_step_batched_dpsync_loopback"]
 
 
 class Dion2Matrix(ctypes.Structure):
@@ -86,6 +87,14 @@ def _lib():
         lib.dion2_step_batched_loopback.argtypes = [P(Dion2Shard), ctypes.c_int32, P(Dion2Config),
                                                     P(ctypes.c_void_p), ctypes.c_size_t, ctypes.c_int32,
                                                     ctypes.c_void_p, P(ctypes.c_uint64)]
+        lib.dion2_dpsync_workspace_size.argtypes = [P(Dion2Matrix), ctypes.c_int32, P(Dion2Config), ctypes.c_int32,
+                                                    P(ctypes.c_size_t)]
+        lib.dion2_step_batched_dpsync.argtypes = [P(Dion2Matrix), ctypes.c_int32, P(Dion2Config), ctypes.c_void_p,
+                                                  ctypes.c_size_t, ctypes.c_void_p, ctypes.c_int32, ctypes.c_int32,
+                                                  ctypes.c_void_p, P(ctypes.c_uint64)]
+        lib.dion2_step_batched_dpsync_loopback.argtypes = [P(Dion2Matrix), ctypes.c_int32, P(Dion2Config),
+                                                           P(ctypes.c_void_p), ctypes.c_size_t, ctypes.c_int32,
+                                                           ctypes.c_void_p, P(ctypes.c_uint64)]
         _LIB = lib
     return _LIB
 
@@ -353,4 +362,65 @@ class Dion2Loopback:
                                                 ctypes.byref(nbytes))
         if rc:
             raise Dion2Error(rc, "dion2_step_batched_loopback")
+        self.last_comm_bytes = nbytes.value
+
+
+class Dion2DpSync:
+    """Compressed DP-sync (paper 3.2): each rank is a data-parallel replica with full W, M
+    and its local G; only M[K] is all-reduced (averaged).  Requires select="random"."""
+
+    def __init__(self, group=None, loopback_world: int = 0, **cfg_kw):
+        cfg_kw.setdefault("select", "random")
+        self.cfg_kw = dict(cfg_kw)
+        self.group = group
+        self.loopback = loopback_world > 0
+        if self.loopback:
+            self.world, self.rank = loopback_world, 0
+        else:
+            import torch.distributed as dist
+            self.world, self.rank = dist.get_world_size(group), dist.get_rank(group)
+        self._ws: List[torch.Tensor] = []
+        self.last_comm_bytes = 0
+
+    def _cfg(self, Gs0, override):
+        kw = dict(self.cfg_kw)
+        kw.update(override)
+        kw.setdefault("grad_dtype", Gs0.dtype)
+        return make_config(**kw)
+
+    def step(self, Ws, Ms, Gs, sel_out=None, stream=None, **override):
+        """NCCL mode: this rank's full matrices.  Loopback mode: [world][n] lists."""
+        if self.loopback:
+            n, P = len(Ws[0]), self.world
+            cfg = self._cfg(Gs[0][0], override)
+            parts = [describe(Ws[r], Ms[r], Gs[r], sel_out[r] if sel_out is not None else None)[0] for r in range(P)]
+            arr = (Dion2Matrix * (n * P))()
+            for r in range(P):
+                for i in range(n):
+                    arr[r * n + i] = parts[r][i]
+            dev = Ws[0][0].device
+        else:
+            n, P = len(Ws), self.world
+            cfg = self._cfg(Gs[0], override)
+            arr, _ = describe(Ws, Ms, Gs, sel_out)
+            dev = Ws[0].device
+        need = ctypes.c_size_t(0)
+        rc = _lib().dion2_dpsync_workspace_size(arr, n, ctypes.byref(cfg), P, ctypes.byref(need))
+        if rc:
+            raise Dion2Error(rc, "dion2_dpsync_workspace_size")
+        nws = P if self.loopback else 1
+        if len(self._ws) != nws or self._ws[0].numel() < need.value:
+            self._ws = [torch.empty(need.value, dtype=torch.uint8, device=dev) for _ in range(nws)]
+        st = stream if stream is not None else torch.cuda.current_stream(dev)
+        nbytes = ctypes.c_uint64(0)
+        if self.loopback:
+            wsp = (ctypes.c_void_p * P)(*[w.data_ptr() for w in self._ws])
+            rc = _lib().dion2_step_batched_dpsync_loopback(arr, n, ctypes.byref(cfg), wsp, need.value, P,
+                                                           st.cuda_stream, ctypes.byref(nbytes))
+        else:
+            rc = _lib().dion2_step_batched_dpsync(arr, n, ctypes.byref(cfg), self._ws[0].data_ptr(), need.value,
+                                                  _nccl_comm_ptr(self.group), P, self.rank, st.cuda_stream,
+                                                  ctypes.byref(nbytes))
+        if rc:
+            raise Dion2Error(rc, "dion2_step_batched_dpsync")
         self.last_comm_bytes = nbytes.value

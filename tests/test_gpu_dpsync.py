@@ -1,0 +1,80 @@
+"""Compressed DP-sync on the GPU (-m gpu): replicas with local gradients, only M[K] averaged
+(paper 3.2).  Checked against the oracle's replica model, which is itself pinned
+(test_oracle_pins.py) to equal full gradient synchronisation."""
+import os
+import socket
+
+import numpy as np
+import pytest
+import torch
+
+import oracle as O
+from synth import gen_grad, gen_w0
+from paper_2512_16928_b200 import Dion2Error
+from paper_2512_16928_b200 import dion2 as D
+
+pytestmark = pytest.mark.gpu
+
+SHAPES = [(256, 512), (512, 256), (384, 640), (1024, 512)]
+
+
+def _run(world, precision, tol, steps=3, mode="loopback"):
+    seed, alpha = 21, 0.25
+    W0 = [gen_w0(m, n, 0, i) for i, (m, n) in enumerate(SHAPES)]
+    reps = world if mode == "loopback" else 1
+    Wg = [[torch.from_numpy(w).cuda() for w in W0] for _ in range(reps)]
+    Mg = [[torch.zeros(m, n, device="cuda") for (m, n) in SHAPES] for _ in range(reps)]
+    Wr = [[w.astype(np.float64) for w in W0] for _ in range(world)]
+    Mr = [[np.zeros((m, n)) for (m, n) in SHAPES] for _ in range(world)]
+    opt = D.Dion2DpSync(loopback_world=world if mode == "loopback" else 0, alpha=alpha, precision=precision,
+                        seed=seed)
+    for t in range(steps):
+        G = [[gen_grad(m, n, 100 + r, i, t) for i, (m, n) in enumerate(SHAPES)] for r in range(world)]
+        if mode == "loopback":
+            opt.step(Wg, Mg, [[torch.from_numpy(g).cuda() for g in G[r]] for r in range(world)], step=t)
+        else:
+            opt.step(Wg[0], Mg[0], [torch.from_numpy(g).cuda() for g in G[0]], step=t)
+        cfg = O.OracleConfig(alpha=float(np.float32(alpha)), select="random", seed=seed, step=t)
+        for i in range(len(SHAPES)):
+            O.dion2_step_dpsync([Wr[r][i] for r in range(world)], [Mr[r][i] for r in range(world)],
+                                [G[r][i].astype(np.float64) for r in range(world)], cfg, matrix_id=i)
+    torch.cuda.synchronize()
+    for i in range(len(SHAPES)):
+        w0 = W0[i].astype(np.float64)
+        for r in range(reps):
+            assert torch.equal(Wg[r][i], Wg[0][i])          # replicas stay bit-identical
+            wg = Wg[r][i].cpu().double().numpy()
+            err = np.linalg.norm((wg - w0) - (Wr[r][i] - w0)) / np.linalg.norm(Wr[r][i] - w0)
+            assert err <= tol, (i, r, err)
+            mg = Mg[r][i].cpu().double().numpy()
+            assert np.abs(mg - Mr[r][i]).max() <= 1e-5 * np.abs(Mr[r][i]).max()
+    return opt
+
+
+@pytest.mark.parametrize("world", [2, 3])
+@pytest.mark.parametrize("precision,tol", [("bf16", 2e-2), ("fp32", 1e-5)])
+def test_dpsync_loopback(world, precision, tol):
+    opt = _run(world, precision, tol)
+    k_o = sum(O.selected_bytes(m, n, 0.25, O.AXIS_AUTO, 4) for (m, n) in SHAPES)
+    assert opt.last_comm_bytes == int(2.0 * (world - 1) / world * k_o)   # ~alpha of full gradient sync
+
+
+def test_dpsync_nccl_single_rank():
+    import torch.distributed as dist
+    s = socket.socket()
+    s.bind(("127.0.0.1", 0))
+    os.environ["MASTER_ADDR"] = "127.0.0.1"
+    os.environ["MASTER_PORT"] = str(s.getsockname()[1])
+    s.close()
+    dist.init_process_group("nccl", rank=0, world_size=1, device_id=torch.device("cuda", 0))
+    try:
+        _run(1, "bf16", 2e-2, mode="nccl")
+    finally:
+        dist.destroy_process_group()
+
+
+def test_dpsync_requires_random_selection():
+    mk = lambda: [[torch.zeros(64, 64, device="cuda")] for _ in range(2)]  # noqa: E731
+    opt = D.Dion2DpSync(loopback_world=2, select="l1")
+    with pytest.raises(Dion2Error):
+        opt.step(mk(), mk(), mk())

@@ -355,3 +355,30 @@ def test_dion2_step_random_uses_the_keyed_subset():
     K, Omat, ax = O.dion2_step(W, M, G, cfg, matrix_id=3)
     assert ax == O.AXIS_ROWS and np.array_equal(K, O.select_random(m, 12, 9, 3, 4))
     np.testing.assert_allclose(Omat, O.newton_schulz_auto(G[K]), atol=1e-14)
+
+
+# ----------------------------------------------------------------------------- compressed DP-sync
+
+@pytest.mark.parametrize("shape", [(48, 96), (96, 48)])
+def test_compressed_dpsync_equals_full_gradient_sync(shape):
+    """syncing only M[K,:] (random K) "suffices to compute the correct parameter
+    update, just as full DP-sync would": over 20 steps the replicas' W stay identical and equal
+    the trajectory of a single optimizer fed the AVERAGED gradient."""
+    m, n = shape
+    P, steps = 3, 20
+    W0 = gen_w0(m, n).astype(np.float64)
+    Ws = [W0.copy() for _ in range(P)]
+    Ms = [np.zeros((m, n)) for _ in range(P)]
+    Wf, Mf = W0.copy(), np.zeros((m, n))
+    for t in range(steps):
+        cfg = O.OracleConfig(alpha=0.25, select="random", seed=17, step=t)
+        Gs = [gen_grad(m, n, r, 0, t).astype(np.float64) for r in range(P)]
+        K = O.dion2_step_dpsync(Ws, Ms, Gs, cfg, matrix_id=2)
+        Kf, _, _ = O.dion2_step(Wf, Mf, sum(Gs) / P, cfg, matrix_id=2)
+        assert np.array_equal(K, Kf)
+    for r in range(P):
+        assert np.array_equal(Ws[r], Ws[0])
+    assert np.abs(Ws[0] - Wf).max() < 1e-12
+    # the momenta diverge across replicas, but their mean is the full-sync momentum
+    assert not np.array_equal(Ms[0], Ms[1])
+    assert np.abs(sum(Ms) / P - Mf).max() < 1e-12 * np.abs(Mf).max()
