@@ -340,7 +340,10 @@ int build_device_plan(Plan& P, const dion2_matrix* mats, const dion2_config* c, 
   for (int t = 0; t < P.ns_steps; ++t) {
     const float a = c->ns_coeffs[t][0], b = c->ns_coeffs[t][1], cc = c->ns_coeffs[t][2];
     for (int ph = PH_GRAM; ph <= PH_APPLY; ++ph) {
-      const bool pair = P.bf16_ns && (pair_mode == 2 || (pair_mode == 1 && ph == PH_GRAM));
+      const bool pair = P.bf16_ns && (pair_mode == 2 || (pair_mode == 1 && ph != PH_APPLY));
+      // gram and poly outputs are symmetric: the pair kernel computes upper-triangle tiles
+      // only and mirrors them (DION2_NS_SYM=0 disables)
+      const bool sym = pair && ph != PH_APPLY && !(getenv("DION2_NS_SYM") && atoi(getenv("DION2_NS_SYM")) == 0);
       const int MT = pair ? 256 : 128;
       // bucket groups by BN class
       std::vector<int> by_bn[2];
@@ -363,6 +366,7 @@ int build_device_plan(Plan& P, const dion2_matrix* mats, const dion2_config* c, 
           // gram: A = s^2 X X^T; poly: C = a I + b A + c A A^T (consistent bf16 A);
           // apply: X' = s C X (the linear term a X is folded into C: no epilogue read)
           np.diag = 0.f;
+          np.sym = sym ? 1 : 0;
           if (ph == PH_GRAM) { np.cacc = 1.f; np.cC = 0.f; np.scale_sel = t == 0 ? 2 : 0; np.b_kmajor = 1; }
           if (ph == PH_POLY) { np.cacc = cc; np.cC = b; np.diag = a; np.scale_sel = 0; np.b_kmajor = 1; }
           if (ph == PH_APPLY) { np.cacc = 1.f; np.cC = 0.f; np.scale_sel = t == 0 ? 1 : 0; np.b_kmajor = 0; }
@@ -415,7 +419,7 @@ int build_device_plan(Plan& P, const dion2_matrix* mats, const dion2_config* c, 
                 !make_map(&L.tc.mapD[j], G.out, G.out_ld, g.p_pad, g.count, 32, 32, CU_TENSOR_MAP_SWIZZLE_64B))
               return DION2_ECUDA;
             G.tile_base = tiles;
-            tiles += G.count * G.m_tiles * G.n_tiles;
+            tiles += G.count * (sym ? G.m_tiles * (G.m_tiles + 1) / 2 : G.m_tiles * G.n_tiles);
           }
           np.total_tiles = tiles;
           if (P.bf16_ns) {

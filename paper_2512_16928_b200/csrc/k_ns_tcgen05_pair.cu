@@ -40,9 +40,24 @@ __device__ __forceinline__ TileCoord decode_tile(const NsParams& p, int t) {
     if (i < p.ngroups && t >= p.g[i].tile_base) g = i;
   const NsGroup& G = p.g[g];
   const int local = t - G.tile_base;
-  const int per = G.m_tiles * G.n_tiles;
   TileCoord c;
   c.group = g;
+  if (p.sym) {
+    // symmetric output (gram A = X X^T, poly C = aI + bA + cA^2): upper-triangle tiles only,
+    // row tm holds tiles tn = tm .. T-1
+    const int T = G.m_tiles;
+    const int per = T * (T + 1) / 2;
+    c.z = local / per;
+    int r = local % per, tm = 0;
+    while (r >= T - tm) {
+      r -= T - tm;
+      ++tm;
+    }
+    c.tm = tm;
+    c.tn = tm + r;
+    return c;
+  }
+  const int per = G.m_tiles * G.n_tiles;
   c.z = local / per;
   const int r = local % per;
   c.tm = r / G.n_tiles;
@@ -57,7 +72,7 @@ __device__ __forceinline__ uint32_t pack_bf16x2(float lo, float hi) {
 
 }  // namespace
 
-constexpr int ns_pair_smem_bytes() { return 1024 + kStagesPair * (int)kStage + 1024 + 4 * 2 * 2048; }
+constexpr int ns_pair_smem_bytes() { return 1024 + kStagesPair * (int)kStage + 1024 + 4 * 4 * 2048; }
 
 __global__ void __cluster_dims__(2, 1, 1) __launch_bounds__(192, 1)
     k_ns_gemm_tc_pair(const __grid_constant__ NsTcParams P) {
@@ -208,25 +223,44 @@ __global__ void __cluster_dims__(2, 1, 1) __launch_bounds__(192, 1)
         float o[32];
 #pragma unroll
         for (int e = 0; e < 32; ++e) o[e] = ca * v[e] + cc * cv[e] + (e == dcol ? dterm : 0.f);
-        uint8_t* buf = stage_base + (lg * 2 + sbuf) * 2048;
-        if (lane == 0) bulk_wait_read<1>();
+        // 4 staging buffers per warp (SWIZZLE_64B layout: 16-B chunk q of row r at
+        // q ^ ((r >> 1) & 3)); a buffer is rewritten once the store 4 commits back has read it
+        const bool mirror = p.sym && c.tm != c.tn;
+        uint8_t* buf = stage_base + (lg * 4 + sbuf) * 2048;
+        if (lane == 0) bulk_wait_read<3>();
         __syncwarp();
+        uint32_t pk[16];
 #pragma unroll
-        for (int q = 0; q < 4; ++q) {
-          uint4 u;
-          u.x = pack_bf16x2(o[q * 8 + 0], o[q * 8 + 1]);
-          u.y = pack_bf16x2(o[q * 8 + 2], o[q * 8 + 3]);
-          u.z = pack_bf16x2(o[q * 8 + 4], o[q * 8 + 5]);
-          u.w = pack_bf16x2(o[q * 8 + 6], o[q * 8 + 7]);
-          *reinterpret_cast<uint4*>(buf + lane * 64 + ((q ^ ((lane >> 1) & 3)) << 4)) = u;
+        for (int q = 0; q < 16; ++q) pk[q] = pack_bf16x2(o[2 * q], o[2 * q + 1]);
+#pragma unroll
+        for (int q = 0; q < 4; ++q)
+          *reinterpret_cast<uint4*>(buf + lane * 64 + ((q ^ ((lane >> 1) & 3)) << 4)) =
+              make_uint4(pk[4 * q], pk[4 * q + 1], pk[4 * q + 2], pk[4 * q + 3]);
+        uint8_t* tbuf = stage_base + (lg * 4 + ((sbuf + 1) & 3)) * 2048;
+        if (mirror) {
+          // the transposed 32 x 32 chunk: element (row e, col lane) = o[e]; tbuf was used by
+          // the 3rd most recent store (the current one is not issued yet)
+          if (lane == 0) bulk_wait_read<2>();
+          __syncwarp();
+#pragma unroll
+          for (int e = 0; e < 32; ++e) {
+            const __nv_bfloat16 h = __float2bfloat16_rn(o[e]);
+            *reinterpret_cast<__nv_bfloat16*>(tbuf + e * 64 + ((((lane >> 3) ^ ((e >> 1) & 3))) << 4) +
+                                              (lane & 7) * 2) = h;
+          }
         }
         fence_proxy_async_smem();
         __syncwarp();
         if (lane == 0) {
           tma_store_3d(&P.mapD[c.group], buf, c.tn * 256 + cc32 * 32, c.tm * 256 + (int)rank * 128 + lg * 32, c.z);
           bulk_commit();
+          if (mirror) {
+            tma_store_3d(&P.mapD[c.group], tbuf, c.tm * 256 + (int)rank * 128 + lg * 32, c.tn * 256 + cc32 * 32,
+                         c.z);
+            bulk_commit();
+          }
         }
-        sbuf ^= 1;
+        sbuf = (sbuf + (mirror ? 2 : 1)) & 3;
       }
       tc_fence_before();
       __syncwarp();

@@ -84,6 +84,7 @@ struct NsParams {
   float cacc, cC;
   float diag;                // added on the global diagonal (poly: C = a*I + b*A + c*A^2)
   int scale_sel;             // 0: oscale = 1; 1: s; 2: s^2
+  int sym;                   // symmetric output: upper-triangle tiles only, mirrored by the epilogue (pair kernel)
   const float* ns_scale_all; // [n_mats][2]
   int b_kmajor;
 };
