@@ -279,11 +279,22 @@ def run_ours(args):
     if rc != 0:
         raise RuntimeError(f"status {rc} (matrix {bad})")
 
-    # per-phase device time (CUDA events on the launching stream around every launch)
+    # per-phase device time (CUDA events on the launching stream around every launch), with
+    # the chunked two-stream pipeline disabled so every kernel is timed in isolation
+    prev_chunks = os.environ.get("DION2_CHUNKS")
+    os.environ["DION2_CHUNKS"] = "1"
+    opt_iso = make_opt(args.alpha)
+    time_steps(opt_iso, Ws, Ms, Gs, 0, 1, None)
     set_phase_timing(True)
-    ms_timed = time_steps(opt, Ws, Ms, Gs, args.steps, 0, None)
+    ms_timed = time_steps(opt_iso, Ws, Ms, Gs, args.steps, 0, None)
     phases = get_phase_times()
     set_phase_timing(False)
+    del opt_iso
+    if prev_chunks is None:
+        del os.environ["DION2_CHUNKS"]
+    else:
+        os.environ["DION2_CHUNKS"] = prev_chunks
+    torch.cuda.empty_cache()
 
     peaks, peak_src = load_peaks()
     ns_flops, byts = work_model(shapes, args.alpha)
@@ -385,7 +396,9 @@ def run_ours(args):
             "ns_tflops": ns_tflops,
             "ns_frac_bf16_burst": ns_tflops / peaks["bf16_tflops"],
             "ns_frac_bf16_sustained": ns_tflops / peaks["bf16_tflops_sustained"],
-            "ms_per_step_with_phase_events": ms_timed,
+            "ms_per_step_unpipelined_with_phase_events": ms_timed,
+            "phases_note": "per-kernel times from a separate K-step pass with the chunked pipeline off "
+                           "(DION2_CHUNKS=1) so kernels do not overlap; value uses the default pipelined step",
             "phases": per_phase,
             "roofline": roof,
             "cpu_baseline": cpu,
