@@ -98,15 +98,33 @@ __global__ void __launch_bounds__(kSelectThreads) k_topk_select(const MatDesc* _
       if ((key & mask) == prefix) atomicAdd(&hist[(key >> shift) & 255u], 1u);
     }
     __syncthreads();
-    if (tid == 0) {
-      uint32_t above = 0;
-      int b = 255;
-      for (; b > 0; --b) {
-        if (above + hist[b] >= remaining) break;
-        above += hist[b];
+    if (tid < 32) {
+      // warp-parallel scan from the top bin down: lane l owns bins 255-8l .. 248-8l
+      uint32_t c[8], tot = 0;
+#pragma unroll
+      for (int e = 0; e < 8; ++e) {
+        c[e] = hist[255 - 8 * tid - e];
+        tot += c[e];
       }
-      s_prefix = prefix | ((uint32_t)b << shift);
-      s_remaining = remaining - above;
+      uint32_t incl = tot;  // inclusive prefix over lanes (higher bins first)
+#pragma unroll
+      for (int o = 1; o < 32; o <<= 1) {
+        const uint32_t y = __shfl_up_sync(0xffffffffu, incl, o);
+        if (tid >= o) incl += y;
+      }
+      const uint32_t excl = incl - tot;
+      // the lane whose range contains the k-th largest key
+      const unsigned hit = __ballot_sync(0xffffffffu, excl < remaining && incl >= remaining);
+      if (tid == __ffs(hit) - 1) {
+        uint32_t above = excl;
+        int e = 0;
+        for (; e < 7; ++e) {
+          if (above + c[e] >= remaining) break;
+          above += c[e];
+        }
+        s_prefix = prefix | ((uint32_t)(255 - 8 * tid - e) << shift);
+        s_remaining = remaining - above;
+      }
     }
     __syncthreads();
     prefix = s_prefix;
