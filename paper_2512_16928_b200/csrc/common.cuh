@@ -34,7 +34,7 @@ struct MatDesc {
   float update_scale;  // sqrt(fan-out / fan-in) (times eta at launch)
   // workspace slices
   float* scores;          // [d]
-  float* col_partials;    // [ceil(rows/64)][cols]  (cols mode)
+  float* col_partials;    // [rowblocks][cols]  (cols mode)
   int32_t* sel;           // [k] ascending
   float* sumsq_partials;  // [n_gather_tiles]
   float* ns_scale;        // [2] = { s, s^2 },  s = 1 / (||X||_F + eps)
@@ -47,7 +47,7 @@ struct MatDesc {
   int32_t n_sumsq;         // number of sum-of-squares partials K3 writes
   int32_t scores_final;    // select reads `scores` as final (distributed step: combined across ranks)
   int32_t mid;             // matrix id in the batch (random-selection key)
-  int32_t rowblocks;      // ceil(rows/64) (cols mode partials)
+  int32_t rowblocks;      // ceil(rows / kColRowBlock) (cols mode partials)
 };
 
 // ----------------------------------------------------------------------------- small helpers

@@ -158,7 +158,7 @@ int build_layout(Plan& P, const dion2_matrix* mats, int n, const dion2_config* c
     q.q_pad = (int)align_up(q.q, 256);
     if (c->scale_mode == 0) q.fan_sqrt = (float)std::sqrt((double)rows / (double)cols);  // Alg. 1 l.6
     else q.fan_sqrt = (float)std::sqrt((double)q.sr / (double)q.sc);
-    q.rowblocks = (int)ceil_div(rows, 64);
+    q.rowblocks = (int)ceil_div(rows, kColRowBlock);
     // gather tiles cover the padded extent of S (wide(S_pad) = X_pad) so K3 also
     // rewrites X's zero padding every step
     q.sa_pad = q.transposed ? q.q_pad : q.p_pad;

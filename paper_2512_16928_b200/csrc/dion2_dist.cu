@@ -184,7 +184,7 @@ int resolve(DistPlan& D, const dion2_shard* sh, int n, const dion2_config* c, in
   D.off_sumsq_local = take(4 * (size_t)n);
   D.off_sumsq_all = take(4 * (size_t)n * world);
   for (auto& q : D.dm) {
-    q.off_partials = q.axis == DION2_AXIS_COLS ? take(4 * (size_t)ceil_div(q.srows, 64) * q.scols) : 0;
+    q.off_partials = q.axis == DION2_AXIS_COLS ? take(4 * (size_t)ceil_div(q.srows, kColRowBlock) * q.scols) : 0;
     q.off_sel = take(4 * (size_t)q.k);
     q.off_sumsq = take(4 * (size_t)q.n_sumsq);
   }
@@ -278,7 +278,7 @@ int build_tables(DistPlan& D, const dion2_config* c, void* ws) {
     d.X0 = at(ws, D.off_send + D.sdispl[q.owner] + q.soff);
     d.X1 = at(ws, D.off_orecv + D.sdispl[q.owner] + q.soff);
     d.final_in_x1 = 1;
-    d.rowblocks = (int)ceil_div(q.srows, 64);
+    d.rowblocks = (int)ceil_div(q.srows, kColRowBlock);
     d.mid = j;
     d.path = q.path;
     d.n_sumsq = q.n_sumsq;

@@ -98,11 +98,11 @@ __global__ void __launch_bounds__(256) k_momentum_score_rows(const MatDesc* __re
 }
 
 // ------------------------------------------------------------------ cols mode
-// Block = 64 rows x 256 columns; thread (ty in [0,4), tx in [0,64)) owns 4
+// Block = kColRB (256) rows x 256 columns; thread (ty in [0,4), tx in [0,64)) owns 4
 // column slots and rows ty, ty+4, ...; a fixed-order smem reduce over ty gives
 // one partial per (row block, column).  K2 sums the partials in row-block
 // order: no float atomics anywhere.
-constexpr int kColRB = 64;
+constexpr int kColRB = kColRowBlock;
 constexpr int kColCB = 256;
 
 template <bool kBf16G>

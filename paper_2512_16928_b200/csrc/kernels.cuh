@@ -5,6 +5,7 @@
 namespace dion2 {
 
 // ---------------- K1 momentum + l1 score (k_momentum_score.cu)
+constexpr int kColRowBlock = 256;  // rows per column-mode partial-sum block
 __global__ void k_momentum_score_rows(const MatDesc* __restrict__ mats, const int32_t* __restrict__ row_mats,
                                       const int64_t* __restrict__ row_prefix, int n_row_mats, int64_t total_rows);
 __global__ void k_momentum_score_cols(const MatDesc* __restrict__ mats, const int32_t* __restrict__ col_mats,
