@@ -41,7 +41,7 @@
 extern "C" {
 #endif
 
-#define DION2_ABI_VERSION 1
+#define DION2_ABI_VERSION 2
 #define DION2_MAX_NS_STEPS 16
 
 typedef enum {
@@ -74,6 +74,12 @@ typedef struct {
   int32_t* sel_out;    /* optional [k] int32: the selected indices, ascending (NULL = not written) */
   float* O_out;        /* optional fp32 copy of O in natural orientation: [k x cols] (rows mode) or
                           [rows x k] (cols mode), dense row-major (NULL = not written) */
+  int32_t m_transposed; /* 0: M has W's layout.  1: M is stored TRANSPOSED, [cols x ldm] row-major
+                           (element (i, j) of M at M[j*ldm + i]); only for matrices whose resolved
+                           selection axis is COLS, where it turns the column gather of M[:, K] into a
+                           contiguous row gather (DION2_EUNSUPPORTED otherwise) */
+  int32_t reserved;     /* must be 0 */
+  int64_t ldm;          /* row stride of the transposed M (>= rows); ignored when m_transposed = 0 */
 } dion2_matrix;
 
 /* Hyper-parameters of Alg. 1.  Fill with dion2_config_init() first. */

@@ -47,6 +47,8 @@ struct MatDesc {
   int32_t n_sumsq;         // number of sum-of-squares partials K3 writes
   int32_t scores_final;    // select reads `scores` as final (distributed step: combined across ranks)
   int32_t mid;             // matrix id in the batch (random-selection key)
+  int32_t mt;              // M stored transposed ([cols x ldm], cols mode only): K3 gathers rows of M^T
+  int64_t ldm;             // row stride of the transposed M
   int32_t rowblocks;      // ceil(rows / kColRowBlock) (cols mode partials)
 };
 

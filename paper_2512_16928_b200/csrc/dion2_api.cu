@@ -99,6 +99,8 @@ int validate_shape(const dion2_matrix& m, bool need_ptrs) {
   if (m.rows < 1 || m.cols < 1 || m.ld < m.cols) return DION2_EINVAL_SHAPE;
   if (m.rows > (1ll << 31) - 1 || m.cols > (1ll << 31) - 1) return DION2_EINVAL_SHAPE;
   if (need_ptrs && (!m.W || !m.M || !m.G)) return DION2_EINVAL_SHAPE;
+  if (m.reserved != 0 || (m.m_transposed != 0 && m.m_transposed != 1)) return DION2_EINVAL_SHAPE;
+  if (m.m_transposed && m.ldm < m.rows) return DION2_EINVAL_SHAPE;
   return DION2_OK;
 }
 
@@ -167,9 +169,11 @@ int build_layout(Plan& P, const dion2_matrix* mats, int n, const dion2_config* c
     if (axis == DION2_AXIS_ROWS && !q.transposed && P.bf16_ns) q.path = 1;
     else if (axis == DION2_AXIS_COLS && q.transposed && P.bf16_ns && q.k <= kMaxColKFast) q.path = 2;
     else q.path = 0;
+    q.mt = m.m_transposed ? 1 : 0;
+    if (q.mt && q.path != 2) return DION2_EUNSUPPORTED;  // transposed M: column mode, bf16, k <= 1024, k <= rows
     q.ga = q.path == 0 ? (int)ceil_div(q.sa_pad, kTileA) : 0;
     q.gb = q.path == 0 ? (int)ceil_div(q.sb_pad, kTileB) : 0;
-    q.n_sumsq = q.path == 0 ? q.ga * q.gb : (q.path == 1 ? q.p_pad : q.q_pad / 32);
+    q.n_sumsq = q.path == 0 ? q.ga * q.gb : ((q.path == 1 || q.mt) ? q.p_pad : q.q_pad / 32);
     auto key = std::make_pair(q.p_pad, q.q_pad);
     auto it = gidx.find(key);
     if (it == gidx.end()) {
@@ -200,9 +204,12 @@ int build_layout(Plan& P, const dion2_matrix* mats, int n, const dion2_config* c
   P.off_rowprefix = take(8 * (size_t)n);
   P.off_colmats = take(4 * (size_t)n);
   P.off_colprefix = take(8 * (size_t)n);
+  P.off_mtmats = take(4 * (size_t)n);
+  P.off_mtprefix = take(8 * (size_t)n);
   P.off_gprefix = take(4 * (size_t)n);
   for (int l = 0; l < 2; ++l) {
-    P.off_fl_mats[l] = take(4 * (size_t)n);
+    P.off_flg_mats[l] = take(4 * (size_t)n);
+    P.off_fls_mats[l] = take(4 * (size_t)n);
     P.off_fl_gprefix[l] = take(4 * (size_t)n);
     P.off_fl_sprefix[l] = take(4 * (size_t)n);
   }
@@ -242,7 +249,9 @@ int build_device_plan(Plan& P, const dion2_matrix* mats, const dion2_config* c, 
   std::vector<int32_t> rowmats, colmats;
   std::vector<int64_t> rowprefix, colprefix;
   std::vector<int32_t> gprefix(n);
-  std::vector<int32_t> fl_mats[2], fl_gp[2], fl_sp[2];
+  std::vector<int32_t> flg_mats[2], fls_mats[2], fl_gp[2], fl_sp[2], mtmats;
+  std::vector<int64_t> mtprefix;
+  int64_t mt_acc = 0;
   P.fl_gunits[0] = P.fl_gunits[1] = P.fl_sunits[0] = P.fl_sunits[1] = 0;
   P.fl_maxk = 0;
   P.fl_maxn = 0;
@@ -278,18 +287,21 @@ int build_device_plan(Plan& P, const dion2_matrix* mats, const dion2_config* c, 
     d.mid = i;
     d.path = q.path;
     d.n_sumsq = q.n_sumsq;
+    d.mt = q.mt;
+    d.ldm = q.mt ? mats[i].ldm : 0;
     gprefix[i] = gt_acc;
     gt_acc += q.ga * q.gb;
     if (q.path > 0) {
-      const int l = q.path - 1;
-      const int gu = l == 0 ? q.p_pad : q.q_pad / 32;
-      const int su = l == 0 ? q.k : q.q_pad / 32;
-      fl_mats[l].push_back(i);
-      fl_gp[l].push_back(P.fl_gunits[l]);
-      fl_sp[l].push_back(P.fl_sunits[l]);
-      P.fl_gunits[l] += gu;
-      P.fl_sunits[l] += su;
-      if (l == 1) {
+      // gather list: rows streaming (path 1, or transposed-M columns = rows of M^T), else cols
+      const int lg = (q.path == 1 || q.mt) ? 0 : 1;
+      const int ls = q.path - 1;
+      flg_mats[lg].push_back(i);
+      fl_gp[lg].push_back(P.fl_gunits[lg]);
+      P.fl_gunits[lg] += lg == 0 ? q.p_pad : q.q_pad / 32;
+      fls_mats[ls].push_back(i);
+      fl_sp[ls].push_back(P.fl_sunits[ls]);
+      P.fl_sunits[ls] += ls == 0 ? q.k : q.q_pad / 32;
+      if (lg == 1 || ls == 1) {
         P.fl_maxk = std::max(P.fl_maxk, q.k);
         P.fl_maxn = std::max<int64_t>(P.fl_maxn, mats[i].cols);
       }
@@ -298,6 +310,10 @@ int build_device_plan(Plan& P, const dion2_matrix* mats, const dion2_config* c, 
       rowmats.push_back(i);
       rowprefix.push_back(rows_acc);
       rows_acc += mats[i].rows;
+    } else if (q.mt) {
+      mtmats.push_back(i);
+      mtprefix.push_back(mt_acc);
+      mt_acc += (int64_t)q.rowblocks * ceil_div(mats[i].cols, 32);
     } else {
       colmats.push_back(i);
       colprefix.push_back(ctiles_acc);
@@ -310,12 +326,22 @@ int build_device_plan(Plan& P, const dion2_matrix* mats, const dion2_config* c, 
   P.n_col_mats = (int)colmats.size();
   P.total_gather_tiles = gt_acc;
   for (int l = 0; l < 2; ++l) {
-    P.fl_n[l] = (int)fl_mats[l].size();
-    if (P.fl_n[l]) {
-      memcpy(H(P.off_fl_mats[l]), fl_mats[l].data(), 4 * fl_mats[l].size());
+    P.fl_gn[l] = (int)flg_mats[l].size();
+    P.fl_sn[l] = (int)fls_mats[l].size();
+    if (P.fl_gn[l]) {
+      memcpy(H(P.off_flg_mats[l]), flg_mats[l].data(), 4 * flg_mats[l].size());
       memcpy(H(P.off_fl_gprefix[l]), fl_gp[l].data(), 4 * fl_gp[l].size());
+    }
+    if (P.fl_sn[l]) {
+      memcpy(H(P.off_fls_mats[l]), fls_mats[l].data(), 4 * fls_mats[l].size());
       memcpy(H(P.off_fl_sprefix[l]), fl_sp[l].data(), 4 * fl_sp[l].size());
     }
+  }
+  P.n_mt_mats = (int)mtmats.size();
+  P.total_mt_tiles = mt_acc;
+  if (!mtmats.empty()) {
+    memcpy(H(P.off_mtmats), mtmats.data(), 4 * mtmats.size());
+    memcpy(H(P.off_mtprefix), mtprefix.data(), 8 * mtprefix.size());
   }
   if (!rowmats.empty()) {
     memcpy(H(P.off_rowmats), rowmats.data(), 4 * rowmats.size());
@@ -501,7 +527,8 @@ int refresh_tables(Plan& P, const dion2_matrix* mats, const dion2_config* c, cud
     D[i].O_out = mats[i].O_out;
     const size_t gel = c->grad_dtype == DION2_DT_BF16 ? 2 : 4;
     const bool al = ((uintptr_t)mats[i].W % 16 == 0) && ((uintptr_t)mats[i].M % 16 == 0) &&
-                    ((uintptr_t)mats[i].G % (gel == 4 ? 16 : 8) == 0) && (mats[i].ld % 4 == 0);
+                    ((uintptr_t)mats[i].G % (gel == 4 ? 16 : 8) == 0) && (mats[i].ld % 4 == 0) &&
+                    (!mats[i].m_transposed || mats[i].ldm % 4 == 0);
     D[i].vec4 = al ? 1 : 0;
   }
   if (upload &&
@@ -554,6 +581,14 @@ void stage_k1_select(Plan& P, const dion2_config* c, void* ws, int32_t* status, 
                                                  P.total_col_tiles);
     L.end();
   }
+  if (P.n_mt_mats) {
+    L.begin(PH_K1);
+    const int blocks = stream_grid(P.total_mt_tiles, 8, persistent);
+    k_momentum_score_cols_mt<<<blocks, 256, 0, s>>>(dmats, (const int32_t*)tab(P, P.off_mtmats),
+                                                    (const int64_t*)tab(P, P.off_mtprefix), P.n_mt_mats,
+                                                    P.total_mt_tiles);
+    L.end();
+  }
   L.begin(PH_SELECT);
   k_topk_select<<<n, kSelectThreads, 4 * P.max_d, s>>>(dmats, bad, status, c->select == DION2_SELECT_RANDOM, c->seed,
                                                        c->step);
@@ -571,18 +606,18 @@ void stage_gather(Plan& P, const dion2_config* c, void* ws, Launcher& L, cudaStr
                         (const int32_t*)tab(P, P.off_gprefix), n, P.total_gather_tiles, bad, 1, c->mu);
     L.end();
   }
-  if (P.fl_n[0]) {
+  if (P.fl_gn[0]) {
     L.begin(PH_GATHER_ROWS);
     launch_gather_rows(stream_grid(ceil_div(P.fl_gunits[0], 8), 8, persistent), s, dmats,
-                       (const int32_t*)tab(P, P.off_fl_mats[0]), (const int32_t*)tab(P, P.off_fl_gprefix[0]),
-                       P.fl_n[0], P.fl_gunits[0], bad, c->mu);
+                       (const int32_t*)tab(P, P.off_flg_mats[0]), (const int32_t*)tab(P, P.off_fl_gprefix[0]),
+                       P.fl_gn[0], P.fl_gunits[0], bad, c->mu);
     L.end();
   }
-  if (P.fl_n[1]) {
+  if (P.fl_gn[1]) {
     L.begin(PH_GATHER_COLS);
     launch_gather_cols_t(stream_grid(P.fl_gunits[1], 6, persistent), P.fl_maxk, P.fl_maxn, s, dmats,
-                         (const int32_t*)tab(P, P.off_fl_mats[1]), (const int32_t*)tab(P, P.off_fl_gprefix[1]),
-                         P.fl_n[1], P.fl_gunits[1], bad, c->mu);
+                         (const int32_t*)tab(P, P.off_flg_mats[1]), (const int32_t*)tab(P, P.off_fl_gprefix[1]),
+                         P.fl_gn[1], P.fl_gunits[1], bad, c->mu);
     L.end();
   }
 }
@@ -599,18 +634,18 @@ void stage_post(Plan& P, const dion2_matrix* mats, const dion2_config* c, void* 
                           (const int32_t*)tab(P, P.off_gprefix), n, P.total_gather_tiles, bad, c->lr);
     L.end();
   }
-  if (P.fl_n[0]) {
+  if (P.fl_sn[0]) {
     L.begin(PH_SCATTER_ROWS);
     launch_scatter_rows(stream_grid(ceil_div(P.fl_sunits[0], 8), 8, persistent), s, dmats,
-                        (const int32_t*)tab(P, P.off_fl_mats[0]), (const int32_t*)tab(P, P.off_fl_sprefix[0]),
-                        P.fl_n[0], P.fl_sunits[0], bad, c->lr);
+                        (const int32_t*)tab(P, P.off_fls_mats[0]), (const int32_t*)tab(P, P.off_fl_sprefix[0]),
+                        P.fl_sn[0], P.fl_sunits[0], bad, c->lr);
     L.end();
   }
-  if (P.fl_n[1]) {
+  if (P.fl_sn[1]) {
     L.begin(PH_SCATTER_COLS);
     launch_scatter_cols_t(stream_grid(P.fl_sunits[1], 6, persistent), P.fl_maxk, P.fl_maxn, s, dmats,
-                          (const int32_t*)tab(P, P.off_fl_mats[1]), (const int32_t*)tab(P, P.off_fl_sprefix[1]),
-                          P.fl_n[1], P.fl_sunits[1], bad, c->lr);
+                          (const int32_t*)tab(P, P.off_fls_mats[1]), (const int32_t*)tab(P, P.off_fl_sprefix[1]),
+                          P.fl_sn[1], P.fl_sunits[1], bad, c->lr);
     L.end();
   }
   if (c->decay_mode == 1) {

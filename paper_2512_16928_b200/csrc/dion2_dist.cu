@@ -700,6 +700,8 @@ std::map<std::string, std::unique_ptr<DpPlan>> g_dp_plans;
 int dp_layout(DpPlan& D, const dion2_matrix* mats, int n, const dion2_config* c, int world) {
   if (c->select != DION2_SELECT_RANDOM) return DION2_EUNSUPPORTED;  // l1 scores need the full momentum
   if (world < 1) return DION2_EINVAL_SHAPE;
+  for (int i = 0; i < n; ++i)
+    if (mats[i].m_transposed) return DION2_EUNSUPPORTED;
   D.world = world;
   int rc = build_layout(D.P, mats, n, c);
   if (rc) return rc;

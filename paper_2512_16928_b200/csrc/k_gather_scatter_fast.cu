@@ -54,9 +54,10 @@ __global__ void __launch_bounds__(256) k_gather_rows(const MatDesc* __restrict__
     __nv_bfloat16* xrow = reinterpret_cast<__nv_bfloat16*>(md.X0) + (int64_t)r * md.q_pad;
     float ss = 0.f;
     if (r < md.k) {
-      float* mrow = md.M + (int64_t)md.sel[r] * md.ld;
+      // rows mode: row sel[r] of M; cols mode with transposed M: row sel[r] of M^T (= X row r)
+      float* mrow = md.M + (int64_t)md.sel[r] * (md.mt ? md.ldm : md.ld);
       const float f = bad[mi] ? 1.f : mu;
-      const int n = (int)md.cols;
+      const int n = (int)(md.mt ? md.rows : md.cols);
       if (md.vec4) {
         const int n4 = n >> 2;
         float4* m4 = reinterpret_cast<float4*>(mrow);

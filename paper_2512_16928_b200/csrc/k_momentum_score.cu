@@ -183,4 +183,69 @@ __global__ void __launch_bounds__(256) k_momentum_score_cols(const MatDesc* __re
   }
 }
 
+// ------------------------------------------------------------------ cols mode, M stored transposed
+// M^T (cols x rows) += G^T through a 32 x 32 shared-memory transpose of the row-major G;
+// the column l1 score of M is the row sum of M^T.  Unit = (block of kColRB rows of M,
+// 32 columns): warp w owns columns j0 + 4w .. 4w+3 and accumulates their |M| over the
+// block; one partial per (row block, column) exactly like the row-major kernel.
+template <bool kBf16G>
+__device__ __forceinline__ float load_g(const MatDesc& md, int64_t i, int64_t j) {
+  if constexpr (kBf16G) return bf16_to_f(reinterpret_cast<const __nv_bfloat16*>(md.G)[i * md.ld + j]);
+  else return __ldg(reinterpret_cast<const float*>(md.G) + i * md.ld + j);
+}
+
+template <bool kBf16G>
+__device__ __forceinline__ void col_tile_mt(const MatDesc& md, int rb, int cb, float (*gs)[33]) {
+  const int lane = threadIdx.x & 31, w = threadIdx.x >> 5;
+  const int64_t j0 = (int64_t)cb * 32;
+  const int64_t ib = (int64_t)rb * kColRB;
+  const int64_t ie = md.rows < ib + kColRB ? md.rows : ib + kColRB;
+  float acc[4] = {0.f, 0.f, 0.f, 0.f};
+  for (int64_t i0 = ib; i0 < ie; i0 += 32) {
+#pragma unroll
+    for (int r = 0; r < 4; ++r) {
+      const int64_t gi = i0 + 4 * w + r, gj = j0 + lane;
+      gs[4 * w + r][lane] = (gi < ie && gj < md.cols) ? load_g<kBf16G>(md, gi, gj) : 0.f;
+    }
+    __syncthreads();
+#pragma unroll
+    for (int r = 0; r < 4; ++r) {
+      const int64_t j = j0 + 4 * w + r, i = i0 + lane;
+      if (j < md.cols && i < ie) {
+        float* p = md.M + j * md.ldm + i;
+        const float m = *p + gs[lane][4 * w + r];
+        *p = m;
+        acc[r] += fabsf(m);
+      }
+    }
+    __syncthreads();
+  }
+#pragma unroll
+  for (int r = 0; r < 4; ++r) {
+    const float s = warp_sum(acc[r]);
+    const int64_t j = j0 + 4 * w + r;
+    if (lane == 0 && j < md.cols) md.col_partials[(int64_t)rb * md.cols + j] = s;
+  }
+}
+
+__global__ void __launch_bounds__(256) k_momentum_score_cols_mt(const MatDesc* __restrict__ mats,
+                                                                const int32_t* __restrict__ col_mats,
+                                                                const int64_t* __restrict__ tile_prefix,
+                                                                int n_col_mats, int64_t total_tiles) {
+  __shared__ float gs[32][33];
+  for (int64_t t = blockIdx.x; t < total_tiles; t += gridDim.x) {
+    int lo = 0, hi = n_col_mats - 1;
+    while (lo < hi) {
+      int mid = (lo + hi + 1) >> 1;
+      if (tile_prefix[mid] <= t) lo = mid; else hi = mid - 1;
+    }
+    const MatDesc& md = mats[col_mats[lo]];
+    const int64_t local = t - tile_prefix[lo];
+    const int cbs = (int)((md.cols + 31) / 32);
+    const int rb = (int)(local / cbs), cb = (int)(local % cbs);
+    if (md.grad_bf16) col_tile_mt<true>(md, rb, cb, gs);
+    else col_tile_mt<false>(md, rb, cb, gs);
+  }
+}
+
 }  // namespace dion2

@@ -10,6 +10,10 @@ __global__ void k_momentum_score_rows(const MatDesc* __restrict__ mats, const in
                                       const int64_t* __restrict__ row_prefix, int n_row_mats, int64_t total_rows);
 __global__ void k_momentum_score_cols(const MatDesc* __restrict__ mats, const int32_t* __restrict__ col_mats,
                                       const int64_t* __restrict__ tile_prefix, int n_col_mats, int64_t total_tiles);
+// cols mode with M stored transposed: units = (row block of kColRowBlock rows, 32 columns)
+__global__ void k_momentum_score_cols_mt(const MatDesc* __restrict__ mats, const int32_t* __restrict__ col_mats,
+                                         const int64_t* __restrict__ tile_prefix, int n_col_mats,
+                                         int64_t total_tiles);
 
 // ---------------- K2 top-k select (k_select.cu)
 constexpr int kSelectThreads = 1024;

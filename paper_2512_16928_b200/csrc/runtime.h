@@ -44,6 +44,7 @@ int validate_config(const dion2_config* c);
 int validate_shape(const dion2_matrix& m, bool need_ptrs);
 
 struct MatPlan {
+  int mt;  // M stored transposed (cols mode): gather = rows path on M^T, scatter = path (cols / generic)
   int axis, d, o, k, sr, sc, transposed, p, q, p_pad, q_pad, group, zi, rowblocks, ga, gb, sa_pad, sb_pad, path,
       n_sumsq;
   float fan_sqrt;
@@ -76,8 +77,14 @@ struct Plan {
   int n_row_mats = 0, n_col_mats = 0, total_gather_tiles = 0, max_d = 0;
   // streaming fast paths: list 0 = rows (units: X rows p_pad / selected rows k),
   // list 1 = cols with X = S^T (units: 32-row slabs of X's columns, q_pad / 32)
-  size_t off_fl_mats[2], off_fl_gprefix[2], off_fl_sprefix[2];
-  int fl_n[2] = {0, 0}, fl_gunits[2] = {0, 0}, fl_sunits[2] = {0, 0}, fl_maxk = 0;
+  // gather and scatter memberships differ for transposed-M column matrices (rows gather
+  // on M^T, column scatter on W)
+  size_t off_flg_mats[2], off_fls_mats[2], off_fl_gprefix[2], off_fl_sprefix[2];
+  int fl_gn[2] = {0, 0}, fl_sn[2] = {0, 0}, fl_gunits[2] = {0, 0}, fl_sunits[2] = {0, 0}, fl_maxk = 0;
+  // K1 for column matrices with transposed M
+  size_t off_mtmats = 0, off_mtprefix = 0;
+  int n_mt_mats = 0;
+  int64_t total_mt_tiles = 0;
   int64_t fl_maxn = 0;
   std::vector<uint8_t> host_tables;  // [off_desc, off_ns_begin) image (descriptors + aux)
   std::vector<Launch> ns_launches;

@@ -32,7 +32,8 @@ EXPORTED = ["dion2_config_init", "dion2_workspace_size", "dion2_step", "dion2_st
 class Dion2Matrix(ctypes.Structure):
     _fields_ = [("rows", ctypes.c_int64), ("cols", ctypes.c_int64), ("ld", ctypes.c_int64),
                 ("W", ctypes.c_void_p), ("M", ctypes.c_void_p), ("G", ctypes.c_void_p),
-                ("sel_out", ctypes.c_void_p), ("O_out", ctypes.c_void_p)]
+                ("sel_out", ctypes.c_void_p), ("O_out", ctypes.c_void_p),
+                ("m_transposed", ctypes.c_int32), ("reserved", ctypes.c_int32), ("ldm", ctypes.c_int64)]
 
 
 class Dion2Config(ctypes.Structure):
@@ -134,7 +135,9 @@ def _check_tensor(t: torch.Tensor, name: str, dtype: torch.dtype, like: Optional
 
 def describe(Ws: Sequence[torch.Tensor], Ms: Sequence[torch.Tensor], Gs: Sequence[torch.Tensor],
              sel_out: Optional[Sequence[Optional[torch.Tensor]]] = None,
-             O_out: Optional[Sequence[Optional[torch.Tensor]]] = None):
+             O_out: Optional[Sequence[Optional[torch.Tensor]]] = None,
+             m_transposed: Optional[Sequence[bool]] = None):
+    """m_transposed[i]: M[i] is stored transposed, shape (cols, rows) (column-mode matrices)."""
     n = len(Ws)
     if not (len(Ms) == n and len(Gs) == n) or n == 0:
         raise ValueError("Ws, Ms, Gs must be non-empty and equally long")
@@ -142,7 +145,14 @@ def describe(Ws: Sequence[torch.Tensor], Ms: Sequence[torch.Tensor], Gs: Sequenc
     gdt = Gs[0].dtype
     for i, (W, M, G) in enumerate(zip(Ws, Ms, Gs)):
         _check_tensor(W, "W", torch.float32)
-        _check_tensor(M, "M", torch.float32, W)
+        mt = bool(m_transposed[i]) if m_transposed is not None else False
+        if mt:
+            _check_tensor(M, "M (transposed)", torch.float32)
+            if tuple(M.shape) != (W.shape[1], W.shape[0]):
+                raise ValueError("a transposed M must have shape (cols, rows)")
+            arr[i].m_transposed, arr[i].ldm = 1, M.stride(0)
+        else:
+            _check_tensor(M, "M", torch.float32, W)
         _check_tensor(G, "G", gdt, W)
         arr[i].rows, arr[i].cols, arr[i].ld = W.shape[0], W.shape[1], W.stride(0)
         arr[i].W, arr[i].M, arr[i].G = W.data_ptr(), M.data_ptr(), G.data_ptr()
@@ -185,10 +195,11 @@ class Dion2:
             self._ws = torch.empty(need.value, dtype=torch.uint8, device=device)
         return self._ws
 
-    def step(self, Ws, Ms, Gs, sel_out=None, O_out=None, stream: Optional[torch.cuda.Stream] = None, **override):
+    def step(self, Ws, Ms, Gs, sel_out=None, O_out=None, stream: Optional[torch.cuda.Stream] = None,
+             m_transposed=None, **override):
         kw = dict(self.cfg_kw)
         kw.update(override)
-        arr, gdt = describe(Ws, Ms, Gs, sel_out, O_out)
+        arr, gdt = describe(Ws, Ms, Gs, sel_out, O_out, m_transposed)
         kw.setdefault("grad_dtype", gdt)
         cfg = make_config(**kw)
         dev = Ws[0].device

@@ -55,13 +55,16 @@ def _tie_equivalent(K_gpu, K_ref, scores):
 def run_parity(shapes: Sequence[Tuple[int, int]], alpha: float, axis: str = "auto", precision: str = "bf16",
                steps: int = 10, seed: int = 0, mu: float = 0.95, lr: float = 0.02, row_scaled: bool = False,
                decay_mode: int = 0, check_bitwise: bool = True, device: str = "cuda", select: str = "l1",
-               sel_seed: int = 0) -> ParityResult:
+               sel_seed: int = 0, m_transposed: bool = False, grad_bf16: bool = False) -> ParityResult:
+    """m_transposed: store M transposed (cols x rows) for every column-mode matrix."""
     res = ParityResult()
     cfg_o = oracle_cfg(alpha, axis, mu, lr, decay_mode)
     cfg_o.select, cfg_o.seed = select, sel_seed
     W0 = [gen_w0(m, n, seed, i) for i, (m, n) in enumerate(shapes)]
     Wg = [torch.from_numpy(w).to(device) for w in W0]
-    Mg = [torch.zeros(m, n, device=device) for (m, n) in shapes]
+    mts = [m_transposed and O.resolve_axis(m, n, cfg_o.axis) == O.AXIS_COLS for (m, n) in shapes]
+    Mg = [torch.zeros((n, m) if mt else (m, n), device=device) for (m, n), mt in zip(shapes, mts)]
+    Mv = lambda i: Mg[i].T if mts[i] else Mg[i]  # noqa: E731  (the m x n view of M)
     Wr = [w.astype(np.float64) for w in W0]
     Mr = [np.zeros((m, n)) for (m, n) in shapes]
     opt = Dion2(alpha=alpha, mu=mu, lr=lr, axis=axis, precision=precision, decay_mode=decay_mode, select=select,
@@ -72,7 +75,11 @@ def run_parity(shapes: Sequence[Tuple[int, int]], alpha: float, axis: str = "aut
         ks.append(O.select_count(cfg_o.alpha, m if ax == O.AXIS_ROWS else n))
     for t in range(steps):
         G = [gen_grad(m, n, seed, i, t, row_scaled=row_scaled) for i, (m, n) in enumerate(shapes)]
-        Gg = [torch.from_numpy(g).to(device) for g in G]
+        if grad_bf16:  # the oracle sees exactly the bf16 values the kernels read
+            Gg = [torch.from_numpy(g).to(device).to(torch.bfloat16) for g in G]
+            G = [g.float().cpu().numpy() for g in Gg]
+        else:
+            Gg = [torch.from_numpy(g).to(device) for g in G]
         sel = [torch.empty(k, dtype=torch.int32, device=device) for k in ks]
         Oo = []
         for i, (m, n) in enumerate(shapes):
@@ -80,8 +87,8 @@ def run_parity(shapes: Sequence[Tuple[int, int]], alpha: float, axis: str = "aut
             Oo.append(torch.empty((ks[i], n) if ax == O.AXIS_ROWS else (m, ks[i]), device=device))
         if check_bitwise:
             Wb = [w.clone() for w in Wg]
-            Mb = [mm.clone() for mm in Mg]
-        opt.step(Wg, Mg, Gg, sel_out=sel, O_out=Oo, step=t)
+            Mb = [Mv(i).clone() for i in range(len(shapes))]
+        opt.step(Wg, Mg, Gg, sel_out=sel, O_out=Oo, step=t, m_transposed=mts)
         cfg_o.step = t
         torch.cuda.synchronize()
         for i, (m, n) in enumerate(shapes):
@@ -107,7 +114,7 @@ def run_parity(shapes: Sequence[Tuple[int, int]], alpha: float, axis: str = "aut
                 unsel = np.ones(m if ax == O.AXIS_ROWS else n, bool)
                 unsel[Kg] = False
                 wb, wa = Wb[i].cpu().numpy(), Wg[i].cpu().numpy()
-                mb, ma = Mb[i].cpu().numpy(), Mg[i].cpu().numpy()
+                mb, ma = Mb[i].cpu().numpy(), Mv(i).cpu().numpy()
                 expect_m = (mb + G[i]).astype(np.float32)
                 if decay_mode == 0:
                     if ax == O.AXIS_ROWS:
@@ -116,7 +123,7 @@ def run_parity(shapes: Sequence[Tuple[int, int]], alpha: float, axis: str = "aut
                     else:
                         res.unselected_w_bitwise &= bool(np.array_equal(wb[:, unsel], wa[:, unsel]))
                         res.unselected_m_bitwise &= bool(np.array_equal(expect_m[:, unsel], ma[:, unsel]))
-    _finish(res, shapes, Wg, Mg, Wr, Mr, W0)
+    _finish(res, shapes, Wg, [Mv(i) for i in range(len(shapes))], Wr, Mr, W0)
     return res
 
 

@@ -116,6 +116,13 @@ def test_chunked_nonfinite_reports_global_index(monkeypatch):
     assert torch.equal(Ws[4], W0[4]) and not torch.equal(Ws[5], W0[5])
 
 
+def test_transposed_momentum_for_column_mode():
+    """f4: M stored transposed for column-mode matrices (row gather of M^T, transpose-add K1)."""
+    shapes = [(520, 300), (1000, 256), (8192, 2048), (300, 520)]
+    _assert(run_parity(shapes, 0.25, "auto", "bf16", steps=3, m_transposed=True, row_scaled=True), BF16_TOL)
+    _assert(run_parity(shapes[:2], 0.25, "auto", "bf16", steps=2, m_transposed=True, grad_bf16=True), BF16_TOL)
+
+
 def test_full_decay_ablation_fp32():
     _assert(run_parity([(96, 160)], 0.25, "auto", "fp32", steps=3, decay_mode=1), FP32_TOL)
 
