@@ -54,7 +54,7 @@ def model_shapes(name: str, layers: int = 0):
     raise ValueError(name)
 
 
-def work_model(shapes, alpha, steps=5):
+def work_model(shapes, alpha, steps=5, mt=False):
     """Algorithmic work per Dion2 step: NS FLOPs T(4p^2 q + 2p^3) and
     per-phase algorithmic HBM bytes."""
     ns_flops = {"ns_gram": 0.0, "ns_poly": 0.0, "ns_apply": 0.0}
@@ -77,7 +77,8 @@ def work_model(shapes, alpha, steps=5):
             sfx = "_cols"
         else:
             sfx = ""
-        byts["gather" + sfx] += k * o * (4.0 + 4.0 + 2.0)     # read M[K], write mu*M[K], write bf16 X
+        gsfx = "_rows" if (mt and sfx == "_cols") else sfx     # transposed M: row gather of M^T
+        byts["gather" + gsfx] += k * o * (4.0 + 4.0 + 2.0)    # read M[K], write mu*M[K], write bf16 X
         byts["scatter" + sfx] += k * o * (2.0 + 4.0 + 4.0)    # read bf16 O, read+write W[K]
     return ns_flops, byts
 
@@ -141,8 +142,9 @@ class ClockSampler:
 
 # ---------------------------------------------------------------------------------- our arm
 
-def build_state(shapes, device, seed=0, fan_in=None):
-    """Flat fp32 W / M / G buffers with one row-major view per matrix (W0 ~ N(0, 1/fan-in))."""
+def build_state(shapes, device, seed=0, fan_in=None, m_transposed=None):
+    """Flat fp32 W / M / G buffers with one row-major view per matrix (W0 ~ N(0, 1/fan-in));
+    M[i] is a (cols, rows) view when m_transposed[i] (column-mode matrices)."""
     import torch
     total = sum(m * n for m, n in shapes)
     gen = torch.Generator(device=device)
@@ -155,7 +157,8 @@ def build_state(shapes, device, seed=0, fan_in=None):
     Ws, Ms, Gs, off = [], [], [], 0
     for i, (m, n) in enumerate(shapes):
         Ws.append(W[off:off + m * n].view(m, n).mul_(1.0 / math.sqrt(fan_in[i] if fan_in else n)))
-        Ms.append(M[off:off + m * n].view(m, n))
+        mt = bool(m_transposed[i]) if m_transposed else False
+        Ms.append(M[off:off + m * n].view((n, m) if mt else (m, n)))
         Gs.append(G[off:off + m * n].view(m, n))
         off += m * n
     return (W, M, G), Ws, Ms, Gs
@@ -268,8 +271,11 @@ def run_ours(args):
         make_opt = lambda a: D.Dion2Dist(shapes, alpha=a, axis="auto", precision="bf16")  # noqa: E731
     else:
         info = None
-        bufs, Ws, Ms, Gs = build_state(shapes, dev, seed=rank)
-        make_opt = lambda a: Dion2(alpha=a, axis="auto", precision="bf16")  # noqa: E731
+        # optimizer-state layout: momentum of column-mode matrices stored transposed (the
+        # column gather of M[:, K] becomes a contiguous row gather of M^T); --no-mt disables
+        mts = [(not args.no_mt) and m > n for (m, n) in shapes]
+        bufs, Ws, Ms, Gs = build_state(shapes, dev, seed=rank, m_transposed=mts)
+        make_opt = lambda a: Dion2(alpha=a, axis="auto", precision="bf16", m_transposed=mts)  # noqa: E731
     opt = make_opt(args.alpha)
 
     with ClockSampler(local) as clk:
@@ -297,7 +303,7 @@ def run_ours(args):
     torch.cuda.empty_cache()
 
     peaks, peak_src = load_peaks()
-    ns_flops, byts = work_model(shapes, args.alpha)
+    ns_flops, byts = work_model(shapes, args.alpha, mt=(not use_dist) and not args.no_mt)
     if use_dist:  # this rank's share: 1/world of every streaming pass, NS of its owned matrices
         owned = [s for s, o in zip(shapes, info["owner"]) if o == rank]
         ns_flops = work_model(owned, args.alpha)[0] if owned else {k: 0.0 for k in ns_flops}
@@ -388,6 +394,8 @@ def run_ours(args):
             "data": "synthetic (W0~N(0,1/n), G~N(0,1), M0=0; seeded device RNG)",
             "config": {"workload": f"{args.config}-set Dion2 step (configs[1])", "matrices": len(shapes),
                        "params": n_params, "alpha": args.alpha, "axis": "auto", "ns_steps": 5,
+                       "momentum_layout": "column-mode matrices transposed" if (not use_dist and not args.no_mt)
+                       else "as W",
                        "l2_flush": "not needed: 14.5 GB touched per step >> 126 MB L2",
                        "parallelism": "single GPU" if not use_dist else
                        f"owner-compute over {world} GPUs (NCCL; shards along the non-selection axis)"},
@@ -467,6 +475,7 @@ def main():
     ap.add_argument("--cpu-budget", type=float, default=20.0)
     ap.add_argument("--layers", type=int, default=0, help="override the layer count (profiling only)")
     ap.add_argument("--no-e2e", action="store_true")
+    ap.add_argument("--no-mt", action="store_true", help="keep column-mode momentum in W's layout")
     args = ap.parse_args()
     if args.impl == "reference":
         run_reference(args)

@@ -182,8 +182,10 @@ class Dion2:
     opt = Dion2(alpha=0.25); opt.step(Ws, Ms, Gs)   # all on one CUDA device
     """
 
-    def __init__(self, **cfg_kw):
+    def __init__(self, m_transposed=None, **cfg_kw):
+        """m_transposed: default per-matrix flags (M stored (cols, rows)) used by step()."""
         self.cfg_kw = dict(cfg_kw)
+        self.m_transposed = m_transposed
         self._ws: Optional[torch.Tensor] = None
 
     def workspace(self, arr, n, cfg, device) -> torch.Tensor:
@@ -199,6 +201,8 @@ class Dion2:
              m_transposed=None, **override):
         kw = dict(self.cfg_kw)
         kw.update(override)
+        if m_transposed is None:
+            m_transposed = self.m_transposed
         arr, gdt = describe(Ws, Ms, Gs, sel_out, O_out, m_transposed)
         kw.setdefault("grad_dtype", gdt)
         cfg = make_config(**kw)
