@@ -170,10 +170,11 @@ int build_layout(Plan& P, const dion2_matrix* mats, int n, const dion2_config* c
     else if (axis == DION2_AXIS_COLS && q.transposed && P.bf16_ns && q.k <= kMaxColKFast) q.path = 2;
     else q.path = 0;
     q.mt = m.m_transposed ? 1 : 0;
-    if (q.mt && q.path != 2) return DION2_EUNSUPPORTED;  // transposed M: column mode, bf16, k <= 1024, k <= rows
+    // transposed M: column mode with X = S^T (k <= rows), bf16; the gather is the row path on M^T
+    if (q.mt && !(axis == DION2_AXIS_COLS && q.transposed && P.bf16_ns)) return DION2_EUNSUPPORTED;
     q.ga = q.path == 0 ? (int)ceil_div(q.sa_pad, kTileA) : 0;
     q.gb = q.path == 0 ? (int)ceil_div(q.sb_pad, kTileB) : 0;
-    q.n_sumsq = q.path == 0 ? q.ga * q.gb : ((q.path == 1 || q.mt) ? q.p_pad : q.q_pad / 32);
+    q.n_sumsq = (q.path == 1 || q.mt) ? q.p_pad : (q.path == 0 ? q.ga * q.gb : q.q_pad / 32);
     auto key = std::make_pair(q.p_pad, q.q_pad);
     auto it = gidx.find(key);
     if (it == gidx.end()) {
@@ -291,20 +292,23 @@ int build_device_plan(Plan& P, const dion2_matrix* mats, const dion2_config* c, 
     d.ldm = q.mt ? mats[i].ldm : 0;
     gprefix[i] = gt_acc;
     gt_acc += q.ga * q.gb;
-    if (q.path > 0) {
-      // gather list: rows streaming (path 1, or transposed-M columns = rows of M^T), else cols
-      const int lg = (q.path == 1 || q.mt) ? 0 : 1;
-      const int ls = q.path - 1;
+    // gather: rows streaming (path 1, or transposed-M columns = rows of M^T), cols streaming
+    // (path 2) or generic tiles; scatter: by path (generic tiles for path 0)
+    const int lg = (q.path == 1 || q.mt) ? 0 : (q.path == 2 ? 1 : -1);
+    const int ls = q.path - 1;
+    if (lg >= 0) {
       flg_mats[lg].push_back(i);
       fl_gp[lg].push_back(P.fl_gunits[lg]);
       P.fl_gunits[lg] += lg == 0 ? q.p_pad : q.q_pad / 32;
+    }
+    if (ls >= 0) {
       fls_mats[ls].push_back(i);
       fl_sp[ls].push_back(P.fl_sunits[ls]);
       P.fl_sunits[ls] += ls == 0 ? q.k : q.q_pad / 32;
-      if (lg == 1 || ls == 1) {
-        P.fl_maxk = std::max(P.fl_maxk, q.k);
-        P.fl_maxn = std::max<int64_t>(P.fl_maxn, mats[i].cols);
-      }
+    }
+    if (lg == 1 || ls == 1) {
+      P.fl_maxk = std::max(P.fl_maxk, q.k);
+      P.fl_maxn = std::max<int64_t>(P.fl_maxn, mats[i].cols);
     }
     if (q.axis == DION2_AXIS_ROWS) {
       rowmats.push_back(i);

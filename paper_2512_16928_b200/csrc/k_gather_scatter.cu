@@ -43,6 +43,7 @@ __global__ void __launch_bounds__(256) k_gather_decay(const MatDesc* __restrict_
   for (int t = blockIdx.x; t < total_tiles; t += gridDim.x) {
     const int mi = find_mat(tile_prefix_mats, n_mats, t);
     const MatDesc& md = mats[mi];
+    if (md.mt) continue;  // transposed M: gathered by the row path on M^T (block-uniform)
     const int local = t - md.gather_tile_base;
     const int ta = local / md.gather_tiles_b, tb = local % md.gather_tiles_b;
     const int a0 = ta * kTileA, b0 = tb * kTileB;
