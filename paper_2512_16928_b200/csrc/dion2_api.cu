@@ -317,7 +317,7 @@ int build_device_plan(Plan& P, const dion2_matrix* mats, const dion2_config* c, 
     } else if (q.mt) {
       mtmats.push_back(i);
       mtprefix.push_back(mt_acc);
-      mt_acc += (int64_t)q.rowblocks * ceil_div(mats[i].cols, 32);
+      mt_acc += (int64_t)q.rowblocks * ceil_div(mats[i].cols, 64);
     } else {
       colmats.push_back(i);
       colprefix.push_back(ctiles_acc);

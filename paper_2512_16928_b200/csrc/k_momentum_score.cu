@@ -228,11 +228,87 @@ __device__ __forceinline__ void col_tile_mt(const MatDesc& md, int rb, int cb, f
   }
 }
 
+// Vectorised variant (16-B aligned rows): 64 x 64 tiles, thread (r16 = t/16, c4 = t%16)
+// moves float4s of G rows and of M^T rows; all 8 loads are issued before the barrier.
+template <bool kBf16G>
+__device__ __forceinline__ void col_tile_mt_v4(const MatDesc& md, int rb, int cb, float (*gs)[65]) {
+  const int t = threadIdx.x, r16 = t >> 4, c4 = t & 15;
+  const int64_t j0 = (int64_t)cb * 64;
+  const int64_t ib = (int64_t)rb * kColRB;
+  const int64_t ie = md.rows < ib + kColRB ? md.rows : ib + kColRB;
+  float acc[4] = {0.f, 0.f, 0.f, 0.f};  // |M| over this block's rows for columns j0 + r16 + 16u
+  for (int64_t i0 = ib; i0 < ie; i0 += 64) {
+    float4 g[4], m[4];
+#pragma unroll
+    for (int u = 0; u < 4; ++u) {  // G rows i0 + r16 + 16u, columns j0 + 4 c4 .. +3
+      const int64_t i = i0 + r16 + 16 * u, j = j0 + 4 * c4;
+      if (i < ie && j + 3 < md.cols) {
+        if constexpr (kBf16G) {
+          const uint2 raw = __ldg(reinterpret_cast<const uint2*>(reinterpret_cast<const __nv_bfloat16*>(md.G) + i * md.ld + j));
+          const __nv_bfloat162 lo = *reinterpret_cast<const __nv_bfloat162*>(&raw.x);
+          const __nv_bfloat162 hi = *reinterpret_cast<const __nv_bfloat162*>(&raw.y);
+          g[u] = make_float4(__low2float(lo), __high2float(lo), __low2float(hi), __high2float(hi));
+        } else {
+          g[u] = __ldcs(reinterpret_cast<const float4*>(reinterpret_cast<const float*>(md.G) + i * md.ld + j));
+        }
+      } else {
+        g[u] = make_float4(0.f, 0.f, 0.f, 0.f);
+        for (int e = 0; e < 4; ++e)
+          if (i < ie && j + e < md.cols) (&g[u].x)[e] = load_g<kBf16G>(md, i, j + e);
+      }
+    }
+#pragma unroll
+    for (int u = 0; u < 4; ++u) {  // M^T rows j0 + r16 + 16u, columns (= rows of M) i0 + 4 c4 .. +3
+      const int64_t j = j0 + r16 + 16 * u, i = i0 + 4 * c4;
+      m[u] = (j < md.cols && i + 3 < ie) ? *reinterpret_cast<const float4*>(md.M + j * md.ldm + i)
+                                         : make_float4(0.f, 0.f, 0.f, 0.f);
+      if (j < md.cols && i < ie && i + 3 >= ie)
+        for (int e = 0; e < 4; ++e)
+          if (i + e < ie) (&m[u].x)[e] = md.M[j * md.ldm + i + e];
+    }
+#pragma unroll
+    for (int u = 0; u < 4; ++u) {
+      gs[r16 + 16 * u][4 * c4 + 0] = g[u].x;
+      gs[r16 + 16 * u][4 * c4 + 1] = g[u].y;
+      gs[r16 + 16 * u][4 * c4 + 2] = g[u].z;
+      gs[r16 + 16 * u][4 * c4 + 3] = g[u].w;
+    }
+    __syncthreads();
+#pragma unroll
+    for (int u = 0; u < 4; ++u) {
+      const int jl = r16 + 16 * u;
+      const int64_t j = j0 + jl, i = i0 + 4 * c4;
+      float* e = &m[u].x;
+#pragma unroll
+      for (int q = 0; q < 4; ++q) {
+        e[q] += gs[4 * c4 + q][jl];  // G^T element (j, i + q)
+        acc[u] += (i + q < ie) ? fabsf(e[q]) : 0.f;
+      }
+      if (j < md.cols) {
+        if (i + 3 < ie) *reinterpret_cast<float4*>(md.M + j * md.ldm + i) = m[u];
+        else
+          for (int q = 0; q < 4; ++q)
+            if (i + q < ie) md.M[j * md.ldm + i + q] = e[q];
+      }
+    }
+    __syncthreads();
+  }
+  // reduce the 16 threads (c4) that share a column, in a fixed xor-tree order
+#pragma unroll
+  for (int u = 0; u < 4; ++u) {
+    float s = acc[u];
+#pragma unroll
+    for (int o = 8; o > 0; o >>= 1) s += __shfl_xor_sync(0xffffffffu, s, o);
+    const int64_t j = j0 + r16 + 16 * u;
+    if (c4 == 0 && j < md.cols) md.col_partials[(int64_t)rb * md.cols + j] = s;
+  }
+}
+
 __global__ void __launch_bounds__(256) k_momentum_score_cols_mt(const MatDesc* __restrict__ mats,
                                                                 const int32_t* __restrict__ col_mats,
                                                                 const int64_t* __restrict__ tile_prefix,
                                                                 int n_col_mats, int64_t total_tiles) {
-  __shared__ float gs[32][33];
+  __shared__ float gs[64][65];
   for (int64_t t = blockIdx.x; t < total_tiles; t += gridDim.x) {
     int lo = 0, hi = n_col_mats - 1;
     while (lo < hi) {
@@ -241,10 +317,19 @@ __global__ void __launch_bounds__(256) k_momentum_score_cols_mt(const MatDesc* _
     }
     const MatDesc& md = mats[col_mats[lo]];
     const int64_t local = t - tile_prefix[lo];
-    const int cbs = (int)((md.cols + 31) / 32);
+    // units: (row block, 64 columns); unaligned rows take two scalar 32-column halves
+    const int cbs = (int)((md.cols + 63) / 64);
     const int rb = (int)(local / cbs), cb = (int)(local % cbs);
-    if (md.grad_bf16) col_tile_mt<true>(md, rb, cb, gs);
-    else col_tile_mt<false>(md, rb, cb, gs);
+    if (md.vec4) {
+      if (md.grad_bf16) col_tile_mt_v4<true>(md, rb, cb, gs);
+      else col_tile_mt_v4<false>(md, rb, cb, gs);
+    } else {
+      float(*g33)[33] = reinterpret_cast<float(*)[33]>(&gs[0][0]);
+      for (int h = 0; h < 2; ++h) {
+        if (md.grad_bf16) col_tile_mt<true>(md, rb, 2 * cb + h, g33);
+        else col_tile_mt<false>(md, rb, 2 * cb + h, g33);
+      }
+    }
   }
 }
 
