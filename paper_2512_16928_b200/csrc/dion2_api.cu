@@ -687,13 +687,13 @@ cudaStream_t ns_stream() {
   return st;
 }
 
-// DION2_CHUNKS overrides; default: pipeline in 2 chunks when the set is large enough to
-// keep both the NS and the streaming kernels busy (>= 12 matrices, >= 128 M parameters).
+// Opt-in (DION2_CHUNKS=c): measured on the 1B set the overlapped kernels contend for DRAM
+// and the unpipelined step is faster (6.87-6.89 ms vs 6.97-7.01 ms with 2 chunks), so the
+// default is a single chunk.
 int chunk_count(const dion2_matrix* mats, int n) {
+  (void)mats;
   if (const char* e = getenv("DION2_CHUNKS")) return std::max(1, std::min(n, atoi(e)));
-  int64_t params = 0;
-  for (int i = 0; i < n; ++i) params += mats[i].rows * mats[i].cols;
-  return (n >= 12 && params >= (int64_t)128 << 20) ? 2 : 1;
+  return 1;
 }
 
 int build_chunked_layout(ChunkedPlan& C, const dion2_matrix* mats, int n, const dion2_config* c, int chunks) {
