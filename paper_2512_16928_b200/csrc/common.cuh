@@ -234,8 +234,11 @@ __device__ __forceinline__ uint32_t mapa_shared(uint32_t saddr, uint32_t rank) {
   asm volatile("mapa.shared::cluster.u32 %0, %1, %2;" : "=r"(r) : "r"(saddr), "r"(rank));
   return r;
 }
+// Relaxed: used only to hand TMEM back to the leader's MMA (the tcgen05.ld's are complete
+// after tcgen05.wait::ld + tcgen05.fence::before_thread_sync); .release here emitted a
+// MEMBAR.ALL.CTA that stalled the epilogue behind its own TMA stores (ncu: 25% of samples).
 __device__ __forceinline__ void mbar_arrive_cluster(uint32_t cluster_addr) {
-  asm volatile("mbarrier.arrive.release.cluster.shared::cluster.b64 _, [%0];" ::"r"(cluster_addr) : "memory");
+  asm volatile("mbarrier.arrive.relaxed.cluster.shared::cluster.b64 _, [%0];" ::"r"(cluster_addr) : "memory");
 }
 // TMA load into the local CTA's smem, completion counted on the pair leader's barrier
 __device__ __forceinline__ void tma_load_3d_pair(void* smem_dst, const CUtensorMap* map, uint32_t leader_bar, int c0,
