@@ -54,10 +54,22 @@ def model_shapes(name: str, layers: int = 0):
     raise ValueError(name)
 
 
-def work_model(shapes, alpha, steps=5, mt=False):
-    """Algorithmic work per Dion2 step: NS FLOPs T(4p^2 q + 2p^3) and
-    per-phase algorithmic HBM bytes."""
-    ns_flops = {"ns_gram": 0.0, "ns_poly": 0.0, "ns_apply": 0.0}
+def ns_uses_gram_form(p, q, ns_form="auto"):
+    """The library's choice (dion2_api.cu build_layout, reading R23): Gram space iff the
+    256-padded wide X has q >= 2p (AUTO)."""
+    if ns_form != "auto":
+        return ns_form == "gram"
+    pad = lambda v: (v + 255) // 256 * 256  # noqa: E731
+    return pad(q) >= 2 * pad(p)
+
+
+def work_model(shapes, alpha, steps=5, mt=False, ns_form="auto"):
+    """Algorithmic work per Dion2 step and per-phase algorithmic HBM bytes.
+    NS FLOPs of the form the library evaluates (full products; symmetric tiles not credited):
+      direct: T(4p^2 q + 2p^3)  -- gram 2p^2q, poly 2p^3, apply 2p^2q per iteration
+      Gram space (R23): 4p^2 q + (4T - 3) 2p^3 (T >= 2) -- gram + apply once, T polys,
+      3T - 3 products C.Q / C.A / C.(CA)."""
+    ns_flops = {"ns_gram": 0.0, "ns_poly": 0.0, "ns_apply": 0.0, "ns_mul": 0.0}
     byts = {"momentum_score": 0.0}
     for ph in ("gather", "gather_rows", "gather_cols", "scatter", "scatter_rows", "scatter_cols"):
         byts[ph] = 0.0
@@ -66,9 +78,15 @@ def work_model(shapes, alpha, steps=5, mt=False):
         d, o = (m, n) if rows else (n, m)
         k = max(1, min(d, int(math.floor(alpha * d + 0.5))))
         p, q = min(k, o), max(k, o)
-        ns_flops["ns_gram"] += steps * 2.0 * p * p * q
-        ns_flops["ns_poly"] += steps * 2.0 * p ** 3
-        ns_flops["ns_apply"] += steps * 2.0 * p * p * q
+        if ns_uses_gram_form(p, q, ns_form):
+            ns_flops["ns_gram"] += 2.0 * p * p * q
+            ns_flops["ns_poly"] += steps * 2.0 * p ** 3
+            ns_flops["ns_mul"] += max(0, 3 * steps - 3) * 2.0 * p ** 3
+            ns_flops["ns_apply"] += 2.0 * p * p * q
+        else:
+            ns_flops["ns_gram"] += steps * 2.0 * p * p * q
+            ns_flops["ns_poly"] += steps * 2.0 * p ** 3
+            ns_flops["ns_apply"] += steps * 2.0 * p * p * q
         byts["momentum_score"] += m * n * 12.0 + d * 4.0       # read G, read M, write M, write scores
         # the library's path choice (dion2_api.cu build_layout)
         if rows and k <= n:
@@ -268,14 +286,16 @@ def run_ours(args):
         # owner-compute over all ranks: every matrix sharded along its non-selection axis
         info = D.dist_info(shapes, world, rank, alpha=args.alpha)
         bufs, Ws, Ms, Gs = build_state(info["shard"], dev, seed=rank, fan_in=[n for (_, n) in shapes])
-        make_opt = lambda a: D.Dion2Dist(shapes, alpha=a, axis="auto", precision="bf16")  # noqa: E731
+        make_opt = lambda a: D.Dion2Dist(shapes, alpha=a, axis="auto", precision="bf16",  # noqa: E731
+                                          ns_form=args.ns_form)
     else:
         info = None
         # optimizer-state layout: momentum of column-mode matrices stored transposed (the
         # column gather of M[:, K] becomes a contiguous row gather of M^T); --no-mt disables
         mts = [(not args.no_mt) and m > n for (m, n) in shapes]
         bufs, Ws, Ms, Gs = build_state(shapes, dev, seed=rank, m_transposed=mts)
-        make_opt = lambda a: Dion2(alpha=a, axis="auto", precision="bf16", m_transposed=mts)  # noqa: E731
+        make_opt = lambda a: Dion2(alpha=a, axis="auto", precision="bf16", m_transposed=mts,  # noqa: E731
+                                   ns_form=args.ns_form)
     opt = make_opt(args.alpha)
 
     with ClockSampler(local) as clk:
@@ -303,10 +323,10 @@ def run_ours(args):
     torch.cuda.empty_cache()
 
     peaks, peak_src = load_peaks()
-    ns_flops, byts = work_model(shapes, args.alpha, mt=(not use_dist) and not args.no_mt)
+    ns_flops, byts = work_model(shapes, args.alpha, mt=(not use_dist) and not args.no_mt, ns_form=args.ns_form)
     if use_dist:  # this rank's share: 1/world of every streaming pass, NS of its owned matrices
         owned = [s for s, o in zip(shapes, info["owner"]) if o == rank]
-        ns_flops = work_model(owned, args.alpha)[0] if owned else {k: 0.0 for k in ns_flops}
+        ns_flops = work_model(owned, args.alpha, ns_form=args.ns_form)[0] if owned else {k: 0.0 for k in ns_flops}
         byts = {k: v / world for k, v in byts.items()}
     per_phase = {}
     for name, (t_ms, cnt) in phases.items():
@@ -390,10 +410,10 @@ def run_ours(args):
             "higher_is_better": False,
             "scaling": "weak" if world == 1 else "strong",
             "vs_baseline": None,
-            "dtype": "f32 state / bf16 NS",
+            "dtype": "f32 state / bf16 X, fp16 Gram-space NS (fp32 accumulate)",
             "data": "synthetic (W0~N(0,1/n), G~N(0,1), M0=0; seeded device RNG)",
             "config": {"workload": f"{args.config}-set Dion2 step (configs[1])", "matrices": len(shapes),
-                       "params": n_params, "alpha": args.alpha, "axis": "auto", "ns_steps": 5,
+                       "params": n_params, "alpha": args.alpha, "axis": "auto", "ns_steps": 5, "ns_form": args.ns_form,
                        "momentum_layout": "column-mode matrices transposed" if (not use_dist and not args.no_mt)
                        else "as W",
                        "l2_flush": "not needed: 14.5 GB touched per step >> 126 MB L2",
@@ -405,8 +425,8 @@ def run_ours(args):
             "ns_frac_bf16_burst": ns_tflops / peaks["bf16_tflops"],
             "ns_frac_bf16_sustained": ns_tflops / peaks["bf16_tflops_sustained"],
             "ms_per_step_unpipelined_with_phase_events": ms_timed,
-            "phases_note": "per-kernel times from a separate K-step pass with the chunked pipeline off "
-                           "(DION2_CHUNKS=1) so kernels do not overlap; value uses the default pipelined step",
+            "phases_note": "per-kernel times (CUDA events around every launch) from a separate K-step pass "
+                           "with the chunked pipeline off (DION2_CHUNKS=1, also the default)",
             "phases": per_phase,
             "roofline": roof,
             "cpu_baseline": cpu,
@@ -476,6 +496,8 @@ def main():
     ap.add_argument("--layers", type=int, default=0, help="override the layer count (profiling only)")
     ap.add_argument("--no-e2e", action="store_true")
     ap.add_argument("--no-mt", action="store_true", help="keep column-mode momentum in W's layout")
+    ap.add_argument("--ns-form", choices=["auto", "direct", "gram"], default="auto",
+                    help="Newton-Schulz evaluation form (DESIGN.md reading R23)")
     args = ap.parse_args()
     if args.impl == "reference":
         run_reference(args)

@@ -41,7 +41,7 @@
 extern "C" {
 #endif
 
-#define DION2_ABI_VERSION 2
+#define DION2_ABI_VERSION 3
 #define DION2_MAX_NS_STEPS 16
 
 typedef enum {
@@ -62,6 +62,14 @@ typedef enum { DION2_AXIS_ROWS = 0, DION2_AXIS_COLS = 1, DION2_AXIS_AUTO = 2 } d
 typedef enum { DION2_SELECT_L1 = 0, DION2_SELECT_RANDOM = 1 } dion2_select;                /* P:198-199 */
 typedef enum { DION2_NS_BF16 = 0, DION2_NS_FP32 = 1 } dion2_precision;
 typedef enum { DION2_DT_F32 = 0, DION2_DT_BF16 = 1 } dion2_dtype;
+/* How the BF16 Newton-Schulz map is evaluated (reading R23).  Both forms compute the same
+   polynomial map X_T = p_T(... p_1(X_0)) of Alg. 1 l.4; they differ only in rounding.
+   DIRECT: T iterations on X (p x q): A = X X^T, C = a I + b A + c A^2, X <- C X (bf16).
+   GRAM:   the iteration carried out on p x p matrices: A_0 = X_0 X_0^T once, then
+           C_t = a I + b A_t + c A_t^2, Q_{t+1} = C_t Q_t, A_{t+1} = C_t (C_t A_t) in fp16
+           with fp32 accumulation, and X_T = Q_T X_0 once (bf16).  Fewer FLOPs when q >= 2p.
+   AUTO:   GRAM for a matrix whose wide X has q >= 2p, DIRECT otherwise. */
+typedef enum { DION2_NS_FORM_AUTO = 0, DION2_NS_FORM_DIRECT = 1, DION2_NS_FORM_GRAM = 2 } dion2_ns_form;
 
 /* One weight matrix and its optimizer state. */
 typedef struct {
@@ -100,6 +108,8 @@ typedef struct {
   int32_t scale_mode; /* 0 = eta*sqrt(rows/cols) of the full W (Alg. 1 l.6); 1 = sqrt of the submatrix dims (SPEC S:360 flag) */
   uint64_t seed;      /* random selection key (unused for L1) */
   uint64_t step;      /* random selection counter: the caller's step index (unused for L1) */
+  int32_t ns_form;    /* dion2_ns_form, default AUTO (BF16 precision only; FP32 is always DIRECT) */
+  int32_t reserved0;  /* must be 0 */
 } dion2_config;
 
 /* Fill *cfg with the defaults above.  Always returns DION2_OK. */

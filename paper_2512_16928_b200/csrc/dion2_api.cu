@@ -25,7 +25,7 @@ namespace dion2rt {
 const char* kPhaseNames[kNumPhases] = {"momentum_score", "select",       "gather",       "norm",
                                        "ns_gram",        "ns_poly",      "ns_apply",     "scatter",
                                        "full_decay",     "gather_rows",  "gather_cols",  "scatter_rows",
-                                       "scatter_cols"};
+                                       "scatter_cols",   "ns_mul"};
 
 std::mutex g_mu;
 int g_sm_count = 0;
@@ -92,6 +92,8 @@ int validate_config(const dion2_config* c) {
   if (c->grad_dtype != DION2_DT_F32 && c->grad_dtype != DION2_DT_BF16) return DION2_EINVAL_CONFIG;
   if (c->decay_mode < 0 || c->decay_mode > 1) return DION2_EINVAL_CONFIG;
   if (c->scale_mode < 0 || c->scale_mode > 1) return DION2_EINVAL_CONFIG;
+  if (c->ns_form < DION2_NS_FORM_AUTO || c->ns_form > DION2_NS_FORM_GRAM || c->reserved0 != 0)
+    return DION2_EINVAL_CONFIG;
   return DION2_OK;
 }
 
@@ -128,6 +130,7 @@ std::string plan_key(const dion2_matrix* mats, int n, const dion2_config* c, voi
   put(&c->grad_dtype, 4);
   put(&c->decay_mode, 4);
   put(&c->scale_mode, 4);
+  put(&c->ns_form, 4);
   return k;
 }
 
@@ -232,12 +235,124 @@ int build_layout(Plan& P, const dion2_matrix* mats, int n, const dion2_config* c
     g.off_X1 = off; off = align_up(off + xb, 4096);
     g.off_A = off;  off = align_up(off + ab, 4096);
     g.off_B = off;  off = align_up(off + ab, 4096);
+    // Gram-space form (reading R23): bf16 hot path, wide X with q >= 2p (AUTO) or forced
+    g.gs = P.bf16_ns && (c->ns_form == DION2_NS_FORM_GRAM || (c->ns_form == DION2_NS_FORM_AUTO && g.q_pad >= 2 * g.p_pad));
+    g.off_C = g.off_Q0 = g.off_Q1 = 0;
+    if (g.gs) {
+      g.off_C = off;  off = align_up(off + ab, 4096);
+      g.off_Q0 = off; off = align_up(off + ab, 4096);
+      g.off_Q1 = off; off = align_up(off + ab, 4096);
+    }
   }
   P.off_ns_end = off;
   P.total = off + 4096;  // slack for base alignment
   return DION2_OK;
 }
 
+
+// Launch list of the Gram-space Newton-Schulz form (reading R23) for the groups with g.gs:
+//   gram   A   = s^2 X0 X0^T                         (bf16 in, fp16 out)
+//   t = 0 .. T-1:
+//     poly   C_t = a_t I + b_t A + c_t A A            (fp16; C_0 doubles as Q_1)
+//     mul    Q_{t+1} = C_t Q_t (t >= 1),  B = C_t A (t < T-1)
+//     mul    A   = C_t B                              (t < T-1)
+//   apply  X1  = s Q_T X0                             (bf16)
+// Every p x p product is a polynomial in A_0, hence symmetric: upper-triangle pair tiles,
+// mirrored.  Q_T is written as bf16 (the apply operand), everything else as fp16.
+static int append_gram_space_launches(Plan& P, const dion2_config* c, void* ws, int pair_mode) {
+  std::vector<int> gl;
+  for (int gi = 0; gi < (int)P.groups.size(); ++gi)
+    if (P.groups[gi].gs) gl.push_back(gi);
+  if (gl.empty()) return DION2_OK;
+  const float* scale_all = (const float*)at(ws, P.off_nsscale);
+  const int T = P.ns_steps;
+  struct Entry {
+    int gi;
+    void *a, *b, *out, *cin;
+  };
+  // one launch per kMaxGroups entries; kind: 3 = pair (sym p x p products, or apply under
+  // DION2_NS_PAIR=all), 1 = 1-SM BN 256 (apply)
+  auto emit = [&](int phase, const std::vector<Entry>& es, float cacc, float cC, float diag, int scale_sel,
+                  int in_f16, int out_f16) -> int {
+    const bool apply = phase == PH_APPLY;
+    const bool pair = !apply || pair_mode == 2;
+    const int MT = pair ? 256 : 128, BN = 256;
+    for (size_t s0 = 0; s0 < es.size(); s0 += kMaxGroups) {
+      Launch L{};
+      L.phase = phase;
+      L.bn = BN;
+      L.kind = pair ? 3 : 1;
+      NsParams& np = L.tc.p;
+      np.ngroups = (int)std::min<size_t>(kMaxGroups, es.size() - s0);
+      np.ns_scale_all = scale_all;
+      np.cacc = cacc; np.cC = cC; np.diag = diag; np.scale_sel = scale_sel;
+      np.sym = apply ? 0 : 1;
+      np.b_kmajor = apply ? 0 : 1;
+      np.in_f16 = in_f16; np.out_f16 = out_f16;
+      int tiles = 0;
+      for (int j = 0; j < np.ngroups; ++j) {
+        const Entry& e = es[s0 + j];
+        const Group& g = P.groups[e.gi];
+        const long long xs = (long long)g.p_pad * g.q_pad, as = (long long)g.p_pad * g.p_pad;
+        const int K = phase == PH_GRAM ? g.q_pad : g.p_pad;
+        NsGroup& G = np.g[j];
+        G.count = g.count;
+        G.gmats = (const int32_t*)tab(P, g.off_gmats);
+        G.m_tiles = g.p_pad / MT;
+        G.n_tiles = apply ? g.q_pad / BN : g.p_pad / BN;
+        G.k_blocks = K / 64;
+        G.a = e.a; G.a_mstride = phase == PH_GRAM ? xs : as; G.lda = K;
+        G.b = e.b; G.b_mstride = (phase == PH_GRAM || apply) ? xs : as; G.ldb = apply ? g.q_pad : K;
+        G.out = e.out; G.out_mstride = apply ? xs : as; G.out_ld = apply ? g.q_pad : g.p_pad;
+        G.cin = e.cin; G.cin_mstride = e.cin ? as : 0; G.cin_ld = e.cin ? g.p_pad : 0;
+        if (!make_map(&L.tc.mapA[j], e.a, K, g.p_pad, g.count, 64, 128)) return DION2_ECUDA;
+        if (apply) {
+          if (!make_map(&L.tc.mapB[j], e.b, g.q_pad, g.p_pad, g.count, 64, 64)) return DION2_ECUDA;
+        } else {
+          if (!make_map(&L.tc.mapB[j], e.b, K, g.p_pad, g.count, 64, 128)) return DION2_ECUDA;
+        }
+        if (!make_map(&L.tc.mapD[j], e.out, G.out_ld, g.p_pad, g.count, 32, 32, CU_TENSOR_MAP_SWIZZLE_64B))
+          return DION2_ECUDA;
+        G.tile_base = tiles;
+        tiles += G.count * (np.sym ? G.m_tiles * (G.m_tiles + 1) / 2 : G.m_tiles * G.n_tiles);
+      }
+      np.total_tiles = tiles;
+      P.ns_launches.push_back(L);
+    }
+    return DION2_OK;
+  };
+  auto X0 = [&](int gi) { return at(ws, P.groups[gi].off_X0); };
+  auto X1 = [&](int gi) { return at(ws, P.groups[gi].off_X1); };
+  auto Ab = [&](int gi) { return at(ws, P.groups[gi].off_A); };
+  auto Bb = [&](int gi) { return at(ws, P.groups[gi].off_B); };
+  auto Cb = [&](int gi, int t) { return t == 0 ? at(ws, P.groups[gi].off_Q0) : at(ws, P.groups[gi].off_C); };
+  auto Qb = [&](int gi, int j) { return at(ws, (j & 1) ? P.groups[gi].off_Q0 : P.groups[gi].off_Q1); };  // Q_j, j >= 1
+  int rc;
+  std::vector<Entry> es;
+  for (int gi : gl) es.push_back({gi, X0(gi), X0(gi), Ab(gi), nullptr});
+  if ((rc = emit(PH_GRAM, es, 1.f, 0.f, 0.f, 2, 0, 1))) return rc;
+  for (int t = 0; t < T; ++t) {
+    const float a = c->ns_coeffs[t][0], b = c->ns_coeffs[t][1], cc = c->ns_coeffs[t][2];
+    const int last = t == T - 1;
+    es.clear();
+    for (int gi : gl) es.push_back({gi, Ab(gi), Ab(gi), Cb(gi, t), Ab(gi)});
+    if ((rc = emit(PH_POLY, es, cc, b, a, 0, 1, T == 1 ? 0 : 1))) return rc;
+    es.clear();
+    for (int gi : gl) {
+      if (t >= 1) es.push_back({gi, Cb(gi, t), Qb(gi, t), Qb(gi, t + 1), nullptr});
+      if (!last) es.push_back({gi, Cb(gi, t), Ab(gi), Bb(gi), nullptr});
+    }
+    if (!es.empty() && (rc = emit(PH_NSMUL, es, 1.f, 0.f, 0.f, 0, 1, last ? 0 : 1))) return rc;
+    if (!last) {
+      es.clear();
+      for (int gi : gl) es.push_back({gi, Cb(gi, t), Bb(gi), Ab(gi), nullptr});
+      if ((rc = emit(PH_NSMUL, es, 1.f, 0.f, 0.f, 0, 1, 1))) return rc;
+    }
+  }
+  es.clear();
+  for (int gi : gl) es.push_back({gi, Qb(gi, T), X0(gi), X1(gi), nullptr});
+  return emit(PH_APPLY, es, 1.f, 0.f, 0.f, 1, 0, 0);
+}
 
 // Fill host tables and NS launches for a concrete workspace.
 int build_device_plan(Plan& P, const dion2_matrix* mats, const dion2_config* c, void* ws) {
@@ -278,7 +393,7 @@ int build_device_plan(Plan& P, const dion2_matrix* mats, const dion2_config* c, 
     const size_t xel = P.bf16_ns ? 2 : 4;
     d.X0 = at(ws, g.off_X0 + (size_t)q.zi * g.p_pad * g.q_pad * xel);
     d.X1 = at(ws, g.off_X1 + (size_t)q.zi * g.p_pad * g.q_pad * xel);
-    d.final_in_x1 = (P.ns_steps & 1);
+    d.final_in_x1 = g.gs ? 1 : (P.ns_steps & 1);  // Gram-space: X_T = Q_T X_0 is written to X1
     d.gather_tile_base = gt_acc;
     d.gather_tiles_a = q.ga;
     d.gather_tiles_b = q.gb;
@@ -379,6 +494,7 @@ int build_device_plan(Plan& P, const dion2_matrix* mats, const dion2_config* c, 
       std::vector<int> by_bn[2];
       for (int gi = 0; gi < (int)P.groups.size(); ++gi) {
         const Group& g = P.groups[gi];
+        if (g.gs) continue;  // Gram-space groups: append_gram_space_launches
         int bn256 = ph == PH_APPLY ? 1 : (g.p_pad % 256 == 0);
         by_bn[bn256].push_back(gi);
       }
@@ -466,7 +582,7 @@ int build_device_plan(Plan& P, const dion2_matrix* mats, const dion2_config* c, 
       }
     }
   }
-  return DION2_OK;
+  return append_gram_space_launches(P, c, ws, pair_mode);
 }
 
 void ensure_device_attrs() {

@@ -10,6 +10,9 @@
 // (TMA write + MMA read), which caps the 1-CTA 128 x 256 tile near 65-70% of
 // peak (ncu: profiles/).
 //
+// Operand / output element type per launch: bf16 or fp16 (p.in_f16, p.out_f16; the
+// Gram-space products of reading R23 run on fp16 with fp32 accumulation).
+//
 // Roles per CTA (192 threads): warp 0 TMA producer (both CTAs; completion is
 // counted on the leader's full barrier), warp 1 TMEM allocator (both) + MMA
 // issuer (leader only), warps 2-5 epilogue (both; TMEM -> bf16 -> swizzled
@@ -69,6 +72,12 @@ __device__ __forceinline__ uint32_t pack_bf16x2(float lo, float hi) {
   __nv_bfloat162 v = __floats2bfloat162_rn(lo, hi);
   return *reinterpret_cast<uint32_t*>(&v);
 }
+__device__ __forceinline__ uint32_t pack_f16x2(float lo, float hi) {
+  __half2 v = __floats2half2_rn(lo, hi);
+  return *reinterpret_cast<uint32_t*>(&v);
+}
+// a/b operand format fields of the instruction descriptor: 1 = bf16, 0 = fp16
+constexpr uint32_t kIdescAbFmt = (7u << 7) | (7u << 10);
 
 }  // namespace
 
@@ -143,7 +152,7 @@ __global__ void __cluster_dims__(2, 1, 1) __launch_bounds__(192, 1)
   } else if (warp == 1) {
     if (lane == 0 && rank == 0) {
       // ---------------- MMA issuer (leader CTA)
-      const uint32_t idesc = p.b_kmajor ? kIdescK : kIdescMN;
+      const uint32_t idesc = (p.b_kmajor ? kIdescK : kIdescMN) & (p.in_f16 ? ~kIdescAbFmt : ~0u);
       int stage = 0;
       uint32_t phase = 0;
       int it = 0;
@@ -190,8 +199,9 @@ __global__ void __cluster_dims__(2, 1, 1) __launch_bounds__(192, 1)
       if (p.scale_sel) osc = p.ns_scale_all[2 * G.gmats[c.z] + (p.scale_sel - 1)];
       const float ca = p.cacc * osc, cc = p.cC * osc, dterm = p.diag * osc;
       const int64_t row = (int64_t)c.tm * 256 + row_in_tile;
-      const __nv_bfloat16* cin =
-          G.cin ? reinterpret_cast<const __nv_bfloat16*>(G.cin) + (int64_t)c.z * G.cin_mstride + row * G.cin_ld +
+      // cin holds 2-byte elements (bf16, or fp16 when in_f16)
+      const uint16_t* cin =
+          G.cin ? reinterpret_cast<const uint16_t*>(G.cin) + (int64_t)c.z * G.cin_mstride + row * G.cin_ld +
                       (int64_t)c.tn * 256
                 : nullptr;
       uint4 craw[4] = {};
@@ -206,13 +216,25 @@ __global__ void __cluster_dims__(2, 1, 1) __launch_bounds__(192, 1)
         float v[32];
         tmem_ld_32x32b_x32(tmem_base + acc * 256 + cc32 * 32 + ((uint32_t)(lg * 32) << 16), v);
         float cv[32];
+        if (p.in_f16) {
 #pragma unroll
-        for (int q = 0; q < 4; ++q) {
-          const __nv_bfloat162* h = reinterpret_cast<const __nv_bfloat162*>(&craw[q]);
+          for (int q = 0; q < 4; ++q) {
+            const __half2* h = reinterpret_cast<const __half2*>(&craw[q]);
 #pragma unroll
-          for (int e = 0; e < 4; ++e) {
-            cv[q * 8 + 2 * e] = __low2float(h[e]);
-            cv[q * 8 + 2 * e + 1] = __high2float(h[e]);
+            for (int e = 0; e < 4; ++e) {
+              cv[q * 8 + 2 * e] = __low2float(h[e]);
+              cv[q * 8 + 2 * e + 1] = __high2float(h[e]);
+            }
+          }
+        } else {
+#pragma unroll
+          for (int q = 0; q < 4; ++q) {
+            const __nv_bfloat162* h = reinterpret_cast<const __nv_bfloat162*>(&craw[q]);
+#pragma unroll
+            for (int e = 0; e < 4; ++e) {
+              cv[q * 8 + 2 * e] = __low2float(h[e]);
+              cv[q * 8 + 2 * e + 1] = __high2float(h[e]);
+            }
           }
         }
         if (cin && cc32 + 1 < 8) {
@@ -231,7 +253,7 @@ __global__ void __cluster_dims__(2, 1, 1) __launch_bounds__(192, 1)
         __syncwarp();
         uint32_t pk[16];
 #pragma unroll
-        for (int q = 0; q < 16; ++q) pk[q] = pack_bf16x2(o[2 * q], o[2 * q + 1]);
+        for (int q = 0; q < 16; ++q) pk[q] = p.out_f16 ? pack_f16x2(o[2 * q], o[2 * q + 1]) : pack_bf16x2(o[2 * q], o[2 * q + 1]);
 #pragma unroll
         for (int q = 0; q < 4; ++q)
           *reinterpret_cast<uint4*>(buf + lane * 64 + ((q ^ ((lane >> 1) & 3)) << 4)) =
@@ -244,9 +266,9 @@ __global__ void __cluster_dims__(2, 1, 1) __launch_bounds__(192, 1)
           __syncwarp();
 #pragma unroll
           for (int e = 0; e < 32; ++e) {
-            const __nv_bfloat16 h = __float2bfloat16_rn(o[e]);
-            *reinterpret_cast<__nv_bfloat16*>(tbuf + e * 64 + ((((lane >> 3) ^ ((e >> 1) & 3))) << 4) +
-                                              (lane & 7) * 2) = h;
+            const uint16_t h = p.out_f16 ? __half_as_ushort(__float2half_rn(o[e]))
+                                         : __bfloat16_as_ushort(__float2bfloat16_rn(o[e]));
+            *reinterpret_cast<uint16_t*>(tbuf + e * 64 + ((((lane >> 3) ^ ((e >> 1) & 3))) << 4) + (lane & 7) * 2) = h;
           }
         }
         fence_proxy_async_smem();

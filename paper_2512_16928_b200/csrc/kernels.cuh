@@ -92,6 +92,8 @@ struct NsParams {
   int sym;                   // symmetric output: upper-triangle tiles only, mirrored by the epilogue (pair kernel)
   const float* ns_scale_all; // [n_mats][2]
   int b_kmajor;
+  int in_f16;                // operands (and cin) are fp16, else bf16 (pair kernel only)
+  int out_f16;               // output written as fp16, else bf16 (pair kernel only)
 };
 
 // tcgen05 path (k_ns_tcgen05.cu): tensor maps for the TMA operand loads.

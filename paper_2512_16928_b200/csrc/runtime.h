@@ -15,11 +15,11 @@
 namespace dion2rt {
 using namespace dion2;
 
-constexpr int kNumPhases = 13;
+constexpr int kNumPhases = 14;
 extern const char* kPhaseNames[kNumPhases];
 enum Phase {
   PH_K1 = 0, PH_SELECT, PH_GATHER, PH_NORM, PH_GRAM, PH_POLY, PH_APPLY, PH_SCATTER, PH_FULLDECAY,
-  PH_GATHER_ROWS, PH_GATHER_COLS, PH_SCATTER_ROWS, PH_SCATTER_COLS
+  PH_GATHER_ROWS, PH_GATHER_COLS, PH_SCATTER_ROWS, PH_SCATTER_COLS, PH_NSMUL
 };
 
 extern std::mutex g_mu;
@@ -55,6 +55,8 @@ struct Group {
   int p_pad, q_pad, count;
   std::vector<int> mats;  // global matrix indices
   size_t off_X0, off_X1, off_A, off_B, off_gmats;
+  int gs;                           // Newton-Schulz in Gram space (reading R23)
+  size_t off_C, off_Q0, off_Q1;     // Gram-space p x p buffers (gs only)
 };
 
 struct Launch {

@@ -20,6 +20,8 @@ MAX_NS_STEPS = 16
 AXIS = {"rows": 0, "cols": 1, "auto": 2}
 PRECISION = {"bf16": 0, "fp32": 1}
 SELECT = {"l1": 0, "random": 1}
+NS_FORM = {"auto": 0, "direct": 1, "gram": 2}
+ABI_VERSION = 3  # include/dion2.h DION2_ABI_VERSION
 STATUS = {0: "OK", 1: "EINVAL_CONFIG", 2: "EINVAL_SHAPE", 3: "EWORKSPACE", 4: "EUNSUPPORTED",
           5: "ECUDA", 6: "ENCCL", 7: "ENONFINITE"}
 EXPORTED = ["dion2_config_init", "dion2_workspace_size", "dion2_step", "dion2_step_batched", "dion2_get_status",
@@ -41,7 +43,8 @@ class Dion2Config(ctypes.Structure):
                 ("ns_steps", ctypes.c_int32), ("ns_coeffs", (ctypes.c_float * 3) * MAX_NS_STEPS),
                 ("ns_eps", ctypes.c_float), ("axis", ctypes.c_int32), ("select", ctypes.c_int32),
                 ("precision", ctypes.c_int32), ("grad_dtype", ctypes.c_int32), ("decay_mode", ctypes.c_int32),
-                ("scale_mode", ctypes.c_int32), ("seed", ctypes.c_uint64), ("step", ctypes.c_uint64)]
+                ("scale_mode", ctypes.c_int32), ("seed", ctypes.c_uint64), ("step", ctypes.c_uint64),
+                ("ns_form", ctypes.c_int32), ("reserved0", ctypes.c_int32)]
 
 
 class Dion2Shard(ctypes.Structure):
@@ -79,6 +82,8 @@ def _lib():
         lib.dion2_phase_name.restype = ctypes.c_char_p
         lib.dion2_last_launch_count.restype = ctypes.c_int32
         lib.dion2_abi_version.restype = ctypes.c_int32
+        if lib.dion2_abi_version() != ABI_VERSION:
+            raise RuntimeError(f"libdion2.so ABI {lib.dion2_abi_version()} != binding ABI {ABI_VERSION}; rebuild it")
         I32, I64 = P(ctypes.c_int32), P(ctypes.c_int64)
         lib.dion2_dist_info.argtypes = [P(Dion2Shard), ctypes.c_int32, P(Dion2Config), ctypes.c_int32, ctypes.c_int32,
                                         I32, I32, I64, I64, I64, I64, P(ctypes.c_size_t)]
@@ -104,7 +109,9 @@ def make_config(alpha: float = 0.25, mu: float = 0.95, lr: float = 0.02, ns_step
                 ns_coeffs: Optional[Sequence[Tuple[float, float, float]]] = None, ns_eps: float = 1e-7,
                 axis: str = "auto", precision: str = "bf16", grad_dtype: Optional[torch.dtype] = None,
                 decay_mode: int = 0, scale_mode: int = 0, select: str = "l1", seed: int = 0,
-                step: int = 0) -> Dion2Config:
+                step: int = 0, ns_form: str = "auto") -> Dion2Config:
+    """ns_form: "auto" | "direct" | "gram" -- how the bf16 Newton-Schulz map is evaluated
+    (include/dion2.h dion2_ns_form, reading R23)."""
     cfg = Dion2Config()
     _lib().dion2_config_init(ctypes.byref(cfg))
     cfg.alpha, cfg.mu, cfg.lr, cfg.ns_steps, cfg.ns_eps = alpha, mu, lr, ns_steps, ns_eps
@@ -119,6 +126,7 @@ def make_config(alpha: float = 0.25, mu: float = 0.95, lr: float = 0.02, ns_step
     cfg.decay_mode, cfg.scale_mode = decay_mode, scale_mode
     cfg.select = SELECT[select]
     cfg.seed, cfg.step = seed, step
+    cfg.ns_form = NS_FORM[ns_form]
     return cfg
 
 

@@ -55,11 +55,19 @@ def _tie_equivalent(K_gpu, K_ref, scores):
 def run_parity(shapes: Sequence[Tuple[int, int]], alpha: float, axis: str = "auto", precision: str = "bf16",
                steps: int = 10, seed: int = 0, mu: float = 0.95, lr: float = 0.02, row_scaled: bool = False,
                decay_mode: int = 0, check_bitwise: bool = True, device: str = "cuda", select: str = "l1",
-               sel_seed: int = 0, m_transposed: bool = False, grad_bf16: bool = False) -> ParityResult:
-    """m_transposed: store M transposed (cols x rows) for every column-mode matrix."""
+               sel_seed: int = 0, m_transposed: bool = False, grad_bf16: bool = False, ns_form: str = "auto",
+               ns_coeffs=None) -> ParityResult:
+    """m_transposed: store M transposed (cols x rows) for every column-mode matrix.
+    ns_form: "auto" | "direct" | "gram" (reading R23); ns_coeffs: per-iteration (a, b, c), T = len."""
     res = ParityResult()
     cfg_o = oracle_cfg(alpha, axis, mu, lr, decay_mode)
     cfg_o.select, cfg_o.seed = select, sel_seed
+    ns_kw = dict(ns_form=ns_form)
+    if ns_coeffs is not None:
+        # the library holds the coefficients as fp32: give the oracle the same values
+        ns_coeffs = [tuple(float(np.float32(v)) for v in abc) for abc in ns_coeffs]
+        cfg_o.ns_coeffs = list(ns_coeffs)
+        ns_kw.update(ns_steps=len(ns_coeffs), ns_coeffs=ns_coeffs)
     W0 = [gen_w0(m, n, seed, i) for i, (m, n) in enumerate(shapes)]
     Wg = [torch.from_numpy(w).to(device) for w in W0]
     mts = [m_transposed and O.resolve_axis(m, n, cfg_o.axis) == O.AXIS_COLS for (m, n) in shapes]
@@ -68,7 +76,7 @@ def run_parity(shapes: Sequence[Tuple[int, int]], alpha: float, axis: str = "aut
     Wr = [w.astype(np.float64) for w in W0]
     Mr = [np.zeros((m, n)) for (m, n) in shapes]
     opt = Dion2(alpha=alpha, mu=mu, lr=lr, axis=axis, precision=precision, decay_mode=decay_mode, select=select,
-                seed=sel_seed)
+                seed=sel_seed, **ns_kw)
     ks = []
     for (m, n) in shapes:
         ax = O.resolve_axis(m, n, cfg_o.axis)

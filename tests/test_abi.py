@@ -37,7 +37,7 @@ def test_exports_every_declared_symbol(lib):
 
 
 def test_abi_version(lib):
-    assert lib.dion2_abi_version() == 2
+    assert lib.dion2_abi_version() == 3
 
 
 def test_config_defaults(lib):
@@ -47,6 +47,31 @@ def test_config_defaults(lib):
     assert cfg.ns_steps == 5 and abs(cfg.ns_eps - 1e-7) < 1e-12
     assert [round(x, 4) for x in cfg.ns_coeffs[0]] == [3.4445, -4.775, 2.0315]
     assert cfg.axis == 2 and cfg.precision == 0 and cfg.decay_mode == 0
+    assert cfg.ns_form == 0 and cfg.reserved0 == 0
+
+
+@pytest.mark.parametrize("form,reserved", [(3, 0), (-1, 0), (0, 1)])
+def test_ns_form_validation(lib, form, reserved):
+    cfg = D.make_config()
+    cfg.ns_form, cfg.reserved0 = form, reserved
+    out = ctypes.c_size_t(0)
+    assert lib.dion2_workspace_size(_mats([(64, 64)]), 1, ctypes.byref(cfg), ctypes.byref(out)) == 1  # DION2_EINVAL_CONFIG
+
+
+def test_gram_form_workspace(lib):
+    # Gram-space NS (reading R23) needs three extra p x p buffers per shape group; AUTO picks
+    # it for q >= 2p only, FP32 precision never uses it
+    wide, square = [(2048, 8192)], [(2048, 2048)]
+    _, auto_w = _size(lib, wide)
+    _, direct_w = _size(lib, wide, ns_form="direct")
+    _, gram_w = _size(lib, wide, ns_form="gram")
+    assert auto_w == gram_w and gram_w - direct_w >= 3 * 512 * 512 * 2
+    _, auto_s = _size(lib, square, alpha=1.0)
+    _, direct_s = _size(lib, square, alpha=1.0, ns_form="direct")
+    assert auto_s == direct_s
+    _, f32_d = _size(lib, wide, precision="fp32", ns_form="direct")
+    _, f32_g = _size(lib, wide, precision="fp32", ns_form="gram")
+    assert f32_d == f32_g
 
 
 def _mats(shapes):

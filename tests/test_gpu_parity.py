@@ -65,6 +65,36 @@ def test_small_p_bf16_error_is_the_recipe_floor():
     _assert(run_parity([(256, 512), (512, 256)], 0.125, "auto", "bf16", steps=3), 3e-2)
 
 
+# ---------------------------------------------------------------- NS evaluation form (reading R23)
+def test_gram_form_is_tighter_on_wide_x():
+    """AUTO picks the Gram-space form for q >= 2p; X is rounded to bf16 once instead of T
+    times, so its error is well inside the bf16 gate (emulated: 0.3-0.5%)."""
+    res = run_parity([(512, 2048), (2048, 512), (1024, 4096)], 0.25, "auto", "bf16", steps=2, row_scaled=True)
+    _assert(res, 1e-2)
+
+
+@pytest.mark.parametrize("form", ["direct", "gram"])
+def test_both_ns_forms_on_the_1b_layer(form):
+    _assert(run_parity(layer_set_1b(layers=1), 0.25, "auto", "bf16", steps=1, ns_form=form), BF16_TOL)
+
+
+@pytest.mark.parametrize("coeffs", [
+    [(3.4445, -4.7750, 2.0315)],                               # T = 1: C_0 is Q_T
+    [(3.4445, -4.7750, 2.0315)] * 2,                           # T = 2: no A update after t = 0
+    [(1.5, -0.5, 0.0)] * 3,                                    # cubic Newton-Schulz (c = 0)
+    [(3.4445, -4.7750, 2.0315)] * 4 + [(2.0, -1.5, 0.5)],      # per-iteration coefficients
+])
+@pytest.mark.parametrize("form", ["direct", "gram"])
+def test_ns_schedules(coeffs, form):
+    shapes = [(256, 1024), (1024, 256), (130, 1030), (300, 520)]
+    _assert(run_parity(shapes, 0.3, "auto", "bf16", steps=2, ns_form=form, ns_coeffs=coeffs), BF16_TOL)
+
+
+def test_gram_form_forced_on_square_x():
+    # q = p: AUTO would pick DIRECT; forcing GRAM must still be within the bf16 gate
+    _assert(run_parity([(384, 384), (512, 768)], 1.0, "auto", "bf16", steps=2, ns_form="gram"), BF16_TOL)
+
+
 def test_alpha1_is_full_muon_fp32():
     _assert(run_parity([(128, 384)], 1.0, "auto", "fp32", steps=5), FP32_TOL)
 

@@ -130,6 +130,25 @@ def test_ns_triple_loop_brute_force():
     np.testing.assert_allclose(O.newton_schulz(X), np.array(Y), rtol=0, atol=1e-14)
 
 
+@pytest.mark.parametrize("shape,coeffs", [((16, 96), None), ((40, 90), [(1.5, -0.5, 0.0)] * 3),
+                                          ((24, 200), [(3.4445, -4.7750, 2.0315)])])
+def test_gram_space_form_is_the_same_map(shape, coeffs):
+    """Reading R23 (the GPU's Gram-space evaluation) computes the oracle's map: with
+    A_t = X_t X_t^T and C_t = a I + b A_t + c A_t^2, X_{t+1} = C_t X_t gives
+    A_{t+1} = C_t A_t C_t and X_T = (C_{T-1} ... C_0) X_0.  Checked in fp64 against
+    O.newton_schulz (independent: the test carries its own p x p recursion)."""
+    coeffs = coeffs or O.DEFAULT_NS_COEFFS
+    X = np.random.default_rng(11).standard_normal(shape)
+    X0 = X / (np.linalg.norm(X) + O.DEFAULT_NS_EPS)
+    A, Q = X0 @ X0.T, np.eye(shape[0])
+    for a, b, c in coeffs:
+        C = a * np.eye(shape[0]) + b * A + c * (A @ A)
+        Q, A = C @ Q, C @ (C @ A)
+    got = Q @ X0
+    want = O.newton_schulz(X, coeffs)
+    assert np.linalg.norm(got - want) / np.linalg.norm(want) < 1e-12
+
+
 def test_ns_symmetries():
     rng = np.random.default_rng(7)
     X = rng.standard_normal((16, 48))
