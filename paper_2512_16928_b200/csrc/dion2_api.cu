@@ -131,6 +131,12 @@ std::string plan_key(const dion2_matrix* mats, int n, const dion2_config* c, voi
   put(&c->decay_mode, 4);
   put(&c->scale_mode, 4);
   put(&c->ns_form, 4);
+  // kernel-variant switches read at plan build (tests and measurements flip them)
+  for (const char* v : {"DION2_NS_PAIR", "DION2_NS_SYM", "DION2_NS_CHAIN", "DION2_NS_SERPENTINE"}) {
+    const char* e = getenv(v);
+    k.append(e ? e : "-");
+    k.push_back('|');
+  }
   return k;
 }
 
@@ -218,6 +224,7 @@ int build_layout(Plan& P, const dion2_matrix* mats, int n, const dion2_config* c
     P.off_fl_sprefix[l] = take(4 * (size_t)n);
   }
   for (auto& g : P.groups) g.off_gmats = take(4 * (size_t)g.count);
+  P.off_chain_entries = take(4 * (size_t)n);
   P.off_nsscale = take(8 * (size_t)n);
   for (int i = 0; i < n; ++i) {
     MatPlan& q = P.mp[i];
@@ -259,6 +266,86 @@ int build_layout(Plan& P, const dion2_matrix* mats, int n, const dion2_config* c
 //   apply  X1  = s Q_T X0                             (bf16)
 // Every p x p product is a polynomial in A_0, hence symmetric: upper-triangle pair tiles,
 // mirrored.  Q_T is written as bf16 (the apply operand), everything else as fp16.
+// The Gram-space op list of one matrix on the five p x p buffers (A, C, Q0, Q1, B), in the
+// order poly, C.A, C.Q, C.B per iteration (C.Q between the two dependent products hides
+// C.B's wait for C.A), with each op's dependency: the latest earlier op that wrote one of
+// its operands or read / wrote its output buffer.
+static std::vector<ChainOp> chain_ops(const dion2_config* c, int T) {
+  enum { bA = 0, bC = 1, bQ0 = 2, bQ1 = 3, bB = 4 };
+  auto Cb = [](int t) { return t == 0 ? (int)bQ0 : (int)bC; };  // C_0 doubles as Q_1
+  auto Qb = [](int j) { return (j & 1) ? (int)bQ0 : (int)bQ1; };  // Q_j, j >= 1
+  std::vector<ChainOp> ops;
+  int last_w[kChainBufs], last_r[kChainBufs];
+  for (int i = 0; i < kChainBufs; ++i) last_w[i] = last_r[i] = -1;
+  auto add = [&](int a, int b, int out, int cin, int out_f16, float cacc, float cC, float diag) {
+    ChainOp o{};
+    o.a = (int8_t)a; o.b = (int8_t)b; o.out = (int8_t)out; o.cin = (int8_t)cin; o.out_f16 = (int8_t)out_f16;
+    o.cacc = cacc; o.cC = cC; o.diag = diag;
+    int dep = std::max({last_w[a], last_w[b], last_w[out], last_r[out]});
+    if (cin >= 0) dep = std::max(dep, last_w[cin]);
+    o.dep = (int8_t)dep;
+    o.cin_dep = (int8_t)(cin >= 0 ? last_w[cin] : -1);
+    const int idx = (int)ops.size();
+    last_r[a] = std::max(last_r[a], idx);
+    last_r[b] = std::max(last_r[b], idx);
+    if (cin >= 0) last_r[cin] = std::max(last_r[cin], idx);
+    last_w[out] = idx;
+    ops.push_back(o);
+  };
+  for (int t = 0; t < T; ++t) {
+    const float a = c->ns_coeffs[t][0], b = c->ns_coeffs[t][1], cc = c->ns_coeffs[t][2];
+    const bool last = t == T - 1;
+    add(bA, bA, Cb(t), bA, T == 1 ? 0 : 1, cc, b, a);                  // C_t = a I + b A + c A A
+    if (!last) add(Cb(t), bA, bB, -1, 1, 1.f, 0.f, 0.f);               // B = C_t A
+    if (t >= 1) add(Cb(t), Qb(t), Qb(t + 1), -1, last ? 0 : 1, 1.f, 0.f, 0.f);  // Q_{t+1} = C_t Q_t
+    if (!last) add(Cb(t), bB, bA, -1, 1, 1.f, 0.f, 0.f);               // A = C_t B
+  }
+  return ops;
+}
+
+// One chain launch per kMaxGroups Gram-space groups; the entry table (group, z), largest
+// p first, lives in the plan's uploaded table region.
+static int append_chain_launches(Plan& P, const dion2_config* c, void* ws, const std::vector<int>& gl) {
+  const std::vector<ChainOp> ops = chain_ops(c, P.ns_steps);
+  if ((int)ops.size() > kMaxChainOps) return DION2_EUNSUPPORTED;
+  int32_t* ent_host = reinterpret_cast<int32_t*>(P.host_tables.data() + (P.off_chain_entries - P.off_desc));
+  const int32_t* ent_dev = (const int32_t*)tab(P, P.off_chain_entries);
+  int ent_off = 0;
+  for (size_t s0 = 0; s0 < gl.size(); s0 += kMaxGroups) {
+    Launch L{};
+    L.phase = PH_NSMUL;
+    L.kind = 4;
+    L.chain = std::make_shared<NsChainParams>();
+    NsChainParams& cp = *L.chain;
+    memset(&cp, 0, sizeof(cp));
+    cp.ngroups = (int)std::min<size_t>(kMaxGroups, gl.size() - s0);
+    cp.nops = (int)ops.size();
+    for (size_t i = 0; i < ops.size(); ++i) cp.ops[i] = ops[i];
+    std::vector<std::pair<int, int32_t>> ents;  // (p_pad, packed)
+    for (int j = 0; j < cp.ngroups; ++j) {
+      const Group& g = P.groups[gl[s0 + j]];
+      const size_t offs[kChainBufs] = {g.off_A, g.off_C, g.off_Q0, g.off_Q1, g.off_B};
+      for (int b = 0; b < kChainBufs; ++b) {
+        void* base = at(ws, offs[b]);
+        cp.buf[j][b] = base;
+        if (!make_map(&cp.ld[j][b], base, g.p_pad, g.p_pad, g.count, 64, 128)) return DION2_ECUDA;
+        if (!make_map(&cp.st[j][b], base, g.p_pad, g.p_pad, g.count, 32, 32, CU_TENSOR_MAP_SWIZZLE_64B))
+          return DION2_ECUDA;
+      }
+      cp.mstride[j] = (long long)g.p_pad * g.p_pad;
+      cp.p_pad[j] = g.p_pad;
+      for (int z = 0; z < g.count; ++z) ents.push_back({g.p_pad, (int32_t)((j << 24) | z)});
+    }
+    std::stable_sort(ents.begin(), ents.end(), [](const auto& x, const auto& y) { return x.first > y.first; });
+    for (size_t i = 0; i < ents.size(); ++i) ent_host[ent_off + i] = ents[i].second;
+    cp.entries = ent_dev + ent_off;
+    cp.n_entries = (int)ents.size();
+    ent_off += (int)ents.size();
+    P.ns_launches.push_back(L);
+  }
+  return DION2_OK;
+}
+
 static int append_gram_space_launches(Plan& P, const dion2_config* c, void* ws, int pair_mode) {
   std::vector<int> gl;
   for (int gi = 0; gi < (int)P.groups.size(); ++gi)
@@ -272,6 +359,10 @@ static int append_gram_space_launches(Plan& P, const dion2_config* c, void* ws, 
   };
   // one launch per kMaxGroups entries; kind: 3 = pair (sym p x p products, or apply under
   // DION2_NS_PAIR=all), 1 = 1-SM BN 256 (apply)
+  const bool sym_on = !(getenv("DION2_NS_SYM") && atoi(getenv("DION2_NS_SYM")) == 0);
+  const char* serp_env = getenv("DION2_NS_SERPENTINE");
+  const bool serpentine = !serp_env || atoi(serp_env) != 0;
+  unsigned flip = 0;
   auto emit = [&](int phase, const std::vector<Entry>& es, float cacc, float cC, float diag, int scale_sel,
                   int in_f16, int out_f16) -> int {
     const bool apply = phase == PH_APPLY;
@@ -286,9 +377,12 @@ static int append_gram_space_launches(Plan& P, const dion2_config* c, void* ws, 
       np.ngroups = (int)std::min<size_t>(kMaxGroups, es.size() - s0);
       np.ns_scale_all = scale_all;
       np.cacc = cacc; np.cC = cC; np.diag = diag; np.scale_sel = scale_sel;
-      np.sym = apply ? 0 : 1;
+      np.sym = (apply || !sym_on) ? 0 : 1;
       np.b_kmajor = apply ? 0 : 1;
       np.in_f16 = in_f16; np.out_f16 = out_f16;
+      // alternate the walk direction between consecutive p x p launches: a launch starts on the
+      // matrices the previous one wrote last (still in L2)
+      np.reverse = (!apply && serpentine) ? (int)(flip++ & 1) : 0;
       int tiles = 0;
       for (int j = 0; j < np.ngroups; ++j) {
         const Entry& e = es[s0 + j];
@@ -331,6 +425,20 @@ static int append_gram_space_launches(Plan& P, const dion2_config* c, void* ws, 
   std::vector<Entry> es;
   for (int gi : gl) es.push_back({gi, X0(gi), X0(gi), Ab(gi), nullptr});
   if ((rc = emit(PH_GRAM, es, 1.f, 0.f, 0.f, 2, 0, 1))) return rc;
+  // p x p products: one persistent chain launch (a CTA pair runs one matrix's whole op list,
+  // k_ns_chain_pair.cu) when there are enough matrices to fill the GPU, else one flat launch
+  // per op over all matrices.  DION2_NS_CHAIN=0|1 overrides.
+  int n_gs = 0;
+  for (int gi : gl) n_gs += P.groups[gi].count;
+  const char* chain_env = getenv("DION2_NS_CHAIN");
+  const int pairs = (g_sm_count > 0 ? g_sm_count : 148) / 2;
+  const bool use_chain = chain_env ? atoi(chain_env) != 0 : false && n_gs >= pairs / 2;
+  if (use_chain) {
+    if ((rc = append_chain_launches(P, c, ws, gl))) return rc;
+    es.clear();
+    for (int gi : gl) es.push_back({gi, Qb(gi, T), X0(gi), X1(gi), nullptr});
+    return emit(PH_APPLY, es, 1.f, 0.f, 0.f, 1, 0, 0);
+  }
   for (int t = 0; t < T; ++t) {
     const float a = c->ns_coeffs[t][0], b = c->ns_coeffs[t][1], cc = c->ns_coeffs[t][2];
     const int last = t == T - 1;
@@ -593,6 +701,7 @@ void ensure_device_attrs() {
   ns_tc_set_attrs();
   launch_fast_paths_attrs();
   ns_pair_set_attrs();
+  ns_chain_set_attrs();
   cudaFuncSetAttribute(k_topk_select, cudaFuncAttributeMaxDynamicSharedMemorySize, 4 * DION2_MAX_SELECT_DIM);
   cudaFuncSetAttribute(k_full_decay, cudaFuncAttributeMaxDynamicSharedMemorySize, DION2_MAX_SELECT_DIM);
   g_attr_done = true;
@@ -610,7 +719,12 @@ int run_ns(Plan& P, const dion2_config* c, Launcher& L, cudaStream_t s, bool do_
   }
   for (const Launch& ln : P.ns_launches) {
     L.begin(ln.phase);
-    if (ln.kind == 3) {
+    if (ln.kind == 4) {
+      static const int chain_pairs = getenv("DION2_CHAIN_PAIRS") ? atoi(getenv("DION2_CHAIN_PAIRS")) : 0;
+      int grid = std::min(2 * ln.chain->n_entries, sms & ~1);
+      if (chain_pairs > 0) grid = std::min(grid, 2 * chain_pairs);
+      launch_ns_chain(grid, s, *ln.chain);
+    } else if (ln.kind == 3) {
       launch_ns_pair(std::min(2 * ln.tc.p.total_tiles, sms & ~1), s, ln.tc);
     } else if (ln.kind == 0 || ln.kind == 1) {
       launch_ns_tc(ln.bn, std::min(ln.tc.p.total_tiles, sms), s, ln.tc);

@@ -216,7 +216,7 @@ __global__ void __launch_bounds__(192, 1) k_ns_gemm_tc(const __grid_constant__ N
           u.y = pack_bf16x2(o[q * 8 + 2], o[q * 8 + 3]);
           u.z = pack_bf16x2(o[q * 8 + 4], o[q * 8 + 5]);
           u.w = pack_bf16x2(o[q * 8 + 6], o[q * 8 + 7]);
-          *reinterpret_cast<uint4*>(buf + lane * 64 + ((q ^ ((lane >> 1) & 3)) << 4)) = u;
+          sts128(smem_u32(buf) + lane * 64 + ((q ^ ((lane >> 1) & 3)) << 4), u);
         }
         fence_proxy_async_smem();
         __syncwarp();

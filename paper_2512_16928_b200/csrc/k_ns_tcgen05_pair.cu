@@ -13,7 +13,7 @@
 // Operand / output element type per launch: bf16 or fp16 (p.in_f16, p.out_f16; the
 // Gram-space products of reading R23 run on fp16 with fp32 accumulation).
 //
-// Roles per CTA (192 threads): warp 0 TMA producer (both CTAs; completion is
+// Roles per CTA (320 threads): warp 0 TMA producer (both CTAs; completion is
 // counted on the leader's full barrier), warp 1 TMEM allocator (both) + MMA
 // issuer (leader only), warps 2-5 epilogue (both; TMEM -> bf16 -> swizzled
 // smem -> TMA store).  TMEM: two 256-column fp32 accumulators.
@@ -24,7 +24,12 @@ namespace dion2 {
 namespace {
 
 constexpr int kBK = 64;
-constexpr int kStagesPair = 6;
+constexpr int kStagesPair = 5;
+// 8 epilogue warps: two per TMEM lane group, each draining half of the tile's 256 columns
+// (with K = p = 512 the 1-warp-per-lane-group epilogue was the bottleneck: ncu showed the
+// MMA waiting on TMEM release while the producer waited on a full ring)
+constexpr int kEpiWarps = 8;
+constexpr int kPairThreads = 64 + 32 * kEpiWarps;
 constexpr uint32_t kAB = 128 * kBK * 2;      // A half-tile per CTA (128 rows x 64 k)
 constexpr uint32_t kBB = 128 * kBK * 2;      // B half-tile per CTA (128 n x 64 k)
 constexpr uint32_t kStage = kAB + kBB;       // 32 KiB
@@ -37,6 +42,7 @@ struct TileCoord {
 };
 
 __device__ __forceinline__ TileCoord decode_tile(const NsParams& p, int t) {
+  if (p.reverse) t = p.total_tiles - 1 - t;
   int g = 0;
 #pragma unroll
   for (int i = 1; i < kMaxGroups; ++i)
@@ -81,9 +87,9 @@ constexpr uint32_t kIdescAbFmt = (7u << 7) | (7u << 10);
 
 }  // namespace
 
-constexpr int ns_pair_smem_bytes() { return 1024 + kStagesPair * (int)kStage + 1024 + 4 * 4 * 2048; }
+constexpr int ns_pair_smem_bytes() { return 1024 + kStagesPair * (int)kStage + 1024 + kEpiWarps * 4 * 2048; }
 
-__global__ void __cluster_dims__(2, 1, 1) __launch_bounds__(192, 1)
+__global__ void __cluster_dims__(2, 1, 1) __launch_bounds__(kPairThreads, 1)
     k_ns_gemm_tc_pair(const __grid_constant__ NsTcParams P) {
   constexpr int S = kStagesPair;
   extern __shared__ uint8_t smem_raw[];
@@ -107,7 +113,7 @@ __global__ void __cluster_dims__(2, 1, 1) __launch_bounds__(192, 1)
     }
     for (int i = 0; i < 2; ++i) {
       mbar_init(&tfull_bar[i], 1);
-      mbar_init(&tempty_bar[i], 8);  // one arrival per epilogue warp of both CTAs
+      mbar_init(&tempty_bar[i], 2 * kEpiWarps);  // one arrival per epilogue warp of both CTAs
     }
     fence_mbar_init();
     for (int gi = 0; gi < p.ngroups; ++gi) {
@@ -183,8 +189,11 @@ __global__ void __cluster_dims__(2, 1, 1) __launch_bounds__(192, 1)
       }
     }
   } else {
-    // ---------------- epilogue (both CTAs; warps 2..5 -> TMEM lane groups 2,3,0,1)
+    // ---------------- epilogue (both CTAs; warps 2..9 -> TMEM lane groups 2,3,0,1,2,3,0,1;
+    // warps 2..5 drain columns 0..127, warps 6..9 columns 128..255)
+    const int ew = warp - 2;
     const int lg = warp & 3;
+    const int c0 = (ew >> 2) * 4;  // first 32-column chunk of this warp
     const int row_in_tile = (int)rank * 128 + lg * 32 + lane;
     const uint32_t leader_tempty[2] = {mapa_shared(smem_u32(&tempty_bar[0]), 0),
                                        mapa_shared(smem_u32(&tempty_bar[1]), 0)};
@@ -207,12 +216,12 @@ __global__ void __cluster_dims__(2, 1, 1) __launch_bounds__(192, 1)
       uint4 craw[4] = {};
       if (cin) {
 #pragma unroll
-        for (int q = 0; q < 4; ++q) craw[q] = reinterpret_cast<const uint4*>(cin)[q];
+        for (int q = 0; q < 4; ++q) craw[q] = reinterpret_cast<const uint4*>(cin + c0 * 32)[q];
       }
       mbar_wait(&tfull_bar[acc], acc_phase);
       tc_fence_after();
 #pragma unroll 1
-      for (int cc32 = 0; cc32 < 8; ++cc32) {
+      for (int cc32 = c0; cc32 < c0 + 4; ++cc32) {
         float v[32];
         tmem_ld_32x32b_x32(tmem_base + acc * 256 + cc32 * 32 + ((uint32_t)(lg * 32) << 16), v);
         float cv[32];
@@ -237,7 +246,7 @@ __global__ void __cluster_dims__(2, 1, 1) __launch_bounds__(192, 1)
             }
           }
         }
-        if (cin && cc32 + 1 < 8) {
+        if (cin && cc32 + 1 < c0 + 4) {
 #pragma unroll
           for (int q = 0; q < 4; ++q) craw[q] = reinterpret_cast<const uint4*>(cin + (cc32 + 1) * 32)[q];
         }
@@ -248,7 +257,7 @@ __global__ void __cluster_dims__(2, 1, 1) __launch_bounds__(192, 1)
         // 4 staging buffers per warp (SWIZZLE_64B layout: 16-B chunk q of row r at
         // q ^ ((r >> 1) & 3)); a buffer is rewritten once the store 4 commits back has read it
         const bool mirror = p.sym && c.tm != c.tn;
-        uint8_t* buf = stage_base + (lg * 4 + sbuf) * 2048;
+        uint8_t* buf = stage_base + (ew * 4 + sbuf) * 2048;
         if (lane == 0) bulk_wait_read<3>();
         __syncwarp();
         uint32_t pk[16];
@@ -256,9 +265,9 @@ __global__ void __cluster_dims__(2, 1, 1) __launch_bounds__(192, 1)
         for (int q = 0; q < 16; ++q) pk[q] = p.out_f16 ? pack_f16x2(o[2 * q], o[2 * q + 1]) : pack_bf16x2(o[2 * q], o[2 * q + 1]);
 #pragma unroll
         for (int q = 0; q < 4; ++q)
-          *reinterpret_cast<uint4*>(buf + lane * 64 + ((q ^ ((lane >> 1) & 3)) << 4)) =
-              make_uint4(pk[4 * q], pk[4 * q + 1], pk[4 * q + 2], pk[4 * q + 3]);
-        uint8_t* tbuf = stage_base + (lg * 4 + ((sbuf + 1) & 3)) * 2048;
+          sts128(smem_u32(buf) + lane * 64 + ((q ^ ((lane >> 1) & 3)) << 4),
+                 make_uint4(pk[4 * q], pk[4 * q + 1], pk[4 * q + 2], pk[4 * q + 3]));
+        uint8_t* tbuf = stage_base + (ew * 4 + ((sbuf + 1) & 3)) * 2048;
         if (mirror) {
           // the transposed 32 x 32 chunk: element (row e, col lane) = o[e]; tbuf was used by
           // the 3rd most recent store (the current one is not issued yet)
@@ -268,7 +277,7 @@ __global__ void __cluster_dims__(2, 1, 1) __launch_bounds__(192, 1)
           for (int e = 0; e < 32; ++e) {
             const uint16_t h = p.out_f16 ? __half_as_ushort(__float2half_rn(o[e]))
                                          : __bfloat16_as_ushort(__float2bfloat16_rn(o[e]));
-            *reinterpret_cast<uint16_t*>(tbuf + e * 64 + ((((lane >> 3) ^ ((e >> 1) & 3))) << 4) + (lane & 7) * 2) = h;
+            sts16(smem_u32(tbuf) + e * 64 + ((((lane >> 3) ^ ((e >> 1) & 3))) << 4) + (lane & 7) * 2, h);
           }
         }
         fence_proxy_async_smem();
@@ -304,7 +313,7 @@ void ns_pair_set_attrs() {
 }
 
 void launch_ns_pair(int grid, cudaStream_t s, const NsTcParams& P) {
-  k_ns_gemm_tc_pair<<<grid, 192, ns_pair_smem_bytes(), s>>>(P);
+  k_ns_gemm_tc_pair<<<grid, kPairThreads, ns_pair_smem_bytes(), s>>>(P);
 }
 
 }  // namespace dion2

@@ -94,6 +94,7 @@ struct NsParams {
   int b_kmajor;
   int in_f16;                // operands (and cin) are fp16, else bf16 (pair kernel only)
   int out_f16;               // output written as fp16, else bf16 (pair kernel only)
+  int reverse;               // walk the tile list backwards (L2 reuse of the previous launch's last writes)
 };
 
 // tcgen05 path (k_ns_tcgen05.cu): tensor maps for the TMA operand loads.
@@ -107,6 +108,31 @@ void ns_tc_set_attrs();
 void launch_ns_tc(int bn, int grid, cudaStream_t s, const NsTcParams& P);
 void ns_pair_set_attrs();
 void launch_ns_pair(int grid, cudaStream_t s, const NsTcParams& P);
+// Gram-space chain (k_ns_chain_pair.cu, reading R23): one CTA pair runs every p x p product
+// of one matrix in sequence (ops), on the five fp16/bf16 p x p buffers of its shape group.
+constexpr int kChainBufs = 5;  // 0 A, 1 C, 2 Q0, 3 Q1, 4 B
+constexpr int kMaxChainOps = 64;
+struct ChainOp {
+  int8_t a, b, out, cin;  // buffer indices; cin < 0: none
+  int8_t out_f16;
+  int8_t dep;             // op (same matrix) whose completion gates this op's loads; < 0: none
+  int8_t cin_dep;         // op whose completion gates the epilogue's cin reads; < 0: none
+  int8_t pad;
+  float cacc, cC, diag;   // out = cacc * a.b^T + cC * cin + diag * I
+};
+struct NsChainParams {
+  CUtensorMap ld[kMaxGroups][kChainBufs];  // operand loads: box {64, 128, 1}, SWIZZLE_128B
+  CUtensorMap st[kMaxGroups][kChainBufs];  // output stores: box {32, 32, 1}, SWIZZLE_64B
+  const void* buf[kMaxGroups][kChainBufs]; // [count][p_pad][p_pad] 2-byte elements
+  long long mstride[kMaxGroups];
+  int p_pad[kMaxGroups];
+  int ngroups, nops, n_entries;
+  const int32_t* entries;                  // [n_entries] (group << 24) | z, largest p first
+  ChainOp ops[kMaxChainOps];
+};
+void ns_chain_set_attrs();
+void launch_ns_chain(int grid, cudaStream_t s, const NsChainParams& P);
+
 template <int BN>
 constexpr int ns_tc_stages() { return BN == 256 ? 4 : 6; }
 template <int BN>

@@ -62,9 +62,10 @@ struct Group {
 struct Launch {
   int phase;
   int bn;
-  int kind;  // 0 = tc BN128, 1 = tc BN256, 2 = simt
+  int kind;  // 0 = tc BN128, 1 = tc BN256, 2 = simt, 3 = 2-SM pair, 4 = Gram-space chain
   NsTcParams tc;
   int simt_group;
+  std::shared_ptr<NsChainParams> chain;  // kind 4
 };
 
 struct Plan {
@@ -75,6 +76,7 @@ struct Plan {
   std::vector<Group> groups;
   size_t off_status, off_bad, off_desc, off_rowmats, off_rowprefix, off_colmats, off_colprefix, off_gprefix,
       off_nsscale, off_ns_begin, off_ns_end, total;
+  size_t off_chain_entries = 0;  // Gram-space chain entry table (in the uploaded table region)
   int64_t total_rows = 0, total_col_tiles = 0;
   int n_row_mats = 0, n_col_mats = 0, total_gather_tiles = 0, max_d = 0;
   // streaming fast paths: list 0 = rows (units: X rows p_pad / selected rows k),

@@ -73,9 +73,24 @@ def test_gram_form_is_tighter_on_wide_x():
     _assert(res, 1e-2)
 
 
-@pytest.mark.parametrize("form", ["direct", "gram"])
-def test_both_ns_forms_on_the_1b_layer(form):
+@pytest.mark.parametrize("form,chain", [("direct", "0"), ("gram", "0"), ("gram", "1")])
+def test_both_ns_forms_on_the_1b_layer(form, chain, monkeypatch):
+    monkeypatch.setenv("DION2_NS_CHAIN", chain)
     _assert(run_parity(layer_set_1b(layers=1), 0.25, "auto", "bf16", steps=1, ns_form=form), BF16_TOL)
+
+
+@pytest.mark.parametrize("coeffs", [
+    None,
+    [(3.4445, -4.7750, 2.0315)],
+    [(3.4445, -4.7750, 2.0315)] * 2,
+    [(1.5, -0.5, 0.0)] * 3,
+])
+def test_gram_chain_kernel(coeffs, monkeypatch):
+    """The persistent chain launch (k_ns_chain_pair.cu): five shape groups (two chain launches,
+    p_pad 256 / 512 / 768, several matrices per pair), every schedule length."""
+    monkeypatch.setenv("DION2_NS_CHAIN", "1")
+    shapes = [(256, 1024), (1024, 256), (600, 2400), (1024, 4096), (2048, 5120), (130, 1030), (300, 1200)] * 2
+    _assert(run_parity(shapes, 0.3, "auto", "bf16", steps=2, ns_form="gram", ns_coeffs=coeffs), BF16_TOL)
 
 
 @pytest.mark.parametrize("coeffs", [
