@@ -70,7 +70,7 @@ def work_model(shapes, alpha, steps=5, mt=False, ns_form="auto"):
       Gram space (R23): 4p^2 q + (4T - 3) 2p^3 (T >= 2) -- gram + apply once, T polys,
       3T - 3 products C.Q / C.A / C.(CA)."""
     ns_flops = {"ns_gram": 0.0, "ns_poly": 0.0, "ns_apply": 0.0, "ns_mul": 0.0}
-    byts = {"momentum_score": 0.0}
+    byts = {"momentum_score": 0.0, "momentum_score_mt": 0.0}
     for ph in ("gather", "gather_rows", "gather_cols", "scatter", "scatter_rows", "scatter_cols"):
         byts[ph] = 0.0
     for (m, n) in shapes:
@@ -87,7 +87,8 @@ def work_model(shapes, alpha, steps=5, mt=False, ns_form="auto"):
             ns_flops["ns_gram"] += steps * 2.0 * p * p * q
             ns_flops["ns_poly"] += steps * 2.0 * p ** 3
             ns_flops["ns_apply"] += steps * 2.0 * p * p * q
-        byts["momentum_score"] += m * n * 12.0 + d * 4.0       # read G, read M, write M, write scores
+        k1 = "momentum_score_mt" if (mt and not rows) else "momentum_score"
+        byts[k1] += m * n * 12.0 + d * 4.0                    # read G, read M, write M, write scores
         # the library's path choice (dion2_api.cu build_layout)
         if rows and k <= n:
             sfx = "_rows"

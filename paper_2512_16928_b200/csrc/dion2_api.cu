@@ -25,7 +25,7 @@ namespace dion2rt {
 const char* kPhaseNames[kNumPhases] = {"momentum_score", "select",       "gather",       "norm",
                                        "ns_gram",        "ns_poly",      "ns_apply",     "scatter",
                                        "full_decay",     "gather_rows",  "gather_cols",  "scatter_rows",
-                                       "scatter_cols",   "ns_mul"};
+                                       "scatter_cols",   "ns_mul",       "momentum_score_mt"};
 
 std::mutex g_mu;
 int g_sm_count = 0;
@@ -816,7 +816,7 @@ void stage_k1_select(Plan& P, const dion2_config* c, void* ws, int32_t* status, 
     L.end();
   }
   if (P.n_mt_mats) {
-    L.begin(PH_K1);
+    L.begin(PH_K1_MT);
     const int blocks = stream_grid(P.total_mt_tiles, 8, persistent);
     k_momentum_score_cols_mt<<<blocks, 256, 0, s>>>(dmats, (const int32_t*)tab(P, P.off_mtmats),
                                                     (const int64_t*)tab(P, P.off_mtprefix), P.n_mt_mats,

@@ -228,64 +228,75 @@ __device__ __forceinline__ void col_tile_mt(const MatDesc& md, int rb, int cb, f
   }
 }
 
-// Vectorised variant (16-B aligned rows): 64 x 64 tiles, thread (r16 = t/16, c4 = t%16)
-// moves float4s of G rows and of M^T rows; all 8 loads are issued before the barrier.
+// Vectorised variant (16-B aligned rows): 64 x 64 tiles through a [64][65] shared transpose.
+// Lane = (g = lane / 8, c8 = lane % 8) in both phases: warp w moves rows 8 w + 4 jg + g
+// (jg = 0, 1) and float4 chunks c8 + 8 h (h = 0, 1), so every instruction covers 4 rows x
+// 128 contiguous bytes, and the shared accesses (row + column) mod 32 hit 32 distinct banks
+// (scalar stores of G rows, column reads for M^T rows).  All loads of a tile are issued
+// before the barrier.
+template <bool kBf16G>
+__device__ __forceinline__ float4 load_g4(const MatDesc& md, int64_t i, int64_t j) {
+  if constexpr (kBf16G) {
+    const uint2 raw = __ldcs(reinterpret_cast<const uint2*>(reinterpret_cast<const __nv_bfloat16*>(md.G) + i * md.ld + j));
+    const __nv_bfloat162 lo = *reinterpret_cast<const __nv_bfloat162*>(&raw.x);
+    const __nv_bfloat162 hi = *reinterpret_cast<const __nv_bfloat162*>(&raw.y);
+    return make_float4(__low2float(lo), __high2float(lo), __low2float(hi), __high2float(hi));
+  } else {
+    return __ldcs(reinterpret_cast<const float4*>(reinterpret_cast<const float*>(md.G) + i * md.ld + j));
+  }
+}
+
 template <bool kBf16G>
 __device__ __forceinline__ void col_tile_mt_v4(const MatDesc& md, int rb, int cb, float (*gs)[65]) {
-  const int t = threadIdx.x, r16 = t >> 4, c4 = t & 15;
+  const int lane = threadIdx.x & 31, w = threadIdx.x >> 5;
+  const int g = lane >> 3, c8 = lane & 7;
   const int64_t j0 = (int64_t)cb * 64;
   const int64_t ib = (int64_t)rb * kColRB;
   const int64_t ie = md.rows < ib + kColRB ? md.rows : ib + kColRB;
-  float acc[4] = {0.f, 0.f, 0.f, 0.f};  // |M| over this block's rows for columns j0 + r16 + 16u
+  float acc[2] = {0.f, 0.f};  // |M| over the block's rows, M^T rows j0 + 8w + 4jg + g
   for (int64_t i0 = ib; i0 < ie; i0 += 64) {
-    float4 g[4], m[4];
+    float4 gv[4], mv[4];
 #pragma unroll
-    for (int u = 0; u < 4; ++u) {  // G rows i0 + r16 + 16u, columns j0 + 4 c4 .. +3
-      const int64_t i = i0 + r16 + 16 * u, j = j0 + 4 * c4;
+    for (int u = 0; u < 4; ++u) {  // G row i0 + 8w + 4(u>>1) + g, columns j0 + 4(c8 + 8(u&1)) .. +3
+      const int64_t i = i0 + 8 * w + 4 * (u >> 1) + g, j = j0 + 4 * (c8 + 8 * (u & 1));
       if (i < ie && j + 3 < md.cols) {
-        if constexpr (kBf16G) {
-          const uint2 raw = __ldg(reinterpret_cast<const uint2*>(reinterpret_cast<const __nv_bfloat16*>(md.G) + i * md.ld + j));
-          const __nv_bfloat162 lo = *reinterpret_cast<const __nv_bfloat162*>(&raw.x);
-          const __nv_bfloat162 hi = *reinterpret_cast<const __nv_bfloat162*>(&raw.y);
-          g[u] = make_float4(__low2float(lo), __high2float(lo), __low2float(hi), __high2float(hi));
-        } else {
-          g[u] = __ldcs(reinterpret_cast<const float4*>(reinterpret_cast<const float*>(md.G) + i * md.ld + j));
-        }
+        gv[u] = load_g4<kBf16G>(md, i, j);
       } else {
-        g[u] = make_float4(0.f, 0.f, 0.f, 0.f);
+        gv[u] = make_float4(0.f, 0.f, 0.f, 0.f);
         for (int e = 0; e < 4; ++e)
-          if (i < ie && j + e < md.cols) (&g[u].x)[e] = load_g<kBf16G>(md, i, j + e);
+          if (i < ie && j + e < md.cols) (&gv[u].x)[e] = load_g<kBf16G>(md, i, j + e);
       }
     }
 #pragma unroll
-    for (int u = 0; u < 4; ++u) {  // M^T rows j0 + r16 + 16u, columns (= rows of M) i0 + 4 c4 .. +3
-      const int64_t j = j0 + r16 + 16 * u, i = i0 + 4 * c4;
-      m[u] = (j < md.cols && i + 3 < ie) ? *reinterpret_cast<const float4*>(md.M + j * md.ldm + i)
-                                         : make_float4(0.f, 0.f, 0.f, 0.f);
+    for (int u = 0; u < 4; ++u) {  // M^T row j0 + 8w + 4(u>>1) + g, columns i0 + 4(c8 + 8(u&1)) .. +3
+      const int64_t j = j0 + 8 * w + 4 * (u >> 1) + g, i = i0 + 4 * (c8 + 8 * (u & 1));
+      mv[u] = (j < md.cols && i + 3 < ie) ? *reinterpret_cast<const float4*>(md.M + j * md.ldm + i)
+                                          : make_float4(0.f, 0.f, 0.f, 0.f);
       if (j < md.cols && i < ie && i + 3 >= ie)
         for (int e = 0; e < 4; ++e)
-          if (i + e < ie) (&m[u].x)[e] = md.M[j * md.ldm + i + e];
+          if (i + e < ie) (&mv[u].x)[e] = md.M[j * md.ldm + i + e];
     }
 #pragma unroll
     for (int u = 0; u < 4; ++u) {
-      gs[r16 + 16 * u][4 * c4 + 0] = g[u].x;
-      gs[r16 + 16 * u][4 * c4 + 1] = g[u].y;
-      gs[r16 + 16 * u][4 * c4 + 2] = g[u].z;
-      gs[r16 + 16 * u][4 * c4 + 3] = g[u].w;
+      const int r = 8 * w + 4 * (u >> 1) + g, c = 4 * (c8 + 8 * (u & 1));
+      gs[r][c + 0] = gv[u].x;
+      gs[r][c + 1] = gv[u].y;
+      gs[r][c + 2] = gv[u].z;
+      gs[r][c + 3] = gv[u].w;
     }
     __syncthreads();
 #pragma unroll
     for (int u = 0; u < 4; ++u) {
-      const int jl = r16 + 16 * u;
-      const int64_t j = j0 + jl, i = i0 + 4 * c4;
-      float* e = &m[u].x;
+      const int jl = 8 * w + 4 * (u >> 1) + g, il = 4 * (c8 + 8 * (u & 1));
+      const int64_t j = j0 + jl, i = i0 + il;
+      float* e = &mv[u].x;
 #pragma unroll
       for (int q = 0; q < 4; ++q) {
-        e[q] += gs[4 * c4 + q][jl];  // G^T element (j, i + q)
-        acc[u] += (i + q < ie) ? fabsf(e[q]) : 0.f;
+        e[q] += gs[il + q][jl];  // G^T element (j, i + q)
+        acc[u >> 1] += (i + q < ie) ? fabsf(e[q]) : 0.f;
       }
       if (j < md.cols) {
-        if (i + 3 < ie) *reinterpret_cast<float4*>(md.M + j * md.ldm + i) = m[u];
+        if (i + 3 < ie) *reinterpret_cast<float4*>(md.M + j * md.ldm + i) = mv[u];
         else
           for (int q = 0; q < 4; ++q)
             if (i + q < ie) md.M[j * md.ldm + i + q] = e[q];
@@ -293,18 +304,18 @@ __device__ __forceinline__ void col_tile_mt_v4(const MatDesc& md, int rb, int cb
     }
     __syncthreads();
   }
-  // reduce the 16 threads (c4) that share a column, in a fixed xor-tree order
+  // reduce the 8 lanes (c8) that share an M^T row, in a fixed xor-tree order
 #pragma unroll
-  for (int u = 0; u < 4; ++u) {
-    float s = acc[u];
+  for (int jg = 0; jg < 2; ++jg) {
+    float s = acc[jg];
 #pragma unroll
-    for (int o = 8; o > 0; o >>= 1) s += __shfl_xor_sync(0xffffffffu, s, o);
-    const int64_t j = j0 + r16 + 16 * u;
-    if (c4 == 0 && j < md.cols) md.col_partials[(int64_t)rb * md.cols + j] = s;
+    for (int o = 4; o > 0; o >>= 1) s += __shfl_xor_sync(0xffffffffu, s, o);
+    const int64_t j = j0 + 8 * w + 4 * jg + g;
+    if (c8 == 0 && j < md.cols) md.col_partials[(int64_t)rb * md.cols + j] = s;
   }
 }
 
-__global__ void __launch_bounds__(256) k_momentum_score_cols_mt(const MatDesc* __restrict__ mats,
+__global__ void __launch_bounds__(256, 4) k_momentum_score_cols_mt(const MatDesc* __restrict__ mats,
                                                                 const int32_t* __restrict__ col_mats,
                                                                 const int64_t* __restrict__ tile_prefix,
                                                                 int n_col_mats, int64_t total_tiles) {

@@ -15,11 +15,11 @@
 namespace dion2rt {
 using namespace dion2;
 
-constexpr int kNumPhases = 14;
+constexpr int kNumPhases = 15;
 extern const char* kPhaseNames[kNumPhases];
 enum Phase {
   PH_K1 = 0, PH_SELECT, PH_GATHER, PH_NORM, PH_GRAM, PH_POLY, PH_APPLY, PH_SCATTER, PH_FULLDECAY,
-  PH_GATHER_ROWS, PH_GATHER_COLS, PH_SCATTER_ROWS, PH_SCATTER_COLS, PH_NSMUL
+  PH_GATHER_ROWS, PH_GATHER_COLS, PH_SCATTER_ROWS, PH_SCATTER_COLS, PH_NSMUL, PH_K1_MT
 };
 
 extern std::mutex g_mu;
