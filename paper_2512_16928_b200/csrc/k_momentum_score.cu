@@ -329,8 +329,10 @@ __global__ void __launch_bounds__(256, 4) k_momentum_score_cols_mt(const MatDesc
     const MatDesc& md = mats[col_mats[lo]];
     const int64_t local = t - tile_prefix[lo];
     // units: (row block, 64 columns); unaligned rows take two scalar 32-column halves
-    const int cbs = (int)((md.cols + 63) / 64);
-    const int rb = (int)(local / cbs), cb = (int)(local % cbs);
+    // column-block-major: consecutive blocks take consecutive row blocks of the same 64
+    // columns, so together they stream whole M^T rows (2/3 of the traffic) page by page
+    const int rbs = (int)((md.rows + kColRB - 1) / kColRB);
+    const int cb = (int)(local / rbs), rb = (int)(local % rbs);
     if (md.vec4) {
       if (md.grad_bf16) col_tile_mt_v4<true>(md, rb, cb, gs);
       else col_tile_mt_v4<false>(md, rb, cb, gs);
