@@ -132,7 +132,7 @@ std::string plan_key(const dion2_matrix* mats, int n, const dion2_config* c, voi
   put(&c->scale_mode, 4);
   put(&c->ns_form, 4);
   // kernel-variant switches read at plan build (tests and measurements flip them)
-  for (const char* v : {"DION2_NS_PAIR", "DION2_NS_SYM", "DION2_NS_CHAIN", "DION2_NS_SERPENTINE"}) {
+  for (const char* v : {"DION2_NS_PAIR", "DION2_NS_SYM", "DION2_NS_CHAIN", "DION2_NS_SERPENTINE", "DION2_NS_UPPER"}) {
     const char* e = getenv(v);
     k.append(e ? e : "-");
     k.push_back('|');
@@ -363,8 +363,11 @@ static int append_gram_space_launches(Plan& P, const dion2_config* c, void* ws, 
   const char* serp_env = getenv("DION2_NS_SERPENTINE");
   const bool serpentine = !serp_env || atoi(serp_env) != 0;
   unsigned flip = 0;
+  // p x p buffers hold only their upper 256 x 256 tiles (the kernel reads lower k-blocks
+  // transposed); Q_T, read by the 1-SM apply, is written mirrored.  DION2_NS_UPPER=0: mirror all.
+  const bool upper_only = !(getenv("DION2_NS_UPPER") && atoi(getenv("DION2_NS_UPPER")) == 0) && sym_on;
   auto emit = [&](int phase, const std::vector<Entry>& es, float cacc, float cC, float diag, int scale_sel,
-                  int in_f16, int out_f16) -> int {
+                  int in_f16, int out_f16, bool mirror_out = false) -> int {
     const bool apply = phase == PH_APPLY;
     const bool pair = !apply || pair_mode == 2;
     const int MT = pair ? 256 : 128, BN = 256;
@@ -380,6 +383,8 @@ static int append_gram_space_launches(Plan& P, const dion2_config* c, void* ws, 
       np.sym = (apply || !sym_on) ? 0 : 1;
       np.b_kmajor = apply ? 0 : 1;
       np.in_f16 = in_f16; np.out_f16 = out_f16;
+      np.sym_in = (upper_only && !apply && phase != PH_GRAM) ? 1 : 0;
+      np.no_mirror = (upper_only && !apply && !mirror_out) ? 1 : 0;
       // alternate the walk direction between consecutive p x p launches: a launch starts on the
       // matrices the previous one wrote last (still in L2)
       np.reverse = (!apply && serpentine) ? (int)(flip++ & 1) : 0;
@@ -407,6 +412,10 @@ static int append_gram_space_launches(Plan& P, const dion2_config* c, void* ws, 
         }
         if (!make_map(&L.tc.mapD[j], e.out, G.out_ld, g.p_pad, g.count, 32, 32, CU_TENSOR_MAP_SWIZZLE_64B))
           return DION2_ECUDA;
+        if (np.sym_in) {
+          if (!make_map(&L.tc.mapAT[j], e.a, g.p_pad, g.p_pad, g.count, 64, 64)) return DION2_ECUDA;
+          if (!make_map(&L.tc.mapBT[j], e.b, g.p_pad, g.p_pad, g.count, 64, 64)) return DION2_ECUDA;
+        }
         G.tile_base = tiles;
         tiles += G.count * (np.sym ? G.m_tiles * (G.m_tiles + 1) / 2 : G.m_tiles * G.n_tiles);
       }
@@ -423,16 +432,13 @@ static int append_gram_space_launches(Plan& P, const dion2_config* c, void* ws, 
   auto Qb = [&](int gi, int j) { return at(ws, (j & 1) ? P.groups[gi].off_Q0 : P.groups[gi].off_Q1); };  // Q_j, j >= 1
   int rc;
   std::vector<Entry> es;
-  for (int gi : gl) es.push_back({gi, X0(gi), X0(gi), Ab(gi), nullptr});
-  if ((rc = emit(PH_GRAM, es, 1.f, 0.f, 0.f, 2, 0, 1))) return rc;
-  // p x p products: one persistent chain launch (a CTA pair runs one matrix's whole op list,
-  // k_ns_chain_pair.cu) when there are enough matrices to fill the GPU, else one flat launch
-  // per op over all matrices.  DION2_NS_CHAIN=0|1 overrides.
-  int n_gs = 0;
-  for (int gi : gl) n_gs += P.groups[gi].count;
+  // p x p products: one flat launch per op over all matrices, or (DION2_NS_CHAIN=1) one
+  // persistent chain launch in which a CTA pair runs one matrix's whole op list
+  // (k_ns_chain_pair.cu; measured slower, kept as an option)
   const char* chain_env = getenv("DION2_NS_CHAIN");
-  const int pairs = (g_sm_count > 0 ? g_sm_count : 148) / 2;
-  const bool use_chain = chain_env ? atoi(chain_env) != 0 : false && n_gs >= pairs / 2;
+  const bool use_chain = chain_env && atoi(chain_env) != 0;
+  for (int gi : gl) es.push_back({gi, X0(gi), X0(gi), Ab(gi), nullptr});
+  if ((rc = emit(PH_GRAM, es, 1.f, 0.f, 0.f, 2, 0, 1, /*mirror_out=*/use_chain))) return rc;
   if (use_chain) {
     if ((rc = append_chain_launches(P, c, ws, gl))) return rc;
     es.clear();
@@ -444,13 +450,13 @@ static int append_gram_space_launches(Plan& P, const dion2_config* c, void* ws, 
     const int last = t == T - 1;
     es.clear();
     for (int gi : gl) es.push_back({gi, Ab(gi), Ab(gi), Cb(gi, t), Ab(gi)});
-    if ((rc = emit(PH_POLY, es, cc, b, a, 0, 1, T == 1 ? 0 : 1))) return rc;
+    if ((rc = emit(PH_POLY, es, cc, b, a, 0, 1, T == 1 ? 0 : 1, T == 1))) return rc;
     es.clear();
     for (int gi : gl) {
       if (t >= 1) es.push_back({gi, Cb(gi, t), Qb(gi, t), Qb(gi, t + 1), nullptr});
       if (!last) es.push_back({gi, Cb(gi, t), Ab(gi), Bb(gi), nullptr});
     }
-    if (!es.empty() && (rc = emit(PH_NSMUL, es, 1.f, 0.f, 0.f, 0, 1, last ? 0 : 1))) return rc;
+    if (!es.empty() && (rc = emit(PH_NSMUL, es, 1.f, 0.f, 0.f, 0, 1, last ? 0 : 1, last))) return rc;
     if (!last) {
       es.clear();
       for (int gi : gl) es.push_back({gi, Cb(gi, t), Bb(gi), Ab(gi), nullptr});

@@ -89,6 +89,7 @@ constexpr uint32_t kIdescAbFmt = (7u << 7) | (7u << 10);
 
 constexpr int ns_pair_smem_bytes() { return 1024 + kStagesPair * (int)kStage + 1024 + kEpiWarps * 4 * 2048; }
 
+template <bool kSymIn>  // = P.p.sym_in (a template so non-symmetric launches carry no per-k-block logic)
 __global__ void __cluster_dims__(2, 1, 1) __launch_bounds__(kPairThreads, 1)
     k_ns_gemm_tc_pair(const __grid_constant__ NsTcParams P) {
   constexpr int S = kStagesPair;
@@ -120,6 +121,10 @@ __global__ void __cluster_dims__(2, 1, 1) __launch_bounds__(kPairThreads, 1)
       tma_prefetch_desc(&P.mapA[gi]);
       tma_prefetch_desc(&P.mapB[gi]);
       tma_prefetch_desc(&P.mapD[gi]);
+      if (kSymIn) {
+        tma_prefetch_desc(&P.mapAT[gi]);
+        tma_prefetch_desc(&P.mapBT[gi]);
+      }
     }
   }
   if (warp == 1) tmem_alloc_pair(tmem_base_slot, kTmemCols);
@@ -142,8 +147,23 @@ __global__ void __cluster_dims__(2, 1, 1) __launch_bounds__(kPairThreads, 1)
           uint8_t* sb = sa + kAB;
           const uint32_t leader_full = mapa_shared(smem_u32(&full_bar[stage]), 0);
           if (rank == 0) mbar_arrive_expect_tx(&full_bar[stage], 2 * kStage);
-          tma_load_3d_pair(sa, &P.mapA[c.group], leader_full, kb * kBK, c.tm * 256 + (int)rank * 128, c.z);
-          if (p.b_kmajor) {
+          // sym_in: a k-block left of the diagonal tile is stored only as its transpose
+          const bool at = kSymIn && ((kb * kBK) >> 8) < c.tm;
+          const bool bt = kSymIn && ((kb * kBK) >> 8) < c.tn;
+          if (!at) {
+            tma_load_3d_pair(sa, &P.mapA[c.group], leader_full, kb * kBK, c.tm * 256 + (int)rank * 128, c.z);
+          } else {
+#pragma unroll
+            for (int j = 0; j < 2; ++j)
+              tma_load_3d_pair(sa + j * 64 * kBK * 2, &P.mapAT[c.group], leader_full,
+                               c.tm * 256 + (int)rank * 128 + j * 64, kb * kBK, c.z);
+          }
+          if (p.b_kmajor && bt) {
+#pragma unroll
+            for (int j = 0; j < 2; ++j)
+              tma_load_3d_pair(sb + j * 64 * kBK * 2, &P.mapBT[c.group], leader_full,
+                               c.tn * 256 + (int)rank * 128 + j * 64, kb * kBK, c.z);
+          } else if (p.b_kmajor) {
             tma_load_3d_pair(sb, &P.mapB[c.group], leader_full, kb * kBK, c.tn * 256 + (int)rank * 128, c.z);
           } else {
 #pragma unroll
@@ -158,7 +178,7 @@ __global__ void __cluster_dims__(2, 1, 1) __launch_bounds__(kPairThreads, 1)
   } else if (warp == 1) {
     if (lane == 0 && rank == 0) {
       // ---------------- MMA issuer (leader CTA)
-      const uint32_t idesc = (p.b_kmajor ? kIdescK : kIdescMN) & (p.in_f16 ? ~kIdescAbFmt : ~0u);
+      const uint32_t idesc0 = (p.b_kmajor ? kIdescK : kIdescMN) & (p.in_f16 ? ~kIdescAbFmt : ~0u);
       int stage = 0;
       uint32_t phase = 0;
       int it = 0;
@@ -175,12 +195,27 @@ __global__ void __cluster_dims__(2, 1, 1) __launch_bounds__(kPairThreads, 1)
           tc_fence_after();
           const uint32_t a_addr = smem_u32(smem + stage * kStage);
           const uint32_t b_addr = a_addr + kAB;
+          if constexpr (!kSymIn) {
 #pragma unroll
-          for (int k = 0; k < kBK / 16; ++k) {
-            const uint64_t adesc = umma_desc_sw128(a_addr + k * 32, 16, 1024);
-            const uint64_t bdesc = p.b_kmajor ? umma_desc_sw128(b_addr + k * 32, 16, 1024)
-                                              : umma_desc_sw128(b_addr + k * 2048, 64 * kBK * 2, 1024);
-            umma_bf16_ss_pair(tmem_d, adesc, bdesc, idesc, (kb | k) != 0);
+            for (int k = 0; k < kBK / 16; ++k) {
+              const uint64_t adesc = umma_desc_sw128(a_addr + k * 32, 16, 1024);
+              const uint64_t bdesc = p.b_kmajor ? umma_desc_sw128(b_addr + k * 32, 16, 1024)
+                                                : umma_desc_sw128(b_addr + k * 2048, 64 * kBK * 2, 1024);
+              umma_bf16_ss_pair(tmem_d, adesc, bdesc, idesc0, (kb | k) != 0);
+            }
+          } else {
+            // transposed (MN-major) operands of this k-block, as loaded by the producer
+            const bool at = ((kb * kBK) >> 8) < c.tm;
+            const bool bt = ((kb * kBK) >> 8) < c.tn;
+            const uint32_t idesc = idesc0 | (at ? (1u << 15) : 0u) | (bt ? (1u << 16) : 0u);
+#pragma unroll
+            for (int k = 0; k < kBK / 16; ++k) {
+              const uint64_t adesc = at ? umma_desc_sw128(a_addr + k * 2048, 64 * kBK * 2, 1024)
+                                        : umma_desc_sw128(a_addr + k * 32, 16, 1024);
+              const uint64_t bdesc = bt ? umma_desc_sw128(b_addr + k * 2048, 64 * kBK * 2, 1024)
+                                        : umma_desc_sw128(b_addr + k * 32, 16, 1024);
+              umma_bf16_ss_pair(tmem_d, adesc, bdesc, idesc, (kb | k) != 0);
+            }
           }
           umma_commit_pair(&empty_bar[stage]);
           if (++stage == S) { stage = 0; phase ^= 1; }
@@ -256,7 +291,7 @@ __global__ void __cluster_dims__(2, 1, 1) __launch_bounds__(kPairThreads, 1)
         for (int e = 0; e < 32; ++e) o[e] = ca * v[e] + cc * cv[e] + (e == dcol ? dterm : 0.f);
         // 4 staging buffers per warp (SWIZZLE_64B layout: 16-B chunk q of row r at
         // q ^ ((r >> 1) & 3)); a buffer is rewritten once the store 4 commits back has read it
-        const bool mirror = p.sym && c.tm != c.tn;
+        const bool mirror = p.sym && !p.no_mirror && c.tm != c.tn;
         uint8_t* buf = stage_base + (ew * 4 + sbuf) * 2048;
         if (lane == 0) bulk_wait_read<3>();
         __syncwarp();
@@ -309,11 +344,15 @@ __global__ void __cluster_dims__(2, 1, 1) __launch_bounds__(kPairThreads, 1)
 }
 
 void ns_pair_set_attrs() {
-  cudaFuncSetAttribute(k_ns_gemm_tc_pair, cudaFuncAttributeMaxDynamicSharedMemorySize, ns_pair_smem_bytes());
+  cudaFuncSetAttribute(k_ns_gemm_tc_pair<false>, cudaFuncAttributeMaxDynamicSharedMemorySize, ns_pair_smem_bytes());
+  cudaFuncSetAttribute(k_ns_gemm_tc_pair<true>, cudaFuncAttributeMaxDynamicSharedMemorySize, ns_pair_smem_bytes());
 }
 
 void launch_ns_pair(int grid, cudaStream_t s, const NsTcParams& P) {
-  k_ns_gemm_tc_pair<<<grid, kPairThreads, ns_pair_smem_bytes(), s>>>(P);
+  if (P.p.sym_in)
+    k_ns_gemm_tc_pair<true><<<grid, kPairThreads, ns_pair_smem_bytes(), s>>>(P);
+  else
+    k_ns_gemm_tc_pair<false><<<grid, kPairThreads, ns_pair_smem_bytes(), s>>>(P);
 }
 
 }  // namespace dion2

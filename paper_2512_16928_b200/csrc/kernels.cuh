@@ -95,6 +95,10 @@ struct NsParams {
   int in_f16;                // operands (and cin) are fp16, else bf16 (pair kernel only)
   int out_f16;               // output written as fp16, else bf16 (pair kernel only)
   int reverse;               // walk the tile list backwards (L2 reuse of the previous launch's last writes)
+  // upper-triangle storage of symmetric p x p buffers (pair kernel, Gram-space launches):
+  int sym_in;                // operands hold only their upper 256 x 256 tiles: a lower k-block is read
+                             // transposed (MN-major) from the stored upper tile
+  int no_mirror;             // sym output: do not write the mirrored lower tiles
 };
 
 // tcgen05 path (k_ns_tcgen05.cu): tensor maps for the TMA operand loads.
@@ -102,6 +106,8 @@ struct NsTcParams {
   CUtensorMap mapA[kMaxGroups];
   CUtensorMap mapB[kMaxGroups];
   CUtensorMap mapD[kMaxGroups];  // output (TMA store): box {32 cols, 32 rows, 1}, SWIZZLE_64B
+  CUtensorMap mapAT[kMaxGroups]; // sym_in: the A buffer with box {64, 64} for transposed k-blocks
+  CUtensorMap mapBT[kMaxGroups]; // sym_in: the B buffer with box {64, 64}
   NsParams p;
 };
 void ns_tc_set_attrs();
