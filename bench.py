@@ -382,6 +382,36 @@ def run_ours(args):
         opt = make_opt(args.alpha)
         opt.step(Ws, Ms, Gs)
 
+    # BASELINE configs[1]: the alpha sweep and the forced row / column modes (single GPU; a few
+    # steps each; the momentum buffer is re-viewed in W's layout for the forced modes)
+    sweep = None
+    if not args.no_sweep and not use_dist:
+        del opt
+        torch.cuda.empty_cache()
+        sweep = {"alpha_ms_per_step": {}, "axis_ms_per_step": {}, "steps": 3}
+        for a in (1.0, 0.5, 0.25, 0.125):
+            if a == 1.0 and ms_a1 is not None:
+                sweep["alpha_ms_per_step"]["1.0"] = ms_a1
+                continue
+            if a == args.alpha:
+                sweep["alpha_ms_per_step"][str(a)] = ms
+                continue
+            o_ = make_opt(a)
+            sweep["alpha_ms_per_step"][str(a)] = time_steps(o_, Ws, Ms, Gs, 3, 1, None)
+            del o_
+            torch.cuda.empty_cache()
+        Ms_w, off = [], 0
+        for (m, n) in shapes:
+            Ms_w.append(bufs[1][off:off + m * n].view(m, n))
+            off += m * n
+        for ax in ("rows", "cols"):
+            o_ = Dion2(alpha=args.alpha, axis=ax, precision="bf16", ns_form=args.ns_form)
+            sweep["axis_ms_per_step"][ax] = time_steps(o_, Ws, Ms_w, Gs, 3, 1, None)
+            del o_
+            torch.cuda.empty_cache()
+        opt = make_opt(args.alpha)
+        opt.step(Ws, Ms, Gs)
+
     # end to end through the public API (host G)
     e2e_ms, h2d, d2h = None, None, None
     if not args.no_e2e:
@@ -426,6 +456,7 @@ def run_ours(args):
                        "parallelism": "single GPU" if not use_dist else
                        f"owner-compute over {world} GPUs (NCCL; shards along the non-selection axis)"},
             "alpha1_ms_per_step": ms_a1,
+            "configs1_sweep": sweep,
             "speedup_vs_alpha1": (ms_a1 / ms) if ms_a1 else None,
             "ns_tflops": ns_tflops,
             "ns_tflops_note": "executed form's FLOPs (Gram space: 4p^2q + (4T-3)2p^3 per matrix, full products) "
@@ -506,6 +537,7 @@ def main():
     ap.add_argument("--cpu-budget", type=float, default=20.0)
     ap.add_argument("--layers", type=int, default=0, help="override the layer count (profiling only)")
     ap.add_argument("--no-e2e", action="store_true")
+    ap.add_argument("--no-sweep", action="store_true", help="skip the alpha sweep / forced axis modes")
     ap.add_argument("--no-mt", action="store_true", help="keep column-mode momentum in W's layout")
     ap.add_argument("--ns-form", choices=["auto", "direct", "gram"], default="auto",
                     help="Newton-Schulz evaluation form (DESIGN.md reading R23)")
