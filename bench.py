@@ -409,6 +409,16 @@ def run_ours(args):
             sweep["axis_ms_per_step"][ax] = time_steps(o_, Ws, Ms_w, Gs, 3, 1, None)
             del o_
             torch.cuda.empty_cache()
+        # the same step with bf16 gradients (mixed-precision training): K1 reads 10 B/param
+        Gb = bufs[2].to(torch.bfloat16)
+        Gbs, off = [], 0
+        for (m, n) in shapes:
+            Gbs.append(Gb[off:off + m * n].view(m, n))
+            off += m * n
+        o_ = make_opt(args.alpha)
+        sweep["bf16_grad_ms_per_step"] = time_steps(o_, Ws, Ms, Gbs, 3, 1, None)
+        del o_, Gbs, Gb
+        torch.cuda.empty_cache()
         opt = make_opt(args.alpha)
         opt.step(Ws, Ms, Gs)
 
