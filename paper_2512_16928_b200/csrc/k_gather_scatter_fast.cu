@@ -338,12 +338,14 @@ __global__ void __launch_bounds__(256) k_gather_cols_t(const MatDesc* __restrict
   }
 }
 
+// slab_h (32 or 16): rows of the 32-row unit processed per staged O tile; 16 halves the
+// shared tile for large k (k = 1024: 66 KB -> 33 KB, 2 -> 4 resident blocks per SM)
 template <int kScU, bool kScAll>
 __global__ void __launch_bounds__(256) k_scatter_cols_t(const MatDesc* __restrict__ mats,
                                                         const int32_t* __restrict__ list_mats,
                                                         const int32_t* __restrict__ list_prefix, int n_list,
                                                         int total_units, const int32_t* __restrict__ bad, float lr,
-                                                        int mask_words) {
+                                                        int mask_words, int slab_h) {
   extern __shared__ __align__(16) uint8_t sm[];
   uint32_t* mask = reinterpret_cast<uint32_t*>(sm);
   int32_t* rank = reinterpret_cast<int32_t*>(sm + 4 * mask_words);
@@ -355,80 +357,84 @@ __global__ void __launch_bounds__(256) k_scatter_cols_t(const MatDesc* __restric
     const int mi = list_mats[li];
     const MatDesc& md = mats[mi];
     const int slab = u - list_prefix[li];
-    const int i0 = slab * kSlab;
-    if (bad[mi] || i0 >= md.rows) continue;  // block-uniform
+    if (bad[mi] || slab * kSlab >= md.rows) continue;  // block-uniform
     if (mi != cur_mat) {
       build_mask(md, mask, rank);
       cur_mat = mi;
     }
     const int k = md.k;
     const int ldt = scatter_tile_ld(k);
-    // O tile: tile[il][r] = X_T[r][i0 + il]
-    const __nv_bfloat16* X = reinterpret_cast<const __nv_bfloat16*>(md.final_in_x1 ? md.X1 : md.X0);
-    for (int t = threadIdx.x; t < k * 4; t += blockDim.x) {
-      const int r = t >> 2, part = (t & 3) * 8;
-      const uint4 in = *reinterpret_cast<const uint4*>(X + (int64_t)r * md.q_pad + i0 + part);
-      const __nv_bfloat16* h = reinterpret_cast<const __nv_bfloat16*>(&in);
+    const int parts = slab_h / 8;
+    for (int h0 = 0; h0 < kSlab; h0 += slab_h) {
+      const int i0 = slab * kSlab + h0;
+      if (i0 >= md.rows) break;
+      // O tile: tile[il][r] = X_T[r][i0 + il]
+      const __nv_bfloat16* X = reinterpret_cast<const __nv_bfloat16*>(md.final_in_x1 ? md.X1 : md.X0);
+      for (int t = threadIdx.x; t < k * parts; t += blockDim.x) {
+        const int r = t / parts, part = (t % parts) * 8;
+        const uint4 in = *reinterpret_cast<const uint4*>(X + (int64_t)r * md.q_pad + i0 + part);
+        const __nv_bfloat16* h = reinterpret_cast<const __nv_bfloat16*>(&in);
 #pragma unroll
-      for (int e = 0; e < 8; ++e) tile[(part + e) * ldt + r] = h[e];
-    }
-    __syncthreads();
-    const float sc = lr * md.update_scale;
-    const int n = (int)md.cols;
-    for (int il = wid; il < kSlab; il += 8) {
-      const int64_t i = (int64_t)i0 + il;
-      if (i >= md.rows) break;
-      const __nv_bfloat16* trow = tile + il * ldt;
-      float* wrow = md.W + i * md.ld;
-      float* orow = md.O_out ? md.O_out + i * k : nullptr;
-      if (md.vec4) {
-        float4* w4 = reinterpret_cast<float4*>(wrow);
-        const int n4 = n >> 2;
-        for (int j0 = lane; j0 < n4; j0 += 32 * kScU) {
-          float4 w[kScU];
-          uint32_t bits[kScU];
+        for (int e = 0; e < 8; ++e) tile[(part + e) * ldt + r] = h[e];
+      }
+      __syncthreads();
+      const float sc = lr * md.update_scale;
+      const int n = (int)md.cols;
+      for (int il = wid; il < slab_h; il += 8) {
+        const int64_t i = (int64_t)i0 + il;
+        if (i >= md.rows) break;
+        const __nv_bfloat16* trow = tile + il * ldt;
+        float* wrow = md.W + i * md.ld;
+        float* orow = md.O_out ? md.O_out + i * k : nullptr;
+        if (md.vec4) {
+          float4* w4 = reinterpret_cast<float4*>(wrow);
+          const int n4 = n >> 2;
+          for (int j0 = lane; j0 < n4; j0 += 32 * kScU) {
+            float4 w[kScU];
+            uint32_t bits[kScU];
 #pragma unroll
-          for (int u = 0; u < kScU; ++u) {
-            const int j = j0 + 32 * u, c = 4 * j;
-            bits[u] = j < n4 ? (mask[c >> 5] >> (c & 31)) & 0xFu : 0u;
-            if (kScAll ? j < n4 : bits[u] != 0) w[u] = w4[j];
-          }
-#pragma unroll
-          for (int u = 0; u < kScU; ++u) {
-            if (!bits[u]) continue;
-            const int j = j0 + 32 * u, c = 4 * j;
-            int rk = col_rank(mask, rank, c);
-            float e[4] = {w[u].x, w[u].y, w[u].z, w[u].w};
-#pragma unroll
-            for (int q = 0; q < 4; ++q) {
-              if (bits[u] & (1u << q)) {
-                const float o = __bfloat162float(trow[rk]);
-                e[q] -= sc * o;
-                if (orow) orow[rk] = o;
-                ++rk;
-              }
+            for (int u = 0; u < kScU; ++u) {
+              const int j = j0 + 32 * u, c = 4 * j;
+              bits[u] = j < n4 ? (mask[c >> 5] >> (c & 31)) & 0xFu : 0u;
+              if (kScAll ? j < n4 : bits[u] != 0) w[u] = w4[j];
             }
-            w4[j] = make_float4(e[0], e[1], e[2], e[3]);
+#pragma unroll
+            for (int u = 0; u < kScU; ++u) {
+              if (!bits[u]) continue;
+              const int j = j0 + 32 * u, c = 4 * j;
+              int rk = col_rank(mask, rank, c);
+              float e[4] = {w[u].x, w[u].y, w[u].z, w[u].w};
+#pragma unroll
+              for (int q = 0; q < 4; ++q) {
+                if (bits[u] & (1u << q)) {
+                  const float o = __bfloat162float(trow[rk]);
+                  e[q] -= sc * o;
+                  if (orow) orow[rk] = o;
+                  ++rk;
+                }
+              }
+              w4[j] = make_float4(e[0], e[1], e[2], e[3]);
+            }
           }
-        }
-        for (int c = 4 * n4 + lane; c < n; c += 32) {
-          if (!((mask[c >> 5] >> (c & 31)) & 1u)) continue;
-          const int rk = col_rank(mask, rank, c);
-          const float o = __bfloat162float(trow[rk]);
-          wrow[c] -= sc * o;
-          if (orow) orow[rk] = o;
-        }
-      } else {
-        for (int c = lane; c < n; c += 32) {
-          if (!((mask[c >> 5] >> (c & 31)) & 1u)) continue;
-          const int rk = col_rank(mask, rank, c);
-          const float o = __bfloat162float(trow[rk]);
-          wrow[c] -= sc * o;
-          if (orow) orow[rk] = o;
+          for (int c = 4 * n4 + lane; c < n; c += 32) {
+            if (!((mask[c >> 5] >> (c & 31)) & 1u)) continue;
+            const int rk = col_rank(mask, rank, c);
+            const float o = __bfloat162float(trow[rk]);
+            wrow[c] -= sc * o;
+            if (orow) orow[rk] = o;
+          }
+        } else {
+          for (int c = lane; c < n; c += 32) {
+            if (!((mask[c >> 5] >> (c & 31)) & 1u)) continue;
+            const int rk = col_rank(mask, rank, c);
+            const float o = __bfloat162float(trow[rk]);
+            wrow[c] -= sc * o;
+            if (orow) orow[rk] = o;
+          }
         }
       }
-    }
-    __syncthreads();
+      __syncthreads();
+    }  // h0
   }
 }
 
@@ -461,7 +467,9 @@ void launch_scatter_cols_t(int blocks, int max_k, int64_t max_n, cudaStream_t s,
   const int mw = mask_words_for(max_n);
   // 8 whole-row float4 loads in flight per lane (measured on the 1B set's 24 up-projections:
   // 4 selected-only loads 0.669 ms, 8 unconditional 0.613 ms, 16 0.731 ms)
-  k_scatter_cols_t<8, true><<<blocks, 256, cols_t_smem_bytes(max_k, mw), s>>>(mats, lm, lp, nl, units, bad, lr, mw);
+  const int slab_h = max_k > 512 ? 16 : 32;
+  const size_t smem = 8 * (size_t)mw + (size_t)slab_h * (max_k + 8) * 2;
+  k_scatter_cols_t<8, true><<<blocks, 256, smem, s>>>(mats, lm, lp, nl, units, bad, lr, mw, slab_h);
 }
 
 }  // namespace dion2
