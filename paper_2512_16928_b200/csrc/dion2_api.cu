@@ -726,10 +726,7 @@ int run_ns(Plan& P, const dion2_config* c, Launcher& L, cudaStream_t s, bool do_
   for (const Launch& ln : P.ns_launches) {
     L.begin(ln.phase);
     if (ln.kind == 4) {
-      static const int chain_pairs = getenv("DION2_CHAIN_PAIRS") ? atoi(getenv("DION2_CHAIN_PAIRS")) : 0;
-      int grid = std::min(2 * ln.chain->n_entries, sms & ~1);
-      if (chain_pairs > 0) grid = std::min(grid, 2 * chain_pairs);
-      launch_ns_chain(grid, s, *ln.chain);
+      launch_ns_chain(std::min(2 * ln.chain->n_entries, sms & ~1), s, *ln.chain);
     } else if (ln.kind == 3) {
       launch_ns_pair(std::min(2 * ln.tc.p.total_tiles, sms & ~1), s, ln.tc);
     } else if (ln.kind == 0 || ln.kind == 1) {
