@@ -19,9 +19,11 @@
  *  - Every pointer is a DEVICE pointer unless marked HOST.
  *  - Matrices are row-major: element (i, j) of W is W[i*ld + j]; rows =
  *    fan-out, cols = fan-in (y = W x).
- *  - The caller owns every buffer (W, M, G, workspace, optional outputs).
- *    The library never allocates device memory inside a step; size the
- *    workspace with dion2_workspace_size() and pass it to every step.
+ *  - The caller owns every buffer (W, M, G, workspace, optional outputs); size
+ *    the workspace with dion2_workspace_size() and pass it to every step.  The
+ *    library's only device allocation is a small plan-owned table (matrix
+ *    descriptors and work lists, ~200 B per matrix), made once per (shapes,
+ *    config, workspace) plan on its first step and reused by every later step.
  *  - All work is enqueued asynchronously on `stream` (a cudaStream_t passed
  *    as void*; NULL = legacy default stream).  No host synchronisation
  *    happens inside a step.  Calls that touch the same matrices must not
@@ -51,7 +53,7 @@ typedef enum {
   DION2_EWORKSPACE = 3,    /* workspace NULL or smaller than dion2_workspace_size() */
   DION2_EUNSUPPORTED = 4,  /* a configuration this build does not implement */
   DION2_ECUDA = 5,         /* a CUDA runtime / launch error */
-  DION2_ENCCL = 6,         /* reserved for the multi-GPU entry point */
+  DION2_ENCCL = 6,         /* an NCCL call failed (distributed / DP-sync entry points) */
   DION2_ENONFINITE = 7     /* (device-side) a matrix's scores were NaN/Inf */
 } dion2_status;
 
