@@ -22,7 +22,7 @@
  *  - The caller owns every buffer (W, M, G, workspace, optional outputs); size
  *    the workspace with dion2_workspace_size() and pass it to every step.  The
  *    library's only device allocation is a small plan-owned table (matrix
- *    descriptors and work lists, ~200 B per matrix), made once per (shapes,
+ *    descriptors and work lists, a few hundred bytes per matrix), made once per (shapes,
  *    config, workspace) plan on its first step and reused by every later step.
  *  - All work is enqueued asynchronously on `stream` (a cudaStream_t passed
  *    as void*; NULL = legacy default stream).  No host synchronisation
