@@ -105,6 +105,12 @@ def test_ns_schedules(coeffs, form):
     _assert(run_parity(shapes, 0.3, "auto", "bf16", steps=2, ns_form=form, ns_coeffs=coeffs), BF16_TOL)
 
 
+def test_gram_form_large_tile_grid():
+    """p_pad = 1280 (5 x 5 tile grid, 15 stored upper tiles; lower k-blocks read transposed
+    from four different tile rows) and p_pad = 768, ragged p and q."""
+    _assert(run_parity([(1100, 4400), (3000, 700)], 1.0, "auto", "bf16", steps=2, row_scaled=True), BF16_TOL)
+
+
 def test_gram_form_forced_on_square_x():
     # q = p: AUTO would pick DIRECT; forcing GRAM must still be within the bf16 gate
     _assert(run_parity([(384, 384), (512, 768)], 1.0, "auto", "bf16", steps=2, ns_form="gram"), BF16_TOL)
