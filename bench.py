@@ -285,10 +285,14 @@ def run_ours(args):
     n_params = sum(m * n for m, n in shapes)
     if use_dist:
         # owner-compute over all ranks: every matrix sharded along its non-selection axis
-        info = D.dist_info(shapes, world, rank, alpha=args.alpha)
-        bufs, Ws, Ms, Gs = build_state(info["shard"], dev, seed=rank, fan_in=[n for (_, n) in shapes])
+        # column-mode shards keep their momentum transposed (local to each rank), as on one GPU
+        info0 = D.dist_info(shapes, world, rank, alpha=args.alpha)
+        mts = [(not args.no_mt) and ax == 1 for ax in info0["axis"]]
+        info = D.dist_info(shapes, world, rank, alpha=args.alpha, m_transposed=mts)
+        bufs, Ws, Ms, Gs = build_state(info["shard"], dev, seed=rank, fan_in=[n for (_, n) in shapes],
+                                       m_transposed=mts)
         make_opt = lambda a: D.Dion2Dist(shapes, alpha=a, axis="auto", precision="bf16",  # noqa: E731
-                                          ns_form=args.ns_form)
+                                          ns_form=args.ns_form, m_transposed=mts)
     else:
         info = None
         # optimizer-state layout: momentum of column-mode matrices stored transposed (the
@@ -324,7 +328,7 @@ def run_ours(args):
     torch.cuda.empty_cache()
 
     peaks, peak_src = load_peaks()
-    ns_flops, byts = work_model(shapes, args.alpha, mt=(not use_dist) and not args.no_mt, ns_form=args.ns_form)
+    ns_flops, byts = work_model(shapes, args.alpha, mt=not args.no_mt, ns_form=args.ns_form)
     if use_dist:  # this rank's share: 1/world of every streaming pass, NS of its owned matrices
         owned = [s for s, o in zip(shapes, info["owner"]) if o == rank]
         ns_flops = work_model(owned, args.alpha, ns_form=args.ns_form)[0] if owned else {k: 0.0 for k in ns_flops}
@@ -460,8 +464,7 @@ def run_ours(args):
             "data": "synthetic (W0~N(0,1/n), G~N(0,1), M0=0; seeded device RNG)",
             "config": {"workload": f"{args.config}-set Dion2 step (configs[1])", "matrices": len(shapes),
                        "params": n_params, "alpha": args.alpha, "axis": "auto", "ns_steps": 5, "ns_form": args.ns_form,
-                       "momentum_layout": "column-mode matrices transposed" if (not use_dist and not args.no_mt)
-                       else "as W",
+                       "momentum_layout": "column-mode matrices transposed" if not args.no_mt else "as W",
                        "l2_flush": "not needed: 14.5 GB touched per step >> 126 MB L2",
                        "parallelism": "single GPU" if not use_dist else
                        f"owner-compute over {world} GPUs (NCCL; shards along the non-selection axis)"},

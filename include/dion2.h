@@ -43,7 +43,7 @@
 extern "C" {
 #endif
 
-#define DION2_ABI_VERSION 3
+#define DION2_ABI_VERSION 4
 #define DION2_MAX_NS_STEPS 16
 
 typedef enum {
@@ -178,6 +178,12 @@ typedef struct {
   float* M;            /* local shard of M, fp32 */
   const void* G;       /* local shard of G, dtype cfg.grad_dtype */
   int32_t* sel_out;    /* optional [k]: the selected indices (identical on every rank) */
+  int32_t m_transposed; /* 1: the local M shard is stored TRANSPOSED, [shard cols x ldm] row-major
+                           (column-mode matrices only, DION2_EUNSUPPORTED otherwise): the local
+                           column gather becomes a row gather; local to this rank, the exchanged
+                           pieces are the same either way */
+  int32_t reserved;     /* must be 0 */
+  int64_t ldm;          /* row stride of the transposed M shard (>= shard rows) */
 } dion2_shard;
 
 /* Host-only layout query for rank `rank` of `world` (no device work).  Any output may be NULL.

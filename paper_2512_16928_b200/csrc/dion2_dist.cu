@@ -69,6 +69,7 @@ struct DistMat {
   double flops;
   int path, ga, gb;
   int n_sumsq;
+  int mt;                  // local M shard stored transposed (cols mode): K1 transpose-add, row gather
   size_t off_partials, off_sel, off_sumsq;
 };
 
@@ -84,11 +85,13 @@ struct DistPlan {
   // device tables (plan-owned)
   std::vector<uint8_t> htab;
   void* dtab = nullptr;
-  size_t t_desc, t_rowmats, t_rowprefix, t_colmats, t_colprefix, t_flm[2], t_flg[2], t_fls[2], t_gidx, t_roff,
-      t_gprefix;
-  int n_row_mats = 0, n_col_mats = 0, fl_n[2] = {0, 0}, fl_gunits[2] = {0, 0}, fl_sunits[2] = {0, 0}, fl_maxk = 0,
-      max_d = 0, total_gather_tiles = 0;
-  int64_t total_rows = 0, total_col_tiles = 0, max_cols_col = 0;
+  // streaming lists: gather and scatter membership differ for transposed-M column matrices
+  // (row gather on M^T, column scatter on W)
+  size_t t_desc, t_rowmats, t_rowprefix, t_colmats, t_colprefix, t_mtmats, t_mtprefix, t_allcols, t_flgm[2],
+      t_flsm[2], t_flg[2], t_fls[2], t_gidx, t_roff, t_gprefix;
+  int n_row_mats = 0, n_col_mats = 0, n_mt_mats = 0, n_allcols = 0, fl_gn[2] = {0, 0}, fl_sn[2] = {0, 0},
+      fl_gunits[2] = {0, 0}, fl_sunits[2] = {0, 0}, fl_maxk = 0, max_d = 0, total_gather_tiles = 0;
+  int64_t total_rows = 0, total_col_tiles = 0, total_mt_tiles = 0, max_cols_col = 0;
   std::vector<const void*> last_ptrs;
   bool uploaded = false;
   // owner side
@@ -130,6 +133,10 @@ int resolve(DistPlan& D, const dion2_shard* sh, int n, const dion2_config* c, in
       q.scols = q.n;
     }
     if (sh[j].ld < q.scols) return DION2_EINVAL_SHAPE;
+    if (sh[j].reserved != 0 || (sh[j].m_transposed != 0 && sh[j].m_transposed != 1)) return DION2_EINVAL_SHAPE;
+    q.mt = sh[j].m_transposed;
+    if (q.mt && q.axis != DION2_AXIS_COLS) return DION2_EUNSUPPORTED;
+    if (q.mt && sh[j].ldm < q.srows) return DION2_EINVAL_SHAPE;
     q.piece = (int64_t)align_up((size_t)q.k * q.qo * 2, 256);
     const double p = q.k, qq = q.o;
     q.flops = c->ns_steps * (4.0 * p * p * qq + 2.0 * p * p * p);
@@ -137,7 +144,7 @@ int resolve(DistPlan& D, const dion2_shard* sh, int n, const dion2_config* c, in
     q.path = q.axis == DION2_AXIS_ROWS ? 1 : ((q.qo % 32 == 0 && q.k <= kMaxColKFast) ? 2 : 0);
     q.ga = q.path == 0 ? (int)ceil_div(q.srows, kTileA) : 0;
     q.gb = q.path == 0 ? (int)ceil_div(q.k, kTileB) : 0;
-    q.n_sumsq = q.path == 1 ? q.k : (q.path == 2 ? q.qo / 32 : q.ga * q.gb);
+    q.n_sumsq = (q.path == 1 || q.mt) ? q.k : (q.path == 2 ? q.qo / 32 : q.ga * q.gb);
   }
   // owners: LPT on NS FLOPs (descending, ties -> lower index), least-loaded rank (ties -> lower rank)
   std::vector<int> order(n);
@@ -227,8 +234,12 @@ int build_tables(DistPlan& D, const dion2_config* c, void* ws) {
   D.t_rowprefix = take(8 * (size_t)n);
   D.t_colmats = take(4 * (size_t)n);
   D.t_colprefix = take(8 * (size_t)n);
+  D.t_mtmats = take(4 * (size_t)n);
+  D.t_mtprefix = take(8 * (size_t)n);
+  D.t_allcols = take(4 * (size_t)n);
   for (int l = 0; l < 2; ++l) {
-    D.t_flm[l] = take(4 * (size_t)n);
+    D.t_flgm[l] = take(4 * (size_t)n);
+    D.t_flsm[l] = take(4 * (size_t)n);
     D.t_flg[l] = take(4 * (size_t)n);
     D.t_fls[l] = take(4 * (size_t)n);
   }
@@ -239,11 +250,11 @@ int build_tables(DistPlan& D, const dion2_config* c, void* ws) {
   if (!D.dtab && cudaMalloc(&D.dtab, off) != cudaSuccess) return DION2_ECUDA;
   auto H = [&](size_t o) { return D.htab.data() + o; };
   MatDesc* md = reinterpret_cast<MatDesc*>(H(D.t_desc));
-  std::vector<int32_t> rowmats, colmats, flm[2], flg[2], fls[2];
-  std::vector<int64_t> rowprefix, colprefix;
+  std::vector<int32_t> rowmats, colmats, mtmats, allcols, flgm[2], flsm[2], flg[2], fls[2];
+  std::vector<int64_t> rowprefix, colprefix, mtprefix;
   std::vector<int32_t> gprefix(n, 0);
   D.total_gather_tiles = 0;
-  D.total_rows = D.total_col_tiles = 0;
+  D.total_rows = D.total_col_tiles = D.total_mt_tiles = 0;
   D.fl_gunits[0] = D.fl_gunits[1] = D.fl_sunits[0] = D.fl_sunits[1] = 0;
   D.fl_maxk = D.max_d = 0;
   D.max_cols_col = 0;
@@ -282,6 +293,7 @@ int build_tables(DistPlan& D, const dion2_config* c, void* ws) {
     d.mid = j;
     d.path = q.path;
     d.n_sumsq = q.n_sumsq;
+    d.mt = q.mt;
     d.scores_final = 1;
     d.gather_tile_base = D.total_gather_tiles;
     d.gather_tiles_a = q.ga;
@@ -295,23 +307,44 @@ int build_tables(DistPlan& D, const dion2_config* c, void* ws) {
       rowprefix.push_back(D.total_rows);
       D.total_rows += q.srows;
     } else {
-      colmats.push_back(j);
-      colprefix.push_back(D.total_col_tiles);
-      D.total_col_tiles += (int64_t)d.rowblocks * ceil_div(q.scols, 256);
+      allcols.push_back(j);
       D.max_cols_col = std::max<int64_t>(D.max_cols_col, q.scols);
+      if (q.mt) {
+        mtmats.push_back(j);
+        mtprefix.push_back(D.total_mt_tiles);
+        D.total_mt_tiles += (int64_t)d.rowblocks * ceil_div(q.scols, 64);
+      } else {
+        colmats.push_back(j);
+        colprefix.push_back(D.total_col_tiles);
+        D.total_col_tiles += (int64_t)d.rowblocks * ceil_div(q.scols, 256);
+      }
     }
-    if (d.path == 0) continue;
-    const int l = d.path - 1;
-    flm[l].push_back(j);
-    flg[l].push_back(D.fl_gunits[l]);
-    fls[l].push_back(D.fl_sunits[l]);
-    D.fl_gunits[l] += l == 0 ? q.k : q.qo / 32;
-    D.fl_sunits[l] += l == 0 ? q.k : q.qo / 32;
-    if (l == 1) D.fl_maxk = std::max(D.fl_maxk, q.k);
+    // gather: rows streaming (rows mode, or transposed-M columns = rows of M^T), cols streaming,
+    // or generic tiles; scatter: by path
+    const int lg = (d.path == 1 || q.mt) ? 0 : d.path - 1;
+    const int ls = d.path - 1;
+    if (lg >= 0) {
+      flgm[lg].push_back(j);
+      flg[lg].push_back(D.fl_gunits[lg]);
+      D.fl_gunits[lg] += lg == 0 ? q.k : q.qo / 32;
+    }
+    if (ls >= 0) {
+      flsm[ls].push_back(j);
+      fls[ls].push_back(D.fl_sunits[ls]);
+      D.fl_sunits[ls] += ls == 0 ? q.k : q.qo / 32;
+    }
+    if (lg == 1 || ls == 1) D.fl_maxk = std::max(D.fl_maxk, q.k);
   }
   memcpy(H(D.t_gprefix), gprefix.data(), 4 * (size_t)n);
   D.n_row_mats = (int)rowmats.size();
   D.n_col_mats = (int)colmats.size();
+  D.n_mt_mats = (int)mtmats.size();
+  D.n_allcols = (int)allcols.size();
+  if (D.n_mt_mats) {
+    memcpy(H(D.t_mtmats), mtmats.data(), 4 * mtmats.size());
+    memcpy(H(D.t_mtprefix), mtprefix.data(), 8 * mtprefix.size());
+  }
+  if (D.n_allcols) memcpy(H(D.t_allcols), allcols.data(), 4 * allcols.size());
   if (D.n_row_mats) {
     memcpy(H(D.t_rowmats), rowmats.data(), 4 * rowmats.size());
     memcpy(H(D.t_rowprefix), rowprefix.data(), 8 * rowprefix.size());
@@ -321,10 +354,14 @@ int build_tables(DistPlan& D, const dion2_config* c, void* ws) {
     memcpy(H(D.t_colprefix), colprefix.data(), 8 * colprefix.size());
   }
   for (int l = 0; l < 2; ++l) {
-    D.fl_n[l] = (int)flm[l].size();
-    if (D.fl_n[l]) {
-      memcpy(H(D.t_flm[l]), flm[l].data(), 4 * flm[l].size());
+    D.fl_gn[l] = (int)flgm[l].size();
+    D.fl_sn[l] = (int)flsm[l].size();
+    if (D.fl_gn[l]) {
+      memcpy(H(D.t_flgm[l]), flgm[l].data(), 4 * flgm[l].size());
       memcpy(H(D.t_flg[l]), flg[l].data(), 4 * flg[l].size());
+    }
+    if (D.fl_sn[l]) {
+      memcpy(H(D.t_flsm[l]), flsm[l].data(), 4 * flsm[l].size());
       memcpy(H(D.t_fls[l]), fls[l].data(), 4 * fls[l].size());
     }
   }
@@ -376,6 +413,7 @@ std::string dist_key(const dion2_shard* sh, int n, const dion2_config* c, int wo
     put(&sh[i].rows, 8);
     put(&sh[i].cols, 8);
     put(&sh[i].ld, 8);
+    put(&sh[i].m_transposed, 4);
   }
   put(&c->alpha, 4);
   put(&c->ns_steps, 4);
@@ -412,24 +450,27 @@ int get_plan(DistPlan** out, const dion2_shard* sh, int n, const dion2_config* c
 // refresh the caller's shard pointers in the device table (upload only when they change)
 int refresh(DistPlan& D, const dion2_shard* sh, const dion2_config* c, cudaStream_t s) {
   bool up = !D.uploaded;
-  if ((int)D.last_ptrs.size() != 4 * D.n) {
-    D.last_ptrs.assign(4 * D.n, nullptr);
+  if ((int)D.last_ptrs.size() != 5 * D.n) {
+    D.last_ptrs.assign(5 * D.n, nullptr);
     up = true;
   }
   MatDesc* md = reinterpret_cast<MatDesc*>(D.htab.data() + D.t_desc);
   for (int j = 0; j < D.n; ++j) {
-    const void* p[4] = {sh[j].W, sh[j].M, sh[j].G, sh[j].sel_out};
-    for (int t = 0; t < 4; ++t)
-      if (D.last_ptrs[4 * j + t] != p[t]) { up = true; D.last_ptrs[4 * j + t] = p[t]; }
+    const void* p[5] = {sh[j].W, sh[j].M, sh[j].G, sh[j].sel_out,
+                        reinterpret_cast<const void*>((uintptr_t)(sh[j].m_transposed ? sh[j].ldm : 0))};
+    for (int t = 0; t < 5; ++t)
+      if (D.last_ptrs[5 * j + t] != p[t]) { up = true; D.last_ptrs[5 * j + t] = p[t]; }
     md[j].W = sh[j].W;
     md[j].M = sh[j].M;
     md[j].G = sh[j].G;
     md[j].sel_out = sh[j].sel_out;
     md[j].O_out = nullptr;
     md[j].ld = sh[j].ld;
+    md[j].ldm = sh[j].m_transposed ? sh[j].ldm : 0;
     const size_t gel = c->grad_dtype == DION2_DT_BF16 ? 2 : 4;
     md[j].vec4 = ((uintptr_t)sh[j].W % 16 == 0) && ((uintptr_t)sh[j].M % 16 == 0) &&
-                 ((uintptr_t)sh[j].G % (gel == 4 ? 16 : 8) == 0) && (sh[j].ld % 4 == 0);
+                 ((uintptr_t)sh[j].G % (gel == 4 ? 16 : 8) == 0) && (sh[j].ld % 4 == 0) &&
+                 (!sh[j].m_transposed || sh[j].ldm % 4 == 0);
   }
   if (up) {
     if (cudaMemcpyAsync(D.dtab, D.htab.data(), D.htab.size(), cudaMemcpyHostToDevice, s) != cudaSuccess)
@@ -463,8 +504,18 @@ void phase_local_k1(DistPlan& D, void* ws, Launcher& L, cudaStream_t s) {
                                                            (const int64_t*)dt(D, D.t_colprefix), D.n_col_mats,
                                                            D.total_col_tiles);
     L.end();
+  }
+  if (D.n_mt_mats) {
+    L.begin(PH_K1_MT);
+    const int64_t blocks = std::min<int64_t>(D.total_mt_tiles, (int64_t)sms * 8);
+    k_momentum_score_cols_mt<<<(unsigned)blocks, 256, 0, s>>>(dm, (const int32_t*)dt(D, D.t_mtmats),
+                                                              (const int64_t*)dt(D, D.t_mtprefix), D.n_mt_mats,
+                                                              D.total_mt_tiles);
+    L.end();
+  }
+  if (D.n_allcols) {
     L.begin(PH_K1);
-    launch_cols_local_scores(s, dm, (const int32_t*)dt(D, D.t_colmats), D.n_col_mats, D.max_cols_col);
+    launch_cols_local_scores(s, dm, (const int32_t*)dt(D, D.t_allcols), D.n_allcols, D.max_cols_col);
     L.end();
   }
 }
@@ -491,18 +542,18 @@ void phase_gather(DistPlan& D, void* ws, const dion2_config* c, Launcher& L, cud
                         D.total_gather_tiles, bad, 1, c->mu);
     L.end();
   }
-  if (D.fl_n[0]) {
+  if (D.fl_gn[0]) {
     L.begin(PH_GATHER_ROWS);
     const int blocks = (int)std::min<int64_t>(ceil_div(D.fl_gunits[0], 8), (int64_t)sms * 8);
-    launch_gather_rows(blocks, s, dm, (const int32_t*)dt(D, D.t_flm[0]), (const int32_t*)dt(D, D.t_flg[0]), D.fl_n[0],
-                       D.fl_gunits[0], bad, c->mu);
+    launch_gather_rows(blocks, s, dm, (const int32_t*)dt(D, D.t_flgm[0]), (const int32_t*)dt(D, D.t_flg[0]),
+                       D.fl_gn[0], D.fl_gunits[0], bad, c->mu);
     L.end();
   }
-  if (D.fl_n[1]) {
+  if (D.fl_gn[1]) {
     L.begin(PH_GATHER_COLS);
-    const int blocks = std::min(D.fl_gunits[1], sms * 4);
-    launch_gather_cols_t(blocks, D.fl_maxk, D.max_cols_col, s, dm, (const int32_t*)dt(D, D.t_flm[1]),
-                         (const int32_t*)dt(D, D.t_flg[1]), D.fl_n[1], D.fl_gunits[1], bad, c->mu);
+    const int blocks = std::min(D.fl_gunits[1], sms * 6);  // as the single-GPU path
+    launch_gather_cols_t(blocks, D.fl_maxk, D.max_cols_col, s, dm, (const int32_t*)dt(D, D.t_flgm[1]),
+                         (const int32_t*)dt(D, D.t_flg[1]), D.fl_gn[1], D.fl_gunits[1], bad, c->mu);
     L.end();
   }
   L.begin(PH_NORM);
@@ -534,18 +585,18 @@ void phase_scatter(DistPlan& D, void* ws, const dion2_config* c, Launcher& L, cu
                           D.n, D.total_gather_tiles, bad, c->lr);
     L.end();
   }
-  if (D.fl_n[0]) {
+  if (D.fl_sn[0]) {
     L.begin(PH_SCATTER_ROWS);
     const int blocks = (int)std::min<int64_t>(ceil_div(D.fl_sunits[0], 8), (int64_t)sms * 8);
-    launch_scatter_rows(blocks, s, dm, (const int32_t*)dt(D, D.t_flm[0]), (const int32_t*)dt(D, D.t_fls[0]), D.fl_n[0],
-                        D.fl_sunits[0], bad, c->lr);
+    launch_scatter_rows(blocks, s, dm, (const int32_t*)dt(D, D.t_flsm[0]), (const int32_t*)dt(D, D.t_fls[0]),
+                        D.fl_sn[0], D.fl_sunits[0], bad, c->lr);
     L.end();
   }
-  if (D.fl_n[1]) {
+  if (D.fl_sn[1]) {
     L.begin(PH_SCATTER_COLS);
-    const int blocks = std::min(D.fl_sunits[1], sms * 4);
-    launch_scatter_cols_t(blocks, D.fl_maxk, D.max_cols_col, s, dm, (const int32_t*)dt(D, D.t_flm[1]),
-                          (const int32_t*)dt(D, D.t_fls[1]), D.fl_n[1], D.fl_sunits[1], bad, c->lr);
+    const int blocks = std::min(D.fl_sunits[1], sms * 6);  // as the single-GPU path
+    launch_scatter_cols_t(blocks, D.fl_maxk, D.max_cols_col, s, dm, (const int32_t*)dt(D, D.t_flsm[1]),
+                          (const int32_t*)dt(D, D.t_fls[1]), D.fl_sn[1], D.fl_sunits[1], bad, c->lr);
     L.end();
   }
 }

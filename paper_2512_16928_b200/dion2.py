@@ -21,7 +21,7 @@ AXIS = {"rows": 0, "cols": 1, "auto": 2}
 PRECISION = {"bf16": 0, "fp32": 1}
 SELECT = {"l1": 0, "random": 1}
 NS_FORM = {"auto": 0, "direct": 1, "gram": 2}
-ABI_VERSION = 3  # include/dion2.h DION2_ABI_VERSION
+ABI_VERSION = 4  # include/dion2.h DION2_ABI_VERSION
 STATUS = {0: "OK", 1: "EINVAL_CONFIG", 2: "EINVAL_SHAPE", 3: "EWORKSPACE", 4: "EUNSUPPORTED",
           5: "ECUDA", 6: "ENCCL", 7: "ENONFINITE"}
 EXPORTED = ["dion2_config_init", "dion2_workspace_size", "dion2_step", "dion2_step_batched", "dion2_get_status",
@@ -49,7 +49,8 @@ class Dion2Config(ctypes.Structure):
 
 class Dion2Shard(ctypes.Structure):
     _fields_ = [("rows", ctypes.c_int64), ("cols", ctypes.c_int64), ("ld", ctypes.c_int64),
-                ("W", ctypes.c_void_p), ("M", ctypes.c_void_p), ("G", ctypes.c_void_p), ("sel_out", ctypes.c_void_p)]
+                ("W", ctypes.c_void_p), ("M", ctypes.c_void_p), ("G", ctypes.c_void_p), ("sel_out", ctypes.c_void_p),
+                ("m_transposed", ctypes.c_int32), ("reserved", ctypes.c_int32), ("ldm", ctypes.c_int64)]
 
 
 class Dion2Error(RuntimeError):
@@ -252,15 +253,25 @@ def last_launch_count() -> int:
 
 
 # ----------------------------------------------------------------------------------- multi-GPU
-def _shards(shapes, Ws=None, Ms=None, Gs=None, sels=None):
+def _shards(shapes, Ws=None, Ms=None, Gs=None, sels=None, m_transposed=None):
+    """m_transposed[i]: the local M shard is stored transposed, shape (shard cols, shard rows)."""
     n = len(shapes)
     arr = (Dion2Shard * n)()
     for i, (m, nn) in enumerate(shapes):
         arr[i].rows, arr[i].cols = m, nn
+        mt = bool(m_transposed[i]) if m_transposed is not None else False
+        arr[i].m_transposed = 1 if mt else 0
+        arr[i].ldm = 1 << 40
         if Ws is not None:
             W = Ws[i]
             _check_tensor(W, "W shard", torch.float32)
-            _check_tensor(Ms[i], "M shard", torch.float32, W)
+            if mt:
+                _check_tensor(Ms[i], "M shard (transposed)", torch.float32)
+                if tuple(Ms[i].shape) != (W.shape[1], W.shape[0]):
+                    raise ValueError("a transposed M shard must have shape (shard cols, shard rows)")
+                arr[i].ldm = Ms[i].stride(0)
+            else:
+                _check_tensor(Ms[i], "M shard", torch.float32, W)
             _check_tensor(Gs[i], "G shard", Gs[0].dtype, W)
             arr[i].ld = W.stride(0)
             arr[i].W, arr[i].M, arr[i].G = W.data_ptr(), Ms[i].data_ptr(), Gs[i].data_ptr()
@@ -271,12 +282,12 @@ def _shards(shapes, Ws=None, Ms=None, Gs=None, sels=None):
     return arr
 
 
-def dist_info(shapes: Sequence[Tuple[int, int]], world: int, rank: int, **cfg_kw) -> dict:
+def dist_info(shapes: Sequence[Tuple[int, int]], world: int, rank: int, m_transposed=None, **cfg_kw) -> dict:
     """Host-only layout of the owner-compute step (dion2_dist_info): per matrix the
     resolved axis, owner rank and local shard shape; per peer the bytes sent/received in
     one exchange direction; this rank's workspace size."""
     n = len(shapes)
-    arr = _shards(shapes)
+    arr = _shards(shapes, m_transposed=m_transposed)
     cfg = make_config(**cfg_kw)
     ax, own = (ctypes.c_int32 * n)(), (ctypes.c_int32 * n)()
     sr, sc = (ctypes.c_int64 * n)(), (ctypes.c_int64 * n)()
@@ -313,14 +324,16 @@ class Dion2Dist:
     shapes: the GLOBAL (m, n) of every matrix; each rank passes its local shards
     (see dist_info()["shard"] and shard_of())."""
 
-    def __init__(self, shapes, group=None, **cfg_kw):
+    def __init__(self, shapes, group=None, m_transposed=None, **cfg_kw):
+        """m_transposed: per matrix, the local M shard is stored transposed (column-mode only)."""
         import torch.distributed as dist
         self.shapes = [tuple(s) for s in shapes]
         self.group = group
         self.world = dist.get_world_size(group)
         self.rank = dist.get_rank(group)
         self.cfg_kw = dict(cfg_kw)
-        self.info = dist_info(self.shapes, self.world, self.rank, **cfg_kw)
+        self.m_transposed = m_transposed
+        self.info = dist_info(self.shapes, self.world, self.rank, m_transposed=m_transposed, **cfg_kw)
         self._ws: Optional[torch.Tensor] = None
         self.last_comm_bytes = 0
 
@@ -333,7 +346,7 @@ class Dion2Dist:
         need = self.info["workspace_bytes"]
         if self._ws is None or self._ws.numel() < need:
             self._ws = torch.empty(need, dtype=torch.uint8, device=dev)
-        arr = _shards(self.shapes, Ws, Ms, Gs, sel_out)
+        arr = _shards(self.shapes, Ws, Ms, Gs, sel_out, self.m_transposed)
         st = stream if stream is not None else torch.cuda.current_stream(dev)
         nbytes = ctypes.c_uint64(0)
         rc = _lib().dion2_step_batched_dist(arr, len(self.shapes), ctypes.byref(cfg), self._ws.data_ptr(),
@@ -354,11 +367,12 @@ class Dion2Loopback:
     exchanges are device copies (dion2_step_batched_loopback).  For testing the
     distributed layout and kernels without several GPUs."""
 
-    def __init__(self, shapes, world, **cfg_kw):
+    def __init__(self, shapes, world, m_transposed=None, **cfg_kw):
         self.shapes = [tuple(s) for s in shapes]
         self.world = world
         self.cfg_kw = dict(cfg_kw)
-        self.infos = [dist_info(self.shapes, world, r, **cfg_kw) for r in range(world)]
+        self.m_transposed = m_transposed
+        self.infos = [dist_info(self.shapes, world, r, m_transposed=m_transposed, **cfg_kw) for r in range(world)]
         self._ws: List[torch.Tensor] = []
         self.last_comm_bytes = 0
 
@@ -375,7 +389,8 @@ class Dion2Loopback:
             self._ws = [torch.empty(need, dtype=torch.uint8, device=dev) for _ in range(P)]
         arr = (Dion2Shard * (n * P))()
         for r in range(P):
-            part = _shards(self.shapes, Ws[r], Ms[r], Gs[r], sel_out[r] if sel_out is not None else None)
+            part = _shards(self.shapes, Ws[r], Ms[r], Gs[r], sel_out[r] if sel_out is not None else None,
+                           self.m_transposed)
             for i in range(n):
                 arr[r * n + i] = part[i]
         wsp = (ctypes.c_void_p * P)(*[w.data_ptr() for w in self._ws])

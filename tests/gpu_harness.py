@@ -148,7 +148,7 @@ def _finish(res, shapes, Wg, Mg, Wr, Mr, W0):
 
 
 def run_parity_dist(shapes, alpha, world, steps=3, seed=0, mode="loopback", axis="auto", mu=0.95, lr=0.02,
-                    row_scaled=True, device="cuda", select="l1", sel_seed=0):
+                    row_scaled=True, device="cuda", select="l1", sel_seed=0, m_transposed=False):
     """Distributed step (owner-compute, shards along the non-selection axis) against the
     fp64 oracle on the FULL matrices.  mode = "loopback" (all ranks in this process) or
     "nccl" (world must equal the initialised torch.distributed world; this process is
@@ -167,16 +167,22 @@ def run_parity_dist(shapes, alpha, world, steps=3, seed=0, mode="loopback", axis
     for (m, n) in shapes:
         ax = O.resolve_axis(m, n, cfg_o.axis)
         ks.append(O.select_count(cfg_o.alpha, m if ax == O.AXIS_ROWS else n))
+    # transposed local M shards for the column-mode matrices (m_transposed)
+    mts = [bool(m_transposed) and axes[i] == 1 for i in range(len(shapes))]
     if mode == "loopback":
         ranks = list(range(world))
-        opt = D.Dion2Loopback(shapes, world, alpha=alpha, axis=axis, mu=mu, lr=lr, select=select, seed=sel_seed)
+        opt = D.Dion2Loopback(shapes, world, alpha=alpha, axis=axis, mu=mu, lr=lr, select=select, seed=sel_seed,
+                              m_transposed=mts)
     else:
         import torch.distributed as dist
         ranks = [dist.get_rank()]
-        opt = D.Dion2Dist(shapes, alpha=alpha, axis=axis, mu=mu, lr=lr, select=select, seed=sel_seed)
+        opt = D.Dion2Dist(shapes, alpha=alpha, axis=axis, mu=mu, lr=lr, select=select, seed=sel_seed,
+                          m_transposed=mts)
     full = lambda a, i: torch.from_numpy(a)  # noqa: E731
     Wg = {r: [D.shard_of(full(W0[i], i), axes[i], world, r).to(device) for i in range(len(shapes))] for r in ranks}
-    Mg = {r: [torch.zeros_like(w) for w in Wg[r]] for r in ranks}
+    Mg = {r: [torch.zeros((w.shape[1], w.shape[0]), device=device) if mts[i] else torch.zeros_like(w)
+              for i, w in enumerate(Wg[r])] for r in ranks}
+    Mv = {r: [Mg[r][i].T if mts[i] else Mg[r][i] for i in range(len(shapes))] for r in ranks}  # W-layout views
 
     def assemble(parts_by_rank, i):
         if mode == "loopback":
@@ -216,7 +222,7 @@ def run_parity_dist(shapes, alpha, world, steps=3, seed=0, mode="loopback", axis
                 else:
                     res.index_mismatch += 1
     Wfull = [assemble(Wg, i) for i in range(len(shapes))]
-    Mfull = [assemble(Mg, i) for i in range(len(shapes))]
+    Mfull = [assemble(Mv, i) for i in range(len(shapes))]
     _finish(res, shapes, Wfull, Mfull, Wr, Mr, W0)
     res.comm_bytes = opt.last_comm_bytes
     return res

@@ -35,6 +35,18 @@ def test_loopback_parity(world):
     _assert(run_parity_dist(SHAPES, 0.25, world, steps=3))
 
 
+@pytest.mark.parametrize("world", [1, 2, 4])
+def test_loopback_transposed_momentum(world):
+    """Column-mode matrices with their local M shards stored transposed (K1 transpose-add,
+    row gather of M^T into the pieces; the exchanged pieces are unchanged)."""
+    _assert(run_parity_dist(SHAPES + [(1024, 256), (4096, 1024)], 0.25, world, steps=3, m_transposed=True))
+
+
+@pytest.mark.parametrize("world", [2, 8])
+def test_loopback_1b_layer_transposed_momentum(world):
+    _assert(run_parity_dist(layer_set_1b(1), 0.25, world, steps=2, m_transposed=True))
+
+
 @pytest.mark.parametrize("world", [2, 8])
 def test_loopback_one_layer_of_the_1b_set(world):
     _assert(run_parity_dist(layer_set_1b(1), 0.25, world, steps=2))
@@ -76,5 +88,6 @@ def test_nccl_transport_single_rank():
     try:
         res = run_parity_dist(SHAPES, 0.25, 1, steps=3, mode="nccl")
         _assert(res)
+        _assert(run_parity_dist(SHAPES + [(1024, 256)], 0.25, 1, steps=2, mode="nccl", m_transposed=True))
     finally:
         dist.destroy_process_group()
