@@ -751,8 +751,6 @@ std::map<std::string, std::unique_ptr<DpPlan>> g_dp_plans;
 int dp_layout(DpPlan& D, const dion2_matrix* mats, int n, const dion2_config* c, int world) {
   if (c->select != DION2_SELECT_RANDOM) return DION2_EUNSUPPORTED;  // l1 scores need the full momentum
   if (world < 1) return DION2_EINVAL_SHAPE;
-  for (int i = 0; i < n; ++i)
-    if (mats[i].m_transposed) return DION2_EUNSUPPORTED;
   D.world = world;
   int rc = build_layout(D.P, mats, n, c);
   if (rc) return rc;
@@ -760,7 +758,7 @@ int dp_layout(DpPlan& D, const dion2_matrix* mats, int n, const dion2_config* c,
   D.total_rows = 0;
   for (auto& q : D.P.mp) {
     D.buf_floats += (int64_t)q.sr * q.sc;
-    D.total_rows += q.sr;
+    D.total_rows += q.mt ? q.sc : q.sr;  // pack units: rows of S, or rows of S^T (transposed M)
   }
   D.off_buf = align_up(D.P.total, 4096);
   D.off_gather = align_up(D.off_buf + 4 * (size_t)D.buf_floats, 4096);
@@ -781,6 +779,7 @@ int dp_get_plan(DpPlan** out, const dion2_matrix* mats, int n, const dion2_confi
     put(&mats[i].rows, 8);
     put(&mats[i].cols, 8);
     put(&mats[i].ld, 8);
+    put(&mats[i].m_transposed, 4);
   }
   put(&c->alpha, 4);
   put(&c->ns_steps, 4);
@@ -790,6 +789,7 @@ int dp_get_plan(DpPlan** out, const dion2_matrix* mats, int n, const dion2_confi
   put(&c->grad_dtype, 4);
   put(&c->decay_mode, 4);
   put(&c->scale_mode, 4);
+  put(&c->ns_form, 4);
   auto it = g_dp_plans.find(key);
   if (it == g_dp_plans.end()) {
     auto D = std::make_unique<DpPlan>();
@@ -807,7 +807,7 @@ int dp_get_plan(DpPlan** out, const dion2_matrix* mats, int n, const dion2_confi
     for (int i = 0; i < n; ++i) {
       pre[i] = rows;
       off[i] = fo;
-      rows += D->P.mp[i].sr;
+      rows += D->P.mp[i].mt ? D->P.mp[i].sc : D->P.mp[i].sr;
       fo += (int64_t)D->P.mp[i].sr * D->P.mp[i].sc;
     }
     if (cudaMalloc(&D->dtab, D->htab.size()) != cudaSuccess) return DION2_ECUDA;

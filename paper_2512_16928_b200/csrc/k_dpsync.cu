@@ -1,7 +1,9 @@
 // Compressed DP-sync: pack the selected fp32 submatrix
 // S = M[K, :] (or M[:, K]) of every matrix into one contiguous buffer for the
 // all-reduce, and write the averaged rows back.  One warp per row of S; rows
-// mode streams contiguous rows of M, cols mode gathers the selected columns.
+// mode streams contiguous rows of M, cols mode gathers the selected columns, and cols
+// mode with transposed M packs the contiguous rows of S^T (every replica must use the
+// same layout).
 #include "kernels.cuh"
 
 namespace dion2 {
@@ -28,6 +30,16 @@ __global__ void __launch_bounds__(256) k_dp_pack(const MatDesc* __restrict__ mat
     const MatDesc& md = mats[mi];
     if (kUnpack && bad[mi]) continue;
     const int a = u - row_prefix[mi];
+    if (md.mt) {
+      // transposed M (cols mode): unit a = row sel[a] of M^T = S^T row a, contiguous
+      float* b = buf + buf_off[mi] + (int64_t)a * md.rows;
+      float* mrow = md.M + (int64_t)md.sel[a] * md.ldm;
+      for (int c = lane; c < md.rows; c += 32) {
+        if (kUnpack) mrow[c] = scale * b[c];
+        else b[c] = mrow[c];
+      }
+      continue;
+    }
     float* b = buf + buf_off[mi] + (int64_t)a * md.sc;
     if (md.axis == kAxisRows) {
       float* mrow = md.M + (int64_t)md.sel[a] * md.ld;

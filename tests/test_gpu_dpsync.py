@@ -18,16 +18,19 @@ pytestmark = pytest.mark.gpu
 SHAPES = [(256, 512), (512, 256), (384, 640), (1024, 512)]
 
 
-def _run(world, precision, tol, steps=3, mode="loopback"):
+def _run(world, precision, tol, steps=3, mode="loopback", m_transposed=False):
+    """m_transposed: column-mode matrices keep M transposed (cols, rows) on every replica."""
     seed, alpha = 21, 0.25
     W0 = [gen_w0(m, n, 0, i) for i, (m, n) in enumerate(SHAPES)]
     reps = world if mode == "loopback" else 1
+    mts = [m_transposed and m > n for (m, n) in SHAPES]
     Wg = [[torch.from_numpy(w).cuda() for w in W0] for _ in range(reps)]
-    Mg = [[torch.zeros(m, n, device="cuda") for (m, n) in SHAPES] for _ in range(reps)]
+    Mg = [[torch.zeros((n, m) if mt else (m, n), device="cuda") for (m, n), mt in zip(SHAPES, mts)]
+          for _ in range(reps)]
     Wr = [[w.astype(np.float64) for w in W0] for _ in range(world)]
     Mr = [[np.zeros((m, n)) for (m, n) in SHAPES] for _ in range(world)]
     opt = D.Dion2DpSync(loopback_world=world if mode == "loopback" else 0, alpha=alpha, precision=precision,
-                        seed=seed)
+                        seed=seed, m_transposed=mts)
     for t in range(steps):
         G = [[gen_grad(m, n, 100 + r, i, t) for i, (m, n) in enumerate(SHAPES)] for r in range(world)]
         if mode == "loopback":
@@ -46,7 +49,7 @@ def _run(world, precision, tol, steps=3, mode="loopback"):
             wg = Wg[r][i].cpu().double().numpy()
             err = np.linalg.norm((wg - w0) - (Wr[r][i] - w0)) / np.linalg.norm(Wr[r][i] - w0)
             assert err <= tol, (i, r, err)
-            mg = Mg[r][i].cpu().double().numpy()
+            mg = (Mg[r][i].T if mts[i] else Mg[r][i]).cpu().double().numpy()
             assert np.abs(mg - Mr[r][i]).max() <= 1e-5 * np.abs(Mr[r][i]).max()
     return opt
 
@@ -57,6 +60,11 @@ def test_dpsync_loopback(world, precision, tol):
     opt = _run(world, precision, tol)
     k_o = sum(O.selected_bytes(m, n, 0.25, O.AXIS_AUTO, 4) for (m, n) in SHAPES)
     assert opt.last_comm_bytes == int(2.0 * (world - 1) / world * k_o)   # ~alpha of full gradient sync
+
+
+@pytest.mark.parametrize("world", [2, 3])
+def test_dpsync_loopback_transposed_momentum(world):
+    _run(world, "bf16", 2e-2, m_transposed=True)
 
 
 def test_dpsync_nccl_single_rank():
