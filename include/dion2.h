@@ -221,7 +221,9 @@ int dion2_step_batched_loopback(const dion2_shard* shards, int32_t n, const dion
  * rest of Alg. 1 on identical rows, so W stays identical while unselected momentum rows diverge;
  * by linearity the mean momentum equals the full-sync momentum and the W trajectory equals
  * full gradient sync ("the information that is synchronized suffices to compute the correct
- * parameter update").  cfg.select must be RANDOM (EUNSUPPORTED otherwise).
+ * parameter update").  cfg.select must be RANDOM (EUNSUPPORTED otherwise).  Matrices
+ * with m_transposed = 1 contribute the rows of S^T = M^T[K, :] to the averaged buffer; every
+ * replica must pass the same m_transposed flags.
  * ------------------------------------------------------------------------------------------ */
 int dion2_dpsync_workspace_size(const dion2_matrix* mats, int32_t n, const dion2_config* cfg, int32_t world,
                                 size_t* bytes_out);
