@@ -90,3 +90,12 @@ def test_gram_form_short_schedules(coeffs):
     X = gen_grad(48, 300, seed=1)
     want = O.newton_schulz(X.astype(np.float64), coeffs)
     assert _rel(gram_form(X, coeffs), want) < 1e-2
+
+
+def test_gram_form_at_large_p():
+    """AUTO also takes the Gram form for the 8B set's wide matrices (p = 1024 .. 4096): fp16
+    Gram entries of order 1/(p sqrt(q)) reach the subnormal range there; the error must stay
+    well inside the gate (emulated: p = 2048 0.35%, p = 4096 0.46%)."""
+    X = gen_grad(2048, 8192, seed=0)
+    want = O.newton_schulz(X.astype(np.float64))
+    assert _rel(gram_form(X), want) < 1e-2
