@@ -77,6 +77,39 @@ def test_volume_scales_with_alpha(world):
     assert t25 == expect
 
 
+@pytest.mark.parametrize("world", [1, 2, 8])
+def test_transposed_momentum_shards_leave_the_exchange_unchanged(world):
+    """ABI v4 dion2_shard.m_transposed is local to a rank: axis, owners and every byte count
+    of the exchange are identical with and without it."""
+    base = D.dist_info(SHAPES, world, 0, alpha=0.25)
+    mts = [ax == 1 for ax in base["axis"]]
+    assert any(mts)
+    for r in range(world):
+        a = D.dist_info(SHAPES, world, r, alpha=0.25)
+        b = D.dist_info(SHAPES, world, r, alpha=0.25, m_transposed=mts)
+        for key in ("axis", "owner", "shard", "send_bytes", "recv_bytes"):
+            assert a[key] == b[key], key
+        assert b["workspace_bytes"] > 0
+
+
+def test_transposed_momentum_shard_validation():
+    # rows-mode matrices cannot take a transposed momentum shard
+    with pytest.raises(D.Dion2Error) as e:
+        D.dist_info([(256, 512)], 2, 0, alpha=0.25, m_transposed=[True])
+    assert e.value.code == 4  # DION2_EUNSUPPORTED
+    arr = D._shards([(512, 256)], m_transposed=[True])
+    arr[0].reserved = 1
+    cfg = D.make_config(alpha=0.25)
+    import ctypes
+    n = 1
+    ax, own = (ctypes.c_int32 * n)(), (ctypes.c_int32 * n)()
+    sr, sc = (ctypes.c_int64 * n)(), (ctypes.c_int64 * n)()
+    sb, rb = (ctypes.c_int64 * 2)(), (ctypes.c_int64 * 2)()
+    ws = ctypes.c_size_t(0)
+    rc = D._lib().dion2_dist_info(arr, n, ctypes.byref(cfg), 2, 0, ax, own, sr, sc, sb, rb, ctypes.byref(ws))
+    assert rc == 2  # DION2_EINVAL_SHAPE: reserved must be 0
+
+
 def test_unsupported_layouts_are_rejected():
     with pytest.raises(D.Dion2Error):
         D.dist_info([(100, 300)], 3, 0, alpha=0.25)     # 300 / 3 = 100 columns: not a multiple of 8
