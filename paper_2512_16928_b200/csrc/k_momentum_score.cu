@@ -254,17 +254,33 @@ __device__ __forceinline__ void col_tile_mt_v4(const MatDesc& md, int rb, int cb
   const int64_t ib = (int64_t)rb * kColRB;
   const int64_t ie = md.rows < ib + kColRB ? md.rows : ib + kColRB;
   float acc[2] = {0.f, 0.f};  // |M| over the block's rows, M^T rows j0 + 8w + 4jg + g
+  // bf16 G with 16-B aligned rows: each thread loads 8 consecutive columns (8 c8 .. +7) of a
+  // row instead of two 4-column chunks 32 apart; the G tile column of slot u follows
+  const bool g16 = kBf16G && (reinterpret_cast<uintptr_t>(md.G) % 16 == 0) && (md.ld % 8 == 0);
+  auto gcol = [&](int u) { return g16 ? 8 * c8 + 4 * (u & 1) : 4 * (c8 + 8 * (u & 1)); };
   for (int64_t i0 = ib; i0 < ie; i0 += 64) {
     float4 gv[4], mv[4];
 #pragma unroll
-    for (int u = 0; u < 4; ++u) {  // G row i0 + 8w + 4(u>>1) + g, columns j0 + 4(c8 + 8(u&1)) .. +3
-      const int64_t i = i0 + 8 * w + 4 * (u >> 1) + g, j = j0 + 4 * (c8 + 8 * (u & 1));
-      if (i < ie && j + 3 < md.cols) {
+    for (int u = 0; u < 4; ++u) {  // G row i0 + 8w + 4(u>>1) + g, columns gcol(u) .. +3
+      const int64_t i = i0 + 8 * w + 4 * (u >> 1) + g, j = j0 + gcol(u);
+      if (kBf16G && g16 && (u & 1)) continue;  // loaded with its even partner below
+      if (kBf16G && g16 && i < ie && j + 7 < md.cols) {
+        // bf16 G: one 16-B load = 8 columns (both halves), 128 contiguous bytes per row per warp
+        const uint4 raw = __ldcs(reinterpret_cast<const uint4*>(reinterpret_cast<const __nv_bfloat16*>(md.G) +
+                                                                i * md.ld + j));
+        const __nv_bfloat162* h = reinterpret_cast<const __nv_bfloat162*>(&raw);
+        gv[u] = make_float4(__low2float(h[0]), __high2float(h[0]), __low2float(h[1]), __high2float(h[1]));
+        gv[u + 1] = make_float4(__low2float(h[2]), __high2float(h[2]), __low2float(h[3]), __high2float(h[3]));
+      } else if (!(kBf16G && g16) && i < ie && j + 3 < md.cols) {
         gv[u] = load_g4<kBf16G>(md, i, j);
       } else {
-        gv[u] = make_float4(0.f, 0.f, 0.f, 0.f);
-        for (int e = 0; e < 4; ++e)
-          if (i < ie && j + e < md.cols) (&gv[u].x)[e] = load_g<kBf16G>(md, i, j + e);
+        const int nh = (kBf16G && g16) ? 2 : 1;  // bf16 16-B path: this slot covers both halves
+        for (int hh = 0; hh < nh; ++hh) {
+          float4& t = gv[u + hh];
+          t = make_float4(0.f, 0.f, 0.f, 0.f);
+          for (int e = 0; e < 4; ++e)
+            if (i < ie && j + 4 * hh + e < md.cols) (&t.x)[e] = load_g<kBf16G>(md, i, j + 4 * hh + e);
+        }
       }
     }
 #pragma unroll
@@ -278,7 +294,7 @@ __device__ __forceinline__ void col_tile_mt_v4(const MatDesc& md, int rb, int cb
     }
 #pragma unroll
     for (int u = 0; u < 4; ++u) {
-      const int r = 8 * w + 4 * (u >> 1) + g, c = 4 * (c8 + 8 * (u & 1));
+      const int r = 8 * w + 4 * (u >> 1) + g, c = gcol(u);
       gs[r][c + 0] = gv[u].x;
       gs[r][c + 1] = gv[u].y;
       gs[r][c + 2] = gv[u].z;
