@@ -96,7 +96,7 @@ def work_model(shapes, alpha, steps=5, mt=False, ns_form="auto"):
             sfx = "_cols"
         else:
             sfx = ""
-        gsfx = "_rows" if (mt and sfx == "_cols") else sfx     # transposed M: row gather of M^T
+        gsfx = "_rows" if (mt and not rows) else sfx           # transposed M: row gather of M^T
         byts["gather" + gsfx] += k * o * (4.0 + 4.0 + 2.0)    # read M[K], write mu*M[K], write bf16 X
         byts["scatter" + sfx] += k * o * (2.0 + 4.0 + 4.0)    # read bf16 O, read+write W[K]
     return ns_flops, byts

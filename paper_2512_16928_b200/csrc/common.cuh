@@ -49,6 +49,8 @@ struct MatDesc {
   int32_t scores_final;    // select reads `scores` as final (distributed step: combined across ranks)
   int32_t mid;             // matrix id in the batch (random-selection key)
   int32_t mt;              // M stored transposed ([cols x ldm], cols mode only): K3 gathers rows of M^T
+  int32_t spath;           // scatter path when it differs from `path` (single-GPU plans: 2 = cols streaming
+                           // for k > kMaxColKFast); the generic K7 tiles skip matrices with spath != 0
   int64_t ldm;             // row stride of the transposed M
   int32_t rowblocks;      // ceil(rows / kColRowBlock) (cols mode partials)
 };

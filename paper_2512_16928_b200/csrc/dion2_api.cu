@@ -120,6 +120,7 @@ std::string plan_key(const dion2_matrix* mats, int n, const dion2_config* c, voi
     put(&mats[i].rows, 8);
     put(&mats[i].cols, 8);
     put(&mats[i].ld, 8);
+    put(&mats[i].m_transposed, 4);  // selects the gather / K1 paths and the sum-of-squares layout
   }
   put(&c->alpha, 4);
   put(&c->ns_steps, 4);
@@ -181,8 +182,11 @@ int build_layout(Plan& P, const dion2_matrix* mats, int n, const dion2_config* c
     q.mt = m.m_transposed ? 1 : 0;
     // transposed M: column mode with X = S^T (k <= rows), bf16; the gather is the row path on M^T
     if (q.mt && !(axis == DION2_AXIS_COLS && q.transposed && P.bf16_ns)) return DION2_EUNSUPPORTED;
-    q.ga = q.path == 0 ? (int)ceil_div(q.sa_pad, kTileA) : 0;
-    q.gb = q.path == 0 ? (int)ceil_div(q.sb_pad, kTileB) : 0;
+    // the cols streaming scatter takes larger k than the gather (8-row O tiles above k = 1024)
+    q.spath = (axis == DION2_AXIS_COLS && q.transposed && P.bf16_ns && q.k <= kMaxColKScatter) ? 2 : q.path;
+    const bool generic = (q.path == 0 && !q.mt) || q.spath == 0;  // a generic gather or scatter needs tiles
+    q.ga = generic ? (int)ceil_div(q.sa_pad, kTileA) : 0;
+    q.gb = generic ? (int)ceil_div(q.sb_pad, kTileB) : 0;
     q.n_sumsq = (q.path == 1 || q.mt) ? q.p_pad : (q.path == 0 ? q.ga * q.gb : q.q_pad / 32);
     auto key = std::make_pair(q.p_pad, q.q_pad);
     auto it = gidx.find(key);
@@ -484,9 +488,12 @@ int build_device_plan(Plan& P, const dion2_matrix* mats, const dion2_config* c, 
   int64_t mt_acc = 0;
   P.fl_gunits[0] = P.fl_gunits[1] = P.fl_sunits[0] = P.fl_sunits[1] = 0;
   P.fl_maxk = 0;
+  P.fl_smaxk = 0;
   P.fl_maxn = 0;
   int64_t rows_acc = 0, ctiles_acc = 0;
   int gt_acc = 0;
+  P.generic_gather_mats = 0;
+  P.generic_scatter_mats = 0;
   for (int i = 0; i < n; ++i) {
     const MatPlan& q = P.mp[i];
     const Group& g = P.groups[q.group];
@@ -516,15 +523,18 @@ int build_device_plan(Plan& P, const dion2_matrix* mats, const dion2_config* c, 
     d.rowblocks = q.rowblocks;
     d.mid = i;
     d.path = q.path;
+    d.spath = q.spath;
     d.n_sumsq = q.n_sumsq;
     d.mt = q.mt;
     d.ldm = q.mt ? mats[i].ldm : 0;
     gprefix[i] = gt_acc;
     gt_acc += q.ga * q.gb;
+    if (q.ga * q.gb > 0 && !q.mt && q.path == 0) P.generic_gather_mats++;  // transposed-M matrices: row gather
+    if (q.ga * q.gb > 0 && q.spath == 0) P.generic_scatter_mats++;
     // gather: rows streaming (path 1, or transposed-M columns = rows of M^T), cols streaming
     // (path 2) or generic tiles; scatter: by path (generic tiles for path 0)
     const int lg = (q.path == 1 || q.mt) ? 0 : (q.path == 2 ? 1 : -1);
-    const int ls = q.path - 1;
+    const int ls = q.spath - 1;
     if (lg >= 0) {
       flg_mats[lg].push_back(i);
       fl_gp[lg].push_back(P.fl_gunits[lg]);
@@ -535,10 +545,9 @@ int build_device_plan(Plan& P, const dion2_matrix* mats, const dion2_config* c, 
       fl_sp[ls].push_back(P.fl_sunits[ls]);
       P.fl_sunits[ls] += ls == 0 ? q.k : q.q_pad / 32;
     }
-    if (lg == 1 || ls == 1) {
-      P.fl_maxk = std::max(P.fl_maxk, q.k);
-      P.fl_maxn = std::max<int64_t>(P.fl_maxn, mats[i].cols);
-    }
+    if (lg == 1 || ls == 1) P.fl_maxn = std::max<int64_t>(P.fl_maxn, mats[i].cols);
+    if (lg == 1) P.fl_maxk = std::max(P.fl_maxk, q.k);
+    if (ls == 1) P.fl_smaxk = std::max(P.fl_smaxk, q.k);
     if (q.axis == DION2_AXIS_ROWS) {
       rowmats.push_back(i);
       rowprefix.push_back(rows_acc);
@@ -748,15 +757,17 @@ int run_ns(Plan& P, const dion2_config* c, Launcher& L, cudaStream_t s, bool do_
 int refresh_tables(Plan& P, const dion2_matrix* mats, const dion2_config* c, cudaStream_t s) {
   const int n = P.n;
   bool upload = false;
-  if ((int)P.last_ptrs.size() != 5 * n) {
-    P.last_ptrs.assign(5 * n, nullptr);
+  if ((int)P.last_ptrs.size() != 6 * n) {
+    P.last_ptrs.assign(6 * n, nullptr);
     upload = true;
   }
   MatDesc* D = reinterpret_cast<MatDesc*>(P.host_tables.data());
   for (int i = 0; i < n; ++i) {
-    const void* ptrs[5] = {mats[i].W, mats[i].M, mats[i].G, mats[i].sel_out, mats[i].O_out};
-    for (int j = 0; j < 5; ++j)
-      if (P.last_ptrs[5 * i + j] != ptrs[j]) { upload = true; P.last_ptrs[5 * i + j] = ptrs[j]; }
+    const void* ptrs[6] = {mats[i].W, mats[i].M, mats[i].G, mats[i].sel_out, mats[i].O_out,
+                           reinterpret_cast<const void*>((uintptr_t)(mats[i].m_transposed ? mats[i].ldm : 0))};
+    for (int j = 0; j < 6; ++j)
+      if (P.last_ptrs[6 * i + j] != ptrs[j]) { upload = true; P.last_ptrs[6 * i + j] = ptrs[j]; }
+    D[i].ldm = mats[i].m_transposed ? mats[i].ldm : 0;
     D[i].W = mats[i].W;
     D[i].M = mats[i].M;
     D[i].G = mats[i].G;
@@ -837,7 +848,7 @@ void stage_gather(Plan& P, const dion2_config* c, void* ws, Launcher& L, cudaStr
   const int n = P.n;
   const MatDesc* dmats = (const MatDesc*)tab(P, P.off_desc);
   int32_t* bad = (int32_t*)at(ws, P.off_bad);
-  if (P.total_gather_tiles > 0) {
+  if (P.total_gather_tiles > 0 && P.generic_gather_mats > 0) {
     L.begin(PH_GATHER);
     launch_gather_decay(P.bf16_ns, stream_grid(P.total_gather_tiles, 8, persistent), s, dmats,
                         (const int32_t*)tab(P, P.off_gprefix), n, P.total_gather_tiles, bad, 1, c->mu);
@@ -865,7 +876,7 @@ void stage_post(Plan& P, const dion2_matrix* mats, const dion2_config* c, void* 
   const int n = P.n;
   const MatDesc* dmats = (const MatDesc*)tab(P, P.off_desc);
   int32_t* bad = (int32_t*)at(ws, P.off_bad);
-  if (P.total_gather_tiles > 0) {
+  if (P.total_gather_tiles > 0 && P.generic_scatter_mats > 0) {
     L.begin(PH_SCATTER);
     launch_scatter_update(P.bf16_ns, stream_grid(P.total_gather_tiles, 8, persistent), s, dmats,
                           (const int32_t*)tab(P, P.off_gprefix), n, P.total_gather_tiles, bad, c->lr);
@@ -880,7 +891,7 @@ void stage_post(Plan& P, const dion2_matrix* mats, const dion2_config* c, void* 
   }
   if (P.fl_sn[1]) {
     L.begin(PH_SCATTER_COLS);
-    launch_scatter_cols_t(stream_grid(P.fl_sunits[1], 6, persistent), P.fl_maxk, P.fl_maxn, s, dmats,
+    launch_scatter_cols_t(stream_grid(P.fl_sunits[1], 6, persistent), P.fl_smaxk, P.fl_maxn, s, dmats,
                           (const int32_t*)tab(P, P.off_fls_mats[1]), (const int32_t*)tab(P, P.off_fl_sprefix[1]),
                           P.fl_sn[1], P.fl_sunits[1], bad, c->lr);
     L.end();

@@ -155,7 +155,7 @@ __global__ void __launch_bounds__(256) k_scatter_update(const MatDesc* __restric
   for (int t = blockIdx.x; t < total_tiles; t += gridDim.x) {
     const int mi = find_mat(tile_prefix_mats, n_mats, t);
     const MatDesc& md = mats[mi];
-    if (bad[mi]) continue;  // block-uniform
+    if (bad[mi] || md.spath != 0) continue;  // block-uniform; spath != 0: a streaming scatter owns it
     const int local = t - md.gather_tile_base;
     const int ta = local / md.gather_tiles_b, tb = local % md.gather_tiles_b;
     const int a0 = ta * kTileA, b0 = tb * kTileB;

@@ -467,7 +467,7 @@ void launch_scatter_cols_t(int blocks, int max_k, int64_t max_n, cudaStream_t s,
   const int mw = mask_words_for(max_n);
   // 8 whole-row float4 loads in flight per lane (measured on the 1B set's 24 up-projections:
   // 4 selected-only loads 0.669 ms, 8 unconditional 0.613 ms, 16 0.731 ms)
-  const int slab_h = max_k > 512 ? 16 : 32;
+  const int slab_h = max_k <= 512 ? 32 : (max_k <= 1024 ? 16 : 8);
   const size_t smem = 8 * (size_t)mw + (size_t)slab_h * (max_k + 8) * 2;
   k_scatter_cols_t<8, true><<<blocks, 256, smem, s>>>(mats, lm, lp, nl, units, bad, lr, mw, slab_h);
 }

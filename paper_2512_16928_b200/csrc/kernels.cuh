@@ -33,7 +33,8 @@ __global__ void k_norm_finalize(const MatDesc* __restrict__ mats, int n_mats, fl
 
 // streaming fast paths (k_gather_scatter_fast.cu): rows mode X = S, cols mode X = S^T
 #define DION2_MAX_SELECT_DIM_WORDS 1536  // DION2_MAX_SELECT_DIM / 32
-constexpr int kMaxColKFast = 1024;          // largest k of the cols streaming path (smem tile)
+constexpr int kMaxColKFast = 1024;          // largest k of the cols streaming gather (32-row smem tile)
+constexpr int kMaxColKScatter = 4096;       // largest k of the cols streaming scatter (8-row tile above 1024)
 size_t cols_t_smem_bytes(int k, int mask_words);
 void launch_fast_paths_attrs();
 void launch_gather_rows(int blocks, cudaStream_t s, const MatDesc* mats, const int32_t* lm, const int32_t* lp, int nl,

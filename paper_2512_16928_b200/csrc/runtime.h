@@ -46,7 +46,7 @@ int validate_shape(const dion2_matrix& m, bool need_ptrs);
 struct MatPlan {
   int mt;  // M stored transposed (cols mode): gather = rows path on M^T, scatter = path (cols / generic)
   int axis, d, o, k, sr, sc, transposed, p, q, p_pad, q_pad, group, zi, rowblocks, ga, gb, sa_pad, sb_pad, path,
-      n_sumsq;
+      n_sumsq, spath;  // spath: scatter path (the cols streaming scatter takes k up to kMaxColKScatter)
   float fan_sqrt;
   size_t off_scores, off_partials, off_sel, off_sumsq;
 };
@@ -78,13 +78,16 @@ struct Plan {
       off_nsscale, off_ns_begin, off_ns_end, total;
   size_t off_chain_entries = 0;  // Gram-space chain entry table (in the uploaded table region)
   int64_t total_rows = 0, total_col_tiles = 0;
+  int generic_gather_mats = 0;   // matrices the generic K3 tile kernel gathers (not transposed-M ones)
+  int generic_scatter_mats = 0;  // matrices the generic K7 tile kernel updates (spath == 0)
   int n_row_mats = 0, n_col_mats = 0, total_gather_tiles = 0, max_d = 0;
   // streaming fast paths: list 0 = rows (units: X rows p_pad / selected rows k),
   // list 1 = cols with X = S^T (units: 32-row slabs of X's columns, q_pad / 32)
   // gather and scatter memberships differ for transposed-M column matrices (rows gather
   // on M^T, column scatter on W)
   size_t off_flg_mats[2], off_fls_mats[2], off_fl_gprefix[2], off_fl_sprefix[2];
-  int fl_gn[2] = {0, 0}, fl_sn[2] = {0, 0}, fl_gunits[2] = {0, 0}, fl_sunits[2] = {0, 0}, fl_maxk = 0;
+  int fl_gn[2] = {0, 0}, fl_sn[2] = {0, 0}, fl_gunits[2] = {0, 0}, fl_sunits[2] = {0, 0}, fl_maxk = 0,
+      fl_smaxk = 0;  // largest k of the cols streaming gather / scatter lists
   // K1 for column matrices with transposed M
   size_t off_mtmats = 0, off_mtprefix = 0;
   int n_mt_mats = 0;
@@ -94,7 +97,7 @@ struct Plan {
   std::vector<Launch> ns_launches;
   void* ws = nullptr;
   uint64_t id = 0;
-  std::vector<const void*> last_ptrs;  // W, M, G, sel_out, O_out per matrix as last uploaded
+  std::vector<const void*> last_ptrs;  // W, M, G, sel_out, O_out, ldm per matrix as last uploaded
   void* dtab = nullptr;                // plan-owned device copy of host_tables
 };
 

@@ -167,6 +167,14 @@ def test_chunked_nonfinite_reports_global_index(monkeypatch):
     assert torch.equal(Ws[4], W0[4]) and not torch.equal(Ws[5], W0[5])
 
 
+@pytest.mark.parametrize("mt", [False, True])
+def test_column_scatter_large_k(mt):
+    """Column-mode scatter with 1024 < k <= 4096 (8-row staged O tiles; k = 1500, 2250, 2048
+    ragged): the streaming scatter, with a generic or a transposed-M row gather."""
+    _assert(run_parity([(4096, 2000), (6000, 3000), (8192, 2048)], 0.75, "auto", "bf16", steps=2,
+                       m_transposed=mt, row_scaled=True), BF16_TOL)
+
+
 def test_transposed_momentum_for_column_mode():
     """f4: M stored transposed for column-mode matrices (row gather of M^T, transpose-add K1)."""
     shapes = [(520, 300), (1000, 256), (8192, 2048), (300, 520)]
@@ -265,6 +273,27 @@ def test_bitwise_determinism():
             opt.step(Ws, Ms, [torch.from_numpy(gen_grad(m, n, 1, i, t)).cuda() for i, (m, n) in enumerate(shapes)])
         outs.append([w.clone() for w in Ws] + [mm.clone() for mm in Ms])
     for a, b in zip(*outs):
+        assert torch.equal(a, b)
+
+
+def test_plan_cache_distinguishes_the_momentum_layout():
+    """Same shapes, same config, same workspace: a step with transposed momentum after one with
+    M in W's layout must not reuse the first plan (bitwise equal to a fresh optimizer)."""
+    shapes = [(2048, 512), (1024, 256)]
+    def fresh():
+        W = [torch.from_numpy(gen_w0(m, n, 5, i)).cuda() for i, (m, n) in enumerate(shapes)]
+        G = [torch.from_numpy(gen_grad(m, n, 5, i)).cuda() for i, (m, n) in enumerate(shapes)]
+        Mt = [torch.zeros(n, m, device="cuda") for (m, n) in shapes]
+        return W, Mt, G
+    opt = Dion2(alpha=0.25)
+    W0, G0 = [torch.from_numpy(gen_w0(m, n, 6, i)).cuda() for i, (m, n) in enumerate(shapes)], None
+    opt.step(W0, [torch.zeros_like(w) for w in W0], [torch.ones_like(w) for w in W0])
+    Wa, Ma, Ga = fresh()
+    opt.step(Wa, Ma, Ga, m_transposed=[True, True])
+    Wb, Mb, Gb = fresh()
+    Dion2(alpha=0.25).step(Wb, Mb, Gb, m_transposed=[True, True])
+    torch.cuda.synchronize()
+    for a, b in zip(Wa + Ma, Wb + Mb):
         assert torch.equal(a, b)
 
 
