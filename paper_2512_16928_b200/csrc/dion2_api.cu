@@ -132,7 +132,14 @@ std::string plan_key(const dion2_matrix* mats, int n, const dion2_config* c, voi
   put(&c->decay_mode, 4);
   put(&c->scale_mode, 4);
   put(&c->ns_form, 4);
-  // kernel-variant switches read at plan build (tests and measurements flip them)
+  k += env_key();
+  return k;
+}
+
+// kernel-variant switches read at plan build (tests and measurements flip them): part of
+// every plan-cache key
+std::string env_key() {
+  std::string k;
   for (const char* v : {"DION2_NS_PAIR", "DION2_NS_SYM", "DION2_NS_CHAIN", "DION2_NS_SERPENTINE", "DION2_NS_UPPER"}) {
     const char* e = getenv(v);
     k.append(e ? e : "-");

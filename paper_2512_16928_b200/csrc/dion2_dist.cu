@@ -423,6 +423,8 @@ std::string dist_key(const dion2_shard* sh, int n, const dion2_config* c, int wo
   put(&c->grad_dtype, 4);
   put(&c->decay_mode, 4);
   put(&c->scale_mode, 4);
+  put(&c->ns_form, 4);  // shapes the owner's NS plan
+  k += env_key();
   return k;
 }
 
@@ -790,6 +792,7 @@ int dp_get_plan(DpPlan** out, const dion2_matrix* mats, int n, const dion2_confi
   put(&c->decay_mode, 4);
   put(&c->scale_mode, 4);
   put(&c->ns_form, 4);
+  key += env_key();
   auto it = g_dp_plans.find(key);
   if (it == g_dp_plans.end()) {
     auto D = std::make_unique<DpPlan>();
