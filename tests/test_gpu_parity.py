@@ -98,6 +98,7 @@ def test_gram_chain_kernel(coeffs, monkeypatch):
     [(3.4445, -4.7750, 2.0315)] * 2,                           # T = 2: no A update after t = 0
     [(1.5, -0.5, 0.0)] * 3,                                    # cubic Newton-Schulz (c = 0)
     [(3.4445, -4.7750, 2.0315)] * 4 + [(2.0, -1.5, 0.5)],      # per-iteration coefficients
+    [(1.5, -0.5, 0.0)] * 16,                                   # T = DION2_MAX_NS_STEPS (61 Gram products)
 ])
 @pytest.mark.parametrize("form", ["direct", "gram"])
 def test_ns_schedules(coeffs, form):
