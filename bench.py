@@ -56,11 +56,12 @@ def model_shapes(name: str, layers: int = 0):
 
 def ns_uses_gram_form(p, q, ns_form="auto"):
     """The library's choice (dion2_api.cu build_layout, reading R23): Gram space iff the
-    256-padded wide X has q >= 2p (AUTO)."""
+    256-padded wide X has q >= 2p or the unpadded one does (AUTO; per matrix here, per shape
+    group in the library, identical for the benchmark sets)."""
     if ns_form != "auto":
         return ns_form == "gram"
     pad = lambda v: (v + 255) // 256 * 256  # noqa: E731
-    return pad(q) >= 2 * pad(p)
+    return pad(q) >= 2 * pad(p) or q >= 2 * p
 
 
 def work_model(shapes, alpha, steps=5, mt=False, ns_form="auto"):

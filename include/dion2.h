@@ -70,7 +70,8 @@ typedef enum { DION2_DT_F32 = 0, DION2_DT_BF16 = 1 } dion2_dtype;
    GRAM:   the iteration carried out on p x p matrices: A_0 = X_0 X_0^T once, then
            C_t = a I + b A_t + c A_t^2, Q_{t+1} = C_t Q_t, A_{t+1} = C_t (C_t A_t) in fp16
            with fp32 accumulation, and X_T = Q_T X_0 once (bf16).  Fewer FLOPs when q >= 2p.
-   AUTO:   GRAM for a matrix whose wide X has q >= 2p, DIRECT otherwise. */
+   AUTO:   GRAM for a shape group whose padded X has q_pad >= 2 p_pad or whose every member has
+           q >= 2p, DIRECT otherwise. */
 typedef enum { DION2_NS_FORM_AUTO = 0, DION2_NS_FORM_DIRECT = 1, DION2_NS_FORM_GRAM = 2 } dion2_ns_form;
 
 /* One weight matrix and its optimizer state. */
