@@ -114,6 +114,13 @@ def test_gram_form_large_tile_grid():
     _assert(run_parity([(1100, 4400), (3000, 700)], 1.0, "auto", "bf16", steps=2, row_scaled=True), BF16_TOL)
 
 
+def test_auto_mixes_both_ns_forms_in_one_call():
+    """alpha = 0.8: (1024, 1024) keeps the direct form (p = 819, q = 1024: q < 2p padded or
+    not), the other three take the Gram form: one batched call runs both launch lists."""
+    _assert(run_parity([(600, 800), (512, 2048), (1024, 1024), (3000, 1000)], 0.8, "auto", "bf16", steps=2,
+                       row_scaled=True), BF16_TOL)
+
+
 def test_gram_form_forced_on_square_x():
     # q = p: AUTO would pick DIRECT; forcing GRAM must still be within the bf16 gate
     _assert(run_parity([(384, 384), (512, 768)], 1.0, "auto", "bf16", steps=2, ns_form="gram"), BF16_TOL)
