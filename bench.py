@@ -414,6 +414,20 @@ def run_ours(args):
             sweep["axis_ms_per_step"][ax] = time_steps(o_, Ws, Ms_w, Gs, 3, 1, None)
             del o_
             torch.cuda.empty_cache()
+        # the column-mode matrices (fan-out > fan-in) stored (in, out) as JAX / Flax kernels are
+        # (ABI v5 storage_transposed): every selection is then a contiguous row selection
+        sts = [m > n for (m, n) in shapes]
+        Wt, Mt, Gt, off = [], [], [], 0
+        for (m, n), st in zip(shapes, sts):
+            sh = (n, m) if st else (m, n)
+            Wt.append(bufs[0][off:off + m * n].view(*sh))
+            Mt.append(bufs[1][off:off + m * n].view(*sh))
+            Gt.append(bufs[2][off:off + m * n].view(*sh))
+            off += m * n
+        o_ = Dion2(alpha=args.alpha, axis="auto", precision="bf16", ns_form=args.ns_form, storage_transposed=sts)
+        sweep["row_selection_layout_ms_per_step"] = time_steps(o_, Wt, Mt, Gt, 3, 1, None)
+        del o_
+        torch.cuda.empty_cache()
         # the same step with bf16 gradients (mixed-precision training): K1 reads 10 B/param
         Gb = bufs[2].to(torch.bfloat16)
         Gbs, off = [], 0

@@ -43,7 +43,7 @@
 extern "C" {
 #endif
 
-#define DION2_ABI_VERSION 4
+#define DION2_ABI_VERSION 5
 #define DION2_MAX_NS_STEPS 16
 
 typedef enum {
@@ -89,8 +89,15 @@ typedef struct {
                            (element (i, j) of M at M[j*ldm + i]); only for matrices whose resolved
                            selection axis is COLS, where it turns the column gather of M[:, K] into a
                            contiguous row gather (DION2_EUNSUPPORTED otherwise) */
-  int32_t reserved;     /* must be 0 */
-  int64_t ldm;          /* row stride of the transposed M (>= rows); ignored when m_transposed = 0 */
+  int32_t storage_transposed; /* 0: W, M, G are stored [rows x ld] (PyTorch (out, in)).  1: they are stored
+                           TRANSPOSED, [cols x ld] row-major, ld >= rows (JAX / Flax (in, out) kernels):
+                           element (i, j) of the logical m x n matrix at W[j*ld + i].  rows / cols stay
+                           the LOGICAL fan-out / fan-in: the axis (with its square tie-break), k and the
+                           sqrt(fan-out/fan-in) scale follow them, while every kernel runs on the storage
+                           layout (a logical column selection becomes a contiguous row selection).
+                           sel_out holds logical indices; O_out is written in the storage orientation.
+                           m_transposed then means M in the logical layout ([rows x ldm]) */
+  int64_t ldm;          /* row stride of the transposed M (>= the storage rows); ignored when m_transposed = 0 */
 } dion2_matrix;
 
 /* Hyper-parameters of Alg. 1.  Fill with dion2_config_init() first. */

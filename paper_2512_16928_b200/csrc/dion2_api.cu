@@ -76,6 +76,13 @@ bool make_map(CUtensorMap* m, const void* base, int64_t cols, int64_t rows, int6
   return r == CUDA_SUCCESS;
 }
 
+std::vector<dion2_matrix> storage_view(const dion2_matrix* mats, int n) {
+  std::vector<dion2_matrix> v(mats, mats + n);
+  for (auto& m : v)
+    if (m.storage_transposed == 1) std::swap(m.rows, m.cols);
+  return v;
+}
+
 int validate_config(const dion2_config* c) {
   if (!c) return DION2_EINVAL_CONFIG;
   if (!(c->alpha > 0.f && c->alpha <= 1.f)) return DION2_EINVAL_CONFIG;
@@ -101,7 +108,8 @@ int validate_shape(const dion2_matrix& m, bool need_ptrs) {
   if (m.rows < 1 || m.cols < 1 || m.ld < m.cols) return DION2_EINVAL_SHAPE;
   if (m.rows > (1ll << 31) - 1 || m.cols > (1ll << 31) - 1) return DION2_EINVAL_SHAPE;
   if (need_ptrs && (!m.W || !m.M || !m.G)) return DION2_EINVAL_SHAPE;
-  if (m.reserved != 0 || (m.m_transposed != 0 && m.m_transposed != 1)) return DION2_EINVAL_SHAPE;
+  if ((m.storage_transposed != 0 && m.storage_transposed != 1) || (m.m_transposed != 0 && m.m_transposed != 1))
+    return DION2_EINVAL_SHAPE;
   if (m.m_transposed && m.ldm < m.rows) return DION2_EINVAL_SHAPE;
   return DION2_OK;
 }
@@ -121,6 +129,7 @@ std::string plan_key(const dion2_matrix* mats, int n, const dion2_config* c, voi
     put(&mats[i].cols, 8);
     put(&mats[i].ld, 8);
     put(&mats[i].m_transposed, 4);  // selects the gather / K1 paths and the sum-of-squares layout
+    put(&mats[i].storage_transposed, 4);
   }
   put(&c->alpha, 4);
   put(&c->ns_steps, 4);
@@ -159,8 +168,12 @@ int build_layout(Plan& P, const dion2_matrix* mats, int n, const dion2_config* c
   for (int i = 0; i < n; ++i) {
     const dion2_matrix& m = mats[i];
     MatPlan& q = P.mp[i];
+    // m is the storage view (storage_view()); the paper's rules apply to the LOGICAL matrix
     const int64_t rows = m.rows, cols = m.cols;
-    int axis = c->axis == DION2_AXIS_AUTO ? (rows <= cols ? DION2_AXIS_ROWS : DION2_AXIS_COLS) : c->axis;
+    const bool st = m.storage_transposed == 1;
+    const int64_t lrows = st ? cols : rows, lcols = st ? rows : cols;
+    int laxis = c->axis == DION2_AXIS_AUTO ? (lrows <= lcols ? DION2_AXIS_ROWS : DION2_AXIS_COLS) : c->axis;
+    int axis = st ? (laxis == DION2_AXIS_ROWS ? DION2_AXIS_COLS : DION2_AXIS_ROWS) : laxis;
     q.axis = axis;
     q.d = (int)(axis == DION2_AXIS_ROWS ? rows : cols);
     q.o = (int)(axis == DION2_AXIS_ROWS ? cols : rows);
@@ -175,8 +188,8 @@ int build_layout(Plan& P, const dion2_matrix* mats, int n, const dion2_config* c
     q.q = std::max(q.sr, q.sc);
     q.p_pad = (int)align_up(q.p, 256);  // 256-row CTA-pair tiles
     q.q_pad = (int)align_up(q.q, 256);
-    if (c->scale_mode == 0) q.fan_sqrt = (float)std::sqrt((double)rows / (double)cols);  // Alg. 1 l.6
-    else q.fan_sqrt = (float)std::sqrt((double)q.sr / (double)q.sc);
+    if (c->scale_mode == 0) q.fan_sqrt = (float)std::sqrt((double)lrows / (double)lcols);  // Alg. 1 l.6
+    else q.fan_sqrt = (float)(st ? std::sqrt((double)q.sc / (double)q.sr) : std::sqrt((double)q.sr / (double)q.sc));
     q.rowblocks = (int)ceil_div(rows, kColRowBlock);
     // gather tiles cover the padded extent of S (wide(S_pad) = X_pad) so K3 also
     // rewrites X's zero padding every step
@@ -1057,11 +1070,13 @@ int dion2_config_init(dion2_config* cfg) {
   return DION2_OK;
 }
 
-int dion2_workspace_size(const dion2_matrix* mats, int32_t n, const dion2_config* cfg, size_t* bytes_out) {
+int dion2_workspace_size(const dion2_matrix* user_mats, int32_t n, const dion2_config* cfg, size_t* bytes_out) {
   if (!bytes_out) return DION2_EINVAL_CONFIG;
   int rc = validate_config(cfg);
   if (rc) return rc;
-  if (n < 1 || !mats) return DION2_EINVAL_SHAPE;
+  if (n < 1 || !user_mats) return DION2_EINVAL_SHAPE;
+  const std::vector<dion2_matrix> sv = storage_view(user_mats, n);
+  const dion2_matrix* mats = sv.data();
   for (int i = 0; i < n; ++i)
     if ((rc = validate_shape(mats[i], false))) return rc;
   const int chunks = chunk_count(mats, n);
@@ -1079,11 +1094,13 @@ int dion2_workspace_size(const dion2_matrix* mats, int32_t n, const dion2_config
   return DION2_OK;
 }
 
-int dion2_step_batched(const dion2_matrix* mats, int32_t n, const dion2_config* cfg, void* workspace,
+int dion2_step_batched(const dion2_matrix* user_mats, int32_t n, const dion2_config* cfg, void* workspace,
                        size_t ws_bytes, void* stream) {
   int rc = validate_config(cfg);
   if (rc) return rc;
-  if (n < 1 || !mats) return DION2_EINVAL_SHAPE;
+  if (n < 1 || !user_mats) return DION2_EINVAL_SHAPE;
+  const std::vector<dion2_matrix> sv = storage_view(user_mats, n);
+  const dion2_matrix* mats = sv.data();
   for (int i = 0; i < n; ++i)
     if ((rc = validate_shape(mats[i], true))) return rc;
   if (!workspace) return DION2_EWORKSPACE;

@@ -782,6 +782,7 @@ int dp_get_plan(DpPlan** out, const dion2_matrix* mats, int n, const dion2_confi
     put(&mats[i].cols, 8);
     put(&mats[i].ld, 8);
     put(&mats[i].m_transposed, 4);
+    put(&mats[i].storage_transposed, 4);
   }
   put(&c->alpha, 4);
   put(&c->ns_steps, 4);
@@ -935,12 +936,14 @@ int dion2_step_batched_loopback(const dion2_shard* shards, int32_t n, const dion
 // ------------------------------------------------------------------ compressed DP-sync ABI
 extern "C" {
 
-int dion2_dpsync_workspace_size(const dion2_matrix* mats, int32_t n, const dion2_config* cfg, int32_t world,
+int dion2_dpsync_workspace_size(const dion2_matrix* user_mats, int32_t n, const dion2_config* cfg, int32_t world,
                                 size_t* bytes_out) {
   int rc = validate_config(cfg);
   if (rc) return rc;
   if (!bytes_out) return DION2_EINVAL_CONFIG;
-  if (n < 1 || !mats) return DION2_EINVAL_SHAPE;
+  if (n < 1 || !user_mats) return DION2_EINVAL_SHAPE;
+  const std::vector<dion2_matrix> sv = storage_view(user_mats, n);
+  const dion2_matrix* mats = sv.data();
   for (int i = 0; i < n; ++i)
     if ((rc = validate_shape(mats[i], false))) return rc;
   DpPlan D;
@@ -949,12 +952,14 @@ int dion2_dpsync_workspace_size(const dion2_matrix* mats, int32_t n, const dion2
   return DION2_OK;
 }
 
-int dion2_step_batched_dpsync(const dion2_matrix* mats, int32_t n, const dion2_config* cfg, void* workspace,
+int dion2_step_batched_dpsync(const dion2_matrix* user_mats, int32_t n, const dion2_config* cfg, void* workspace,
                               size_t ws_bytes, void* nccl_comm, int32_t world, int32_t rank, void* stream,
                               uint64_t* comm_bytes_out) {
   int rc = validate_config(cfg);
   if (rc) return rc;
-  if (n < 1 || !mats) return DION2_EINVAL_SHAPE;
+  if (n < 1 || !user_mats) return DION2_EINVAL_SHAPE;
+  const std::vector<dion2_matrix> sv = storage_view(user_mats, n);
+  const dion2_matrix* mats = sv.data();
   for (int i = 0; i < n; ++i)
     if ((rc = validate_shape(mats[i], true))) return rc;
   if (!workspace) return DION2_EWORKSPACE;
@@ -977,12 +982,14 @@ int dion2_step_batched_dpsync(const dion2_matrix* mats, int32_t n, const dion2_c
   return L.err;
 }
 
-int dion2_step_batched_dpsync_loopback(const dion2_matrix* mats, int32_t n, const dion2_config* cfg,
+int dion2_step_batched_dpsync_loopback(const dion2_matrix* user_mats, int32_t n, const dion2_config* cfg,
                                        void* const* workspaces, size_t ws_bytes, int32_t world, void* stream,
                                        uint64_t* comm_bytes_out) {
   int rc = validate_config(cfg);
   if (rc) return rc;
-  if (n < 1 || !mats || world < 1 || !workspaces) return DION2_EINVAL_SHAPE;
+  if (n < 1 || !user_mats || world < 1 || !workspaces) return DION2_EINVAL_SHAPE;
+  const std::vector<dion2_matrix> sv = storage_view(user_mats, n * world);
+  const dion2_matrix* mats = sv.data();
   for (int i = 0; i < n * world; ++i)
     if ((rc = validate_shape(mats[i], true))) return rc;
   std::lock_guard<std::mutex> lock(g_mu);

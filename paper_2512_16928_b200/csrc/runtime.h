@@ -41,6 +41,9 @@ inline int64_t ceil_div(int64_t a, int64_t b) { return (a + b - 1) / b; }
 bool make_map(CUtensorMap* m, const void* base, int64_t cols, int64_t rows, int64_t count, int box_cols, int box_rows,
               CUtensorMapSwizzle swz = CU_TENSOR_MAP_SWIZZLE_128B);
 int validate_config(const dion2_config* c);
+// The kernels' view of the caller's matrices: storage_transposed ones get their storage shape
+// (rows and cols swapped); build_layout recovers the logical shape for the axis, k and scale.
+std::vector<dion2_matrix> storage_view(const dion2_matrix* mats, int n);
 std::string env_key();
 int validate_shape(const dion2_matrix& m, bool need_ptrs);
 

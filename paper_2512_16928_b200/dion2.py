@@ -21,7 +21,7 @@ AXIS = {"rows": 0, "cols": 1, "auto": 2}
 PRECISION = {"bf16": 0, "fp32": 1}
 SELECT = {"l1": 0, "random": 1}
 NS_FORM = {"auto": 0, "direct": 1, "gram": 2}
-ABI_VERSION = 4  # include/dion2.h DION2_ABI_VERSION
+ABI_VERSION = 5  # include/dion2.h DION2_ABI_VERSION
 STATUS = {0: "OK", 1: "EINVAL_CONFIG", 2: "EINVAL_SHAPE", 3: "EWORKSPACE", 4: "EUNSUPPORTED",
           5: "ECUDA", 6: "ENCCL", 7: "ENONFINITE"}
 EXPORTED = ["dion2_config_init", "dion2_workspace_size", "dion2_step", "dion2_step_batched", "dion2_get_status",
@@ -35,7 +35,7 @@ class Dion2Matrix(ctypes.Structure):
     _fields_ = [("rows", ctypes.c_int64), ("cols", ctypes.c_int64), ("ld", ctypes.c_int64),
                 ("W", ctypes.c_void_p), ("M", ctypes.c_void_p), ("G", ctypes.c_void_p),
                 ("sel_out", ctypes.c_void_p), ("O_out", ctypes.c_void_p),
-                ("m_transposed", ctypes.c_int32), ("reserved", ctypes.c_int32), ("ldm", ctypes.c_int64)]
+                ("m_transposed", ctypes.c_int32), ("storage_transposed", ctypes.c_int32), ("ldm", ctypes.c_int64)]
 
 
 class Dion2Config(ctypes.Structure):
@@ -145,8 +145,12 @@ def _check_tensor(t: torch.Tensor, name: str, dtype: torch.dtype, like: Optional
 def describe(Ws: Sequence[torch.Tensor], Ms: Sequence[torch.Tensor], Gs: Sequence[torch.Tensor],
              sel_out: Optional[Sequence[Optional[torch.Tensor]]] = None,
              O_out: Optional[Sequence[Optional[torch.Tensor]]] = None,
-             m_transposed: Optional[Sequence[bool]] = None):
-    """m_transposed[i]: M[i] is stored transposed, shape (cols, rows) (column-mode matrices)."""
+             m_transposed: Optional[Sequence[bool]] = None,
+             storage_transposed: Optional[Sequence[bool]] = None):
+    """m_transposed[i]: M[i] is stored transposed relative to W[i] (column-mode matrices).
+    storage_transposed[i]: W[i], M[i], G[i] hold the logical m x n matrix transposed, i.e. the
+    tensors have shape (n, m) = (fan-in, fan-out) as JAX / Flax (in, out) kernels do; the
+    axis, k and the sqrt(fan-out / fan-in) scale follow the logical shape."""
     n = len(Ws)
     if not (len(Ms) == n and len(Gs) == n) or n == 0:
         raise ValueError("Ws, Ms, Gs must be non-empty and equally long")
@@ -155,6 +159,8 @@ def describe(Ws: Sequence[torch.Tensor], Ms: Sequence[torch.Tensor], Gs: Sequenc
     for i, (W, M, G) in enumerate(zip(Ws, Ms, Gs)):
         _check_tensor(W, "W", torch.float32)
         mt = bool(m_transposed[i]) if m_transposed is not None else False
+        stt = bool(storage_transposed[i]) if storage_transposed is not None else False
+        arr[i].storage_transposed = 1 if stt else 0
         if mt:
             _check_tensor(M, "M (transposed)", torch.float32)
             if tuple(M.shape) != (W.shape[1], W.shape[0]):
@@ -163,7 +169,9 @@ def describe(Ws: Sequence[torch.Tensor], Ms: Sequence[torch.Tensor], Gs: Sequenc
         else:
             _check_tensor(M, "M", torch.float32, W)
         _check_tensor(G, "G", gdt, W)
-        arr[i].rows, arr[i].cols, arr[i].ld = W.shape[0], W.shape[1], W.stride(0)
+        # rows / cols are the LOGICAL fan-out / fan-in (the tensor is (n, m) under storage_transposed)
+        arr[i].rows, arr[i].cols = (W.shape[1], W.shape[0]) if stt else (W.shape[0], W.shape[1])
+        arr[i].ld = W.stride(0)
         arr[i].W, arr[i].M, arr[i].G = W.data_ptr(), M.data_ptr(), G.data_ptr()
         s = sel_out[i] if sel_out is not None else None
         o = O_out[i] if O_out is not None else None
@@ -191,10 +199,12 @@ class Dion2:
     opt = Dion2(alpha=0.25); opt.step(Ws, Ms, Gs)   # all on one CUDA device
     """
 
-    def __init__(self, m_transposed=None, **cfg_kw):
-        """m_transposed: default per-matrix flags (M stored (cols, rows)) used by step()."""
+    def __init__(self, m_transposed=None, storage_transposed=None, **cfg_kw):
+        """m_transposed / storage_transposed: default per-matrix layout flags used by step()
+        (see describe())."""
         self.cfg_kw = dict(cfg_kw)
         self.m_transposed = m_transposed
+        self.storage_transposed = storage_transposed
         self._ws: Optional[torch.Tensor] = None
 
     def workspace(self, arr, n, cfg, device) -> torch.Tensor:
@@ -207,12 +217,14 @@ class Dion2:
         return self._ws
 
     def step(self, Ws, Ms, Gs, sel_out=None, O_out=None, stream: Optional[torch.cuda.Stream] = None,
-             m_transposed=None, **override):
+             m_transposed=None, storage_transposed=None, **override):
         kw = dict(self.cfg_kw)
         kw.update(override)
         if m_transposed is None:
             m_transposed = self.m_transposed
-        arr, gdt = describe(Ws, Ms, Gs, sel_out, O_out, m_transposed)
+        if storage_transposed is None:
+            storage_transposed = self.storage_transposed
+        arr, gdt = describe(Ws, Ms, Gs, sel_out, O_out, m_transposed, storage_transposed)
         kw.setdefault("grad_dtype", gdt)
         cfg = make_config(**kw)
         dev = Ws[0].device

@@ -56,8 +56,10 @@ def run_parity(shapes: Sequence[Tuple[int, int]], alpha: float, axis: str = "aut
                steps: int = 10, seed: int = 0, mu: float = 0.95, lr: float = 0.02, row_scaled: bool = False,
                decay_mode: int = 0, check_bitwise: bool = True, device: str = "cuda", select: str = "l1",
                sel_seed: int = 0, m_transposed: bool = False, grad_bf16: bool = False, ns_form: str = "auto",
-               ns_coeffs=None) -> ParityResult:
+               ns_coeffs=None, storage_transposed: bool = False) -> ParityResult:
     """m_transposed: store M transposed (cols x rows) for every column-mode matrix.
+    storage_transposed: W, M, G of every matrix live as (n, m) tensors (JAX / Flax (in, out)
+    layout, ABI v5); the comparisons use their logical (m, n) views.
     ns_form: "auto" | "direct" | "gram" (reading R23); ns_coeffs: per-iteration (a, b, c), T = len."""
     res = ParityResult()
     cfg_o = oracle_cfg(alpha, axis, mu, lr, decay_mode)
@@ -69,10 +71,16 @@ def run_parity(shapes: Sequence[Tuple[int, int]], alpha: float, axis: str = "aut
         cfg_o.ns_coeffs = list(ns_coeffs)
         ns_kw.update(ns_steps=len(ns_coeffs), ns_coeffs=ns_coeffs)
     W0 = [gen_w0(m, n, seed, i) for i, (m, n) in enumerate(shapes)]
-    Wg = [torch.from_numpy(w).to(device) for w in W0]
-    mts = [m_transposed and O.resolve_axis(m, n, cfg_o.axis) == O.AXIS_COLS for (m, n) in shapes]
-    Mg = [torch.zeros((n, m) if mt else (m, n), device=device) for (m, n), mt in zip(shapes, mts)]
-    Mv = lambda i: Mg[i].T if mts[i] else Mg[i]  # noqa: E731  (the m x n view of M)
+    stt = bool(storage_transposed)
+    lay = lambda a: a.T.contiguous() if stt else a  # noqa: E731  (logical m x n -> device storage)
+    Wg = [lay(torch.from_numpy(w).to(device)) for w in W0]
+    Wv = lambda i: Wg[i].T if stt else Wg[i]  # noqa: E731  (the m x n view of W)
+    # m_transposed applies to matrices whose STORAGE selection axis is columns (logical rows mode
+    # under storage_transposed); "transposed" is relative to W's storage, i.e. the logical layout then
+    mts = [m_transposed and ((O.resolve_axis(m, n, cfg_o.axis) == O.AXIS_COLS) != stt) for (m, n) in shapes]
+    Mg = [torch.zeros(((n, m) if mt else (m, n)) if not stt else ((m, n) if mt else (n, m)), device=device)
+          for (m, n), mt in zip(shapes, mts)]
+    Mv = lambda i: Mg[i] if (stt and mts[i]) else (Mg[i].T if (mts[i] or stt) else Mg[i])  # noqa: E731
     Wr = [w.astype(np.float64) for w in W0]
     Mr = [np.zeros((m, n)) for (m, n) in shapes]
     opt = Dion2(alpha=alpha, mu=mu, lr=lr, axis=axis, precision=precision, decay_mode=decay_mode, select=select,
@@ -86,17 +94,20 @@ def run_parity(shapes: Sequence[Tuple[int, int]], alpha: float, axis: str = "aut
         if grad_bf16:  # the oracle sees exactly the bf16 values the kernels read
             Gg = [torch.from_numpy(g).to(device).to(torch.bfloat16) for g in G]
             G = [g.float().cpu().numpy() for g in Gg]
+            Gg = [lay(g) for g in Gg]
         else:
-            Gg = [torch.from_numpy(g).to(device) for g in G]
+            Gg = [lay(torch.from_numpy(g).to(device)) for g in G]
         sel = [torch.empty(k, dtype=torch.int32, device=device) for k in ks]
         Oo = []
         for i, (m, n) in enumerate(shapes):
             ax = O.resolve_axis(m, n, cfg_o.axis)
-            Oo.append(torch.empty((ks[i], n) if ax == O.AXIS_ROWS else (m, ks[i]), device=device))
+            oshape = (ks[i], n) if ax == O.AXIS_ROWS else (m, ks[i])
+            Oo.append(torch.empty(oshape[::-1] if stt else oshape, device=device))  # storage orientation
         if check_bitwise:
-            Wb = [w.clone() for w in Wg]
+            Wb = [Wv(i).clone() for i in range(len(shapes))]
             Mb = [Mv(i).clone() for i in range(len(shapes))]
-        opt.step(Wg, Mg, Gg, sel_out=sel, O_out=Oo, step=t, m_transposed=mts)
+        opt.step(Wg, Mg, Gg, sel_out=sel, O_out=Oo, step=t, m_transposed=mts,
+                 storage_transposed=[stt] * len(shapes))
         cfg_o.step = t
         torch.cuda.synchronize()
         for i, (m, n) in enumerate(shapes):
@@ -115,13 +126,13 @@ def run_parity(shapes: Sequence[Tuple[int, int]], alpha: float, axis: str = "aut
             elif not np.array_equal(K, Kg):
                 res.index_mismatch += 1  # random rule: integer-exact, no tie allowance
             if t == steps - 1:
-                og = Oo[i].cpu().numpy().astype(np.float64)
+                og = (Oo[i].T if stt else Oo[i]).cpu().numpy().astype(np.float64)
                 res.O_rel.append(float(np.linalg.norm(og - Oref) / max(np.linalg.norm(Oref), 1e-300)))
             if check_bitwise:
                 # unselected rows/cols: W bit-identical, M == fp32(M_prev + G) bit-identical
                 unsel = np.ones(m if ax == O.AXIS_ROWS else n, bool)
                 unsel[Kg] = False
-                wb, wa = Wb[i].cpu().numpy(), Wg[i].cpu().numpy()
+                wb, wa = Wb[i].cpu().numpy(), Wv(i).cpu().numpy()
                 mb, ma = Mb[i].cpu().numpy(), Mv(i).cpu().numpy()
                 expect_m = (mb + G[i]).astype(np.float32)
                 if decay_mode == 0:
@@ -131,7 +142,7 @@ def run_parity(shapes: Sequence[Tuple[int, int]], alpha: float, axis: str = "aut
                     else:
                         res.unselected_w_bitwise &= bool(np.array_equal(wb[:, unsel], wa[:, unsel]))
                         res.unselected_m_bitwise &= bool(np.array_equal(expect_m[:, unsel], ma[:, unsel]))
-    _finish(res, shapes, Wg, [Mv(i) for i in range(len(shapes))], Wr, Mr, W0)
+    _finish(res, shapes, [Wv(i) for i in range(len(shapes))], [Mv(i) for i in range(len(shapes))], Wr, Mr, W0)
     return res
 
 

@@ -37,7 +37,7 @@ def test_exports_every_declared_symbol(lib):
 
 
 def test_abi_version(lib):
-    assert lib.dion2_abi_version() == 4
+    assert lib.dion2_abi_version() == 5
 
 
 def test_config_defaults(lib):
@@ -112,6 +112,26 @@ def test_select_rule_validation(lib):
     assert lib.dion2_workspace_size(_mats([(8, 8)]), 1, ctypes.byref(cfg), ctypes.byref(out)) == 0
     cfg.select = 2
     assert lib.dion2_workspace_size(_mats([(8, 8)]), 1, ctypes.byref(cfg), ctypes.byref(out)) == 1
+
+
+def test_storage_transposed_flag(lib):
+    """ABI v5 dion2_matrix.storage_transposed: rows / cols stay logical; a logical 8192 x 2048
+    (cols mode) stored transposed is processed as the 2048 x 8192 storage's row selection, so
+    it needs the rows-mode plan's workspace; invalid flag values are shape errors."""
+    cfg = D.make_config(alpha=0.25)
+    out = ctypes.c_size_t(0)
+    logical = _mats([(8192, 2048)])
+    logical[0].ld = 8192                     # storage is 2048 x 8192
+    logical[0].storage_transposed = 1
+    assert lib.dion2_workspace_size(logical, 1, ctypes.byref(cfg), ctypes.byref(out)) == 0
+    st_bytes = out.value
+    rows_mode = _mats([(2048, 8192)])
+    assert lib.dion2_workspace_size(rows_mode, 1, ctypes.byref(cfg), ctypes.byref(out)) == 0
+    assert st_bytes == out.value
+    logical[0].ld = 2048                     # < the storage's 8192 columns
+    assert lib.dion2_workspace_size(logical, 1, ctypes.byref(cfg), ctypes.byref(out)) == 2
+    logical[0].ld, logical[0].storage_transposed = 8192, 2
+    assert lib.dion2_workspace_size(logical, 1, ctypes.byref(cfg), ctypes.byref(out)) == 2
 
 
 def test_shape_validation(lib):

@@ -185,6 +185,17 @@ def test_column_scatter_large_k(mt):
                        m_transposed=mt, row_scaled=True), BF16_TOL)
 
 
+@pytest.mark.parametrize("precision,tol,mt", [("bf16", BF16_TOL, False), ("fp32", FP32_TOL, False),
+                                              ("bf16", BF16_TOL, True)])
+def test_storage_transposed_layout(precision, tol, mt):
+    """ABI v5: W, M, G stored (fan-in, fan-out) as JAX / Flax kernels are; axis (incl. the square
+    tie-break), k and scale follow the logical shape.  Wide, tall, square and ragged matrices;
+    with mt, the logical-layout momentum of the storage's column-mode matrices."""
+    shapes = [(2048, 512), (512, 2048), (384, 384), (300, 520), (1000, 256)]
+    _assert(run_parity(shapes, 0.25, "auto", precision, steps=3, row_scaled=True, storage_transposed=True,
+                       m_transposed=mt), tol)
+
+
 def test_transposed_momentum_for_column_mode():
     """f4: M stored transposed for column-mode matrices (row gather of M^T, transpose-add K1)."""
     shapes = [(520, 300), (1000, 256), (8192, 2048), (300, 520)]
