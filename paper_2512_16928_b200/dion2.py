@@ -419,12 +419,14 @@ class Dion2DpSync:
     """Compressed DP-sync (paper 3.2): each rank is a data-parallel replica with full W, M
     and its local G; only M[K] is all-reduced (averaged).  Requires select="random"."""
 
-    def __init__(self, group=None, loopback_world: int = 0, m_transposed=None, **cfg_kw):
+    def __init__(self, group=None, loopback_world: int = 0, m_transposed=None, storage_transposed=None, **cfg_kw):
         """m_transposed: per matrix, M stored transposed (column-mode matrices; every replica
-        must use the same flags: the all-reduced buffer holds S^T for those)."""
+        must use the same flags: the all-reduced buffer holds S^T for those).
+        storage_transposed: per matrix, W, M, G held (in, out) (see describe())."""
         cfg_kw.setdefault("select", "random")
         self.cfg_kw = dict(cfg_kw)
         self.m_transposed = m_transposed
+        self.storage_transposed = storage_transposed
         self.group = group
         self.loopback = loopback_world > 0
         if self.loopback:
@@ -447,7 +449,8 @@ class Dion2DpSync:
             n, P = len(Ws[0]), self.world
             cfg = self._cfg(Gs[0][0], override)
             parts = [describe(Ws[r], Ms[r], Gs[r], sel_out[r] if sel_out is not None else None,
-                              m_transposed=self.m_transposed)[0] for r in range(P)]
+                              m_transposed=self.m_transposed, storage_transposed=self.storage_transposed)[0]
+                     for r in range(P)]
             arr = (Dion2Matrix * (n * P))()
             for r in range(P):
                 for i in range(n):
@@ -456,7 +459,8 @@ class Dion2DpSync:
         else:
             n, P = len(Ws), self.world
             cfg = self._cfg(Gs[0], override)
-            arr, _ = describe(Ws, Ms, Gs, sel_out, m_transposed=self.m_transposed)
+            arr, _ = describe(Ws, Ms, Gs, sel_out, m_transposed=self.m_transposed,
+                              storage_transposed=self.storage_transposed)
             dev = Ws[0].device
         need = ctypes.c_size_t(0)
         rc = _lib().dion2_dpsync_workspace_size(arr, n, ctypes.byref(cfg), P, ctypes.byref(need))
