@@ -64,14 +64,16 @@ def ns_uses_gram_form(p, q, ns_form="auto"):
     return pad(q) >= 2 * pad(p) or q >= 2 * p
 
 
-def work_model(shapes, alpha, steps=5, mt=False, ns_form="auto"):
+def work_model(shapes, alpha, steps=5, mt=False, ns_form="auto", fused=None):
     """Algorithmic work per Dion2 step and per-phase algorithmic HBM bytes.
     NS FLOPs of the form the library evaluates (full products; symmetric tiles not credited):
       direct: T(4p^2 q + 2p^3)  -- gram 2p^2q, poly 2p^3, apply 2p^2q per iteration
       Gram space (R23): 4p^2 q + (4T - 3) 2p^3 (T >= 2) -- gram + apply once, T polys,
       3T - 3 products C.Q / C.A / C.(CA)."""
     ns_flops = {"ns_gram": 0.0, "ns_poly": 0.0, "ns_apply": 0.0, "ns_mul": 0.0}
-    byts = {"momentum_score": 0.0, "momentum_score_mt": 0.0}
+    if fused is None:  # the library default: separate launches (DION2_PRE_FUSE=1 opts in)
+        fused = os.environ.get("DION2_PRE_FUSE", "0") == "1"
+    byts = {"momentum_score": 0.0, "momentum_score_mt": 0.0, "pre_fused": 0.0}
     for ph in ("gather", "gather_rows", "gather_cols", "scatter", "scatter_rows", "scatter_cols"):
         byts[ph] = 0.0
     for (m, n) in shapes:
@@ -98,6 +100,12 @@ def work_model(shapes, alpha, steps=5, mt=False, ns_form="auto"):
         else:
             sfx = ""
         gsfx = "_rows" if (mt and not rows) else sfx           # transposed M: row gather of M^T
+        if fused and rows and sfx == "_rows" and d <= 8192:
+            # k_pre_fused_rows: K1 + select + gather of this matrix in one launch (same algorithmic bytes)
+            byts[k1] -= m * n * 12.0 + d * 4.0
+            byts["pre_fused"] += m * n * 12.0 + d * 4.0 + k * o * (4.0 + 4.0 + 2.0)
+            byts["scatter" + sfx] += k * o * (2.0 + 4.0 + 4.0)
+            continue
         byts["gather" + gsfx] += k * o * (4.0 + 4.0 + 2.0)    # read M[K], write mu*M[K], write bf16 X
         byts["scatter" + sfx] += k * o * (2.0 + 4.0 + 4.0)    # read bf16 O, read+write W[K]
     return ns_flops, byts
@@ -329,7 +337,9 @@ def run_ours(args):
     torch.cuda.empty_cache()
 
     peaks, peak_src = load_peaks()
-    ns_flops, byts = work_model(shapes, args.alpha, mt=not args.no_mt, ns_form=args.ns_form)
+    fused = (not use_dist and os.environ.get("DION2_PRE_FUSE", "0") == "1"
+             and os.environ.get("DION2_CHUNKS", "1") == "1")
+    ns_flops, byts = work_model(shapes, args.alpha, mt=not args.no_mt, ns_form=args.ns_form, fused=fused)
     if use_dist:  # this rank's share: 1/world of every streaming pass, NS of its owned matrices
         owned = [s for s, o in zip(shapes, info["owner"]) if o == rank]
         ns_flops = work_model(owned, args.alpha, ns_form=args.ns_form)[0] if owned else {k: 0.0 for k in ns_flops}

@@ -25,7 +25,7 @@ namespace dion2rt {
 const char* kPhaseNames[kNumPhases] = {"momentum_score", "select",       "gather",       "norm",
                                        "ns_gram",        "ns_poly",      "ns_apply",     "scatter",
                                        "full_decay",     "gather_rows",  "gather_cols",  "scatter_rows",
-                                       "scatter_cols",   "ns_mul",       "momentum_score_mt"};
+                                       "scatter_cols",   "ns_mul",       "momentum_score_mt", "pre_fused"};
 
 std::mutex g_mu;
 int g_sm_count = 0;
@@ -149,7 +149,8 @@ std::string plan_key(const dion2_matrix* mats, int n, const dion2_config* c, voi
 // every plan-cache key
 std::string env_key() {
   std::string k;
-  for (const char* v : {"DION2_NS_PAIR", "DION2_NS_SYM", "DION2_NS_CHAIN", "DION2_NS_SERPENTINE", "DION2_NS_UPPER"}) {
+  for (const char* v : {"DION2_NS_PAIR", "DION2_NS_SYM", "DION2_NS_CHAIN", "DION2_NS_SERPENTINE", "DION2_NS_UPPER",
+                        "DION2_PRE_FUSE", "DION2_FUSE_LAG_MB"}) {
     const char* e = getenv(v);
     k.append(e ? e : "-");
     k.push_back('|');
@@ -498,6 +499,69 @@ static int append_gram_space_launches(Plan& P, const dion2_config* c, void* ws, 
   return emit(PH_APPLY, es, 1.f, 0.f, 0.f, 1, 0, 0);
 }
 
+// Task table of the fused pre-stage (k_pre_fused.cu).  Ticket order: each fused matrix's
+// K1 row tasks, then its select; its gather tasks are handed out once DION2_FUSE_LAG_MB
+// (default 96) MB of later K1 traffic has been handed out, so the select has finished
+// when the gathers start while the matrix's selected rows of M are still L2-resident.
+int build_fuse_tables(Plan& P, const dion2_matrix* mats, const std::vector<char>& fused) {
+  const int n = P.n;
+  P.fuse_tasks = 0;
+  P.fuse_rest_n = 0;
+  P.fuse_max_d = 0;
+  P.fuse_host.clear();
+  int nf = 0;
+  for (int i = 0; i < n; ++i) nf += fused[i];
+  if (nf == 0) return DION2_OK;
+  const char* e = getenv("DION2_FUSE_LAG_MB");
+  const int64_t lag = (int64_t)(e ? atof(e) : 96.0) * (1 << 20);
+  std::vector<int4> tasks;
+  std::vector<int32_t> need(n, 0), rest;
+  std::vector<std::pair<int, int64_t>> pending;  // (matrix, K1 bytes handed out at its select)
+  size_t head = 0;
+  int64_t k1_bytes = 0;
+  auto emit_gathers = [&](int i) {
+    const int pp = P.mp[i].p_pad;
+    for (int r0 = 0; r0 < pp; r0 += 8) tasks.push_back(make_int4(2, i, r0, std::min(pp, r0 + 8)));
+  };
+  for (int i = 0; i < n; ++i) {
+    if (!fused[i]) {
+      rest.push_back(i);
+      continue;
+    }
+    const int64_t rows = mats[i].rows, cols = mats[i].cols;
+    const int rpt = 2;  // a row pair per task: the CTA streams both rows at once
+    for (int64_t r0 = 0; r0 < rows; r0 += rpt) {
+      const int64_t r1 = std::min<int64_t>(rows, r0 + rpt);
+      tasks.push_back(make_int4(0, i, (int)r0, (int)r1));
+      need[i]++;
+      k1_bytes += (r1 - r0) * cols * 12;
+      while (head < pending.size() && k1_bytes - pending[head].second >= lag) emit_gathers(pending[head++].first);
+    }
+    tasks.push_back(make_int4(1, i, 0, 0));
+    pending.push_back({i, k1_bytes});
+    P.fuse_max_d = std::max(P.fuse_max_d, P.mp[i].d);
+  }
+  while (head < pending.size()) emit_gathers(pending[head++].first);
+  P.fuse_tasks = (int)tasks.size();
+  P.fuse_rest_n = (int)rest.size();
+  size_t off = align_up(16 * tasks.size(), 256);
+  P.fuse_off_need = off;
+  off = align_up(off + 4 * (size_t)n, 256);
+  P.fuse_off_ctr = off;
+  off = align_up(off + 4 * (size_t)(1 + 2 * n), 256);
+  P.fuse_off_rest = off;
+  off = align_up(off + 4 * (size_t)std::max(1, n), 256);
+  P.fuse_host.assign(off, 0);
+  memcpy(P.fuse_host.data(), tasks.data(), 16 * tasks.size());
+  memcpy(P.fuse_host.data() + P.fuse_off_need, need.data(), 4 * (size_t)n);
+  if (!rest.empty()) memcpy(P.fuse_host.data() + P.fuse_off_rest, rest.data(), 4 * rest.size());
+  if (P.dfuse) cudaFree(P.dfuse);
+  P.dfuse = nullptr;
+  if (cudaMalloc(&P.dfuse, off) != cudaSuccess) return DION2_ECUDA;
+  P.last_ptrs.clear();  // forces the table upload (refresh_tables) before the first step
+  return DION2_OK;
+}
+
 // Fill host tables and NS launches for a concrete workspace.
 int build_device_plan(Plan& P, const dion2_matrix* mats, const dion2_config* c, void* ws) {
   P.ws = ws;
@@ -518,6 +582,13 @@ int build_device_plan(Plan& P, const dion2_matrix* mats, const dion2_config* c, 
   P.fl_maxn = 0;
   int64_t rows_acc = 0, ctiles_acc = 0;
   int gt_acc = 0;
+  // fused pre-stage membership: rows-mode matrices on the rows streaming gather
+  std::vector<char> fused(n, 0);
+  if (P.allow_fuse)
+    for (int i = 0; i < n; ++i) {
+      const MatPlan& q = P.mp[i];
+      fused[i] = q.axis == DION2_AXIS_ROWS && q.path == 1 && !q.mt && q.d <= kFuseMaxD;
+    }
   P.generic_gather_mats = 0;
   P.generic_scatter_mats = 0;
   for (int i = 0; i < n; ++i) {
@@ -561,7 +632,7 @@ int build_device_plan(Plan& P, const dion2_matrix* mats, const dion2_config* c, 
     // (path 2) or generic tiles; scatter: by path (generic tiles for path 0)
     const int lg = (q.path == 1 || q.mt) ? 0 : (q.path == 2 ? 1 : -1);
     const int ls = q.spath - 1;
-    if (lg >= 0) {
+    if (lg >= 0 && !fused[i]) {
       flg_mats[lg].push_back(i);
       fl_gp[lg].push_back(P.fl_gunits[lg]);
       P.fl_gunits[lg] += lg == 0 ? q.p_pad : q.q_pad / 32;
@@ -575,6 +646,7 @@ int build_device_plan(Plan& P, const dion2_matrix* mats, const dion2_config* c, 
     if (lg == 1) P.fl_maxk = std::max(P.fl_maxk, q.k);
     if (ls == 1) P.fl_smaxk = std::max(P.fl_smaxk, q.k);
     if (q.axis == DION2_AXIS_ROWS) {
+      if (fused[i]) continue;
       rowmats.push_back(i);
       rowprefix.push_back(rows_acc);
       rows_acc += mats[i].rows;
@@ -620,6 +692,7 @@ int build_device_plan(Plan& P, const dion2_matrix* mats, const dion2_config* c, 
     memcpy(H(P.off_colprefix), colprefix.data(), 8 * colprefix.size());
   }
   memcpy(H(P.off_gprefix), gprefix.data(), 4 * n);
+  if (int rc = build_fuse_tables(P, mats, fused)) return rc;
   for (auto& g : P.groups) memcpy(H(g.off_gmats), g.mats.data(), 4 * g.mats.size());
 
   // ---- Newton-Schulz launch list: per iteration t: gram, poly, apply; per phase the
@@ -808,6 +881,9 @@ int refresh_tables(Plan& P, const dion2_matrix* mats, const dion2_config* c, cud
   if (upload &&
       cudaMemcpyAsync(P.dtab, P.host_tables.data(), P.host_tables.size(), cudaMemcpyHostToDevice, s) != cudaSuccess)
     return DION2_ECUDA;
+  if (upload && P.fuse_tasks &&
+      cudaMemcpyAsync(P.dfuse, P.fuse_host.data(), P.fuse_host.size(), cudaMemcpyHostToDevice, s) != cudaSuccess)
+    return DION2_ECUDA;
   return DION2_OK;
 }
 
@@ -840,6 +916,22 @@ void stage_k1_select(Plan& P, const dion2_config* c, void* ws, int32_t* status, 
   const int n = P.n;
   const MatDesc* dmats = (const MatDesc*)tab(P, P.off_desc);
   int32_t* bad = (int32_t*)at(ws, P.off_bad);
+  if (P.fuse_tasks) {
+    // K1 + K2 + K3 of the rows-mode matrices in one launch (k_pre_fused.cu)
+    static const bool hint = !getenv("DION2_FUSE_NOHINT");
+    uint8_t* fb = static_cast<uint8_t*>(P.dfuse);
+    int32_t* ctr = reinterpret_cast<int32_t*>(fb + P.fuse_off_ctr);
+    const size_t smem = 4 * (size_t)P.fuse_max_d;
+    const int sms = g_sm_count > 0 ? g_sm_count : 148;
+    const int per_sm = std::max(1, pre_fused_blocks_per_sm(hint, smem));
+    L.begin(PH_PRE_FUSED);
+    if (cudaMemsetAsync(ctr, 0, 4 * (size_t)(1 + 2 * n), s) != cudaSuccess) L.err = DION2_ECUDA;
+    launch_pre_fused_rows(hint, std::min(per_sm * sms, P.fuse_tasks), smem, s, dmats,
+                          reinterpret_cast<const int4*>(fb), P.fuse_tasks, ctr,
+                          reinterpret_cast<const int32_t*>(fb + P.fuse_off_need), n, bad, status, c->mu,
+                          c->select == DION2_SELECT_RANDOM, c->seed, c->step);
+    L.end();
+  }
   if (P.n_row_mats) {
     L.begin(PH_K1);
     const int blocks = stream_grid(ceil_div(P.total_rows, 8), 8, persistent);
@@ -863,10 +955,15 @@ void stage_k1_select(Plan& P, const dion2_config* c, void* ws, int32_t* status, 
                                                     P.total_mt_tiles);
     L.end();
   }
-  L.begin(PH_SELECT);
-  k_topk_select<<<n, kSelectThreads, 4 * P.max_d, s>>>(dmats, bad, status, c->select == DION2_SELECT_RANDOM, c->seed,
-                                                       c->step);
-  L.end();
+  const int n_sel = P.fuse_tasks ? P.fuse_rest_n : n;
+  if (n_sel) {
+    L.begin(PH_SELECT);
+    const int32_t* list =
+        P.fuse_tasks ? reinterpret_cast<const int32_t*>(static_cast<uint8_t*>(P.dfuse) + P.fuse_off_rest) : nullptr;
+    k_topk_select<<<n_sel, kSelectThreads, 4 * P.max_d, s>>>(dmats, list, bad, status,
+                                                             c->select == DION2_SELECT_RANDOM, c->seed, c->step);
+    L.end();
+  }
 }
 
 // K3 gather + selective decay (Alg. 1 l.4-5)
@@ -1142,6 +1239,10 @@ int dion2_step_batched(const dion2_matrix* user_mats, int32_t n, const dion2_con
     rc = build_layout(*np, mats, n, cfg);
     if (rc) return rc;
     if (np->total - 4096 + slack > ws_bytes) return DION2_EWORKSPACE;
+    // run_step runs K1/K2 and K3 back to back, so the fused pre-stage may apply: opt-in
+    // (DION2_PRE_FUSE=1), measured slower than the separate launches
+    const char* fz = getenv("DION2_PRE_FUSE");
+    np->allow_fuse = fz && fz[0] == '1';
     rc = build_device_plan(*np, mats, cfg, ws);
     if (rc) return rc;
     np->id = g_next_plan_id++;

@@ -528,7 +528,7 @@ void phase_select(DistPlan& D, void* ws, const dion2_config* c, Launcher& L, cud
   launch_sum_rank_scores(s, (const float*)at(ws, D.off_scores_all), (float*)at(ws, D.off_scores), D.total_d, D.world);
   L.end();
   L.begin(PH_SELECT);
-  k_topk_select<<<D.n, kSelectThreads, 4 * D.max_d, s>>>(dm, (int32_t*)at(ws, D.off_bad),
+  k_topk_select<<<D.n, kSelectThreads, 4 * D.max_d, s>>>(dm, nullptr, (int32_t*)at(ws, D.off_bad),
                                                          (int32_t*)at(ws, D.off_status),
                                                          c->select == DION2_SELECT_RANDOM, c->seed, c->step);
   L.end();

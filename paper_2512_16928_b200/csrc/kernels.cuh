@@ -18,8 +18,19 @@ __global__ void k_momentum_score_cols_mt(const MatDesc* __restrict__ mats, const
 // ---------------- K2 top-k select (k_select.cu)
 constexpr int kSelectThreads = 1024;
 // random_sel = 1: Random rule with Philox keys (seed, step, md.mid); else the l1 rule
-__global__ void k_topk_select(const MatDesc* __restrict__ mats, int32_t* __restrict__ bad, int32_t* __restrict__ status,
+// list: [gridDim.x] matrix indices, or null = matrices 0 .. gridDim.x - 1
+__global__ void k_topk_select(const MatDesc* __restrict__ mats, const int32_t* __restrict__ list,
+                              int32_t* __restrict__ bad, int32_t* __restrict__ status,
                               int random_sel, uint64_t seed, uint64_t step);
+
+// ---------------- fused K1 + K2 + K3 of rows-mode matrices (k_pre_fused.cu)
+// tasks: int4 {type (0 K1 rows, 1 select, 2 gather X rows), matrix, u0, u1} in ticket order;
+// ctr: [1 + 2 n] zeroed before the launch (ticket, k1_done[n], sel_ready[n])
+void launch_pre_fused_rows(bool hint, int blocks, size_t smem, cudaStream_t s, const MatDesc* mats,
+                           const int4* tasks, int n_tasks, int32_t* ctr, const int32_t* k1_need, int n_mats,
+                           int32_t* bad, int32_t* status, float mu, int random_sel, uint64_t seed, uint64_t step);
+int pre_fused_blocks_per_sm(bool hint, size_t smem);
+constexpr int kFuseMaxD = 8192;  // largest selection length the fused kernel's select takes (32 KB keys)
 
 // ---------------- K3 gather + decay + sum of squares, norm finalize; K7 scatter (k_gather_scatter.cu)
 constexpr int kTileA = 32;   // S rows per gather/scatter tile

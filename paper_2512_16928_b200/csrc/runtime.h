@@ -15,11 +15,11 @@
 namespace dion2rt {
 using namespace dion2;
 
-constexpr int kNumPhases = 15;
+constexpr int kNumPhases = 16;
 extern const char* kPhaseNames[kNumPhases];
 enum Phase {
   PH_K1 = 0, PH_SELECT, PH_GATHER, PH_NORM, PH_GRAM, PH_POLY, PH_APPLY, PH_SCATTER, PH_FULLDECAY,
-  PH_GATHER_ROWS, PH_GATHER_COLS, PH_SCATTER_ROWS, PH_SCATTER_COLS, PH_NSMUL, PH_K1_MT
+  PH_GATHER_ROWS, PH_GATHER_COLS, PH_SCATTER_ROWS, PH_SCATTER_COLS, PH_NSMUL, PH_K1_MT, PH_PRE_FUSED
 };
 
 extern std::mutex g_mu;
@@ -97,6 +97,13 @@ struct Plan {
   int n_mt_mats = 0;
   int64_t total_mt_tiles = 0;
   int64_t fl_maxn = 0;
+  // fused pre-stage (k_pre_fused.cu: K1 + K2 + K3 of the rows-mode matrices in one launch);
+  // only plans whose caller runs stage_k1_select and stage_gather back to back enable it
+  bool allow_fuse = false;
+  int fuse_tasks = 0, fuse_rest_n = 0, fuse_max_d = 0;
+  size_t fuse_off_need = 0, fuse_off_ctr = 0, fuse_off_rest = 0;
+  std::vector<uint8_t> fuse_host;  // device image: int4 tasks, int32 k1_need[n], ctr[1 + 2n], rest[n]
+  void* dfuse = nullptr;
   std::vector<uint8_t> host_tables;  // [off_desc, off_ns_begin) image (descriptors + aux)
   std::vector<Launch> ns_launches;
   void* ws = nullptr;

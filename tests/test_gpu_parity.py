@@ -334,7 +334,9 @@ def test_bf16_gradient_input():
     assert np.linalg.norm(dgpu - dref) / np.linalg.norm(dref) <= BF16_TOL
 
 
-def test_phase_timing_and_launch_count():
+@pytest.mark.parametrize("fuse", ["0", "1"])
+def test_phase_timing_and_launch_count(fuse, monkeypatch):
+    monkeypatch.setenv("DION2_PRE_FUSE", fuse)
     Ws = [torch.from_numpy(gen_w0(256, 512)).cuda()]
     Ms = [torch.zeros_like(Ws[0])]
     set_phase_timing(True)
@@ -343,6 +345,48 @@ def test_phase_timing_and_launch_count():
         times = get_phase_times()
     finally:
         set_phase_timing(False)
-    assert last_launch_count() >= 7
-    for ph in ("momentum_score", "select", "gather_rows", "ns_gram", "ns_poly", "ns_apply", "scatter_rows"):
+    pre = ("momentum_score", "select", "gather_rows") if fuse == "0" else ("pre_fused",)
+    assert last_launch_count() >= 5 + len(pre)
+    for ph in pre + ("ns_gram", "ns_poly", "ns_apply", "scatter_rows"):
         assert times[ph][1] >= 1 and times[ph][0] > 0
+    if fuse == "1":
+        assert times["momentum_score"][1] == 0 and times["gather_rows"][1] == 0
+
+
+def _run_steps(shapes, steps, seed, **kw):
+    Ws = [torch.from_numpy(gen_w0(m, n, seed, i)).cuda() for i, (m, n) in enumerate(shapes)]
+    Ms = [torch.zeros_like(w) for w in Ws]
+    sels = [torch.empty(max(1, int(0.25 * (m if m <= n else n) + 0.5)), dtype=torch.int32, device="cuda")
+            for (m, n) in shapes]
+    opt = Dion2(alpha=0.25, **kw)
+    for t in range(steps):
+        Gs = [torch.from_numpy(gen_grad(m, n, seed, i, t, row_scaled=True)).cuda() for i, (m, n) in enumerate(shapes)]
+        opt.step(Ws, Ms, Gs, sel_out=sels)
+    torch.cuda.synchronize()
+    return [w.clone() for w in Ws] + [mm.clone() for mm in Ms] + [s.clone() for s in sels]
+
+
+@pytest.mark.parametrize("lag_mb", ["0", "1", "96", "100000"])
+def test_pre_fused_equals_separate_launches(lag_mb, monkeypatch):
+    """The fused K1 + K2 + K3 launch (k_pre_fused.cu) against the separate kernels: the l1
+    scores are summed in another fixed order, but on row-scaled inputs (no near-ties) the
+    selected sets, hence X, its norm, the NS and every W and M word, are identical.  The
+    gather lag spans 'gathers queued right behind the select' (0: CTAs wait on the select)
+    to 'all gathers after all K1 work'.  Mixed rows / transposed-M column / generic matrices,
+    ragged rows and an unaligned ld-free shape."""
+    shapes = [(2048, 2048), (512, 2048), (2048, 512), (300, 520), (7, 33), (1024, 4096), (256, 256), (130, 1030)]
+    monkeypatch.setenv("DION2_PRE_FUSE", "0")
+    ref = _run_steps(shapes, 3, 11)
+    monkeypatch.setenv("DION2_PRE_FUSE", "1")
+    monkeypatch.setenv("DION2_FUSE_LAG_MB", lag_mb)
+    got = _run_steps(shapes, 3, 11)
+    for i, (a, b) in enumerate(zip(ref, got)):
+        assert torch.equal(a, b), i
+
+
+def test_pre_fused_random_selection_and_bf16_grad(monkeypatch):
+    monkeypatch.setenv("DION2_PRE_FUSE", "1")
+    monkeypatch.setenv("DION2_FUSE_LAG_MB", "4")
+    _assert(run_parity([(1024, 2048), (512, 1536), (2048, 1024)], 0.25, "auto", "bf16", steps=3,
+                       select="random", sel_seed=77), BF16_TOL)
+    _assert(run_parity([(1024, 2048), (384, 640)], 0.25, "auto", "bf16", steps=2, grad_bf16=True), BF16_TOL)
