@@ -51,7 +51,14 @@ def model_shapes(name: str, layers: int = 0):
         return layer_set_1b(16)
     if name == "8b":
         return layer_set_8b(32)
+    if name == "stress":  # configs[4]: embedding-like and MLP stress shapes (run at alpha = 0.0625)
+        return [(4096, 32768), (28672, 8192)]
     raise ValueError(name)
+
+
+LAYER_MATS = {"1b": 6, "1b16": 6, "8b": 7, "stress": 2}  # matrices per layer (the oracle's sample unit)
+CONFIG_LABEL = {"1b": "configs[1]", "1b16": "configs[1], 16-layer variant (paper Table 1 depth)",
+                "8b": "configs[3] matrix set on one GPU", "stress": "configs[4] stress shapes on one GPU"}
 
 
 def ns_uses_gram_form(p, q, ns_form="auto"):
@@ -212,12 +219,12 @@ def time_steps(opt, Ws, Ms, Gs, steps, warmup, dist_barrier=None):
     return e0.elapsed_time(e1) / steps
 
 
-def cpu_oracle_baseline(shapes, alpha, budget_s=20.0):
+def cpu_oracle_baseline(shapes, alpha, budget_s=20.0, per_layer=6):
     """Time the fp64 oracle (as it stands) on a bounded sample of the workload:
-    whole layers (6 matrices each) until ~budget_s; scaled to ms per model step."""
+    whole layers (per_layer matrices each) until ~budget_s; scaled to ms per model step."""
     import oracle as O
     from synth import gen_grad, gen_w0
-    per_layer = 6
+    per_layer = min(per_layer, len(shapes))
     layers = len(shapes) // per_layer
     cfg = O.OracleConfig(alpha=alpha)
     t_used, done = 0.0, 0
@@ -471,7 +478,7 @@ def run_ours(args):
 
     cpu = None
     if rank == 0 and world == 1 and not args.no_cpu:
-        cpu = cpu_oracle_baseline(shapes, args.alpha, budget_s=args.cpu_budget)
+        cpu = cpu_oracle_baseline(shapes, args.alpha, budget_s=args.cpu_budget, per_layer=LAYER_MATS[args.config])
 
     if rank == 0:
         out = {
@@ -487,10 +494,11 @@ def run_ours(args):
             "vs_baseline": None,
             "dtype": "f32 state / bf16 X, fp16 Gram-space NS (fp32 accumulate)",
             "data": "synthetic (W0~N(0,1/n), G~N(0,1), M0=0; seeded device RNG)",
-            "config": {"workload": f"{args.config}-set Dion2 step (configs[1])", "matrices": len(shapes),
+            "config": {"workload": f"{args.config}-set Dion2 step ({CONFIG_LABEL[args.config]})",
+                       "matrices": len(shapes),
                        "params": n_params, "alpha": args.alpha, "axis": "auto", "ns_steps": 5, "ns_form": args.ns_form,
                        "momentum_layout": "column-mode matrices transposed" if not args.no_mt else "as W",
-                       "l2_flush": "not needed: 14.5 GB touched per step >> 126 MB L2",
+                       "l2_flush": f"not needed: {12 * n_params / 1e9:.1f} GB touched per step >> 126 MB L2",
                        "parallelism": "single GPU" if not use_dist else
                        f"owner-compute over {world} GPUs (NCCL; shards along the non-selection axis)"},
             "alpha1_ms_per_step": ms_a1,
@@ -534,8 +542,9 @@ def run_reference(args):
     import oracle as O
     from synth import gen_grad, gen_w0
     shapes = model_shapes(args.config)
-    layer = shapes[:6]
-    layers = len(shapes) // 6
+    per_layer = min(LAYER_MATS[args.config], len(shapes))
+    layer = shapes[:per_layer]
+    layers = len(shapes) // per_layer
     cfg = O.OracleConfig(alpha=args.alpha)
     data = [(gen_w0(m, n, 0, i).astype(np.float64), np.zeros((m, n)), gen_grad(m, n, 0, i, 0).astype(np.float64))
             for i, (m, n) in enumerate(layer)]
@@ -554,10 +563,10 @@ def run_reference(args):
            "value": ms, "unit": "ms/step", "n_gpus": world, "steps": args.steps, "warmup": args.warmup,
            "ms_per_step": ms, "higher_is_better": False, "scaling": "weak", "vs_baseline": None, "dtype": "f64",
            "data": "synthetic (W0~N(0,1/n), G~N(0,1), M0=0; seeded host RNG)",
-           "config": {"workload": f"{args.config}-set Dion2 step (configs[1])", "alpha": args.alpha, "axis": "auto",
+           "config": {"workload": f"{args.config}-set Dion2 step ({CONFIG_LABEL[args.config]})", "alpha": args.alpha, "axis": "auto",
                       "ns_steps": 5},
            "cpu_baseline": {"value": ms, "unit": "ms/step", "cores": cores, "kind": "oracle",
-                            "sample": f"1 of {layers} layers (6 matrices) per step, fp64 NumPy, scaled x{layers}"},
+                            "sample": f"1 of {layers} layers ({per_layer} matrices) per step, fp64 NumPy, scaled x{layers}"},
            "e2e": {"value": ms, "unit": "ms/step", "h2d_bytes_per_step": 0, "d2h_bytes_per_step": 0}}
     print(json.dumps(out))
 

@@ -90,6 +90,12 @@ __device__ __forceinline__ uint32_t philox_word0(uint32_t c0, uint32_t c1, uint3
   return c0;
 }
 
+// Programmatic dependent launch (the NS kernels are launched with the programmatic stream
+// serialization attribute): a kernel may start its prologue (barriers, TMEM, tensor-map
+// prefetch) while the previous launch drains, and waits here before touching global memory.
+__device__ __forceinline__ void pdl_wait() { asm volatile("griddepcontrol.wait;" ::: "memory"); }
+__device__ __forceinline__ void pdl_launch_dependents() { asm volatile("griddepcontrol.launch_dependents;" ::: "memory"); }
+
 __device__ __forceinline__ void set_status_bad(int32_t* status, int mat) {
   atomicOr(&status[0], 1);
   atomicMin(&status[1], mat);

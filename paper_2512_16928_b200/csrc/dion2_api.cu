@@ -150,7 +150,7 @@ std::string plan_key(const dion2_matrix* mats, int n, const dion2_config* c, voi
 std::string env_key() {
   std::string k;
   for (const char* v : {"DION2_NS_PAIR", "DION2_NS_SYM", "DION2_NS_CHAIN", "DION2_NS_SERPENTINE", "DION2_NS_UPPER",
-                        "DION2_PRE_FUSE", "DION2_FUSE_LAG_MB"}) {
+                        "DION2_PRE_FUSE", "DION2_FUSE_LAG_MB", "DION2_GRAM_SPLITK"}) {
     const char* e = getenv(v);
     k.append(e ? e : "-");
     k.push_back('|');
@@ -250,6 +250,8 @@ int build_layout(Plan& P, const dion2_matrix* mats, int n, const dion2_config* c
   }
   for (auto& g : P.groups) g.off_gmats = take(4 * (size_t)g.count);
   P.off_chain_entries = take(4 * (size_t)n);
+  P.off_cf_mats = take(4 * (size_t)n);
+  P.off_cf_prefix = take(8 * (size_t)n);
   P.off_nsscale = take(8 * (size_t)n);
   for (int i = 0; i < n; ++i) {
     MatPlan& q = P.mp[i];
@@ -280,6 +282,32 @@ int build_layout(Plan& P, const dion2_matrix* mats, int n, const dion2_config* c
       g.off_C = off;  off = align_up(off + ab, 4096);
       g.off_Q0 = off; off = align_up(off + ab, 4096);
       g.off_Q1 = off; off = align_up(off + ab, 4096);
+    }
+  }
+  // split-K for the gram launches (K = q_pad) when all their upper-triangle pair tiles
+  // together cover at most half of the CTA pairs (few, large matrices: configs[4]); each
+  // slice keeps >= 4 k-blocks.  The fp32 partials live after the NS buffers.
+  P.gram_splitk = 1;
+  P.off_splitk = 0;
+  const char* pe = getenv("DION2_NS_PAIR");
+  const char* se = getenv("DION2_GRAM_SPLITK");
+  if (P.bf16_ns && !(pe && strcmp(pe, "none") == 0) && !(se && atoi(se) == 1)) {
+    int64_t tt = 0;
+    int min_kb = 1 << 30;
+    for (auto& g : P.groups) {
+      const int T = g.p_pad / 256;
+      tt += (int64_t)g.count * T * (T + 1) / 2;
+      min_kb = std::min(min_kb, g.q_pad / 64);
+    }
+    const int pairs = (g_sm_count > 0 ? g_sm_count : 148) / 2;
+    if (tt > 0 && 2 * tt <= pairs) {
+      int S = (int)std::min<int64_t>((pairs + tt - 1) / tt, min_kb / 4);
+      if (se && atoi(se) > 1) S = std::min(atoi(se), min_kb);
+      if (S > 1) {
+        P.gram_splitk = S;
+        P.off_splitk = off;
+        off = align_up(off + (size_t)tt * S * 256 * 256 * 4, 4096);
+      }
     }
   }
   P.off_ns_end = off;
@@ -419,6 +447,10 @@ static int append_gram_space_launches(Plan& P, const dion2_config* c, void* ws, 
       // alternate the walk direction between consecutive p x p launches: a launch starts on the
       // matrices the previous one wrote last (still in L2)
       np.reverse = (!apply && serpentine) ? (int)(flip++ & 1) : 0;
+      if (phase == PH_GRAM && pair && np.sym && P.gram_splitk > 1) {  // partials sized for sym tiles
+        np.splitk = P.gram_splitk;
+        np.partial = (float*)at(ws, P.off_splitk);
+      }
       int tiles = 0;
       for (int j = 0; j < np.ngroups; ++j) {
         const Entry& e = es[s0 + j];
@@ -576,6 +608,9 @@ int build_device_plan(Plan& P, const dion2_matrix* mats, const dion2_config* c, 
   std::vector<int32_t> flg_mats[2], fls_mats[2], fl_gp[2], fl_sp[2], mtmats;
   std::vector<int64_t> mtprefix;
   int64_t mt_acc = 0;
+  std::vector<int32_t> cf_mats;
+  std::vector<int64_t> cf_prefix;
+  P.cf_total = 0;
   P.fl_gunits[0] = P.fl_gunits[1] = P.fl_sunits[0] = P.fl_sunits[1] = 0;
   P.fl_maxk = 0;
   P.fl_smaxk = 0;
@@ -618,6 +653,16 @@ int build_device_plan(Plan& P, const dion2_matrix* mats, const dion2_config* c, 
     d.sa_pad = q.sa_pad;
     d.sb_pad = q.sb_pad;
     d.rowblocks = q.rowblocks;
+    // cols mode on tall matrices (> 32 row blocks of partials, e.g. 28672 rows): the column
+    // sums are finalised by a grid-wide kernel before K2 (one K2 CTA summing 112 partials per
+    // column was latency-bound); shorter ones are summed by K2 itself (one launch fewer)
+    const bool cf = q.axis == DION2_AXIS_COLS && q.rowblocks > 32;
+    d.scores_final = cf ? 1 : 0;
+    if (cf) {
+      cf_mats.push_back(i);
+      cf_prefix.push_back(P.cf_total);
+      P.cf_total += mats[i].cols;
+    }
     d.mid = i;
     d.path = q.path;
     d.spath = q.spath;
@@ -692,6 +737,11 @@ int build_device_plan(Plan& P, const dion2_matrix* mats, const dion2_config* c, 
     memcpy(H(P.off_colprefix), colprefix.data(), 8 * colprefix.size());
   }
   memcpy(H(P.off_gprefix), gprefix.data(), 4 * n);
+  P.cf_n = (int)cf_mats.size();
+  if (P.cf_n) {
+    memcpy(H(P.off_cf_mats), cf_mats.data(), 4 * cf_mats.size());
+    memcpy(H(P.off_cf_prefix), cf_prefix.data(), 8 * cf_prefix.size());
+  }
   if (int rc = build_fuse_tables(P, mats, fused)) return rc;
   for (auto& g : P.groups) memcpy(H(g.off_gmats), g.mats.data(), 4 * g.mats.size());
 
@@ -736,6 +786,10 @@ int build_device_plan(Plan& P, const dion2_matrix* mats, const dion2_config* c, 
           np.diag = 0.f;
           np.sym = sym ? 1 : 0;
           if (ph == PH_GRAM) { np.cacc = 1.f; np.cC = 0.f; np.scale_sel = t == 0 ? 2 : 0; np.b_kmajor = 1; }
+          if (ph == PH_GRAM && pair && sym && P.gram_splitk > 1) {  // partials sized for sym tiles
+            np.splitk = P.gram_splitk;
+            np.partial = (float*)at(ws, P.off_splitk);
+          }
           if (ph == PH_POLY) { np.cacc = cc; np.cC = b; np.diag = a; np.scale_sel = 0; np.b_kmajor = 1; }
           if (ph == PH_APPLY) { np.cacc = 1.f; np.cC = 0.f; np.scale_sel = t == 0 ? 1 : 0; np.b_kmajor = 0; }
           int tiles = 0;
@@ -836,7 +890,9 @@ int run_ns(Plan& P, const dion2_config* c, Launcher& L, cudaStream_t s, bool do_
     if (ln.kind == 4) {
       launch_ns_chain(std::min(2 * ln.chain->n_entries, sms & ~1), s, *ln.chain);
     } else if (ln.kind == 3) {
-      launch_ns_pair(std::min(2 * ln.tc.p.total_tiles, sms & ~1), s, ln.tc);
+      const int sk = ln.tc.p.splitk > 1 ? ln.tc.p.splitk : 1;
+      launch_ns_pair(std::min(2 * ln.tc.p.total_tiles * sk, sms & ~1), s, ln.tc);
+      if (sk > 1) launch_splitk_reduce(s, ln.tc.p);
     } else if (ln.kind == 0 || ln.kind == 1) {
       launch_ns_tc(ln.bn, std::min(ln.tc.p.total_tiles, sms), s, ln.tc);
     } else {
@@ -956,6 +1012,12 @@ void stage_k1_select(Plan& P, const dion2_config* c, void* ws, int32_t* status, 
     L.end();
   }
   const int n_sel = P.fuse_tasks ? P.fuse_rest_n : n;
+  if (P.cf_n) {
+    L.begin(PH_SELECT);
+    k_col_scores_finalize<<<(unsigned)ceil_div(P.cf_total, 256), 256, 0, s>>>(
+        dmats, (const int32_t*)tab(P, P.off_cf_mats), (const int64_t*)tab(P, P.off_cf_prefix), P.cf_n, P.cf_total);
+    L.end();
+  }
   if (n_sel) {
     L.begin(PH_SELECT);
     const int32_t* list =

@@ -446,6 +446,7 @@ void launch_fast_paths_attrs() {
   const int mx = (int)cols_t_smem_bytes(kMaxColK, kMaskWords);
   cudaFuncSetAttribute(k_gather_cols_t, cudaFuncAttributeMaxDynamicSharedMemorySize, mx);
   cudaFuncSetAttribute(k_scatter_cols_t<8, true>, cudaFuncAttributeMaxDynamicSharedMemorySize, mx);
+  cudaFuncSetAttribute(k_scatter_cols_t<8, false>, cudaFuncAttributeMaxDynamicSharedMemorySize, mx);
 }
 
 void launch_gather_rows(int blocks, cudaStream_t s, const MatDesc* mats, const int32_t* lm, const int32_t* lp, int nl,
@@ -469,7 +470,13 @@ void launch_scatter_cols_t(int blocks, int max_k, int64_t max_n, cudaStream_t s,
   // 4 selected-only loads 0.669 ms, 8 unconditional 0.613 ms, 16 0.731 ms)
   const int slab_h = max_k <= 512 ? 32 : (max_k <= 1024 ? 16 : 8);
   const size_t smem = 8 * (size_t)mw + (size_t)slab_h * (max_k + 8) * 2;
-  k_scatter_cols_t<8, true><<<blocks, 256, smem, s>>>(mats, lm, lp, nl, units, bad, lr, mw, slab_h);
+  // whole-row loads pay off while a 16-B chunk of a row almost always holds a selected column
+  // (alpha = 0.25: 68% of chunks, 90% of sectors); below ~1/8 density (configs[4]'s
+  // alpha = 0.0625: 23% of chunks) only the chunks holding a selected column are loaded
+  if ((int64_t)max_k * 8 >= max_n)
+    k_scatter_cols_t<8, true><<<blocks, 256, smem, s>>>(mats, lm, lp, nl, units, bad, lr, mw, slab_h);
+  else
+    k_scatter_cols_t<8, false><<<blocks, 256, smem, s>>>(mats, lm, lp, nl, units, bad, lr, mw, slab_h);
 }
 
 }  // namespace dion2

@@ -92,6 +92,8 @@ __global__ void __launch_bounds__(192, 1) k_ns_gemm_tc(const __grid_constant__ N
   __syncthreads();
   tc_fence_after();
   const uint32_t tmem_base = *tmem_base_slot;
+  pdl_wait();               // the previous launch's outputs are complete and visible
+  pdl_launch_dependents();  // the next NS launch may begin its prologue on SMs we free
 
   if (warp == 0) {
     if (lane == 0) {
@@ -245,10 +247,22 @@ void ns_tc_set_attrs() {
 }
 
 void launch_ns_tc(int bn, int grid, cudaStream_t s, const NsTcParams& P) {
-  if (bn == 256)
-    k_ns_gemm_tc<256><<<grid, 192, ns_tc_smem_bytes<256>(), s>>>(P);
-  else
-    k_ns_gemm_tc<128><<<grid, 192, ns_tc_smem_bytes<128>(), s>>>(P);
+  cudaLaunchConfig_t cfg = {};
+  cudaLaunchAttribute at[1];
+  at[0].id = cudaLaunchAttributeProgrammaticStreamSerialization;
+  at[0].val.programmaticStreamSerializationAllowed = 1;
+  cfg.gridDim = dim3(grid);
+  cfg.blockDim = dim3(192);
+  cfg.stream = s;
+  cfg.attrs = at;
+  cfg.numAttrs = 1;
+  if (bn == 256) {
+    cfg.dynamicSmemBytes = ns_tc_smem_bytes<256>();
+    cudaLaunchKernelEx(&cfg, k_ns_gemm_tc<256>, P);
+  } else {
+    cfg.dynamicSmemBytes = ns_tc_smem_bytes<128>();
+    cudaLaunchKernelEx(&cfg, k_ns_gemm_tc<128>, P);
+  }
 }
 
 }  // namespace dion2

@@ -103,6 +103,8 @@ __global__ void __cluster_dims__(2, 1, 1) __launch_bounds__(kPairThreads, 1)
   uint8_t* stage_base = smem + S * kStage + 1024;
 
   const NsParams& p = P.p;
+  const int SK = p.splitk > 1 ? p.splitk : 1;
+  const int nwork = p.total_tiles * SK;
   const int warp = threadIdx.x >> 5, lane = threadIdx.x & 31;
   const uint32_t rank = cluster_ctarank();
   const int cid = (int)cluster_id_x(), ncl = (int)nclusters_x();
@@ -132,16 +134,20 @@ __global__ void __cluster_dims__(2, 1, 1) __launch_bounds__(kPairThreads, 1)
   cluster_sync();
   tc_fence_after();
   const uint32_t tmem_base = *tmem_base_slot;
+  pdl_wait();               // the previous launch's outputs are complete and visible
+  pdl_launch_dependents();  // the next NS launch may begin its prologue on SMs we free
 
   if (warp == 0) {
     if (lane == 0) {
       // ---------------- TMA producer (both CTAs)
       int stage = 0;
       uint32_t phase = 0;
-      for (int t = cid; t < p.total_tiles; t += ncl) {
+      for (int w = cid; w < nwork; w += ncl) {
+        const int t = w / SK, slice = w - (w / SK) * SK;
         const TileCoord c = decode_tile(p, t);
         const NsGroup& G = p.g[c.group];
-        for (int kb = 0; kb < G.k_blocks; ++kb) {
+        const int kb1 = (slice + 1) * G.k_blocks / SK;
+        for (int kb = slice * G.k_blocks / SK; kb < kb1; ++kb) {
           mbar_wait(&empty_bar[stage], phase ^ 1);
           uint8_t* sa = smem + stage * kStage;
           uint8_t* sb = sa + kAB;
@@ -182,7 +188,8 @@ __global__ void __cluster_dims__(2, 1, 1) __launch_bounds__(kPairThreads, 1)
       int stage = 0;
       uint32_t phase = 0;
       int it = 0;
-      for (int t = cid; t < p.total_tiles; t += ncl, ++it) {
+      for (int w = cid; w < nwork; w += ncl, ++it) {
+        const int t = w / SK, slice = w - (w / SK) * SK;
         const TileCoord c = decode_tile(p, t);
         const NsGroup& G = p.g[c.group];
         const int acc = it & 1;
@@ -190,7 +197,8 @@ __global__ void __cluster_dims__(2, 1, 1) __launch_bounds__(kPairThreads, 1)
         mbar_wait(&tempty_bar[acc], acc_phase ^ 1);
         tc_fence_after();
         const uint32_t tmem_d = tmem_base + acc * 256;
-        for (int kb = 0; kb < G.k_blocks; ++kb) {
+        const int kb0 = slice * G.k_blocks / SK, kb1 = (slice + 1) * G.k_blocks / SK;
+        for (int kb = kb0; kb < kb1; ++kb) {
           mbar_wait(&full_bar[stage], phase);
           tc_fence_after();
           const uint32_t a_addr = smem_u32(smem + stage * kStage);
@@ -201,7 +209,7 @@ __global__ void __cluster_dims__(2, 1, 1) __launch_bounds__(kPairThreads, 1)
               const uint64_t adesc = umma_desc_sw128(a_addr + k * 32, 16, 1024);
               const uint64_t bdesc = p.b_kmajor ? umma_desc_sw128(b_addr + k * 32, 16, 1024)
                                                 : umma_desc_sw128(b_addr + k * 2048, 64 * kBK * 2, 1024);
-              umma_bf16_ss_pair(tmem_d, adesc, bdesc, idesc0, (kb | k) != 0);
+              umma_bf16_ss_pair(tmem_d, adesc, bdesc, idesc0, (kb != kb0) || (k != 0));
             }
           } else {
             // transposed (MN-major) operands of this k-block, as loaded by the producer
@@ -214,7 +222,7 @@ __global__ void __cluster_dims__(2, 1, 1) __launch_bounds__(kPairThreads, 1)
                                         : umma_desc_sw128(a_addr + k * 32, 16, 1024);
               const uint64_t bdesc = bt ? umma_desc_sw128(b_addr + k * 2048, 64 * kBK * 2, 1024)
                                         : umma_desc_sw128(b_addr + k * 32, 16, 1024);
-              umma_bf16_ss_pair(tmem_d, adesc, bdesc, idesc, (kb | k) != 0);
+              umma_bf16_ss_pair(tmem_d, adesc, bdesc, idesc, (kb != kb0) || (k != 0));
             }
           }
           umma_commit_pair(&empty_bar[stage]);
@@ -234,11 +242,30 @@ __global__ void __cluster_dims__(2, 1, 1) __launch_bounds__(kPairThreads, 1)
                                        mapa_shared(smem_u32(&tempty_bar[1]), 0)};
     int sbuf = 0;
     int it = 0;
-    for (int t = cid; t < p.total_tiles; t += ncl, ++it) {
+    for (int w = cid; w < nwork; w += ncl, ++it) {
+      const int t = w / SK;
       const TileCoord c = decode_tile(p, t);
       const NsGroup& G = p.g[c.group];
       const int acc = it & 1;
       const uint32_t acc_phase = (it >> 1) & 1;
+      if (SK > 1) {
+        // split-K: raw fp32 partial of this slice (row row_in_tile, this warp's 128 columns)
+        mbar_wait(&tfull_bar[acc], acc_phase);
+        tc_fence_after();
+        float* dst = p.partial + ((int64_t)w * 256 + row_in_tile) * 256;
+#pragma unroll 1
+        for (int cc32 = c0; cc32 < c0 + 4; ++cc32) {
+          float v[32];
+          tmem_ld_32x32b_x32(tmem_base + acc * 256 + cc32 * 32 + ((uint32_t)(lg * 32) << 16), v);
+#pragma unroll
+          for (int q = 0; q < 8; ++q)
+            reinterpret_cast<float4*>(dst + cc32 * 32)[q] = make_float4(v[4 * q], v[4 * q + 1], v[4 * q + 2], v[4 * q + 3]);
+        }
+        tc_fence_before();
+        __syncwarp();
+        if (lane == 0) mbar_arrive_cluster(leader_tempty[acc]);
+        continue;
+      }
       float osc = 1.f;
       if (p.scale_sel) osc = p.ns_scale_all[2 * G.gmats[c.z] + (p.scale_sel - 1)];
       const float ca = p.cacc * osc, cc = p.cC * osc, dterm = p.diag * osc;
@@ -343,16 +370,67 @@ __global__ void __cluster_dims__(2, 1, 1) __launch_bounds__(kPairThreads, 1)
   }
 }
 
+// Split-K reduction: block = 4 rows x 256 columns of one output tile; thread = 4 columns.
+// Sums the slices in slice order (deterministic), applies the epilogue algebra of the pair
+// kernel (oscale * cacc * acc + diag; split-K launches carry no cin) and writes the 2-byte
+// output, plus the transposed copy of an off-diagonal symmetric tile unless no_mirror.
+__global__ void __launch_bounds__(256) k_splitk_reduce(const NsParams p) {
+  const int t = blockIdx.x >> 6;
+  const int r = ((blockIdx.x & 63) << 2) + (threadIdx.x >> 6);
+  const int c4 = (threadIdx.x & 63) << 2;
+  const int S = p.splitk;
+  const TileCoord c = decode_tile(p, t);
+  const NsGroup& G = p.g[c.group];
+  float4 a = make_float4(0.f, 0.f, 0.f, 0.f);
+  for (int sl = 0; sl < S; ++sl) {
+    const float4 v = *reinterpret_cast<const float4*>(p.partial + (((int64_t)t * S + sl) * 256 + r) * 256 + c4);
+    a.x += v.x; a.y += v.y; a.z += v.z; a.w += v.w;
+  }
+  float osc = 1.f;
+  if (p.scale_sel) osc = p.ns_scale_all[2 * G.gmats[c.z] + (p.scale_sel - 1)];
+  const float ca = p.cacc * osc, dterm = p.diag * osc;
+  const int64_t row = (int64_t)c.tm * 256 + r, col = (int64_t)c.tn * 256 + c4;
+  float o[4] = {ca * a.x, ca * a.y, ca * a.z, ca * a.w};
+#pragma unroll
+  for (int e = 0; e < 4; ++e)
+    if (row == col + e) o[e] += dterm;
+  uint16_t h[4];
+#pragma unroll
+  for (int e = 0; e < 4; ++e)
+    h[e] = p.out_f16 ? __half_as_ushort(__float2half_rn(o[e])) : __bfloat16_as_ushort(__float2bfloat16_rn(o[e]));
+  uint16_t* out = reinterpret_cast<uint16_t*>(G.out) + (int64_t)c.z * G.out_mstride;
+  *reinterpret_cast<uint2*>(out + row * G.out_ld + col) =
+      make_uint2((uint32_t)h[0] | ((uint32_t)h[1] << 16), (uint32_t)h[2] | ((uint32_t)h[3] << 16));
+  if (p.sym && !p.no_mirror && c.tm != c.tn) {
+#pragma unroll
+    for (int e = 0; e < 4; ++e) out[(col + e) * G.out_ld + row] = h[e];
+  }
+}
+
+void launch_splitk_reduce(cudaStream_t s, const NsParams& p) {
+  k_splitk_reduce<<<p.total_tiles * 64, 256, 0, s>>>(p);
+}
+
 void ns_pair_set_attrs() {
   cudaFuncSetAttribute(k_ns_gemm_tc_pair<false>, cudaFuncAttributeMaxDynamicSharedMemorySize, ns_pair_smem_bytes());
   cudaFuncSetAttribute(k_ns_gemm_tc_pair<true>, cudaFuncAttributeMaxDynamicSharedMemorySize, ns_pair_smem_bytes());
 }
 
 void launch_ns_pair(int grid, cudaStream_t s, const NsTcParams& P) {
+  cudaLaunchConfig_t cfg = {};
+  cudaLaunchAttribute at[1];
+  at[0].id = cudaLaunchAttributeProgrammaticStreamSerialization;
+  at[0].val.programmaticStreamSerializationAllowed = 1;
+  cfg.gridDim = dim3(grid);
+  cfg.blockDim = dim3(kPairThreads);
+  cfg.dynamicSmemBytes = ns_pair_smem_bytes();
+  cfg.stream = s;
+  cfg.attrs = at;
+  cfg.numAttrs = 1;
   if (P.p.sym_in)
-    k_ns_gemm_tc_pair<true><<<grid, kPairThreads, ns_pair_smem_bytes(), s>>>(P);
+    cudaLaunchKernelEx(&cfg, k_ns_gemm_tc_pair<true>, P);
   else
-    k_ns_gemm_tc_pair<false><<<grid, kPairThreads, ns_pair_smem_bytes(), s>>>(P);
+    cudaLaunchKernelEx(&cfg, k_ns_gemm_tc_pair<false>, P);
 }
 
 }  // namespace dion2

@@ -15,6 +15,12 @@ __global__ void k_momentum_score_cols_mt(const MatDesc* __restrict__ mats, const
                                          const int64_t* __restrict__ tile_prefix, int n_col_mats,
                                          int64_t total_tiles);
 
+// cols mode: scores[j] = sum of the K1 row-block partials of column j in row-block order
+// (the same order K2 used when it summed them itself: bit-identical), one thread per column
+// over all listed matrices (prefix: int64 column offsets); K2 then reads final scores
+__global__ void k_col_scores_finalize(const MatDesc* __restrict__ mats, const int32_t* __restrict__ list,
+                                      const int64_t* __restrict__ prefix, int n_list, int64_t total);
+
 // ---------------- K2 top-k select (k_select.cu)
 constexpr int kSelectThreads = 1024;
 // random_sel = 1: Random rule with Philox keys (seed, step, md.mid); else the l1 rule
@@ -111,6 +117,12 @@ struct NsParams {
   int sym_in;                // operands hold only their upper 256 x 256 tiles: a lower k-block is read
                              // transposed (MN-major) from the stored upper tile
   int no_mirror;             // sym output: do not write the mirrored lower tiles
+  // split-K (pair kernel, long-K gram launches that cannot fill the GPU): work item w =
+  // tile * splitk + slice runs k-blocks [slice KB / splitk, (slice + 1) KB / splitk) and
+  // stores raw fp32 accumulators to partial[w][256][256]; k_splitk_reduce sums the slices
+  // in order (deterministic) and applies the epilogue
+  int splitk;                // <= 1: off
+  float* partial;
 };
 
 // tcgen05 path (k_ns_tcgen05.cu): tensor maps for the TMA operand loads.
@@ -126,6 +138,7 @@ void ns_tc_set_attrs();
 void launch_ns_tc(int bn, int grid, cudaStream_t s, const NsTcParams& P);
 void ns_pair_set_attrs();
 void launch_ns_pair(int grid, cudaStream_t s, const NsTcParams& P);
+void launch_splitk_reduce(cudaStream_t s, const NsParams& p);  // after a split-K pair launch
 // Gram-space chain (k_ns_chain_pair.cu, reading R23): one CTA pair runs every p x p product
 // of one matrix in sequence (ops), on the five fp16/bf16 p x p buffers of its shape group.
 constexpr int kChainBufs = 5;  // 0 A, 1 C, 2 Q0, 3 Q1, 4 B

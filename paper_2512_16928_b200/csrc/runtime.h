@@ -81,6 +81,9 @@ struct Plan {
   size_t off_status, off_bad, off_desc, off_rowmats, off_rowprefix, off_colmats, off_colprefix, off_gprefix,
       off_nsscale, off_ns_begin, off_ns_end, total;
   size_t off_chain_entries = 0;  // Gram-space chain entry table (in the uploaded table region)
+  size_t off_cf_mats = 0, off_cf_prefix = 0;  // cols-mode matrices whose scores k_col_scores_finalize sums
+  int cf_n = 0;
+  int64_t cf_total = 0;
   int64_t total_rows = 0, total_col_tiles = 0;
   int generic_gather_mats = 0;   // matrices the generic K3 tile kernel gathers (not transposed-M ones)
   int generic_scatter_mats = 0;  // matrices the generic K7 tile kernel updates (spath == 0)
@@ -100,6 +103,9 @@ struct Plan {
   // fused pre-stage (k_pre_fused.cu: K1 + K2 + K3 of the rows-mode matrices in one launch);
   // only plans whose caller runs stage_k1_select and stage_gather back to back enable it
   bool allow_fuse = false;
+  // split-K of the long-K gram launches when their tiles cannot fill the GPU (bf16 pair path)
+  int gram_splitk = 1;
+  size_t off_splitk = 0;
   int fuse_tasks = 0, fuse_rest_n = 0, fuse_max_d = 0;
   size_t fuse_off_need = 0, fuse_off_ctr = 0, fuse_off_rest = 0;
   std::vector<uint8_t> fuse_host;  // device image: int4 tasks, int32 k1_need[n], ctr[1 + 2n], rest[n]

@@ -100,9 +100,17 @@ __device__ __forceinline__ void select_matrix(const MatDesc& md, int mi, uint32_
     const int shift = 24 - 8 * pass;
     for (int i = tid; i < 256; i += blockDim.x) hist[i] = 0;
     __syncthreads();
-    for (int i = tid; i < d; i += blockDim.x) {
-      const uint32_t key = keys[i];
-      if ((key & mask) == prefix) atomicAdd(&hist[(key >> shift) & 255u], 1u);
+    // warp-aggregated: lanes sharing a bin add once (scores of similar magnitude share
+    // their top bits, so unaggregated shared atomics serialise on one bin)
+    for (int base = 0; base < d; base += blockDim.x) {
+      const int i = base + tid;
+      uint32_t bin = 256u;  // 256: not counted
+      if (i < d) {
+        const uint32_t key = keys[i];
+        if ((key & mask) == prefix) bin = (key >> shift) & 255u;
+      }
+      const unsigned peers = __match_any_sync(0xffffffffu, bin);
+      if (bin < 256u && (threadIdx.x & 31) == __ffs(peers) - 1) atomicAdd(&hist[bin], (uint32_t)__popc(peers));
     }
     __syncthreads();
     if (tid < 32) {

@@ -126,6 +126,18 @@ def test_gram_form_forced_on_square_x():
     _assert(run_parity([(384, 384), (512, 768)], 1.0, "auto", "bf16", steps=2, ns_form="gram"), BF16_TOL)
 
 
+@pytest.mark.parametrize("form", ["auto", "direct"])
+@pytest.mark.parametrize("splitk", [None, "1", "3"])
+def test_gram_split_k(form, splitk, monkeypatch):
+    """Few long-K matrices (configs[4]-like): the gram launch splits K across CTA pairs (fp32
+    partials, slices summed in order by k_splitk_reduce).  None: the library's choice (5 sym
+    tiles -> 15 slices); "1": off; "3": forced.  Ragged q (9000), p_pad 256 and 512."""
+    if splitk:
+        monkeypatch.setenv("DION2_GRAM_SPLITK", splitk)
+    _assert(run_parity([(512, 8192), (300, 9000), (2048, 4096)], 0.25, "auto", "bf16", steps=2, ns_form=form,
+                       row_scaled=True), BF16_TOL)
+
+
 def test_alpha1_is_full_muon_fp32():
     _assert(run_parity([(128, 384)], 1.0, "auto", "fp32", steps=5), FP32_TOL)
 
