@@ -1014,7 +1014,7 @@ void stage_k1_select(Plan& P, const dion2_config* c, void* ws, int32_t* status, 
   const int n_sel = P.fuse_tasks ? P.fuse_rest_n : n;
   if (P.cf_n) {
     L.begin(PH_SELECT);
-    k_col_scores_finalize<<<(unsigned)ceil_div(P.cf_total, 256), 256, 0, s>>>(
+    k_col_scores_finalize<<<(unsigned)ceil_div(P.cf_total, 32), 256, 0, s>>>(
         dmats, (const int32_t*)tab(P, P.off_cf_mats), (const int64_t*)tab(P, P.off_cf_prefix), P.cf_n, P.cf_total);
     L.end();
   }

@@ -15,8 +15,8 @@ __global__ void k_momentum_score_cols_mt(const MatDesc* __restrict__ mats, const
                                          const int64_t* __restrict__ tile_prefix, int n_col_mats,
                                          int64_t total_tiles);
 
-// cols mode: scores[j] = sum of the K1 row-block partials of column j in row-block order
-// (the same order K2 used when it summed them itself: bit-identical), one thread per column
+// cols mode on tall matrices: scores[j] = sum of the K1 row-block partials of column j in a
+// fixed order (8 strided row-block groups, then the groups in order), 32 columns per block
 // over all listed matrices (prefix: int64 column offsets); K2 then reads final scores
 __global__ void k_col_scores_finalize(const MatDesc* __restrict__ mats, const int32_t* __restrict__ list,
                                       const int64_t* __restrict__ prefix, int n_list, int64_t total);

@@ -63,6 +63,7 @@ __device__ __forceinline__ void select_matrix(const MatDesc& md, int mi, uint32_
 
   // 1. scores -> keys (cols mode: fixed-order sum of the K1 row-block partials)
   int nonfinite = 0;
+#pragma unroll 4
   for (int i = tid; i < d; i += blockDim.x) {
     float s;
     if (md.axis == kAxisCols && !md.scores_final) {

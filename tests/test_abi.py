@@ -88,6 +88,30 @@ def _size(lib, shapes, **kw):
     return rc, out.value
 
 
+def test_gram_split_k_workspace(lib, monkeypatch):
+    """Split-K gram (few long-K matrices: configs[4]): the plan reserves fp32 partials of
+    tiles x slices x 256 x 256 only when the gram's upper-triangle pair tiles cover at most
+    half of the 74 CTA pairs; slices = min(ceil(74 / tiles), k_blocks / 4)."""
+    stress = [(4096, 32768), (28672, 8192)]      # alpha 1/16: (256, 32768) 1 tile + (512, 28672) 3 tiles
+    monkeypatch.setenv("DION2_GRAM_SPLITK", "1")
+    _, off = _size(lib, stress, alpha=0.0625)
+    monkeypatch.delenv("DION2_GRAM_SPLITK")
+    _, on = _size(lib, stress, alpha=0.0625)
+    assert on - off >= 4 * 19 * 256 * 256 * 4 and on - off < 4 * 19 * 256 * 256 * 4 + 8192
+    # the 1B set fills the GPU (432 tiles): no partials
+    one_b = [(2048, 2048)] * 4 + [(8192, 2048), (2048, 8192)]
+    monkeypatch.setenv("DION2_GRAM_SPLITK", "1")
+    _, off1 = _size(lib, one_b * 24)
+    monkeypatch.delenv("DION2_GRAM_SPLITK")
+    _, on1 = _size(lib, one_b * 24)
+    assert on1 == off1
+    # fp32 validation path (SIMT NS): never split
+    _, f32a = _size(lib, stress, alpha=0.0625, precision="fp32")
+    monkeypatch.setenv("DION2_GRAM_SPLITK", "1")
+    _, f32b = _size(lib, stress, alpha=0.0625, precision="fp32")
+    assert f32a == f32b
+
+
 def test_workspace_size_scales_with_alpha(lib):
     shapes = [(2048, 2048), (8192, 2048), (2048, 8192)]
     rc1, b1 = _size(lib, shapes, alpha=1.0)
