@@ -1003,7 +1003,29 @@ void stage_k1_select(Plan& P, const dion2_config* c, void* ws, int32_t* status, 
                                                  P.total_col_tiles);
     L.end();
   }
-  if (P.n_mt_mats) {
+  // transposed-M K1: the cp.async-pipelined kernel when every listed matrix has fp32 G and
+  // aligned whole 256 x 64 units (DION2_K1MT_PIPE=0: the register-staged kernel; =2/3/4/6:
+  // stages; 3 = two 96 KB CTAs per SM measured best: 0.93 -> 0.76 ms on the 1B set)
+  bool mt_pipe = P.n_mt_mats > 0 && c->grad_dtype == DION2_DT_F32;
+  static const char* pe = getenv("DION2_K1MT_PIPE");
+  static const int pipe_stages = pe ? atoi(pe) : 3;
+  if (pipe_stages == 0) mt_pipe = false;
+  if (mt_pipe) {
+    const MatDesc* hd = reinterpret_cast<const MatDesc*>(P.host_tables.data());
+    for (int i = 0; i < n && mt_pipe; ++i)
+      if (hd[i].mt && hd[i].axis == kAxisCols)
+        mt_pipe = hd[i].vec4 && hd[i].rows % kColRowBlock == 0 && hd[i].cols % 64 == 0 && hd[i].ldm % 4 == 0;
+  }
+  if (P.n_mt_mats && mt_pipe) {
+    static int per_sm = -1;
+    if (per_sm < 0) per_sm = std::max(1, momentum_score_cols_mt_pipe_attrs(pipe_stages));
+    const int sms = g_sm_count > 0 ? g_sm_count : 148;
+    L.begin(PH_K1_MT);
+    launch_momentum_score_cols_mt_pipe(pipe_stages, (int)std::min<int64_t>(P.total_mt_tiles, (int64_t)per_sm * sms), s,
+                                       dmats, (const int32_t*)tab(P, P.off_mtmats), (const int64_t*)tab(P, P.off_mtprefix),
+                                       P.n_mt_mats, P.total_mt_tiles);
+    L.end();
+  } else if (P.n_mt_mats) {
     L.begin(PH_K1_MT);
     const int blocks = stream_grid(P.total_mt_tiles, 8, persistent);
     k_momentum_score_cols_mt<<<blocks, 256, 0, s>>>(dmats, (const int32_t*)tab(P, P.off_mtmats),

@@ -362,4 +362,164 @@ __global__ void __launch_bounds__(256, 4) k_momentum_score_cols_mt(const MatDesc
   }
 }
 
+// ------------------------------------------------------------------ cols mode, M^T, cp.async pipeline
+// Same unit decomposition and column-block-major order as k_momentum_score_cols_mt (unit =
+// 256 rows of M x 64 columns = four 64 x 64 sub-tiles), for fp32 G on aligned, whole tiles.
+// Every sub-tile's G tile and M^T tile (16 KB each) are copied global -> shared with 16-byte
+// cp.async S - 1 sub-tiles ahead (across unit boundaries), so loads stay in flight while the
+// CTA transposes and stores: one barrier per sub-tile, no registers held by loads.
+// G's 16-byte chunk cj of tile row r sits at chunk cj ^ ((r >> 2) & 7): the transposed reads
+// (lane = (g, c8) -> G rows 4 c8 + q, column 4 jb + g) then hit 32 distinct banks.
+namespace {
+__device__ __forceinline__ void cp_async16(float* dst, const float* src) {
+  asm volatile("cp.async.cg.shared.global [%0], [%1], 16;" ::"r"(smem_u32(dst)), "l"(src) : "memory");
+}
+__device__ __forceinline__ void cp_async_commit() { asm volatile("cp.async.commit_group;" ::: "memory"); }
+template <int N>
+__device__ __forceinline__ void cp_async_wait() { asm volatile("cp.async.wait_group %0;" ::"n"(N) : "memory"); }
+
+struct MtUnit {
+  const MatDesc* md;
+  int64_t i0, j0;  // first row of M (column of M^T), first column of M (row of M^T)
+  int rb;
+};
+
+__device__ __forceinline__ MtUnit mt_unit(const MatDesc* __restrict__ mats, const int32_t* __restrict__ col_mats,
+                                          const int64_t* __restrict__ tile_prefix, int n_col_mats, int64_t u) {
+  int lo = 0, hi = n_col_mats - 1;
+  while (lo < hi) {
+    const int mid = (lo + hi + 1) >> 1;
+    if (tile_prefix[mid] <= u) lo = mid; else hi = mid - 1;
+  }
+  MtUnit r;
+  r.md = &mats[col_mats[lo]];
+  const int64_t local = u - tile_prefix[lo];
+  const int rbs = (int)(r.md->rows / kColRB);
+  const int cb = (int)(local / rbs);
+  r.rb = (int)(local % rbs);
+  r.i0 = (int64_t)r.rb * kColRB;
+  r.j0 = (int64_t)cb * 64;
+  return r;
+}
+}  // namespace
+
+template <int S>
+__global__ void __launch_bounds__(256) k_momentum_score_cols_mt_pipe(const MatDesc* __restrict__ mats,
+                                                                     const int32_t* __restrict__ col_mats,
+                                                                     const int64_t* __restrict__ tile_prefix,
+                                                                     int n_col_mats, int64_t total_units) {
+  extern __shared__ float4 sm4[];
+  float* sm = reinterpret_cast<float*>(sm4);  // [S][G 64 x 64 | M^T 64 x 64]
+  const int tid = threadIdx.x, lane = tid & 31, w = tid >> 5;
+  const int g = lane >> 3, c8 = lane & 7;
+  if (blockIdx.x >= total_units) return;
+  const int64_t my_units = (total_units - 1 - blockIdx.x) / gridDim.x + 1;
+  const int64_t n_st = my_units * 4;
+
+  MtUnit iu = mt_unit(mats, col_mats, tile_prefix, n_col_mats, blockIdx.x);  // issue cursor's unit
+  int64_t iu_idx = 0;
+  auto issue = [&](int64_t st) {
+    const int64_t ui = st >> 2;
+    if (ui != iu_idx) {
+      iu = mt_unit(mats, col_mats, tile_prefix, n_col_mats, blockIdx.x + ui * gridDim.x);
+      iu_idx = ui;
+    }
+    const MatDesc& md = *iu.md;
+    const int64_t i0 = iu.i0 + (st & 3) * 64;
+    float* gdst = sm + (int)(st % S) * 8192;
+    float* mdst = gdst + 4096;
+    const float* G = reinterpret_cast<const float*>(md.G);
+#pragma unroll
+    for (int q = 0; q < 4; ++q) {
+      const int c = tid + 256 * q, r = c >> 4, cj = c & 15;
+      cp_async16(gdst + r * 64 + ((cj ^ ((r >> 2) & 7)) << 2), G + (i0 + r) * md.ld + iu.j0 + 4 * cj);
+      cp_async16(mdst + r * 64 + 4 * cj, md.M + (iu.j0 + r) * md.ldm + i0 + 4 * cj);
+    }
+  };
+#pragma unroll
+  for (int s0 = 0; s0 < S - 1; ++s0) {
+    if (s0 < n_st) issue(s0);
+    cp_async_commit();
+  }
+  MtUnit cu = mt_unit(mats, col_mats, tile_prefix, n_col_mats, blockIdx.x);  // compute cursor's unit
+  float acc[2] = {0.f, 0.f};
+  for (int64_t st = 0; st < n_st; ++st) {
+    cp_async_wait<S - 2>();
+    __syncthreads();
+    if (st + S - 1 < n_st) issue(st + S - 1);
+    cp_async_commit();
+    if ((st & 3) == 0 && st) cu = mt_unit(mats, col_mats, tile_prefix, n_col_mats, blockIdx.x + (st >> 2) * gridDim.x);
+    const MatDesc& md = *cu.md;
+    const int64_t i0 = cu.i0 + (st & 3) * 64;
+    const float* gs = sm + (int)(st % S) * 8192;
+    const float* ms = gs + 4096;
+#pragma unroll
+    for (int u = 0; u < 4; ++u) {
+      const int jl = 8 * w + 4 * (u >> 1) + g, il = 4 * (c8 + 8 * (u & 1));
+      float4 m = *reinterpret_cast<const float4*>(ms + jl * 64 + il);
+      const int sw = ((jl >> 2) ^ ((il >> 2) & 7)) << 2;  // (il + q) >> 2 == il >> 2
+      const int jw = jl & 3;
+      m.x += gs[(il + 0) * 64 + sw + jw];
+      m.y += gs[(il + 1) * 64 + sw + jw];
+      m.z += gs[(il + 2) * 64 + sw + jw];
+      m.w += gs[(il + 3) * 64 + sw + jw];
+      *reinterpret_cast<float4*>(md.M + (cu.j0 + jl) * md.ldm + i0 + il) = m;
+      acc[u >> 1] += fabsf(m.x) + fabsf(m.y) + fabsf(m.z) + fabsf(m.w);
+    }
+    if ((st & 3) == 3) {
+      // unit done: reduce the 8 lanes (c8) sharing an M^T row in a fixed xor-tree order
+#pragma unroll
+      for (int jg = 0; jg < 2; ++jg) {
+        float v = acc[jg];
+#pragma unroll
+        for (int o = 4; o > 0; o >>= 1) v += __shfl_xor_sync(0xffffffffu, v, o);
+        if (c8 == 0) md.col_partials[(int64_t)cu.rb * md.cols + cu.j0 + 8 * w + 4 * jg + g] = v;
+        acc[jg] = 0.f;
+      }
+    }
+  }
+  cp_async_wait<0>();
+}
+
+template <int S>
+constexpr size_t mt_pipe_smem() { return (size_t)S * 8192 * sizeof(float); }
+
+void launch_momentum_score_cols_mt_pipe(int stages, int blocks, cudaStream_t s, const MatDesc* mats,
+                                        const int32_t* col_mats, const int64_t* tile_prefix, int n_col_mats,
+                                        int64_t total_units) {
+  if (stages == 3)
+    k_momentum_score_cols_mt_pipe<3><<<blocks, 256, mt_pipe_smem<3>(), s>>>(mats, col_mats, tile_prefix, n_col_mats,
+                                                                             total_units);
+  else if (stages == 2)
+    k_momentum_score_cols_mt_pipe<2><<<blocks, 256, mt_pipe_smem<2>(), s>>>(mats, col_mats, tile_prefix, n_col_mats,
+                                                                             total_units);
+  else if (stages == 6)
+    k_momentum_score_cols_mt_pipe<6><<<blocks, 256, mt_pipe_smem<6>(), s>>>(mats, col_mats, tile_prefix, n_col_mats,
+                                                                             total_units);
+  else
+    k_momentum_score_cols_mt_pipe<4><<<blocks, 256, mt_pipe_smem<4>(), s>>>(mats, col_mats, tile_prefix, n_col_mats,
+                                                                             total_units);
+}
+
+int momentum_score_cols_mt_pipe_attrs(int stages) {
+  cudaFuncSetAttribute(k_momentum_score_cols_mt_pipe<2>, cudaFuncAttributeMaxDynamicSharedMemorySize,
+                       (int)mt_pipe_smem<2>());
+  cudaFuncSetAttribute(k_momentum_score_cols_mt_pipe<3>, cudaFuncAttributeMaxDynamicSharedMemorySize,
+                       (int)mt_pipe_smem<3>());
+  cudaFuncSetAttribute(k_momentum_score_cols_mt_pipe<4>, cudaFuncAttributeMaxDynamicSharedMemorySize,
+                       (int)mt_pipe_smem<4>());
+  cudaFuncSetAttribute(k_momentum_score_cols_mt_pipe<6>, cudaFuncAttributeMaxDynamicSharedMemorySize,
+                       (int)mt_pipe_smem<6>());
+  int nb = 0;
+  if (stages == 3)
+    cudaOccupancyMaxActiveBlocksPerMultiprocessor(&nb, k_momentum_score_cols_mt_pipe<3>, 256, mt_pipe_smem<3>());
+  else if (stages == 2)
+    cudaOccupancyMaxActiveBlocksPerMultiprocessor(&nb, k_momentum_score_cols_mt_pipe<2>, 256, mt_pipe_smem<2>());
+  else if (stages == 6)
+    cudaOccupancyMaxActiveBlocksPerMultiprocessor(&nb, k_momentum_score_cols_mt_pipe<6>, 256, mt_pipe_smem<6>());
+  else
+    cudaOccupancyMaxActiveBlocksPerMultiprocessor(&nb, k_momentum_score_cols_mt_pipe<4>, 256, mt_pipe_smem<4>());
+  return nb;
+}
+
 }  // namespace dion2
