@@ -966,6 +966,35 @@ void stage_pre(Plan& P, const dion2_config* c, void* ws, int32_t* status, Launch
   stage_gather(P, c, ws, L, s, persistent);
 }
 
+// Transposed-M K1 over a list of column-mode matrices: the cp.async-pipelined kernel when
+// every transposed-M matrix of the host descriptor table has fp32 G and aligned whole
+// 256 x 64 units (DION2_K1MT_PIPE=0: the register-staged kernel; =2/3/4: stages; 3 = two
+// 96 KB CTAs per SM measured best: 0.93 -> 0.76 ms on the 1B set), else the register-staged
+// kernel on `legacy_grid` blocks.
+void launch_k1_mt(const MatDesc* host_desc, int n_desc, int grad_dtype, int64_t total_tiles, int legacy_grid,
+                  cudaStream_t s, const MatDesc* dmats, const int32_t* list, const int64_t* prefix, int n_list) {
+  const char* pe = getenv("DION2_K1MT_PIPE");  // read per call (tests flip it)
+  int pipe_stages = pe ? atoi(pe) : 3;
+  if (pipe_stages != 0 && (pipe_stages < 2 || pipe_stages > 4)) pipe_stages = 3;
+  const bool bf16 = grad_dtype == DION2_DT_BF16;
+  bool pipe = pipe_stages != 0;
+  for (int i = 0; i < n_desc && pipe; ++i)
+    if (host_desc[i].mt && host_desc[i].axis == kAxisCols)
+      pipe = (host_desc[i].grad_bf16 != 0) == bf16 && host_desc[i].vec4 && host_desc[i].rows % kColRowBlock == 0 &&
+             host_desc[i].cols % 64 == 0 && host_desc[i].ldm % 4 == 0 &&
+             (!bf16 || (host_desc[i].ld % 8 == 0 && (uintptr_t)host_desc[i].G % 16 == 0));
+  if (pipe) {
+    static int per_sm[5][2] = {{-1, -1}, {-1, -1}, {-1, -1}, {-1, -1}, {-1, -1}};
+    int& nb = per_sm[pipe_stages][bf16];
+    if (nb < 0) nb = std::max(1, momentum_score_cols_mt_pipe_attrs(pipe_stages, bf16));
+    const int sms = g_sm_count > 0 ? g_sm_count : 148;
+    launch_momentum_score_cols_mt_pipe(pipe_stages, bf16, (int)std::min<int64_t>(total_tiles, (int64_t)nb * sms), s,
+                                       dmats, list, prefix, n_list, total_tiles);
+  } else {
+    k_momentum_score_cols_mt<<<legacy_grid, 256, 0, s>>>(dmats, list, prefix, n_list, total_tiles);
+  }
+}
+
 // K1 momentum + score, K2 select (Alg. 1 l.2-3)
 void stage_k1_select(Plan& P, const dion2_config* c, void* ws, int32_t* status, Launcher& L, cudaStream_t s,
                      bool persistent) {
@@ -1003,34 +1032,11 @@ void stage_k1_select(Plan& P, const dion2_config* c, void* ws, int32_t* status, 
                                                  P.total_col_tiles);
     L.end();
   }
-  // transposed-M K1: the cp.async-pipelined kernel when every listed matrix has fp32 G and
-  // aligned whole 256 x 64 units (DION2_K1MT_PIPE=0: the register-staged kernel; =2/3/4/6:
-  // stages; 3 = two 96 KB CTAs per SM measured best: 0.93 -> 0.76 ms on the 1B set)
-  bool mt_pipe = P.n_mt_mats > 0 && c->grad_dtype == DION2_DT_F32;
-  static const char* pe = getenv("DION2_K1MT_PIPE");
-  static const int pipe_stages = pe ? atoi(pe) : 3;
-  if (pipe_stages == 0) mt_pipe = false;
-  if (mt_pipe) {
-    const MatDesc* hd = reinterpret_cast<const MatDesc*>(P.host_tables.data());
-    for (int i = 0; i < n && mt_pipe; ++i)
-      if (hd[i].mt && hd[i].axis == kAxisCols)
-        mt_pipe = hd[i].vec4 && hd[i].rows % kColRowBlock == 0 && hd[i].cols % 64 == 0 && hd[i].ldm % 4 == 0;
-  }
-  if (P.n_mt_mats && mt_pipe) {
-    static int per_sm = -1;
-    if (per_sm < 0) per_sm = std::max(1, momentum_score_cols_mt_pipe_attrs(pipe_stages));
-    const int sms = g_sm_count > 0 ? g_sm_count : 148;
+  if (P.n_mt_mats) {
     L.begin(PH_K1_MT);
-    launch_momentum_score_cols_mt_pipe(pipe_stages, (int)std::min<int64_t>(P.total_mt_tiles, (int64_t)per_sm * sms), s,
-                                       dmats, (const int32_t*)tab(P, P.off_mtmats), (const int64_t*)tab(P, P.off_mtprefix),
-                                       P.n_mt_mats, P.total_mt_tiles);
-    L.end();
-  } else if (P.n_mt_mats) {
-    L.begin(PH_K1_MT);
-    const int blocks = stream_grid(P.total_mt_tiles, 8, persistent);
-    k_momentum_score_cols_mt<<<blocks, 256, 0, s>>>(dmats, (const int32_t*)tab(P, P.off_mtmats),
-                                                    (const int64_t*)tab(P, P.off_mtprefix), P.n_mt_mats,
-                                                    P.total_mt_tiles);
+    launch_k1_mt(reinterpret_cast<const MatDesc*>(P.host_tables.data()), n, c->grad_dtype, P.total_mt_tiles,
+                 stream_grid(P.total_mt_tiles, 8, persistent), s, dmats, (const int32_t*)tab(P, P.off_mtmats),
+                 (const int64_t*)tab(P, P.off_mtprefix), P.n_mt_mats);
     L.end();
   }
   const int n_sel = P.fuse_tasks ? P.fuse_rest_n : n;

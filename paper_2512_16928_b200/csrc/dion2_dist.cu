@@ -510,9 +510,11 @@ void phase_local_k1(DistPlan& D, void* ws, Launcher& L, cudaStream_t s) {
   if (D.n_mt_mats) {
     L.begin(PH_K1_MT);
     const int64_t blocks = std::min<int64_t>(D.total_mt_tiles, (int64_t)sms * 8);
-    k_momentum_score_cols_mt<<<(unsigned)blocks, 256, 0, s>>>(dm, (const int32_t*)dt(D, D.t_mtmats),
-                                                              (const int64_t*)dt(D, D.t_mtprefix), D.n_mt_mats,
-                                                              D.total_mt_tiles);
+    launch_k1_mt(reinterpret_cast<const MatDesc*>(D.htab.data() + D.t_desc), D.n,
+                 reinterpret_cast<const MatDesc*>(D.htab.data() + D.t_desc)->grad_bf16 ? DION2_DT_BF16 : DION2_DT_F32,
+                 D.total_mt_tiles,
+                 (int)blocks, s, dm, (const int32_t*)dt(D, D.t_mtmats), (const int64_t*)dt(D, D.t_mtprefix),
+                 D.n_mt_mats);
     L.end();
   }
   if (D.n_allcols) {

@@ -403,13 +403,17 @@ __device__ __forceinline__ MtUnit mt_unit(const MatDesc* __restrict__ mats, cons
 }
 }  // namespace
 
-template <int S>
+// bf16 G: the G tile is 64 x 64 bf16 (8 KB, 8 chunks of 8 columns per row), chunk cj of row r
+// at cj ^ ((r >> 2) & 7): a warp's transposed reads then touch 16 distinct words, two lanes each.
+template <int S, bool kBf16>
 __global__ void __launch_bounds__(256) k_momentum_score_cols_mt_pipe(const MatDesc* __restrict__ mats,
                                                                      const int32_t* __restrict__ col_mats,
                                                                      const int64_t* __restrict__ tile_prefix,
                                                                      int n_col_mats, int64_t total_units) {
+  constexpr int kGB = kBf16 ? 8192 : 16384;  // G tile bytes
+  constexpr int kStageB = kGB + 16384;       // + M^T tile
   extern __shared__ float4 sm4[];
-  float* sm = reinterpret_cast<float*>(sm4);  // [S][G 64 x 64 | M^T 64 x 64]
+  uint8_t* sm = reinterpret_cast<uint8_t*>(sm4);  // [S][G tile | M^T 64 x 64 fp32]
   const int tid = threadIdx.x, lane = tid & 31, w = tid >> 5;
   const int g = lane >> 3, c8 = lane & 7;
   if (blockIdx.x >= total_units) return;
@@ -426,13 +430,28 @@ __global__ void __launch_bounds__(256) k_momentum_score_cols_mt_pipe(const MatDe
     }
     const MatDesc& md = *iu.md;
     const int64_t i0 = iu.i0 + (st & 3) * 64;
-    float* gdst = sm + (int)(st % S) * 8192;
-    float* mdst = gdst + 4096;
-    const float* G = reinterpret_cast<const float*>(md.G);
+    uint8_t* gdst = sm + (int)(st % S) * kStageB;
+    float* mdst = reinterpret_cast<float*>(gdst + kGB);
+    if constexpr (kBf16) {
+      const __nv_bfloat16* G = reinterpret_cast<const __nv_bfloat16*>(md.G);
+#pragma unroll
+      for (int q = 0; q < 2; ++q) {
+        const int c = tid + 256 * q, r = c >> 3, cj = c & 7;
+        cp_async16(reinterpret_cast<float*>(gdst + r * 128 + ((cj ^ ((r >> 2) & 7)) << 4)),
+                   reinterpret_cast<const float*>(G + (i0 + r) * md.ld + iu.j0 + 8 * cj));
+      }
+    } else {
+      const float* G = reinterpret_cast<const float*>(md.G);
+      float* gf = reinterpret_cast<float*>(gdst);
+#pragma unroll
+      for (int q = 0; q < 4; ++q) {
+        const int c = tid + 256 * q, r = c >> 4, cj = c & 15;
+        cp_async16(gf + r * 64 + ((cj ^ ((r >> 2) & 7)) << 2), G + (i0 + r) * md.ld + iu.j0 + 4 * cj);
+      }
+    }
 #pragma unroll
     for (int q = 0; q < 4; ++q) {
       const int c = tid + 256 * q, r = c >> 4, cj = c & 15;
-      cp_async16(gdst + r * 64 + ((cj ^ ((r >> 2) & 7)) << 2), G + (i0 + r) * md.ld + iu.j0 + 4 * cj);
       cp_async16(mdst + r * 64 + 4 * cj, md.M + (iu.j0 + r) * md.ldm + i0 + 4 * cj);
     }
   };
@@ -451,18 +470,29 @@ __global__ void __launch_bounds__(256) k_momentum_score_cols_mt_pipe(const MatDe
     if ((st & 3) == 0 && st) cu = mt_unit(mats, col_mats, tile_prefix, n_col_mats, blockIdx.x + (st >> 2) * gridDim.x);
     const MatDesc& md = *cu.md;
     const int64_t i0 = cu.i0 + (st & 3) * 64;
-    const float* gs = sm + (int)(st % S) * 8192;
-    const float* ms = gs + 4096;
+    const uint8_t* gs = sm + (int)(st % S) * kStageB;
+    const float* ms = reinterpret_cast<const float*>(gs + kGB);
 #pragma unroll
     for (int u = 0; u < 4; ++u) {
       const int jl = 8 * w + 4 * (u >> 1) + g, il = 4 * (c8 + 8 * (u & 1));
       float4 m = *reinterpret_cast<const float4*>(ms + jl * 64 + il);
-      const int sw = ((jl >> 2) ^ ((il >> 2) & 7)) << 2;  // (il + q) >> 2 == il >> 2
-      const int jw = jl & 3;
-      m.x += gs[(il + 0) * 64 + sw + jw];
-      m.y += gs[(il + 1) * 64 + sw + jw];
-      m.z += gs[(il + 2) * 64 + sw + jw];
-      m.w += gs[(il + 3) * 64 + sw + jw];
+      float e[4];
+      if constexpr (kBf16) {
+        // (il + q) >> 2 == il >> 2; chunk jl >> 3, element jl & 7
+        const int off = (((jl >> 3) ^ ((il >> 2) & 7)) << 4) + (jl & 7) * 2;
+#pragma unroll
+        for (int q = 0; q < 4; ++q)
+          e[q] = __bfloat162float(*reinterpret_cast<const __nv_bfloat16*>(gs + (il + q) * 128 + off));
+      } else {
+        const float* gf = reinterpret_cast<const float*>(gs);
+        const int off = (((jl >> 2) ^ ((il >> 2) & 7)) << 2) + (jl & 3);
+#pragma unroll
+        for (int q = 0; q < 4; ++q) e[q] = gf[(il + q) * 64 + off];
+      }
+      m.x += e[0];
+      m.y += e[1];
+      m.z += e[2];
+      m.w += e[3];
       *reinterpret_cast<float4*>(md.M + (cu.j0 + jl) * md.ldm + i0 + il) = m;
       acc[u >> 1] += fabsf(m.x) + fabsf(m.y) + fabsf(m.z) + fabsf(m.w);
     }
@@ -481,45 +511,46 @@ __global__ void __launch_bounds__(256) k_momentum_score_cols_mt_pipe(const MatDe
   cp_async_wait<0>();
 }
 
-template <int S>
-constexpr size_t mt_pipe_smem() { return (size_t)S * 8192 * sizeof(float); }
+template <int S, bool kBf16>
+constexpr size_t mt_pipe_smem() { return (size_t)S * ((kBf16 ? 8192 : 16384) + 16384); }
 
-void launch_momentum_score_cols_mt_pipe(int stages, int blocks, cudaStream_t s, const MatDesc* mats,
-                                        const int32_t* col_mats, const int64_t* tile_prefix, int n_col_mats,
-                                        int64_t total_units) {
-  if (stages == 3)
-    k_momentum_score_cols_mt_pipe<3><<<blocks, 256, mt_pipe_smem<3>(), s>>>(mats, col_mats, tile_prefix, n_col_mats,
-                                                                             total_units);
-  else if (stages == 2)
-    k_momentum_score_cols_mt_pipe<2><<<blocks, 256, mt_pipe_smem<2>(), s>>>(mats, col_mats, tile_prefix, n_col_mats,
-                                                                             total_units);
-  else if (stages == 6)
-    k_momentum_score_cols_mt_pipe<6><<<blocks, 256, mt_pipe_smem<6>(), s>>>(mats, col_mats, tile_prefix, n_col_mats,
-                                                                             total_units);
-  else
-    k_momentum_score_cols_mt_pipe<4><<<blocks, 256, mt_pipe_smem<4>(), s>>>(mats, col_mats, tile_prefix, n_col_mats,
-                                                                             total_units);
+template <int S, bool B>
+static void mt_pipe_launch(int blocks, cudaStream_t s, const MatDesc* mats, const int32_t* col_mats,
+                           const int64_t* tile_prefix, int n_col_mats, int64_t total_units) {
+  k_momentum_score_cols_mt_pipe<S, B><<<blocks, 256, mt_pipe_smem<S, B>(), s>>>(mats, col_mats, tile_prefix,
+                                                                                n_col_mats, total_units);
+}
+template <int S, bool B>
+static int mt_pipe_attr() {
+  cudaFuncSetAttribute(k_momentum_score_cols_mt_pipe<S, B>, cudaFuncAttributeMaxDynamicSharedMemorySize,
+                       (int)mt_pipe_smem<S, B>());
+  int nb = 0;
+  cudaOccupancyMaxActiveBlocksPerMultiprocessor(&nb, k_momentum_score_cols_mt_pipe<S, B>, 256, mt_pipe_smem<S, B>());
+  return nb;
 }
 
-int momentum_score_cols_mt_pipe_attrs(int stages) {
-  cudaFuncSetAttribute(k_momentum_score_cols_mt_pipe<2>, cudaFuncAttributeMaxDynamicSharedMemorySize,
-                       (int)mt_pipe_smem<2>());
-  cudaFuncSetAttribute(k_momentum_score_cols_mt_pipe<3>, cudaFuncAttributeMaxDynamicSharedMemorySize,
-                       (int)mt_pipe_smem<3>());
-  cudaFuncSetAttribute(k_momentum_score_cols_mt_pipe<4>, cudaFuncAttributeMaxDynamicSharedMemorySize,
-                       (int)mt_pipe_smem<4>());
-  cudaFuncSetAttribute(k_momentum_score_cols_mt_pipe<6>, cudaFuncAttributeMaxDynamicSharedMemorySize,
-                       (int)mt_pipe_smem<6>());
-  int nb = 0;
-  if (stages == 3)
-    cudaOccupancyMaxActiveBlocksPerMultiprocessor(&nb, k_momentum_score_cols_mt_pipe<3>, 256, mt_pipe_smem<3>());
-  else if (stages == 2)
-    cudaOccupancyMaxActiveBlocksPerMultiprocessor(&nb, k_momentum_score_cols_mt_pipe<2>, 256, mt_pipe_smem<2>());
-  else if (stages == 6)
-    cudaOccupancyMaxActiveBlocksPerMultiprocessor(&nb, k_momentum_score_cols_mt_pipe<6>, 256, mt_pipe_smem<6>());
-  else
-    cudaOccupancyMaxActiveBlocksPerMultiprocessor(&nb, k_momentum_score_cols_mt_pipe<4>, 256, mt_pipe_smem<4>());
-  return nb;
+void launch_momentum_score_cols_mt_pipe(int stages, bool bf16, int blocks, cudaStream_t s, const MatDesc* mats,
+                                        const int32_t* col_mats, const int64_t* tile_prefix, int n_col_mats,
+                                        int64_t total_units) {
+  switch (stages * 2 + (bf16 ? 1 : 0)) {
+    case 4: mt_pipe_launch<2, false>(blocks, s, mats, col_mats, tile_prefix, n_col_mats, total_units); break;
+    case 5: mt_pipe_launch<2, true>(blocks, s, mats, col_mats, tile_prefix, n_col_mats, total_units); break;
+    case 8: mt_pipe_launch<4, false>(blocks, s, mats, col_mats, tile_prefix, n_col_mats, total_units); break;
+    case 9: mt_pipe_launch<4, true>(blocks, s, mats, col_mats, tile_prefix, n_col_mats, total_units); break;
+    case 7: mt_pipe_launch<3, true>(blocks, s, mats, col_mats, tile_prefix, n_col_mats, total_units); break;
+    default: mt_pipe_launch<3, false>(blocks, s, mats, col_mats, tile_prefix, n_col_mats, total_units); break;
+  }
+}
+
+int momentum_score_cols_mt_pipe_attrs(int stages, bool bf16) {
+  switch (stages * 2 + (bf16 ? 1 : 0)) {
+    case 4: return mt_pipe_attr<2, false>();
+    case 5: return mt_pipe_attr<2, true>();
+    case 8: return mt_pipe_attr<4, false>();
+    case 9: return mt_pipe_attr<4, true>();
+    case 7: return mt_pipe_attr<3, true>();
+    default: return mt_pipe_attr<3, false>();
+  }
 }
 
 }  // namespace dion2

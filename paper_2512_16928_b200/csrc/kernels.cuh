@@ -21,12 +21,12 @@ __global__ void k_momentum_score_cols_mt(const MatDesc* __restrict__ mats, const
 __global__ void k_col_scores_finalize(const MatDesc* __restrict__ mats, const int32_t* __restrict__ list,
                                       const int64_t* __restrict__ prefix, int n_list, int64_t total);
 
-// fp32 G, 16-B aligned whole tiles (rows % 256 == 0, cols % 64 == 0): cp.async-pipelined
-// variant of k_momentum_score_cols_mt over the same units; stages 3 / 4 / 6
-void launch_momentum_score_cols_mt_pipe(int stages, int blocks, cudaStream_t s, const MatDesc* mats,
+// 16-B aligned whole tiles (rows % 256 == 0, cols % 64 == 0), fp32 or bf16 G: cp.async-pipelined
+// variant of k_momentum_score_cols_mt over the same units; stages 2 / 3 / 4
+void launch_momentum_score_cols_mt_pipe(int stages, bool bf16, int blocks, cudaStream_t s, const MatDesc* mats,
                                         const int32_t* col_mats, const int64_t* tile_prefix, int n_col_mats,
                                         int64_t total_units);
-int momentum_score_cols_mt_pipe_attrs(int stages);  // sets the smem attributes; returns blocks per SM
+int momentum_score_cols_mt_pipe_attrs(int stages, bool bf16);  // sets the smem attributes; returns blocks per SM
 
 // ---------------- K2 top-k select (k_select.cu)
 constexpr int kSelectThreads = 1024;

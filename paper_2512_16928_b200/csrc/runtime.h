@@ -166,6 +166,8 @@ void ensure_device_attrs();
 int run_ns(Plan& P, const dion2_config* c, Launcher& L, cudaStream_t s, bool do_norm);
 int refresh_tables(Plan& P, const dion2_matrix* mats, const dion2_config* c, cudaStream_t s);
 int reset_status(int32_t* status, cudaStream_t s);
+void launch_k1_mt(const MatDesc* host_desc, int n_desc, int grad_dtype, int64_t total_tiles, int legacy_grid,
+                  cudaStream_t s, const MatDesc* dmats, const int32_t* list, const int64_t* prefix, int n_list);
 void stage_pre(Plan& P, const dion2_config* c, void* ws, int32_t* status, Launcher& L, cudaStream_t s,
                bool persistent);
 void stage_k1_select(Plan& P, const dion2_config* c, void* ws, int32_t* status, Launcher& L, cudaStream_t s,

@@ -217,6 +217,17 @@ def test_transposed_momentum_for_column_mode():
     _assert(run_parity([(2048, 1536), (520, 300)], 1.0, "auto", "bf16", steps=2, m_transposed=True), BF16_TOL)
 
 
+@pytest.mark.parametrize("grad_bf16", [False, True])
+@pytest.mark.parametrize("stages", [None, "2", "4"])
+def test_pipelined_transposed_k1(grad_bf16, stages, monkeypatch):
+    """The cp.async-pipelined transposed-M K1 (every column-mode matrix aligned, whole
+    256 x 64 units): fp32 and bf16 G, the default 3 stages and the 2 / 4 stage variants."""
+    if stages:
+        monkeypatch.setenv("DION2_K1MT_PIPE", stages)
+    shapes = [(8192, 2048), (1024, 512), (2048, 1024), (512, 2048)]
+    _assert(run_parity(shapes, 0.25, "auto", "bf16", steps=3, m_transposed=True, grad_bf16=grad_bf16), BF16_TOL)
+
+
 def test_full_decay_ablation_fp32():
     _assert(run_parity([(96, 160)], 0.25, "auto", "fp32", steps=3, decay_mode=1), FP32_TOL)
 
