@@ -291,6 +291,9 @@ def run_ours(args):
     local = int(os.environ.get("LOCAL_RANK", "0"))
     # DION2_BENCH_DIST=1 runs the owner-compute path even at N = 1 (single-rank NCCL group)
     use_dist = world > 1 or os.environ.get("DION2_BENCH_DIST") == "1"
+    if use_dist and world == 1:  # one-rank NCCL group without torchrun
+        for k, v in (("RANK", "0"), ("WORLD_SIZE", "1"), ("MASTER_ADDR", "127.0.0.1"), ("MASTER_PORT", "29531")):
+            os.environ.setdefault(k, v)
     torch.cuda.set_device(local)
     if use_dist:
         dist.init_process_group("nccl", device_id=torch.device("cuda", local))
