@@ -266,6 +266,7 @@ def e2e_run(opt, Ws, Ms, Gs, G_flat, steps, ks):
         sel_views.append(sel_dev[off:off + k])
         off += k
     sel_host = torch.empty(sum(ks), dtype=torch.int32, pin_memory=True)
+    opt.step(Ws, Ms, Gs, sel_out=sel_views)  # untimed: plan (and, in graph mode, the capture) for this call
     torch.cuda.synchronize()
     s = torch.cuda.current_stream()
     e0, e1 = torch.cuda.Event(enable_timing=True), torch.cuda.Event(enable_timing=True)
@@ -319,7 +320,7 @@ def run_ours(args):
         mts = [(not args.no_mt) and m > n for (m, n) in shapes]
         bufs, Ws, Ms, Gs = build_state(shapes, dev, seed=rank, m_transposed=mts)
         make_opt = lambda a: Dion2(alpha=a, axis="auto", precision="bf16", m_transposed=mts,  # noqa: E731
-                                   ns_form=args.ns_form)
+                                   ns_form=args.ns_form, cuda_graph=not args.no_graph)
     opt = make_opt(args.alpha)
 
     with ClockSampler(local) as clk:
@@ -329,11 +330,19 @@ def run_ours(args):
     if rc != 0:
         raise RuntimeError(f"status {rc} (matrix {bad})")
 
+    # the same step without the CUDA graph (every step's launches enqueued by the host)
+    ms_eager = None
+    if not use_dist and not args.no_graph:
+        opt_e = Dion2(alpha=args.alpha, axis="auto", precision="bf16", m_transposed=mts, ns_form=args.ns_form)
+        ms_eager = time_steps(opt_e, Ws, Ms, Gs, args.steps, args.warmup, None)
+        del opt_e
+
     # per-phase device time (CUDA events on the launching stream around every launch), with
     # the chunked two-stream pipeline disabled so every kernel is timed in isolation
     prev_chunks = os.environ.get("DION2_CHUNKS")
     os.environ["DION2_CHUNKS"] = "1"
-    opt_iso = make_opt(args.alpha)
+    opt_iso = Dion2(alpha=args.alpha, axis="auto", precision="bf16", m_transposed=mts, ns_form=args.ns_form) \
+        if not use_dist else make_opt(args.alpha)  # eager: the phase events are recorded per host launch
     opt_iso.step(Ws, Ms, Gs)  # build the plan outside the timed pass
     set_phase_timing(True)
     ms_timed = time_steps(opt_iso, Ws, Ms, Gs, args.steps, 0, None)
@@ -515,6 +524,9 @@ def run_ours(args):
             "ns_standard_tflop_per_step": ns_std / 1e12,
             "ns_standard_equiv_tflops": ns_std_tflops,
             "ns_standard_equiv_frac_bf16_burst": ns_std_tflops / peaks["bf16_tflops"],
+            "ms_per_step_eager": ms_eager,
+            "step_mode": "CUDA graph replay of the C-ABI step (Dion2(cuda_graph=True))" if (not use_dist and not args.no_graph)
+                         else "eager",
             "ms_per_step_unpipelined_with_phase_events": ms_timed,
             "phases_note": "per-kernel times (CUDA events around every launch) from a separate K-step pass "
                            "with the chunked pipeline off (DION2_CHUNKS=1, also the default)",
@@ -587,6 +599,8 @@ def main():
     ap.add_argument("--cpu-budget", type=float, default=20.0)
     ap.add_argument("--layers", type=int, default=0, help="override the layer count (profiling only)")
     ap.add_argument("--no-e2e", action="store_true")
+    ap.add_argument("--no-graph", action="store_true",
+                    help="eager steps (default: Dion2(cuda_graph=True), the step replayed as a CUDA graph)")
     ap.add_argument("--no-sweep", action="store_true", help="skip the alpha sweep / forced axis modes")
     ap.add_argument("--no-mt", action="store_true", help="keep column-mode momentum in W's layout")
     ap.add_argument("--ns-form", choices=["auto", "direct", "gram"], default="auto",

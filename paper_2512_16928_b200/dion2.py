@@ -7,6 +7,7 @@ not on a CUDA device, these functions raise.
 """
 from __future__ import annotations
 
+import collections
 import ctypes
 import os
 from typing import Dict, List, Optional, Sequence, Tuple
@@ -199,25 +200,72 @@ class Dion2:
     opt = Dion2(alpha=0.25); opt.step(Ws, Ms, Gs)   # all on one CUDA device
     """
 
-    def __init__(self, m_transposed=None, storage_transposed=None, **cfg_kw):
+    def __init__(self, m_transposed=None, storage_transposed=None, cuda_graph: bool = False, **cfg_kw):
         """m_transposed / storage_transposed: default per-matrix layout flags used by step()
-        (see describe())."""
+        (see describe()).  cuda_graph: the first step on a given set of tensors runs eagerly
+        (building the library's plan) and is then captured once into a CUDA graph; later
+        steps on the same tensors, config and stream device replay it (no per-step host
+        work, no launch gaps).  One call is always exactly one optimizer step."""
         self.cfg_kw = dict(cfg_kw)
         self.m_transposed = m_transposed
         self.storage_transposed = storage_transposed
+        self.cuda_graph = cuda_graph
+        self._graphs = collections.OrderedDict()  # key -> (graph, workspace slot), LRU order
         self._ws: Optional[torch.Tensor] = None
+
+    # Graph mode: each captured tensor set gets its own library plan, selected by a workspace
+    # base offset (the plan cache is keyed by the workspace pointer): a plan's device descriptor
+    # table then holds that set's pointers for good, so replaying one graph after another
+    # set's step cannot read another set's pointers.  The scratch itself is shared (graphs
+    # run in stream order).
+    GRAPH_SLOTS = 16
+    SLOT_BYTES = 4096
 
     def workspace(self, arr, n, cfg, device) -> torch.Tensor:
         need = ctypes.c_size_t(0)
         rc = _lib().dion2_workspace_size(arr, n, ctypes.byref(cfg), ctypes.byref(need))
         if rc:
             raise Dion2Error(rc, "dion2_workspace_size")
+        if self.cuda_graph:
+            need.value += self.GRAPH_SLOTS * self.SLOT_BYTES
         if self._ws is None or self._ws.numel() < need.value or self._ws.device != device:
+            self._graphs.clear()  # captured graphs reference the old workspace
             self._ws = torch.empty(need.value, dtype=torch.uint8, device=device)
         return self._ws
 
     def step(self, Ws, Ms, Gs, sel_out=None, O_out=None, stream: Optional[torch.cuda.Stream] = None,
              m_transposed=None, storage_transposed=None, **override):
+        if self.cuda_graph and stream is None:
+            ptrs = lambda ts: tuple((t.data_ptr(), tuple(t.shape), tuple(t.stride()), t.dtype) if t is not None  # noqa: E731
+                                    else None for t in ts)
+            key = (ptrs(Ws), ptrs(Ms), ptrs(Gs), ptrs(sel_out or ()), ptrs(O_out or ()),
+                   tuple(m_transposed if m_transposed is not None else self.m_transposed or ()),
+                   tuple(storage_transposed if storage_transposed is not None else self.storage_transposed or ()),
+                   tuple(sorted((k, repr(v)) for k, v in {**self.cfg_kw, **override}.items())),
+                   torch.cuda.current_device())
+            hit = self._graphs.get(key)
+            if hit is not None and self._ws is not None:
+                self._graphs.move_to_end(key)
+                hit[0].replay()
+                self._last_slot = hit[1]
+                return
+            used = {slot for (_, slot) in self._graphs.values()}
+            free = [i for i in range(self.GRAPH_SLOTS) if i not in used]
+            if not free:  # evict the least recently replayed graph and reuse its slot
+                _, (_, slot) = self._graphs.popitem(last=False)
+                free = [slot]
+            slot = free[0]
+            self._step(Ws, Ms, Gs, sel_out, O_out, None, m_transposed, storage_transposed, slot, **override)
+            ws_before = self._ws
+            g = torch.cuda.CUDAGraph()
+            with torch.cuda.graph(g):  # captured, not executed: this call's step ran above
+                self._step(Ws, Ms, Gs, sel_out, O_out, None, m_transposed, storage_transposed, slot, **override)
+            if self._ws is ws_before:  # a reallocated workspace invalidated every graph (cleared)
+                self._graphs[key] = (g, slot)
+            return
+        self._step(Ws, Ms, Gs, sel_out, O_out, stream, m_transposed, storage_transposed, 0, **override)
+
+    def _step(self, Ws, Ms, Gs, sel_out, O_out, stream, m_transposed, storage_transposed, slot, **override):
         kw = dict(self.cfg_kw)
         kw.update(override)
         if m_transposed is None:
@@ -230,13 +278,17 @@ class Dion2:
         dev = Ws[0].device
         ws = self.workspace(arr, len(Ws), cfg, dev)
         st = stream if stream is not None else torch.cuda.current_stream(dev)
-        rc = _lib().dion2_step_batched(arr, len(Ws), ctypes.byref(cfg), ws.data_ptr(), ws.numel(), st.cuda_stream)
+        off = slot * self.SLOT_BYTES
+        self._last_slot = slot
+        rc = _lib().dion2_step_batched(arr, len(Ws), ctypes.byref(cfg), ws.data_ptr() + off, ws.numel() - off,
+                                       st.cuda_stream)
         if rc:
             raise Dion2Error(rc, "dion2_step_batched")
 
     def status(self) -> Tuple[int, int]:
         bad = ctypes.c_int32(-1)
-        rc = _lib().dion2_get_status(self._ws.data_ptr() if self._ws is not None else None, ctypes.byref(bad))
+        ws = self._ws.data_ptr() + getattr(self, "_last_slot", 0) * self.SLOT_BYTES if self._ws is not None else None
+        rc = _lib().dion2_get_status(ws, ctypes.byref(bad))
         return rc, bad.value
 
 
