@@ -1,0 +1,77 @@
+"""bench.py's work accounting (-m "not gpu"): the algorithmic FLOPs and bytes behind the
+reported roofline fractions, pinned to SURVEY.md section 8(d)'s table and to closed forms.
+
+The per-unit figures: NS FLOPs T(4p^2 q + 2p^3) per matrix in the
+direct form, 4p^2 q + (4T - 3) 2p^3 in the Gram-space form (reading R23); HBM bytes
+m n (b_G + 8) for momentum + score and 10 k o each for the gather and the scatter.
+"""
+import os
+import sys
+
+import pytest
+
+ROOT = os.path.dirname(os.path.dirname(os.path.abspath(__file__)))
+sys.path.insert(0, ROOT)
+
+import bench  # noqa: E402
+from synth import layer_set_1b, layer_set_8b  # noqa: E402
+
+
+def test_1b_set_shape_census():
+    shapes = layer_set_1b(24)
+    assert len(shapes) == 144
+    assert sum(m * n for m, n in shapes) == 1_207_959_552  # 1.208 B parameters
+    assert len(layer_set_8b(32)) == 224 and abs(sum(m * n for m, n in layer_set_8b(32)) - 6.98e9) < 0.01e9
+
+
+@pytest.mark.parametrize("alpha,tflop", [(1.0, 61.85), (0.5, 13.92), (0.25, 3.29), (0.125, 0.80)])
+def test_direct_ns_flops_match_survey_table(alpha, tflop):
+    """SURVEY 8(d) cfg 2: NS FLOP 61.85 / 13.92 / 3.29 / 0.80 TFLOP for alpha 1 / 0.5 / 0.25 / 0.125."""
+    f, _ = bench.work_model(layer_set_1b(24), alpha, ns_form="direct", fused=False)
+    assert abs(sum(f.values()) / 1e12 - tflop) < 0.01
+
+
+def test_gram_form_flops_closed_form():
+    """Gram space at alpha = 0.25: every matrix has p = 512 and q = 2048 or 8192 (q >= 2p)."""
+    f, _ = bench.work_model(layer_set_1b(24), 0.25, ns_form="auto", fused=False)
+    p, T = 512, 5
+    want = sum(4 * p * p * q + (4 * T - 3) * 2 * p ** 3 for q in [2048] * 96 + [8192] * 48)
+    assert abs(sum(f.values()) - want) < 1e3
+    assert abs(sum(f.values()) / 1e12 - 1.28) < 0.005  # DESIGN 6: 1.28 TFLOP in Gram form (2.6x fewer)
+    # alpha = 1: q = p, the direct form everywhere
+    f1, _ = bench.work_model(layer_set_1b(24), 1.0, ns_form="auto", fused=False)
+    fd, _ = bench.work_model(layer_set_1b(24), 1.0, ns_form="direct", fused=False)
+    assert sum(f1.values()) == sum(fd.values())
+
+
+@pytest.mark.parametrize("alpha,gb", [(1.0, 33.8), (0.5, 24.2), (0.25, 19.3), (0.125, 16.9)])
+def test_hbm_bytes_match_survey_table(alpha, gb):
+    """SURVEY 8(d) cfg 2 algorithmic HBM bytes 33.8 / 24.2 / 19.3 / 16.9 GB: (12 + 16 alpha) B per
+    parameter with fp32 G, plus the bf16 workspace traffic of X and O (4 B per selected
+    element) that the per-phase accounting also charges."""
+    _, b = bench.work_model(layer_set_1b(24), alpha, fused=False)
+    n = 1_207_959_552
+    k1 = b["momentum_score"] + b["momentum_score_mt"]
+    assert abs(k1 - 12 * n) / (12 * n) < 1e-3                     # + 4 d per matrix of scores
+    sel = sum(v for k, v in b.items() if k.startswith(("gather", "scatter")))
+    assert abs(sel - 20 * alpha * n) / (20 * alpha * n) < 1e-9     # 10 B in + 10 B out per selected element
+    assert abs((k1 + sel - 4 * alpha * n) / 1e9 - gb) < 0.1
+
+
+def test_fused_accounting_moves_bytes_not_adds():
+    """The opt-in fused pre-stage reports K1 + gather bytes of its matrices under one phase."""
+    s = layer_set_1b(24)
+    _, a = bench.work_model(s, 0.25, fused=False)
+    _, b = bench.work_model(s, 0.25, fused=True)
+    assert abs(sum(a.values()) - sum(b.values())) < 1.0
+    assert b["pre_fused"] > 0 and b["momentum_score"] < a["momentum_score"]
+
+
+def test_stress_config_shapes():
+    """configs[4]: 4096 x 32768 (rows mode, k = 256) and 28672 x 8192 (cols mode, k = 512) at
+    alpha = 1/16; 43.1 and 151.7 GFLOP of NS (direct count)."""
+    shapes = bench.model_shapes("stress")
+    assert shapes == [(4096, 32768), (28672, 8192)]
+    f0, _ = bench.work_model(shapes[:1], 0.0625, ns_form="direct", fused=False)
+    f1, _ = bench.work_model(shapes[1:], 0.0625, ns_form="direct", fused=False)
+    assert abs(sum(f0.values()) / 1e9 - 43.1) < 0.1 and abs(sum(f1.values()) / 1e9 - 151.7) < 0.1
