@@ -38,10 +38,14 @@ def test_gram_form_flops_closed_form():
     want = sum(4 * p * p * q + (4 * T - 3) * 2 * p ** 3 for q in [2048] * 96 + [8192] * 48)
     assert abs(sum(f.values()) - want) < 1e3
     assert abs(sum(f.values()) / 1e12 - 1.28) < 0.005  # DESIGN 6: 1.28 TFLOP in Gram form (2.6x fewer)
-    # alpha = 1: q = p, the direct form everywhere
-    f1, _ = bench.work_model(layer_set_1b(24), 1.0, ns_form="auto", fused=False)
-    fd, _ = bench.work_model(layer_set_1b(24), 1.0, ns_form="direct", fused=False)
+    # alpha = 1: the square matrices have q = p (direct form), the 2048 x 8192 ones q = 4p (Gram)
+    sq = [(2048, 2048)] * 96
+    f1, _ = bench.work_model(sq, 1.0, ns_form="auto", fused=False)
+    fd, _ = bench.work_model(sq, 1.0, ns_form="direct", fused=False)
     assert sum(f1.values()) == sum(fd.values())
+    rect = [(8192, 2048), (2048, 8192)]
+    fa, _ = bench.work_model(rect, 1.0, ns_form="auto", fused=False)
+    assert sum(fa.values()) == 2 * (4 * 2048 ** 2 * 8192 + 17 * 2 * 2048 ** 3)
 
 
 @pytest.mark.parametrize("alpha,gb", [(1.0, 33.8), (0.5, 24.2), (0.25, 19.3), (0.125, 16.9)])
