@@ -79,3 +79,20 @@ def test_stress_config_shapes():
     f0, _ = bench.work_model(shapes[:1], 0.0625, ns_form="direct", fused=False)
     f1, _ = bench.work_model(shapes[1:], 0.0625, ns_form="direct", fused=False)
     assert abs(sum(f0.values()) / 1e9 - 43.1) < 0.1 and abs(sum(f1.values()) / 1e9 - 151.7) < 0.1
+
+
+def test_reference_arm_json_contract():
+    """`bench.py --impl reference` (the fp64 oracle on the host cores, one layer per step,
+    scaled to the model) prints one JSON line with the contract's keys, no GPU needed."""
+    import json
+    import subprocess
+    r = subprocess.run([sys.executable, os.path.join(ROOT, "bench.py"), "--impl", "reference", "--steps", "1",
+                        "--warmup", "0"], capture_output=True, text=True, timeout=600, cwd=ROOT)
+    assert r.returncode == 0, r.stderr
+    line = json.loads(r.stdout.strip().splitlines()[-1])
+    for key in ("impl", "metric", "value", "unit", "n_gpus", "steps", "warmup", "higher_is_better", "config",
+                "cpu_baseline", "e2e"):
+        assert key in line, key
+    assert line["impl"] == "reference" and line["higher_is_better"] is False and line["unit"] == "ms/step"
+    assert line["cpu_baseline"]["kind"] == "oracle" and line["cpu_baseline"]["cores"] >= 1
+    assert line["e2e"]["h2d_bytes_per_step"] == 0 and line["value"] > 0
