@@ -118,6 +118,26 @@ def work_model(shapes, alpha, steps=5, mt=False, ns_form="auto", fused=None):
     return ns_flops, byts
 
 
+def mma_flops(shapes, alpha, steps=5, ns_form="auto"):
+    """FLOPs the tensor cores actually execute per step: padded dims (p_pad, q_pad multiples of
+    256) and, for the symmetric products (gram, poly, Gram-space p x p products), only the
+    upper-triangle 256 x 256 tiles: T(T+1)/2 of T^2 with T = p_pad / 256.  The apply is a full
+    product.  (work_model's counts are unpadded full products.)"""
+    pad = lambda v: (v + 255) // 256 * 256  # noqa: E731
+    tot = 0.0
+    for (m, n) in shapes:
+        d, o = (m, n) if m <= n else (n, m)
+        k = max(1, min(d, int(math.floor(alpha * d + 0.5))))
+        p, q = pad(min(k, o)), pad(max(k, o))
+        T = p // 256
+        sym = T * (T + 1) / 2 / (T * T)
+        if ns_uses_gram_form(min(k, o), max(k, o), ns_form):
+            tot += sym * 2.0 * p * p * q + 2.0 * p * p * q + sym * (steps + max(0, 3 * steps - 3)) * 2.0 * p ** 3
+        else:
+            tot += steps * (sym * 2.0 * p * p * q + sym * 2.0 * p ** 3 + 2.0 * p * p * q)
+    return tot
+
+
 class ClockSampler:
     """nvidia-smi clocks / throttle reasons sampled DURING the timed region."""
 
@@ -384,6 +404,7 @@ def run_ours(args):
     owned_shapes = shapes if not use_dist else [s for s, o in zip(shapes, info["owner"]) if o == rank]
     ns_std = sum(work_model(owned_shapes, args.alpha, ns_form="direct")[0].values()) if owned_shapes else 0.0
     ns_std_tflops = ns_std / (ns_ms * 1e-3) / 1e12 if ns_ms > 0 else 0.0
+    ns_mma = mma_flops(owned_shapes, args.alpha, ns_form=args.ns_form) if owned_shapes else 0.0
     # dominant kernel (largest per-step device time)
     dom = max(per_phase, key=lambda p: per_phase[p]["ms_per_step"])
     de = per_phase[dom]
@@ -517,10 +538,14 @@ def run_ours(args):
             "configs1_sweep": sweep,
             "speedup_vs_alpha1": (ms_a1 / ms) if ms_a1 else None,
             "ns_tflops": ns_tflops,
-            "ns_tflops_note": "executed form's FLOPs (Gram space: 4p^2q + (4T-3)2p^3 per matrix, full products) "
+            "ns_tflops_note": "the evaluated form's FLOPs (Gram space: 4p^2q + (4T-3)2p^3 per matrix, full products) "
                               "over the NS kernels' time",
             "ns_frac_bf16_burst": ns_tflops / peaks["bf16_tflops"],
             "ns_frac_bf16_sustained": ns_tflops / peaks["bf16_tflops_sustained"],
+            "ns_mma_tflops": ns_mma / (ns_ms * 1e-3) / 1e12 if ns_ms > 0 else 0.0,
+            "ns_mma_frac_bf16_burst": (ns_mma / (ns_ms * 1e-3) / 1e12 / peaks["bf16_tflops"]) if ns_ms > 0 else 0.0,
+            "ns_mma_note": "FLOPs the tensor cores execute (padded dims, upper-triangle tiles of the symmetric "
+                           "products) over the NS kernels' time",
             "ns_standard_tflop_per_step": ns_std / 1e12,
             "ns_standard_equiv_tflops": ns_std_tflops,
             "ns_standard_equiv_frac_bf16_burst": ns_std_tflops / peaks["bf16_tflops"],

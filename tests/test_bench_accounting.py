@@ -96,3 +96,13 @@ def test_reference_arm_json_contract():
     assert line["impl"] == "reference" and line["higher_is_better"] is False and line["unit"] == "ms/step"
     assert line["cpu_baseline"]["kind"] == "oracle" and line["cpu_baseline"]["cores"] >= 1
     assert line["e2e"]["h2d_bytes_per_step"] == 0 and line["value"] > 0
+
+
+def test_mma_flops_credit_only_the_computed_tiles():
+    """Tensor-core work: p = 512 -> 2 x 2 tiles of 256, 3 upper tiles computed for the symmetric
+    products (gram, poly, p x p products); the apply is a full product."""
+    f = bench.mma_flops([(2048, 2048)], 0.25)           # X 512 x 2048, Gram form
+    p, q, T = 512, 2048, 5
+    want = 0.75 * 2 * p * p * q + 2 * p * p * q + 0.75 * (T + 3 * T - 3) * 2 * p ** 3
+    assert f == want
+    assert abs(bench.mma_flops(layer_set_1b(24), 0.25) / 1e12 - 1.034) < 0.001
