@@ -28,6 +28,13 @@
  *    as void*; NULL = legacy default stream).  No host synchronisation
  *    happens inside a step.  Calls that touch the same matrices must not
  *    overlap.  The workspace may not be shared by concurrent calls.
+ *  - CUDA graphs: after a plan's first step, a step on the SAME matrix
+ *    pointers enqueues only kernels and memsets (no allocation, no host copy)
+ *    and may be captured.  The plan's descriptor table holds the pointers of
+ *    its latest eager step, so graphs of different pointer sets need distinct
+ *    plans: pass distinct workspace base pointers (the plan cache is keyed by
+ *    it; the Python Dion2(cuda_graph=True) offsets the base by 4 KiB per set).
+ *    The tensor-core NS kernels use programmatic dependent launch.
  *  - Return value: a dion2_status code.  Codes 1-4 are detected on the host
  *    before anything is enqueued.  Non-finite scores are detected on the
  *    device: that matrix's W and M[K] writes are skipped and
