@@ -286,14 +286,26 @@ def e2e_run(opt, Ws, Ms, Gs, G_flat, steps, ks):
         sel_views.append(sel_dev[off:off + k])
         off += k
     sel_host = torch.empty(sum(ks), dtype=torch.int32, pin_memory=True)
-    opt.step(Ws, Ms, Gs, sel_out=sel_views)  # untimed: plan (and, in graph mode, the capture) for this call
+    # per-matrix views of the pinned host buffer (the user's host gradients)
+    host_views, off = [], 0
+    for g in Gs:
+        host_views.append(host_G[off:off + g.numel()].view(g.shape))
+        off += g.numel()
+    pipelined = hasattr(opt, "step_host")
+    if pipelined:  # untimed: plans (and, in graph mode, the captures) for this call
+        opt.step_host(Ws, Ms, Gs, host_views, sel_out=sel_views)
+    else:
+        opt.step(Ws, Ms, Gs, sel_out=sel_views)
     torch.cuda.synchronize()
     s = torch.cuda.current_stream()
     e0, e1 = torch.cuda.Event(enable_timing=True), torch.cuda.Event(enable_timing=True)
     e0.record(s)
     for _ in range(steps):
-        G_flat.copy_(host_G, non_blocking=True)
-        opt.step(Ws, Ms, Gs, sel_out=sel_views)
+        if pipelined:  # host-to-device upload chunk by chunk, overlapped with the earlier chunks' steps
+            opt.step_host(Ws, Ms, Gs, host_views, sel_out=sel_views)
+        else:
+            G_flat.copy_(host_G, non_blocking=True)
+            opt.step(Ws, Ms, Gs, sel_out=sel_views)
         sel_host.copy_(sel_dev, non_blocking=True)
     e1.record(s)
     torch.cuda.synchronize()
@@ -559,7 +571,7 @@ def run_ours(args):
             "roofline": roof,
             "cpu_baseline": cpu,
             "e2e": {"value": e2e_ms, "unit": "ms/step", "h2d_bytes_per_step": h2d, "d2h_bytes_per_step": d2h,
-                    "what": "pinned host G -> device, dion2_step_batched, selected indices -> host, every step"},
+                    "what": "pinned host G -> device (Dion2.step_host: 4 chunks, upload overlapped with the earlier chunks' steps), dion2_step_batched per chunk, selected indices -> host, every step"},
             "gpu_launches": launches,
             "comm": comm,
             "clocks": clk.summary(),

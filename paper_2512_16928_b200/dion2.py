@@ -235,6 +235,7 @@ class Dion2:
 
     def step(self, Ws, Ms, Gs, sel_out=None, O_out=None, stream: Optional[torch.cuda.Stream] = None,
              m_transposed=None, storage_transposed=None, **override):
+        self._last_sub = None
         if self.cuda_graph and stream is None:
             ptrs = lambda ts: tuple((t.data_ptr(), tuple(t.shape), tuple(t.stride()), t.dtype) if t is not None  # noqa: E731
                                     else None for t in ts)
@@ -285,7 +286,62 @@ class Dion2:
         if rc:
             raise Dion2Error(rc, "dion2_step_batched")
 
+    def step_host(self, Ws, Ms, Gs, G_host, sel_out=None, chunks: int = 4):
+        """One optimizer step whose gradients arrive from the host: G_host[i] is a pinned CPU
+        tensor copied into the device buffer Gs[i].  The matrices are split into `chunks`
+        contiguous groups of about equal parameter count; a side stream copies group c + 1
+        while group c steps on the current stream, so the step hides under the host-to-device
+        transfer.  Each group is its own batched library call (its own plan and workspace)."""
+        n = len(Ws)
+        if not (len(Ms) == n and len(Gs) == n and len(G_host) == n):
+            raise ValueError("Ws, Ms, Gs, G_host must be equally long")
+        for g, h in zip(Gs, G_host):
+            if h.is_cuda or h.shape != g.shape or h.dtype != g.dtype:
+                raise ValueError("G_host[i] must be a CPU tensor shaped and typed like Gs[i]")
+        sizes = [w.numel() for w in Ws]
+        total, bounds, acc, c0 = sum(sizes), [], 0, 0
+        chunks = max(1, min(chunks, n))
+        for i, sz in enumerate(sizes):
+            acc += sz
+            if len(bounds) < chunks - 1 and acc * chunks >= total * (len(bounds) + 1) and i + 1 < n:
+                bounds.append((c0, i + 1))
+                c0 = i + 1
+        bounds.append((c0, n))
+        key = tuple(bounds)
+        if getattr(self, "_host_key", None) != key:
+            mt = self.m_transposed
+            self._host_subs = [Dion2(m_transposed=list(mt[a:b]) if mt is not None else None,
+                                     storage_transposed=list(self.storage_transposed[a:b])
+                                     if self.storage_transposed is not None else None,
+                                     cuda_graph=self.cuda_graph, **self.cfg_kw) for (a, b) in bounds]
+            self._host_key = key
+            self._copy_stream = torch.cuda.Stream(device=Ws[0].device)
+        for sub in self._host_subs:  # the config may have changed since the subs were made
+            sub.cfg_kw = dict(self.cfg_kw)
+        cur = torch.cuda.current_stream(Ws[0].device)
+        cs = self._copy_stream
+        cs.wait_stream(cur)  # the previous step has finished reading the G buffers
+        events = []
+        with torch.cuda.stream(cs):
+            for (a, b) in bounds:
+                for i in range(a, b):
+                    Gs[i].copy_(G_host[i], non_blocking=True)
+                ev = torch.cuda.Event()
+                ev.record(cs)
+                events.append(ev)
+        for (a, b), ev, sub in zip(bounds, events, self._host_subs):
+            cur.wait_event(ev)
+            sub.step(Ws[a:b], Ms[a:b], Gs[a:b], sel_out=list(sel_out[a:b]) if sel_out is not None else None)
+        self._last_sub = self._host_subs
+
     def status(self) -> Tuple[int, int]:
+        if getattr(self, "_last_sub", None):
+            worst, bad = 0, -1
+            for sub, (a, _) in zip(self._last_sub, self._host_key):
+                rc, b = sub.status()
+                if rc and bad < 0:
+                    worst, bad = rc, a + b
+            return worst, bad
         bad = ctypes.c_int32(-1)
         ws = self._ws.data_ptr() + getattr(self, "_last_slot", 0) * self.SLOT_BYTES if self._ws is not None else None
         rc = _lib().dion2_get_status(ws, ctypes.byref(bad))

@@ -364,6 +364,46 @@ def test_cuda_graph_mode_equals_eager():
         assert torch.equal(a, b)
 
 
+@pytest.mark.parametrize("graph", [False, True])
+def test_step_host_pipelined_upload(graph):
+    """Dion2.step_host: gradients from pinned host buffers, uploaded chunk by chunk on a side
+    stream while earlier chunks step; same selections and M as the one-call step, dW within
+    the bf16 rounding of a different split-K/batching (each chunk is its own batched call)."""
+    shapes = [(512, 1024), (2048, 512), (300, 520), (1024, 1024), (512, 2048), (256, 128)]
+    mt = [m > n for (m, n) in shapes]
+    ks = [max(1, int(0.25 * (m if m <= n else n) + 0.5)) for (m, n) in shapes]
+    def init():
+        Ws = [torch.from_numpy(gen_w0(m, n, 9, i)).cuda() for i, (m, n) in enumerate(shapes)]
+        Ms = [torch.zeros(n, m, device="cuda") if t else torch.zeros(m, n, device="cuda")
+              for (m, n), t in zip(shapes, mt)]
+        return Ws, Ms
+    Gh = [[torch.from_numpy(gen_grad(m, n, 9, i, t, row_scaled=True)).pin_memory() for i, (m, n) in enumerate(shapes)]
+          for t in range(3)]
+    W0, _ = init()
+    Wa, Ma = init()
+    Ga = [torch.empty(m, n, device="cuda") for (m, n) in shapes]
+    sa = [torch.empty(k, dtype=torch.int32, device="cuda") for k in ks]
+    ref = Dion2(alpha=0.25, m_transposed=mt)
+    Wb, Mb = init()
+    Gb = [torch.empty(m, n, device="cuda") for (m, n) in shapes]
+    sb = [torch.empty(k, dtype=torch.int32, device="cuda") for k in ks]
+    opt = Dion2(alpha=0.25, m_transposed=mt, cuda_graph=graph)
+    for t in range(3):
+        for g, h in zip(Ga, Gh[t]):
+            g.copy_(h)
+        ref.step(Wa, Ma, Ga, sel_out=sa)
+        opt.step_host(Wb, Mb, Gb, Gh[t], sel_out=sb, chunks=3)
+        torch.cuda.synchronize()
+        for x, y in zip(sa, sb):
+            assert torch.equal(x, y)
+    assert opt.status() == (0, -1)
+    for a, b, w0 in zip(Wa, Wb, W0):
+        da, db = (a - w0).double(), (b - w0).double()
+        assert (da - db).norm() <= 1e-2 * da.norm()
+    for a, b in zip(Ma, Mb):
+        assert (a - b).abs().max() <= 1e-6 * a.abs().max()
+
+
 def test_bitwise_determinism():
     shapes = [(512, 1024), (1024, 512)]
     outs = []
