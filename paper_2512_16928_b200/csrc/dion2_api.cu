@@ -1068,10 +1068,28 @@ void stage_gather(Plan& P, const dion2_config* c, void* ws, Launcher& L, cudaStr
     L.end();
   }
   if (P.fl_gn[0]) {
+    // TMA-staged rows gather when every listed matrix has 16-B aligned rows with n % 8 == 0
+    // (DION2_GATHER_TMA=0: the register-streaming kernel; =4/6: ring stages; 6 = 0.496 ms vs
+    // 0.500 for the register kernel on the 1B set, 4 = 0.52)
+    const char* ge = getenv("DION2_GATHER_TMA");
+    const int gstages = ge ? atoi(ge) : 6;
+    bool tma = gstages != 0;
+    const MatDesc* hd = reinterpret_cast<const MatDesc*>(P.host_tables.data());
+    const int32_t* lm = reinterpret_cast<const int32_t*>(P.host_tables.data() + (P.off_flg_mats[0] - P.off_desc));
+    for (int j = 0; j < P.fl_gn[0] && tma; ++j) {
+      const MatDesc& m = hd[lm[j]];
+      tma = m.vec4 && ((m.mt ? m.rows : m.cols) % 8 == 0) && (!m.mt || m.ldm % 4 == 0);
+    }
     L.begin(PH_GATHER_ROWS);
-    launch_gather_rows(stream_grid(ceil_div(P.fl_gunits[0], 8), 8, persistent), s, dmats,
-                       (const int32_t*)tab(P, P.off_flg_mats[0]), (const int32_t*)tab(P, P.off_fl_gprefix[0]),
-                       P.fl_gn[0], P.fl_gunits[0], bad, c->mu);
+    if (tma) {
+      launch_gather_rows_tma(gstages, 16, s, dmats, (const int32_t*)tab(P, P.off_flg_mats[0]),
+                             (const int32_t*)tab(P, P.off_fl_gprefix[0]), P.fl_gn[0], P.fl_gunits[0], bad, c->mu,
+                             g_sm_count > 0 ? g_sm_count : 148);
+    } else {
+      launch_gather_rows(stream_grid(ceil_div(P.fl_gunits[0], 8), 8, persistent), s, dmats,
+                         (const int32_t*)tab(P, P.off_flg_mats[0]), (const int32_t*)tab(P, P.off_fl_gprefix[0]),
+                         P.fl_gn[0], P.fl_gunits[0], bad, c->mu);
+    }
     L.end();
   }
   if (P.fl_gn[1]) {

@@ -63,6 +63,9 @@ size_t cols_t_smem_bytes(int k, int mask_words);
 void launch_fast_paths_attrs();
 void launch_gather_rows(int blocks, cudaStream_t s, const MatDesc* mats, const int32_t* lm, const int32_t* lp, int nl,
                         int units, const int32_t* bad, float mu);
+// TMA-staged rows gather (k_gather_tma.cu): 16-B aligned rows, n % 8 == 0; stages 4 or 6
+void launch_gather_rows_tma(int stages, int blocks_per_sm_cap, cudaStream_t s, const MatDesc* mats, const int32_t* lm,
+                            const int32_t* lp, int nl, int units, const int32_t* bad, float mu, int sms);
 void launch_scatter_rows(int blocks, cudaStream_t s, const MatDesc* mats, const int32_t* lm, const int32_t* lp, int nl,
                          int units, const int32_t* bad, float lr);
 // max_k / max_n: largest k and column count over the matrices of the list (sizes the smem)
