@@ -228,6 +228,17 @@ def test_pipelined_transposed_k1(grad_bf16, stages, monkeypatch):
     _assert(run_parity(shapes, 0.25, "auto", "bf16", steps=3, m_transposed=True, grad_bf16=grad_bf16), BF16_TOL)
 
 
+@pytest.mark.parametrize("stages", ["0", "4", "6"])
+def test_tma_staged_rows_gather(stages, monkeypatch):
+    """K3 rows path: the TMA-staged bulk-copy ring (4 / 6 stages) and the register-streaming
+    fallback ("0"); rows of M and of M^T, multi-chunk rows (8192 > 2048), ragged k with zero
+    X rows (k = 75 of p_pad = 256), bf16 gradients."""
+    monkeypatch.setenv("DION2_GATHER_TMA", stages)
+    shapes = [(512, 8192), (8192, 1024), (300, 520), (1024, 2048)]
+    _assert(run_parity(shapes, 0.25, "auto", "bf16", steps=3, m_transposed=True, row_scaled=True), BF16_TOL)
+    _assert(run_parity(shapes[:2], 0.25, "auto", "bf16", steps=2, grad_bf16=True), BF16_TOL)
+
+
 def test_full_decay_ablation_fp32():
     _assert(run_parity([(96, 160)], 0.25, "auto", "fp32", steps=3, decay_mode=1), FP32_TOL)
 
