@@ -76,6 +76,22 @@ bool make_map(CUtensorMap* m, const void* base, int64_t cols, int64_t rows, int6
   return r == CUDA_SUCCESS;
 }
 
+// 3-D bf16 tensor map over `count` row-major [rows][cols] arrays spaced zstride_bytes apart
+// (the distributed step's rank pieces: piece size rounded up to 256 B).
+bool make_map_strided(CUtensorMap* m, const void* base, int64_t cols, int64_t rows, int64_t count,
+                      int64_t zstride_bytes, int box_cols, int box_rows, CUtensorMapSwizzle swz) {
+  auto enc = get_encode_fn();
+  if (!enc) return false;
+  cuuint64_t dims[3] = {(cuuint64_t)cols, (cuuint64_t)rows, (cuuint64_t)count};
+  cuuint64_t strides[2] = {(cuuint64_t)(cols * 2), (cuuint64_t)zstride_bytes};
+  cuuint32_t box[3] = {(cuuint32_t)box_cols, (cuuint32_t)box_rows, 1};
+  cuuint32_t estr[3] = {1, 1, 1};
+  CUresult r = enc(m, CU_TENSOR_MAP_DATA_TYPE_BFLOAT16, 3, const_cast<void*>(base), dims, strides, box, estr,
+                   CU_TENSOR_MAP_INTERLEAVE_NONE, swz, CU_TENSOR_MAP_L2_PROMOTION_L2_256B,
+                   CU_TENSOR_MAP_FLOAT_OOB_FILL_NONE);
+  return r == CUDA_SUCCESS;
+}
+
 std::vector<dion2_matrix> storage_view(const dion2_matrix* mats, int n) {
   std::vector<dion2_matrix> v(mats, mats + n);
   for (auto& m : v)
@@ -150,7 +166,7 @@ std::string plan_key(const dion2_matrix* mats, int n, const dion2_config* c, voi
 std::string env_key() {
   std::string k;
   for (const char* v : {"DION2_NS_PAIR", "DION2_NS_SYM", "DION2_NS_CHAIN", "DION2_NS_SERPENTINE", "DION2_NS_UPPER",
-                        "DION2_PRE_FUSE", "DION2_FUSE_LAG_MB", "DION2_GRAM_SPLITK"}) {
+                        "DION2_PRE_FUSE", "DION2_FUSE_LAG_MB", "DION2_GRAM_SPLITK", "DION2_DIST_INPLACE"}) {
     const char* e = getenv(v);
     k.append(e ? e : "-");
     k.push_back('|');

@@ -88,7 +88,7 @@ struct DistPlan {
   // streaming lists: gather and scatter membership differ for transposed-M column matrices
   // (row gather on M^T, column scatter on W)
   size_t t_desc, t_rowmats, t_rowprefix, t_colmats, t_colprefix, t_mtmats, t_mtprefix, t_allcols, t_flgm[2],
-      t_flsm[2], t_flg[2], t_fls[2], t_gidx, t_roff, t_gprefix;
+      t_flsm[2], t_flg[2], t_fls[2], t_gidx, t_roff, t_gprefix, t_inpl = 0, t_pmaps = 0;
   int n_row_mats = 0, n_col_mats = 0, n_mt_mats = 0, n_allcols = 0, fl_gn[2] = {0, 0}, fl_sn[2] = {0, 0},
       fl_gunits[2] = {0, 0}, fl_sunits[2] = {0, 0}, fl_maxk = 0, max_d = 0, total_gather_tiles = 0;
   int64_t total_rows = 0, total_col_tiles = 0, total_mt_tiles = 0, max_cols_col = 0;
@@ -161,14 +161,32 @@ int resolve(DistPlan& D, const dion2_shard* sh, int n, const dion2_config* c, in
   // send sections (by owner) and my recv section size
   D.sdispl.assign(world, 0);
   D.scount.assign(world, 0);
+  // Inside an owner's section the pieces are grouped by the owner plan's NS shape groups
+  // ((p_pad, q_pad) in first-appearance order, members in index order), so a group's pieces
+  // from one rank form a uniform [matrix][k][qo] array the owner's NS kernels can address with
+  // one tensor map per rank (in-place pieces, build_tables).  Shapes only: same on every rank.
   int64_t run = 0;
   for (int o = 0; o < world; ++o) {
     D.sdispl[o] = run;
+    std::vector<int> mine;
+    std::vector<std::pair<int64_t, int64_t>> keys;
+    std::vector<int> key_of;
     for (int j = 0; j < n; ++j)
       if (D.dm[j].owner == o) {
-        D.dm[j].soff = run - D.sdispl[o];
-        run += D.dm[j].piece;
+        const std::pair<int64_t, int64_t> key((int64_t)align_up(D.dm[j].k, 256), (int64_t)align_up(D.dm[j].o, 256));
+        int ki = (int)(std::find(keys.begin(), keys.end(), key) - keys.begin());
+        if (ki == (int)keys.size()) keys.push_back(key);
+        mine.push_back(j);
+        key_of.push_back(ki);
       }
+    std::vector<int> ord(mine.size());
+    std::iota(ord.begin(), ord.end(), 0);
+    std::stable_sort(ord.begin(), ord.end(), [&](int a, int b) { return key_of[a] < key_of[b]; });
+    for (int t : ord) {
+      const int j = mine[t];
+      D.dm[j].soff = run - D.sdispl[o];
+      run += D.dm[j].piece;
+    }
     D.scount[o] = run - D.sdispl[o];
   }
   D.R = D.scount[rank];
@@ -246,6 +264,9 @@ int build_tables(DistPlan& D, const dion2_config* c, void* ws) {
   D.t_gprefix = take(4 * (size_t)n);
   D.t_gidx = take(4 * std::max<size_t>(1, D.owned.size()));
   D.t_roff = take(8 * std::max<size_t>(1, D.owned.size()) * P);
+  D.t_inpl = take(4 * std::max<size_t>(1, D.owned.size()));
+  const size_t n_owner_groups = D.owner ? D.owner->groups.size() : 0;
+  D.t_pmaps = take(sizeof(CUtensorMap) * std::max<size_t>(1, n_owner_groups * 3 * (size_t)P));
   D.htab.assign(off, 0);
   if (!D.dtab && cudaMalloc(&D.dtab, off) != cudaSuccess) return DION2_ECUDA;
   auto H = [&](size_t o) { return D.htab.data() + o; };
@@ -379,12 +400,10 @@ int build_tables(DistPlan& D, const dion2_config* c, void* ws) {
     if (rc) return rc;
     std::vector<int32_t> gidx(D.owned.size());
     std::vector<int64_t> roff(D.owned.size() * P);
-    int64_t acc = 0;
     for (size_t i = 0; i < D.owned.size(); ++i) {
       const DistMat& q = D.dm[D.owned[i]];
       gidx[i] = D.owned[i];
-      for (int r = 0; r < P; ++r) roff[i * P + r] = acc;
-      acc += q.piece;
+      for (int r = 0; r < P; ++r) roff[i * P + r] = q.soff;
       D.max_p_pad = std::max(D.max_p_pad, D.owner->mp[i].p_pad);
       D.max_k_owned = std::max(D.max_k_owned, q.k);
       // the owner's NS runs on the global orientation: X = k x o (k <= o)
@@ -392,6 +411,58 @@ int build_tables(DistPlan& D, const dion2_config* c, void* ws) {
     }
     memcpy(H(D.t_gidx), gidx.data(), 4 * gidx.size());
     memcpy(H(D.t_roff), roff.data(), 8 * roff.size());
+    // In-place pieces: a Gram-space owner group whose q is a whole number of 256-column tiles
+    // and of 64-column k-blocks per rank piece (q_pad == q, qo % 64 == 0, P <= 8) has its gram
+    // and apply read X0 straight from the received pieces and its apply write X_T straight into
+    // the outgoing pieces (no assemble / disassemble copies).  DION2_DIST_INPLACE=0 disables.
+    std::vector<int32_t> inpl(D.owned.size(), 0);
+    const char* ie = getenv("DION2_DIST_INPLACE");
+    const bool inplace_on = !(ie && ie[0] == '0') && P <= kMaxPieceRanks;
+    CUtensorMap* hmaps = reinterpret_cast<CUtensorMap*>(H(D.t_pmaps));
+    std::vector<int> g_ok(D.owner->groups.size(), 0);
+    for (size_t gi = 0; gi < D.owner->groups.size() && inplace_on; ++gi) {
+      const Group& g = D.owner->groups[gi];
+      if (!g.gs) continue;
+      const DistMat& q0 = D.dm[D.owned[g.mats[0]]];
+      bool ok = true;
+      for (size_t zi = 0; zi < g.mats.size() && ok; ++zi) {
+        const DistMat& q = D.dm[D.owned[g.mats[zi]]];
+        ok = q.o == g.q_pad && q.qo % 64 == 0 && q.k == q0.k && q.qo == q0.qo && q.piece == q0.piece &&
+             q.soff == q0.soff + (int64_t)zi * q0.piece;
+      }
+      if (!ok) continue;
+      for (int r = 0; r < P; ++r) {
+        uint8_t* rb = static_cast<uint8_t*>(at(ws, D.off_recv)) + (int64_t)r * D.R + q0.soff;
+        uint8_t* sb = static_cast<uint8_t*>(at(ws, D.off_osend)) + (int64_t)r * D.R + q0.soff;
+        CUtensorMap* m = hmaps + gi * 3 * P;
+        if (!make_map_strided(&m[r], rb, q0.qo, q0.k, g.count, q0.piece, 64, 128, CU_TENSOR_MAP_SWIZZLE_128B) ||
+            !make_map_strided(&m[P + r], rb, q0.qo, q0.k, g.count, q0.piece, 64, 64, CU_TENSOR_MAP_SWIZZLE_128B) ||
+            !make_map_strided(&m[2 * P + r], sb, q0.qo, q0.k, g.count, q0.piece, 32, 32, CU_TENSOR_MAP_SWIZZLE_64B))
+          return DION2_ECUDA;
+      }
+      g_ok[gi] = 1;
+      for (int i : g.mats) inpl[i] = 1;
+    }
+    // point the owner plan's gram (A = B = X0) and apply (B = X0, D = X_T) launches at the pieces
+    for (Launch& ln : D.owner->ns_launches) {
+      if (ln.phase != PH_GRAM && ln.phase != PH_APPLY) continue;
+      for (int j = 0; j < ln.tc.p.ngroups; ++j) {
+        NsGroup& G = ln.tc.p.g[j];
+        for (size_t gi = 0; gi < D.owner->groups.size(); ++gi) {
+          if (!g_ok[gi]) continue;
+          const void* x0 = at(at(ws, D.off_owner), D.owner->groups[gi].off_X0);
+          const bool hit = ln.phase == PH_GRAM ? G.a == x0 : G.b == x0;
+          if (!hit) continue;
+          const DistMat& q0 = D.dm[D.owned[D.owner->groups[gi].mats[0]]];
+          G.pieces_qo = q0.qo;
+          G.pieces_P = P;
+          G.pieces_map = (int)(gi * 3 * P);
+          for (int k = 0; k < 3 * P; ++k) ln.tc.mapP[j][k] = hmaps[gi * 3 * P + k];
+        }
+      }
+    }
+    memcpy(H(D.t_inpl), inpl.data(), 4 * inpl.size());
+    D.ptab.inplace = (const int32_t*)dt(D, D.t_inpl);
     D.ptab.gidx = (const int32_t*)dt(D, D.t_gidx);
     D.ptab.roff = (const int64_t*)dt(D, D.t_roff);
     D.ptab.rstride = D.R;

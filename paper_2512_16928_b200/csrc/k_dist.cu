@@ -61,7 +61,9 @@ __global__ void k_assemble_pieces(const MatDesc* __restrict__ omats, PieceTable 
   if (i >= md.p_pad) return;
   const int qo = md.q / T.world;
   __nv_bfloat16* xrow = reinterpret_cast<__nv_bfloat16*>(md.X0) + (int64_t)i * md.q_pad;
-  if (i < md.k) {
+  if (T.inplace[jj]) {
+    // the NS kernels read the pieces in place: only the norm below
+  } else if (i < md.k) {
     for (int r = 0; r < T.world; ++r) {
       const __nv_bfloat16* src = reinterpret_cast<const __nv_bfloat16*>(recv + r * T.rstride + T.roff[jj * T.world + r]) +
                                  (int64_t)i * qo;
@@ -88,7 +90,7 @@ __global__ void k_disassemble_pieces(const MatDesc* __restrict__ omats, PieceTab
   const int jj = blockIdx.y;
   const MatDesc& md = omats[jj];
   const int i = blockIdx.x;
-  if (i >= md.k) return;
+  if (i >= md.k || T.inplace[jj]) return;  // in place: the apply wrote the pieces itself
   const int qo = md.q / T.world;
   const __nv_bfloat16* xrow =
       reinterpret_cast<const __nv_bfloat16*>(md.final_in_x1 ? md.X1 : md.X0) + (int64_t)i * md.q_pad;

@@ -111,6 +111,14 @@ __global__ void __launch_bounds__(192, 1) k_ns_gemm_tc(const __grid_constant__ N
           tma_load_3d(sa, &P.mapA[c.group], &full_bar[stage], kb * kBK, c.tm * kBM, c.z);
           if (p.b_kmajor) {
             tma_load_3d(sb, &P.mapB[c.group], &full_bar[stage], kb * kBK, c.tn * BN, c.z);
+          } else if (G.pieces_qo) {
+            // distributed owner apply: the N axis (q) of X0 runs over the P rank pieces
+#pragma unroll
+            for (int j = 0; j < BN / 64; ++j) {
+              const int nn = c.tn * BN + j * 64, pr = nn / G.pieces_qo;
+              tma_load_3d(sb + j * 64 * kBK * 2, &P.mapP[c.group][G.pieces_P + pr], &full_bar[stage],
+                          nn - pr * G.pieces_qo, kb * kBK, c.z);
+            }
           } else {
 #pragma unroll
             for (int j = 0; j < BN / 64; ++j)
@@ -223,7 +231,15 @@ __global__ void __launch_bounds__(192, 1) k_ns_gemm_tc(const __grid_constant__ N
         fence_proxy_async_smem();
         __syncwarp();
         if (lane == 0) {
-          tma_store_3d(&P.mapD[c.group], buf, c.tn * BN + cc32 * 32, c.tm * kBM + lg * 32, c.z);
+          const NsGroup& Gs = p.g[c.group];
+          const int col = c.tn * BN + cc32 * 32;
+          if (Gs.pieces_qo) {  // X_T straight into the rank pieces of the exchange buffer
+            const int pr = col / Gs.pieces_qo;
+            tma_store_3d(&P.mapP[c.group][2 * Gs.pieces_P + pr], buf, col - pr * Gs.pieces_qo,
+                         c.tm * kBM + lg * 32, c.z);
+          } else {
+            tma_store_3d(&P.mapD[c.group], buf, col, c.tm * kBM + lg * 32, c.z);
+          }
           bulk_commit();
         }
         sbuf ^= 1;

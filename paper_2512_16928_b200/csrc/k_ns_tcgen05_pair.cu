@@ -127,6 +127,7 @@ __global__ void __cluster_dims__(2, 1, 1) __launch_bounds__(kPairThreads, 1)
         tma_prefetch_desc(&P.mapAT[gi]);
         tma_prefetch_desc(&P.mapBT[gi]);
       }
+
     }
   }
   if (warp == 1) tmem_alloc_pair(tmem_base_slot, kTmemCols);
@@ -156,8 +157,12 @@ __global__ void __cluster_dims__(2, 1, 1) __launch_bounds__(kPairThreads, 1)
           // sym_in: a k-block left of the diagonal tile is stored only as its transpose
           const bool at = kSymIn && ((kb * kBK) >> 8) < c.tm;
           const bool bt = kSymIn && ((kb * kBK) >> 8) < c.tn;
+          // distributed owner gram: the K axis (q) runs over the P rank pieces of X0
+          const int pr = G.pieces_qo ? (kb * kBK) / G.pieces_qo : 0;
+          const int pc = G.pieces_qo ? kb * kBK - pr * G.pieces_qo : kb * kBK;
+          const CUtensorMap* pmap = G.pieces_qo ? &P.mapP[c.group][pr] : nullptr;
           if (!at) {
-            tma_load_3d_pair(sa, &P.mapA[c.group], leader_full, kb * kBK, c.tm * 256 + (int)rank * 128, c.z);
+            tma_load_3d_pair(sa, pmap ? pmap : &P.mapA[c.group], leader_full, pc, c.tm * 256 + (int)rank * 128, c.z);
           } else {
 #pragma unroll
             for (int j = 0; j < 2; ++j)
@@ -170,7 +175,7 @@ __global__ void __cluster_dims__(2, 1, 1) __launch_bounds__(kPairThreads, 1)
               tma_load_3d_pair(sb + j * 64 * kBK * 2, &P.mapBT[c.group], leader_full,
                                c.tn * 256 + (int)rank * 128 + j * 64, kb * kBK, c.z);
           } else if (p.b_kmajor) {
-            tma_load_3d_pair(sb, &P.mapB[c.group], leader_full, kb * kBK, c.tn * 256 + (int)rank * 128, c.z);
+            tma_load_3d_pair(sb, pmap ? pmap : &P.mapB[c.group], leader_full, pc, c.tn * 256 + (int)rank * 128, c.z);
           } else {
 #pragma unroll
             for (int j = 0; j < 2; ++j)

@@ -4,6 +4,8 @@
 
 namespace dion2 {
 
+constexpr int kMaxPieceRanks = 8;  // distributed owner step: piece tensor maps are made for P <= 8
+
 // ---------------- K1 momentum + l1 score (k_momentum_score.cu)
 constexpr int kColRowBlock = 256;  // rows per column-mode partial-sum block
 __global__ void k_momentum_score_rows(const MatDesc* __restrict__ mats, const int32_t* __restrict__ row_mats,
@@ -78,6 +80,7 @@ __global__ void k_full_decay(const MatDesc* __restrict__ mats, int n_mats, const
 // ---------------- distributed step (k_dist.cu)
 struct PieceTable {
   const int32_t* gidx;     // [n_owned] global matrix index
+  const int32_t* inplace;  // [n_owned] 1: the NS kernels read / write the pieces in place (no copy)
   const int64_t* roff;     // [n_owned * world] byte offset of owned matrix jj's piece in rank r's section
   int64_t rstride;         // bytes between consecutive ranks' sections
   int32_t world;
@@ -90,6 +93,7 @@ void launch_assemble(cudaStream_t s, const MatDesc* omats, int n_owned, int max_
                      const uint8_t* recv, const float* sumsq_all, int n_total, float eps);
 void launch_disassemble(cudaStream_t s, const MatDesc* omats, int n_owned, int max_k, const PieceTable& T,
                         uint8_t* send);
+
 
 // ---------------- compressed DP-sync (k_dpsync.cu): M[K] <-> contiguous fp32 buffer
 void launch_dp_pack(bool unpack, cudaStream_t s, const MatDesc* mats, const int32_t* row_prefix, const int64_t* buf_off,
@@ -109,6 +113,11 @@ struct NsGroup {
   const void* b;  long long b_mstride; int ldb;
   void* out;      long long out_mstride; int out_ld;
   const void* cin; long long cin_mstride; int cin_ld;
+  // distributed owner step (dion2_dist.cu): X0 / X_T live as P column pieces [rank][matrix][k][qo]
+  // in the exchange buffers; the gram / apply read (and the apply writes) them through the
+  // per-rank tensor maps NsTcParams::mapP[group][kind * P + r] (kind 0: box {64, 128} loads,
+  // 1: box {64, 64} MN-major loads, 2: box {32, 32} stores).  pieces_qo = 0: plain layout.
+  int pieces_qo, pieces_P, pieces_map;
 };
 
 struct NsParams {
@@ -142,6 +151,8 @@ struct NsTcParams {
   CUtensorMap mapD[kMaxGroups];  // output (TMA store): box {32 cols, 32 rows, 1}, SWIZZLE_64B
   CUtensorMap mapAT[kMaxGroups]; // sym_in: the A buffer with box {64, 64} for transposed k-blocks
   CUtensorMap mapBT[kMaxGroups]; // sym_in: the B buffer with box {64, 64}
+  // distributed owner step: per-rank piece maps of each group (see NsGroup::pieces_qo), kind-major
+  CUtensorMap mapP[kMaxGroups][3 * kMaxPieceRanks];
   NsParams p;
 };
 void ns_tc_set_attrs();

@@ -40,6 +40,8 @@ inline int64_t ceil_div(int64_t a, int64_t b) { return (a + b - 1) / b; }
 
 bool make_map(CUtensorMap* m, const void* base, int64_t cols, int64_t rows, int64_t count, int box_cols, int box_rows,
               CUtensorMapSwizzle swz = CU_TENSOR_MAP_SWIZZLE_128B);
+bool make_map_strided(CUtensorMap* m, const void* base, int64_t cols, int64_t rows, int64_t count,
+                      int64_t zstride_bytes, int box_cols, int box_rows, CUtensorMapSwizzle swz);
 int validate_config(const dion2_config* c);
 // The kernels' view of the caller's matrices: storage_transposed ones get their storage shape
 // (rows and cols swapped); build_layout recovers the logical shape for the axis, k and scale.
