@@ -99,6 +99,7 @@ struct DistPlan {
   std::unique_ptr<Plan> owner;
   PieceTable ptab{};
   int max_p_pad = 0, max_k_owned = 0;
+  bool all_inplace = false;  // every owned matrix's NS reads / writes the exchange pieces in place
 };
 
 void* dt(DistPlan& D, size_t off) { return static_cast<uint8_t*>(D.dtab) + off; }
@@ -462,6 +463,7 @@ int build_tables(DistPlan& D, const dion2_config* c, void* ws) {
       }
     }
     memcpy(H(D.t_inpl), inpl.data(), 4 * inpl.size());
+    D.all_inplace = std::all_of(inpl.begin(), inpl.end(), [](int32_t v) { return v != 0; });
     D.ptab.inplace = (const int32_t*)dt(D, D.t_inpl);
     D.ptab.gidx = (const int32_t*)dt(D, D.t_gidx);
     D.ptab.roff = (const int64_t*)dt(D, D.t_roff);
@@ -641,13 +643,16 @@ void phase_owner_ns(DistPlan& D, void* ws, const dion2_config* c, Launcher& L, c
   Plan& P = *D.owner;
   const MatDesc* om = (const MatDesc*)tab(P, P.off_desc);
   L.begin(PH_NORM);
-  launch_assemble(s, om, (int)D.owned.size(), D.max_p_pad, D.ptab, (const uint8_t*)at(ws, D.off_recv),
+  // all owned matrices in place: one block per matrix computes the norm scale only
+  launch_assemble(s, om, (int)D.owned.size(), D.all_inplace ? 1 : D.max_p_pad, D.ptab, (const uint8_t*)at(ws, D.off_recv),
                   (const float*)at(ws, D.off_sumsq_all), D.n, c->ns_eps);
   L.end();
   run_ns(P, c, L, s, false);
-  L.begin(PH_SCATTER);
-  launch_disassemble(s, om, (int)D.owned.size(), D.max_k_owned, D.ptab, (uint8_t*)at(ws, D.off_osend));
-  L.end();
+  if (!D.all_inplace) {
+    L.begin(PH_SCATTER);
+    launch_disassemble(s, om, (int)D.owned.size(), D.max_k_owned, D.ptab, (uint8_t*)at(ws, D.off_osend));
+    L.end();
+  }
 }
 
 void phase_scatter(DistPlan& D, void* ws, const dion2_config* c, Launcher& L, cudaStream_t s) {
