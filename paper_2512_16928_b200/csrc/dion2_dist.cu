@@ -99,7 +99,8 @@ struct DistPlan {
   std::unique_ptr<Plan> owner;
   PieceTable ptab{};
   int max_p_pad = 0, max_k_owned = 0;
-  bool all_inplace = false;  // every owned matrix's NS reads / writes the exchange pieces in place
+  bool all_inplace = false;     // every owned matrix's NS reads and writes the exchange pieces in place
+  bool all_inplace_in = false;  // ... reads them in place (inplace value 1 or 2)
 };
 
 void* dt(DistPlan& D, size_t off) { return static_cast<uint8_t*>(D.dtab) + off; }
@@ -419,6 +420,7 @@ int build_tables(DistPlan& D, const dion2_config* c, void* ws) {
     std::vector<int32_t> inpl(D.owned.size(), 0);
     const char* ie = getenv("DION2_DIST_INPLACE");
     const bool inplace_on = !(ie && ie[0] == '0') && P <= kMaxPieceRanks;
+    const bool inplace_in_only = ie && ie[0] == '2';  // A/B: pieces read in place, X_T still copied out
     CUtensorMap* hmaps = reinterpret_cast<CUtensorMap*>(H(D.t_pmaps));
     std::vector<int> g_ok(D.owner->groups.size(), 0);
     for (size_t gi = 0; gi < D.owner->groups.size() && inplace_on; ++gi) {
@@ -442,7 +444,7 @@ int build_tables(DistPlan& D, const dion2_config* c, void* ws) {
           return DION2_ECUDA;
       }
       g_ok[gi] = 1;
-      for (int i : g.mats) inpl[i] = 1;
+      for (int i : g.mats) inpl[i] = inplace_in_only ? 2 : 1;
     }
     // point the owner plan's gram (A = B = X0) and apply (B = X0, D = X_T) launches at the pieces
     for (Launch& ln : D.owner->ns_launches) {
@@ -458,12 +460,14 @@ int build_tables(DistPlan& D, const dion2_config* c, void* ws) {
           G.pieces_qo = q0.qo;
           G.pieces_P = P;
           G.pieces_map = (int)(gi * 3 * P);
+          G.pieces_store = ln.phase == PH_APPLY && !inplace_in_only;
           for (int k = 0; k < 3 * P; ++k) ln.tc.mapP[j][k] = hmaps[gi * 3 * P + k];
         }
       }
     }
     memcpy(H(D.t_inpl), inpl.data(), 4 * inpl.size());
-    D.all_inplace = std::all_of(inpl.begin(), inpl.end(), [](int32_t v) { return v != 0; });
+    D.all_inplace = std::all_of(inpl.begin(), inpl.end(), [](int32_t v) { return v == 1; });
+    D.all_inplace_in = std::all_of(inpl.begin(), inpl.end(), [](int32_t v) { return v != 0; });
     D.ptab.inplace = (const int32_t*)dt(D, D.t_inpl);
     D.ptab.gidx = (const int32_t*)dt(D, D.t_gidx);
     D.ptab.roff = (const int64_t*)dt(D, D.t_roff);
@@ -644,7 +648,7 @@ void phase_owner_ns(DistPlan& D, void* ws, const dion2_config* c, Launcher& L, c
   const MatDesc* om = (const MatDesc*)tab(P, P.off_desc);
   L.begin(PH_NORM);
   // all owned matrices in place: one block per matrix computes the norm scale only
-  launch_assemble(s, om, (int)D.owned.size(), D.all_inplace ? 1 : D.max_p_pad, D.ptab, (const uint8_t*)at(ws, D.off_recv),
+  launch_assemble(s, om, (int)D.owned.size(), D.all_inplace_in ? 1 : D.max_p_pad, D.ptab, (const uint8_t*)at(ws, D.off_recv),
                   (const float*)at(ws, D.off_sumsq_all), D.n, c->ns_eps);
   L.end();
   run_ns(P, c, L, s, false);

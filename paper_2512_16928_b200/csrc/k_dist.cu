@@ -90,7 +90,7 @@ __global__ void k_disassemble_pieces(const MatDesc* __restrict__ omats, PieceTab
   const int jj = blockIdx.y;
   const MatDesc& md = omats[jj];
   const int i = blockIdx.x;
-  if (i >= md.k || T.inplace[jj]) return;  // in place: the apply wrote the pieces itself
+  if (i >= md.k || T.inplace[jj] == 1) return;  // in place: the apply wrote the pieces itself
   const int qo = md.q / T.world;
   const __nv_bfloat16* xrow =
       reinterpret_cast<const __nv_bfloat16*>(md.final_in_x1 ? md.X1 : md.X0) + (int64_t)i * md.q_pad;

@@ -233,7 +233,7 @@ __global__ void __launch_bounds__(192, 1) k_ns_gemm_tc(const __grid_constant__ N
         if (lane == 0) {
           const NsGroup& Gs = p.g[c.group];
           const int col = c.tn * BN + cc32 * 32;
-          if (Gs.pieces_qo) {  // X_T straight into the rank pieces of the exchange buffer
+          if (Gs.pieces_store) {  // X_T straight into the rank pieces of the exchange buffer
             const int pr = col / Gs.pieces_qo;
             tma_store_3d(&P.mapP[c.group][2 * Gs.pieces_P + pr], buf, col - pr * Gs.pieces_qo,
                          c.tm * kBM + lg * 32, c.z);

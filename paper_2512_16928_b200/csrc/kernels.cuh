@@ -118,6 +118,7 @@ struct NsGroup {
   // per-rank tensor maps NsTcParams::mapP[group][kind * P + r] (kind 0: box {64, 128} loads,
   // 1: box {64, 64} MN-major loads, 2: box {32, 32} stores).  pieces_qo = 0: plain layout.
   int pieces_qo, pieces_P, pieces_map;
+  int pieces_store;          // apply: X_T TMA-stored into the outgoing pieces (else into `out`)
 };
 
 struct NsParams {
