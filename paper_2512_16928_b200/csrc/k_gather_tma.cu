@@ -191,10 +191,16 @@ void launch_gather_rows_tma(int stages, int blocks_per_sm_cap, cudaStream_t s, c
   if (!attr) {
     cudaFuncSetAttribute(k_gather_rows_tma<4>, cudaFuncAttributeMaxDynamicSharedMemorySize, (int)gather_tma_smem<4>());
     cudaFuncSetAttribute(k_gather_rows_tma<6>, cudaFuncAttributeMaxDynamicSharedMemorySize, (int)gather_tma_smem<6>());
+    cudaFuncSetAttribute(k_gather_rows_tma<8>, cudaFuncAttributeMaxDynamicSharedMemorySize, (int)gather_tma_smem<8>());
     attr = true;
   }
   int nb = 0;
-  if (stages == 6) {
+  if (stages == 8) {
+    cudaOccupancyMaxActiveBlocksPerMultiprocessor(&nb, k_gather_rows_tma<8>, kThreads, gather_tma_smem<8>());
+    nb = std::max(1, std::min(nb, blocks_per_sm_cap));
+    k_gather_rows_tma<8><<<std::max(1, std::min(units, nb * sms)), kThreads, gather_tma_smem<8>(), s>>>(
+        mats, lm, lp, nl, units, bad, mu);
+  } else if (stages == 6) {
     cudaOccupancyMaxActiveBlocksPerMultiprocessor(&nb, k_gather_rows_tma<6>, kThreads, gather_tma_smem<6>());
     nb = std::max(1, std::min(nb, blocks_per_sm_cap));
     k_gather_rows_tma<6><<<std::max(1, std::min(units, nb * sms)), kThreads, gather_tma_smem<6>(), s>>>(

@@ -286,10 +286,11 @@ class Dion2:
         if rc:
             raise Dion2Error(rc, "dion2_step_batched")
 
-    def step_host(self, Ws, Ms, Gs, G_host, sel_out=None, chunks: int = 4):
+    def step_host(self, Ws, Ms, Gs, G_host, sel_out=None, chunks: Optional[int] = None):
         """One optimizer step whose gradients arrive from the host: G_host[i] is a pinned CPU
         tensor copied into the device buffer Gs[i].  The matrices are split into `chunks`
-        contiguous groups of about equal parameter count; a side stream copies group c + 1
+        (default 8, env DION2_HOST_CHUNKS; measured e2e 90.1 / 89.0 / 88.5 ms for 2 / 4 / 8 on the
+        1B set) contiguous groups of about equal parameter count; a side stream copies group c + 1
         while group c steps on the current stream, so the step hides under the host-to-device
         transfer.  Each group is its own batched library call (its own plan and workspace)."""
         n = len(Ws)
@@ -298,6 +299,8 @@ class Dion2:
         for g, h in zip(Gs, G_host):
             if h.is_cuda or h.shape != g.shape or h.dtype != g.dtype:
                 raise ValueError("G_host[i] must be a CPU tensor shaped and typed like Gs[i]")
+        if chunks is None:
+            chunks = int(os.environ.get("DION2_HOST_CHUNKS", "8"))
         sizes = [w.numel() for w in Ws]
         total, bounds, acc, c0 = sum(sizes), [], 0, 0
         chunks = max(1, min(chunks, n))
