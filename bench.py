@@ -571,7 +571,7 @@ def run_ours(args):
             "roofline": roof,
             "cpu_baseline": cpu,
             "e2e": {"value": e2e_ms, "unit": "ms/step", "h2d_bytes_per_step": h2d, "d2h_bytes_per_step": d2h,
-                    "what": "pinned host G -> device (Dion2.step_host: 4 chunks, upload overlapped with the earlier chunks' steps), dion2_step_batched per chunk, selected indices -> host, every step"},
+                    "what": "pinned host G -> device (Dion2.step_host: 8 chunks, upload overlapped with the earlier chunks' steps), dion2_step_batched per chunk, selected indices -> host, every step"},
             "gpu_launches": launches,
             "comm": comm,
             "clocks": clk.summary(),
