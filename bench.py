@@ -292,10 +292,11 @@ def e2e_run(opt, Ws, Ms, Gs, G_flat, steps, ks):
         host_views.append(host_G[off:off + g.numel()].view(g.shape))
         off += g.numel()
     pipelined = hasattr(opt, "step_host")
-    if pipelined:  # untimed: plans (and, in graph mode, the captures) for this call
-        opt.step_host(Ws, Ms, Gs, host_views, sel_out=sel_views)
-    else:
-        opt.step(Ws, Ms, Gs, sel_out=sel_views)
+    for _ in range(2):  # untimed: plans and, in graph mode, the captures (a key's second call)
+        if pipelined:
+            opt.step_host(Ws, Ms, Gs, host_views, sel_out=sel_views)
+        else:
+            opt.step(Ws, Ms, Gs, sel_out=sel_views)
     torch.cuda.synchronize()
     s = torch.cuda.current_stream()
     e0, e1 = torch.cuda.Event(enable_timing=True), torch.cuda.Event(enable_timing=True)

@@ -202,10 +202,10 @@ class Dion2:
 
     def __init__(self, m_transposed=None, storage_transposed=None, cuda_graph: bool = False, **cfg_kw):
         """m_transposed / storage_transposed: default per-matrix layout flags used by step()
-        (see describe()).  cuda_graph: the first step on a given set of tensors runs eagerly
-        (building the library's plan) and is then captured once into a CUDA graph; later
-        steps on the same tensors, config and stream device replay it (no per-step host
-        work, no launch gaps).  One call is always exactly one optimizer step."""
+        (see describe()).  cuda_graph: a step whose tensors and config repeat the previous call's
+        runs eagerly and is captured once into a CUDA graph; later steps with that key replay
+        it (no per-step host work, no launch gaps).  A key seen once (e.g. under a learning-rate
+        schedule) just runs eagerly.  One call is always exactly one optimizer step."""
         self.cfg_kw = dict(cfg_kw)
         self.m_transposed = m_transposed
         self.storage_transposed = storage_transposed
@@ -227,7 +227,7 @@ class Dion2:
         if rc:
             raise Dion2Error(rc, "dion2_workspace_size")
         if self.cuda_graph:
-            need.value += self.GRAPH_SLOTS * self.SLOT_BYTES
+            need.value += (self.GRAPH_SLOTS + 1) * self.SLOT_BYTES  # + the slot of uncaptured steps
         if self._ws is None or self._ws.numel() < need.value or self._ws.device != device:
             self._graphs.clear()  # captured graphs reference the old workspace
             self._ws = torch.empty(need.value, dtype=torch.uint8, device=device)
@@ -249,6 +249,13 @@ class Dion2:
                 self._graphs.move_to_end(key)
                 hit[0].replay()
                 self._last_slot = hit[1]
+                return
+            prev, self._prev_key = getattr(self, "_prev_key", None), key
+            if key != prev:
+                # first call with this key: eager, in the slot reserved for uncaptured steps (a
+                # config that changes every step, e.g. a learning-rate schedule, never captures)
+                self._step(Ws, Ms, Gs, sel_out, O_out, None, m_transposed, storage_transposed, self.GRAPH_SLOTS,
+                           **override)
                 return
             used = {slot for (_, slot) in self._graphs.values()}
             free = [i for i in range(self.GRAPH_SLOTS) if i not in used]

@@ -347,8 +347,10 @@ def test_cuda_graph_capture_replays_the_step():
 
 
 def test_cuda_graph_mode_equals_eager():
-    """Dion2(cuda_graph=True): first step eager + capture, later steps replay; a new tensor set
-    or a changed learning rate captures again.  Bitwise equal to the eager optimizer."""
+    """Dion2(cuda_graph=True): a key (tensors + config) repeated on consecutive calls is
+    captured on its second call and replayed afterwards; keys that change every call (the
+    alternating gradient buffers, a learning-rate schedule) run eagerly; a second tensor set
+    and a changed learning rate capture again.  Bitwise equal to the eager optimizer."""
     shapes = [(512, 1024), (2048, 512), (300, 520)]
     mt = [m > n for (m, n) in shapes]
     def init(seed):
@@ -356,21 +358,31 @@ def test_cuda_graph_mode_equals_eager():
         Ms = [torch.zeros(n, m, device="cuda") if t else torch.zeros(m, n, device="cuda")
               for (m, n), t in zip(shapes, mt)]
         return Ws, Ms
-    Gs = [[torch.from_numpy(gen_grad(m, n, 4, i, t, row_scaled=True)).cuda() for i, (m, n) in enumerate(shapes)]
-          for t in range(2)]
+    data = [[torch.from_numpy(gen_grad(m, n, 4, i, t, row_scaled=True)).cuda() for i, (m, n) in enumerate(shapes)]
+            for t in range(6)]
     outs = []
     for graph in (False, True):
         opt = Dion2(alpha=0.25, m_transposed=mt, cuda_graph=graph)
         Wa, Ma = init(7)
         Wb, Mb = init(8)
-        for t in range(5):
-            opt.step(Wa, Ma, Gs[t % 2])
-            if t == 2:
-                opt.cfg_kw["lr"] = 0.01
-        opt.step(Wb, Mb, Gs[0])
-        opt.step(Wb, Mb, Gs[1])
+        G = [torch.empty(m, n, device="cuda") for (m, n) in shapes]
+        for t in range(6):                     # same buffers: eager, eager + capture, replays
+            for g, d in zip(G, data[t]):
+                g.copy_(d)
+            opt.step(Wa, Ma, G)
+            if t == 3:
+                opt.cfg_kw["lr"] = 0.01        # new key: eager, then capture, then replay
+        for t in range(4):                     # alternating buffers: every key new, all eager
+            opt.step(Wa, Ma, data[t % 2])
+        for t in range(4):                     # a learning-rate schedule: never captured
+            opt.cfg_kw["lr"] = 0.02 / (t + 1)
+            opt.step(Wa, Ma, data[t + 2])
+        for t in range(3):
+            opt.step(Wb, Mb, data[t])
         torch.cuda.synchronize()
         outs.append([x.clone() for x in Wa + Ma + Wb + Mb])
+        if graph:
+            assert len(opt._graphs) >= 2
     for a, b in zip(*outs):
         assert torch.equal(a, b)
 
