@@ -52,6 +52,12 @@ extern "C" {
 
 #define DION2_ABI_VERSION 5
 #define DION2_MAX_NS_STEPS 16
+/* dion2_config.reserved0 flag: the sparse update reads eta on the device from the fp32 word at
+   byte offset 8 of the workspace's 4096-byte-aligned base (the first multiple of 4096 at or
+   after `workspace`; the caller writes it, stream-ordered, before the step)
+   instead of cfg.lr, so a CUDA graph of the step follows a learning-rate schedule without being
+   re-captured.  cfg.lr must still be a valid eta (it is validated, then ignored by the kernels). */
+#define DION2_FLAG_LR_DEVICE 1
 
 typedef enum {
   DION2_OK = 0,
@@ -126,7 +132,7 @@ typedef struct {
   uint64_t seed;      /* random selection key (unused for L1) */
   uint64_t step;      /* random selection counter: the caller's step index (unused for L1) */
   int32_t ns_form;    /* dion2_ns_form, default AUTO (BF16 precision only; FP32 is always DIRECT) */
-  int32_t reserved0;  /* must be 0 */
+  int32_t reserved0;  /* flags: 0, or DION2_FLAG_LR_DEVICE (other bits must be 0) */
 } dion2_config;
 
 /* Fill *cfg with the defaults above.  Always returns DION2_OK. */

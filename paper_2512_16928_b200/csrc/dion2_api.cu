@@ -115,7 +115,7 @@ int validate_config(const dion2_config* c) {
   if (c->grad_dtype != DION2_DT_F32 && c->grad_dtype != DION2_DT_BF16) return DION2_EINVAL_CONFIG;
   if (c->decay_mode < 0 || c->decay_mode > 1) return DION2_EINVAL_CONFIG;
   if (c->scale_mode < 0 || c->scale_mode > 1) return DION2_EINVAL_CONFIG;
-  if (c->ns_form < DION2_NS_FORM_AUTO || c->ns_form > DION2_NS_FORM_GRAM || c->reserved0 != 0)
+  if (c->ns_form < DION2_NS_FORM_AUTO || c->ns_form > DION2_NS_FORM_GRAM || (c->reserved0 & ~DION2_FLAG_LR_DEVICE) != 0)
     return DION2_EINVAL_CONFIG;
   return DION2_OK;
 }
@@ -1123,24 +1123,26 @@ void stage_post(Plan& P, const dion2_matrix* mats, const dion2_config* c, void* 
   const int n = P.n;
   const MatDesc* dmats = (const MatDesc*)tab(P, P.off_desc);
   int32_t* bad = (int32_t*)at(ws, P.off_bad);
+  // DION2_FLAG_LR_DEVICE: eta is the fp32 word at workspace byte 8 (written by the caller)
+  const float* lr_dev = (c->reserved0 & DION2_FLAG_LR_DEVICE) ? (const float*)at(ws, P.off_status + 8) : nullptr;
   if (P.total_gather_tiles > 0 && P.generic_scatter_mats > 0) {
     L.begin(PH_SCATTER);
     launch_scatter_update(P.bf16_ns, stream_grid(P.total_gather_tiles, 8, persistent), s, dmats,
-                          (const int32_t*)tab(P, P.off_gprefix), n, P.total_gather_tiles, bad, c->lr);
+                          (const int32_t*)tab(P, P.off_gprefix), n, P.total_gather_tiles, bad, c->lr, lr_dev);
     L.end();
   }
   if (P.fl_sn[0]) {
     L.begin(PH_SCATTER_ROWS);
     launch_scatter_rows(stream_grid(ceil_div(P.fl_sunits[0], 8), 8, persistent), s, dmats,
                         (const int32_t*)tab(P, P.off_fls_mats[0]), (const int32_t*)tab(P, P.off_fl_sprefix[0]),
-                        P.fl_sn[0], P.fl_sunits[0], bad, c->lr);
+                        P.fl_sn[0], P.fl_sunits[0], bad, c->lr, lr_dev);
     L.end();
   }
   if (P.fl_sn[1]) {
     L.begin(PH_SCATTER_COLS);
     launch_scatter_cols_t(stream_grid(P.fl_sunits[1], 6, persistent), P.fl_smaxk, P.fl_maxn, s, dmats,
                           (const int32_t*)tab(P, P.off_fls_mats[1]), (const int32_t*)tab(P, P.off_fl_sprefix[1]),
-                          P.fl_sn[1], P.fl_sunits[1], bad, c->lr);
+                          P.fl_sn[1], P.fl_sunits[1], bad, c->lr, lr_dev);
     L.end();
   }
   if (c->decay_mode == 1) {
@@ -1228,6 +1230,11 @@ int run_chunked(ChunkedPlan& C, const dion2_matrix* mats, const dion2_config* c,
     if ((rc = refresh_tables(*C.subs[j], mats + C.first[j], c, s0))) return rc;
   int32_t* status = (int32_t*)at(ws, C.off[0] + C.subs[0]->off_status);  // the workspace's status word
   if ((rc = reset_status(status, s0))) return rc;
+  if (c->reserved0 & DION2_FLAG_LR_DEVICE)  // every chunk's K7 reads eta from its own status block
+    for (int j = 1; j < nc; ++j)
+      if (cudaMemcpyAsync(at(ws, C.off[j] + C.subs[j]->off_status + 8), at(ws, C.subs[0]->off_status + 8), 4,
+                          cudaMemcpyDeviceToDevice, s0) != cudaSuccess)
+        return DION2_ECUDA;
   Launcher L0{s0}, L1{s1};
   cudaEventRecord(C.ev[0], s0);  // fork: s1 follows everything enqueued on s0 so far
   cudaStreamWaitEvent(s1, C.ev[0], 0);

@@ -661,26 +661,27 @@ void phase_owner_ns(DistPlan& D, void* ws, const dion2_config* c, Launcher& L, c
 
 void phase_scatter(DistPlan& D, void* ws, const dion2_config* c, Launcher& L, cudaStream_t s) {
   const int sms = g_sm_count > 0 ? g_sm_count : 148;
+  const float* lr_dev = (c->reserved0 & DION2_FLAG_LR_DEVICE) ? (const float*)at(ws, D.off_status + 8) : nullptr;
   const MatDesc* dm = (const MatDesc*)dt(D, D.t_desc);
   const int32_t* bad = (const int32_t*)at(ws, D.off_bad);
   if (D.total_gather_tiles) {
     L.begin(PH_SCATTER);
     launch_scatter_update(true, std::min(D.total_gather_tiles, sms * 8), s, dm, (const int32_t*)dt(D, D.t_gprefix),
-                          D.n, D.total_gather_tiles, bad, c->lr);
+                          D.n, D.total_gather_tiles, bad, c->lr, lr_dev);
     L.end();
   }
   if (D.fl_sn[0]) {
     L.begin(PH_SCATTER_ROWS);
     const int blocks = (int)std::min<int64_t>(ceil_div(D.fl_sunits[0], 8), (int64_t)sms * 8);
     launch_scatter_rows(blocks, s, dm, (const int32_t*)dt(D, D.t_flsm[0]), (const int32_t*)dt(D, D.t_fls[0]),
-                        D.fl_sn[0], D.fl_sunits[0], bad, c->lr);
+                        D.fl_sn[0], D.fl_sunits[0], bad, c->lr, lr_dev);
     L.end();
   }
   if (D.fl_sn[1]) {
     L.begin(PH_SCATTER_COLS);
     const int blocks = std::min(D.fl_sunits[1], sms * 6);  // as the single-GPU path
     launch_scatter_cols_t(blocks, D.fl_maxk, D.max_cols_col, s, dm, (const int32_t*)dt(D, D.t_flsm[1]),
-                          (const int32_t*)dt(D, D.t_fls[1]), D.fl_sn[1], D.fl_sunits[1], bad, c->lr);
+                          (const int32_t*)dt(D, D.t_fls[1]), D.fl_sn[1], D.fl_sunits[1], bad, c->lr, lr_dev);
     L.end();
   }
 }

@@ -149,7 +149,8 @@ __global__ void k_norm_finalize(const MatDesc* __restrict__ mats, int n_mats, fl
 template <typename XT>
 __global__ void __launch_bounds__(256) k_scatter_update(const MatDesc* __restrict__ mats,
                                                         const int32_t* __restrict__ tile_prefix_mats, int n_mats,
-                                                        int total_tiles, const int32_t* __restrict__ bad, float lr) {
+                                                        int total_tiles, const int32_t* __restrict__ bad, float lr,
+                                                        const float* __restrict__ lr_dev) {
   __shared__ float tile[kTileA][kTileB + 1];
   const int tx = threadIdx.x & 15, ty = threadIdx.x >> 4;
   for (int t = blockIdx.x; t < total_tiles; t += gridDim.x) {
@@ -172,7 +173,7 @@ __global__ void __launch_bounds__(256) k_scatter_update(const MatDesc* __restric
       }
       __syncthreads();
     }
-    const float sc = lr * md.update_scale;
+    const float sc = (lr_dev ? __ldg(lr_dev) : lr) * md.update_scale;
 #pragma unroll
     for (int rr = 0; rr < 2; ++rr) {
       const int al = ty + 16 * rr, a = a0 + al;
@@ -211,11 +212,11 @@ __global__ void __launch_bounds__(256) k_scatter_update(const MatDesc* __restric
   }
 }
 void launch_scatter_update(bool bf16, int blocks, cudaStream_t s, const MatDesc* mats, const int32_t* tile_prefix_mats,
-                           int n_mats, int total_tiles, const int32_t* bad, float lr) {
+                           int n_mats, int total_tiles, const int32_t* bad, float lr, const float* lr_dev) {
   if (bf16)
-    k_scatter_update<__nv_bfloat16><<<blocks, 256, 0, s>>>(mats, tile_prefix_mats, n_mats, total_tiles, bad, lr);
+    k_scatter_update<__nv_bfloat16><<<blocks, 256, 0, s>>>(mats, tile_prefix_mats, n_mats, total_tiles, bad, lr, lr_dev);
   else
-    k_scatter_update<float><<<blocks, 256, 0, s>>>(mats, tile_prefix_mats, n_mats, total_tiles, bad, lr);
+    k_scatter_update<float><<<blocks, 256, 0, s>>>(mats, tile_prefix_mats, n_mats, total_tiles, bad, lr, lr_dev);
 }
 
 // Full-decay ablation: M <- mu * M on the UNSELECTED part (the

@@ -110,7 +110,8 @@ template <int D>
 __global__ void __launch_bounds__(256) k_scatter_rows(const MatDesc* __restrict__ mats,
                                                       const int32_t* __restrict__ list_mats,
                                                       const int32_t* __restrict__ list_prefix, int n_list,
-                                                      int total_units, const int32_t* __restrict__ bad, float lr) {
+                                                      int total_units, const int32_t* __restrict__ bad, float lr,
+                                                      const float* __restrict__ lr_dev) {
   const int lane = threadIdx.x & 31;
   const int warp = blockIdx.x * (blockDim.x >> 5) + (threadIdx.x >> 5);
   const int nwarps = gridDim.x * (blockDim.x >> 5);
@@ -124,7 +125,7 @@ __global__ void __launch_bounds__(256) k_scatter_rows(const MatDesc* __restrict_
         reinterpret_cast<const __nv_bfloat16*>(md.final_in_x1 ? md.X1 : md.X0) + (int64_t)r * md.q_pad;
     float* wrow = md.W + (int64_t)md.sel[r] * md.ld;
     float* orow = md.O_out ? md.O_out + (int64_t)r * md.cols : nullptr;
-    const float sc = lr * md.update_scale;
+    const float sc = (lr_dev ? __ldg(lr_dev) : lr) * md.update_scale;
     const int n = (int)md.cols;
     if (md.vec4) {
       const int n4 = n >> 2;
@@ -345,7 +346,7 @@ __global__ void __launch_bounds__(256) k_scatter_cols_t(const MatDesc* __restric
                                                         const int32_t* __restrict__ list_mats,
                                                         const int32_t* __restrict__ list_prefix, int n_list,
                                                         int total_units, const int32_t* __restrict__ bad, float lr,
-                                                        int mask_words, int slab_h) {
+                                                        const float* __restrict__ lr_dev, int mask_words, int slab_h) {
   extern __shared__ __align__(16) uint8_t sm[];
   uint32_t* mask = reinterpret_cast<uint32_t*>(sm);
   int32_t* rank = reinterpret_cast<int32_t*>(sm + 4 * mask_words);
@@ -378,7 +379,7 @@ __global__ void __launch_bounds__(256) k_scatter_cols_t(const MatDesc* __restric
         for (int e = 0; e < 8; ++e) tile[(part + e) * ldt + r] = h[e];
       }
       __syncthreads();
-      const float sc = lr * md.update_scale;
+      const float sc = (lr_dev ? __ldg(lr_dev) : lr) * md.update_scale;
       const int n = (int)md.cols;
       for (int il = wid; il < slab_h; il += 8) {
         const int64_t i = (int64_t)i0 + il;
@@ -447,7 +448,8 @@ __global__ void __launch_bounds__(256, 4) k_scatter_cols_idx(const MatDesc* __re
                                                              const int32_t* __restrict__ list_mats,
                                                              const int32_t* __restrict__ list_prefix, int n_list,
                                                              int total_units, const int32_t* __restrict__ bad,
-                                                             float lr, int max_k, int slab_h);
+                                                             float lr, const float* __restrict__ lr_dev, int max_k,
+                                                             int slab_h);
 
 void launch_fast_paths_attrs() {
   const int mx = (int)cols_t_smem_bytes(kMaxColK, kMaskWords);
@@ -469,7 +471,8 @@ __global__ void __launch_bounds__(256, 4) k_scatter_cols_idx(const MatDesc* __re
                                                              const int32_t* __restrict__ list_mats,
                                                              const int32_t* __restrict__ list_prefix, int n_list,
                                                              int total_units, const int32_t* __restrict__ bad,
-                                                             float lr, int max_k, int slab_h) {
+                                                             float lr, const float* __restrict__ lr_dev, int max_k,
+                                                             int slab_h) {
   extern __shared__ __align__(16) uint8_t sm[];
   int32_t* ssel = reinterpret_cast<int32_t*>(sm);                                   // [max_k]
   __nv_bfloat16* tile = reinterpret_cast<__nv_bfloat16*>(sm + 4 * ((max_k + 3) & ~3));  // [slab_h][ldt]
@@ -502,7 +505,7 @@ __global__ void __launch_bounds__(256, 4) k_scatter_cols_idx(const MatDesc* __re
         for (int e = 0; e < 8; ++e) tile[(part + e) * ldt + r] = h[e];
       }
       __syncthreads();
-      const float sc = lr * md.update_scale;
+      const float sc = (lr_dev ? __ldg(lr_dev) : lr) * md.update_scale;
       for (int il = wid; il < slab_h; il += 8) {
         const int64_t i = (int64_t)i0 + il;
         if (i >= md.rows) break;
@@ -541,8 +544,8 @@ void launch_gather_rows(int blocks, cudaStream_t s, const MatDesc* mats, const i
   k_gather_rows<8><<<blocks, 256, 0, s>>>(mats, lm, lp, nl, units, bad, mu);
 }
 void launch_scatter_rows(int blocks, cudaStream_t s, const MatDesc* mats, const int32_t* lm, const int32_t* lp, int nl,
-                         int units, const int32_t* bad, float lr) {
-  k_scatter_rows<8><<<blocks, 256, 0, s>>>(mats, lm, lp, nl, units, bad, lr);
+                         int units, const int32_t* bad, float lr, const float* lr_dev) {
+  k_scatter_rows<8><<<blocks, 256, 0, s>>>(mats, lm, lp, nl, units, bad, lr, lr_dev);
 }
 void launch_gather_cols_t(int blocks, int max_k, int64_t max_n, cudaStream_t s, const MatDesc* mats, const int32_t* lm,
                           const int32_t* lp, int nl, int units, const int32_t* bad, float mu) {
@@ -550,11 +553,12 @@ void launch_gather_cols_t(int blocks, int max_k, int64_t max_n, cudaStream_t s, 
   k_gather_cols_t<<<blocks, 256, cols_t_smem_bytes(max_k, mw), s>>>(mats, lm, lp, nl, units, bad, mu, mw);
 }
 void launch_scatter_cols_t(int blocks, int max_k, int64_t max_n, cudaStream_t s, const MatDesc* mats,
-                           const int32_t* lm, const int32_t* lp, int nl, int units, const int32_t* bad, float lr) {
+                           const int32_t* lm, const int32_t* lp, int nl, int units, const int32_t* bad, float lr,
+                           const float* lr_dev) {
   if (!getenv("DION2_SCATTER_MASK")) {
     const int slab_h = max_k <= 512 ? 32 : (max_k <= 1024 ? 16 : 8);
     const size_t smem = 4 * (size_t)((max_k + 3) & ~3) + (size_t)slab_h * (max_k + 8) * 2;
-    k_scatter_cols_idx<8><<<blocks, 256, smem, s>>>(mats, lm, lp, nl, units, bad, lr, max_k, slab_h);
+    k_scatter_cols_idx<8><<<blocks, 256, smem, s>>>(mats, lm, lp, nl, units, bad, lr, lr_dev, max_k, slab_h);
     return;
   }
   const int mw = mask_words_for(max_n);
@@ -566,9 +570,9 @@ void launch_scatter_cols_t(int blocks, int max_k, int64_t max_n, cudaStream_t s,
   // (alpha = 0.25: 68% of chunks, 90% of sectors); below ~1/8 density (configs[4]'s
   // alpha = 0.0625: 23% of chunks) only the chunks holding a selected column are loaded
   if ((int64_t)max_k * 8 >= max_n)
-    k_scatter_cols_t<8, true><<<blocks, 256, smem, s>>>(mats, lm, lp, nl, units, bad, lr, mw, slab_h);
+    k_scatter_cols_t<8, true><<<blocks, 256, smem, s>>>(mats, lm, lp, nl, units, bad, lr, lr_dev, mw, slab_h);
   else
-    k_scatter_cols_t<8, false><<<blocks, 256, smem, s>>>(mats, lm, lp, nl, units, bad, lr, mw, slab_h);
+    k_scatter_cols_t<8, false><<<blocks, 256, smem, s>>>(mats, lm, lp, nl, units, bad, lr, lr_dev, mw, slab_h);
 }
 
 }  // namespace dion2

@@ -53,8 +53,9 @@ constexpr int kTileB = 64;   // S cols per gather/scatter tile
 // host launchers (the templates are instantiated in their own translation unit)
 void launch_gather_decay(bool bf16, int blocks, cudaStream_t s, const MatDesc* mats, const int32_t* tile_prefix_mats,
                          int n_mats, int total_tiles, const int32_t* bad, int decay, float mu);
+// lr_dev (optional): eta read on the device at run time (CUDA graphs under a schedule), else lr
 void launch_scatter_update(bool bf16, int blocks, cudaStream_t s, const MatDesc* mats, const int32_t* tile_prefix_mats,
-                           int n_mats, int total_tiles, const int32_t* bad, float lr);
+                           int n_mats, int total_tiles, const int32_t* bad, float lr, const float* lr_dev);
 __global__ void k_norm_finalize(const MatDesc* __restrict__ mats, int n_mats, float eps);
 
 // streaming fast paths (k_gather_scatter_fast.cu): rows mode X = S, cols mode X = S^T
@@ -69,12 +70,13 @@ void launch_gather_rows(int blocks, cudaStream_t s, const MatDesc* mats, const i
 void launch_gather_rows_tma(int stages, int blocks_per_sm_cap, cudaStream_t s, const MatDesc* mats, const int32_t* lm,
                             const int32_t* lp, int nl, int units, const int32_t* bad, float mu, int sms);
 void launch_scatter_rows(int blocks, cudaStream_t s, const MatDesc* mats, const int32_t* lm, const int32_t* lp, int nl,
-                         int units, const int32_t* bad, float lr);
+                         int units, const int32_t* bad, float lr, const float* lr_dev);
 // max_k / max_n: largest k and column count over the matrices of the list (sizes the smem)
 void launch_gather_cols_t(int blocks, int max_k, int64_t max_n, cudaStream_t s, const MatDesc* mats, const int32_t* lm,
                           const int32_t* lp, int nl, int units, const int32_t* bad, float mu);
 void launch_scatter_cols_t(int blocks, int max_k, int64_t max_n, cudaStream_t s, const MatDesc* mats,
-                           const int32_t* lm, const int32_t* lp, int nl, int units, const int32_t* bad, float lr);
+                           const int32_t* lm, const int32_t* lp, int nl, int units, const int32_t* bad, float lr,
+                           const float* lr_dev);
 __global__ void k_full_decay(const MatDesc* __restrict__ mats, int n_mats, const int32_t* __restrict__ bad, float mu);
 
 // ---------------- distributed step (k_dist.cu)

@@ -111,7 +111,7 @@ def make_config(alpha: float = 0.25, mu: float = 0.95, lr: float = 0.02, ns_step
                 ns_coeffs: Optional[Sequence[Tuple[float, float, float]]] = None, ns_eps: float = 1e-7,
                 axis: str = "auto", precision: str = "bf16", grad_dtype: Optional[torch.dtype] = None,
                 decay_mode: int = 0, scale_mode: int = 0, select: str = "l1", seed: int = 0,
-                step: int = 0, ns_form: str = "auto") -> Dion2Config:
+                step: int = 0, ns_form: str = "auto", lr_device: bool = False) -> Dion2Config:
     """ns_form: "auto" | "direct" | "gram" -- how the bf16 Newton-Schulz map is evaluated
     (include/dion2.h dion2_ns_form, reading R23)."""
     cfg = Dion2Config()
@@ -129,6 +129,7 @@ def make_config(alpha: float = 0.25, mu: float = 0.95, lr: float = 0.02, ns_step
     cfg.select = SELECT[select]
     cfg.seed, cfg.step = seed, step
     cfg.ns_form = NS_FORM[ns_form]
+    cfg.reserved0 = 1 if lr_device else 0  # DION2_FLAG_LR_DEVICE: eta read from the workspace word
     return cfg
 
 
@@ -242,20 +243,24 @@ class Dion2:
             key = (ptrs(Ws), ptrs(Ms), ptrs(Gs), ptrs(sel_out or ()), ptrs(O_out or ()),
                    tuple(m_transposed if m_transposed is not None else self.m_transposed or ()),
                    tuple(storage_transposed if storage_transposed is not None else self.storage_transposed or ()),
-                   tuple(sorted((k, repr(v)) for k, v in {**self.cfg_kw, **override}.items())),
+                   # eta is not part of the key: the graph reads it from the workspace word
+                   # (DION2_FLAG_LR_DEVICE), so a learning-rate schedule replays one graph
+                   tuple(sorted((k, repr(v)) for k, v in {**self.cfg_kw, **override}.items() if k != "lr")),
                    torch.cuda.current_device())
+            lr = float({**self.cfg_kw, **override}.get("lr", 0.02))
             hit = self._graphs.get(key)
             if hit is not None and self._ws is not None:
                 self._graphs.move_to_end(key)
+                self._write_lr(hit[1], lr)
                 hit[0].replay()
                 self._last_slot = hit[1]
                 return
             prev, self._prev_key = getattr(self, "_prev_key", None), key
             if key != prev:
                 # first call with this key: eager, in the slot reserved for uncaptured steps (a
-                # config that changes every step, e.g. a learning-rate schedule, never captures)
+                # config that changes every step, e.g. the random-selection counter, never captures)
                 self._step(Ws, Ms, Gs, sel_out, O_out, None, m_transposed, storage_transposed, self.GRAPH_SLOTS,
-                           **override)
+                           lr_device=True, write_lr=lr, **override)
                 return
             used = {slot for (_, slot) in self._graphs.values()}
             free = [i for i in range(self.GRAPH_SLOTS) if i not in used]
@@ -263,19 +268,30 @@ class Dion2:
                 _, (_, slot) = self._graphs.popitem(last=False)
                 free = [slot]
             slot = free[0]
-            self._step(Ws, Ms, Gs, sel_out, O_out, None, m_transposed, storage_transposed, slot, **override)
+            self._step(Ws, Ms, Gs, sel_out, O_out, None, m_transposed, storage_transposed, slot, lr_device=True,
+                       write_lr=lr, **override)
             ws_before = self._ws
             g = torch.cuda.CUDAGraph()
             with torch.cuda.graph(g):  # captured, not executed: this call's step ran above
-                self._step(Ws, Ms, Gs, sel_out, O_out, None, m_transposed, storage_transposed, slot, **override)
+                self._step(Ws, Ms, Gs, sel_out, O_out, None, m_transposed, storage_transposed, slot, lr_device=True,
+                           **override)
             if self._ws is ws_before:  # a reallocated workspace invalidated every graph (cleared)
                 self._graphs[key] = (g, slot)
             return
         self._step(Ws, Ms, Gs, sel_out, O_out, stream, m_transposed, storage_transposed, 0, **override)
 
-    def _step(self, Ws, Ms, Gs, sel_out, O_out, stream, m_transposed, storage_transposed, slot, **override):
+    def _write_lr(self, slot: int, lr: float) -> None:
+        """eta into the fp32 word at byte 8 of the slot's 4096-aligned workspace base (stream-ordered)."""
+        base = self._ws.data_ptr()
+        aligned = (base + slot * self.SLOT_BYTES + 4095) & ~4095
+        off = aligned - base + 8
+        self._ws[off:off + 4].view(torch.float32).fill_(lr)
+
+    def _step(self, Ws, Ms, Gs, sel_out, O_out, stream, m_transposed, storage_transposed, slot,
+              lr_device: bool = False, write_lr: Optional[float] = None, **override):
         kw = dict(self.cfg_kw)
         kw.update(override)
+        kw["lr_device"] = lr_device
         if m_transposed is None:
             m_transposed = self.m_transposed
         if storage_transposed is None:
@@ -288,6 +304,8 @@ class Dion2:
         st = stream if stream is not None else torch.cuda.current_stream(dev)
         off = slot * self.SLOT_BYTES
         self._last_slot = slot
+        if write_lr is not None:
+            self._write_lr(slot, write_lr)
         rc = _lib().dion2_step_batched(arr, len(Ws), ctypes.byref(cfg), ws.data_ptr() + off, ws.numel() - off,
                                        st.cuda_stream)
         if rc:

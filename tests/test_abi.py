@@ -50,12 +50,20 @@ def test_config_defaults(lib):
     assert cfg.ns_form == 0 and cfg.reserved0 == 0
 
 
-@pytest.mark.parametrize("form,reserved", [(3, 0), (-1, 0), (0, 1)])
+@pytest.mark.parametrize("form,reserved", [(3, 0), (-1, 0), (0, 2), (0, 3)])
 def test_ns_form_validation(lib, form, reserved):
     cfg = D.make_config()
     cfg.ns_form, cfg.reserved0 = form, reserved
     out = ctypes.c_size_t(0)
     assert lib.dion2_workspace_size(_mats([(64, 64)]), 1, ctypes.byref(cfg), ctypes.byref(out)) == 1  # DION2_EINVAL_CONFIG
+
+
+def test_lr_device_flag_is_valid(lib):
+    """reserved0 bit 0 = DION2_FLAG_LR_DEVICE (eta read from the workspace word); other bits reserved."""
+    cfg = D.make_config(lr_device=True)
+    assert cfg.reserved0 == 1
+    out = ctypes.c_size_t(0)
+    assert lib.dion2_workspace_size(_mats([(64, 64)]), 1, ctypes.byref(cfg), ctypes.byref(out)) == 0
 
 
 def test_gram_form_workspace(lib):

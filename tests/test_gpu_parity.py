@@ -347,10 +347,11 @@ def test_cuda_graph_capture_replays_the_step():
 
 
 def test_cuda_graph_mode_equals_eager():
-    """Dion2(cuda_graph=True): a key (tensors + config) repeated on consecutive calls is
-    captured on its second call and replayed afterwards; keys that change every call (the
-    alternating gradient buffers, a learning-rate schedule) run eagerly; a second tensor set
-    and a changed learning rate capture again.  Bitwise equal to the eager optimizer."""
+    """Dion2(cuda_graph=True): a key (tensors + config minus eta) repeated on consecutive calls
+    is captured on its second call and replayed afterwards; keys that change every call (the
+    alternating gradient buffers) run eagerly; a learning-rate schedule replays one graph (eta
+    is read on the device, DION2_FLAG_LR_DEVICE); a second tensor set captures again.  Bitwise
+    equal to the eager optimizer."""
     shapes = [(512, 1024), (2048, 512), (300, 520)]
     mt = [m > n for (m, n) in shapes]
     def init(seed):
@@ -374,9 +375,12 @@ def test_cuda_graph_mode_equals_eager():
                 opt.cfg_kw["lr"] = 0.01        # new key: eager, then capture, then replay
         for t in range(4):                     # alternating buffers: every key new, all eager
             opt.step(Wa, Ma, data[t % 2])
-        for t in range(4):                     # a learning-rate schedule: never captured
-            opt.cfg_kw["lr"] = 0.02 / (t + 1)
-            opt.step(Wa, Ma, data[t + 2])
+        G2 = [torch.empty(m, n, device="cuda") for (m, n) in shapes]
+        for t in range(5):                     # a learning-rate schedule on fixed buffers: eta is read
+            opt.cfg_kw["lr"] = 0.02 / (t + 1)  # from the workspace, so the graph replays (no re-capture)
+            for g, d in zip(G2, data[t]):
+                g.copy_(d)
+            opt.step(Wa, Ma, G2)
         for t in range(3):
             opt.step(Wb, Mb, data[t])
         torch.cuda.synchronize()
