@@ -431,6 +431,38 @@ def test_step_host_pipelined_upload(graph):
         assert (a - b).abs().max() <= 1e-6 * a.abs().max()
 
 
+@pytest.mark.parametrize("chunks", [None, "3"])
+def test_lr_device_flag_through_the_c_abi(chunks, monkeypatch):
+    """DION2_FLAG_LR_DEVICE: eta comes from the fp32 word at byte 8 of the 4096-aligned workspace
+    base (cfg.lr, deliberately different, is ignored by the kernels); bitwise equal to a step with
+    cfg.lr = that eta.  Rows and column (index-walk) scatters; the chunked pipeline
+    copies the word to every chunk."""
+    import ctypes
+    from paper_2512_16928_b200 import dion2 as D
+    if chunks:
+        monkeypatch.setenv("DION2_CHUNKS", chunks)
+    shapes = [(512, 1024), (2048, 512), (300, 520), (1000, 200)]
+    def run(lr_device):
+        Ws = [torch.from_numpy(gen_w0(m, n, 12, i)).cuda() for i, (m, n) in enumerate(shapes)]
+        Ms = [torch.zeros_like(w) for w in Ws]
+        Gs = [torch.from_numpy(gen_grad(m, n, 12, i, 0, row_scaled=True)).cuda() for i, (m, n) in enumerate(shapes)]
+        arr, _ = D.describe(Ws, Ms, Gs)
+        cfg = D.make_config(alpha=0.3, lr=0.5 if lr_device else 0.0123, lr_device=lr_device)
+        need = ctypes.c_size_t(0)
+        assert D._lib().dion2_workspace_size(arr, len(Ws), ctypes.byref(cfg), ctypes.byref(need)) == 0
+        ws = torch.zeros(need.value, dtype=torch.uint8, device="cuda")
+        base = ws.data_ptr()
+        off = ((base + 4095) & ~4095) - base + 8
+        ws[off:off + 4].view(torch.float32).fill_(0.0123)
+        rc = D._lib().dion2_step_batched(arr, len(Ws), ctypes.byref(cfg), base, ws.numel(),
+                                         torch.cuda.current_stream().cuda_stream)
+        assert rc == 0
+        torch.cuda.synchronize()
+        return Ws + Ms
+    for a, b in zip(run(False), run(True)):
+        assert torch.equal(a, b)
+
+
 def test_bitwise_determinism():
     shapes = [(512, 1024), (1024, 512)]
     outs = []
