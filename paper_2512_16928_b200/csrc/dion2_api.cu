@@ -669,10 +669,12 @@ int build_device_plan(Plan& P, const dion2_matrix* mats, const dion2_config* c, 
     d.sa_pad = q.sa_pad;
     d.sb_pad = q.sb_pad;
     d.rowblocks = q.rowblocks;
-    // cols mode on tall matrices (> 32 row blocks of partials, e.g. 28672 rows): the column
-    // sums are finalised by a grid-wide kernel before K2 (one K2 CTA summing 112 partials per
-    // column was latency-bound); shorter ones are summed by K2 itself (one launch fewer)
-    const bool cf = q.axis == DION2_AXIS_COLS && q.rowblocks > 32;
+    // cols mode: the column sums of the K1 row-block partials are finalised by a grid-wide
+    // kernel before K2 (one K2 CTA summing m / 256 partials per column is latency-bound: 112
+    // partials on 28672 rows; even the 1B set's 32 gain, select 0.038 -> 0.029 ms);
+    // DION2_CF_MIN_RB = r: only matrices with >= r row blocks (the rest are summed by K2)
+    static const int cf_min = getenv("DION2_CF_MIN_RB") ? atoi(getenv("DION2_CF_MIN_RB")) : 1;
+    const bool cf = q.axis == DION2_AXIS_COLS && q.rowblocks >= cf_min;
     d.scores_final = cf ? 1 : 0;
     if (cf) {
       cf_mats.push_back(i);
