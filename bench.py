@@ -71,16 +71,14 @@ def ns_uses_gram_form(p, q, ns_form="auto"):
     return pad(q) >= 2 * pad(p) or q >= 2 * p
 
 
-def work_model(shapes, alpha, steps=5, mt=False, ns_form="auto", fused=None):
+def work_model(shapes, alpha, steps=5, mt=False, ns_form="auto"):
     """Algorithmic work per Dion2 step and per-phase algorithmic HBM bytes.
     NS FLOPs of the form the library evaluates (full products; symmetric tiles not credited):
       direct: T(4p^2 q + 2p^3)  -- gram 2p^2q, poly 2p^3, apply 2p^2q per iteration
       Gram space (R23): 4p^2 q + (4T - 3) 2p^3 (T >= 2) -- gram + apply once, T polys,
       3T - 3 products C.Q / C.A / C.(CA)."""
     ns_flops = {"ns_gram": 0.0, "ns_poly": 0.0, "ns_apply": 0.0, "ns_mul": 0.0}
-    if fused is None:  # the library default: separate launches (DION2_PRE_FUSE=1 opts in)
-        fused = os.environ.get("DION2_PRE_FUSE", "0") == "1"
-    byts = {"momentum_score": 0.0, "momentum_score_mt": 0.0, "pre_fused": 0.0}
+    byts = {"momentum_score": 0.0, "momentum_score_mt": 0.0}
     for ph in ("gather", "gather_rows", "gather_cols", "scatter", "scatter_rows", "scatter_cols"):
         byts[ph] = 0.0
     for (m, n) in shapes:
@@ -107,12 +105,6 @@ def work_model(shapes, alpha, steps=5, mt=False, ns_form="auto", fused=None):
         else:
             sfx = ""
         gsfx = "_rows" if (mt and not rows) else sfx           # transposed M: row gather of M^T
-        if fused and rows and sfx == "_rows" and d <= 8192:
-            # k_pre_fused_rows: K1 + select + gather of this matrix in one launch (same algorithmic bytes)
-            byts[k1] -= m * n * 12.0 + d * 4.0
-            byts["pre_fused"] += m * n * 12.0 + d * 4.0 + k * o * (4.0 + 4.0 + 2.0)
-            byts["scatter" + sfx] += k * o * (2.0 + 4.0 + 4.0)
-            continue
         byts["gather" + gsfx] += k * o * (4.0 + 4.0 + 2.0)    # read M[K], write mu*M[K], write bf16 X
         byts["scatter" + sfx] += k * o * (2.0 + 4.0 + 4.0)    # read bf16 O, read+write W[K]
     return ns_flops, byts
@@ -372,10 +364,7 @@ def run_ours(args):
         ms_eager = time_steps(opt_e, Ws, Ms, Gs, args.steps, args.warmup, None)
         del opt_e
 
-    # per-phase device time (CUDA events on the launching stream around every launch), with
-    # the chunked two-stream pipeline disabled so every kernel is timed in isolation
-    prev_chunks = os.environ.get("DION2_CHUNKS")
-    os.environ["DION2_CHUNKS"] = "1"
+    # per-phase device time (CUDA events on the launching stream around every launch)
     opt_iso = Dion2(alpha=args.alpha, axis="auto", precision="bf16", m_transposed=mts, ns_form=args.ns_form) \
         if not use_dist else make_opt(args.alpha)  # eager: the phase events are recorded per host launch
     opt_iso.step(Ws, Ms, Gs)  # build the plan outside the timed pass
@@ -384,16 +373,10 @@ def run_ours(args):
     phases = get_phase_times()
     set_phase_timing(False)
     del opt_iso
-    if prev_chunks is None:
-        del os.environ["DION2_CHUNKS"]
-    else:
-        os.environ["DION2_CHUNKS"] = prev_chunks
     torch.cuda.empty_cache()
 
     peaks, peak_src = load_peaks()
-    fused = (not use_dist and os.environ.get("DION2_PRE_FUSE", "0") == "1"
-             and os.environ.get("DION2_CHUNKS", "1") == "1")
-    ns_flops, byts = work_model(shapes, args.alpha, mt=not args.no_mt, ns_form=args.ns_form, fused=fused)
+    ns_flops, byts = work_model(shapes, args.alpha, mt=not args.no_mt, ns_form=args.ns_form)
     if use_dist:  # this rank's share: 1/world of every streaming pass, NS of its owned matrices
         owned = [s for s, o in zip(shapes, info["owner"]) if o == rank]
         ns_flops = work_model(owned, args.alpha, ns_form=args.ns_form)[0] if owned else {k: 0.0 for k in ns_flops}
@@ -568,8 +551,7 @@ def run_ours(args):
             "step_mode": "CUDA graph replay of the C-ABI step (Dion2(cuda_graph=True))" if (not use_dist and not args.no_graph)
                          else "eager",
             "ms_per_step_unpipelined_with_phase_events": ms_timed,
-            "phases_note": "per-kernel times (CUDA events around every launch) from a separate K-step pass "
-                           "with the chunked pipeline off (DION2_CHUNKS=1, also the default)",
+            "phases_note": "per-kernel times (CUDA events around every launch) from a separate K-step pass",
             "phases": per_phase,
             "roofline": roof,
             "cpu_baseline": cpu,

@@ -25,7 +25,7 @@ namespace dion2rt {
 const char* kPhaseNames[kNumPhases] = {"momentum_score", "select",       "gather",       "norm",
                                        "ns_gram",        "ns_poly",      "ns_apply",     "scatter",
                                        "full_decay",     "gather_rows",  "gather_cols",  "scatter_rows",
-                                       "scatter_cols",   "ns_mul",       "momentum_score_mt", "pre_fused"};
+                                       "scatter_cols",   "ns_mul",       "momentum_score_mt"};
 
 std::mutex g_mu;
 int g_sm_count = 0;
@@ -165,8 +165,8 @@ std::string plan_key(const dion2_matrix* mats, int n, const dion2_config* c, voi
 // every plan-cache key
 std::string env_key() {
   std::string k;
-  for (const char* v : {"DION2_NS_PAIR", "DION2_NS_SYM", "DION2_NS_CHAIN", "DION2_NS_SERPENTINE", "DION2_NS_UPPER",
-                        "DION2_PRE_FUSE", "DION2_FUSE_LAG_MB", "DION2_GRAM_SPLITK", "DION2_DIST_INPLACE"}) {
+  for (const char* v : {"DION2_NS_PAIR", "DION2_NS_SYM", "DION2_NS_SERPENTINE", "DION2_NS_UPPER",
+                        "DION2_GRAM_SPLITK"}) {
     const char* e = getenv(v);
     k.append(e ? e : "-");
     k.push_back('|');
@@ -265,7 +265,6 @@ int build_layout(Plan& P, const dion2_matrix* mats, int n, const dion2_config* c
     P.off_fl_sprefix[l] = take(4 * (size_t)n);
   }
   for (auto& g : P.groups) g.off_gmats = take(4 * (size_t)g.count);
-  P.off_chain_entries = take(4 * (size_t)n);
   P.off_cf_mats = take(4 * (size_t)n);
   P.off_cf_prefix = take(8 * (size_t)n);
   P.off_nsscale = take(8 * (size_t)n);
@@ -341,86 +340,6 @@ int build_layout(Plan& P, const dion2_matrix* mats, int n, const dion2_config* c
 //   apply  X1  = s Q_T X0                             (bf16)
 // Every p x p product is a polynomial in A_0, hence symmetric: upper-triangle pair tiles,
 // mirrored.  Q_T is written as bf16 (the apply operand), everything else as fp16.
-// The Gram-space op list of one matrix on the five p x p buffers (A, C, Q0, Q1, B), in the
-// order poly, C.A, C.Q, C.B per iteration (C.Q between the two dependent products hides
-// C.B's wait for C.A), with each op's dependency: the latest earlier op that wrote one of
-// its operands or read / wrote its output buffer.
-static std::vector<ChainOp> chain_ops(const dion2_config* c, int T) {
-  enum { bA = 0, bC = 1, bQ0 = 2, bQ1 = 3, bB = 4 };
-  auto Cb = [](int t) { return t == 0 ? (int)bQ0 : (int)bC; };  // C_0 doubles as Q_1
-  auto Qb = [](int j) { return (j & 1) ? (int)bQ0 : (int)bQ1; };  // Q_j, j >= 1
-  std::vector<ChainOp> ops;
-  int last_w[kChainBufs], last_r[kChainBufs];
-  for (int i = 0; i < kChainBufs; ++i) last_w[i] = last_r[i] = -1;
-  auto add = [&](int a, int b, int out, int cin, int out_f16, float cacc, float cC, float diag) {
-    ChainOp o{};
-    o.a = (int8_t)a; o.b = (int8_t)b; o.out = (int8_t)out; o.cin = (int8_t)cin; o.out_f16 = (int8_t)out_f16;
-    o.cacc = cacc; o.cC = cC; o.diag = diag;
-    int dep = std::max({last_w[a], last_w[b], last_w[out], last_r[out]});
-    if (cin >= 0) dep = std::max(dep, last_w[cin]);
-    o.dep = (int8_t)dep;
-    o.cin_dep = (int8_t)(cin >= 0 ? last_w[cin] : -1);
-    const int idx = (int)ops.size();
-    last_r[a] = std::max(last_r[a], idx);
-    last_r[b] = std::max(last_r[b], idx);
-    if (cin >= 0) last_r[cin] = std::max(last_r[cin], idx);
-    last_w[out] = idx;
-    ops.push_back(o);
-  };
-  for (int t = 0; t < T; ++t) {
-    const float a = c->ns_coeffs[t][0], b = c->ns_coeffs[t][1], cc = c->ns_coeffs[t][2];
-    const bool last = t == T - 1;
-    add(bA, bA, Cb(t), bA, T == 1 ? 0 : 1, cc, b, a);                  // C_t = a I + b A + c A A
-    if (!last) add(Cb(t), bA, bB, -1, 1, 1.f, 0.f, 0.f);               // B = C_t A
-    if (t >= 1) add(Cb(t), Qb(t), Qb(t + 1), -1, last ? 0 : 1, 1.f, 0.f, 0.f);  // Q_{t+1} = C_t Q_t
-    if (!last) add(Cb(t), bB, bA, -1, 1, 1.f, 0.f, 0.f);               // A = C_t B
-  }
-  return ops;
-}
-
-// One chain launch per kMaxGroups Gram-space groups; the entry table (group, z), largest
-// p first, lives in the plan's uploaded table region.
-static int append_chain_launches(Plan& P, const dion2_config* c, void* ws, const std::vector<int>& gl) {
-  const std::vector<ChainOp> ops = chain_ops(c, P.ns_steps);
-  if ((int)ops.size() > kMaxChainOps) return DION2_EUNSUPPORTED;
-  int32_t* ent_host = reinterpret_cast<int32_t*>(P.host_tables.data() + (P.off_chain_entries - P.off_desc));
-  const int32_t* ent_dev = (const int32_t*)tab(P, P.off_chain_entries);
-  int ent_off = 0;
-  for (size_t s0 = 0; s0 < gl.size(); s0 += kMaxGroups) {
-    Launch L{};
-    L.phase = PH_NSMUL;
-    L.kind = 4;
-    L.chain = std::make_shared<NsChainParams>();
-    NsChainParams& cp = *L.chain;
-    memset(&cp, 0, sizeof(cp));
-    cp.ngroups = (int)std::min<size_t>(kMaxGroups, gl.size() - s0);
-    cp.nops = (int)ops.size();
-    for (size_t i = 0; i < ops.size(); ++i) cp.ops[i] = ops[i];
-    std::vector<std::pair<int, int32_t>> ents;  // (p_pad, packed)
-    for (int j = 0; j < cp.ngroups; ++j) {
-      const Group& g = P.groups[gl[s0 + j]];
-      const size_t offs[kChainBufs] = {g.off_A, g.off_C, g.off_Q0, g.off_Q1, g.off_B};
-      for (int b = 0; b < kChainBufs; ++b) {
-        void* base = at(ws, offs[b]);
-        cp.buf[j][b] = base;
-        if (!make_map(&cp.ld[j][b], base, g.p_pad, g.p_pad, g.count, 64, 128)) return DION2_ECUDA;
-        if (!make_map(&cp.st[j][b], base, g.p_pad, g.p_pad, g.count, 32, 32, CU_TENSOR_MAP_SWIZZLE_64B))
-          return DION2_ECUDA;
-      }
-      cp.mstride[j] = (long long)g.p_pad * g.p_pad;
-      cp.p_pad[j] = g.p_pad;
-      for (int z = 0; z < g.count; ++z) ents.push_back({g.p_pad, (int32_t)((j << 24) | z)});
-    }
-    std::stable_sort(ents.begin(), ents.end(), [](const auto& x, const auto& y) { return x.first > y.first; });
-    for (size_t i = 0; i < ents.size(); ++i) ent_host[ent_off + i] = ents[i].second;
-    cp.entries = ent_dev + ent_off;
-    cp.n_entries = (int)ents.size();
-    ent_off += (int)ents.size();
-    P.ns_launches.push_back(L);
-  }
-  return DION2_OK;
-}
-
 static int append_gram_space_launches(Plan& P, const dion2_config* c, void* ws, int pair_mode) {
   std::vector<int> gl;
   for (int gi = 0; gi < (int)P.groups.size(); ++gi)
@@ -511,19 +430,9 @@ static int append_gram_space_launches(Plan& P, const dion2_config* c, void* ws, 
   auto Qb = [&](int gi, int j) { return at(ws, (j & 1) ? P.groups[gi].off_Q0 : P.groups[gi].off_Q1); };  // Q_j, j >= 1
   int rc;
   std::vector<Entry> es;
-  // p x p products: one flat launch per op over all matrices, or (DION2_NS_CHAIN=1) one
-  // persistent chain launch in which a CTA pair runs one matrix's whole op list
-  // (k_ns_chain_pair.cu; measured slower, kept as an option)
-  const char* chain_env = getenv("DION2_NS_CHAIN");
-  const bool use_chain = chain_env && atoi(chain_env) != 0;
+  // p x p products: one flat launch per op over all matrices
   for (int gi : gl) es.push_back({gi, X0(gi), X0(gi), Ab(gi), nullptr});
-  if ((rc = emit(PH_GRAM, es, 1.f, 0.f, 0.f, 2, 0, 1, /*mirror_out=*/use_chain))) return rc;
-  if (use_chain) {
-    if ((rc = append_chain_launches(P, c, ws, gl))) return rc;
-    es.clear();
-    for (int gi : gl) es.push_back({gi, Qb(gi, T), X0(gi), X1(gi), nullptr});
-    return emit(PH_APPLY, es, 1.f, 0.f, 0.f, 1, 0, 0);
-  }
+  if ((rc = emit(PH_GRAM, es, 1.f, 0.f, 0.f, 2, 0, 1))) return rc;
   for (int t = 0; t < T; ++t) {
     const float a = c->ns_coeffs[t][0], b = c->ns_coeffs[t][1], cc = c->ns_coeffs[t][2];
     const int last = t == T - 1;
@@ -545,69 +454,6 @@ static int append_gram_space_launches(Plan& P, const dion2_config* c, void* ws, 
   es.clear();
   for (int gi : gl) es.push_back({gi, Qb(gi, T), X0(gi), X1(gi), nullptr});
   return emit(PH_APPLY, es, 1.f, 0.f, 0.f, 1, 0, 0);
-}
-
-// Task table of the fused pre-stage (k_pre_fused.cu).  Ticket order: each fused matrix's
-// K1 row tasks, then its select; its gather tasks are handed out once DION2_FUSE_LAG_MB
-// (default 96) MB of later K1 traffic has been handed out, so the select has finished
-// when the gathers start while the matrix's selected rows of M are still L2-resident.
-int build_fuse_tables(Plan& P, const dion2_matrix* mats, const std::vector<char>& fused) {
-  const int n = P.n;
-  P.fuse_tasks = 0;
-  P.fuse_rest_n = 0;
-  P.fuse_max_d = 0;
-  P.fuse_host.clear();
-  int nf = 0;
-  for (int i = 0; i < n; ++i) nf += fused[i];
-  if (nf == 0) return DION2_OK;
-  const char* e = getenv("DION2_FUSE_LAG_MB");
-  const int64_t lag = (int64_t)(e ? atof(e) : 96.0) * (1 << 20);
-  std::vector<int4> tasks;
-  std::vector<int32_t> need(n, 0), rest;
-  std::vector<std::pair<int, int64_t>> pending;  // (matrix, K1 bytes handed out at its select)
-  size_t head = 0;
-  int64_t k1_bytes = 0;
-  auto emit_gathers = [&](int i) {
-    const int pp = P.mp[i].p_pad;
-    for (int r0 = 0; r0 < pp; r0 += 8) tasks.push_back(make_int4(2, i, r0, std::min(pp, r0 + 8)));
-  };
-  for (int i = 0; i < n; ++i) {
-    if (!fused[i]) {
-      rest.push_back(i);
-      continue;
-    }
-    const int64_t rows = mats[i].rows, cols = mats[i].cols;
-    const int rpt = 2;  // a row pair per task: the CTA streams both rows at once
-    for (int64_t r0 = 0; r0 < rows; r0 += rpt) {
-      const int64_t r1 = std::min<int64_t>(rows, r0 + rpt);
-      tasks.push_back(make_int4(0, i, (int)r0, (int)r1));
-      need[i]++;
-      k1_bytes += (r1 - r0) * cols * 12;
-      while (head < pending.size() && k1_bytes - pending[head].second >= lag) emit_gathers(pending[head++].first);
-    }
-    tasks.push_back(make_int4(1, i, 0, 0));
-    pending.push_back({i, k1_bytes});
-    P.fuse_max_d = std::max(P.fuse_max_d, P.mp[i].d);
-  }
-  while (head < pending.size()) emit_gathers(pending[head++].first);
-  P.fuse_tasks = (int)tasks.size();
-  P.fuse_rest_n = (int)rest.size();
-  size_t off = align_up(16 * tasks.size(), 256);
-  P.fuse_off_need = off;
-  off = align_up(off + 4 * (size_t)n, 256);
-  P.fuse_off_ctr = off;
-  off = align_up(off + 4 * (size_t)(1 + 2 * n), 256);
-  P.fuse_off_rest = off;
-  off = align_up(off + 4 * (size_t)std::max(1, n), 256);
-  P.fuse_host.assign(off, 0);
-  memcpy(P.fuse_host.data(), tasks.data(), 16 * tasks.size());
-  memcpy(P.fuse_host.data() + P.fuse_off_need, need.data(), 4 * (size_t)n);
-  if (!rest.empty()) memcpy(P.fuse_host.data() + P.fuse_off_rest, rest.data(), 4 * rest.size());
-  if (P.dfuse) cudaFree(P.dfuse);
-  P.dfuse = nullptr;
-  if (cudaMalloc(&P.dfuse, off) != cudaSuccess) return DION2_ECUDA;
-  P.last_ptrs.clear();  // forces the table upload (refresh_tables) before the first step
-  return DION2_OK;
 }
 
 // Fill host tables and NS launches for a concrete workspace.
@@ -633,13 +479,6 @@ int build_device_plan(Plan& P, const dion2_matrix* mats, const dion2_config* c, 
   P.fl_maxn = 0;
   int64_t rows_acc = 0, ctiles_acc = 0;
   int gt_acc = 0;
-  // fused pre-stage membership: rows-mode matrices on the rows streaming gather
-  std::vector<char> fused(n, 0);
-  if (P.allow_fuse)
-    for (int i = 0; i < n; ++i) {
-      const MatPlan& q = P.mp[i];
-      fused[i] = q.axis == DION2_AXIS_ROWS && q.path == 1 && !q.mt && q.d <= kFuseMaxD;
-    }
   P.generic_gather_mats = 0;
   P.generic_scatter_mats = 0;
   for (int i = 0; i < n; ++i) {
@@ -695,7 +534,7 @@ int build_device_plan(Plan& P, const dion2_matrix* mats, const dion2_config* c, 
     // (path 2) or generic tiles; scatter: by path (generic tiles for path 0)
     const int lg = (q.path == 1 || q.mt) ? 0 : (q.path == 2 ? 1 : -1);
     const int ls = q.spath - 1;
-    if (lg >= 0 && !fused[i]) {
+    if (lg >= 0) {
       flg_mats[lg].push_back(i);
       fl_gp[lg].push_back(P.fl_gunits[lg]);
       P.fl_gunits[lg] += lg == 0 ? q.p_pad : q.q_pad / 32;
@@ -709,7 +548,6 @@ int build_device_plan(Plan& P, const dion2_matrix* mats, const dion2_config* c, 
     if (lg == 1) P.fl_maxk = std::max(P.fl_maxk, q.k);
     if (ls == 1) P.fl_smaxk = std::max(P.fl_smaxk, q.k);
     if (q.axis == DION2_AXIS_ROWS) {
-      if (fused[i]) continue;
       rowmats.push_back(i);
       rowprefix.push_back(rows_acc);
       rows_acc += mats[i].rows;
@@ -760,7 +598,6 @@ int build_device_plan(Plan& P, const dion2_matrix* mats, const dion2_config* c, 
     memcpy(H(P.off_cf_mats), cf_mats.data(), 4 * cf_mats.size());
     memcpy(H(P.off_cf_prefix), cf_prefix.data(), 8 * cf_prefix.size());
   }
-  if (int rc = build_fuse_tables(P, mats, fused)) return rc;
   for (auto& g : P.groups) memcpy(H(g.off_gmats), g.mats.data(), 4 * g.mats.size());
 
   // ---- Newton-Schulz launch list: per iteration t: gram, poly, apply; per phase the
@@ -887,7 +724,6 @@ void ensure_device_attrs() {
   ns_tc_set_attrs();
   launch_fast_paths_attrs();
   ns_pair_set_attrs();
-  ns_chain_set_attrs();
   cudaFuncSetAttribute(k_topk_select, cudaFuncAttributeMaxDynamicSharedMemorySize, 4 * DION2_MAX_SELECT_DIM);
   cudaFuncSetAttribute(k_full_decay, cudaFuncAttributeMaxDynamicSharedMemorySize, DION2_MAX_SELECT_DIM);
   g_attr_done = true;
@@ -905,9 +741,7 @@ int run_ns(Plan& P, const dion2_config* c, Launcher& L, cudaStream_t s, bool do_
   }
   for (const Launch& ln : P.ns_launches) {
     L.begin(ln.phase);
-    if (ln.kind == 4) {
-      launch_ns_chain(std::min(2 * ln.chain->n_entries, sms & ~1), s, *ln.chain);
-    } else if (ln.kind == 3) {
+    if (ln.kind == 3) {
       const int sk = ln.tc.p.splitk > 1 ? ln.tc.p.splitk : 1;
       launch_ns_pair(std::min(2 * ln.tc.p.total_tiles * sk, sms & ~1), s, ln.tc);
       if (sk > 1) launch_splitk_reduce(s, ln.tc.p);
@@ -954,9 +788,6 @@ int refresh_tables(Plan& P, const dion2_matrix* mats, const dion2_config* c, cud
   }
   if (upload &&
       cudaMemcpyAsync(P.dtab, P.host_tables.data(), P.host_tables.size(), cudaMemcpyHostToDevice, s) != cudaSuccess)
-    return DION2_ECUDA;
-  if (upload && P.fuse_tasks &&
-      cudaMemcpyAsync(P.dfuse, P.fuse_host.data(), P.fuse_host.size(), cudaMemcpyHostToDevice, s) != cudaSuccess)
     return DION2_ECUDA;
   return DION2_OK;
 }
@@ -1019,22 +850,6 @@ void stage_k1_select(Plan& P, const dion2_config* c, void* ws, int32_t* status, 
   const int n = P.n;
   const MatDesc* dmats = (const MatDesc*)tab(P, P.off_desc);
   int32_t* bad = (int32_t*)at(ws, P.off_bad);
-  if (P.fuse_tasks) {
-    // K1 + K2 + K3 of the rows-mode matrices in one launch (k_pre_fused.cu)
-    static const bool hint = !getenv("DION2_FUSE_NOHINT");
-    uint8_t* fb = static_cast<uint8_t*>(P.dfuse);
-    int32_t* ctr = reinterpret_cast<int32_t*>(fb + P.fuse_off_ctr);
-    const size_t smem = 4 * (size_t)P.fuse_max_d;
-    const int sms = g_sm_count > 0 ? g_sm_count : 148;
-    const int per_sm = std::max(1, pre_fused_blocks_per_sm(hint, smem));
-    L.begin(PH_PRE_FUSED);
-    if (cudaMemsetAsync(ctr, 0, 4 * (size_t)(1 + 2 * n), s) != cudaSuccess) L.err = DION2_ECUDA;
-    launch_pre_fused_rows(hint, std::min(per_sm * sms, P.fuse_tasks), smem, s, dmats,
-                          reinterpret_cast<const int4*>(fb), P.fuse_tasks, ctr,
-                          reinterpret_cast<const int32_t*>(fb + P.fuse_off_need), n, bad, status, c->mu,
-                          c->select == DION2_SELECT_RANDOM, c->seed, c->step);
-    L.end();
-  }
   if (P.n_row_mats) {
     L.begin(PH_K1);
     const int blocks = stream_grid(ceil_div(P.total_rows, 8), 8, persistent);
@@ -1057,7 +872,7 @@ void stage_k1_select(Plan& P, const dion2_config* c, void* ws, int32_t* status, 
                  (const int64_t*)tab(P, P.off_mtprefix), P.n_mt_mats);
     L.end();
   }
-  const int n_sel = P.fuse_tasks ? P.fuse_rest_n : n;
+  const int n_sel = n;
   if (P.cf_n) {
     L.begin(PH_SELECT);
     k_col_scores_finalize<<<(unsigned)ceil_div(P.cf_total, 32), 256, 0, s>>>(
@@ -1066,8 +881,7 @@ void stage_k1_select(Plan& P, const dion2_config* c, void* ws, int32_t* status, 
   }
   if (n_sel) {
     L.begin(PH_SELECT);
-    const int32_t* list =
-        P.fuse_tasks ? reinterpret_cast<const int32_t*>(static_cast<uint8_t*>(P.dfuse) + P.fuse_off_rest) : nullptr;
+    const int32_t* list = nullptr;
     k_topk_select<<<n_sel, kSelectThreads, 4 * P.max_d, s>>>(dmats, list, bad, status,
                                                              c->select == DION2_SELECT_RANDOM, c->seed, c->step);
     L.end();
@@ -1157,108 +971,6 @@ void stage_post(Plan& P, const dion2_matrix* mats, const dion2_config* c, void* 
   }
 }
 
-// ------------------------------------------------------------------ chunked pipeline
-// The matrices are split into C contiguous chunks (equal parameter counts), each with its
-// own sub-plan and workspace region.  Chunk c's Newton-Schulz runs on a library-owned
-// high-priority stream while the caller's stream runs chunk c+1's momentum/score/select/
-// gather and chunk c-1's scatter: the tensor-bound NS and the HBM-bound passes overlap.
-// (Matrices are independent; every matrix still sees Alg. 1 in order.)
-struct ChunkedPlan {
-  std::vector<std::unique_ptr<Plan>> subs;
-  std::vector<int> first, count;
-  std::vector<size_t> off;        // sub-plan workspace offsets from the aligned base
-  size_t total = 0;
-  std::vector<cudaEvent_t> ev;    // fork + pre/ns done per chunk
-};
-std::map<std::string, std::unique_ptr<ChunkedPlan>> g_cplans;
-
-cudaStream_t ns_stream() {
-  static cudaStream_t st = nullptr;
-  if (!st) {
-    int least = 0, greatest = 0;
-    cudaDeviceGetStreamPriorityRange(&least, &greatest);
-    cudaStreamCreateWithPriority(&st, cudaStreamNonBlocking, greatest);
-  }
-  return st;
-}
-
-// Opt-in (DION2_CHUNKS=c): measured on the 1B set the overlapped kernels contend for DRAM
-// and the unpipelined step is faster (6.87-6.89 ms vs 6.97-7.01 ms with 2 chunks), so the
-// default is a single chunk.
-int chunk_count(const dion2_matrix* mats, int n) {
-  (void)mats;
-  if (const char* e = getenv("DION2_CHUNKS")) return std::max(1, std::min(n, atoi(e)));
-  return 1;
-}
-
-int build_chunked_layout(ChunkedPlan& C, const dion2_matrix* mats, int n, const dion2_config* c, int chunks) {
-  int64_t total = 0;
-  for (int i = 0; i < n; ++i) total += mats[i].rows * mats[i].cols;
-  int64_t acc = 0;
-  int start = 0;
-  for (int i = 0; i < n; ++i) {
-    acc += mats[i].rows * mats[i].cols;
-    const int j = (int)C.first.size();
-    if (j < chunks - 1 && acc * chunks >= total * (j + 1) && i + 1 < n) {
-      C.first.push_back(start);
-      C.count.push_back(i + 1 - start);
-      start = i + 1;
-    }
-  }
-  C.first.push_back(start);
-  C.count.push_back(n - start);
-  size_t off = 0;
-  for (size_t j = 0; j < C.first.size(); ++j) {
-    auto P = std::make_unique<Plan>();
-    int rc = build_layout(*P, mats + C.first[j], C.count[j], c);
-    if (rc) return rc;
-    C.off.push_back(off);
-    off = align_up(off + P->total, 4096);
-    C.subs.push_back(std::move(P));
-  }
-  C.total = off + 4096;
-  return DION2_OK;
-}
-
-int run_chunked(ChunkedPlan& C, const dion2_matrix* mats, const dion2_config* c, void* ws, cudaStream_t s0) {
-  const int nc = (int)C.subs.size();
-  cudaStream_t s1 = ns_stream();
-  if (C.ev.empty()) {
-    C.ev.resize(2 * nc + 1);
-    for (auto& e : C.ev) cudaEventCreateWithFlags(&e, cudaEventDisableTiming);
-  }
-  int rc = 0;
-  for (int j = 0; j < nc; ++j)
-    if ((rc = refresh_tables(*C.subs[j], mats + C.first[j], c, s0))) return rc;
-  int32_t* status = (int32_t*)at(ws, C.off[0] + C.subs[0]->off_status);  // the workspace's status word
-  if ((rc = reset_status(status, s0))) return rc;
-  if (c->reserved0 & DION2_FLAG_LR_DEVICE)  // every chunk's K7 reads eta from its own status block
-    for (int j = 1; j < nc; ++j)
-      if (cudaMemcpyAsync(at(ws, C.off[j] + C.subs[j]->off_status + 8), at(ws, C.subs[0]->off_status + 8), 4,
-                          cudaMemcpyDeviceToDevice, s0) != cudaSuccess)
-        return DION2_ECUDA;
-  Launcher L0{s0}, L1{s1};
-  cudaEventRecord(C.ev[0], s0);  // fork: s1 follows everything enqueued on s0 so far
-  cudaStreamWaitEvent(s1, C.ev[0], 0);
-  for (int j = 0; j < nc; ++j) {
-    Plan& P = *C.subs[j];
-    void* wsj = at(ws, C.off[j]);
-    stage_pre(P, c, wsj, status, L0, s0, false);
-    cudaEventRecord(C.ev[1 + 2 * j], s0);
-    cudaStreamWaitEvent(s1, C.ev[1 + 2 * j], 0);
-    run_ns(P, c, L1, s1, true);
-    cudaEventRecord(C.ev[2 + 2 * j], s1);
-    if (j > 0) {
-      cudaStreamWaitEvent(s0, C.ev[2 + 2 * (j - 1)], 0);
-      stage_post(*C.subs[j - 1], mats + C.first[j - 1], c, at(ws, C.off[j - 1]), L0, s0, false);
-    }
-  }
-  cudaStreamWaitEvent(s0, C.ev[2 + 2 * (nc - 1)], 0);  // join
-  stage_post(*C.subs[nc - 1], mats + C.first[nc - 1], c, at(ws, C.off[nc - 1]), L0, s0, false);
-  g_last_launches = L0.count + L1.count;
-  return L0.err ? L0.err : L1.err;
-}
-
 int run_step(Plan& P, const dion2_matrix* mats, const dion2_config* c, void* ws, cudaStream_t s) {
   int rc = refresh_tables(P, mats, c, s);
   if (rc) return rc;
@@ -1309,14 +1021,6 @@ int dion2_workspace_size(const dion2_matrix* user_mats, int32_t n, const dion2_c
   const dion2_matrix* mats = sv.data();
   for (int i = 0; i < n; ++i)
     if ((rc = validate_shape(mats[i], false))) return rc;
-  const int chunks = chunk_count(mats, n);
-  if (chunks > 1) {
-    ChunkedPlan C;
-    rc = build_chunked_layout(C, mats, n, cfg, chunks);
-    if (rc) return rc;
-    *bytes_out = C.total;
-    return DION2_OK;
-  }
   Plan P;
   rc = build_layout(P, mats, n, cfg);
   if (rc) return rc;
@@ -1340,31 +1044,6 @@ int dion2_step_batched(const dion2_matrix* user_mats, int32_t n, const dion2_con
   void* ws = reinterpret_cast<void*>(align_up(reinterpret_cast<uintptr_t>(workspace), 4096));
   const size_t slack = (uintptr_t)ws - (uintptr_t)workspace;
   std::string key = plan_key(mats, n, cfg, ws);
-  const int chunks = chunk_count(mats, n);
-  if (chunks > 1) {
-    key.append(reinterpret_cast<const char*>(&chunks), sizeof chunks);
-    auto ct = g_cplans.find(key);
-    ChunkedPlan* C;
-    if (ct == g_cplans.end()) {
-      auto nc = std::make_unique<ChunkedPlan>();
-      rc = build_chunked_layout(*nc, mats, n, cfg, chunks);
-      if (rc) return rc;
-      if (nc->total - 4096 + slack > ws_bytes) return DION2_EWORKSPACE;
-      for (size_t j = 0; j < nc->subs.size(); ++j) {
-        Plan& S = *nc->subs[j];
-        if ((rc = build_device_plan(S, mats + nc->first[j], cfg, at(ws, nc->off[j])))) return rc;
-        MatDesc* D = reinterpret_cast<MatDesc*>(S.host_tables.data());
-        for (int i = 0; i < S.n; ++i) D[i].mid = nc->first[j] + i;  // global matrix id (status, random keys)
-        S.id = g_next_plan_id++;
-      }
-      C = nc.get();
-      g_cplans[key] = std::move(nc);
-    } else {
-      C = ct->second.get();
-      if (C->total - 4096 + slack > ws_bytes) return DION2_EWORKSPACE;
-    }
-    return run_chunked(*C, mats, cfg, ws, reinterpret_cast<cudaStream_t>(stream));
-  }
   auto it = g_plans.find(key);
   Plan* P;
   if (it == g_plans.end()) {
@@ -1372,10 +1051,6 @@ int dion2_step_batched(const dion2_matrix* user_mats, int32_t n, const dion2_con
     rc = build_layout(*np, mats, n, cfg);
     if (rc) return rc;
     if (np->total - 4096 + slack > ws_bytes) return DION2_EWORKSPACE;
-    // run_step runs K1/K2 and K3 back to back, so the fused pre-stage may apply: opt-in
-    // (DION2_PRE_FUSE=1), measured slower than the separate launches
-    const char* fz = getenv("DION2_PRE_FUSE");
-    np->allow_fuse = fz && fz[0] == '1';
     rc = build_device_plan(*np, mats, cfg, ws);
     if (rc) return rc;
     np->id = g_next_plan_id++;

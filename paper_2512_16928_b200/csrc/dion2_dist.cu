@@ -416,11 +416,9 @@ int build_tables(DistPlan& D, const dion2_config* c, void* ws) {
     // In-place pieces: a Gram-space owner group whose q is a whole number of 256-column tiles
     // and of 64-column k-blocks per rank piece (q_pad == q, qo % 64 == 0, P <= 8) has its gram
     // and apply read X0 straight from the received pieces and its apply write X_T straight into
-    // the outgoing pieces (no assemble / disassemble copies).  DION2_DIST_INPLACE=0 disables.
+    // the outgoing pieces (no assemble / disassemble copies); other groups are copied.
     std::vector<int32_t> inpl(D.owned.size(), 0);
-    const char* ie = getenv("DION2_DIST_INPLACE");
-    const bool inplace_on = !(ie && ie[0] == '0') && P <= kMaxPieceRanks;
-    const bool inplace_in_only = ie && ie[0] == '2';  // A/B: pieces read in place, X_T still copied out
+    const bool inplace_on = P <= kMaxPieceRanks;
     CUtensorMap* hmaps = reinterpret_cast<CUtensorMap*>(H(D.t_pmaps));
     std::vector<int> g_ok(D.owner->groups.size(), 0);
     for (size_t gi = 0; gi < D.owner->groups.size() && inplace_on; ++gi) {
@@ -444,7 +442,7 @@ int build_tables(DistPlan& D, const dion2_config* c, void* ws) {
           return DION2_ECUDA;
       }
       g_ok[gi] = 1;
-      for (int i : g.mats) inpl[i] = inplace_in_only ? 2 : 1;
+      for (int i : g.mats) inpl[i] = 1;
     }
     // point the owner plan's gram (A = B = X0) and apply (B = X0, D = X_T) launches at the pieces
     for (Launch& ln : D.owner->ns_launches) {
@@ -460,7 +458,7 @@ int build_tables(DistPlan& D, const dion2_config* c, void* ws) {
           G.pieces_qo = q0.qo;
           G.pieces_P = P;
           G.pieces_map = (int)(gi * 3 * P);
-          G.pieces_store = ln.phase == PH_APPLY && !inplace_in_only;
+          G.pieces_store = ln.phase == PH_APPLY;
           for (int k = 0; k < 3 * P; ++k) ln.tc.mapP[j][k] = hmaps[gi * 3 * P + k];
         }
       }

@@ -339,106 +339,6 @@ __global__ void __launch_bounds__(256) k_gather_cols_t(const MatDesc* __restrict
   }
 }
 
-// slab_h (32 or 16): rows of the 32-row unit processed per staged O tile; 16 halves the
-// shared tile for large k (k = 1024: 66 KB -> 33 KB, 2 -> 4 resident blocks per SM)
-template <int kScU, bool kScAll>
-__global__ void __launch_bounds__(256) k_scatter_cols_t(const MatDesc* __restrict__ mats,
-                                                        const int32_t* __restrict__ list_mats,
-                                                        const int32_t* __restrict__ list_prefix, int n_list,
-                                                        int total_units, const int32_t* __restrict__ bad, float lr,
-                                                        const float* __restrict__ lr_dev, int mask_words, int slab_h) {
-  extern __shared__ __align__(16) uint8_t sm[];
-  uint32_t* mask = reinterpret_cast<uint32_t*>(sm);
-  int32_t* rank = reinterpret_cast<int32_t*>(sm + 4 * mask_words);
-  __nv_bfloat16* tile = reinterpret_cast<__nv_bfloat16*>(sm + 8 * mask_words);  // [kSlab][ldt]
-  int cur_mat = -1;
-  const int lane = threadIdx.x & 31, wid = threadIdx.x >> 5;
-  for (int u = blockIdx.x; u < total_units; u += gridDim.x) {
-    const int li = find_unit(list_prefix, n_list, u);
-    const int mi = list_mats[li];
-    const MatDesc& md = mats[mi];
-    const int slab = u - list_prefix[li];
-    if (bad[mi] || slab * kSlab >= md.rows) continue;  // block-uniform
-    if (mi != cur_mat) {
-      build_mask(md, mask, rank);
-      cur_mat = mi;
-    }
-    const int k = md.k;
-    const int ldt = scatter_tile_ld(k);
-    const int parts = slab_h / 8;
-    for (int h0 = 0; h0 < kSlab; h0 += slab_h) {
-      const int i0 = slab * kSlab + h0;
-      if (i0 >= md.rows) break;
-      // O tile: tile[il][r] = X_T[r][i0 + il]
-      const __nv_bfloat16* X = reinterpret_cast<const __nv_bfloat16*>(md.final_in_x1 ? md.X1 : md.X0);
-      for (int t = threadIdx.x; t < k * parts; t += blockDim.x) {
-        const int r = t / parts, part = (t % parts) * 8;
-        const uint4 in = *reinterpret_cast<const uint4*>(X + (int64_t)r * md.q_pad + i0 + part);
-        const __nv_bfloat16* h = reinterpret_cast<const __nv_bfloat16*>(&in);
-#pragma unroll
-        for (int e = 0; e < 8; ++e) tile[(part + e) * ldt + r] = h[e];
-      }
-      __syncthreads();
-      const float sc = (lr_dev ? __ldg(lr_dev) : lr) * md.update_scale;
-      const int n = (int)md.cols;
-      for (int il = wid; il < slab_h; il += 8) {
-        const int64_t i = (int64_t)i0 + il;
-        if (i >= md.rows) break;
-        const __nv_bfloat16* trow = tile + il * ldt;
-        float* wrow = md.W + i * md.ld;
-        float* orow = md.O_out ? md.O_out + i * k : nullptr;
-        if (md.vec4) {
-          float4* w4 = reinterpret_cast<float4*>(wrow);
-          const int n4 = n >> 2;
-          for (int j0 = lane; j0 < n4; j0 += 32 * kScU) {
-            float4 w[kScU];
-            uint32_t bits[kScU];
-#pragma unroll
-            for (int u = 0; u < kScU; ++u) {
-              const int j = j0 + 32 * u, c = 4 * j;
-              bits[u] = j < n4 ? (mask[c >> 5] >> (c & 31)) & 0xFu : 0u;
-              if (kScAll ? j < n4 : bits[u] != 0) w[u] = w4[j];
-            }
-#pragma unroll
-            for (int u = 0; u < kScU; ++u) {
-              if (!bits[u]) continue;
-              const int j = j0 + 32 * u, c = 4 * j;
-              int rk = col_rank(mask, rank, c);
-              float e[4] = {w[u].x, w[u].y, w[u].z, w[u].w};
-#pragma unroll
-              for (int q = 0; q < 4; ++q) {
-                if (bits[u] & (1u << q)) {
-                  const float o = __bfloat162float(trow[rk]);
-                  e[q] -= sc * o;
-                  if (orow) orow[rk] = o;
-                  ++rk;
-                }
-              }
-              w4[j] = make_float4(e[0], e[1], e[2], e[3]);
-            }
-          }
-          for (int c = 4 * n4 + lane; c < n; c += 32) {
-            if (!((mask[c >> 5] >> (c & 31)) & 1u)) continue;
-            const int rk = col_rank(mask, rank, c);
-            const float o = __bfloat162float(trow[rk]);
-            wrow[c] -= sc * o;
-            if (orow) orow[rk] = o;
-          }
-        } else {
-          for (int c = lane; c < n; c += 32) {
-            if (!((mask[c >> 5] >> (c & 31)) & 1u)) continue;
-            const int rk = col_rank(mask, rank, c);
-            const float o = __bfloat162float(trow[rk]);
-            wrow[c] -= sc * o;
-            if (orow) orow[rk] = o;
-          }
-        }
-      }
-      __syncthreads();
-    }  // h0
-  }
-}
-
 // smem: column bitmask + popcount prefix (mask_words each) + the [kSlab][ldt >= k + 8] bf16 tile
 size_t cols_t_smem_bytes(int k, int mask_words) { return 8 * (size_t)mask_words + (size_t)kSlab * (k + 8) * 2; }
 static int mask_words_for(int64_t max_n) { return (int)((((max_n + 31) / 32) + 3) / 4 * 4); }
@@ -454,8 +354,6 @@ __global__ void __launch_bounds__(256, 4) k_scatter_cols_idx(const MatDesc* __re
 void launch_fast_paths_attrs() {
   const int mx = (int)cols_t_smem_bytes(kMaxColK, kMaskWords);
   cudaFuncSetAttribute(k_gather_cols_t, cudaFuncAttributeMaxDynamicSharedMemorySize, mx);
-  cudaFuncSetAttribute(k_scatter_cols_t<8, true>, cudaFuncAttributeMaxDynamicSharedMemorySize, mx);
-  cudaFuncSetAttribute(k_scatter_cols_t<8, false>, cudaFuncAttributeMaxDynamicSharedMemorySize, mx);
   cudaFuncSetAttribute(k_scatter_cols_idx<8>, cudaFuncAttributeMaxDynamicSharedMemorySize,
                        4 * kMaxColKScatter + 8 * (kMaxColKScatter + 8) * 2);
 }
@@ -463,9 +361,8 @@ void launch_fast_paths_attrs() {
 // Column-mode K7 by index walk: per W row, lane l updates the selected columns sel[l],
 // sel[l + 32], ... (ascending, so a warp's 32 accesses span a short stretch of the row)
 // with U independent loads in flight.  Same units (32-row slabs), same staged O tile and the
-// same arithmetic (w -= sc * o) as k_scatter_cols_t, but O(k) instead of O(n) work per row
-// and no mask / rank logic: at alpha = 0.25 a quarter of the instructions, at 1/16 a
-// sixteenth.  DRAM traffic is unchanged (the touched sectors are the same).
+// arithmetic w -= sc * o; O(k) work per row (a whole-row streaming variant with a column
+// bitmask, O(n) per row, measured slower and was removed: DESIGN.md §6).
 template <int U>
 __global__ void __launch_bounds__(256, 4) k_scatter_cols_idx(const MatDesc* __restrict__ mats,
                                                              const int32_t* __restrict__ list_mats,
@@ -555,24 +452,10 @@ void launch_gather_cols_t(int blocks, int max_k, int64_t max_n, cudaStream_t s, 
 void launch_scatter_cols_t(int blocks, int max_k, int64_t max_n, cudaStream_t s, const MatDesc* mats,
                            const int32_t* lm, const int32_t* lp, int nl, int units, const int32_t* bad, float lr,
                            const float* lr_dev) {
-  if (!getenv("DION2_SCATTER_MASK")) {
-    const int slab_h = max_k <= 512 ? 32 : (max_k <= 1024 ? 16 : 8);
-    const size_t smem = 4 * (size_t)((max_k + 3) & ~3) + (size_t)slab_h * (max_k + 8) * 2;
-    k_scatter_cols_idx<8><<<blocks, 256, smem, s>>>(mats, lm, lp, nl, units, bad, lr, lr_dev, max_k, slab_h);
-    return;
-  }
-  const int mw = mask_words_for(max_n);
-  // 8 whole-row float4 loads in flight per lane (measured on the 1B set's 24 up-projections:
-  // 4 selected-only loads 0.669 ms, 8 unconditional 0.613 ms, 16 0.731 ms)
   const int slab_h = max_k <= 512 ? 32 : (max_k <= 1024 ? 16 : 8);
-  const size_t smem = 8 * (size_t)mw + (size_t)slab_h * (max_k + 8) * 2;
-  // whole-row loads pay off while a 16-B chunk of a row almost always holds a selected column
-  // (alpha = 0.25: 68% of chunks, 90% of sectors); below ~1/8 density (configs[4]'s
-  // alpha = 0.0625: 23% of chunks) only the chunks holding a selected column are loaded
-  if ((int64_t)max_k * 8 >= max_n)
-    k_scatter_cols_t<8, true><<<blocks, 256, smem, s>>>(mats, lm, lp, nl, units, bad, lr, lr_dev, mw, slab_h);
-  else
-    k_scatter_cols_t<8, false><<<blocks, 256, smem, s>>>(mats, lm, lp, nl, units, bad, lr, lr_dev, mw, slab_h);
+  const size_t smem = 4 * (size_t)((max_k + 3) & ~3) + (size_t)slab_h * (max_k + 8) * 2;
+  (void)max_n;
+  k_scatter_cols_idx<8><<<blocks, 256, smem, s>>>(mats, lm, lp, nl, units, bad, lr, lr_dev, max_k, slab_h);
 }
 
 }  // namespace dion2

@@ -38,14 +38,6 @@ __global__ void k_topk_select(const MatDesc* __restrict__ mats, const int32_t* _
                               int32_t* __restrict__ bad, int32_t* __restrict__ status,
                               int random_sel, uint64_t seed, uint64_t step);
 
-// ---------------- fused K1 + K2 + K3 of rows-mode matrices (k_pre_fused.cu)
-// tasks: int4 {type (0 K1 rows, 1 select, 2 gather X rows), matrix, u0, u1} in ticket order;
-// ctr: [1 + 2 n] zeroed before the launch (ticket, k1_done[n], sel_ready[n])
-void launch_pre_fused_rows(bool hint, int blocks, size_t smem, cudaStream_t s, const MatDesc* mats,
-                           const int4* tasks, int n_tasks, int32_t* ctr, const int32_t* k1_need, int n_mats,
-                           int32_t* bad, int32_t* status, float mu, int random_sel, uint64_t seed, uint64_t step);
-int pre_fused_blocks_per_sm(bool hint, size_t smem);
-constexpr int kFuseMaxD = 8192;  // largest selection length the fused kernel's select takes (32 KB keys)
 
 // ---------------- K3 gather + decay + sum of squares, norm finalize; K7 scatter (k_gather_scatter.cu)
 constexpr int kTileA = 32;   // S rows per gather/scatter tile
@@ -163,30 +155,6 @@ void launch_ns_tc(int bn, int grid, cudaStream_t s, const NsTcParams& P);
 void ns_pair_set_attrs();
 void launch_ns_pair(int grid, cudaStream_t s, const NsTcParams& P);
 void launch_splitk_reduce(cudaStream_t s, const NsParams& p);  // after a split-K pair launch
-// Gram-space chain (k_ns_chain_pair.cu, reading R23): one CTA pair runs every p x p product
-// of one matrix in sequence (ops), on the five fp16/bf16 p x p buffers of its shape group.
-constexpr int kChainBufs = 5;  // 0 A, 1 C, 2 Q0, 3 Q1, 4 B
-constexpr int kMaxChainOps = 64;
-struct ChainOp {
-  int8_t a, b, out, cin;  // buffer indices; cin < 0: none
-  int8_t out_f16;
-  int8_t dep;             // op (same matrix) whose completion gates this op's loads; < 0: none
-  int8_t cin_dep;         // op whose completion gates the epilogue's cin reads; < 0: none
-  int8_t pad;
-  float cacc, cC, diag;   // out = cacc * a.b^T + cC * cin + diag * I
-};
-struct NsChainParams {
-  CUtensorMap ld[kMaxGroups][kChainBufs];  // operand loads: box {64, 128, 1}, SWIZZLE_128B
-  CUtensorMap st[kMaxGroups][kChainBufs];  // output stores: box {32, 32, 1}, SWIZZLE_64B
-  const void* buf[kMaxGroups][kChainBufs]; // [count][p_pad][p_pad] 2-byte elements
-  long long mstride[kMaxGroups];
-  int p_pad[kMaxGroups];
-  int ngroups, nops, n_entries;
-  const int32_t* entries;                  // [n_entries] (group << 24) | z, largest p first
-  ChainOp ops[kMaxChainOps];
-};
-void ns_chain_set_attrs();
-void launch_ns_chain(int grid, cudaStream_t s, const NsChainParams& P);
 
 template <int BN>
 constexpr int ns_tc_stages() { return BN == 256 ? 4 : 6; }

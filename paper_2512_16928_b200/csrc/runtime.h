@@ -15,11 +15,11 @@
 namespace dion2rt {
 using namespace dion2;
 
-constexpr int kNumPhases = 16;
+constexpr int kNumPhases = 15;
 extern const char* kPhaseNames[kNumPhases];
 enum Phase {
   PH_K1 = 0, PH_SELECT, PH_GATHER, PH_NORM, PH_GRAM, PH_POLY, PH_APPLY, PH_SCATTER, PH_FULLDECAY,
-  PH_GATHER_ROWS, PH_GATHER_COLS, PH_SCATTER_ROWS, PH_SCATTER_COLS, PH_NSMUL, PH_K1_MT, PH_PRE_FUSED
+  PH_GATHER_ROWS, PH_GATHER_COLS, PH_SCATTER_ROWS, PH_SCATTER_COLS, PH_NSMUL, PH_K1_MT
 };
 
 extern std::mutex g_mu;
@@ -68,10 +68,9 @@ struct Group {
 struct Launch {
   int phase;
   int bn;
-  int kind;  // 0 = tc BN128, 1 = tc BN256, 2 = simt, 3 = 2-SM pair, 4 = Gram-space chain
+  int kind;  // 0 = tc BN128, 1 = tc BN256, 2 = simt, 3 = 2-SM pair
   NsTcParams tc;
   int simt_group;
-  std::shared_ptr<NsChainParams> chain;  // kind 4
 };
 
 struct Plan {
@@ -82,7 +81,6 @@ struct Plan {
   std::vector<Group> groups;
   size_t off_status, off_bad, off_desc, off_rowmats, off_rowprefix, off_colmats, off_colprefix, off_gprefix,
       off_nsscale, off_ns_begin, off_ns_end, total;
-  size_t off_chain_entries = 0;  // Gram-space chain entry table (in the uploaded table region)
   size_t off_cf_mats = 0, off_cf_prefix = 0;  // cols-mode matrices whose scores k_col_scores_finalize sums
   int cf_n = 0;
   int64_t cf_total = 0;
@@ -102,16 +100,9 @@ struct Plan {
   int n_mt_mats = 0;
   int64_t total_mt_tiles = 0;
   int64_t fl_maxn = 0;
-  // fused pre-stage (k_pre_fused.cu: K1 + K2 + K3 of the rows-mode matrices in one launch);
-  // only plans whose caller runs stage_k1_select and stage_gather back to back enable it
-  bool allow_fuse = false;
   // split-K of the long-K gram launches when their tiles cannot fill the GPU (bf16 pair path)
   int gram_splitk = 1;
   size_t off_splitk = 0;
-  int fuse_tasks = 0, fuse_rest_n = 0, fuse_max_d = 0;
-  size_t fuse_off_need = 0, fuse_off_ctr = 0, fuse_off_rest = 0;
-  std::vector<uint8_t> fuse_host;  // device image: int4 tasks, int32 k1_need[n], ctr[1 + 2n], rest[n]
-  void* dfuse = nullptr;
   std::vector<uint8_t> host_tables;  // [off_desc, off_ns_begin) image (descriptors + aux)
   std::vector<Launch> ns_launches;
   void* ws = nullptr;

@@ -8,9 +8,7 @@
 // prefix sums in index order.  Integer-only after the scores exist: bit-exact and
 // deterministic for any block size (a multiple of 32, at most 1024).
 //
-// Used by k_topk_select (one CTA per matrix) and by the fused pre-stage kernel
-// (k_pre_fused.cu), where the scores were written by other CTAs of the same launch:
-// they are read with ld.global.cg (L2), never through L1.
+// Used by k_topk_select (one CTA per matrix); scores are read with ld.global.cg (L2).
 #pragma once
 #include "common.cuh"
 

@@ -1,7 +1,7 @@
 """A few small Dion2 steps exercising every kernel family (row / transposed-M / generic
-paths, split-K gram, both NS forms, column scatter by index walk, random selection, the
-opt-in fused pre-stage); with DION2_DEBUG_SYNC=1 every launch is synchronised and checked.
-(compute-sanitizer is not available on the GPU pool.)
+paths, split-K gram, both NS forms, column scatter by index walk, random selection); with
+DION2_DEBUG_SYNC=1 every launch is synchronised and checked.  Under compute-sanitizer:
+    compute-sanitizer --tool memcheck python scripts/sanitize_step.py
 
     DION2_DEBUG_SYNC=1 python scripts/sanitize_step.py
 """
@@ -27,10 +27,4 @@ for form in ("auto", "direct"):
             opt.step(Ws, Ms, Gs)
         torch.cuda.synchronize()
         assert opt.status() == (0, -1), opt.status()
-os.environ["DION2_PRE_FUSE"] = "1"
-Ws = [torch.from_numpy(gen_w0(m, n, 2, i)).cuda() for i, (m, n) in enumerate(shapes)]
-Ms = [torch.zeros_like(w) for w in Ws]
-opt = Dion2(alpha=0.25)
-opt.step(Ws, Ms, [torch.from_numpy(gen_grad(m, n, 2, i)).cuda() for i, (m, n) in enumerate(shapes)])
-torch.cuda.synchronize()
 print("sanitize_step ok")

@@ -27,24 +27,24 @@ def test_1b_set_shape_census():
 @pytest.mark.parametrize("alpha,tflop", [(1.0, 61.85), (0.5, 13.92), (0.25, 3.29), (0.125, 0.80)])
 def test_direct_ns_flops_match_survey_table(alpha, tflop):
     """SURVEY 8(d) cfg 2: NS FLOP 61.85 / 13.92 / 3.29 / 0.80 TFLOP for alpha 1 / 0.5 / 0.25 / 0.125."""
-    f, _ = bench.work_model(layer_set_1b(24), alpha, ns_form="direct", fused=False)
+    f, _ = bench.work_model(layer_set_1b(24), alpha, ns_form="direct")
     assert abs(sum(f.values()) / 1e12 - tflop) < 0.01
 
 
 def test_gram_form_flops_closed_form():
     """Gram space at alpha = 0.25: every matrix has p = 512 and q = 2048 or 8192 (q >= 2p)."""
-    f, _ = bench.work_model(layer_set_1b(24), 0.25, ns_form="auto", fused=False)
+    f, _ = bench.work_model(layer_set_1b(24), 0.25, ns_form="auto")
     p, T = 512, 5
     want = sum(4 * p * p * q + (4 * T - 3) * 2 * p ** 3 for q in [2048] * 96 + [8192] * 48)
     assert abs(sum(f.values()) - want) < 1e3
     assert abs(sum(f.values()) / 1e12 - 1.28) < 0.005  # DESIGN 6: 1.28 TFLOP in Gram form (2.6x fewer)
     # alpha = 1: the square matrices have q = p (direct form), the 2048 x 8192 ones q = 4p (Gram)
     sq = [(2048, 2048)] * 96
-    f1, _ = bench.work_model(sq, 1.0, ns_form="auto", fused=False)
-    fd, _ = bench.work_model(sq, 1.0, ns_form="direct", fused=False)
+    f1, _ = bench.work_model(sq, 1.0, ns_form="auto")
+    fd, _ = bench.work_model(sq, 1.0, ns_form="direct")
     assert sum(f1.values()) == sum(fd.values())
     rect = [(8192, 2048), (2048, 8192)]
-    fa, _ = bench.work_model(rect, 1.0, ns_form="auto", fused=False)
+    fa, _ = bench.work_model(rect, 1.0, ns_form="auto")
     assert sum(fa.values()) == 2 * (4 * 2048 ** 2 * 8192 + 17 * 2 * 2048 ** 3)
 
 
@@ -53,7 +53,7 @@ def test_hbm_bytes_match_survey_table(alpha, gb):
     """SURVEY 8(d) cfg 2 algorithmic HBM bytes 33.8 / 24.2 / 19.3 / 16.9 GB: (12 + 16 alpha) B per
     parameter with fp32 G, plus the bf16 workspace traffic of X and O (4 B per selected
     element) that the per-phase accounting also charges."""
-    _, b = bench.work_model(layer_set_1b(24), alpha, fused=False)
+    _, b = bench.work_model(layer_set_1b(24), alpha)
     n = 1_207_959_552
     k1 = b["momentum_score"] + b["momentum_score_mt"]
     assert abs(k1 - 12 * n) / (12 * n) < 1e-3                     # + 4 d per matrix of scores
@@ -62,22 +62,13 @@ def test_hbm_bytes_match_survey_table(alpha, gb):
     assert abs((k1 + sel - 4 * alpha * n) / 1e9 - gb) < 0.1
 
 
-def test_fused_accounting_moves_bytes_not_adds():
-    """The opt-in fused pre-stage reports K1 + gather bytes of its matrices under one phase."""
-    s = layer_set_1b(24)
-    _, a = bench.work_model(s, 0.25, fused=False)
-    _, b = bench.work_model(s, 0.25, fused=True)
-    assert abs(sum(a.values()) - sum(b.values())) < 1.0
-    assert b["pre_fused"] > 0 and b["momentum_score"] < a["momentum_score"]
-
-
 def test_stress_config_shapes():
     """configs[4]: 4096 x 32768 (rows mode, k = 256) and 28672 x 8192 (cols mode, k = 512) at
     alpha = 1/16; 43.1 and 151.7 GFLOP of NS (direct count)."""
     shapes = bench.model_shapes("stress")
     assert shapes == [(4096, 32768), (28672, 8192)]
-    f0, _ = bench.work_model(shapes[:1], 0.0625, ns_form="direct", fused=False)
-    f1, _ = bench.work_model(shapes[1:], 0.0625, ns_form="direct", fused=False)
+    f0, _ = bench.work_model(shapes[:1], 0.0625, ns_form="direct")
+    f1, _ = bench.work_model(shapes[1:], 0.0625, ns_form="direct")
     assert abs(sum(f0.values()) / 1e9 - 43.1) < 0.1 and abs(sum(f1.values()) / 1e9 - 151.7) < 0.1
 
 

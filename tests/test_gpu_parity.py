@@ -75,24 +75,9 @@ def test_gram_form_is_tighter_on_wide_x():
     _assert(res, 1e-2)
 
 
-@pytest.mark.parametrize("form,chain", [("direct", "0"), ("gram", "0"), ("gram", "1")])
-def test_both_ns_forms_on_the_1b_layer(form, chain, monkeypatch):
-    monkeypatch.setenv("DION2_NS_CHAIN", chain)
+@pytest.mark.parametrize("form", ["direct", "gram"])
+def test_both_ns_forms_on_the_1b_layer(form):
     _assert(run_parity(layer_set_1b(layers=1), 0.25, "auto", "bf16", steps=1, ns_form=form), BF16_TOL)
-
-
-@pytest.mark.parametrize("coeffs", [
-    None,
-    [(3.4445, -4.7750, 2.0315)],
-    [(3.4445, -4.7750, 2.0315)] * 2,
-    [(1.5, -0.5, 0.0)] * 3,
-])
-def test_gram_chain_kernel(coeffs, monkeypatch):
-    """The persistent chain launch (k_ns_chain_pair.cu): five shape groups (two chain launches,
-    p_pad 256 / 512 / 768, several matrices per pair), every schedule length."""
-    monkeypatch.setenv("DION2_NS_CHAIN", "1")
-    shapes = [(256, 1024), (1024, 256), (600, 2400), (1024, 4096), (2048, 5120), (130, 1030), (300, 1200)] * 2
-    _assert(run_parity(shapes, 0.3, "auto", "bf16", steps=2, ns_form="gram", ns_coeffs=coeffs), BF16_TOL)
 
 
 @pytest.mark.parametrize("coeffs", [
@@ -164,29 +149,6 @@ def test_random_selection(precision, tol):
     """Random rule: GPU Philox keys must select exactly the oracle's subset."""
     _assert(run_parity([(256, 128), (300, 520), (1024, 2048)], 0.25, "auto", precision, steps=4,
                        select="random", sel_seed=1234), tol)
-
-
-@pytest.mark.parametrize("chunks", ["2", "3"])
-def test_chunked_pipeline(chunks, monkeypatch):
-    """The two-stream chunked pipeline (NS of chunk c overlapping the streaming passes of
-    its neighbours) computes the same step; random keys use the global matrix id."""
-    monkeypatch.setenv("DION2_CHUNKS", chunks)
-    shapes = [(256, 512), (512, 256), (384, 640), (1024, 512), (256, 256), (640, 384), (512, 1024)]
-    _assert(run_parity(shapes, 0.25, "auto", "bf16", steps=3), BF16_TOL)
-    _assert(run_parity(shapes, 0.25, "auto", "bf16", steps=2, select="random", sel_seed=5), BF16_TOL)
-
-
-def test_chunked_nonfinite_reports_global_index(monkeypatch):
-    monkeypatch.setenv("DION2_CHUNKS", "3")
-    Ws = [torch.from_numpy(gen_w0(64, 128, 0, i)).cuda() for i in range(6)]
-    W0 = [w.clone() for w in Ws]
-    Ms = [torch.zeros_like(w) for w in Ws]
-    Gs = [torch.from_numpy(gen_grad(64, 128, 0, i)).cuda() for i in range(6)]
-    Gs[4][1, 2] = float("inf")
-    opt = Dion2(alpha=0.25)
-    opt.step(Ws, Ms, Gs)
-    assert opt.status() == (7, 4)
-    assert torch.equal(Ws[4], W0[4]) and not torch.equal(Ws[5], W0[5])
 
 
 @pytest.mark.parametrize("mt", [False, True])
@@ -431,16 +393,12 @@ def test_step_host_pipelined_upload(graph):
         assert (a - b).abs().max() <= 1e-6 * a.abs().max()
 
 
-@pytest.mark.parametrize("chunks", [None, "3"])
-def test_lr_device_flag_through_the_c_abi(chunks, monkeypatch):
+def test_lr_device_flag_through_the_c_abi():
     """DION2_FLAG_LR_DEVICE: eta comes from the fp32 word at byte 8 of the 4096-aligned workspace
     base (cfg.lr, deliberately different, is ignored by the kernels); bitwise equal to a step with
-    cfg.lr = that eta.  Rows and column (index-walk) scatters; the chunked pipeline
-    copies the word to every chunk."""
+    cfg.lr = that eta.  Rows and column (index-walk) scatters."""
     import ctypes
     from paper_2512_16928_b200 import dion2 as D
-    if chunks:
-        monkeypatch.setenv("DION2_CHUNKS", chunks)
     shapes = [(512, 1024), (2048, 512), (300, 520), (1000, 200)]
     def run(lr_device):
         Ws = [torch.from_numpy(gen_w0(m, n, 12, i)).cuda() for i, (m, n) in enumerate(shapes)]
@@ -514,9 +472,7 @@ def test_bf16_gradient_input():
     assert np.linalg.norm(dgpu - dref) / np.linalg.norm(dref) <= BF16_TOL
 
 
-@pytest.mark.parametrize("fuse", ["0", "1"])
-def test_phase_timing_and_launch_count(fuse, monkeypatch):
-    monkeypatch.setenv("DION2_PRE_FUSE", fuse)
+def test_phase_timing_and_launch_count():
     Ws = [torch.from_numpy(gen_w0(256, 512)).cuda()]
     Ms = [torch.zeros_like(Ws[0])]
     set_phase_timing(True)
@@ -525,48 +481,7 @@ def test_phase_timing_and_launch_count(fuse, monkeypatch):
         times = get_phase_times()
     finally:
         set_phase_timing(False)
-    pre = ("momentum_score", "select", "gather_rows") if fuse == "0" else ("pre_fused",)
+    pre = ("momentum_score", "select", "gather_rows")
     assert last_launch_count() >= 5 + len(pre)
     for ph in pre + ("ns_gram", "ns_poly", "ns_apply", "scatter_rows"):
         assert times[ph][1] >= 1 and times[ph][0] > 0
-    if fuse == "1":
-        assert times["momentum_score"][1] == 0 and times["gather_rows"][1] == 0
-
-
-def _run_steps(shapes, steps, seed, **kw):
-    Ws = [torch.from_numpy(gen_w0(m, n, seed, i)).cuda() for i, (m, n) in enumerate(shapes)]
-    Ms = [torch.zeros_like(w) for w in Ws]
-    sels = [torch.empty(max(1, int(0.25 * (m if m <= n else n) + 0.5)), dtype=torch.int32, device="cuda")
-            for (m, n) in shapes]
-    opt = Dion2(alpha=0.25, **kw)
-    for t in range(steps):
-        Gs = [torch.from_numpy(gen_grad(m, n, seed, i, t, row_scaled=True)).cuda() for i, (m, n) in enumerate(shapes)]
-        opt.step(Ws, Ms, Gs, sel_out=sels)
-    torch.cuda.synchronize()
-    return [w.clone() for w in Ws] + [mm.clone() for mm in Ms] + [s.clone() for s in sels]
-
-
-@pytest.mark.parametrize("lag_mb", ["0", "1", "96", "100000"])
-def test_pre_fused_equals_separate_launches(lag_mb, monkeypatch):
-    """The fused K1 + K2 + K3 launch (k_pre_fused.cu) against the separate kernels: the l1
-    scores are summed in another fixed order, but on row-scaled inputs (no near-ties) the
-    selected sets, hence X, its norm, the NS and every W and M word, are identical.  The
-    gather lag spans 'gathers queued right behind the select' (0: CTAs wait on the select)
-    to 'all gathers after all K1 work'.  Mixed rows / transposed-M column / generic matrices,
-    ragged rows and an unaligned ld-free shape."""
-    shapes = [(2048, 2048), (512, 2048), (2048, 512), (300, 520), (7, 33), (1024, 4096), (256, 256), (130, 1030)]
-    monkeypatch.setenv("DION2_PRE_FUSE", "0")
-    ref = _run_steps(shapes, 3, 11)
-    monkeypatch.setenv("DION2_PRE_FUSE", "1")
-    monkeypatch.setenv("DION2_FUSE_LAG_MB", lag_mb)
-    got = _run_steps(shapes, 3, 11)
-    for i, (a, b) in enumerate(zip(ref, got)):
-        assert torch.equal(a, b), i
-
-
-def test_pre_fused_random_selection_and_bf16_grad(monkeypatch):
-    monkeypatch.setenv("DION2_PRE_FUSE", "1")
-    monkeypatch.setenv("DION2_FUSE_LAG_MB", "4")
-    _assert(run_parity([(1024, 2048), (512, 1536), (2048, 1024)], 0.25, "auto", "bf16", steps=3,
-                       select="random", sel_seed=77), BF16_TOL)
-    _assert(run_parity([(1024, 2048), (384, 640)], 0.25, "auto", "bf16", steps=2, grad_bf16=True), BF16_TOL)
