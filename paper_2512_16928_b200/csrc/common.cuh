@@ -38,8 +38,12 @@ struct MatDesc {
   float* col_partials;    // [rowblocks][cols]  (cols mode)
   int32_t* sel;           // [k] ascending
   float* sumsq_partials;  // [n_gather_tiles]
-  float* ns_scale;        // [2] = { s, s^2 },  s = 1 / (||X||_F + eps)
-  void* X0;               // [p_pad x q_pad] bf16 or fp32: NS input / ping
+  // [4] = { s', s'^2, xs, smax }: xs = 2^e, the power-of-two prescale K3 applies when it stores X as
+  // fp16 (written by K2 from the largest l1 score, reading R24; 1 on the fp32 path), and
+  // s' = s / xs with s = 1 / (||X||_F + eps) of the unscaled fp32 values (K3's sum of squares),
+  // so s' * X0_stored = s * X exactly (powers of two); smax = the largest score (K2)
+  float* ns_scale;
+  void* X0;               // [p_pad x q_pad] fp16 (tensor-core path) or fp32: NS input / ping
   void* X1;               // pong
   int32_t final_in_x1;    // X_T lives in X1 (T odd)
   int32_t gather_tile_base, gather_tiles_a, gather_tiles_b;
@@ -53,6 +57,7 @@ struct MatDesc {
                            // for k > kMaxColKFast); the generic K7 tiles skip matrices with spath != 0
   int64_t ldm;             // row stride of the transposed M
   int32_t rowblocks;      // ceil(rows / kColRowBlock) (cols mode partials)
+  int32_t x16;            // X is stored as fp16 with the prescale xs (tensor-core path); 0: fp32, xs = 1
 };
 
 // ----------------------------------------------------------------------------- small helpers
@@ -64,6 +69,32 @@ __device__ __forceinline__ float warp_sum(float v) {
 }
 
 __device__ __forceinline__ float bf16_to_f(__nv_bfloat16 x) { return __bfloat162float(x); }
+
+// X / O storage of the tensor-core path: fp16 (10-bit mantissa; reading R24).  K3 stores
+// X * xs (xs = 2^e, exact) so the largest entry sits near 2^15; O (|o| <= ~1.2) is unscaled.
+__device__ __forceinline__ uint2 pack4_h(float a, float b, float c, float d) {
+  __half2 lo = __floats2half2_rn(a, b), hi = __floats2half2_rn(c, d);
+  uint2 u;
+  u.x = *reinterpret_cast<uint32_t*>(&lo);
+  u.y = *reinterpret_cast<uint32_t*>(&hi);
+  return u;
+}
+// Reading R24: the power-of-two prescale of the fp16 X.  Every entry of X lies in a selected
+// row (column) of M, whose l1 norm bounds it, so max|x| <= smax and x * 2^e with
+// e = 15 - exponent(smax) stays below 2^15 (fp16 max 65504); e is clamped to [-100, 64]
+// (all-zero input: e = 0).
+__device__ __forceinline__ float x16_prescale(float smax) {
+  if (!(smax > 0.f)) return 1.f;
+  int E;
+  frexpf(smax, &E);  // smax = m 2^E, m in [0.5, 1)
+  const int e = max(-100, min(64, 15 - E));
+  return ldexpf(1.f, e);
+}
+
+__device__ __forceinline__ uint32_t pack2_h(float a, float b) {
+  __half2 v = __floats2half2_rn(a, b);
+  return *reinterpret_cast<uint32_t*>(&v);
+}
 
 __device__ __forceinline__ uint32_t smem_u32(const void* p) {
   return static_cast<uint32_t>(__cvta_generic_to_shared(p));

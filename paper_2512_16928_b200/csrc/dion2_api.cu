@@ -267,7 +267,7 @@ int build_layout(Plan& P, const dion2_matrix* mats, int n, const dion2_config* c
   for (auto& g : P.groups) g.off_gmats = take(4 * (size_t)g.count);
   P.off_cf_mats = take(4 * (size_t)n);
   P.off_cf_prefix = take(8 * (size_t)n);
-  P.off_nsscale = take(8 * (size_t)n);
+  P.off_nsscale = take(16 * (size_t)n);
   for (int i = 0; i < n; ++i) {
     MatPlan& q = P.mp[i];
     q.off_scores = take(4 * (size_t)q.d);
@@ -331,15 +331,40 @@ int build_layout(Plan& P, const dion2_matrix* mats, int n, const dion2_config* c
 }
 
 
-// Launch list of the Gram-space Newton-Schulz form (reading R23) for the groups with g.gs:
-//   gram   A   = s^2 X0 X0^T                         (bf16 in, fp16 out)
-//   t = 0 .. T-1:
-//     poly   C_t = a_t I + b_t A + c_t A A            (fp16; C_0 doubles as Q_1)
-//     mul    Q_{t+1} = C_t Q_t (t >= 1),  B = C_t A (t < T-1)
-//     mul    A   = C_t B                              (t < T-1)
-//   apply  X1  = s Q_T X0                             (bf16)
-// Every p x p product is a polynomial in A_0, hence symmetric: upper-triangle pair tiles,
-// mirrored.  Q_T is written as bf16 (the apply operand), everything else as fp16.
+// Restart segments of the Gram-space form (reading R24): consecutive iterations [t0, t1) whose
+// growth prod |a_t| stays <= kRestartGrowth share one p x p recursion; each later segment
+// restarts from its X, formed explicitly by the previous segment's apply.  The default
+// quintic (a = 3.4445) gives [0, 3) + [3, 5): Q's eigenvalues span at most a^3 / 0.68 ~ 60
+// instead of a^5 / 0.68 ~ 700.
+constexpr double kRestartGrowth = 64.0;
+std::vector<std::pair<int, int>> ns_segments(const dion2_config* c, int T) {
+  std::vector<std::pair<int, int>> v;
+  int t0 = 0;
+  double prod = 1.0;
+  for (int t = 0; t < T; ++t) {
+    const double a = std::max(1.0, std::fabs((double)c->ns_coeffs[t][0]));
+    if (t > t0 && prod * a > kRestartGrowth) {
+      v.push_back({t0, t});
+      t0 = t;
+      prod = 1.0;
+    }
+    prod *= a;
+  }
+  v.push_back({t0, T});
+  return v;
+}
+
+// Launch list of the Gram-space Newton-Schulz form (readings R23, R24) for the groups with
+// g.gs, per restart segment j (iterations t0 .. t1-1, Ts = t1 - t0) on Xin = X_{t0}:
+//   gram   A   = s_j^2 Xin Xin^T                     (s_0 = s' of the prescaled X0; s_j = 1 after)
+//   tl = 0 .. Ts-1 (t = t0 + tl):
+//     poly   C   = a_t I + b_t A + c_t A A            (C of tl = 0 doubles as Q_1)
+//     mul    Q_{tl+1} = C Q_tl (tl >= 1),  B = C A (tl < Ts-1)
+//     mul    A   = C B                                (tl < Ts-1)
+//   apply  Xout = s_j Q_Ts Xin                         (X_{t1}; the last segment's is X_T = O)
+// Xin / Xout alternate between the X0 and X1 buffers.  Every p x p product is a polynomial in
+// the segment's A, hence symmetric: upper-triangle pair tiles.  All operands and outputs are
+// fp16 with fp32 accumulation; Q_Ts is written mirrored (the 1-SM apply reads it whole).
 static int append_gram_space_launches(Plan& P, const dion2_config* c, void* ws, int pair_mode) {
   std::vector<int> gl;
   for (int gi = 0; gi < (int)P.groups.size(); ++gi)
@@ -430,30 +455,39 @@ static int append_gram_space_launches(Plan& P, const dion2_config* c, void* ws, 
   auto Qb = [&](int gi, int j) { return at(ws, (j & 1) ? P.groups[gi].off_Q0 : P.groups[gi].off_Q1); };  // Q_j, j >= 1
   int rc;
   std::vector<Entry> es;
-  // p x p products: one flat launch per op over all matrices
-  for (int gi : gl) es.push_back({gi, X0(gi), X0(gi), Ab(gi), nullptr});
-  if ((rc = emit(PH_GRAM, es, 1.f, 0.f, 0.f, 2, 0, 1))) return rc;
-  for (int t = 0; t < T; ++t) {
-    const float a = c->ns_coeffs[t][0], b = c->ns_coeffs[t][1], cc = c->ns_coeffs[t][2];
-    const int last = t == T - 1;
+  const std::vector<std::pair<int, int>> segs = ns_segments(c, T);
+  for (size_t sg = 0; sg < segs.size(); ++sg) {
+    const int t0 = segs[sg].first, Ts = segs[sg].second - t0;
+    auto Xin = [&](int gi) { return (sg & 1) ? X1(gi) : X0(gi); };
+    auto Xout = [&](int gi) { return (sg & 1) ? X0(gi) : X1(gi); };
     es.clear();
-    for (int gi : gl) es.push_back({gi, Ab(gi), Ab(gi), Cb(gi, t), Ab(gi)});
-    if ((rc = emit(PH_POLY, es, cc, b, a, 0, 1, T == 1 ? 0 : 1, T == 1))) return rc;
-    es.clear();
-    for (int gi : gl) {
-      if (t >= 1) es.push_back({gi, Cb(gi, t), Qb(gi, t), Qb(gi, t + 1), nullptr});
-      if (!last) es.push_back({gi, Cb(gi, t), Ab(gi), Bb(gi), nullptr});
-    }
-    if (!es.empty() && (rc = emit(PH_NSMUL, es, 1.f, 0.f, 0.f, 0, 1, last ? 0 : 1, last))) return rc;
-    if (!last) {
+    for (int gi : gl) es.push_back({gi, Xin(gi), Xin(gi), Ab(gi), nullptr});
+    if ((rc = emit(PH_GRAM, es, 1.f, 0.f, 0.f, sg == 0 ? 2 : 0, 1, 1))) return rc;
+    // p x p products: one flat launch per op over all matrices
+    for (int tl = 0; tl < Ts; ++tl) {
+      const int t = t0 + tl;
+      const float a = c->ns_coeffs[t][0], b = c->ns_coeffs[t][1], cc = c->ns_coeffs[t][2];
+      const bool last = tl == Ts - 1;
       es.clear();
-      for (int gi : gl) es.push_back({gi, Cb(gi, t), Bb(gi), Ab(gi), nullptr});
-      if ((rc = emit(PH_NSMUL, es, 1.f, 0.f, 0.f, 0, 1, 1))) return rc;
+      for (int gi : gl) es.push_back({gi, Ab(gi), Ab(gi), Cb(gi, tl), Ab(gi)});
+      if ((rc = emit(PH_POLY, es, cc, b, a, 0, 1, 1, Ts == 1))) return rc;
+      es.clear();
+      for (int gi : gl) {
+        if (tl >= 1) es.push_back({gi, Cb(gi, tl), Qb(gi, tl), Qb(gi, tl + 1), nullptr});
+        if (!last) es.push_back({gi, Cb(gi, tl), Ab(gi), Bb(gi), nullptr});
+      }
+      if (!es.empty() && (rc = emit(PH_NSMUL, es, 1.f, 0.f, 0.f, 0, 1, 1, last))) return rc;
+      if (!last) {
+        es.clear();
+        for (int gi : gl) es.push_back({gi, Cb(gi, tl), Bb(gi), Ab(gi), nullptr});
+        if ((rc = emit(PH_NSMUL, es, 1.f, 0.f, 0.f, 0, 1, 1))) return rc;
+      }
     }
+    es.clear();
+    for (int gi : gl) es.push_back({gi, Qb(gi, Ts), Xin(gi), Xout(gi), nullptr});
+    if ((rc = emit(PH_APPLY, es, 1.f, 0.f, 0.f, sg == 0 ? 1 : 0, 1, 1))) return rc;
   }
-  es.clear();
-  for (int gi : gl) es.push_back({gi, Qb(gi, T), X0(gi), X1(gi), nullptr});
-  return emit(PH_APPLY, es, 1.f, 0.f, 0.f, 1, 0, 0);
+  return DION2_OK;
 }
 
 // Fill host tables and NS launches for a concrete workspace.
@@ -497,11 +531,13 @@ int build_device_plan(Plan& P, const dion2_matrix* mats, const dion2_config* c, 
     d.col_partials = q.axis == DION2_AXIS_COLS ? (float*)at(ws, q.off_partials) : nullptr;
     d.sel = (int32_t*)at(ws, q.off_sel);
     d.sumsq_partials = (float*)at(ws, q.off_sumsq);
-    d.ns_scale = (float*)at(ws, P.off_nsscale) + 2 * i;
+    d.ns_scale = (float*)at(ws, P.off_nsscale) + 4 * i;
+    d.x16 = P.bf16_ns ? 1 : 0;
     const size_t xel = P.bf16_ns ? 2 : 4;
     d.X0 = at(ws, g.off_X0 + (size_t)q.zi * g.p_pad * g.q_pad * xel);
     d.X1 = at(ws, g.off_X1 + (size_t)q.zi * g.p_pad * g.q_pad * xel);
-    d.final_in_x1 = g.gs ? 1 : (P.ns_steps & 1);  // Gram-space: X_T = Q_T X_0 is written to X1
+    // X_T lands in X1 after an odd number of applies (direct: T; Gram space: one per segment)
+    d.final_in_x1 = g.gs ? (int)(ns_segments(c, P.ns_steps).size() & 1) : (P.ns_steps & 1);
     d.gather_tile_base = gt_acc;
     d.gather_tiles_a = q.ga;
     d.gather_tiles_b = q.gb;
@@ -636,7 +672,8 @@ int build_device_plan(Plan& P, const dion2_matrix* mats, const dion2_config* c, 
           NsParams& np = L.tc.p;
           np.ngroups = (int)std::min<size_t>(kMaxGroups, gl.size() - s0);
           np.ns_scale_all = scale_all;
-          // gram: A = s^2 X X^T; poly: C = a I + b A + c A A^T (consistent bf16 A);
+          np.in_f16 = np.out_f16 = P.bf16_ns ? 1 : 0;  // fp16 X / A / C (reading R24)
+          // gram: A = s^2 X X^T; poly: C = a I + b A + c A A^T (consistent 16-bit A);
           // apply: X' = s C X (the linear term a X is folded into C: no epilogue read)
           np.diag = 0.f;
           np.sym = sym ? 1 : 0;

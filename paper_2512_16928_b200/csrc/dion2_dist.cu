@@ -78,8 +78,8 @@ struct DistPlan {
   std::vector<DistMat> dm;
   int64_t total_d = 0;
   // workspace offsets
-  size_t off_status, off_bad, off_scores, off_scores_all, off_sumsq_local, off_sumsq_all, off_send, off_recv,
-      off_osend, off_orecv, off_owner, total;
+  size_t off_status, off_bad, off_scores, off_scores_all, off_sumsq_local, off_sumsq_all, off_nsscale, off_send,
+      off_recv, off_osend, off_orecv, off_owner, total;
   std::vector<int64_t> sdispl, scount;  // per owner: my send section
   int64_t R = 0;                         // bytes per rank section of my recv / osend buffers
   // device tables (plan-owned)
@@ -210,6 +210,7 @@ int resolve(DistPlan& D, const dion2_shard* sh, int n, const dion2_config* c, in
   D.off_scores_all = take(4 * (size_t)D.total_d * world);
   D.off_sumsq_local = take(4 * (size_t)n);
   D.off_sumsq_all = take(4 * (size_t)n * world);
+  D.off_nsscale = take(16 * (size_t)n);  // per matrix: word 2 = the fp16 prescale K2 writes (R24)
   for (auto& q : D.dm) {
     q.off_partials = q.axis == DION2_AXIS_COLS ? take(4 * (size_t)ceil_div(q.srows, kColRowBlock) * q.scols) : 0;
     q.off_sel = take(4 * (size_t)q.k);
@@ -309,6 +310,8 @@ int build_tables(DistPlan& D, const dion2_config* c, void* ws) {
     d.col_partials = q.axis == DION2_AXIS_COLS ? (float*)at(ws, q.off_partials) : nullptr;
     d.sel = (int32_t*)at(ws, q.off_sel);
     d.sumsq_partials = (float*)at(ws, q.off_sumsq);
+    d.ns_scale = (float*)at(ws, D.off_nsscale) + 4 * j;
+    d.x16 = 1;
     d.X0 = at(ws, D.off_send + D.sdispl[q.owner] + q.soff);
     d.X1 = at(ws, D.off_orecv + D.sdispl[q.owner] + q.soff);
     d.final_in_x1 = 1;
@@ -444,21 +447,32 @@ int build_tables(DistPlan& D, const dion2_config* c, void* ws) {
       g_ok[gi] = 1;
       for (int i : g.mats) inpl[i] = 1;
     }
-    // point the owner plan's gram (A = B = X0) and apply (B = X0, D = X_T) launches at the pieces
-    for (Launch& ln : D.owner->ns_launches) {
+    // point the owner plan's launches that read X0 (the first gram: A = B = X0; the first apply:
+    // B = X0) at the received pieces, and the last apply (D = X_T) at the outgoing pieces
+    // (the last segment's apply reads X0 after an odd number of restart segments, else X1)
+    const bool last_reads_x0 = ns_segments(c, c->ns_steps).size() & 1;
+    for (int li = 0; li < (int)D.owner->ns_launches.size(); ++li) {
+      Launch& ln = D.owner->ns_launches[li];
       if (ln.phase != PH_GRAM && ln.phase != PH_APPLY) continue;
       for (int j = 0; j < ln.tc.p.ngroups; ++j) {
         NsGroup& G = ln.tc.p.g[j];
         for (size_t gi = 0; gi < D.owner->groups.size(); ++gi) {
           if (!g_ok[gi]) continue;
-          const void* x0 = at(at(ws, D.off_owner), D.owner->groups[gi].off_X0);
-          const bool hit = ln.phase == PH_GRAM ? G.a == x0 : G.b == x0;
-          if (!hit) continue;
-          const DistMat& q0 = D.dm[D.owned[D.owner->groups[gi].mats[0]]];
+          const Group& og = D.owner->groups[gi];
+          const void* x0 = at(at(ws, D.off_owner), og.off_X0);
+          const void* x1 = at(at(ws, D.off_owner), og.off_X1);
+          // this entry belongs to group gi iff it reads or writes one of gi's X buffers
+          const bool mine = ln.phase == PH_GRAM ? (G.a == x0 || G.a == x1) : (G.b == x0 || G.b == x1);
+          if (!mine) continue;
+          const bool load = ln.phase == PH_GRAM ? G.a == x0 : G.b == x0;
+          const bool store = ln.phase == PH_APPLY && G.b == (last_reads_x0 ? x0 : x1);
+          if (!load && !store) continue;
+          const DistMat& q0 = D.dm[D.owned[og.mats[0]]];
           G.pieces_qo = q0.qo;
           G.pieces_P = P;
           G.pieces_map = (int)(gi * 3 * P);
-          G.pieces_store = ln.phase == PH_APPLY;
+          G.pieces_load = load ? 1 : 0;
+          G.pieces_store = store ? 1 : 0;
           for (int k = 0; k < 3 * P; ++k) ln.tc.mapP[j][k] = hmaps[gi * 3 * P + k];
         }
       }
@@ -647,7 +661,7 @@ void phase_owner_ns(DistPlan& D, void* ws, const dion2_config* c, Launcher& L, c
   L.begin(PH_NORM);
   // all owned matrices in place: one block per matrix computes the norm scale only
   launch_assemble(s, om, (int)D.owned.size(), D.all_inplace_in ? 1 : D.max_p_pad, D.ptab, (const uint8_t*)at(ws, D.off_recv),
-                  (const float*)at(ws, D.off_sumsq_all), D.n, c->ns_eps);
+                  (const float*)at(ws, D.off_sumsq_all), (const float*)at(ws, D.off_nsscale), D.n, c->ns_eps);
   L.end();
   run_ns(P, c, L, s, false);
   if (!D.all_inplace) {
@@ -822,7 +836,8 @@ struct DpPlan {
   Plan P;
   int world = 1;
   size_t off_buf = 0, off_gather = 0, total = 0;
-  int64_t buf_floats = 0;
+  int64_t buf_floats = 0;   // selected rows of every matrix, then the 2 n tail floats (k_dp_tail)
+  int64_t data_floats = 0;
   int total_rows = 0;
   void* dtab = nullptr;  // [n] int32 row prefix, then [n] int64 buffer offsets
   size_t t_prefix = 0, t_off = 0;
@@ -843,6 +858,8 @@ int dp_layout(DpPlan& D, const dion2_matrix* mats, int n, const dion2_config* c,
     D.buf_floats += (int64_t)q.sr * q.sc;
     D.total_rows += q.mt ? q.sc : q.sr;  // pack units: rows of S, or rows of S^T (transposed M)
   }
+  D.data_floats = D.buf_floats;
+  D.buf_floats += 2 * (int64_t)n;
   D.off_buf = align_up(D.P.total, 4096);
   D.off_gather = align_up(D.off_buf + 4 * (size_t)D.buf_floats, 4096);
   D.total = D.off_gather + 4 * (size_t)D.buf_floats * world + 4096;
@@ -926,11 +943,19 @@ int dp_phase1(DpPlan& D, const dion2_matrix* mats, const dion2_config* c, void* 
   if ((rc = reset_status(status, s))) return rc;
   stage_k1_select(D.P, c, ws, status, L, s, true);
   dp_pack(D, ws, false, 1.f, s, L);
+  L.begin(PH_SELECT);
+  launch_dp_tail(s, (const MatDesc*)tab(D.P, D.P.off_desc), D.P.n, (float*)at(ws, D.off_buf) + D.data_floats,
+                 (int32_t*)at(ws, D.P.off_bad), status, false);
+  L.end();
   return DION2_OK;
 }
 
 void dp_phase2(DpPlan& D, const dion2_matrix* mats, const dion2_config* c, void* ws, cudaStream_t s, Launcher& L) {
-  dp_pack(D, ws, true, 1.f / (float)D.world, s, L);  // M[K] <- mean over replicas
+  L.begin(PH_SELECT);  // global non-finite flags and the common fp16 prescale
+  launch_dp_tail(s, (const MatDesc*)tab(D.P, D.P.off_desc), D.P.n, (float*)at(ws, D.off_buf) + D.data_floats,
+                 (int32_t*)at(ws, D.P.off_bad), (int32_t*)at(ws, D.P.off_status), true);
+  L.end();
+  dp_pack(D, ws, true, 1.f / (float)D.world, s, L);  // M[K] <- mean over replicas (skips bad matrices)
   stage_gather(D.P, c, ws, L, s, true);
   run_ns(D.P, c, L, s, true);
   stage_post(D.P, mats, c, ws, L, s, true);

@@ -53,25 +53,28 @@ __global__ void k_piece_sumsq(const MatDesc* __restrict__ mats, int n_mats, floa
 
 // Owner side.  For owned matrix jj (global index gj): X0[i][r*qo + c] = piece_r[i][c]
 // for i < k, c < qo; zeros elsewhere in [p_pad x q_pad].  One block per (row i, matrix).
+// xs_all: the rank's [n_total][4] NS scale words; word 2 of matrix g is its fp16 prescale (K2 ran
+// on every rank with the same combined scores, so it is the prescale of every piece)
 __global__ void k_assemble_pieces(const MatDesc* __restrict__ omats, PieceTable T, const uint8_t* __restrict__ recv,
-                                  const float* __restrict__ sumsq_all, int n_total, float eps) {
+                                  const float* __restrict__ sumsq_all, const float* __restrict__ xs_all, int n_total,
+                                  float eps) {
   const int jj = blockIdx.y;
   const MatDesc& md = omats[jj];
   const int i = blockIdx.x;
   if (i >= md.p_pad) return;
   const int qo = md.q / T.world;
-  __nv_bfloat16* xrow = reinterpret_cast<__nv_bfloat16*>(md.X0) + (int64_t)i * md.q_pad;
+  __half* xrow = reinterpret_cast<__half*>(md.X0) + (int64_t)i * md.q_pad;
   if (T.inplace[jj]) {
     // the NS kernels read the pieces in place: only the norm below
   } else if (i < md.k) {
     for (int r = 0; r < T.world; ++r) {
-      const __nv_bfloat16* src = reinterpret_cast<const __nv_bfloat16*>(recv + r * T.rstride + T.roff[jj * T.world + r]) +
+      const __half* src = reinterpret_cast<const __half*>(recv + r * T.rstride + T.roff[jj * T.world + r]) +
                                  (int64_t)i * qo;
       const uint4* s16 = reinterpret_cast<const uint4*>(src);
       uint4* d16 = reinterpret_cast<uint4*>(xrow + (int64_t)r * qo);
       for (int c = threadIdx.x; c < qo / 8; c += blockDim.x) d16[c] = s16[c];
     }
-    for (int c = md.q + threadIdx.x; c < md.q_pad; c += blockDim.x) xrow[c] = __float2bfloat16_rn(0.f);
+    for (int c = md.q + threadIdx.x; c < md.q_pad; c += blockDim.x) xrow[c] = __float2half_rn(0.f);
   } else {
     uint4* d16 = reinterpret_cast<uint4*>(xrow);
     for (int c = threadIdx.x; c < md.q_pad / 8; c += blockDim.x) d16[c] = make_uint4(0, 0, 0, 0);
@@ -79,7 +82,7 @@ __global__ void k_assemble_pieces(const MatDesc* __restrict__ omats, PieceTable 
   if (i == 0 && threadIdx.x == 0) {
     float s = 0.f;
     for (int r = 0; r < T.world; ++r) s += sumsq_all[(int64_t)r * n_total + T.gidx[jj]];
-    const float inv = 1.0f / (sqrtf(s) + eps);
+    const float inv = 1.0f / (sqrtf(s) + eps) / xs_all[4 * (int64_t)T.gidx[jj] + 2];  // reading R24
     md.ns_scale[0] = inv;
     md.ns_scale[1] = inv * inv;
   }
@@ -92,10 +95,10 @@ __global__ void k_disassemble_pieces(const MatDesc* __restrict__ omats, PieceTab
   const int i = blockIdx.x;
   if (i >= md.k || T.inplace[jj] == 1) return;  // in place: the apply wrote the pieces itself
   const int qo = md.q / T.world;
-  const __nv_bfloat16* xrow =
-      reinterpret_cast<const __nv_bfloat16*>(md.final_in_x1 ? md.X1 : md.X0) + (int64_t)i * md.q_pad;
+  const __half* xrow =
+      reinterpret_cast<const __half*>(md.final_in_x1 ? md.X1 : md.X0) + (int64_t)i * md.q_pad;
   for (int r = 0; r < T.world; ++r) {
-    __nv_bfloat16* dst = reinterpret_cast<__nv_bfloat16*>(send + r * T.rstride + T.roff[jj * T.world + r]) +
+    __half* dst = reinterpret_cast<__half*>(send + r * T.rstride + T.roff[jj * T.world + r]) +
                          (int64_t)i * qo;
     const uint4* s16 = reinterpret_cast<const uint4*>(xrow + (int64_t)r * qo);
     uint4* d16 = reinterpret_cast<uint4*>(dst);
@@ -116,9 +119,9 @@ void launch_piece_sumsq(cudaStream_t s, const MatDesc* mats, int n, float* out) 
   k_piece_sumsq<<<(n + 7) / 8, 256, 0, s>>>(mats, n, out);
 }
 void launch_assemble(cudaStream_t s, const MatDesc* omats, int n_owned, int max_p_pad, const PieceTable& T,
-                     const uint8_t* recv, const float* sumsq_all, int n_total, float eps) {
+                     const uint8_t* recv, const float* sumsq_all, const float* xs_all, int n_total, float eps) {
   dim3 grid(max_p_pad, n_owned);
-  k_assemble_pieces<<<grid, 256, 0, s>>>(omats, T, recv, sumsq_all, n_total, eps);
+  k_assemble_pieces<<<grid, 256, 0, s>>>(omats, T, recv, sumsq_all, xs_all, n_total, eps);
 }
 void launch_disassemble(cudaStream_t s, const MatDesc* omats, int n_owned, int max_k, const PieceTable& T,
                         uint8_t* send) {

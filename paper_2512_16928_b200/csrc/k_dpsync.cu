@@ -58,6 +58,34 @@ __global__ void __launch_bounds__(256) k_dp_pack(const MatDesc* __restrict__ mat
   }
 }
 
+// The all-reduced buffer ends with two floats per matrix: the replica's largest score and its
+// non-finite flag.  After the sum every replica sees the same totals, so every replica skips a
+// matrix that is non-finite on ANY replica (no NaN rows unpacked, no W / M[K] writes, status
+// reported everywhere) and takes the same fp16 prescale from the summed bound (>= the largest
+// score of every replica, hence >= any entry of the averaged rows; reading R24).
+__global__ void k_dp_tail(const MatDesc* __restrict__ mats, int n_mats, float* __restrict__ tail,
+                          int32_t* __restrict__ bad, int32_t* __restrict__ status, int combine) {
+  const int mi = blockIdx.x * blockDim.x + threadIdx.x;
+  if (mi >= n_mats) return;
+  const MatDesc& md = mats[mi];
+  if (!combine) {
+    tail[2 * mi] = bad[mi] ? 0.f : md.ns_scale[3];
+    tail[2 * mi + 1] = bad[mi] ? 1.f : 0.f;
+    return;
+  }
+  const bool any_bad = tail[2 * mi + 1] != 0.f || !(tail[2 * mi] <= 3.402823466e38f);
+  if (any_bad) {
+    bad[mi] = 1;
+    set_status_bad(status, md.mid);
+  }
+  md.ns_scale[2] = (md.x16 && !any_bad) ? x16_prescale(tail[2 * mi]) : 1.f;
+}
+
+void launch_dp_tail(cudaStream_t s, const MatDesc* mats, int n_mats, float* tail, int32_t* bad, int32_t* status,
+                    bool combine) {
+  k_dp_tail<<<(n_mats + 127) / 128, 128, 0, s>>>(mats, n_mats, tail, bad, status, combine ? 1 : 0);
+}
+
 void launch_dp_pack(bool unpack, cudaStream_t s, const MatDesc* mats, const int32_t* row_prefix, const int64_t* buf_off,
                     int n_mats, int total_rows, float* buf, float scale, const int32_t* bad) {
   const int blocks = (total_rows + 7) / 8;

@@ -16,9 +16,9 @@ namespace dion2 {
 
 template <typename XT> __device__ __forceinline__ XT to_x(float v);
 template <> __device__ __forceinline__ float to_x<float>(float v) { return v; }
-template <> __device__ __forceinline__ __nv_bfloat16 to_x<__nv_bfloat16>(float v) { return __float2bfloat16_rn(v); }
+template <> __device__ __forceinline__ __half to_x<__half>(float v) { return __float2half_rn(v); }
 __device__ __forceinline__ float from_x(float v) { return v; }
-__device__ __forceinline__ float from_x(__nv_bfloat16 v) { return __bfloat162float(v); }
+__device__ __forceinline__ float from_x(__half v) { return __half2float(v); }
 
 __device__ __forceinline__ int find_mat(const int32_t* __restrict__ prefix, int n, int t) {
   int lo = 0, hi = n - 1;
@@ -93,6 +93,7 @@ __global__ void __launch_bounds__(256) k_gather_decay(const MatDesc* __restrict_
     // X's zero padding (zero rows / columns are exact no-ops for NS) and the
     // workspace needs no state between calls.
     XT* X = reinterpret_cast<XT*>(md.X0);
+    const float xs = md.ns_scale[2];  // fp16 prescale (K2, reading R24); 1 on the fp32 path
     if (!md.transposed) {
       // X[a][b] = S[a][b]
 #pragma unroll
@@ -102,7 +103,7 @@ __global__ void __launch_bounds__(256) k_gather_decay(const MatDesc* __restrict_
 #pragma unroll
           for (int c = 0; c < 4; ++c) {
             const int b = b0 + tx * 4 + c;
-            if (b < md.sb_pad) X[(int64_t)a * md.q_pad + b] = to_x<XT>(tile[al][tx * 4 + c]);
+            if (b < md.sb_pad) X[(int64_t)a * md.q_pad + b] = to_x<XT>(xs * tile[al][tx * 4 + c]);
           }
         }
       }
@@ -114,22 +115,23 @@ __global__ void __launch_bounds__(256) k_gather_decay(const MatDesc* __restrict_
 #pragma unroll
         for (int i = 0; i < 8; ++i) {
           const int a = a0 + ac + i;
-          if (a < md.sa_pad) X[(int64_t)b * md.q_pad + a] = to_x<XT>(tile[ac + i][bl]);
+          if (a < md.sa_pad) X[(int64_t)b * md.q_pad + a] = to_x<XT>(xs * tile[ac + i][bl]);
         }
       }
     }
     __syncthreads();
   }
 }
-void launch_gather_decay(bool bf16, int blocks, cudaStream_t s, const MatDesc* mats, const int32_t* tile_prefix_mats,
+void launch_gather_decay(bool x16, int blocks, cudaStream_t s, const MatDesc* mats, const int32_t* tile_prefix_mats,
                          int n_mats, int total_tiles, const int32_t* bad, int decay, float mu) {
-  if (bf16)
-    k_gather_decay<__nv_bfloat16><<<blocks, 256, 0, s>>>(mats, tile_prefix_mats, n_mats, total_tiles, bad, decay, mu);
+  if (x16)
+    k_gather_decay<__half><<<blocks, 256, 0, s>>>(mats, tile_prefix_mats, n_mats, total_tiles, bad, decay, mu);
   else
     k_gather_decay<float><<<blocks, 256, 0, s>>>(mats, tile_prefix_mats, n_mats, total_tiles, bad, decay, mu);
 }
 
-// One warp per matrix: fixed-order sum of the tile partials -> s = 1 / (||X||_F + eps).
+// One warp per matrix: fixed-order sum of the tile partials -> s = 1 / (||X||_F + eps), stored
+// as s' = s / xs (the stored X is xs X, reading R24) with s'^2.
 __global__ void k_norm_finalize(const MatDesc* __restrict__ mats, int n_mats, float eps) {
   const int lane = threadIdx.x & 31;
   const int mi = blockIdx.x * (blockDim.x >> 5) + (threadIdx.x >> 5);
@@ -140,7 +142,7 @@ __global__ void k_norm_finalize(const MatDesc* __restrict__ mats, int n_mats, fl
   for (int i = lane; i < nt; i += 32) s += md.sumsq_partials[i];
   s = warp_sum(s);
   if (lane == 0) {
-    const float inv = 1.0f / (sqrtf(s) + eps);
+    const float inv = 1.0f / (sqrtf(s) + eps) / md.ns_scale[2];
     md.ns_scale[0] = inv;
     md.ns_scale[1] = inv * inv;
   }
@@ -211,10 +213,10 @@ __global__ void __launch_bounds__(256) k_scatter_update(const MatDesc* __restric
     if (md.transposed) __syncthreads();
   }
 }
-void launch_scatter_update(bool bf16, int blocks, cudaStream_t s, const MatDesc* mats, const int32_t* tile_prefix_mats,
+void launch_scatter_update(bool x16, int blocks, cudaStream_t s, const MatDesc* mats, const int32_t* tile_prefix_mats,
                            int n_mats, int total_tiles, const int32_t* bad, float lr, const float* lr_dev) {
-  if (bf16)
-    k_scatter_update<__nv_bfloat16><<<blocks, 256, 0, s>>>(mats, tile_prefix_mats, n_mats, total_tiles, bad, lr, lr_dev);
+  if (x16)
+    k_scatter_update<__half><<<blocks, 256, 0, s>>>(mats, tile_prefix_mats, n_mats, total_tiles, bad, lr, lr_dev);
   else
     k_scatter_update<float><<<blocks, 256, 0, s>>>(mats, tile_prefix_mats, n_mats, total_tiles, bad, lr, lr_dev);
 }

@@ -29,14 +29,6 @@ __device__ __forceinline__ int find_unit(const int32_t* __restrict__ prefix, int
   return lo;
 }
 
-__device__ __forceinline__ uint2 pack4_bf16(float a, float b, float c, float d) {
-  __nv_bfloat162 lo = __floats2bfloat162_rn(a, b), hi = __floats2bfloat162_rn(c, d);
-  uint2 u;
-  u.x = *reinterpret_cast<uint32_t*>(&lo);
-  u.y = *reinterpret_cast<uint32_t*>(&hi);
-  return u;
-}
-
 // ------------------------------------------------------------------ rows mode
 // unit = one X row r in [0, p_pad) of one matrix
 template <int D>  // float4 loads in flight per lane
@@ -52,9 +44,10 @@ __global__ void __launch_bounds__(256) k_gather_rows(const MatDesc* __restrict__
     const int mi = list_mats[li];
     const MatDesc& md = mats[mi];
     const int r = u - list_prefix[li];
-    __nv_bfloat16* xrow = reinterpret_cast<__nv_bfloat16*>(md.X0) + (int64_t)r * md.q_pad;
+    __half* xrow = reinterpret_cast<__half*>(md.X0) + (int64_t)r * md.q_pad;
     float ss = 0.f;
     if (r < md.k) {
+      const float xs = md.ns_scale[2];  // fp16 prescale (K2, reading R24)
       // rows mode: row sel[r] of M; cols mode with transposed M: row sel[r] of M^T (= X row r)
       float* mrow = md.M + (int64_t)md.sel[r] * (md.mt ? md.ldm : md.ld);
       const float f = bad[mi] ? 1.f : mu;
@@ -71,31 +64,31 @@ __global__ void __launch_bounds__(256) k_gather_rows(const MatDesc* __restrict__
 #pragma unroll
           for (int q = 0; q < D; ++q) {
             ss += v[q].x * v[q].x + v[q].y * v[q].y + v[q].z * v[q].z + v[q].w * v[q].w;
-            x4[j + 32 * q] = pack4_bf16(v[q].x, v[q].y, v[q].z, v[q].w);
+            x4[j + 32 * q] = pack4_h(xs * v[q].x, xs * v[q].y, xs * v[q].z, xs * v[q].w);
             m4[j + 32 * q] = make_float4(f * v[q].x, f * v[q].y, f * v[q].z, f * v[q].w);
           }
         }
         for (; j < n4; j += 32) {
           float4 v = m4[j];
           ss += v.x * v.x + v.y * v.y + v.z * v.z + v.w * v.w;
-          x4[j] = pack4_bf16(v.x, v.y, v.z, v.w);
+          x4[j] = pack4_h(xs * v.x, xs * v.y, xs * v.z, xs * v.w);
           m4[j] = make_float4(f * v.x, f * v.y, f * v.z, f * v.w);
         }
         for (int c = 4 * n4 + lane; c < n; c += 32) {
           float v = mrow[c];
           ss += v * v;
-          xrow[c] = __float2bfloat16_rn(v);
+          xrow[c] = __float2half_rn(xs * v);
           mrow[c] = f * v;
         }
       } else {
         for (int c = lane; c < n; c += 32) {
           float v = mrow[c];
           ss += v * v;
-          xrow[c] = __float2bfloat16_rn(v);
+          xrow[c] = __float2half_rn(xs * v);
           mrow[c] = f * v;
         }
       }
-      for (int c = n + lane; c < md.q_pad; c += 32) xrow[c] = __float2bfloat16_rn(0.f);
+      for (int c = n + lane; c < md.q_pad; c += 32) xrow[c] = __float2half_rn(0.f);
     } else {
       uint4* x16 = reinterpret_cast<uint4*>(xrow);  // q_pad % 256 == 0: whole 16-B chunks
       for (int c = lane; c < md.q_pad / 8; c += 32) x16[c] = make_uint4(0, 0, 0, 0);
@@ -121,8 +114,7 @@ __global__ void __launch_bounds__(256) k_scatter_rows(const MatDesc* __restrict_
     const MatDesc& md = mats[mi];
     if (bad[mi]) continue;
     const int r = u - list_prefix[li];
-    const __nv_bfloat16* xrow =
-        reinterpret_cast<const __nv_bfloat16*>(md.final_in_x1 ? md.X1 : md.X0) + (int64_t)r * md.q_pad;
+    const __half* xrow = reinterpret_cast<const __half*>(md.final_in_x1 ? md.X1 : md.X0) + (int64_t)r * md.q_pad;
     float* wrow = md.W + (int64_t)md.sel[r] * md.ld;
     float* orow = md.O_out ? md.O_out + (int64_t)r * md.cols : nullptr;
     const float sc = (lr_dev ? __ldg(lr_dev) : lr) * md.update_scale;
@@ -142,8 +134,8 @@ __global__ void __launch_bounds__(256) k_scatter_rows(const MatDesc* __restrict_
         }
 #pragma unroll
         for (int q = 0; q < D; ++q) {
-          const __nv_bfloat162 lo = *reinterpret_cast<const __nv_bfloat162*>(&o[q].x);
-          const __nv_bfloat162 hi = *reinterpret_cast<const __nv_bfloat162*>(&o[q].y);
+          const __half2 lo = *reinterpret_cast<const __half2*>(&o[q].x);
+          const __half2 hi = *reinterpret_cast<const __half2*>(&o[q].y);
           const float o0 = __low2float(lo), o1 = __high2float(lo), o2 = __low2float(hi), o3 = __high2float(hi);
           w[q].x -= sc * o0; w[q].y -= sc * o1; w[q].z -= sc * o2; w[q].w -= sc * o3;
           w4[j + 32 * q] = w[q];
@@ -156,8 +148,8 @@ __global__ void __launch_bounds__(256) k_scatter_rows(const MatDesc* __restrict_
       for (; j < n4; j += 32) {
         float4 w = w4[j];
         const uint2 o = x4[j];
-        const __nv_bfloat162 lo = *reinterpret_cast<const __nv_bfloat162*>(&o.x);
-        const __nv_bfloat162 hi = *reinterpret_cast<const __nv_bfloat162*>(&o.y);
+        const __half2 lo = *reinterpret_cast<const __half2*>(&o.x);
+        const __half2 hi = *reinterpret_cast<const __half2*>(&o.y);
         const float o0 = __low2float(lo), o1 = __high2float(lo), o2 = __low2float(hi), o3 = __high2float(hi);
         w.x -= sc * o0; w.y -= sc * o1; w.z -= sc * o2; w.w -= sc * o3;
         w4[j] = w;
@@ -166,13 +158,13 @@ __global__ void __launch_bounds__(256) k_scatter_rows(const MatDesc* __restrict_
         }
       }
       for (int c = 4 * n4 + lane; c < n; c += 32) {
-        const float o = __bfloat162float(xrow[c]);
+        const float o = __half2float(xrow[c]);
         wrow[c] -= sc * o;
         if (orow) orow[c] = o;
       }
     } else {
       for (int c = lane; c < n; c += 32) {
-        const float o = __bfloat162float(xrow[c]);
+        const float o = __half2float(xrow[c]);
         wrow[c] -= sc * o;
         if (orow) orow[c] = o;
       }
@@ -184,7 +176,7 @@ __global__ void __launch_bounds__(256) k_scatter_rows(const MatDesc* __restrict_
 // unit = one 32-row slab of X's column range [0, q_pad) (i.e. rows i0..i0+31 of M)
 constexpr int kSlab = 32;
 
-// scatter tile row pitch (bf16 elements): an odd number of 4-byte words, so the transposed
+// scatter tile row pitch (2-byte elements): an odd number of 4-byte words, so the transposed
 // fill tile[part + e][r] (part = 0, 8, 16, 24) spreads over distinct banks; <= k + 8
 __host__ __device__ __forceinline__ int scatter_tile_ld(int k) {
   const int w = (k + 1) / 2;
@@ -227,7 +219,7 @@ __device__ __forceinline__ int col_rank(const uint32_t* mask, const int32_t* ran
   return rank[c >> 5] + __popc(mask[c >> 5] & ((1u << (c & 31)) - 1u));
 }
 
-// smem: mask [1536] u32, rank [1536] i32, tile [kSlab][kMaxColK + 8] bf16
+// smem: mask [1536] u32, rank [1536] i32, tile [kSlab][kMaxColK + 8] fp16
 constexpr int kMaxColK = kMaxColKFast;
 constexpr int kMaskWords = DION2_MAX_SELECT_DIM_WORDS;
 
@@ -239,7 +231,7 @@ __global__ void __launch_bounds__(256) k_gather_cols_t(const MatDesc* __restrict
   extern __shared__ __align__(16) uint8_t sm[];
   uint32_t* mask = reinterpret_cast<uint32_t*>(sm);
   int32_t* rank = reinterpret_cast<int32_t*>(sm + 4 * mask_words);
-  __nv_bfloat16* tile = reinterpret_cast<__nv_bfloat16*>(sm + 8 * mask_words);  // [kSlab][ldt]
+  __half* tile = reinterpret_cast<__half*>(sm + 8 * mask_words);  // [kSlab][ldt]
   __shared__ float wsum[8];
   int cur_mat = -1;
   const int lane = threadIdx.x & 31, wid = threadIdx.x >> 5;
@@ -254,16 +246,17 @@ __global__ void __launch_bounds__(256) k_gather_cols_t(const MatDesc* __restrict
     const int slab = u - list_prefix[li];
     const int i0 = slab * kSlab;
     const int k = md.k;
-    const int ldt = k + 8;  // bf16 elements per tile row (padding breaks bank conflicts)
+    const int ldt = k + 8;  // fp16 elements per tile row (padding breaks bank conflicts)
     const float f = bad[mi] ? 1.f : mu;
+    const float xs = md.ns_scale[2];  // fp16 prescale (K2, reading R24)
     const int n = (int)md.cols;
     float ss = 0.f;
     // each warp streams rows i0 + wid + 8*j (4 rows per warp)
     for (int il = wid; il < kSlab; il += 8) {
       const int64_t i = (int64_t)i0 + il;
-      __nv_bfloat16* trow = tile + il * ldt;
+      __half* trow = tile + il * ldt;
       if (i >= md.rows) {
-        for (int r = lane; r < k; r += 32) trow[r] = __float2bfloat16_rn(0.f);
+        for (int r = lane; r < k; r += 32) trow[r] = __float2half_rn(0.f);
         continue;
       }
       float* mrow = md.M + i * md.ld;
@@ -289,7 +282,7 @@ __global__ void __launch_bounds__(256) k_gather_cols_t(const MatDesc* __restrict
 #pragma unroll
             for (int q = 0; q < 4; ++q) {
               if (bits[u] & (1u << q)) {
-                trow[rk++] = __float2bfloat16_rn(e[q]);
+                trow[rk++] = __float2half_rn(xs * e[q]);
                 ss += e[q] * e[q];
                 e[q] *= f;
               }
@@ -300,7 +293,7 @@ __global__ void __launch_bounds__(256) k_gather_cols_t(const MatDesc* __restrict
         for (int c = 4 * n4 + lane; c < n; c += 32) {
           if (!((mask[c >> 5] >> (c & 31)) & 1u)) continue;
           const float v = mrow[c];
-          trow[col_rank(mask, rank, c)] = __float2bfloat16_rn(v);
+          trow[col_rank(mask, rank, c)] = __float2half_rn(xs * v);
           ss += v * v;
           mrow[c] = f * v;
         }
@@ -308,7 +301,7 @@ __global__ void __launch_bounds__(256) k_gather_cols_t(const MatDesc* __restrict
         for (int c = lane; c < n; c += 32) {
           if (!((mask[c >> 5] >> (c & 31)) & 1u)) continue;
           const float v = mrow[c];
-          trow[col_rank(mask, rank, c)] = __float2bfloat16_rn(v);
+          trow[col_rank(mask, rank, c)] = __float2half_rn(xs * v);
           ss += v * v;
           mrow[c] = f * v;
         }
@@ -323,12 +316,12 @@ __global__ void __launch_bounds__(256) k_gather_cols_t(const MatDesc* __restrict
       md.sumsq_partials[slab] = s;
     }
     // X[r][i0 .. i0+31] = tile[0..31][r]  (64 contiguous bytes per X row), rows r >= k are zero
-    __nv_bfloat16* X = reinterpret_cast<__nv_bfloat16*>(md.X0);
+    __half* X = reinterpret_cast<__half*>(md.X0);
     for (int t = threadIdx.x; t < md.p_pad * 4; t += blockDim.x) {
       const int r = t >> 2, part = (t & 3) * 8;
       uint4 out = make_uint4(0, 0, 0, 0);
       if (r < k) {
-        __nv_bfloat16 h[8];
+        __half h[8];
 #pragma unroll
         for (int e = 0; e < 8; ++e) h[e] = tile[(part + e) * ldt + r];
         out = *reinterpret_cast<uint4*>(h);
@@ -339,7 +332,7 @@ __global__ void __launch_bounds__(256) k_gather_cols_t(const MatDesc* __restrict
   }
 }
 
-// smem: column bitmask + popcount prefix (mask_words each) + the [kSlab][ldt >= k + 8] bf16 tile
+// smem: column bitmask + popcount prefix (mask_words each) + the [kSlab][ldt >= k + 8] fp16 tile
 size_t cols_t_smem_bytes(int k, int mask_words) { return 8 * (size_t)mask_words + (size_t)kSlab * (k + 8) * 2; }
 static int mask_words_for(int64_t max_n) { return (int)((((max_n + 31) / 32) + 3) / 4 * 4); }
 
@@ -372,7 +365,7 @@ __global__ void __launch_bounds__(256, 4) k_scatter_cols_idx(const MatDesc* __re
                                                              int slab_h) {
   extern __shared__ __align__(16) uint8_t sm[];
   int32_t* ssel = reinterpret_cast<int32_t*>(sm);                                   // [max_k]
-  __nv_bfloat16* tile = reinterpret_cast<__nv_bfloat16*>(sm + 4 * ((max_k + 3) & ~3));  // [slab_h][ldt]
+  __half* tile = reinterpret_cast<__half*>(sm + 4 * ((max_k + 3) & ~3));  // [slab_h][ldt]
   int cur_mat = -1;
   const int lane = threadIdx.x & 31, wid = threadIdx.x >> 5;
   for (int u = blockIdx.x; u < total_units; u += gridDim.x) {
@@ -393,11 +386,11 @@ __global__ void __launch_bounds__(256, 4) k_scatter_cols_idx(const MatDesc* __re
       const int i0 = slab * kSlab + h0;
       if (i0 >= md.rows) break;
       // O tile: tile[il][r] = X_T[r][i0 + il]
-      const __nv_bfloat16* X = reinterpret_cast<const __nv_bfloat16*>(md.final_in_x1 ? md.X1 : md.X0);
+      const __half* X = reinterpret_cast<const __half*>(md.final_in_x1 ? md.X1 : md.X0);
       for (int t = threadIdx.x; t < k * parts; t += blockDim.x) {
         const int r = t / parts, part = (t % parts) * 8;
         const uint4 in = *reinterpret_cast<const uint4*>(X + (int64_t)r * md.q_pad + i0 + part);
-        const __nv_bfloat16* h = reinterpret_cast<const __nv_bfloat16*>(&in);
+        const __half* h = reinterpret_cast<const __half*>(&in);
 #pragma unroll
         for (int e = 0; e < 8; ++e) tile[(part + e) * ldt + r] = h[e];
       }
@@ -406,7 +399,7 @@ __global__ void __launch_bounds__(256, 4) k_scatter_cols_idx(const MatDesc* __re
       for (int il = wid; il < slab_h; il += 8) {
         const int64_t i = (int64_t)i0 + il;
         if (i >= md.rows) break;
-        const __nv_bfloat16* trow = tile + il * ldt;
+        const __half* trow = tile + il * ldt;
         float* wrow = md.W + i * md.ld;
         float* orow = md.O_out ? md.O_out + i * k : nullptr;
         for (int r0 = lane; r0 < k; r0 += 32 * U) {
@@ -422,7 +415,7 @@ __global__ void __launch_bounds__(256, 4) k_scatter_cols_idx(const MatDesc* __re
           for (int q = 0; q < U; ++q) {
             const int r = r0 + 32 * q;
             if (r < k) {
-              const float o = __bfloat162float(trow[r]);
+              const float o = __half2float(trow[r]);
               w[q] -= sc * o;
               wrow[c[q]] = w[q];
               if (orow) orow[r] = o;

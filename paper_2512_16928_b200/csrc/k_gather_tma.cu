@@ -1,4 +1,4 @@
-// K3 rows path, TMA-staged (Alg. 1 l.4-5): X row r = bf16(M[sel[r], :])
+// K3 rows path, TMA-staged (Alg. 1 l.4-5): X row r = fp16(xs * M[sel[r], :]) (xs: reading R24)
 // (rows mode; with transposed momentum the row sel[r] of M^T), M[sel[r], :] <- mu * M[sel[r], :],
 // per-row sum of squares for ||X||_F.  Same semantics, unit list and outputs as
 // k_gather_rows (k_gather_scatter_fast.cu); the data moves through the bulk-copy (TMA) engine:
@@ -7,7 +7,7 @@
 //                       (mbarrier complete_tx), S - 1 chunks ahead of the consumers
 //   warps 1..4          decay + convert in shared memory; one elected thread then issues
 //                       cp.async.bulk shared -> global stores of the decayed M chunk and the
-//                       bf16 X chunk, and releases the stage once the stores have read it
+//                       fp16 X chunk, and releases the stage once the stores have read it
 //
 // so the loads in flight per SM are bounded by shared memory, not by registers.  Requires
 // 16-byte aligned rows with a multiple of 8 elements (vec4 and n % 8 == 0); the launcher
@@ -74,7 +74,7 @@ __global__ void __launch_bounds__(kThreads) k_gather_rows_tma(const MatDesc* __r
                                                               const int32_t* __restrict__ bad, float mu) {
   extern __shared__ __align__(128) uint8_t sm[];
   float* sm_m = reinterpret_cast<float*>(sm);                                    // [S][kCh]
-  __nv_bfloat16* sm_x = reinterpret_cast<__nv_bfloat16*>(sm + S * kCh * 4);      // [S][kCh]
+  __half* sm_x = reinterpret_cast<__half*>(sm + S * kCh * 4);                    // [S][kCh]
   uint64_t* full = reinterpret_cast<uint64_t*>(sm + S * kCh * 6);
   uint64_t* empty = full + S;
   __shared__ float red[4];
@@ -119,7 +119,7 @@ __global__ void __launch_bounds__(kThreads) k_gather_rows_tma(const MatDesc* __r
   for (int u = blockIdx.x; u < total_units; u += gridDim.x) {
     const RowUnit w = row_unit(mats, lm, lp, nl, u);
     const MatDesc& md = *w.md;
-    __nv_bfloat16* xrow = reinterpret_cast<__nv_bfloat16*>(md.X0) + (int64_t)w.r * md.q_pad;
+    __half* xrow = reinterpret_cast<__half*>(md.X0) + (int64_t)w.r * md.q_pad;
     if (!w.mrow) {
       // X row r >= k: zeros (q_pad % 256 == 0: whole 16-B chunks), no M traffic
       mbar_wait(&full[stage], phase);
@@ -139,6 +139,7 @@ __global__ void __launch_bounds__(kThreads) k_gather_rows_tma(const MatDesc* __r
       continue;
     }
     const float f = bad[w.mi] ? 1.f : mu;
+    const float xs = md.ns_scale[2];  // fp16 prescale (K2, reading R24)
     float ss = 0.f;
     for (int c = 0; c < w.nch; ++c) {
       mbar_wait(&full[stage], phase);
@@ -149,8 +150,7 @@ __global__ void __launch_bounds__(kThreads) k_gather_rows_tma(const MatDesc* __r
       for (int j = ct; j < len / 4; j += kConsumers) {
         const float4 v = m4[j];
         ss += v.x * v.x + v.y * v.y + v.z * v.z + v.w * v.w;
-        __nv_bfloat162 lo = __floats2bfloat162_rn(v.x, v.y), hi = __floats2bfloat162_rn(v.z, v.w);
-        x4[j] = make_uint2(*reinterpret_cast<uint32_t*>(&lo), *reinterpret_cast<uint32_t*>(&hi));
+        x4[j] = pack4_h(xs * v.x, xs * v.y, xs * v.z, xs * v.w);
         m4[j] = make_float4(f * v.x, f * v.y, f * v.z, f * v.w);
       }
       fence_proxy_async_smem();  // the shared writes are visible to the bulk-copy engine

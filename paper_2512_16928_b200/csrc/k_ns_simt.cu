@@ -53,7 +53,7 @@ __global__ void __launch_bounds__(256) k_ns_gemm_simt_f32(const NsParams P, int 
     __syncthreads();
   }
   float osc = 1.f;
-  if (P.scale_sel) osc = P.ns_scale_all[2 * g.gmats[z] + (P.scale_sel - 1)];
+  if (P.scale_sel) osc = P.ns_scale_all[4 * g.gmats[z] + (P.scale_sel - 1)];
 #pragma unroll
   for (int i = 0; i < 4; ++i) {
     const int r = m0 + ty * 4 + i;

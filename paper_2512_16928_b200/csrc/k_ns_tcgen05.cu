@@ -6,9 +6,9 @@
 //   poly  : B  = b*A + c*A A^T        (A symmetric, so A A^T = A^2; K-major)
 //   apply : X' = s_t * (a*X + B X)    (M = p, N = q, K = p; X is the MN-major B operand)
 // with s_1 = 1/(||X||_F + eps) folding the pre-normalisation into the first
-// iteration and s_t = 1 afterwards.  Each output is rounded once to bf16;
-// the poly epilogue reuses the same bf16 A for the b*A term as the MMA saw
-// ("consistent A", SURVEY finding 3).
+// iteration and s_t = 1 afterwards.  Each output is rounded once to fp16 (or bf16,
+// p.in_f16 / p.out_f16; reading R24); the poly epilogue reuses the same 16-bit A for the
+// b*A term as the MMA saw ("consistent A", SURVEY finding 3).
 //
 // Kernel: persistent, warp-specialised, one CTA per SM.
 //   warp 0      TMA producer (one elected lane): A tile 128x64, B tile BNx64 per stage
@@ -49,6 +49,8 @@ __device__ __forceinline__ uint32_t pack_bf16x2(float lo, float hi) {
   __nv_bfloat162 v = __floats2bfloat162_rn(lo, hi);
   return *reinterpret_cast<uint32_t*>(&v);
 }
+// a/b operand format fields of the instruction descriptor: 1 = bf16, 0 = fp16
+constexpr uint32_t kIdescAbFmt1 = (7u << 7) | (7u << 10);
 
 template <int BN>
 __global__ void __launch_bounds__(192, 1) k_ns_gemm_tc(const __grid_constant__ NsTcParams P) {
@@ -111,7 +113,7 @@ __global__ void __launch_bounds__(192, 1) k_ns_gemm_tc(const __grid_constant__ N
           tma_load_3d(sa, &P.mapA[c.group], &full_bar[stage], kb * kBK, c.tm * kBM, c.z);
           if (p.b_kmajor) {
             tma_load_3d(sb, &P.mapB[c.group], &full_bar[stage], kb * kBK, c.tn * BN, c.z);
-          } else if (G.pieces_qo) {
+          } else if (G.pieces_load) {
             // distributed owner apply: the N axis (q) of X0 runs over the P rank pieces
 #pragma unroll
             for (int j = 0; j < BN / 64; ++j) {
@@ -131,7 +133,7 @@ __global__ void __launch_bounds__(192, 1) k_ns_gemm_tc(const __grid_constant__ N
   } else if (warp == 1) {
     if (lane == 0) {
       // ---------------- MMA issuer
-      const uint32_t idesc = p.b_kmajor ? kIdescK : kIdescMN;
+      const uint32_t idesc = (p.b_kmajor ? kIdescK : kIdescMN) & (p.in_f16 ? ~kIdescAbFmt1 : ~0u);
       int stage = 0;
       uint32_t phase = 0;
       int it = 0;
@@ -174,11 +176,12 @@ __global__ void __launch_bounds__(192, 1) k_ns_gemm_tc(const __grid_constant__ N
       const int acc = it & 1;
       const uint32_t acc_phase = (it >> 1) & 1;
       float osc = 1.f;
-      if (p.scale_sel) osc = p.ns_scale_all[2 * G.gmats[c.z] + (p.scale_sel - 1)];
+      if (p.scale_sel) osc = p.ns_scale_all[4 * G.gmats[c.z] + (p.scale_sel - 1)];
       const float ca = p.cacc * osc, cc = p.cC * osc, dterm = p.diag * osc;
       const int64_t row = (int64_t)c.tm * kBM + row_in_tile;
-      const __nv_bfloat16* cin =
-          G.cin ? reinterpret_cast<const __nv_bfloat16*>(G.cin) + (int64_t)c.z * G.cin_mstride + row * G.cin_ld +
+      // cin holds 2-byte elements (bf16, or fp16 when in_f16)
+      const uint16_t* cin =
+          G.cin ? reinterpret_cast<const uint16_t*>(G.cin) + (int64_t)c.z * G.cin_mstride + row * G.cin_ld +
                       (int64_t)c.tn * BN
                 : nullptr;
       // C-term (poly: b*A) for chunk 0 is fetched before the accumulator is ready,
@@ -195,13 +198,25 @@ __global__ void __launch_bounds__(192, 1) k_ns_gemm_tc(const __grid_constant__ N
         float v[32];
         tmem_ld_32x32b_x32(tmem_base + acc * BN + cc32 * 32 + ((uint32_t)(lg * 32) << 16), v);
         float cv[32];
+        if (p.in_f16) {
 #pragma unroll
-        for (int q = 0; q < 4; ++q) {
-          const __nv_bfloat162* h = reinterpret_cast<const __nv_bfloat162*>(&craw[q]);
+          for (int q = 0; q < 4; ++q) {
+            const __half2* h = reinterpret_cast<const __half2*>(&craw[q]);
 #pragma unroll
-          for (int e = 0; e < 4; ++e) {
-            cv[q * 8 + 2 * e] = __low2float(h[e]);
-            cv[q * 8 + 2 * e + 1] = __high2float(h[e]);
+            for (int e = 0; e < 4; ++e) {
+              cv[q * 8 + 2 * e] = __low2float(h[e]);
+              cv[q * 8 + 2 * e + 1] = __high2float(h[e]);
+            }
+          }
+        } else {
+#pragma unroll
+          for (int q = 0; q < 4; ++q) {
+            const __nv_bfloat162* h = reinterpret_cast<const __nv_bfloat162*>(&craw[q]);
+#pragma unroll
+            for (int e = 0; e < 4; ++e) {
+              cv[q * 8 + 2 * e] = __low2float(h[e]);
+              cv[q * 8 + 2 * e + 1] = __high2float(h[e]);
+            }
           }
         }
         if (cin && cc32 + 1 < BN / 32) {
@@ -214,20 +229,18 @@ __global__ void __launch_bounds__(192, 1) k_ns_gemm_tc(const __grid_constant__ N
         float o[32];
 #pragma unroll
         for (int e = 0; e < 32; ++e) o[e] = ca * v[e] + cc * cv[e] + (e == dcol ? dterm : 0.f);
-        // stage the 32x32 bf16 chunk in SWIZZLE_64B layout (row = lane, 16-B chunk
+        // stage the 32x32 16-bit chunk in SWIZZLE_64B layout (row = lane, 16-B chunk
         // q stored at q ^ ((row >> 1) & 3): conflict-free) and TMA-store it
         uint8_t* buf = stage_base + (lg * 2 + sbuf) * 2048;
         if (lane == 0) bulk_wait_read<1>();  // the store that used this buffer two chunks ago is done reading
         __syncwarp();
+        uint32_t pk[16];
 #pragma unroll
-        for (int q = 0; q < 4; ++q) {
-          uint4 u;
-          u.x = pack_bf16x2(o[q * 8 + 0], o[q * 8 + 1]);
-          u.y = pack_bf16x2(o[q * 8 + 2], o[q * 8 + 3]);
-          u.z = pack_bf16x2(o[q * 8 + 4], o[q * 8 + 5]);
-          u.w = pack_bf16x2(o[q * 8 + 6], o[q * 8 + 7]);
-          sts128(smem_u32(buf) + lane * 64 + ((q ^ ((lane >> 1) & 3)) << 4), u);
-        }
+        for (int q = 0; q < 16; ++q) pk[q] = p.out_f16 ? pack2_h(o[2 * q], o[2 * q + 1]) : pack_bf16x2(o[2 * q], o[2 * q + 1]);
+#pragma unroll
+        for (int q = 0; q < 4; ++q)
+          sts128(smem_u32(buf) + lane * 64 + ((q ^ ((lane >> 1) & 3)) << 4),
+                 make_uint4(pk[4 * q], pk[4 * q + 1], pk[4 * q + 2], pk[4 * q + 3]));
         fence_proxy_async_smem();
         __syncwarp();
         if (lane == 0) {

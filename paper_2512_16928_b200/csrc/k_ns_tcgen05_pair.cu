@@ -158,9 +158,9 @@ __global__ void __cluster_dims__(2, 1, 1) __launch_bounds__(kPairThreads, 1)
           const bool at = kSymIn && ((kb * kBK) >> 8) < c.tm;
           const bool bt = kSymIn && ((kb * kBK) >> 8) < c.tn;
           // distributed owner gram: the K axis (q) runs over the P rank pieces of X0
-          const int pr = G.pieces_qo ? (kb * kBK) / G.pieces_qo : 0;
-          const int pc = G.pieces_qo ? kb * kBK - pr * G.pieces_qo : kb * kBK;
-          const CUtensorMap* pmap = G.pieces_qo ? &P.mapP[c.group][pr] : nullptr;
+          const int pr = G.pieces_load ? (kb * kBK) / G.pieces_qo : 0;
+          const int pc = G.pieces_load ? kb * kBK - pr * G.pieces_qo : kb * kBK;
+          const CUtensorMap* pmap = G.pieces_load ? &P.mapP[c.group][pr] : nullptr;
           if (!at) {
             tma_load_3d_pair(sa, pmap ? pmap : &P.mapA[c.group], leader_full, pc, c.tm * 256 + (int)rank * 128, c.z);
           } else {
@@ -272,7 +272,7 @@ __global__ void __cluster_dims__(2, 1, 1) __launch_bounds__(kPairThreads, 1)
         continue;
       }
       float osc = 1.f;
-      if (p.scale_sel) osc = p.ns_scale_all[2 * G.gmats[c.z] + (p.scale_sel - 1)];
+      if (p.scale_sel) osc = p.ns_scale_all[4 * G.gmats[c.z] + (p.scale_sel - 1)];
       const float ca = p.cacc * osc, cc = p.cC * osc, dterm = p.diag * osc;
       const int64_t row = (int64_t)c.tm * 256 + row_in_tile;
       // cin holds 2-byte elements (bf16, or fp16 when in_f16)
@@ -392,7 +392,7 @@ __global__ void __launch_bounds__(256) k_splitk_reduce(const NsParams p) {
     a.x += v.x; a.y += v.y; a.z += v.z; a.w += v.w;
   }
   float osc = 1.f;
-  if (p.scale_sel) osc = p.ns_scale_all[2 * G.gmats[c.z] + (p.scale_sel - 1)];
+  if (p.scale_sel) osc = p.ns_scale_all[4 * G.gmats[c.z] + (p.scale_sel - 1)];
   const float ca = p.cacc * osc, dterm = p.diag * osc;
   const int64_t row = (int64_t)c.tm * 256 + r, col = (int64_t)c.tn * 256 + c4;
   float o[4] = {ca * a.x, ca * a.y, ca * a.z, ca * a.w};

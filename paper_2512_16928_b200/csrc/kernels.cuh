@@ -43,10 +43,10 @@ __global__ void k_topk_select(const MatDesc* __restrict__ mats, const int32_t* _
 constexpr int kTileA = 32;   // S rows per gather/scatter tile
 constexpr int kTileB = 64;   // S cols per gather/scatter tile
 // host launchers (the templates are instantiated in their own translation unit)
-void launch_gather_decay(bool bf16, int blocks, cudaStream_t s, const MatDesc* mats, const int32_t* tile_prefix_mats,
+void launch_gather_decay(bool x16, int blocks, cudaStream_t s, const MatDesc* mats, const int32_t* tile_prefix_mats,
                          int n_mats, int total_tiles, const int32_t* bad, int decay, float mu);
 // lr_dev (optional): eta read on the device at run time (CUDA graphs under a schedule), else lr
-void launch_scatter_update(bool bf16, int blocks, cudaStream_t s, const MatDesc* mats, const int32_t* tile_prefix_mats,
+void launch_scatter_update(bool x16, int blocks, cudaStream_t s, const MatDesc* mats, const int32_t* tile_prefix_mats,
                            int n_mats, int total_tiles, const int32_t* bad, float lr, const float* lr_dev);
 __global__ void k_norm_finalize(const MatDesc* __restrict__ mats, int n_mats, float eps);
 
@@ -84,12 +84,16 @@ void launch_cols_local_scores(cudaStream_t s, const MatDesc* mats, const int32_t
 void launch_sum_rank_scores(cudaStream_t s, const float* gathered, float* out, int64_t total, int world);
 void launch_piece_sumsq(cudaStream_t s, const MatDesc* mats, int n, float* out);
 void launch_assemble(cudaStream_t s, const MatDesc* omats, int n_owned, int max_p_pad, const PieceTable& T,
-                     const uint8_t* recv, const float* sumsq_all, int n_total, float eps);
+                     const uint8_t* recv, const float* sumsq_all, const float* xs_all, int n_total, float eps);
 void launch_disassemble(cudaStream_t s, const MatDesc* omats, int n_owned, int max_k, const PieceTable& T,
                         uint8_t* send);
 
 
 // ---------------- compressed DP-sync (k_dpsync.cu): M[K] <-> contiguous fp32 buffer
+// tail[2 n]: combine = 0 packs {largest score, non-finite flag} per matrix before the all-reduce;
+// combine = 1 reads the sums back: global non-finite flag (bad, status) and the fp16 prescale
+void launch_dp_tail(cudaStream_t s, const MatDesc* mats, int n_mats, float* tail, int32_t* bad, int32_t* status,
+                    bool combine);
 void launch_dp_pack(bool unpack, cudaStream_t s, const MatDesc* mats, const int32_t* row_prefix, const int64_t* buf_off,
                     int n_mats, int total_rows, float* buf, float scale, const int32_t* bad);
 
@@ -112,6 +116,7 @@ struct NsGroup {
   // per-rank tensor maps NsTcParams::mapP[group][kind * P + r] (kind 0: box {64, 128} loads,
   // 1: box {64, 64} MN-major loads, 2: box {32, 32} stores).  pieces_qo = 0: plain layout.
   int pieces_qo, pieces_P, pieces_map;
+  int pieces_load;           // gram / apply: the X operand is read from the received pieces
   int pieces_store;          // apply: X_T TMA-stored into the outgoing pieces (else into `out`)
 };
 
@@ -122,10 +127,10 @@ struct NsParams {
   float diag;                // added on the global diagonal (poly: C = a*I + b*A + c*A^2)
   int scale_sel;             // 0: oscale = 1; 1: s; 2: s^2
   int sym;                   // symmetric output: upper-triangle tiles only, mirrored by the epilogue (pair kernel)
-  const float* ns_scale_all; // [n_mats][2]
+  const float* ns_scale_all; // [n_mats][4] (MatDesc::ns_scale)
   int b_kmajor;
-  int in_f16;                // operands (and cin) are fp16, else bf16 (pair kernel only)
-  int out_f16;               // output written as fp16, else bf16 (pair kernel only)
+  int in_f16;                // operands (and cin) are fp16, else bf16
+  int out_f16;               // output written as fp16, else bf16
   int reverse;               // walk the tile list backwards (L2 reuse of the previous launch's last writes)
   // upper-triangle storage of symmetric p x p buffers (pair kernel, Gram-space launches):
   int sym_in;                // operands hold only their upper 256 x 256 tiles: a lower k-block is read

@@ -154,6 +154,8 @@ struct Launcher {
 };
 
 int build_layout(Plan& P, const dion2_matrix* mats, int n, const dion2_config* c);
+// restart segments [t0, t1) of the Gram-space NS form (reading R24)
+std::vector<std::pair<int, int>> ns_segments(const dion2_config* c, int T);
 int build_device_plan(Plan& P, const dion2_matrix* mats, const dion2_config* c, void* ws);
 void ensure_device_attrs();
 int run_ns(Plan& P, const dion2_config* c, Launcher& L, cudaStream_t s, bool do_norm);

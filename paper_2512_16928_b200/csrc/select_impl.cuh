@@ -18,7 +18,9 @@ struct SelectSmem {
   uint32_t hist[256];
   int warp_tot[33];
   uint32_t s_prefix, s_remaining;
+  uint32_t smax;  // bits of the largest score (non-negative floats order like their bits)
 };
+
 
 __device__ __forceinline__ int block_exclusive_scan(int v, int* warp_tot, int* total_out) {
   const int lane = threadIdx.x & 31, wid = threadIdx.x >> 5;
@@ -61,6 +63,9 @@ __device__ __forceinline__ void select_matrix(const MatDesc& md, int mi, uint32_
 
   // 1. scores -> keys (cols mode: fixed-order sum of the K1 row-block partials)
   int nonfinite = 0;
+  uint32_t smax = 0u;
+  if (tid == 0) sh.smax = 0u;
+  __syncthreads();
 #pragma unroll 4
   for (int i = tid; i < d; i += blockDim.x) {
     float s;
@@ -72,13 +77,20 @@ __device__ __forceinline__ void select_matrix(const MatDesc& md, int mi, uint32_
       s = __ldcg(md.scores + i);
     }
     if (!(s <= 3.402823466e38f)) nonfinite = 1;  // NaN or +Inf
+    smax = max(smax, __float_as_uint(s));
     // Random rule: the k SMALLEST Philox keys = the k largest complemented keys;
     // ties (p ~ 2^-32) go to the lower index exactly as for the l1 rule.
     keys[i] = random_sel ? ~philox_word0((uint32_t)i, (uint32_t)step, (uint32_t)(step >> 32), (uint32_t)md.mid,
                                          (uint32_t)seed, (uint32_t)(seed >> 32))
                          : __float_as_uint(s);
   }
+  smax = __reduce_max_sync(0xffffffffu, smax);
+  if ((tid & 31) == 0) atomicMax(&sh.smax, smax);
   nonfinite = __syncthreads_or(nonfinite);
+  if (tid == 0 && md.ns_scale) {
+    md.ns_scale[2] = (md.x16 && !nonfinite) ? x16_prescale(__uint_as_float(sh.smax)) : 1.f;
+    md.ns_scale[3] = __uint_as_float(sh.smax);  // the bound itself (compressed DP-sync combines it)
+  }
   if (nonfinite) {
     if (tid == 0) {
       bad[mi] = 1;

@@ -1,17 +1,13 @@
 #!/bin/bash
-# One gpurun call: GPU parity tests, then a short bench.  Output under gpurun_out/.
-set -u
+# GPU suite + smoke + a short bench line (run through gpurun; logs in gpurun_out/)
+cd "$(dirname "$0")/.."
 mkdir -p gpurun_out
-nvidia-smi --query-gpu=name,clocks.sm,clocks.max.sm --format=csv > gpurun_out/gpu.txt 2>&1
-if [ "${RUN_DEBUG:-0}" = "1" ]; then
-  DION2_DEBUG_SYNC=1 timeout 600 python scripts/debug_step.py > gpurun_out/debug.log 2>&1
-  echo "debug exit $?" >> gpurun_out/debug.log
-fi
-if [ "${RUN_TESTS:-1}" = "1" ]; then
-  timeout 900 python -m pytest tests -m gpu -q --timeout 300 -p no:cacheprovider > gpurun_out/gputest.log 2>&1
-  echo "pytest exit $?" >> gpurun_out/gputest.log
-fi
-if [ "${RUN_BENCH:-1}" = "1" ]; then
-  timeout 900 python bench.py --steps ${STEPS:-10} --warmup 3 > gpurun_out/bench.log 2>&1
-  echo "bench exit $?" >> gpurun_out/bench.log
+python -c "import __graft_entry__ as g; g.build()" > gpurun_out/build.log 2>&1
+timeout ${TEST_TIMEOUT:-1500} python -m pytest tests -m gpu -q -x --timeout 600 -p no:cacheprovider ${TESTK:+-k "$TESTK"} > gpurun_out/gpu_tests.log 2>&1
+echo "tests rc=$?" >> gpurun_out/gpu_tests.log
+timeout 300 python -c "import __graft_entry__ as g; g.smoke()" > gpurun_out/smoke.log 2>&1
+echo "smoke rc=$?" >> gpurun_out/smoke.log
+if [ -z "$NO_BENCH" ]; then
+  timeout 600 python bench.py --steps 10 --warmup 3 ${BENCH_ARGS} > gpurun_out/bench.log 2> gpurun_out/bench.err
+  echo "bench rc=$?" >> gpurun_out/bench.err
 fi

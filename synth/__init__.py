@@ -44,6 +44,38 @@ def gen_grad(m: int, n: int, seed: int = 0, mid: int = 0, step: int = 0, row_sca
     return g
 
 
+def _orthonormal(r: np.random.Generator, rows: int, cols: int) -> np.ndarray:
+    q, _ = np.linalg.qr(r.standard_normal((rows, cols)))
+    return q
+
+
+def gen_grad_structured(m: int, n: int, seed: int = 0, mid: int = 0, step: int = 0, kind: str = "spike",
+                        rank: int = 1, ratio: float = 50.0, gamma: float = 1.0) -> np.ndarray:
+    """Ill-conditioned gradients (the low-rank-dominated momenta real training produces; DESIGN.md
+    "Input recipe").  The singular directions U (m x r), V (n x r) are fixed per (seed, matrix),
+    so they accumulate coherently in the momentum over steps; only the noise is per step.
+
+    kind="spike": G = Z + ratio * sqrt(max(m, n)) * U V^T with r = rank equal spikes and
+        Z ~ N(0, 1): sqrt(max(m, n)) is the scale of Z's singular values, so sigma_1 / median of
+        G (and of a selected submatrix) is of order ``ratio``.
+    kind="power": G = sqrt(max(m, n)) * U diag(i^-gamma) V^T + 1e-3 Z, r = min(m, n)."""
+    fixed = rng(seed, mid, (1 << 29) + 1)
+    r = rng(seed, mid, step)
+    z = r.standard_normal((m, n), dtype=np.float32)
+    big = float(np.sqrt(max(m, n)))
+    if kind == "spike":
+        u, v = _orthonormal(fixed, m, rank), _orthonormal(fixed, n, rank)
+        g = z.astype(np.float64) + ratio * big * (u @ v.T)
+    elif kind == "power":
+        k = min(m, n)
+        u, v = _orthonormal(fixed, m, k), _orthonormal(fixed, n, k)
+        sig = np.arange(1, k + 1, dtype=np.float64) ** (-gamma)
+        g = big * ((u * sig) @ v.T) + 1e-3 * z
+    else:
+        raise ValueError(kind)
+    return g.astype(np.float32)
+
+
 def gen_scores_with_ties(d: int, seed: int, n_distinct: int) -> np.ndarray:
     """Non-negative scores with many exact duplicates (tie-break tests)."""
     r = rng(seed, 0, 0)

@@ -18,7 +18,7 @@ import numpy as np
 import torch
 
 import oracle as O
-from synth import gen_grad, gen_w0
+from synth import gen_grad, gen_grad_structured, gen_w0
 from paper_2512_16928_b200 import Dion2
 
 TIE_REL = 1e-6
@@ -56,13 +56,16 @@ def run_parity(shapes: Sequence[Tuple[int, int]], alpha: float, axis: str = "aut
                steps: int = 10, seed: int = 0, mu: float = 0.95, lr: float = 0.02, row_scaled: bool = False,
                decay_mode: int = 0, check_bitwise: bool = True, device: str = "cuda", select: str = "l1",
                sel_seed: int = 0, m_transposed: bool = False, grad_bf16: bool = False, ns_form: str = "auto",
-               ns_coeffs=None, storage_transposed: bool = False) -> ParityResult:
+               ns_coeffs=None, storage_transposed: bool = False, structure: Optional[dict] = None,
+               scale_mode: int = 0) -> ParityResult:
     """m_transposed: store M transposed (cols x rows) for every column-mode matrix.
     storage_transposed: W, M, G of every matrix live as (n, m) tensors (JAX / Flax (in, out)
     layout, ABI v5); the comparisons use their logical (m, n) views.
-    ns_form: "auto" | "direct" | "gram" (reading R23); ns_coeffs: per-iteration (a, b, c), T = len."""
+    ns_form: "auto" | "direct" | "gram" (reading R23); ns_coeffs: per-iteration (a, b, c), T = len.
+    structure: kwargs of synth.gen_grad_structured (ill-conditioned gradients) instead of N(0, 1).
+    scale_mode: 1 = the submatrix scale sqrt(k/n) variant (f3)."""
     res = ParityResult()
-    cfg_o = oracle_cfg(alpha, axis, mu, lr, decay_mode)
+    cfg_o = oracle_cfg(alpha, axis, mu, lr, decay_mode, scale_mode)
     cfg_o.select, cfg_o.seed = select, sel_seed
     ns_kw = dict(ns_form=ns_form)
     if ns_coeffs is not None:
@@ -84,13 +87,16 @@ def run_parity(shapes: Sequence[Tuple[int, int]], alpha: float, axis: str = "aut
     Wr = [w.astype(np.float64) for w in W0]
     Mr = [np.zeros((m, n)) for (m, n) in shapes]
     opt = Dion2(alpha=alpha, mu=mu, lr=lr, axis=axis, precision=precision, decay_mode=decay_mode, select=select,
-                seed=sel_seed, **ns_kw)
+                seed=sel_seed, scale_mode=scale_mode, **ns_kw)
     ks = []
     for (m, n) in shapes:
         ax = O.resolve_axis(m, n, cfg_o.axis)
         ks.append(O.select_count(cfg_o.alpha, m if ax == O.AXIS_ROWS else n))
     for t in range(steps):
-        G = [gen_grad(m, n, seed, i, t, row_scaled=row_scaled) for i, (m, n) in enumerate(shapes)]
+        if structure:
+            G = [gen_grad_structured(m, n, seed, i, t, **structure) for i, (m, n) in enumerate(shapes)]
+        else:
+            G = [gen_grad(m, n, seed, i, t, row_scaled=row_scaled) for i, (m, n) in enumerate(shapes)]
         if grad_bf16:  # the oracle sees exactly the bf16 values the kernels read
             Gg = [torch.from_numpy(g).to(device).to(torch.bfloat16) for g in G]
             G = [g.float().cpu().numpy() for g in Gg]
