@@ -71,26 +71,43 @@ def ns_uses_gram_form(p, q, ns_form="auto"):
     return pad(q) >= 2 * pad(p) or q >= 2 * p
 
 
+def ns_segments(steps=5, a=3.4445, growth=64.0):
+    """Restart segment lengths of the Gram-space form (dion2_api.cu ns_segments, reading R24):
+    [3, 2] for the default quintic at T = 5."""
+    segs, cur, prod = [], 0, 1.0
+    for _ in range(steps):
+        if cur and prod * a > growth:
+            segs.append(cur)
+            cur, prod = 0, 1.0
+        cur += 1
+        prod *= a
+    segs.append(cur)
+    return segs
+
+
 def work_model(shapes, alpha, steps=5, mt=False, ns_form="auto"):
     """Algorithmic work per Dion2 step and per-phase algorithmic HBM bytes.
     NS FLOPs of the form the library evaluates (full products; symmetric tiles not credited):
       direct: T(4p^2 q + 2p^3)  -- gram 2p^2q, poly 2p^3, apply 2p^2q per iteration
-      Gram space (R23): 4p^2 q + (4T - 3) 2p^3 (T >= 2) -- gram + apply once, T polys,
-      3T - 3 products C.Q / C.A / C.(CA)."""
+      Gram space with restarts (R23, R24): per segment of Ts iterations a gram and an apply
+      (4p^2 q) and (4 Ts - 3) p x p products (Ts polys, 3 Ts - 3 products C.Q / C.A / C.(CA)):
+      8p^2 q + 28 p^3 at T = 5 (segments 3 + 2)."""
     ns_flops = {"ns_gram": 0.0, "ns_poly": 0.0, "ns_apply": 0.0, "ns_mul": 0.0}
     byts = {"momentum_score": 0.0, "momentum_score_mt": 0.0}
     for ph in ("gather", "gather_rows", "gather_cols", "scatter", "scatter_rows", "scatter_cols"):
         byts[ph] = 0.0
+    segs = ns_segments(steps)
     for (m, n) in shapes:
         rows = m <= n
         d, o = (m, n) if rows else (n, m)
         k = max(1, min(d, int(math.floor(alpha * d + 0.5))))
         p, q = min(k, o), max(k, o)
         if ns_uses_gram_form(p, q, ns_form):
-            ns_flops["ns_gram"] += 2.0 * p * p * q
-            ns_flops["ns_poly"] += steps * 2.0 * p ** 3
-            ns_flops["ns_mul"] += max(0, 3 * steps - 3) * 2.0 * p ** 3
-            ns_flops["ns_apply"] += 2.0 * p * p * q
+            for ts in segs:
+                ns_flops["ns_gram"] += 2.0 * p * p * q
+                ns_flops["ns_poly"] += ts * 2.0 * p ** 3
+                ns_flops["ns_mul"] += max(0, 3 * ts - 3) * 2.0 * p ** 3
+                ns_flops["ns_apply"] += 2.0 * p * p * q
         else:
             ns_flops["ns_gram"] += steps * 2.0 * p * p * q
             ns_flops["ns_poly"] += steps * 2.0 * p ** 3
@@ -105,8 +122,8 @@ def work_model(shapes, alpha, steps=5, mt=False, ns_form="auto"):
         else:
             sfx = ""
         gsfx = "_rows" if (mt and not rows) else sfx           # transposed M: row gather of M^T
-        byts["gather" + gsfx] += k * o * (4.0 + 4.0 + 2.0)    # read M[K], write mu*M[K], write bf16 X
-        byts["scatter" + sfx] += k * o * (2.0 + 4.0 + 4.0)    # read bf16 O, read+write W[K]
+        byts["gather" + gsfx] += k * o * (4.0 + 4.0 + 2.0)    # read M[K], write mu*M[K], write fp16 X
+        byts["scatter" + sfx] += k * o * (2.0 + 4.0 + 4.0)    # read fp16 O, read+write W[K]
     return ns_flops, byts
 
 
@@ -117,6 +134,7 @@ def mma_flops(shapes, alpha, steps=5, ns_form="auto"):
     product.  (work_model's counts are unpadded full products.)"""
     pad = lambda v: (v + 255) // 256 * 256  # noqa: E731
     tot = 0.0
+    segs = ns_segments(steps)
     for (m, n) in shapes:
         d, o = (m, n) if m <= n else (n, m)
         k = max(1, min(d, int(math.floor(alpha * d + 0.5))))
@@ -124,7 +142,8 @@ def mma_flops(shapes, alpha, steps=5, ns_form="auto"):
         T = p // 256
         sym = T * (T + 1) / 2 / (T * T)
         if ns_uses_gram_form(min(k, o), max(k, o), ns_form):
-            tot += sym * 2.0 * p * p * q + 2.0 * p * p * q + sym * (steps + max(0, 3 * steps - 3)) * 2.0 * p ** 3
+            for ts in segs:
+                tot += sym * 2.0 * p * p * q + 2.0 * p * p * q + sym * (ts + max(0, 3 * ts - 3)) * 2.0 * p ** 3
         else:
             tot += steps * (sym * 2.0 * p * p * q + sym * 2.0 * p ** 3 + 2.0 * p * p * q)
     return tot
@@ -512,6 +531,32 @@ def run_ours(args):
         cpu = cpu_oracle_baseline(shapes, args.alpha, budget_s=args.cpu_budget, per_layer=LAYER_MATS[args.config])
 
     if rank == 0:
+        ns_std_frac = ns_std_tflops / peaks["bf16_tflops"]
+        details = {
+            "configs1_sweep": sweep,
+            "ns_tflops_evaluated": ns_tflops,
+            "ns_evaluated_note": "the evaluated form's FLOPs (Gram space with restarts: per segment of Ts "
+                                 "iterations 4p^2q + (4Ts-3)2p^3, full products) over the NS kernels' time",
+            "ns_frac_bf16_sustained": ns_tflops / peaks["bf16_tflops_sustained"],
+            "ns_mma_tflops": ns_mma / (ns_ms * 1e-3) / 1e12 if ns_ms > 0 else 0.0,
+            "ns_mma_note": "FLOPs the tensor cores execute (padded dims, upper-triangle tiles of the symmetric "
+                           "products) over the NS kernels' time",
+            "ns_standard_tflop_per_step": ns_std / 1e12,
+            "ns_standard_equiv_tflops": ns_std_tflops,
+            "ns_standard_equiv_frac_bf16_burst": ns_std_frac,
+            "ns_ms_per_step": ns_ms,
+            "ms_per_step_eager": ms_eager,
+            "ms_per_step_with_phase_events": ms_timed,
+            "phases_note": "per-kernel times (CUDA events around every launch) from a separate K-step pass",
+            "phases": per_phase,
+        }
+        det_path = None
+        if not args.no_details:
+            det_dir = os.path.join(ROOT, "gpurun_out")
+            os.makedirs(det_dir, exist_ok=True)
+            det_path = os.path.join(det_dir, f"bench_details_{args.config}_n{world}.json")
+            with open(det_path, "w") as f:
+                json.dump(details, f, indent=1)
         out = {
             "metric": "Dion2 optimizer-step ms per model at alpha=0.25 vs alpha=1; NS tensor-peak fraction",
             "value": ms,
@@ -523,44 +568,31 @@ def run_ours(args):
             "higher_is_better": False,
             "scaling": "weak" if world == 1 else "strong",
             "vs_baseline": None,
-            "dtype": "f32 state / bf16 X, fp16 Gram-space NS (fp32 accumulate)",
+            "dtype": "f32 state; fp16 NS operands, f32 accumulate",
             "data": "synthetic (W0~N(0,1/n), G~N(0,1), M0=0; seeded device RNG)",
             "config": {"workload": f"{args.config}-set Dion2 step ({CONFIG_LABEL[args.config]})",
-                       "matrices": len(shapes),
-                       "params": n_params, "alpha": args.alpha, "axis": "auto", "ns_steps": 5, "ns_form": args.ns_form,
-                       "momentum_layout": "column-mode matrices transposed" if not args.no_mt else "as W",
+                       "matrices": len(shapes), "params": n_params, "alpha": args.alpha, "ns_steps": 5,
+                       "ns_form": args.ns_form,
                        "l2_flush": f"not needed: {12 * n_params / 1e9:.1f} GB touched per step >> 126 MB L2",
                        "parallelism": "single GPU" if not use_dist else
-                       f"owner-compute over {world} GPUs (NCCL; shards along the non-selection axis)"},
-            "alpha1_ms_per_step": ms_a1,
-            "configs1_sweep": sweep,
-            "speedup_vs_alpha1": (ms_a1 / ms) if ms_a1 else None,
-            "ns_tflops": ns_tflops,
-            "ns_tflops_note": "the evaluated form's FLOPs (Gram space: 4p^2q + (4T-3)2p^3 per matrix, full products) "
-                              "over the NS kernels' time",
-            "ns_frac_bf16_burst": ns_tflops / peaks["bf16_tflops"],
-            "ns_frac_bf16_sustained": ns_tflops / peaks["bf16_tflops_sustained"],
-            "ns_mma_tflops": ns_mma / (ns_ms * 1e-3) / 1e12 if ns_ms > 0 else 0.0,
-            "ns_mma_frac_bf16_burst": (ns_mma / (ns_ms * 1e-3) / 1e12 / peaks["bf16_tflops"]) if ns_ms > 0 else 0.0,
-            "ns_mma_note": "FLOPs the tensor cores execute (padded dims, upper-triangle tiles of the symmetric "
-                           "products) over the NS kernels' time",
-            "ns_standard_tflop_per_step": ns_std / 1e12,
-            "ns_standard_equiv_tflops": ns_std_tflops,
-            "ns_standard_equiv_frac_bf16_burst": ns_std_tflops / peaks["bf16_tflops"],
-            "ms_per_step_eager": ms_eager,
-            "step_mode": "CUDA graph replay of the C-ABI step (Dion2(cuda_graph=True))" if (not use_dist and not args.no_graph)
-                         else "eager",
-            "ms_per_step_unpipelined_with_phase_events": ms_timed,
-            "phases_note": "per-kernel times (CUDA events around every launch) from a separate K-step pass",
-            "phases": per_phase,
+                       f"owner-compute over {world} GPUs (NCCL; shards along the non-selection axis)",
+                       "step_mode": "CUDA graph" if (not use_dist and not args.no_graph) else "eager"},
             "roofline": roof,
             "cpu_baseline": cpu,
-            "e2e": {"value": e2e_ms, "unit": "ms/step", "h2d_bytes_per_step": h2d, "d2h_bytes_per_step": d2h,
-                    "what": "pinned host G -> device (Dion2.step_host: 8 chunks, upload overlapped with the earlier chunks' steps), dion2_step_batched per chunk, selected indices -> host, every step"},
+            "e2e": {"value": e2e_ms, "unit": "ms/step", "h2d_bytes_per_step": h2d, "d2h_bytes_per_step": d2h},
             "gpu_launches": launches,
-            "comm": comm,
             "clocks": clk.summary(),
         }
+        if comm:
+            out["comm"] = comm
+        if det_path:
+            out["details"] = os.path.relpath(det_path, ROOT)
+        # the gate numbers last (BASELINE metric: alpha = 0.25 vs alpha = 1, NS tensor-peak fraction)
+        out["alpha1_ms_per_step"] = ms_a1
+        out["speedup_vs_alpha1"] = (ms_a1 / ms) if ms_a1 else None
+        out["ns_frac_bf16_burst"] = ns_tflops / peaks["bf16_tflops"]
+        out["ns_frac_flops"] = "evaluated form (Gram space with restarts), full products"
+        out["ns_mma_frac_bf16_burst"] = (ns_mma / (ns_ms * 1e-3) / 1e12 / peaks["bf16_tflops"]) if ns_ms > 0 else 0.0
         print(json.dumps(out))
     if use_dist:
         dist.destroy_process_group()
@@ -608,6 +640,18 @@ def run_reference(args):
     print(json.dumps(out))
 
 
+def relaunch(n: int) -> int:
+    """`python bench.py --gpus N` without torchrun: re-run this command under
+    torch.distributed.run with N ranks on this node (rank 0 prints the line)."""
+    import socket
+    with socket.socket() as sk:
+        sk.bind(("127.0.0.1", 0))
+        port = sk.getsockname()[1]
+    cmd = [sys.executable, "-m", "torch.distributed.run", "--nnodes=1", f"--nproc-per-node={n}",
+           "--master-addr=127.0.0.1", f"--master-port={port}", os.path.abspath(__file__)] + sys.argv[1:]
+    return subprocess.call(cmd)
+
+
 def main():
     ap = argparse.ArgumentParser()
     ap.add_argument("--gpus", type=int, default=1)
@@ -627,7 +671,10 @@ def main():
     ap.add_argument("--no-mt", action="store_true", help="keep column-mode momentum in W's layout")
     ap.add_argument("--ns-form", choices=["auto", "direct", "gram"], default="auto",
                     help="Newton-Schulz evaluation form (DESIGN.md reading R23)")
+    ap.add_argument("--no-details", action="store_true", help="do not write gpurun_out/bench_details_*.json")
     args = ap.parse_args()
+    if args.gpus > 1 and "WORLD_SIZE" not in os.environ:
+        sys.exit(relaunch(args.gpus))
     if args.impl == "reference":
         run_reference(args)
     else:

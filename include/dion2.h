@@ -50,7 +50,7 @@
 extern "C" {
 #endif
 
-#define DION2_ABI_VERSION 5
+#define DION2_ABI_VERSION 6
 #define DION2_MAX_NS_STEPS 16
 /* dion2_config.reserved0 flag: the sparse update reads eta on the device from the fp32 word at
    byte offset 8 of the workspace's 4096-byte-aligned base (the first multiple of 4096 at or
@@ -152,11 +152,19 @@ int dion2_step(const dion2_matrix* mat, const dion2_config* cfg, void* workspace
 int dion2_step_batched(const dion2_matrix* mats, int32_t n, const dion2_config* cfg,
                        void* workspace, size_t ws_bytes, void* stream);
 
-/* Synchronises the device, then reads the workspace's status word.
- * Returns DION2_OK or DION2_ENONFINITE (and the index of the first matrix
- * whose scores were non-finite in *first_bad_matrix, -1 if none).  The status
- * word is cleared at the start of every step. */
-int dion2_get_status(const void* workspace, int32_t* first_bad_matrix);
+/* Reads the workspace's status word after the work already enqueued on `stream` (the stream
+ * the step ran on) has finished: an asynchronous copy on `stream`, then a synchronisation of
+ * that stream only (other streams keep running).  Returns DION2_OK or DION2_ENONFINITE (and the
+ * index of the first matrix whose scores were non-finite in *first_bad_matrix, -1 if none),
+ * DION2_ECUDA on a CUDA error.  The status word is cleared at the start of every step. */
+int dion2_get_status(const void* workspace, void* stream, int32_t* first_bad_matrix);
+
+/* Drops every cached plan (and frees its device tables) whose workspace base lies in
+ * [workspace, workspace + bytes): call it before freeing or reusing a workspace allocation.
+ * Plans are otherwise kept for the life of the process, one per (shapes, config, workspace
+ * address).  Synchronises the device (the tables may be in use).  Returns the number of plans
+ * dropped. */
+int32_t dion2_release_workspace(const void* workspace, size_t bytes);
 
 /* Human-readable name of a status code (static storage). */
 const char* dion2_strerror(int code);

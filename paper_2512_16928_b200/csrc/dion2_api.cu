@@ -29,6 +29,18 @@ const char* kPhaseNames[kNumPhases] = {"momentum_score", "select",       "gather
 
 std::mutex g_mu;
 int g_sm_count = 0;
+
+int sm_count() {
+  if (g_sm_count <= 0) {
+    int dev = 0, v = 0;
+    if (cudaGetDevice(&dev) == cudaSuccess &&
+        cudaDeviceGetAttribute(&v, cudaDevAttrMultiProcessorCount, dev) == cudaSuccess && v > 0)
+      g_sm_count = v;
+    else
+      cudaGetLastError();  // no device visible (host-only size query): assume B200's 148
+  }
+  return g_sm_count > 0 ? g_sm_count : 148;
+}
 bool g_attr_done = false;
 int32_t g_last_launches = 0;
 
@@ -314,7 +326,7 @@ int build_layout(Plan& P, const dion2_matrix* mats, int n, const dion2_config* c
       tt += (int64_t)g.count * T * (T + 1) / 2;
       min_kb = std::min(min_kb, g.q_pad / 64);
     }
-    const int pairs = (g_sm_count > 0 ? g_sm_count : 148) / 2;
+    const int pairs = sm_count() / 2;  // the same value the size query and the step see
     if (tt > 0 && 2 * tt <= pairs) {
       int S = (int)std::min<int64_t>((pairs + tt - 1) / tt, min_kb / 4);
       if (se && atoi(se) > 1) S = std::min(atoi(se), min_kb);
@@ -1104,14 +1116,33 @@ int dion2_step(const dion2_matrix* mat, const dion2_config* cfg, void* workspace
   return dion2_step_batched(mat, 1, cfg, workspace, ws_bytes, stream);
 }
 
-int dion2_get_status(const void* workspace, int32_t* first_bad_matrix) {
+int dion2_get_status(const void* workspace, void* stream, int32_t* first_bad_matrix) {
   if (!workspace) return DION2_EWORKSPACE;
-  if (cudaDeviceSynchronize() != cudaSuccess) return DION2_ECUDA;
   const void* ws = reinterpret_cast<const void*>(align_up(reinterpret_cast<uintptr_t>(workspace), 4096));
   int32_t st[2] = {0, 0};
-  if (cudaMemcpy(st, ws, 8, cudaMemcpyDeviceToHost) != cudaSuccess) return DION2_ECUDA;
+  cudaStream_t s = reinterpret_cast<cudaStream_t>(stream);
+  // pageable destination: the copy is stream-ordered and returns once it has completed
+  if (cudaMemcpyAsync(st, ws, 8, cudaMemcpyDeviceToHost, s) != cudaSuccess) return DION2_ECUDA;
+  if (cudaStreamSynchronize(s) != cudaSuccess) return DION2_ECUDA;
   if (first_bad_matrix) *first_bad_matrix = st[0] ? st[1] : -1;
   return st[0] ? DION2_ENONFINITE : DION2_OK;
+}
+
+int32_t dion2_release_workspace(const void* workspace, size_t bytes) {
+  std::lock_guard<std::mutex> lock(g_mu);
+  const uintptr_t lo = reinterpret_cast<uintptr_t>(workspace), hi = lo + bytes;
+  cudaDeviceSynchronize();
+  int dropped = 0;
+  for (auto it = g_plans.begin(); it != g_plans.end();) {
+    const uintptr_t w = reinterpret_cast<uintptr_t>(it->second->ws);
+    if (w >= lo && w < hi) {
+      it = g_plans.erase(it);
+      ++dropped;
+    } else {
+      ++it;
+    }
+  }
+  return dropped + release_dist_plans(lo, hi);
 }
 
 const char* dion2_strerror(int code) {

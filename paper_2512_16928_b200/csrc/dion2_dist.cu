@@ -74,6 +74,13 @@ struct DistMat {
 };
 
 struct DistPlan {
+  DistPlan() = default;
+  DistPlan(const DistPlan&) = delete;
+  DistPlan& operator=(const DistPlan&) = delete;
+  ~DistPlan() {
+    if (dtab) cudaFree(dtab);
+  }
+  void* ws = nullptr;  // aligned workspace base of the plan (dion2_release_workspace)
   int n = 0, world = 1, rank = 0;
   std::vector<DistMat> dm;
   int64_t total_d = 0;
@@ -530,6 +537,7 @@ int get_plan(DistPlan** out, const dion2_shard* sh, int n, const dion2_config* c
     if (D->total - 4096 + slack > ws_bytes) return DION2_EWORKSPACE;
     rc = build_tables(*D, c, ws);
     if (rc) return rc;
+    D->ws = ws;
     it = g_dist_plans.emplace(key, std::move(D)).first;
   }
   DistPlan& D = *it->second;
@@ -833,6 +841,12 @@ int run_dist(std::vector<DistPlan*>& plans, std::vector<void*>& wss, const std::
 // selection needs no global state, so only the selected fp32 rows M[K] are all-reduced
 // (averaged); every replica then runs the rest of the step on identical rows.
 struct DpPlan {
+  DpPlan() = default;
+  DpPlan(const DpPlan&) = delete;
+  DpPlan& operator=(const DpPlan&) = delete;
+  ~DpPlan() {
+    if (dtab) cudaFree(dtab);
+  }
   Plan P;
   int world = 1;
   size_t off_buf = 0, off_gather = 0, total = 0;
@@ -962,6 +976,20 @@ void dp_phase2(DpPlan& D, const dion2_matrix* mats, const dion2_config* c, void*
 }
 
 }  // namespace
+
+int release_dist_plans(uintptr_t lo, uintptr_t hi) {
+  int dropped = 0;
+  for (auto it = g_dist_plans.begin(); it != g_dist_plans.end();) {
+    const uintptr_t w = reinterpret_cast<uintptr_t>(it->second->ws);
+    if (w >= lo && w < hi) { it = g_dist_plans.erase(it); ++dropped; } else { ++it; }
+  }
+  for (auto it = g_dp_plans.begin(); it != g_dp_plans.end();) {
+    const uintptr_t w = reinterpret_cast<uintptr_t>(it->second->P.ws);
+    if (w >= lo && w < hi) { it = g_dp_plans.erase(it); ++dropped; } else { ++it; }
+  }
+  return dropped;
+}
+
 }  // namespace dion2rt
 
 using namespace dion2rt;

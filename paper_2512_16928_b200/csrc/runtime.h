@@ -23,6 +23,11 @@ enum Phase {
 };
 
 extern std::mutex g_mu;
+extern std::map<std::string, std::unique_ptr<struct Plan>> g_plans;
+// number of SMs of the current device (queried once; 148 if no device is visible)
+int sm_count();
+// drop the cached distributed / DP-sync plans whose workspace lies in [lo, hi) (dion2_dist.cu)
+int release_dist_plans(uintptr_t lo, uintptr_t hi);
 extern int g_sm_count;
 extern bool g_attr_done;
 extern int32_t g_last_launches;
@@ -74,6 +79,12 @@ struct Launch {
 };
 
 struct Plan {
+  Plan() = default;
+  Plan(const Plan&) = delete;
+  Plan& operator=(const Plan&) = delete;
+  ~Plan() {
+    if (dtab) cudaFree(dtab);
+  }
   int n;
   bool bf16_ns;
   int ns_steps;

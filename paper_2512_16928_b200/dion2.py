@@ -22,14 +22,14 @@ AXIS = {"rows": 0, "cols": 1, "auto": 2}
 PRECISION = {"bf16": 0, "fp32": 1}
 SELECT = {"l1": 0, "random": 1}
 NS_FORM = {"auto": 0, "direct": 1, "gram": 2}
-ABI_VERSION = 5  # include/dion2.h DION2_ABI_VERSION
+ABI_VERSION = 6  # include/dion2.h DION2_ABI_VERSION
 STATUS = {0: "OK", 1: "EINVAL_CONFIG", 2: "EINVAL_SHAPE", 3: "EWORKSPACE", 4: "EUNSUPPORTED",
           5: "ECUDA", 6: "ENCCL", 7: "ENONFINITE"}
 EXPORTED = ["dion2_config_init", "dion2_workspace_size", "dion2_step", "dion2_step_batched", "dion2_get_status",
             "dion2_strerror", "dion2_set_phase_timing", "dion2_get_phase_times", "dion2_phase_name",
             "dion2_last_launch_count", "dion2_abi_version", "dion2_dist_info", "dion2_step_batched_dist",
             "dion2_step_batched_loopback", "dion2_dpsync_workspace_size", "dion2_step_batched_dpsync",
-            "dion2_step_batched_dpsync_loopback"]
+            "dion2_step_batched_dpsync_loopback", "dion2_release_workspace"]
 
 
 class Dion2Matrix(ctypes.Structure):
@@ -75,7 +75,9 @@ def _lib():
         lib.dion2_step.argtypes = [P(Dion2Matrix), P(Dion2Config), ctypes.c_void_p, ctypes.c_size_t, ctypes.c_void_p]
         lib.dion2_step_batched.argtypes = [P(Dion2Matrix), ctypes.c_int32, P(Dion2Config), ctypes.c_void_p,
                                            ctypes.c_size_t, ctypes.c_void_p]
-        lib.dion2_get_status.argtypes = [ctypes.c_void_p, P(ctypes.c_int32)]
+        lib.dion2_get_status.argtypes = [ctypes.c_void_p, ctypes.c_void_p, P(ctypes.c_int32)]
+        lib.dion2_release_workspace.argtypes = [ctypes.c_void_p, ctypes.c_size_t]
+        lib.dion2_release_workspace.restype = ctypes.c_int32
         lib.dion2_strerror.argtypes = [ctypes.c_int]
         lib.dion2_strerror.restype = ctypes.c_char_p
         lib.dion2_set_phase_timing.argtypes = [ctypes.c_int32]
@@ -231,12 +233,27 @@ class Dion2:
             need.value += (self.GRAPH_SLOTS + 1) * self.SLOT_BYTES  # + the slot of uncaptured steps
         if self._ws is None or self._ws.numel() < need.value or self._ws.device != device:
             self._graphs.clear()  # captured graphs reference the old workspace
+            self._release()
             self._ws = torch.empty(need.value, dtype=torch.uint8, device=device)
         return self._ws
+
+    def _release(self) -> None:
+        """Drop the library's plans (and their device tables) keyed on this object's workspace."""
+        if self._ws is not None:
+            _lib().dion2_release_workspace(self._ws.data_ptr(), self._ws.numel())
+            self._ws = None
+
+    def __del__(self):
+        try:
+            self._graphs.clear()
+            self._release()
+        except Exception:  # interpreter shutdown: the library may already be gone
+            pass
 
     def step(self, Ws, Ms, Gs, sel_out=None, O_out=None, stream: Optional[torch.cuda.Stream] = None,
              m_transposed=None, storage_transposed=None, **override):
         self._last_sub = None
+        self._last_stream = None
         if self.cuda_graph and stream is None:
             ptrs = lambda ts: tuple((t.data_ptr(), tuple(t.shape), tuple(t.stride()), t.dtype) if t is not None  # noqa: E731
                                     else None for t in ts)
@@ -278,7 +295,11 @@ class Dion2:
             if self._ws is ws_before:  # a reallocated workspace invalidated every graph (cleared)
                 self._graphs[key] = (g, slot)
             return
-        self._step(Ws, Ms, Gs, sel_out, O_out, stream, m_transposed, storage_transposed, 0, **override)
+        # an explicit stream in graph mode runs eagerly in the uncaptured slot: slot 0 may belong to
+        # a captured graph, whose plan's descriptor table must keep that graph's pointers
+        self._step(Ws, Ms, Gs, sel_out, O_out, stream, m_transposed, storage_transposed,
+                   self.GRAPH_SLOTS if self.cuda_graph else 0, **override)
+        self._last_stream = stream
 
     def _write_lr(self, slot: int, lr: float) -> None:
         """eta into the fp32 word at byte 8 of the slot's 4096-aligned workspace base (stream-ordered)."""
@@ -372,7 +393,8 @@ class Dion2:
             return worst, bad
         bad = ctypes.c_int32(-1)
         ws = self._ws.data_ptr() + getattr(self, "_last_slot", 0) * self.SLOT_BYTES if self._ws is not None else None
-        rc = _lib().dion2_get_status(ws, ctypes.byref(bad))
+        st = getattr(self, "_last_stream", None) or torch.cuda.current_stream()
+        rc = _lib().dion2_get_status(ws, st.cuda_stream, ctypes.byref(bad))
         return rc, bad.value
 
 
@@ -506,7 +528,7 @@ class Dion2Dist:
 
     def status(self):
         bad = ctypes.c_int32(-1)
-        rc = _lib().dion2_get_status(self._ws.data_ptr(), ctypes.byref(bad))
+        rc = _lib().dion2_get_status(self._ws.data_ptr(), torch.cuda.current_stream().cuda_stream, ctypes.byref(bad))
         return rc, bad.value
 
 

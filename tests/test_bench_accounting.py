@@ -2,7 +2,8 @@
 reported roofline fractions, pinned to SURVEY.md section 8(d)'s table and to closed forms.
 
 The per-unit figures: NS FLOPs T(4p^2 q + 2p^3) per matrix in the
-direct form, 4p^2 q + (4T - 3) 2p^3 in the Gram-space form (reading R23); HBM bytes
+direct form; in the Gram-space form with restarts (readings R23, R24) 4p^2 q + (4 Ts - 3) 2p^3 per
+segment of Ts iterations (segments 3 + 2 at T = 5: 8p^2 q + 28 p^3); HBM bytes
 m n (b_G + 8) for momentum + score and 10 k o each for the gather and the scatter.
 """
 import os
@@ -31,13 +32,20 @@ def test_direct_ns_flops_match_survey_table(alpha, tflop):
     assert abs(sum(f.values()) / 1e12 - tflop) < 0.01
 
 
+def test_restart_segments():
+    assert bench.ns_segments(5) == [3, 2]
+    assert bench.ns_segments(1) == [1]
+    assert bench.ns_segments(7) == [3, 3, 1]
+
+
 def test_gram_form_flops_closed_form():
-    """Gram space at alpha = 0.25: every matrix has p = 512 and q = 2048 or 8192 (q >= 2p)."""
+    """Gram space at alpha = 0.25: every matrix has p = 512 and q = 2048 or 8192 (q >= 2p);
+    two restart segments (3 + 2 iterations)."""
     f, _ = bench.work_model(layer_set_1b(24), 0.25, ns_form="auto")
-    p, T = 512, 5
-    want = sum(4 * p * p * q + (4 * T - 3) * 2 * p ** 3 for q in [2048] * 96 + [8192] * 48)
+    p = 512
+    want = sum(8 * p * p * q + ((4 * 3 - 3) + (4 * 2 - 3)) * 2 * p ** 3 for q in [2048] * 96 + [8192] * 48)
     assert abs(sum(f.values()) - want) < 1e3
-    assert abs(sum(f.values()) / 1e12 - 1.28) < 0.005  # DESIGN 6: 1.28 TFLOP in Gram form (2.6x fewer)
+    assert abs(sum(f.values()) / 1e12 - 1.78) < 0.005  # DESIGN 6: 1.78 TFLOP with the restart (1.85x fewer)
     # alpha = 1: the square matrices have q = p (direct form), the 2048 x 8192 ones q = 4p (Gram)
     sq = [(2048, 2048)] * 96
     f1, _ = bench.work_model(sq, 1.0, ns_form="auto")
@@ -45,7 +53,7 @@ def test_gram_form_flops_closed_form():
     assert sum(f1.values()) == sum(fd.values())
     rect = [(8192, 2048), (2048, 8192)]
     fa, _ = bench.work_model(rect, 1.0, ns_form="auto")
-    assert sum(fa.values()) == 2 * (4 * 2048 ** 2 * 8192 + 17 * 2 * 2048 ** 3)
+    assert sum(fa.values()) == 2 * (8 * 2048 ** 2 * 8192 + 14 * 2 * 2048 ** 3)
 
 
 @pytest.mark.parametrize("alpha,gb", [(1.0, 33.8), (0.5, 24.2), (0.25, 19.3), (0.125, 16.9)])
@@ -93,7 +101,7 @@ def test_mma_flops_credit_only_the_computed_tiles():
     """Tensor-core work: p = 512 -> 2 x 2 tiles of 256, 3 upper tiles computed for the symmetric
     products (gram, poly, p x p products); the apply is a full product."""
     f = bench.mma_flops([(2048, 2048)], 0.25)           # X 512 x 2048, Gram form
-    p, q, T = 512, 2048, 5
-    want = 0.75 * 2 * p * p * q + 2 * p * p * q + 0.75 * (T + 3 * T - 3) * 2 * p ** 3
+    p, q = 512, 2048
+    want = sum(0.75 * 2 * p * p * q + 2 * p * p * q + 0.75 * (ts + 3 * ts - 3) * 2 * p ** 3 for ts in (3, 2))
     assert f == want
-    assert abs(bench.mma_flops(layer_set_1b(24), 0.25) / 1e12 - 1.034) < 0.001
+    assert abs(bench.mma_flops(layer_set_1b(24), 0.25) / 1e12 - 1.488) < 0.001

@@ -485,3 +485,82 @@ def test_phase_timing_and_launch_count():
     assert last_launch_count() >= 5 + len(pre)
     for ph in pre + ("ns_gram", "ns_poly", "ns_apply", "scatter_rows"):
         assert times[ph][1] >= 1 and times[ph][0] > 0
+
+
+def test_stream_calls_do_not_disturb_captured_graphs():
+    """in graph mode a call with an explicit stream runs eagerly in the uncaptured
+    workspace slot, so it cannot overwrite the descriptor table of a captured graph's plan
+    (same shapes, other tensors).  Replays after such calls must still update their own W/M:
+    bitwise equal to the eager optimizer on the same call sequence."""
+    shapes = [(512, 1024), (1024, 512)]
+    data = [[torch.from_numpy(gen_grad(m, n, 9, i, t, row_scaled=True)).cuda() for i, (m, n) in enumerate(shapes)]
+            for t in range(4)]
+    outs = []
+    for graph in (False, True):
+        opt = Dion2(alpha=0.25, cuda_graph=graph)
+        Wa = [torch.from_numpy(gen_w0(m, n, 1, i)).cuda() for i, (m, n) in enumerate(shapes)]
+        Ma = [torch.zeros_like(w) for w in Wa]
+        Wb = [torch.from_numpy(gen_w0(m, n, 2, i)).cuda() for i, (m, n) in enumerate(shapes)]
+        Mb = [torch.zeros_like(w) for w in Wb]
+        side = torch.cuda.Stream()
+        for t in range(4):
+            opt.step(Wa, Ma, data[0])                      # t >= 1: captured in slot 0, then replayed
+            side.wait_stream(torch.cuda.current_stream())
+            opt.step(Wb, Mb, data[t], stream=side)         # same shapes, other tensors, explicit stream
+            torch.cuda.current_stream().wait_stream(side)
+        torch.cuda.synchronize()
+        outs.append([x.clone() for x in Wa + Ma + Wb + Mb])
+    for a, b in zip(*outs):
+        assert torch.equal(a, b)
+
+
+def test_dion2_step_entry_point():
+    """dion2_step (one matrix) through the C ABI: bitwise equal to dion2_step_batched with n = 1."""
+    import ctypes
+    from paper_2512_16928_b200 import dion2 as D
+    m, n = 384, 1024
+    outs = []
+    for single in (True, False):
+        W = torch.from_numpy(gen_w0(m, n, 3)).cuda()
+        M = torch.zeros_like(W)
+        G = torch.from_numpy(gen_grad(m, n, 3)).cuda()
+        arr, _ = D.describe([W], [M], [G])
+        cfg = D.make_config(alpha=0.25)
+        need = ctypes.c_size_t(0)
+        assert D._lib().dion2_workspace_size(arr, 1, ctypes.byref(cfg), ctypes.byref(need)) == 0
+        ws = torch.zeros(need.value, dtype=torch.uint8, device="cuda")
+        st = torch.cuda.current_stream().cuda_stream
+        for _ in range(2):
+            if single:
+                rc = D._lib().dion2_step(arr, ctypes.byref(cfg), ws.data_ptr(), ws.numel(), st)
+            else:
+                rc = D._lib().dion2_step_batched(arr, 1, ctypes.byref(cfg), ws.data_ptr(), ws.numel(), st)
+            assert rc == 0
+        bad = ctypes.c_int32(5)
+        assert D._lib().dion2_get_status(ws.data_ptr(), st, ctypes.byref(bad)) == 0 and bad.value == -1
+        assert D._lib().dion2_release_workspace(ws.data_ptr(), ws.numel()) >= 1
+        outs.append((W.clone(), M.clone()))
+    assert torch.equal(outs[0][0], outs[1][0]) and torch.equal(outs[0][1], outs[1][1])
+
+
+@pytest.mark.parametrize("precision,tol", [("bf16", BF16_TOL), ("fp32", FP32_TOL)])
+def test_submatrix_scale_mode(precision, tol):
+    """f3: scale_mode = 1 scales the update by sqrt of the SUBMATRIX dimensions
+    instead of the full W's sqrt(fan-out / fan-in); rows and column mode, both NS forms."""
+    _assert(run_parity([(512, 1024), (1024, 512), (300, 520)], 0.25, "auto", precision, steps=3, scale_mode=1), tol)
+
+
+def test_status_is_stream_scoped():
+    """dion2_get_status synchronises the step's stream only: a long kernel on another stream
+    is still running when it returns."""
+    Ws = [torch.from_numpy(gen_w0(256, 512)).cuda()]
+    Ms = [torch.zeros_like(Ws[0])]
+    Gs = [torch.from_numpy(gen_grad(256, 512)).cuda()]
+    opt = Dion2(alpha=0.25)
+    other = torch.cuda.Stream()
+    with torch.cuda.stream(other):
+        torch.cuda._sleep(2_000_000_000)  # ~1 s of spinning on the other stream
+    opt.step(Ws, Ms, Gs)
+    assert opt.status() == (0, -1)
+    assert not other.query()  # the other stream's kernel has not finished
+    other.synchronize()
