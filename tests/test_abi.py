@@ -37,7 +37,7 @@ def test_exports_every_declared_symbol(lib):
 
 
 def test_abi_version(lib):
-    assert lib.dion2_abi_version() == 5
+    assert lib.dion2_abi_version() == 6
 
 
 def test_config_defaults(lib):
