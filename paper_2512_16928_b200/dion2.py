@@ -515,6 +515,8 @@ class Dion2Dist:
         dev = Ws[0].device
         need = self.info["workspace_bytes"]
         if self._ws is None or self._ws.numel() < need:
+            if self._ws is not None:
+                _lib().dion2_release_workspace(self._ws.data_ptr(), self._ws.numel())
             self._ws = torch.empty(need, dtype=torch.uint8, device=dev)
         arr = _shards(self.shapes, Ws, Ms, Gs, sel_out, self.m_transposed)
         st = stream if stream is not None else torch.cuda.current_stream(dev)
@@ -556,6 +558,8 @@ class Dion2Loopback:
         dev = Ws[0][0].device
         need = max(i["workspace_bytes"] for i in self.infos)
         if len(self._ws) != P or self._ws[0].numel() < need:
+            for w in self._ws:
+                _lib().dion2_release_workspace(w.data_ptr(), w.numel())
             self._ws = [torch.empty(need, dtype=torch.uint8, device=dev) for _ in range(P)]
         arr = (Dion2Shard * (n * P))()
         for r in range(P):
@@ -626,6 +630,8 @@ class Dion2DpSync:
             raise Dion2Error(rc, "dion2_dpsync_workspace_size")
         nws = P if self.loopback else 1
         if len(self._ws) != nws or self._ws[0].numel() < need.value:
+            for w in self._ws:
+                _lib().dion2_release_workspace(w.data_ptr(), w.numel())
             self._ws = [torch.empty(need.value, dtype=torch.uint8, device=dev) for _ in range(nws)]
         st = stream if stream is not None else torch.cuda.current_stream(dev)
         nbytes = ctypes.c_uint64(0)
@@ -640,3 +646,11 @@ class Dion2DpSync:
         if rc:
             raise Dion2Error(rc, "dion2_step_batched_dpsync")
         self.last_comm_bytes = nbytes.value
+
+    def status(self, replica: int = 0) -> Tuple[int, int]:
+        """(code, first bad matrix) of this rank's replica (loopback: of replica `replica`); a
+        matrix non-finite on any replica is reported (and skipped) on every replica."""
+        bad = ctypes.c_int32(-1)
+        rc = _lib().dion2_get_status(self._ws[replica].data_ptr(), torch.cuda.current_stream().cuda_stream,
+                                     ctypes.byref(bad))
+        return rc, bad.value

@@ -36,7 +36,9 @@ def _run(world, precision, tol, steps=3, mode="loopback", m_transposed=False):
         if mode == "loopback":
             opt.step(Wg, Mg, [[torch.from_numpy(g).cuda() for g in G[r]] for r in range(world)], step=t)
         else:
-            opt.step(Wg[0], Mg[0], [torch.from_numpy(g).cuda() for g in G[0]], step=t)
+            import torch.distributed as dist
+            me = dist.get_rank()  # this process is replica `me`: its own local gradient
+            opt.step(Wg[0], Mg[0], [torch.from_numpy(g).cuda() for g in G[me]], step=t)
         cfg = O.OracleConfig(alpha=float(np.float32(alpha)), select="random", seed=seed, step=t)
         for i in range(len(SHAPES)):
             O.dion2_step_dpsync([Wr[r][i] for r in range(world)], [Mr[r][i] for r in range(world)],
@@ -49,8 +51,9 @@ def _run(world, precision, tol, steps=3, mode="loopback", m_transposed=False):
             wg = Wg[r][i].cpu().double().numpy()
             err = np.linalg.norm((wg - w0) - (Wr[r][i] - w0)) / np.linalg.norm(Wr[r][i] - w0)
             assert err <= tol, (i, r, err)
+            rr = r if mode == "loopback" else __import__("torch.distributed").distributed.get_rank()
             mg = (Mg[r][i].T if mts[i] else Mg[r][i]).cpu().double().numpy()
-            assert np.abs(mg - Mr[r][i]).max() <= 1e-5 * np.abs(Mr[r][i]).max()
+            assert np.abs(mg - Mr[rr][i]).max() <= 1e-5 * np.abs(Mr[rr][i]).max()
     return opt
 
 
@@ -88,3 +91,26 @@ def test_dpsync_requires_random_selection():
     opt = D.Dion2DpSync(loopback_world=2, select="l1")
     with pytest.raises(Dion2Error):
         opt.step(mk(), mk(), mk())
+
+
+def test_dpsync_nonfinite_on_one_replica_skips_the_matrix_everywhere():
+    """a non-finite gradient on ONE replica must not poison the others.  The replicas
+    combine their non-finite flags with the all-reduce, so every replica skips that matrix (W
+    unchanged, its selected momentum not overwritten with NaN rows) and reports it, and the
+    replicas' W stay bit-identical."""
+    world = 2
+    W0 = [gen_w0(m, n, 0, i) for i, (m, n) in enumerate(SHAPES)]
+    Wg = [[torch.from_numpy(w).cuda() for w in W0] for _ in range(world)]
+    Mg = [[torch.zeros(m, n, device="cuda") for (m, n) in SHAPES] for _ in range(world)]
+    G = [[torch.from_numpy(gen_grad(m, n, 100 + r, i, 0)).cuda() for i, (m, n) in enumerate(SHAPES)]
+         for r in range(world)]
+    G[1][2][3, 5] = float("nan")  # replica 1, matrix 2
+    opt = D.Dion2DpSync(loopback_world=world, alpha=0.25, seed=3)
+    opt.step(Wg, Mg, G, step=0)
+    torch.cuda.synchronize()
+    for r in range(world):
+        assert opt.status(r) == (7, 2), (r, opt.status(r))
+        assert torch.equal(Wg[r][2], Wg[0][2]) and torch.equal(Wg[r][2].cpu(), torch.from_numpy(W0[2]))
+        assert torch.isfinite(Mg[0][2]).all()
+        for i in (0, 1, 3):
+            assert torch.equal(Wg[r][i], Wg[0][i]) and not torch.equal(Wg[r][i].cpu(), torch.from_numpy(W0[i]))
