@@ -400,13 +400,16 @@ static int append_gram_space_launches(Plan& P, const dion2_config* c, void* ws, 
   auto emit = [&](int phase, const std::vector<Entry>& es, float cacc, float cC, float diag, int scale_sel,
                   int in_f16, int out_f16, bool mirror_out = false) -> int {
     const bool apply = phase == PH_APPLY;
-    const bool pair = !apply || pair_mode == 2;
-    const int MT = pair ? 256 : 128, BN = 256;
     for (size_t s0 = 0; s0 < es.size(); s0 += kMaxGroups) {
+      const size_t s1 = std::min(es.size(), s0 + kMaxGroups);
+      bool res_ok = apply && pair_mode == 1;
+      for (size_t e = s0; e < s1; ++e) res_ok = res_ok && P.groups[es[e].gi].p_pad <= 64 * kMaxResidentKB;
+      const bool pair = !apply || pair_mode == 2 || res_ok;
+      const int MT = pair ? 256 : 128, BN = 256;
       Launch L{};
       L.phase = phase;
       L.bn = BN;
-      L.kind = pair ? 3 : 1;
+      L.kind = res_ok ? 5 : (pair ? 3 : 1);
       NsParams& np = L.tc.p;
       np.ngroups = (int)std::min<size_t>(kMaxGroups, es.size() - s0);
       np.ns_scale_all = scale_all;
@@ -455,6 +458,8 @@ static int append_gram_space_launches(Plan& P, const dion2_config* c, void* ws, 
         tiles += G.count * (np.sym ? G.m_tiles * (G.m_tiles + 1) / 2 : G.m_tiles * G.n_tiles);
       }
       np.total_tiles = tiles;
+      np.b_is_a = np.b_kmajor ? 1 : 0;
+      for (int j = 0; j < np.ngroups; ++j) np.b_is_a &= np.g[j].a == np.g[j].b ? 1 : 0;
       P.ns_launches.push_back(L);
     }
     return DION2_OK;
@@ -655,12 +660,22 @@ int build_device_plan(Plan& P, const dion2_matrix* mats, const dion2_config* c, 
   // bf16 path: 2-SM (cta_group::2) 256 x 256 tiles; DION2_NS_1SM=1 selects the 1-SM 128 x 256 kernel
   // (measured: the pair kernel wins on the long-K gram, the 1-SM kernel on the
   // short-K poly and the MN-major apply; DION2_NS_PAIR=all|none overrides)
+  // DION2_NS_PAIR (A/B only): unset = pair kernel for gram / poly / products and the resident-A
+  // pair apply; "all" = the streaming pair kernel for the apply too; "1sm_apply" = the 1-SM
+  // apply (round 1's default); "none" = the 1-SM kernel everywhere
   const char* pair_env = getenv("DION2_NS_PAIR");
-  const int pair_mode = !pair_env ? 1 : (strcmp(pair_env, "all") == 0 ? 2 : (strcmp(pair_env, "none") == 0 ? 0 : 1));
+  const int pair_mode = !pair_env ? 1
+                                  : (strcmp(pair_env, "all") == 0 ? 2
+                                                                  : (strcmp(pair_env, "none") == 0 ? 0
+                                                                                                   : (strcmp(pair_env, "1sm_apply") == 0 ? 3 : 1)));
   for (int t = 0; t < P.ns_steps; ++t) {
     const float a = c->ns_coeffs[t][0], b = c->ns_coeffs[t][1], cc = c->ns_coeffs[t][2];
     for (int ph = PH_GRAM; ph <= PH_APPLY; ++ph) {
-      const bool pair = P.bf16_ns && (pair_mode == 2 || (pair_mode == 1 && ph != PH_APPLY));
+      // apply: the 2-SM kernel with A resident for p_pad <= 512 (k_ns_apply_pair.cu)
+      bool res_all = P.bf16_ns && ph == PH_APPLY && pair_mode == 1;  // (3: the 1-SM apply)
+      for (const Group& g : P.groups)
+        if (!g.gs) res_all = res_all && g.p_pad <= 64 * kMaxResidentKB;
+      const bool pair = P.bf16_ns && (pair_mode == 2 || ((pair_mode == 1 || pair_mode == 3) && (ph != PH_APPLY || res_all)));
       // gram and poly outputs are symmetric: the pair kernel computes upper-triangle tiles
       // only and mirrors them (DION2_NS_SYM=0 disables)
       const bool sym = pair && ph != PH_APPLY && !(getenv("DION2_NS_SYM") && atoi(getenv("DION2_NS_SYM")) == 0);
@@ -680,7 +695,7 @@ int build_device_plan(Plan& P, const dion2_matrix* mats, const dion2_config* c, 
           Launch L{};
           L.phase = ph;
           L.bn = BN;
-          L.kind = P.bf16_ns ? (pair ? 3 : cls) : 2;
+          L.kind = P.bf16_ns ? (res_all ? 5 : (pair ? 3 : cls)) : 2;
           NsParams& np = L.tc.p;
           np.ngroups = (int)std::min<size_t>(kMaxGroups, gl.size() - s0);
           np.ns_scale_all = scale_all;
@@ -748,6 +763,8 @@ int build_device_plan(Plan& P, const dion2_matrix* mats, const dion2_config* c, 
             tiles += G.count * (sym ? G.m_tiles * (G.m_tiles + 1) / 2 : G.m_tiles * G.n_tiles);
           }
           np.total_tiles = tiles;
+          np.b_is_a = np.b_kmajor ? 1 : 0;
+          for (int j = 0; j < np.ngroups; ++j) np.b_is_a &= np.g[j].a == np.g[j].b ? 1 : 0;
           if (P.bf16_ns) {
             P.ns_launches.push_back(L);
           } else {
@@ -773,6 +790,7 @@ void ensure_device_attrs() {
   ns_tc_set_attrs();
   launch_fast_paths_attrs();
   ns_pair_set_attrs();
+  ns_apply_pair_set_attrs();
   cudaFuncSetAttribute(k_topk_select, cudaFuncAttributeMaxDynamicSharedMemorySize, 4 * DION2_MAX_SELECT_DIM);
   cudaFuncSetAttribute(k_full_decay, cudaFuncAttributeMaxDynamicSharedMemorySize, DION2_MAX_SELECT_DIM);
   g_attr_done = true;
@@ -790,7 +808,9 @@ int run_ns(Plan& P, const dion2_config* c, Launcher& L, cudaStream_t s, bool do_
   }
   for (const Launch& ln : P.ns_launches) {
     L.begin(ln.phase);
-    if (ln.kind == 3) {
+    if (ln.kind == 5) {
+      launch_ns_apply_pair(std::min(2 * ln.tc.p.total_tiles, sms & ~1), s, ln.tc);
+    } else if (ln.kind == 3) {
       const int sk = ln.tc.p.splitk > 1 ? ln.tc.p.splitk : 1;
       launch_ns_pair(std::min(2 * ln.tc.p.total_tiles * sk, sms & ~1), s, ln.tc);
       if (sk > 1) launch_splitk_reduce(s, ln.tc.p);

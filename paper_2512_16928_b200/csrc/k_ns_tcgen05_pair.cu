@@ -153,7 +153,10 @@ __global__ void __cluster_dims__(2, 1, 1) __launch_bounds__(kPairThreads, 1)
           uint8_t* sa = smem + stage * kStage;
           uint8_t* sb = sa + kAB;
           const uint32_t leader_full = mapa_shared(smem_u32(&full_bar[stage]), 0);
-          if (rank == 0) mbar_arrive_expect_tx(&full_bar[stage], 2 * kStage);
+          // b_is_a (gram X X^T, poly A A): on a diagonal tile CTA r's B half is its A half, so B
+          // is not loaded (the MMA reads A's stage for both operands)
+          const bool same = p.b_is_a && c.tm == c.tn;
+          if (rank == 0) mbar_arrive_expect_tx(&full_bar[stage], same ? 2 * kAB : 2 * kStage);
           // sym_in: a k-block left of the diagonal tile is stored only as its transpose
           const bool at = kSymIn && ((kb * kBK) >> 8) < c.tm;
           const bool bt = kSymIn && ((kb * kBK) >> 8) < c.tn;
@@ -169,7 +172,8 @@ __global__ void __cluster_dims__(2, 1, 1) __launch_bounds__(kPairThreads, 1)
               tma_load_3d_pair(sa + j * 64 * kBK * 2, &P.mapAT[c.group], leader_full,
                                c.tm * 256 + (int)rank * 128 + j * 64, kb * kBK, c.z);
           }
-          if (p.b_kmajor && bt) {
+          if (same) {
+          } else if (p.b_kmajor && bt) {
 #pragma unroll
             for (int j = 0; j < 2; ++j)
               tma_load_3d_pair(sb + j * 64 * kBK * 2, &P.mapBT[c.group], leader_full,
@@ -207,7 +211,7 @@ __global__ void __cluster_dims__(2, 1, 1) __launch_bounds__(kPairThreads, 1)
           mbar_wait(&full_bar[stage], phase);
           tc_fence_after();
           const uint32_t a_addr = smem_u32(smem + stage * kStage);
-          const uint32_t b_addr = a_addr + kAB;
+          const uint32_t b_addr = (p.b_is_a && c.tm == c.tn) ? a_addr : a_addr + kAB;
           if constexpr (!kSymIn) {
 #pragma unroll
             for (int k = 0; k < kBK / 16; ++k) {

@@ -129,6 +129,8 @@ struct NsParams {
   int sym;                   // symmetric output: upper-triangle tiles only, mirrored by the epilogue (pair kernel)
   const float* ns_scale_all; // [n_mats][4] (MatDesc::ns_scale)
   int b_kmajor;
+  int b_is_a;                // pair kernel: every group's B operand is its A operand (gram X X^T, poly
+                             // A A): diagonal tiles load the A half only and use it for both
   int in_f16;                // operands (and cin) are fp16, else bf16
   int out_f16;               // output written as fp16, else bf16
   int reverse;               // walk the tile list backwards (L2 reuse of the previous launch's last writes)
@@ -160,6 +162,11 @@ void launch_ns_tc(int bn, int grid, cudaStream_t s, const NsTcParams& P);
 void ns_pair_set_attrs();
 void launch_ns_pair(int grid, cudaStream_t s, const NsTcParams& P);
 void launch_splitk_reduce(cudaStream_t s, const NsParams& p);  // after a split-K pair launch
+// apply on a CTA pair with A resident in shared memory (k_ns_apply_pair.cu): groups with
+// k_blocks <= kMaxResidentKB (p_pad <= 512), m_tiles = p_pad / 256, MN-major B
+constexpr int kMaxResidentKB = 8;
+void ns_apply_pair_set_attrs();
+void launch_ns_apply_pair(int grid, cudaStream_t s, const NsTcParams& P);
 
 template <int BN>
 constexpr int ns_tc_stages() { return BN == 256 ? 4 : 6; }
