@@ -343,6 +343,26 @@ int build_layout(Plan& P, const dion2_matrix* mats, int n, const dion2_config* c
 }
 
 
+// Kind-5 launches (resident-A pair apply) count work in chunks of up to L consecutive 256-column
+// blocks of one 256-row block: L = 8, halved while the launch has fewer than two chunks per CTA pair.
+static void apply_chunks(NsParams& np) {
+  const int pairs = sm_count() / 2;
+  auto count = [&](int L) {
+    int n = 0;
+    for (int j = 0; j < np.ngroups; ++j) n += np.g[j].count * ((np.g[j].n_tiles + L - 1) / L) * np.g[j].m_tiles;
+    return n;
+  };
+  int L = 8;
+  while (L > 1 && count(L) < 2 * pairs) L /= 2;
+  np.chunk_len = L;
+  int base = 0;
+  for (int j = 0; j < np.ngroups; ++j) {
+    np.g[j].tile_base = base;
+    base += np.g[j].count * ((np.g[j].n_tiles + L - 1) / L) * np.g[j].m_tiles;
+  }
+  np.total_tiles = base;
+}
+
 // Restart segments of the Gram-space form (reading R24): consecutive iterations [t0, t1) whose
 // growth prod |a_t| stays <= kRestartGrowth share one p x p recursion; each later segment
 // restarts from its X, formed explicitly by the previous segment's apply.  The default
@@ -460,6 +480,7 @@ static int append_gram_space_launches(Plan& P, const dion2_config* c, void* ws, 
       np.total_tiles = tiles;
       np.b_is_a = np.b_kmajor ? 1 : 0;
       for (int j = 0; j < np.ngroups; ++j) np.b_is_a &= np.g[j].a == np.g[j].b ? 1 : 0;
+      if (L.kind == 5) apply_chunks(np);
       P.ns_launches.push_back(L);
     }
     return DION2_OK;
@@ -765,6 +786,7 @@ int build_device_plan(Plan& P, const dion2_matrix* mats, const dion2_config* c, 
           np.total_tiles = tiles;
           np.b_is_a = np.b_kmajor ? 1 : 0;
           for (int j = 0; j < np.ngroups; ++j) np.b_is_a &= np.g[j].a == np.g[j].b ? 1 : 0;
+          if (L.kind == 5) apply_chunks(np);
           if (P.bf16_ns) {
             P.ns_launches.push_back(L);
           } else {

@@ -4,14 +4,15 @@
 // (Alg. 1 l.4).
 //
 // The apply's K is short (p = 512 at alpha = 1/4 on the 1B set) and its N long (q = 2048 ..
-// 8192), so a tile re-reading both operands through L2 moves ~1.5x the FLOPs' worth of
-// bytes the tensor cores can consume (ncu, round 2: the 1-SM 128 x 256 kernel at 20% tensor
-// pipe, 46% L2 throughput, 0.32 ms per launch).  Here each CTA pair walks a CONTIGUOUS range
-// of the flattened (matrix, 256-row block, 256-column block) tile list, column block fastest:
-// the pair's 256 rows of A (128 per CTA, K x 128 fp16 <= 128 KB) are loaded once per
-// (matrix, row block) and stay in shared memory while the pair streams X's column blocks
-// through a 4-stage ring (16 KB per CTA per k-block).  Per CTA and tile: 128 KB of B instead
-// of 128 KB of A + 128 KB of B (pair kernel) or 384 KB (1-SM kernel).
+// 8192).  Work unit = a CHUNK: one 256-row block (tm) of one matrix and a run of up to
+// p.chunk_len consecutive 256-column blocks.  The pair loads its 256 rows of A (128 per CTA,
+// K x 128 fp16 <= 128 KB) once per chunk and keeps them in shared memory while it streams the
+// chunk's X column blocks through a 4-stage ring (16 KB per CTA per k-block): per CTA and tile
+// 128 KB of B, against 128 KB of A + 128 KB of B for the pair kernel and 384 KB for the 1-SM
+// kernel.  Chunks are numbered (matrix, column run, tm) with tm fastest and dealt round-robin
+// to the pairs, so the p / 256 chunks that read the same X column blocks run on neighbouring
+// pairs at the same time and X comes from DRAM once (a pair-contiguous tile range read it
+// twice: ncu 1.30 GB for 0.6 GB of X, 0.353 ms per launch).
 //
 // Roles per CTA (320 threads): warp 0 TMA producer (A blocks on a chunk change, then the B
 // ring; completion counted on the leader's barriers), warp 1 TMEM allocator (both CTAs) + MMA
@@ -39,27 +40,31 @@ constexpr int kBarOff = kBOff + kStages * (int)kBB;
 constexpr int kStageOff = kBarOff + 1024;
 constexpr int kSmem = 1024 + kStageOff + kEpiWarps * 2 * 2048;
 
-struct Tile {
-  int group, z, tm, tn;
+struct Chunk {
+  int group, z, tm, tn0, len;
 };
 
-__device__ __forceinline__ Tile decode(const NsParams& p, int t) {
+// chunk index -> (group, z, tm, first column block, column blocks); NsGroup::tile_base holds
+// the group's first chunk index here
+__device__ __forceinline__ Chunk decode_chunk(const NsParams& p, int c) {
   int g = 0;
 #pragma unroll
   for (int i = 1; i < kMaxGroups; ++i)
-    if (i < p.ngroups && t >= p.g[i].tile_base) g = i;
+    if (i < p.ngroups && c >= p.g[i].tile_base) g = i;
   const NsGroup& G = p.g[g];
-  const int local = t - G.tile_base;
-  const int per = G.m_tiles * G.n_tiles;
-  Tile c;
-  c.group = g;
-  c.z = local / per;
-  const int r = local % per;
-  c.tm = r / G.n_tiles;
-  c.tn = r % G.n_tiles;
-  return c;
+  const int L = p.chunk_len;
+  const int runs = (G.n_tiles + L - 1) / L;
+  const int per_z = runs * G.m_tiles;
+  const int local = c - G.tile_base;
+  Chunk k;
+  k.group = g;
+  k.z = local / per_z;
+  const int r = local % per_z;
+  k.tm = r % G.m_tiles;
+  k.tn0 = (r / G.m_tiles) * L;
+  k.len = min(L, G.n_tiles - k.tn0);
+  return k;
 }
-__device__ __forceinline__ int chunk_key(const Tile& c) { return (c.group << 24) | (c.z << 8) | c.tm; }
 
 __device__ __forceinline__ uint32_t pack_bf16x2(float lo, float hi) {
   __nv_bfloat162 v = __floats2bfloat162_rn(lo, hi);
@@ -87,8 +92,7 @@ __global__ void __cluster_dims__(2, 1, 1) __launch_bounds__(kThreads, 1)
   const int warp = threadIdx.x >> 5, lane = threadIdx.x & 31;
   const uint32_t rank = cluster_ctarank();
   const int cid = (int)cluster_id_x(), ncl = (int)nclusters_x();
-  // this pair's contiguous tile range
-  const int t0 = (int)((long long)p.total_tiles * cid / ncl), t1 = (int)((long long)p.total_tiles * (cid + 1) / ncl);
+  const int nchunks = p.total_tiles;  // kind 5 launches count chunks
 
   if (warp == 0 && lane == 0) {
     for (int i = 0; i < kStages; ++i) {
@@ -119,41 +123,37 @@ __global__ void __cluster_dims__(2, 1, 1) __launch_bounds__(kThreads, 1)
   if (warp == 0) {
     if (lane == 0) {
       // ---------------- TMA producer (both CTAs)
-      int stage = 0, chunk = -1, cur = -1;
+      int stage = 0, chunk = 0;
       uint32_t phase = 0;
       const uint32_t leader_afull = mapa_shared(smem_u32(afull_bar), 0);
-      for (int t = t0; t < t1; ++t) {
-        const Tile c = decode(p, t);
-        const NsGroup& G = p.g[c.group];
-        const int key = chunk_key(c);
-        if (key != cur) {
-          // new (matrix, row block): reload the resident A rows once the previous chunk's MMAs
-          // have read them (the first wait passes on the fresh barrier's preceding phase)
-          ++chunk;
-          cur = key;
-          mbar_wait(aempty_bar, (chunk & 1) ^ 1);
-          if (rank == 0) mbar_arrive_expect_tx(afull_bar, 2 * kABlk * G.k_blocks);
-          for (int kb = 0; kb < G.k_blocks; ++kb)
-            tma_load_3d_pair(sA + kb * kABlk, &P.mapA[c.group], leader_afull, kb * kBK, c.tm * 256 + (int)rank * 128,
-                             c.z);
-        }
-        for (int kb = 0; kb < G.k_blocks; ++kb) {
-          mbar_wait(&empty_bar[stage], phase ^ 1);
-          uint8_t* sb = sB + stage * kBB;
-          const uint32_t leader_full = mapa_shared(smem_u32(&full_bar[stage]), 0);
-          if (rank == 0) mbar_arrive_expect_tx(&full_bar[stage], 2 * kBB);
+      for (int ci = cid; ci < nchunks; ci += ncl, ++chunk) {
+        const Chunk k = decode_chunk(p, ci);
+        const NsGroup& G = p.g[k.group];
+        // reload the resident A rows once the previous chunk's MMAs have read them (the first
+        // wait passes on the fresh barrier's preceding phase)
+        mbar_wait(aempty_bar, (chunk & 1) ^ 1);
+        if (rank == 0) mbar_arrive_expect_tx(afull_bar, 2 * kABlk * G.k_blocks);
+        for (int kb = 0; kb < G.k_blocks; ++kb)
+          tma_load_3d_pair(sA + kb * kABlk, &P.mapA[k.group], leader_afull, kb * kBK, k.tm * 256 + (int)rank * 128, k.z);
+        for (int tn = k.tn0; tn < k.tn0 + k.len; ++tn) {
+          for (int kb = 0; kb < G.k_blocks; ++kb) {
+            mbar_wait(&empty_bar[stage], phase ^ 1);
+            uint8_t* sb = sB + stage * kBB;
+            const uint32_t leader_full = mapa_shared(smem_u32(&full_bar[stage]), 0);
+            if (rank == 0) mbar_arrive_expect_tx(&full_bar[stage], 2 * kBB);
 #pragma unroll
-          for (int j = 0; j < 2; ++j) {
-            const int nn = c.tn * 256 + (int)rank * 128 + j * 64;
-            if (G.pieces_load) {  // distributed owner: the N axis (q) of X0 runs over the rank pieces
-              const int pr = nn / G.pieces_qo;
-              tma_load_3d_pair(sb + j * 64 * kBK * 2, &P.mapP[c.group][G.pieces_P + pr], leader_full,
-                               nn - pr * G.pieces_qo, kb * kBK, c.z);
-            } else {
-              tma_load_3d_pair(sb + j * 64 * kBK * 2, &P.mapB[c.group], leader_full, nn, kb * kBK, c.z);
+            for (int j = 0; j < 2; ++j) {
+              const int nn = tn * 256 + (int)rank * 128 + j * 64;
+              if (G.pieces_load) {  // distributed owner: the N axis (q) of X0 runs over the rank pieces
+                const int pr = nn / G.pieces_qo;
+                tma_load_3d_pair(sb + j * 64 * kBK * 2, &P.mapP[k.group][G.pieces_P + pr], leader_full,
+                                 nn - pr * G.pieces_qo, kb * kBK, k.z);
+              } else {
+                tma_load_3d_pair(sb + j * 64 * kBK * 2, &P.mapB[k.group], leader_full, nn, kb * kBK, k.z);
+              }
             }
+            if (++stage == kStages) { stage = 0; phase ^= 1; }
           }
-          if (++stage == kStages) { stage = 0; phase ^= 1; }
         }
       }
     }
@@ -161,39 +161,36 @@ __global__ void __cluster_dims__(2, 1, 1) __launch_bounds__(kThreads, 1)
     if (lane == 0 && rank == 0) {
       // ---------------- MMA issuer (leader CTA)
       const uint32_t idesc = kIdescMN & (p.in_f16 ? ~kIdescAbFmt : ~0u);
-      int stage = 0, chunk = -1, cur = -1, it = 0;
+      int stage = 0, chunk = 0, it = 0;
       uint32_t phase = 0;
-      for (int t = t0; t < t1; ++t, ++it) {
-        const Tile c = decode(p, t);
-        const NsGroup& G = p.g[c.group];
-        const int key = chunk_key(c);
-        if (key != cur) {
-          if (chunk >= 0) umma_commit_pair(aempty_bar);  // all MMAs so far (the previous chunk) read A
-          ++chunk;
-          cur = key;
-          mbar_wait(afull_bar, chunk & 1);
-          tc_fence_after();
-        }
-        const int acc = it & 1;
-        const uint32_t acc_phase = (it >> 1) & 1;
-        mbar_wait(&tempty_bar[acc], acc_phase ^ 1);
+      for (int ci = cid; ci < nchunks; ci += ncl, ++chunk) {
+        const Chunk k = decode_chunk(p, ci);
+        const NsGroup& G = p.g[k.group];
+        mbar_wait(afull_bar, chunk & 1);
         tc_fence_after();
-        const uint32_t tmem_d = tmem_base + acc * 256;
-        for (int kb = 0; kb < G.k_blocks; ++kb) {
-          mbar_wait(&full_bar[stage], phase);
+        for (int tn = k.tn0; tn < k.tn0 + k.len; ++tn, ++it) {
+          const int acc = it & 1;
+          const uint32_t acc_phase = (it >> 1) & 1;
+          mbar_wait(&tempty_bar[acc], acc_phase ^ 1);
           tc_fence_after();
-          const uint32_t a_addr = smem_u32(sA + kb * kABlk);
-          const uint32_t b_addr = smem_u32(sB + stage * kBB);
+          const uint32_t tmem_d = tmem_base + acc * 256;
+          for (int kb = 0; kb < G.k_blocks; ++kb) {
+            mbar_wait(&full_bar[stage], phase);
+            tc_fence_after();
+            const uint32_t a_addr = smem_u32(sA + kb * kABlk);
+            const uint32_t b_addr = smem_u32(sB + stage * kBB);
 #pragma unroll
-          for (int k = 0; k < kBK / 16; ++k) {
-            const uint64_t adesc = umma_desc_sw128(a_addr + k * 32, 16, 1024);
-            const uint64_t bdesc = umma_desc_sw128(b_addr + k * 2048, 64 * kBK * 2, 1024);
-            umma_bf16_ss_pair(tmem_d, adesc, bdesc, idesc, (kb | k) != 0);
+            for (int kk = 0; kk < kBK / 16; ++kk) {
+              const uint64_t adesc = umma_desc_sw128(a_addr + kk * 32, 16, 1024);
+              const uint64_t bdesc = umma_desc_sw128(b_addr + kk * 2048, 64 * kBK * 2, 1024);
+              umma_bf16_ss_pair(tmem_d, adesc, bdesc, idesc, (kb | kk) != 0);
+            }
+            umma_commit_pair(&empty_bar[stage]);
+            if (++stage == kStages) { stage = 0; phase ^= 1; }
           }
-          umma_commit_pair(&empty_bar[stage]);
-          if (++stage == kStages) { stage = 0; phase ^= 1; }
+          umma_commit_pair(&tfull_bar[acc]);
         }
-        umma_commit_pair(&tfull_bar[acc]);
+        umma_commit_pair(aempty_bar);  // this chunk's MMAs have read the resident A
       }
     }
   } else {
@@ -205,14 +202,15 @@ __global__ void __cluster_dims__(2, 1, 1) __launch_bounds__(kThreads, 1)
     const uint32_t leader_tempty[2] = {mapa_shared(smem_u32(&tempty_bar[0]), 0),
                                        mapa_shared(smem_u32(&tempty_bar[1]), 0)};
     int sbuf = 0, it = 0;
-    for (int t = t0; t < t1; ++t, ++it) {
-      const Tile c = decode(p, t);
-      const NsGroup& G = p.g[c.group];
+    for (int ci = cid; ci < nchunks; ci += ncl) {
+     const Chunk k = decode_chunk(p, ci);
+     const NsGroup& G = p.g[k.group];
+     float osc = 1.f;
+     if (p.scale_sel) osc = p.ns_scale_all[4 * G.gmats[k.z] + (p.scale_sel - 1)];
+     const float ca = p.cacc * osc;
+     for (int tn = k.tn0; tn < k.tn0 + k.len; ++tn, ++it) {
       const int acc = it & 1;
       const uint32_t acc_phase = (it >> 1) & 1;
-      float osc = 1.f;
-      if (p.scale_sel) osc = p.ns_scale_all[4 * G.gmats[c.z] + (p.scale_sel - 1)];
-      const float ca = p.cacc * osc;
       mbar_wait(&tfull_bar[acc], acc_phase);
       tc_fence_after();
 #pragma unroll 1
@@ -233,12 +231,12 @@ __global__ void __cluster_dims__(2, 1, 1) __launch_bounds__(kThreads, 1)
         fence_proxy_async_smem();
         __syncwarp();
         if (lane == 0) {
-          const int col = c.tn * 256 + cc32 * 32, row = c.tm * 256 + (int)rank * 128 + lg * 32;
+          const int col = tn * 256 + cc32 * 32, row = k.tm * 256 + (int)rank * 128 + lg * 32;
           if (G.pieces_store) {  // X_T straight into the rank pieces of the exchange buffer
             const int pr = col / G.pieces_qo;
-            tma_store_3d(&P.mapP[c.group][2 * G.pieces_P + pr], buf, col - pr * G.pieces_qo, row, c.z);
+            tma_store_3d(&P.mapP[k.group][2 * G.pieces_P + pr], buf, col - pr * G.pieces_qo, row, k.z);
           } else {
-            tma_store_3d(&P.mapD[c.group], buf, col, row, c.z);
+            tma_store_3d(&P.mapD[k.group], buf, col, row, k.z);
           }
           bulk_commit();
         }
@@ -247,6 +245,7 @@ __global__ void __cluster_dims__(2, 1, 1) __launch_bounds__(kThreads, 1)
       tc_fence_before();
       __syncwarp();
       if (lane == 0) mbar_arrive_cluster(leader_tempty[acc]);
+     }
     }
     if (lane == 0) bulk_wait_all();
   }

@@ -144,6 +144,9 @@ struct NsParams {
   // in order (deterministic) and applies the epilogue
   int splitk;                // <= 1: off
   float* partial;
+  // resident-A apply (k_ns_apply_pair.cu): total_tiles counts chunks of up to chunk_len column
+  // blocks of one 256-row block, NsGroup::tile_base the group's first chunk
+  int chunk_len;
 };
 
 // tcgen05 path (k_ns_tcgen05.cu): tensor maps for the TMA operand loads.
