@@ -133,6 +133,9 @@ typedef struct {
   uint64_t step;      /* random selection counter: the caller's step index (unused for L1) */
   int32_t ns_form;    /* dion2_ns_form, default AUTO (BF16 precision only; FP32 is always DIRECT) */
   int32_t reserved0;  /* flags: 0, or DION2_FLAG_LR_DEVICE (other bits must be 0) */
+  int32_t w_dtype;    /* dion2_dtype of W (ABI v6): F32 (default) or BF16 -- bf16 weights; the update
+                         is computed in fp32 and rounded to nearest once (w <- bf16(float(w) - s o)).
+                         M stays fp32 (its l1 scores decide the selection) */
 } dion2_config;
 
 /* Fill *cfg with the defaults above.  Always returns DION2_OK. */

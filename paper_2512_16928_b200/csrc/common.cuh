@@ -18,7 +18,7 @@ constexpr int kAxisCols = 1;
 // S = M[:, K] (cols mode, sr = m, sc = k).  X is its wide orientation
 // (p <= q): X = S, or X = S^T when `transposed` (reading R4).
 struct MatDesc {
-  float* W;
+  float* W;             // fp32, or bf16 under dion2_config.w_dtype = DION2_DT_BF16 (the K7 kernels cast)
   float* M;
   const void* G;
   int32_t* sel_out;
@@ -89,6 +89,26 @@ __device__ __forceinline__ float x16_prescale(float smax) {
   frexpf(smax, &E);  // smax = m 2^E, m in [0.5, 1)
   const int e = max(-100, min(64, 15 - E));
   return ldexpf(1.f, e);
+}
+
+// W element access of the sparse update (K7): fp32 W, or bf16 W (f4 "bf16 W variant": the update
+// is computed in fp32 and rounded to nearest once, w <- bf16(float(w) - sc o)).
+__device__ __forceinline__ float ld_w(const float* p) { return *p; }
+__device__ __forceinline__ float ld_w(const __nv_bfloat16* p) { return __bfloat162float(*p); }
+__device__ __forceinline__ void st_w(float* p, float v) { *p = v; }
+__device__ __forceinline__ void st_w(__nv_bfloat16* p, float v) { *p = __float2bfloat16_rn(v); }
+// 4 consecutive elements j*4 .. j*4+3 (16-B aligned fp32 / 8-B aligned bf16 rows)
+__device__ __forceinline__ float4 ld_w4(const float* row, int j) { return reinterpret_cast<const float4*>(row)[j]; }
+__device__ __forceinline__ float4 ld_w4(const __nv_bfloat16* row, int j) {
+  const uint2 u = reinterpret_cast<const uint2*>(row)[j];
+  const __nv_bfloat162 lo = *reinterpret_cast<const __nv_bfloat162*>(&u.x);
+  const __nv_bfloat162 hi = *reinterpret_cast<const __nv_bfloat162*>(&u.y);
+  return make_float4(__low2float(lo), __high2float(lo), __low2float(hi), __high2float(hi));
+}
+__device__ __forceinline__ void st_w4(float* row, int j, float4 v) { reinterpret_cast<float4*>(row)[j] = v; }
+__device__ __forceinline__ void st_w4(__nv_bfloat16* row, int j, float4 v) {
+  __nv_bfloat162 lo = __floats2bfloat162_rn(v.x, v.y), hi = __floats2bfloat162_rn(v.z, v.w);
+  reinterpret_cast<uint2*>(row)[j] = make_uint2(*reinterpret_cast<uint32_t*>(&lo), *reinterpret_cast<uint32_t*>(&hi));
 }
 
 __device__ __forceinline__ uint32_t pack2_h(float a, float b) {

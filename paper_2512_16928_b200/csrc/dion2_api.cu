@@ -125,6 +125,7 @@ int validate_config(const dion2_config* c) {
   if (c->select != DION2_SELECT_L1 && c->select != DION2_SELECT_RANDOM) return DION2_EINVAL_CONFIG;
   if (c->precision != DION2_NS_BF16 && c->precision != DION2_NS_FP32) return DION2_EINVAL_CONFIG;
   if (c->grad_dtype != DION2_DT_F32 && c->grad_dtype != DION2_DT_BF16) return DION2_EINVAL_CONFIG;
+  if (c->w_dtype != DION2_DT_F32 && c->w_dtype != DION2_DT_BF16) return DION2_EINVAL_CONFIG;
   if (c->decay_mode < 0 || c->decay_mode > 1) return DION2_EINVAL_CONFIG;
   if (c->scale_mode < 0 || c->scale_mode > 1) return DION2_EINVAL_CONFIG;
   if (c->ns_form < DION2_NS_FORM_AUTO || c->ns_form > DION2_NS_FORM_GRAM || (c->reserved0 & ~DION2_FLAG_LR_DEVICE) != 0)
@@ -166,6 +167,7 @@ std::string plan_key(const dion2_matrix* mats, int n, const dion2_config* c, voi
   put(&c->select, 4);
   put(&c->precision, 4);
   put(&c->grad_dtype, 4);
+  put(&c->w_dtype, 4);
   put(&c->decay_mode, 4);
   put(&c->scale_mode, 4);
   put(&c->ns_form, 4);
@@ -872,7 +874,8 @@ int refresh_tables(Plan& P, const dion2_matrix* mats, const dion2_config* c, cud
     D[i].sel_out = mats[i].sel_out;
     D[i].O_out = mats[i].O_out;
     const size_t gel = c->grad_dtype == DION2_DT_BF16 ? 2 : 4;
-    const bool al = ((uintptr_t)mats[i].W % 16 == 0) && ((uintptr_t)mats[i].M % 16 == 0) &&
+    const size_t wal = c->w_dtype == DION2_DT_BF16 ? 8 : 16;  // 4 W elements per vector access
+    const bool al = ((uintptr_t)mats[i].W % wal == 0) && ((uintptr_t)mats[i].M % 16 == 0) &&
                     ((uintptr_t)mats[i].G % (gel == 4 ? 16 : 8) == 0) && (mats[i].ld % 4 == 0) &&
                     (!mats[i].m_transposed || mats[i].ldm % 4 == 0);
     D[i].vec4 = al ? 1 : 0;
@@ -1034,20 +1037,20 @@ void stage_post(Plan& P, const dion2_matrix* mats, const dion2_config* c, void* 
   const float* lr_dev = (c->reserved0 & DION2_FLAG_LR_DEVICE) ? (const float*)at(ws, P.off_status + 8) : nullptr;
   if (P.total_gather_tiles > 0 && P.generic_scatter_mats > 0) {
     L.begin(PH_SCATTER);
-    launch_scatter_update(P.bf16_ns, stream_grid(P.total_gather_tiles, 8, persistent), s, dmats,
+    launch_scatter_update(P.bf16_ns, c->w_dtype == DION2_DT_BF16, stream_grid(P.total_gather_tiles, 8, persistent), s, dmats,
                           (const int32_t*)tab(P, P.off_gprefix), n, P.total_gather_tiles, bad, c->lr, lr_dev);
     L.end();
   }
   if (P.fl_sn[0]) {
     L.begin(PH_SCATTER_ROWS);
-    launch_scatter_rows(stream_grid(ceil_div(P.fl_sunits[0], 8), 8, persistent), s, dmats,
+    launch_scatter_rows(c->w_dtype == DION2_DT_BF16, stream_grid(ceil_div(P.fl_sunits[0], 8), 8, persistent), s, dmats,
                         (const int32_t*)tab(P, P.off_fls_mats[0]), (const int32_t*)tab(P, P.off_fl_sprefix[0]),
                         P.fl_sn[0], P.fl_sunits[0], bad, c->lr, lr_dev);
     L.end();
   }
   if (P.fl_sn[1]) {
     L.begin(PH_SCATTER_COLS);
-    launch_scatter_cols_t(stream_grid(P.fl_sunits[1], 6, persistent), P.fl_smaxk, P.fl_maxn, s, dmats,
+    launch_scatter_cols_t(c->w_dtype == DION2_DT_BF16, stream_grid(P.fl_sunits[1], 6, persistent), P.fl_smaxk, P.fl_maxn, s, dmats,
                           (const int32_t*)tab(P, P.off_fls_mats[1]), (const int32_t*)tab(P, P.off_fl_sprefix[1]),
                           P.fl_sn[1], P.fl_sunits[1], bad, c->lr, lr_dev);
     L.end();

@@ -517,6 +517,7 @@ std::string dist_key(const dion2_shard* sh, int n, const dion2_config* c, int wo
   put(&c->axis, 4);
   put(&c->precision, 4);
   put(&c->grad_dtype, 4);
+  put(&c->w_dtype, 4);
   put(&c->decay_mode, 4);
   put(&c->scale_mode, 4);
   put(&c->ns_form, 4);  // shapes the owner's NS plan
@@ -567,7 +568,7 @@ int refresh(DistPlan& D, const dion2_shard* sh, const dion2_config* c, cudaStrea
     md[j].ld = sh[j].ld;
     md[j].ldm = sh[j].m_transposed ? sh[j].ldm : 0;
     const size_t gel = c->grad_dtype == DION2_DT_BF16 ? 2 : 4;
-    md[j].vec4 = ((uintptr_t)sh[j].W % 16 == 0) && ((uintptr_t)sh[j].M % 16 == 0) &&
+    md[j].vec4 = ((uintptr_t)sh[j].W % (c->w_dtype == DION2_DT_BF16 ? 8 : 16) == 0) && ((uintptr_t)sh[j].M % 16 == 0) &&
                  ((uintptr_t)sh[j].G % (gel == 4 ? 16 : 8) == 0) && (sh[j].ld % 4 == 0) &&
                  (!sh[j].m_transposed || sh[j].ldm % 4 == 0);
   }
@@ -686,21 +687,21 @@ void phase_scatter(DistPlan& D, void* ws, const dion2_config* c, Launcher& L, cu
   const int32_t* bad = (const int32_t*)at(ws, D.off_bad);
   if (D.total_gather_tiles) {
     L.begin(PH_SCATTER);
-    launch_scatter_update(true, std::min(D.total_gather_tiles, sms * 8), s, dm, (const int32_t*)dt(D, D.t_gprefix),
+    launch_scatter_update(true, c->w_dtype == DION2_DT_BF16, std::min(D.total_gather_tiles, sms * 8), s, dm, (const int32_t*)dt(D, D.t_gprefix),
                           D.n, D.total_gather_tiles, bad, c->lr, lr_dev);
     L.end();
   }
   if (D.fl_sn[0]) {
     L.begin(PH_SCATTER_ROWS);
     const int blocks = (int)std::min<int64_t>(ceil_div(D.fl_sunits[0], 8), (int64_t)sms * 8);
-    launch_scatter_rows(blocks, s, dm, (const int32_t*)dt(D, D.t_flsm[0]), (const int32_t*)dt(D, D.t_fls[0]),
+    launch_scatter_rows(c->w_dtype == DION2_DT_BF16, blocks, s, dm, (const int32_t*)dt(D, D.t_flsm[0]), (const int32_t*)dt(D, D.t_fls[0]),
                         D.fl_sn[0], D.fl_sunits[0], bad, c->lr, lr_dev);
     L.end();
   }
   if (D.fl_sn[1]) {
     L.begin(PH_SCATTER_COLS);
     const int blocks = std::min(D.fl_sunits[1], sms * 6);  // as the single-GPU path
-    launch_scatter_cols_t(blocks, D.fl_maxk, D.max_cols_col, s, dm, (const int32_t*)dt(D, D.t_flsm[1]),
+    launch_scatter_cols_t(c->w_dtype == DION2_DT_BF16, blocks, D.fl_maxk, D.max_cols_col, s, dm, (const int32_t*)dt(D, D.t_flsm[1]),
                           (const int32_t*)dt(D, D.t_fls[1]), D.fl_sn[1], D.fl_sunits[1], bad, c->lr, lr_dev);
     L.end();
   }
@@ -902,6 +903,7 @@ int dp_get_plan(DpPlan** out, const dion2_matrix* mats, int n, const dion2_confi
   put(&c->axis, 4);
   put(&c->precision, 4);
   put(&c->grad_dtype, 4);
+  put(&c->w_dtype, 4);
   put(&c->decay_mode, 4);
   put(&c->scale_mode, 4);
   put(&c->ns_form, 4);

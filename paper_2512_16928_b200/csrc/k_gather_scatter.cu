@@ -148,7 +148,7 @@ __global__ void k_norm_finalize(const MatDesc* __restrict__ mats, int n_mats, fl
   }
 }
 
-template <typename XT>
+template <typename XT, typename WT>
 __global__ void __launch_bounds__(256) k_scatter_update(const MatDesc* __restrict__ mats,
                                                         const int32_t* __restrict__ tile_prefix_mats, int n_mats,
                                                         int total_tiles, const int32_t* __restrict__ bad, float lr,
@@ -181,7 +181,7 @@ __global__ void __launch_bounds__(256) k_scatter_update(const MatDesc* __restric
       const int al = ty + 16 * rr, a = a0 + al;
       if (a >= md.sr) continue;
       const int64_t row = s_row(md, a);
-      float* wrow = md.W + row * md.ld;
+      WT* wrow = reinterpret_cast<WT*>(md.W) + row * md.ld;
       float o[4];
 #pragma unroll
       for (int c = 0; c < 4; ++c) {
@@ -191,16 +191,15 @@ __global__ void __launch_bounds__(256) k_scatter_update(const MatDesc* __restric
       }
       const int b = b0 + tx * 4;
       if (md.axis == kAxisRows && md.vec4 && b + 3 < md.sc) {
-        float4* p = reinterpret_cast<float4*>(wrow + b);
-        float4 w = *p;
+        float4 w = ld_w4(wrow, b >> 2);
         w.x -= sc * o[0]; w.y -= sc * o[1]; w.z -= sc * o[2]; w.w -= sc * o[3];
-        *p = w;
+        st_w4(wrow, b >> 2, w);
       } else {
 #pragma unroll
         for (int c = 0; c < 4; ++c) {
           if (b + c < md.sc) {
-            float* p = wrow + s_col(md, b + c);
-            *p = *p - sc * o[c];
+            WT* p = wrow + s_col(md, b + c);
+            st_w(p, ld_w(p) - sc * o[c]);
           }
         }
       }
@@ -213,12 +212,19 @@ __global__ void __launch_bounds__(256) k_scatter_update(const MatDesc* __restric
     if (md.transposed) __syncthreads();
   }
 }
-void launch_scatter_update(bool x16, int blocks, cudaStream_t s, const MatDesc* mats, const int32_t* tile_prefix_mats,
-                           int n_mats, int total_tiles, const int32_t* bad, float lr, const float* lr_dev) {
-  if (x16)
-    k_scatter_update<__half><<<blocks, 256, 0, s>>>(mats, tile_prefix_mats, n_mats, total_tiles, bad, lr, lr_dev);
+void launch_scatter_update(bool x16, bool w_bf16, int blocks, cudaStream_t s, const MatDesc* mats,
+                           const int32_t* tile_prefix_mats, int n_mats, int total_tiles, const int32_t* bad, float lr,
+                           const float* lr_dev) {
+  if (x16 && w_bf16)
+    k_scatter_update<__half, __nv_bfloat16><<<blocks, 256, 0, s>>>(mats, tile_prefix_mats, n_mats, total_tiles, bad, lr,
+                                                                   lr_dev);
+  else if (x16)
+    k_scatter_update<__half, float><<<blocks, 256, 0, s>>>(mats, tile_prefix_mats, n_mats, total_tiles, bad, lr, lr_dev);
+  else if (w_bf16)
+    k_scatter_update<float, __nv_bfloat16><<<blocks, 256, 0, s>>>(mats, tile_prefix_mats, n_mats, total_tiles, bad, lr,
+                                                                  lr_dev);
   else
-    k_scatter_update<float><<<blocks, 256, 0, s>>>(mats, tile_prefix_mats, n_mats, total_tiles, bad, lr, lr_dev);
+    k_scatter_update<float, float><<<blocks, 256, 0, s>>>(mats, tile_prefix_mats, n_mats, total_tiles, bad, lr, lr_dev);
 }
 
 // Full-decay ablation: M <- mu * M on the UNSELECTED part (the

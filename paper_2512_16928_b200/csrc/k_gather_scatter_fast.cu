@@ -99,7 +99,7 @@ __global__ void __launch_bounds__(256) k_gather_rows(const MatDesc* __restrict__
 }
 
 // unit = one selected row r in [0, k)
-template <int D>
+template <int D, typename WT>
 __global__ void __launch_bounds__(256) k_scatter_rows(const MatDesc* __restrict__ mats,
                                                       const int32_t* __restrict__ list_mats,
                                                       const int32_t* __restrict__ list_prefix, int n_list,
@@ -115,13 +115,12 @@ __global__ void __launch_bounds__(256) k_scatter_rows(const MatDesc* __restrict_
     if (bad[mi]) continue;
     const int r = u - list_prefix[li];
     const __half* xrow = reinterpret_cast<const __half*>(md.final_in_x1 ? md.X1 : md.X0) + (int64_t)r * md.q_pad;
-    float* wrow = md.W + (int64_t)md.sel[r] * md.ld;
+    WT* wrow = reinterpret_cast<WT*>(md.W) + (int64_t)md.sel[r] * md.ld;
     float* orow = md.O_out ? md.O_out + (int64_t)r * md.cols : nullptr;
     const float sc = (lr_dev ? __ldg(lr_dev) : lr) * md.update_scale;
     const int n = (int)md.cols;
     if (md.vec4) {
       const int n4 = n >> 2;
-      float4* w4 = reinterpret_cast<float4*>(wrow);
       const uint2* x4 = reinterpret_cast<const uint2*>(xrow);
       int j = lane;
       for (; j + 32 * (D - 1) < n4; j += 32 * D) {
@@ -129,7 +128,7 @@ __global__ void __launch_bounds__(256) k_scatter_rows(const MatDesc* __restrict_
         uint2 o[D];
 #pragma unroll
         for (int q = 0; q < D; ++q) {
-          w[q] = w4[j + 32 * q];
+          w[q] = ld_w4(wrow, j + 32 * q);
           o[q] = x4[j + 32 * q];
         }
 #pragma unroll
@@ -138,7 +137,7 @@ __global__ void __launch_bounds__(256) k_scatter_rows(const MatDesc* __restrict_
           const __half2 hi = *reinterpret_cast<const __half2*>(&o[q].y);
           const float o0 = __low2float(lo), o1 = __high2float(lo), o2 = __low2float(hi), o3 = __high2float(hi);
           w[q].x -= sc * o0; w[q].y -= sc * o1; w[q].z -= sc * o2; w[q].w -= sc * o3;
-          w4[j + 32 * q] = w[q];
+          st_w4(wrow, j + 32 * q, w[q]);
           if (orow) {
             const int c = 4 * (j + 32 * q);
             orow[c] = o0; orow[c + 1] = o1; orow[c + 2] = o2; orow[c + 3] = o3;
@@ -146,26 +145,26 @@ __global__ void __launch_bounds__(256) k_scatter_rows(const MatDesc* __restrict_
         }
       }
       for (; j < n4; j += 32) {
-        float4 w = w4[j];
+        float4 w = ld_w4(wrow, j);
         const uint2 o = x4[j];
         const __half2 lo = *reinterpret_cast<const __half2*>(&o.x);
         const __half2 hi = *reinterpret_cast<const __half2*>(&o.y);
         const float o0 = __low2float(lo), o1 = __high2float(lo), o2 = __low2float(hi), o3 = __high2float(hi);
         w.x -= sc * o0; w.y -= sc * o1; w.z -= sc * o2; w.w -= sc * o3;
-        w4[j] = w;
+        st_w4(wrow, j, w);
         if (orow) {
           orow[4 * j] = o0; orow[4 * j + 1] = o1; orow[4 * j + 2] = o2; orow[4 * j + 3] = o3;
         }
       }
       for (int c = 4 * n4 + lane; c < n; c += 32) {
         const float o = __half2float(xrow[c]);
-        wrow[c] -= sc * o;
+        st_w(wrow + c, ld_w(wrow + c) - sc * o);
         if (orow) orow[c] = o;
       }
     } else {
       for (int c = lane; c < n; c += 32) {
         const float o = __half2float(xrow[c]);
-        wrow[c] -= sc * o;
+        st_w(wrow + c, ld_w(wrow + c) - sc * o);
         if (orow) orow[c] = o;
       }
     }
@@ -336,7 +335,7 @@ __global__ void __launch_bounds__(256) k_gather_cols_t(const MatDesc* __restrict
 size_t cols_t_smem_bytes(int k, int mask_words) { return 8 * (size_t)mask_words + (size_t)kSlab * (k + 8) * 2; }
 static int mask_words_for(int64_t max_n) { return (int)((((max_n + 31) / 32) + 3) / 4 * 4); }
 
-template <int U>
+template <int U, typename WT>
 __global__ void __launch_bounds__(256, 4) k_scatter_cols_idx(const MatDesc* __restrict__ mats,
                                                              const int32_t* __restrict__ list_mats,
                                                              const int32_t* __restrict__ list_prefix, int n_list,
@@ -347,7 +346,9 @@ __global__ void __launch_bounds__(256, 4) k_scatter_cols_idx(const MatDesc* __re
 void launch_fast_paths_attrs() {
   const int mx = (int)cols_t_smem_bytes(kMaxColK, kMaskWords);
   cudaFuncSetAttribute(k_gather_cols_t, cudaFuncAttributeMaxDynamicSharedMemorySize, mx);
-  cudaFuncSetAttribute(k_scatter_cols_idx<8>, cudaFuncAttributeMaxDynamicSharedMemorySize,
+  cudaFuncSetAttribute(k_scatter_cols_idx<8, float>, cudaFuncAttributeMaxDynamicSharedMemorySize,
+                       4 * kMaxColKScatter + 8 * (kMaxColKScatter + 8) * 2);
+  cudaFuncSetAttribute(k_scatter_cols_idx<8, __nv_bfloat16>, cudaFuncAttributeMaxDynamicSharedMemorySize,
                        4 * kMaxColKScatter + 8 * (kMaxColKScatter + 8) * 2);
 }
 
@@ -356,7 +357,7 @@ void launch_fast_paths_attrs() {
 // with U independent loads in flight.  Same units (32-row slabs), same staged O tile and the
 // arithmetic w -= sc * o; O(k) work per row (a whole-row streaming variant with a column
 // bitmask, O(n) per row, measured slower and was removed: DESIGN.md §6).
-template <int U>
+template <int U, typename WT>
 __global__ void __launch_bounds__(256, 4) k_scatter_cols_idx(const MatDesc* __restrict__ mats,
                                                              const int32_t* __restrict__ list_mats,
                                                              const int32_t* __restrict__ list_prefix, int n_list,
@@ -400,7 +401,7 @@ __global__ void __launch_bounds__(256, 4) k_scatter_cols_idx(const MatDesc* __re
         const int64_t i = (int64_t)i0 + il;
         if (i >= md.rows) break;
         const __half* trow = tile + il * ldt;
-        float* wrow = md.W + i * md.ld;
+        WT* wrow = reinterpret_cast<WT*>(md.W) + i * md.ld;
         float* orow = md.O_out ? md.O_out + i * k : nullptr;
         for (int r0 = lane; r0 < k; r0 += 32 * U) {
           int c[U];
@@ -409,7 +410,7 @@ __global__ void __launch_bounds__(256, 4) k_scatter_cols_idx(const MatDesc* __re
           for (int q = 0; q < U; ++q) {
             const int r = r0 + 32 * q;
             c[q] = r < k ? ssel[r] : 0;
-            if (r < k) w[q] = wrow[c[q]];
+            if (r < k) w[q] = ld_w(wrow + c[q]);
           }
 #pragma unroll
           for (int q = 0; q < U; ++q) {
@@ -417,7 +418,7 @@ __global__ void __launch_bounds__(256, 4) k_scatter_cols_idx(const MatDesc* __re
             if (r < k) {
               const float o = __half2float(trow[r]);
               w[q] -= sc * o;
-              wrow[c[q]] = w[q];
+              st_w(wrow + c[q], w[q]);
               if (orow) orow[r] = o;
             }
           }
@@ -433,22 +434,29 @@ void launch_gather_rows(int blocks, cudaStream_t s, const MatDesc* mats, const i
   // 8 float4 loads in flight per lane (measured 1% over 4 on the 1B set)
   k_gather_rows<8><<<blocks, 256, 0, s>>>(mats, lm, lp, nl, units, bad, mu);
 }
-void launch_scatter_rows(int blocks, cudaStream_t s, const MatDesc* mats, const int32_t* lm, const int32_t* lp, int nl,
-                         int units, const int32_t* bad, float lr, const float* lr_dev) {
-  k_scatter_rows<8><<<blocks, 256, 0, s>>>(mats, lm, lp, nl, units, bad, lr, lr_dev);
+void launch_scatter_rows(bool w_bf16, int blocks, cudaStream_t s, const MatDesc* mats, const int32_t* lm,
+                         const int32_t* lp, int nl, int units, const int32_t* bad, float lr, const float* lr_dev) {
+  if (w_bf16)
+    k_scatter_rows<8, __nv_bfloat16><<<blocks, 256, 0, s>>>(mats, lm, lp, nl, units, bad, lr, lr_dev);
+  else
+    k_scatter_rows<8, float><<<blocks, 256, 0, s>>>(mats, lm, lp, nl, units, bad, lr, lr_dev);
 }
 void launch_gather_cols_t(int blocks, int max_k, int64_t max_n, cudaStream_t s, const MatDesc* mats, const int32_t* lm,
                           const int32_t* lp, int nl, int units, const int32_t* bad, float mu) {
   const int mw = mask_words_for(max_n);
   k_gather_cols_t<<<blocks, 256, cols_t_smem_bytes(max_k, mw), s>>>(mats, lm, lp, nl, units, bad, mu, mw);
 }
-void launch_scatter_cols_t(int blocks, int max_k, int64_t max_n, cudaStream_t s, const MatDesc* mats,
+void launch_scatter_cols_t(bool w_bf16, int blocks, int max_k, int64_t max_n, cudaStream_t s, const MatDesc* mats,
                            const int32_t* lm, const int32_t* lp, int nl, int units, const int32_t* bad, float lr,
                            const float* lr_dev) {
   const int slab_h = max_k <= 512 ? 32 : (max_k <= 1024 ? 16 : 8);
   const size_t smem = 4 * (size_t)((max_k + 3) & ~3) + (size_t)slab_h * (max_k + 8) * 2;
   (void)max_n;
-  k_scatter_cols_idx<8><<<blocks, 256, smem, s>>>(mats, lm, lp, nl, units, bad, lr, lr_dev, max_k, slab_h);
+  if (w_bf16)
+    k_scatter_cols_idx<8, __nv_bfloat16><<<blocks, 256, smem, s>>>(mats, lm, lp, nl, units, bad, lr, lr_dev, max_k,
+                                                                   slab_h);
+  else
+    k_scatter_cols_idx<8, float><<<blocks, 256, smem, s>>>(mats, lm, lp, nl, units, bad, lr, lr_dev, max_k, slab_h);
 }
 
 }  // namespace dion2

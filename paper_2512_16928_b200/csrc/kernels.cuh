@@ -46,8 +46,10 @@ constexpr int kTileB = 64;   // S cols per gather/scatter tile
 void launch_gather_decay(bool x16, int blocks, cudaStream_t s, const MatDesc* mats, const int32_t* tile_prefix_mats,
                          int n_mats, int total_tiles, const int32_t* bad, int decay, float mu);
 // lr_dev (optional): eta read on the device at run time (CUDA graphs under a schedule), else lr
-void launch_scatter_update(bool x16, int blocks, cudaStream_t s, const MatDesc* mats, const int32_t* tile_prefix_mats,
-                           int n_mats, int total_tiles, const int32_t* bad, float lr, const float* lr_dev);
+// w_bf16: W stored as bf16 (dion2_config.w_dtype), the update computed in fp32 and rounded once
+void launch_scatter_update(bool x16, bool w_bf16, int blocks, cudaStream_t s, const MatDesc* mats,
+                           const int32_t* tile_prefix_mats, int n_mats, int total_tiles, const int32_t* bad, float lr,
+                           const float* lr_dev);
 __global__ void k_norm_finalize(const MatDesc* __restrict__ mats, int n_mats, float eps);
 
 // streaming fast paths (k_gather_scatter_fast.cu): rows mode X = S, cols mode X = S^T
@@ -61,12 +63,12 @@ void launch_gather_rows(int blocks, cudaStream_t s, const MatDesc* mats, const i
 // TMA-staged rows gather (k_gather_tma.cu): 16-B aligned rows, n % 8 == 0; stages 4 or 6
 void launch_gather_rows_tma(int stages, int blocks_per_sm_cap, cudaStream_t s, const MatDesc* mats, const int32_t* lm,
                             const int32_t* lp, int nl, int units, const int32_t* bad, float mu, int sms);
-void launch_scatter_rows(int blocks, cudaStream_t s, const MatDesc* mats, const int32_t* lm, const int32_t* lp, int nl,
-                         int units, const int32_t* bad, float lr, const float* lr_dev);
+void launch_scatter_rows(bool w_bf16, int blocks, cudaStream_t s, const MatDesc* mats, const int32_t* lm,
+                         const int32_t* lp, int nl, int units, const int32_t* bad, float lr, const float* lr_dev);
 // max_k / max_n: largest k and column count over the matrices of the list (sizes the smem)
 void launch_gather_cols_t(int blocks, int max_k, int64_t max_n, cudaStream_t s, const MatDesc* mats, const int32_t* lm,
                           const int32_t* lp, int nl, int units, const int32_t* bad, float mu);
-void launch_scatter_cols_t(int blocks, int max_k, int64_t max_n, cudaStream_t s, const MatDesc* mats,
+void launch_scatter_cols_t(bool w_bf16, int blocks, int max_k, int64_t max_n, cudaStream_t s, const MatDesc* mats,
                            const int32_t* lm, const int32_t* lp, int nl, int units, const int32_t* bad, float lr,
                            const float* lr_dev);
 __global__ void k_full_decay(const MatDesc* __restrict__ mats, int n_mats, const int32_t* __restrict__ bad, float mu);

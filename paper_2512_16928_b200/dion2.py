@@ -45,7 +45,7 @@ class Dion2Config(ctypes.Structure):
                 ("ns_eps", ctypes.c_float), ("axis", ctypes.c_int32), ("select", ctypes.c_int32),
                 ("precision", ctypes.c_int32), ("grad_dtype", ctypes.c_int32), ("decay_mode", ctypes.c_int32),
                 ("scale_mode", ctypes.c_int32), ("seed", ctypes.c_uint64), ("step", ctypes.c_uint64),
-                ("ns_form", ctypes.c_int32), ("reserved0", ctypes.c_int32)]
+                ("ns_form", ctypes.c_int32), ("reserved0", ctypes.c_int32), ("w_dtype", ctypes.c_int32)]
 
 
 class Dion2Shard(ctypes.Structure):
@@ -113,9 +113,11 @@ def make_config(alpha: float = 0.25, mu: float = 0.95, lr: float = 0.02, ns_step
                 ns_coeffs: Optional[Sequence[Tuple[float, float, float]]] = None, ns_eps: float = 1e-7,
                 axis: str = "auto", precision: str = "bf16", grad_dtype: Optional[torch.dtype] = None,
                 decay_mode: int = 0, scale_mode: int = 0, select: str = "l1", seed: int = 0,
-                step: int = 0, ns_form: str = "auto", lr_device: bool = False) -> Dion2Config:
-    """ns_form: "auto" | "direct" | "gram" -- how the bf16 Newton-Schulz map is evaluated
-    (include/dion2.h dion2_ns_form, reading R23)."""
+                step: int = 0, ns_form: str = "auto", lr_device: bool = False,
+                w_dtype: Optional[torch.dtype] = None) -> Dion2Config:
+    """ns_form: "auto" | "direct" | "gram" -- how the tensor-core Newton-Schulz map is evaluated
+    (include/dion2.h dion2_ns_form, readings R23, R24).  w_dtype: torch.bfloat16 for
+    bf16 weights (the update is computed in fp32 and rounded once), else fp32."""
     cfg = Dion2Config()
     _lib().dion2_config_init(ctypes.byref(cfg))
     cfg.alpha, cfg.mu, cfg.lr, cfg.ns_steps, cfg.ns_eps = alpha, mu, lr, ns_steps, ns_eps
@@ -127,6 +129,7 @@ def make_config(alpha: float = 0.25, mu: float = 0.95, lr: float = 0.02, ns_step
     cfg.axis = AXIS[axis]
     cfg.precision = PRECISION[precision]
     cfg.grad_dtype = 1 if grad_dtype == torch.bfloat16 else 0
+    cfg.w_dtype = 1 if w_dtype == torch.bfloat16 else 0
     cfg.decay_mode, cfg.scale_mode = decay_mode, scale_mode
     cfg.select = SELECT[select]
     cfg.seed, cfg.step = seed, step
@@ -161,7 +164,9 @@ def describe(Ws: Sequence[torch.Tensor], Ms: Sequence[torch.Tensor], Gs: Sequenc
     arr = (Dion2Matrix * n)()
     gdt = Gs[0].dtype
     for i, (W, M, G) in enumerate(zip(Ws, Ms, Gs)):
-        _check_tensor(W, "W", torch.float32)
+        _check_tensor(W, "W", Ws[0].dtype)
+        if W.dtype not in (torch.float32, torch.bfloat16):
+            raise ValueError("W must be float32 or bfloat16")
         mt = bool(m_transposed[i]) if m_transposed is not None else False
         stt = bool(storage_transposed[i]) if storage_transposed is not None else False
         arr[i].storage_transposed = 1 if stt else 0
@@ -319,6 +324,7 @@ class Dion2:
             storage_transposed = self.storage_transposed
         arr, gdt = describe(Ws, Ms, Gs, sel_out, O_out, m_transposed, storage_transposed)
         kw.setdefault("grad_dtype", gdt)
+        kw.setdefault("w_dtype", Ws[0].dtype)
         cfg = make_config(**kw)
         dev = Ws[0].device
         ws = self.workspace(arr, len(Ws), cfg, dev)
@@ -434,7 +440,9 @@ def _shards(shapes, Ws=None, Ms=None, Gs=None, sels=None, m_transposed=None):
         arr[i].ldm = 1 << 40
         if Ws is not None:
             W = Ws[i]
-            _check_tensor(W, "W shard", torch.float32)
+            _check_tensor(W, "W shard", Ws[0].dtype)
+            if W.dtype not in (torch.float32, torch.bfloat16):
+                raise ValueError("W shard must be float32 or bfloat16")
             if mt:
                 _check_tensor(Ms[i], "M shard (transposed)", torch.float32)
                 if tuple(Ms[i].shape) != (W.shape[1], W.shape[0]):
@@ -511,6 +519,7 @@ class Dion2Dist:
         kw = dict(self.cfg_kw)
         kw.update(override)
         kw.setdefault("grad_dtype", Gs[0].dtype)
+        kw.setdefault("w_dtype", Ws[0].dtype)
         cfg = make_config(**kw)
         dev = Ws[0].device
         need = self.info["workspace_bytes"]
@@ -553,6 +562,7 @@ class Dion2Loopback:
         kw = dict(self.cfg_kw)
         kw.update(override)
         kw.setdefault("grad_dtype", Gs[0][0].dtype)
+        kw.setdefault("w_dtype", Ws[0][0].dtype)
         cfg = make_config(**kw)
         n, P = len(self.shapes), self.world
         dev = Ws[0][0].device
@@ -599,17 +609,19 @@ class Dion2DpSync:
         self._ws: List[torch.Tensor] = []
         self.last_comm_bytes = 0
 
-    def _cfg(self, Gs0, override):
+    def _cfg(self, Gs0, override, W0=None):
         kw = dict(self.cfg_kw)
         kw.update(override)
         kw.setdefault("grad_dtype", Gs0.dtype)
+        if W0 is not None:
+            kw.setdefault("w_dtype", W0.dtype)
         return make_config(**kw)
 
     def step(self, Ws, Ms, Gs, sel_out=None, stream=None, **override):
         """NCCL mode: this rank's full matrices.  Loopback mode: [world][n] lists."""
         if self.loopback:
             n, P = len(Ws[0]), self.world
-            cfg = self._cfg(Gs[0][0], override)
+            cfg = self._cfg(Gs[0][0], override, Ws[0][0])
             parts = [describe(Ws[r], Ms[r], Gs[r], sel_out[r] if sel_out is not None else None,
                               m_transposed=self.m_transposed, storage_transposed=self.storage_transposed)[0]
                      for r in range(P)]
@@ -620,7 +632,7 @@ class Dion2DpSync:
             dev = Ws[0][0].device
         else:
             n, P = len(Ws), self.world
-            cfg = self._cfg(Gs[0], override)
+            cfg = self._cfg(Gs[0], override, Ws[0])
             arr, _ = describe(Ws, Ms, Gs, sel_out, m_transposed=self.m_transposed,
                               storage_transposed=self.storage_transposed)
             dev = Ws[0].device

@@ -564,3 +564,42 @@ def test_status_is_stream_scoped():
     assert opt.status() == (0, -1)
     assert not other.query()  # the other stream's kernel has not finished
     other.synchronize()
+
+
+@pytest.mark.parametrize("form", ["auto", "direct"])
+def test_bf16_weights(form):
+    """f4 bf16-W variant (dion2_config.w_dtype = BF16): W held in bf16, the update computed in
+    fp32 and rounded to nearest once.  Per-step parity: the oracle starts every
+    step from the GPU's bf16 W (exact in fp64) and M; the GPU's new W must sit within the bf16
+    rounding of the oracle's new W (half an ulp per element) plus the 2e-2 NS tolerance on the
+    update, and unselected rows / columns of W must be bit-identical."""
+    shapes = [(512, 1024), (1024, 512), (300, 520)]
+    cfg = O.OracleConfig(alpha=0.25, mu=float(np.float32(0.95)), lr=float(np.float32(0.02)))
+    Wb = [torch.from_numpy(gen_w0(m, n, 5, i)).cuda().to(torch.bfloat16) for i, (m, n) in enumerate(shapes)]
+    Ms = [torch.zeros(m, n, device="cuda") for (m, n) in shapes]
+    ks = [O.select_count(0.25, min(m, n)) for (m, n) in shapes]
+    opt = Dion2(alpha=0.25, ns_form=form)
+    for t in range(3):
+        G = [gen_grad(m, n, 5, i, t, row_scaled=True) for i, (m, n) in enumerate(shapes)]
+        W_before = [w.double().cpu().numpy() for w in Wb]
+        M_before = [mm.double().cpu().numpy() for mm in Ms]
+        sel = [torch.empty(k, dtype=torch.int32, device="cuda") for k in ks]
+        opt.step(Wb, Ms, [torch.from_numpy(g).cuda() for g in G], sel_out=sel)
+        torch.cuda.synchronize()
+        for i in range(len(shapes)):
+            Wr, Mr = W_before[i].copy(), M_before[i].copy()
+            K, _, ax = O.dion2_step(Wr, Mr, G[i].astype(np.float64), cfg, force_K=sel[i].cpu().numpy())
+            Kref = O.select_l1(O.l1_scores(M_before[i] + G[i], ax), ks[i])
+            assert np.array_equal(K, Kref)
+            wg = Wb[i].double().cpu().numpy()
+            d_ref = Wr - W_before[i]
+            ulp = np.exp2(np.floor(np.log2(np.maximum(np.abs(Wr), 1e-30))) - 7)
+            bound = np.linalg.norm(0.5 * ulp[d_ref != 0]) + 2e-2 * np.linalg.norm(d_ref)
+            assert np.linalg.norm(wg - Wr) <= bound, (i, t, np.linalg.norm(wg - Wr), bound)
+            unsel = np.ones(shapes[i][0] if ax == O.AXIS_ROWS else shapes[i][1], bool)
+            unsel[K] = False
+            if ax == O.AXIS_ROWS:
+                assert np.array_equal(wg[unsel], W_before[i][unsel])
+            else:
+                assert np.array_equal(wg[:, unsel], W_before[i][:, unsel])
+            assert np.abs(Ms[i].double().cpu().numpy() - Mr).max() <= 1e-6 * np.abs(Mr).max()
