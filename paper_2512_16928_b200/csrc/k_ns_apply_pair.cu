@@ -136,6 +136,16 @@ __global__ void __cluster_dims__(2, 1, 1) __launch_bounds__(kThreads, 1)
         for (int kb = 0; kb < G.k_blocks; ++kb)
           tma_load_3d_pair(sA + kb * kABlk, &P.mapA[k.group], leader_afull, kb * kBK, k.tm * 256 + (int)rank * 128, k.z);
         for (int tn = k.tn0; tn < k.tn0 + k.len; ++tn) {
+          // L2 prefetch of the next column block's B (this CTA's half): the ring holds only
+          // 4 k-blocks (~1.6 us of MMA), less than a DRAM round trip under load, so the loads
+          // of the next tile should hit L2 (ncu: the MMA waited on its full barriers while the
+          // producer sat on a full ring, DRAM at 49%)
+          if (tn + 1 < k.tn0 + k.len && !G.pieces_load) {
+            for (int kb = 0; kb < G.k_blocks; ++kb)
+#pragma unroll
+              for (int j = 0; j < 2; ++j)
+                tma_prefetch_3d(&P.mapB[k.group], (tn + 1) * 256 + (int)rank * 128 + j * 64, kb * kBK, k.z);
+          }
           for (int kb = 0; kb < G.k_blocks; ++kb) {
             mbar_wait(&empty_bar[stage], phase ^ 1);
             uint8_t* sb = sB + stage * kBB;

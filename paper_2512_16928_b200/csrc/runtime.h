@@ -2,6 +2,7 @@
 // and the distributed step (dion2_dist.cu).  Not part of the public ABI.
 #pragma once
 #include <cudaTypedefs.h>
+#include <nvtx3/nvToolsExt.h>  // header-only NVTX v3: phase ranges for nsys / ncu --nvtx
 
 #include <map>
 #include <memory>
@@ -136,6 +137,7 @@ struct Launcher {
   cudaEvent_t ev_a = nullptr;
   void begin(int phase) {
     cur_phase = phase;
+    nvtxRangePushA(kPhaseNames[phase]);  // one host range per launch, named by phase
     if (g_timing) {
       ev_a = take_event();
       cudaEventRecord(ev_a, s);
@@ -143,6 +145,7 @@ struct Launcher {
   }
   void end() {
     ++count;
+    nvtxRangePop();
     if (cudaPeekAtLastError() != cudaSuccess) {
       cudaGetLastError();
       err = DION2_ECUDA;

@@ -2,9 +2,11 @@
 
 BASELINE configs[1] (the 1B set, 144 matrices, alpha = 0.25) stepped exactly as bench.py
 times it: one batched call over all matrices, column-mode momentum stored transposed, the
-default (Gram-space) Newton-Schulz plan.  The oracle recomputes a sample of matrices one by
-one (each matrix's step depends only on its own W, M, G); properties that hold at any size
-are checked on every matrix:
+default (Gram-space, restarted, fp16) Newton-Schulz plan.  SURVEY 8(c.3)'s 10-step trajectory:
+the oracle follows a sample of matrices one at a time for all 10 steps (each matrix's step
+depends only on its own W, M, G), on Gaussian gradients and on gradients with a fixed rank-4
+spike (sigma_1 / median of the selected rows ~ 50-100, the momenta real training produces);
+properties that hold at any size are checked on every matrix at every step:
   * the selected set is strictly ascending, in range, of size k;
   * unselected rows/columns of W are bit-identical, unselected M == fp32(M + G) bitwise.
 """
@@ -42,7 +44,8 @@ def _state(shapes, mts, seed):
     return (W, M, G), Ws, Ms, Gs, gen
 
 
-def test_full_1b_set_sampled_parity_and_global_properties():
+@pytest.mark.parametrize("spike", [0.0, 100.0])
+def test_full_1b_set_trajectory(spike):
     shapes = layer_set_1b(24)
     assert len(shapes) == 144
     cfg = O.OracleConfig(alpha=float(np.float32(ALPHA)), mu=float(np.float32(0.95)), lr=float(np.float32(0.02)))
@@ -56,8 +59,16 @@ def test_full_1b_set_sampled_parity_and_global_properties():
     Wr = {i: W0[i].copy() for i in SAMPLE}
     Mr = {i: np.zeros(shapes[i]) for i in SAMPLE}
     ties = 0
-    for t in range(2):
+    spikes = []
+    if spike:  # a fixed rank-4 spike per matrix: G = Z + spike * sqrt(max(m, n)) U V^T (synth recipe)
+        for (m, n) in shapes:
+            u = torch.linalg.qr(torch.randn(m, 4, device="cuda", generator=gen))[0]
+            v = torch.linalg.qr(torch.randn(n, 4, device="cuda", generator=gen))[0]
+            spikes.append((spike * math.sqrt(max(m, n))) * (u @ v.T))
+    for t in range(10):
         Gf.normal_(0.0, 1.0, generator=gen)
+        for i, sp in enumerate(spikes):
+            Gs[i].add_(sp)
         Gc = {i: Gs[i].cpu().numpy().astype(np.float64) for i in SAMPLE}
         sel = [torch.empty(k, dtype=torch.int32, device="cuda") for k in ks]
         W_before, M_before = Wf.clone(), Mf.clone()
