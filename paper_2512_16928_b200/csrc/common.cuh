@@ -239,6 +239,18 @@ __device__ __forceinline__ void sts16(uint32_t addr, uint16_t v) {
 
 // ----------------------------------------------------------------------------- tcgen05
 
+// One lane of the (converged) warp: the MMA issuer runs as a whole warp with warp-uniform loop
+// state, so the descriptors stay in uniform registers and only the issue is predicated (a
+// lane-0-only issuer made the compiler wrap every tcgen05.mma in an R2UR / ELECT waterfall:
+// ~30 instructions per MMA, ncu round 2).
+__device__ __forceinline__ bool elect_one_sync() {
+  uint32_t pred = 0;
+  asm volatile(
+      "{\n\t.reg .pred P;\n\telect.sync _|P, 0xffffffff;\n\tselp.u32 %0, 1, 0, P;\n\t}"
+      : "=r"(pred));
+  return pred != 0;
+}
+
 __device__ __forceinline__ void tc_fence_before() { asm volatile("tcgen05.fence::before_thread_sync;" ::: "memory"); }
 __device__ __forceinline__ void tc_fence_after() { asm volatile("tcgen05.fence::after_thread_sync;" ::: "memory"); }
 

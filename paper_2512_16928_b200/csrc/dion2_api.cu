@@ -180,7 +180,7 @@ std::string plan_key(const dion2_matrix* mats, int n, const dion2_config* c, voi
 std::string env_key() {
   std::string k;
   for (const char* v : {"DION2_NS_PAIR", "DION2_NS_SYM", "DION2_NS_SERPENTINE", "DION2_NS_UPPER",
-                        "DION2_GRAM_SPLITK"}) {
+                        "DION2_GRAM_SPLITK", "DION2_GRAM_PF"}) {
     const char* e = getenv(v);
     k.append(e ? e : "-");
     k.push_back('|');
@@ -345,6 +345,12 @@ int build_layout(Plan& P, const dion2_matrix* mats, int n, const dion2_config* c
 }
 
 
+// L2 prefetch distance (k-blocks) of the gram launches (DION2_GRAM_PF, A/B only; 0 = off)
+static int gram_prefetch_ahead() {
+  const char* e = getenv("DION2_GRAM_PF");
+  return e ? std::max(0, atoi(e)) : 8;
+}
+
 // Kind-5 launches (resident-A pair apply) count work in chunks of up to L consecutive 256-column
 // blocks of one 256-row block: L = 8, halved while the launch has fewer than two chunks per CTA pair.
 static void apply_chunks(NsParams& np) {
@@ -483,6 +489,7 @@ static int append_gram_space_launches(Plan& P, const dion2_config* c, void* ws, 
       np.b_is_a = np.b_kmajor ? 1 : 0;
       for (int j = 0; j < np.ngroups; ++j) np.b_is_a &= np.g[j].a == np.g[j].b ? 1 : 0;
       if (L.kind == 5) apply_chunks(np);
+      if (phase == PH_GRAM) np.pf_ahead = gram_prefetch_ahead();
       P.ns_launches.push_back(L);
     }
     return DION2_OK;
@@ -789,6 +796,7 @@ int build_device_plan(Plan& P, const dion2_matrix* mats, const dion2_config* c, 
           np.b_is_a = np.b_kmajor ? 1 : 0;
           for (int j = 0; j < np.ngroups; ++j) np.b_is_a &= np.g[j].a == np.g[j].b ? 1 : 0;
           if (L.kind == 5) apply_chunks(np);
+          if (ph == PH_GRAM) np.pf_ahead = gram_prefetch_ahead();
           if (P.bf16_ns) {
             P.ns_launches.push_back(L);
           } else {

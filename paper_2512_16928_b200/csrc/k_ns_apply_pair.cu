@@ -168,14 +168,17 @@ __global__ void __cluster_dims__(2, 1, 1) __launch_bounds__(kThreads, 1)
       }
     }
   } else if (warp == 1) {
-    if (lane == 0 && rank == 0) {
-      // ---------------- MMA issuer (leader CTA)
+    if (rank == 0) {
+      // ---------------- MMA issuer (leader CTA; the whole warp runs the loop, one lane issues)
       const uint32_t idesc = kIdescMN & (p.in_f16 ? ~kIdescAbFmt : ~0u);
+      // descriptors of offset 0; a k-step / stage adds its byte offset >> 4 to the address field
+      const uint64_t adesc0 = umma_desc_sw128(smem_u32(sA), 16, 1024);
+      const uint64_t bdesc0 = umma_desc_sw128(smem_u32(sB), 64 * kBK * 2, 1024);
       int stage = 0, chunk = 0, it = 0;
       uint32_t phase = 0;
       for (int ci = cid; ci < nchunks; ci += ncl, ++chunk) {
         const Chunk k = decode_chunk(p, ci);
-        const NsGroup& G = p.g[k.group];
+        const int kblocks = p.g[k.group].k_blocks;
         mbar_wait(afull_bar, chunk & 1);
         tc_fence_after();
         for (int tn = k.tn0; tn < k.tn0 + k.len; ++tn, ++it) {
@@ -184,23 +187,24 @@ __global__ void __cluster_dims__(2, 1, 1) __launch_bounds__(kThreads, 1)
           mbar_wait(&tempty_bar[acc], acc_phase ^ 1);
           tc_fence_after();
           const uint32_t tmem_d = tmem_base + acc * 256;
-          for (int kb = 0; kb < G.k_blocks; ++kb) {
+          for (int kb = 0; kb < kblocks; ++kb) {
             mbar_wait(&full_bar[stage], phase);
             tc_fence_after();
-            const uint32_t a_addr = smem_u32(sA + kb * kABlk);
-            const uint32_t b_addr = smem_u32(sB + stage * kBB);
+            if (elect_one_sync()) {
 #pragma unroll
-            for (int kk = 0; kk < kBK / 16; ++kk) {
-              const uint64_t adesc = umma_desc_sw128(a_addr + kk * 32, 16, 1024);
-              const uint64_t bdesc = umma_desc_sw128(b_addr + kk * 2048, 64 * kBK * 2, 1024);
-              umma_bf16_ss_pair(tmem_d, adesc, bdesc, idesc, (kb | kk) != 0);
+              for (int kk = 0; kk < kBK / 16; ++kk)
+                umma_bf16_ss_pair(tmem_d, adesc0 + (uint64_t)((kb * kABlk + kk * 32) >> 4),
+                                  bdesc0 + (uint64_t)((stage * kBB + kk * 2048) >> 4), idesc, (kb | kk) != 0);
+              umma_commit_pair(&empty_bar[stage]);
             }
-            umma_commit_pair(&empty_bar[stage]);
+            __syncwarp();
             if (++stage == kStages) { stage = 0; phase ^= 1; }
           }
-          umma_commit_pair(&tfull_bar[acc]);
+          if (elect_one_sync()) umma_commit_pair(&tfull_bar[acc]);
+          __syncwarp();
         }
-        umma_commit_pair(aempty_bar);  // this chunk's MMAs have read the resident A
+        if (elect_one_sync()) umma_commit_pair(aempty_bar);  // this chunk's MMAs have read the resident A
+        __syncwarp();
       }
     }
   } else {

@@ -131,36 +131,43 @@ __global__ void __launch_bounds__(192, 1) k_ns_gemm_tc(const __grid_constant__ N
       }
     }
   } else if (warp == 1) {
-    if (lane == 0) {
-      // ---------------- MMA issuer
+    {
+      // ---------------- MMA issuer (the whole warp runs the loop, one lane issues)
       const uint32_t idesc = (p.b_kmajor ? kIdescK : kIdescMN) & (p.in_f16 ? ~kIdescAbFmt1 : ~0u);
+      const uint32_t ring = smem_u32(smem);
+      const uint64_t dK = umma_desc_sw128(ring, 16, 1024);
+      const uint64_t dMN = umma_desc_sw128(ring, 64 * kBK * 2, 1024);
       int stage = 0;
       uint32_t phase = 0;
       int it = 0;
       for (int t = blockIdx.x; t < p.total_tiles; t += gridDim.x, ++it) {
         const TileCoord c = decode_tile(p, t);
-        const NsGroup& G = p.g[c.group];
+        const int kblocks = p.g[c.group].k_blocks;
         const int acc = it & 1;
         const uint32_t acc_phase = (it >> 1) & 1;
         mbar_wait(&tempty_bar[acc], acc_phase ^ 1);
         tc_fence_after();
         const uint32_t tmem_d = tmem_base + acc * BN;
-        for (int kb = 0; kb < G.k_blocks; ++kb) {
+        for (int kb = 0; kb < kblocks; ++kb) {
           mbar_wait(&full_bar[stage], phase);
           tc_fence_after();
-          const uint32_t a_addr = smem_u32(smem + stage * kStageBytes);
-          const uint32_t b_addr = a_addr + kABytes;
+          const uint32_t a_off = stage * kStageBytes;
+          const uint32_t b_off = a_off + kABytes;
+          if (elect_one_sync()) {
 #pragma unroll
-          for (int k = 0; k < kBK / 16; ++k) {
-            const uint64_t adesc = umma_desc_sw128(a_addr + k * 32, 16, 1024);
-            const uint64_t bdesc = p.b_kmajor ? umma_desc_sw128(b_addr + k * 32, 16, 1024)
-                                              : umma_desc_sw128(b_addr + k * 2048, 64 * kBK * 2, 1024);
-            umma_bf16_ss(tmem_d, adesc, bdesc, idesc, (kb | k) != 0);
+            for (int k = 0; k < kBK / 16; ++k) {
+              const uint64_t adesc = dK + (uint64_t)((a_off + k * 32) >> 4);
+              const uint64_t bdesc = p.b_kmajor ? dK + (uint64_t)((b_off + k * 32) >> 4)
+                                                : dMN + (uint64_t)((b_off + k * 2048) >> 4);
+              umma_bf16_ss(tmem_d, adesc, bdesc, idesc, (kb | k) != 0);
+            }
+            umma_commit(&empty_bar[stage]);
           }
-          umma_commit(&empty_bar[stage]);
+          __syncwarp();
           if (++stage == S) { stage = 0; phase ^= 1; }
         }
-        umma_commit(&tfull_bar[acc]);
+        if (elect_one_sync()) umma_commit(&tfull_bar[acc]);
+        __syncwarp();
       }
     }
   } else {

@@ -164,6 +164,11 @@ __global__ void __cluster_dims__(2, 1, 1) __launch_bounds__(kPairThreads, 1)
           const int pr = G.pieces_load ? (kb * kBK) / G.pieces_qo : 0;
           const int pc = G.pieces_load ? kb * kBK - pr * G.pieces_qo : kb * kBK;
           const CUtensorMap* pmap = G.pieces_load ? &P.mapP[c.group][pr] : nullptr;
+          if (p.pf_ahead && kb + p.pf_ahead < kb1 && !G.pieces_load) {
+            const int kp = (kb + p.pf_ahead) * kBK;
+            tma_prefetch_3d(&P.mapA[c.group], kp, c.tm * 256 + (int)rank * 128, c.z);
+            if (!same) tma_prefetch_3d(&P.mapB[c.group], kp, c.tn * 256 + (int)rank * 128, c.z);
+          }
           if (!at) {
             tma_load_3d_pair(sa, pmap ? pmap : &P.mapA[c.group], leader_full, pc, c.tm * 256 + (int)rank * 128, c.z);
           } else {
@@ -191,53 +196,51 @@ __global__ void __cluster_dims__(2, 1, 1) __launch_bounds__(kPairThreads, 1)
       }
     }
   } else if (warp == 1) {
-    if (lane == 0 && rank == 0) {
-      // ---------------- MMA issuer (leader CTA)
+    if (rank == 0) {
+      // ---------------- MMA issuer (leader CTA; the whole warp runs the loop, one lane issues)
       const uint32_t idesc0 = (p.b_kmajor ? kIdescK : kIdescMN) & (p.in_f16 ? ~kIdescAbFmt : ~0u);
+      // descriptors of the stage ring's offset 0 (K-major: 16 B LBO; MN-major: 64-column panels);
+      // a stage / k-step adds its byte offset >> 4 to the 14-bit address field
+      const uint32_t ring = smem_u32(smem);
+      const uint64_t dK = umma_desc_sw128(ring, 16, 1024);
+      const uint64_t dMN = umma_desc_sw128(ring, 64 * kBK * 2, 1024);
       int stage = 0;
       uint32_t phase = 0;
       int it = 0;
       for (int w = cid; w < nwork; w += ncl, ++it) {
         const int t = w / SK, slice = w - (w / SK) * SK;
         const TileCoord c = decode_tile(p, t);
-        const NsGroup& G = p.g[c.group];
+        const int kblocks = p.g[c.group].k_blocks;
         const int acc = it & 1;
         const uint32_t acc_phase = (it >> 1) & 1;
         mbar_wait(&tempty_bar[acc], acc_phase ^ 1);
         tc_fence_after();
         const uint32_t tmem_d = tmem_base + acc * 256;
-        const int kb0 = slice * G.k_blocks / SK, kb1 = (slice + 1) * G.k_blocks / SK;
+        const int kb0 = slice * kblocks / SK, kb1 = (slice + 1) * kblocks / SK;
+        const bool same = p.b_is_a && c.tm == c.tn;
         for (int kb = kb0; kb < kb1; ++kb) {
           mbar_wait(&full_bar[stage], phase);
           tc_fence_after();
-          const uint32_t a_addr = smem_u32(smem + stage * kStage);
-          const uint32_t b_addr = (p.b_is_a && c.tm == c.tn) ? a_addr : a_addr + kAB;
-          if constexpr (!kSymIn) {
+          const uint32_t a_off = stage * kStage;
+          const uint32_t b_off = same ? a_off : a_off + kAB;
+          // sym_in: transposed (MN-major) operands of this k-block, as loaded by the producer
+          const bool at = kSymIn && ((kb * kBK) >> 8) < c.tm;
+          const bool bt = kSymIn ? (((kb * kBK) >> 8) < c.tn) : !p.b_kmajor;
+          const uint32_t idesc = kSymIn ? (idesc0 | (at ? (1u << 15) : 0u) | (bt ? (1u << 16) : 0u)) : idesc0;
+          if (elect_one_sync()) {
 #pragma unroll
             for (int k = 0; k < kBK / 16; ++k) {
-              const uint64_t adesc = umma_desc_sw128(a_addr + k * 32, 16, 1024);
-              const uint64_t bdesc = p.b_kmajor ? umma_desc_sw128(b_addr + k * 32, 16, 1024)
-                                                : umma_desc_sw128(b_addr + k * 2048, 64 * kBK * 2, 1024);
-              umma_bf16_ss_pair(tmem_d, adesc, bdesc, idesc0, (kb != kb0) || (k != 0));
-            }
-          } else {
-            // transposed (MN-major) operands of this k-block, as loaded by the producer
-            const bool at = ((kb * kBK) >> 8) < c.tm;
-            const bool bt = ((kb * kBK) >> 8) < c.tn;
-            const uint32_t idesc = idesc0 | (at ? (1u << 15) : 0u) | (bt ? (1u << 16) : 0u);
-#pragma unroll
-            for (int k = 0; k < kBK / 16; ++k) {
-              const uint64_t adesc = at ? umma_desc_sw128(a_addr + k * 2048, 64 * kBK * 2, 1024)
-                                        : umma_desc_sw128(a_addr + k * 32, 16, 1024);
-              const uint64_t bdesc = bt ? umma_desc_sw128(b_addr + k * 2048, 64 * kBK * 2, 1024)
-                                        : umma_desc_sw128(b_addr + k * 32, 16, 1024);
+              const uint64_t adesc = (at ? dMN : dK) + (uint64_t)((a_off + (at ? k * 2048 : k * 32)) >> 4);
+              const uint64_t bdesc = (bt ? dMN : dK) + (uint64_t)((b_off + (bt ? k * 2048 : k * 32)) >> 4);
               umma_bf16_ss_pair(tmem_d, adesc, bdesc, idesc, (kb != kb0) || (k != 0));
             }
+            umma_commit_pair(&empty_bar[stage]);
           }
-          umma_commit_pair(&empty_bar[stage]);
+          __syncwarp();
           if (++stage == S) { stage = 0; phase ^= 1; }
         }
-        umma_commit_pair(&tfull_bar[acc]);
+        if (elect_one_sync()) umma_commit_pair(&tfull_bar[acc]);
+        __syncwarp();
       }
     }
   } else {
