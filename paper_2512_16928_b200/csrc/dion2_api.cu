@@ -477,8 +477,7 @@ static int append_gram_space_launches(Plan& P, const dion2_config* c, void* ws, 
         } else {
           if (!make_map(&L.tc.mapB[j], e.b, K, g.p_pad, g.count, 64, 128)) return DION2_ECUDA;
         }
-        if (L.kind == 5 ? !make_map(&L.tc.mapD[j], e.out, G.out_ld, g.p_pad, g.count, 64, 32)
-                        : !make_map(&L.tc.mapD[j], e.out, G.out_ld, g.p_pad, g.count, 32, 32, CU_TENSOR_MAP_SWIZZLE_64B))
+        if (!make_map(&L.tc.mapD[j], e.out, G.out_ld, g.p_pad, g.count, 32, 32, CU_TENSOR_MAP_SWIZZLE_64B))
           return DION2_ECUDA;
         if (np.sym_in) {
           if (!make_map(&L.tc.mapAT[j], e.a, g.p_pad, g.p_pad, g.count, 64, 64)) return DION2_ECUDA;
@@ -788,9 +787,8 @@ int build_device_plan(Plan& P, const dion2_matrix* mats, const dion2_config* c, 
               }
             }
             (void)xel;
-            if (P.bf16_ns && (L.kind == 5 ? !make_map(&L.tc.mapD[j], G.out, G.out_ld, g.p_pad, g.count, 64, 32)
-                                          : !make_map(&L.tc.mapD[j], G.out, G.out_ld, g.p_pad, g.count, 32, 32,
-                                                      CU_TENSOR_MAP_SWIZZLE_64B)))
+            if (P.bf16_ns &&
+                !make_map(&L.tc.mapD[j], G.out, G.out_ld, g.p_pad, g.count, 32, 32, CU_TENSOR_MAP_SWIZZLE_64B))
               return DION2_ECUDA;
             G.tile_base = tiles;
             tiles += G.count * (sym ? G.m_tiles * (G.m_tiles + 1) / 2 : G.m_tiles * G.n_tiles);

@@ -17,7 +17,7 @@
 // Roles per CTA (320 threads): warp 0 TMA producer (A blocks on a chunk change, then the B
 // ring; completion counted on the leader's barriers), warp 1 TMEM allocator (both CTAs) + MMA
 // issuer (leader: tcgen05.mma.cta_group::2 256 x 256 x 16, fp16/bf16 -> fp32), warps 2-9
-// epilogue (TMEM -> scale -> 16-bit -> SWIZZLE_128B staging -> TMA store of 32 x 64 boxes; two 256-column TMEM
+// epilogue (TMEM -> scale -> 16-bit -> SWIZZLE_64B staging -> TMA store; two 256-column TMEM
 // accumulators so the epilogue of one tile overlaps the next tile's MMAs).
 #include "kernels.cuh"
 
@@ -227,43 +227,11 @@ __global__ void __cluster_dims__(2, 1, 1) __launch_bounds__(kThreads, 1)
       const uint32_t acc_phase = (it >> 1) & 1;
       mbar_wait(&tfull_bar[acc], acc_phase);
       tc_fence_after();
-      const int row = k.tm * 256 + (int)rank * 128 + lg * 32;
-      if (!G.pieces_store) {
-        // 64 columns per store: a 32 x 64 fp16 box (128 B per row, SWIZZLE_128B: 16-B chunk q of
-        // row r at q ^ (r & 7)) writes whole 128-B lines of X'
-        uint8_t* buf = stage_base + ew * 4096;
-#pragma unroll 1
-        for (int h = 0; h < 2; ++h) {
-          const int cc = c0 + 2 * h;  // first of the two 32-column chunks
-          float v0[32], v1[32];
-          tmem_ld_32x32b_x32(tmem_base + acc * 256 + cc * 32 + ((uint32_t)(lg * 32) << 16), v0);
-          tmem_ld_32x32b_x32(tmem_base + acc * 256 + (cc + 1) * 32 + ((uint32_t)(lg * 32) << 16), v1);
-          if (lane == 0) bulk_wait_read<0>();  // the previous store has read the buffer
-          __syncwarp();
-          uint32_t pk[32];
-#pragma unroll
-          for (int q = 0; q < 16; ++q) {
-            pk[q] = p.out_f16 ? pack2_h(ca * v0[2 * q], ca * v0[2 * q + 1]) : pack_bf16x2(ca * v0[2 * q], ca * v0[2 * q + 1]);
-            pk[16 + q] = p.out_f16 ? pack2_h(ca * v1[2 * q], ca * v1[2 * q + 1])
-                                   : pack_bf16x2(ca * v1[2 * q], ca * v1[2 * q + 1]);
-          }
-#pragma unroll
-          for (int q = 0; q < 8; ++q)
-            sts128(smem_u32(buf) + lane * 128 + ((q ^ (lane & 7)) << 4),
-                   make_uint4(pk[4 * q], pk[4 * q + 1], pk[4 * q + 2], pk[4 * q + 3]));
-          fence_proxy_async_smem();
-          __syncwarp();
-          if (lane == 0) {
-            tma_store_3d(&P.mapD[k.group], buf, tn * 256 + cc * 32, row, k.z);
-            bulk_commit();
-          }
-        }
-      } else {
 #pragma unroll 1
       for (int cc32 = c0; cc32 < c0 + 4; ++cc32) {
         float v[32];
         tmem_ld_32x32b_x32(tmem_base + acc * 256 + cc32 * 32 + ((uint32_t)(lg * 32) << 16), v);
-        uint8_t* buf = stage_base + ew * 4096 + sbuf * 2048;
+        uint8_t* buf = stage_base + (ew * 2 + sbuf) * 2048;
         if (lane == 0) bulk_wait_read<1>();  // the store issued from this buffer two chunks ago has read it
         __syncwarp();
         uint32_t pk[16];
@@ -276,14 +244,17 @@ __global__ void __cluster_dims__(2, 1, 1) __launch_bounds__(kThreads, 1)
                  make_uint4(pk[4 * q], pk[4 * q + 1], pk[4 * q + 2], pk[4 * q + 3]));
         fence_proxy_async_smem();
         __syncwarp();
-        if (lane == 0) {  // X_T straight into the rank pieces of the exchange buffer (32 x 32 boxes)
-          const int col = tn * 256 + cc32 * 32;
-          const int pr = col / G.pieces_qo;
-          tma_store_3d(&P.mapP[k.group][2 * G.pieces_P + pr], buf, col - pr * G.pieces_qo, row, k.z);
+        if (lane == 0) {
+          const int col = tn * 256 + cc32 * 32, row = k.tm * 256 + (int)rank * 128 + lg * 32;
+          if (G.pieces_store) {  // X_T straight into the rank pieces of the exchange buffer
+            const int pr = col / G.pieces_qo;
+            tma_store_3d(&P.mapP[k.group][2 * G.pieces_P + pr], buf, col - pr * G.pieces_qo, row, k.z);
+          } else {
+            tma_store_3d(&P.mapD[k.group], buf, col, row, k.z);
+          }
           bulk_commit();
         }
         sbuf ^= 1;
-      }
       }
       tc_fence_before();
       __syncwarp();
