@@ -87,14 +87,12 @@ constexpr uint32_t kIdescAbFmt = (7u << 7) | (7u << 10);
 
 }  // namespace
 
-// S operand stages, NB epilogue staging buffers per warp (4: symmetric launches also store the
-// mirrored chunk; 2: the apply, whose freed staging space buys a sixth stage)
-template <int S, int NB>
-constexpr int ns_pair_smem_bytes() { return 1024 + S * (int)kStage + 1024 + kEpiWarps * NB * 2048; }
+constexpr int ns_pair_smem_bytes() { return 1024 + kStagesPair * (int)kStage + 1024 + kEpiWarps * 4 * 2048; }
 
-template <bool kSymIn, int S, int NB>  // kSymIn = P.p.sym_in (non-symmetric launches carry no per-k-block logic)
+template <bool kSymIn>  // = P.p.sym_in (a template so non-symmetric launches carry no per-k-block logic)
 __global__ void __cluster_dims__(2, 1, 1) __launch_bounds__(kPairThreads, 1)
     k_ns_gemm_tc_pair(const __grid_constant__ NsTcParams P) {
+  constexpr int S = kStagesPair;
   extern __shared__ uint8_t smem_raw[];
   uint8_t* smem = reinterpret_cast<uint8_t*>((reinterpret_cast<uintptr_t>(smem_raw) + 1023) & ~uintptr_t(1023));
   uint64_t* full_bar = reinterpret_cast<uint64_t*>(smem + S * kStage);
@@ -333,8 +331,8 @@ __global__ void __cluster_dims__(2, 1, 1) __launch_bounds__(kPairThreads, 1)
         // 4 staging buffers per warp (SWIZZLE_64B layout: 16-B chunk q of row r at
         // q ^ ((r >> 1) & 3)); a buffer is rewritten once the store 4 commits back has read it
         const bool mirror = p.sym && !p.no_mirror && c.tm != c.tn;
-        uint8_t* buf = stage_base + (ew * NB + sbuf) * 2048;
-        if (lane == 0) bulk_wait_read<NB - 1>();
+        uint8_t* buf = stage_base + (ew * 4 + sbuf) * 2048;
+        if (lane == 0) bulk_wait_read<3>();
         __syncwarp();
         uint32_t pk[16];
 #pragma unroll
@@ -343,8 +341,8 @@ __global__ void __cluster_dims__(2, 1, 1) __launch_bounds__(kPairThreads, 1)
         for (int q = 0; q < 4; ++q)
           sts128(smem_u32(buf) + lane * 64 + ((q ^ ((lane >> 1) & 3)) << 4),
                  make_uint4(pk[4 * q], pk[4 * q + 1], pk[4 * q + 2], pk[4 * q + 3]));
-        uint8_t* tbuf = stage_base + (ew * NB + ((sbuf + 1) & (NB - 1))) * 2048;
-        if (NB == 4 && mirror) {
+        uint8_t* tbuf = stage_base + (ew * 4 + ((sbuf + 1) & 3)) * 2048;
+        if (mirror) {
           // the transposed 32 x 32 chunk: element (row e, col lane) = o[e]; tbuf was used by
           // the 3rd most recent store (the current one is not issued yet)
           if (lane == 0) bulk_wait_read<2>();
@@ -361,13 +359,13 @@ __global__ void __cluster_dims__(2, 1, 1) __launch_bounds__(kPairThreads, 1)
         if (lane == 0) {
           tma_store_3d(&P.mapD[c.group], buf, c.tn * 256 + cc32 * 32, c.tm * 256 + (int)rank * 128 + lg * 32, c.z);
           bulk_commit();
-          if (NB == 4 && mirror) {
+          if (mirror) {
             tma_store_3d(&P.mapD[c.group], tbuf, c.tm * 256 + (int)rank * 128 + lg * 32, c.tn * 256 + cc32 * 32,
                          c.z);
             bulk_commit();
           }
         }
-        sbuf = (sbuf + ((NB == 4 && mirror) ? 2 : 1)) & (NB - 1);
+        sbuf = (sbuf + (mirror ? 2 : 1)) & 3;
       }
       tc_fence_before();
       __syncwarp();
@@ -426,12 +424,8 @@ void launch_splitk_reduce(cudaStream_t s, const NsParams& p) {
 }
 
 void ns_pair_set_attrs() {
-  cudaFuncSetAttribute(k_ns_gemm_tc_pair<false, kStagesPair, 4>, cudaFuncAttributeMaxDynamicSharedMemorySize,
-                       ns_pair_smem_bytes<kStagesPair, 4>());
-  cudaFuncSetAttribute(k_ns_gemm_tc_pair<true, kStagesPair, 4>, cudaFuncAttributeMaxDynamicSharedMemorySize,
-                       ns_pair_smem_bytes<kStagesPair, 4>());
-  cudaFuncSetAttribute(k_ns_gemm_tc_pair<false, 6, 2>, cudaFuncAttributeMaxDynamicSharedMemorySize,
-                       ns_pair_smem_bytes<6, 2>());
+  cudaFuncSetAttribute(k_ns_gemm_tc_pair<false>, cudaFuncAttributeMaxDynamicSharedMemorySize, ns_pair_smem_bytes());
+  cudaFuncSetAttribute(k_ns_gemm_tc_pair<true>, cudaFuncAttributeMaxDynamicSharedMemorySize, ns_pair_smem_bytes());
 }
 
 void launch_ns_pair(int grid, cudaStream_t s, const NsTcParams& P) {
@@ -441,18 +435,14 @@ void launch_ns_pair(int grid, cudaStream_t s, const NsTcParams& P) {
   at[0].val.programmaticStreamSerializationAllowed = 1;
   cfg.gridDim = dim3(grid);
   cfg.blockDim = dim3(kPairThreads);
-  // non-symmetric launches (the apply: sym = 0, no mirrored stores): 6 stages, 2 staging buffers
-  const bool deep = !P.p.sym && !P.p.sym_in;
-  cfg.dynamicSmemBytes = deep ? ns_pair_smem_bytes<6, 2>() : ns_pair_smem_bytes<kStagesPair, 4>();
+  cfg.dynamicSmemBytes = ns_pair_smem_bytes();
   cfg.stream = s;
   cfg.attrs = at;
   cfg.numAttrs = 1;
   if (P.p.sym_in)
-    cudaLaunchKernelEx(&cfg, k_ns_gemm_tc_pair<true, kStagesPair, 4>, P);
-  else if (deep)
-    cudaLaunchKernelEx(&cfg, k_ns_gemm_tc_pair<false, 6, 2>, P);
+    cudaLaunchKernelEx(&cfg, k_ns_gemm_tc_pair<true>, P);
   else
-    cudaLaunchKernelEx(&cfg, k_ns_gemm_tc_pair<false, kStagesPair, 4>, P);
+    cudaLaunchKernelEx(&cfg, k_ns_gemm_tc_pair<false>, P);
 }
 
 }  // namespace dion2
