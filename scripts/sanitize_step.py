@@ -27,4 +27,19 @@ for form in ("auto", "direct"):
             opt.step(Ws, Ms, Gs)
         torch.cuda.synchronize()
         assert opt.status() == (0, -1), opt.status()
+# bf16 weights, split-K gram (two long matrices), the distributed step and DP-sync in loopback
+Wb = [torch.from_numpy(gen_w0(m, n, 3, i)).cuda().to(torch.bfloat16) for i, (m, n) in enumerate(shapes)]
+Mb = [torch.zeros(m, n, device="cuda") for (m, n) in shapes]
+Dion2(alpha=0.25).step(Wb, Mb, [torch.from_numpy(gen_grad(m, n, 3, i)).cuda() for i, (m, n) in enumerate(shapes)])
+big = [(1024, 16384), (8192, 1024)]
+Ws = [torch.from_numpy(gen_w0(m, n, 4, i)).cuda() for i, (m, n) in enumerate(big)]
+Dion2(alpha=0.0625).step(Ws, [torch.zeros_like(w) for w in Ws],
+                         [torch.from_numpy(gen_grad(m, n, 4, i)).cuda() for i, (m, n) in enumerate(big)])
+torch.cuda.synchronize()
+sys.path.insert(0, os.path.join(ROOT, "tests"))
+from gpu_harness import run_parity_dist  # noqa: E402
+r = run_parity_dist([(256, 512), (512, 256), (1024, 1024)], 0.25, 2, steps=2)
+assert r.index_mismatch == 0, r
+import test_gpu_dpsync as T  # noqa: E402
+T._run(2, "bf16", 2e-2, steps=2)
 print("sanitize_step ok")
