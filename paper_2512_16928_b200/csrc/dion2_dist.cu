@@ -64,7 +64,8 @@ struct DistMat {
   int axis, d, o, k, qo;   // selection axis, its length, other length, selected, block width o/P
   int64_t srows, scols;    // local shard shape
   int owner;
-  int64_t piece;           // bytes of one k x qo bf16 piece (256-B aligned)
+  int chunk;               // owner chunk (C2 / NS / C3 rounds overlap by chunk)
+  int64_t piece;           // bytes of one k x qo fp16 piece (256-B aligned)
   int64_t soff;            // offset of this matrix's piece inside its owner's section
   double flops;
   int path, ga, gb;
@@ -95,19 +96,29 @@ struct DistPlan {
   // streaming lists: gather and scatter membership differ for transposed-M column matrices
   // (row gather on M^T, column scatter on W)
   size_t t_desc, t_rowmats, t_rowprefix, t_colmats, t_colprefix, t_mtmats, t_mtprefix, t_allcols, t_flgm[2],
-      t_flsm[2], t_flg[2], t_fls[2], t_gidx, t_roff, t_gprefix, t_inpl = 0, t_pmaps = 0;
+      t_flsm[2], t_flg[2], t_fls[2], t_gprefix;
   int n_row_mats = 0, n_col_mats = 0, n_mt_mats = 0, n_allcols = 0, fl_gn[2] = {0, 0}, fl_sn[2] = {0, 0},
       fl_gunits[2] = {0, 0}, fl_sunits[2] = {0, 0}, fl_maxk = 0, max_d = 0, total_gather_tiles = 0;
   int64_t total_rows = 0, total_col_tiles = 0, total_mt_tiles = 0, max_cols_col = 0;
   std::vector<const void*> last_ptrs;
   bool uploaded = false;
-  // owner side
-  std::vector<int> owned;
-  std::unique_ptr<Plan> owner;
-  PieceTable ptab{};
-  int max_p_pad = 0, max_k_owned = 0;
-  bool all_inplace = false;     // every owned matrix's NS reads and writes the exchange pieces in place
-  bool all_inplace_in = false;  // ... reads them in place (inplace value 1 or 2)
+  // owner side, in chunks: the exchange to the owners (C2), the owner's NS and the exchange
+  // back (C3) run chunk by chunk on two streams, so C2 of chunk c + 1 and C3 of chunk c - 1
+  // overlap the NS of chunk c.  Every owner's send section is ordered by (chunk, NS shape group,
+  // index); cdispl[o][c] is chunk c's offset inside owner o's section (same on every rank).
+  int nchunks = 1;
+  std::vector<std::vector<int64_t>> cdispl;
+  struct OwnerChunk {
+    std::vector<int> owned;        // global matrix indices (index order)
+    std::unique_ptr<Plan> plan;    // NS plan over their global shapes
+    size_t off = 0;                // workspace offset of the plan
+    PieceTable ptab{};
+    size_t t_gidx = 0, t_roff = 0, t_inpl = 0, t_pmaps = 0;
+    int max_p_pad = 0, max_k = 0;
+    bool all_inplace = false;      // every matrix's NS reads and writes the exchange pieces in place
+    bool all_inplace_in = false;   // ... reads them in place
+  };
+  std::vector<OwnerChunk> oc;
 };
 
 void* dt(DistPlan& D, size_t off) { return static_cast<uint8_t*>(D.dtab) + off; }
@@ -167,41 +178,57 @@ int resolve(DistPlan& D, const dion2_shard* sh, int n, const dion2_config* c, in
     D.dm[j].owner = best;
     load[best] += D.dm[j].flops;
   }
+  // owner chunks (DION2_DIST_CHUNKS, default 2 when there is an exchange): each owner's matrices
+  // in descending NS FLOPs (ties -> lower index) dealt round-robin to the chunks
+  const char* ce = getenv("DION2_DIST_CHUNKS");
+  D.nchunks = world > 1 ? std::max(1, ce ? atoi(ce) : 2) : 1;
+  for (int o = 0; o < world; ++o) {
+    int t = 0;
+    for (int j : order)
+      if (D.dm[j].owner == o) D.dm[j].chunk = (t++) % D.nchunks;
+  }
   // send sections (by owner) and my recv section size
   D.sdispl.assign(world, 0);
   D.scount.assign(world, 0);
-  // Inside an owner's section the pieces are grouped by the owner plan's NS shape groups
-  // ((p_pad, q_pad) in first-appearance order, members in index order), so a group's pieces
-  // from one rank form a uniform [matrix][k][qo] array the owner's NS kernels can address with
-  // one tensor map per rank (in-place pieces, build_tables).  Shapes only: same on every rank.
+  D.cdispl.assign(world, std::vector<int64_t>(D.nchunks + 1, 0));
+  // Inside an owner's section the pieces are ordered by chunk, then by the owner chunk plan's NS
+  // shape groups ((p_pad, q_pad) in first-appearance order, members in index order), so a
+  // group's pieces from one rank form a uniform [matrix][k][qo] array the owner's NS kernels can
+  // address with one tensor map per rank (in-place pieces, build_tables).  Shapes only: the
+  // same on every rank.
   int64_t run = 0;
   for (int o = 0; o < world; ++o) {
     D.sdispl[o] = run;
-    std::vector<int> mine;
-    std::vector<std::pair<int64_t, int64_t>> keys;
-    std::vector<int> key_of;
-    for (int j = 0; j < n; ++j)
-      if (D.dm[j].owner == o) {
-        const std::pair<int64_t, int64_t> key((int64_t)align_up(D.dm[j].k, 256), (int64_t)align_up(D.dm[j].o, 256));
-        int ki = (int)(std::find(keys.begin(), keys.end(), key) - keys.begin());
-        if (ki == (int)keys.size()) keys.push_back(key);
-        mine.push_back(j);
-        key_of.push_back(ki);
+    for (int ch = 0; ch < D.nchunks; ++ch) {
+      D.cdispl[o][ch] = run - D.sdispl[o];
+      std::vector<int> mine;
+      std::vector<std::pair<int64_t, int64_t>> keys;
+      std::vector<int> key_of;
+      for (int j = 0; j < n; ++j)
+        if (D.dm[j].owner == o && D.dm[j].chunk == ch) {
+          const std::pair<int64_t, int64_t> key((int64_t)align_up(D.dm[j].k, 256), (int64_t)align_up(D.dm[j].o, 256));
+          int ki = (int)(std::find(keys.begin(), keys.end(), key) - keys.begin());
+          if (ki == (int)keys.size()) keys.push_back(key);
+          mine.push_back(j);
+          key_of.push_back(ki);
+        }
+      std::vector<int> ord(mine.size());
+      std::iota(ord.begin(), ord.end(), 0);
+      std::stable_sort(ord.begin(), ord.end(), [&](int a, int b) { return key_of[a] < key_of[b]; });
+      for (int t : ord) {
+        const int j = mine[t];
+        D.dm[j].soff = run - D.sdispl[o];
+        run += D.dm[j].piece;
       }
-    std::vector<int> ord(mine.size());
-    std::iota(ord.begin(), ord.end(), 0);
-    std::stable_sort(ord.begin(), ord.end(), [&](int a, int b) { return key_of[a] < key_of[b]; });
-    for (int t : ord) {
-      const int j = mine[t];
-      D.dm[j].soff = run - D.sdispl[o];
-      run += D.dm[j].piece;
     }
+    D.cdispl[o][D.nchunks] = run - D.sdispl[o];
     D.scount[o] = run - D.sdispl[o];
   }
   D.R = D.scount[rank];
-  D.owned.clear();
+  D.oc.clear();
+  D.oc.resize(D.nchunks);
   for (int j = 0; j < n; ++j)
-    if (D.dm[j].owner == rank) D.owned.push_back(j);
+    if (D.dm[j].owner == rank) D.oc[D.dm[j].chunk].owned.push_back(j);
   // workspace
   size_t off = 0;
   auto take = [&](size_t bytes) {
@@ -229,20 +256,22 @@ int resolve(DistPlan& D, const dion2_shard* sh, int n, const dion2_config* c, in
   D.off_osend = take((size_t)D.R * world);
   off = align_up(off, 4096);
   D.off_owner = off;
-  // owner plan over the owned matrices' GLOBAL shapes (NS only)
+  // one owner plan per chunk over its matrices' GLOBAL shapes (NS only)
   size_t owner_bytes = 0;
-  if (!D.owned.empty()) {
-    std::vector<dion2_matrix> om(D.owned.size());
-    for (size_t i = 0; i < D.owned.size(); ++i) {
+  for (auto& ch : D.oc) {
+    ch.off = D.off_owner + owner_bytes;
+    if (ch.owned.empty()) continue;
+    std::vector<dion2_matrix> om(ch.owned.size());
+    for (size_t i = 0; i < ch.owned.size(); ++i) {
       memset(&om[i], 0, sizeof(om[i]));
-      om[i].rows = D.dm[D.owned[i]].m;
-      om[i].cols = D.dm[D.owned[i]].n;
-      om[i].ld = D.dm[D.owned[i]].n;
+      om[i].rows = D.dm[ch.owned[i]].m;
+      om[i].cols = D.dm[ch.owned[i]].n;
+      om[i].ld = D.dm[ch.owned[i]].n;
     }
-    D.owner = std::make_unique<Plan>();
-    int rc = build_layout(*D.owner, om.data(), (int)om.size(), c);
+    ch.plan = std::make_unique<Plan>();
+    int rc = build_layout(*ch.plan, om.data(), (int)om.size(), c);
     if (rc) return rc;
-    owner_bytes = D.owner->total;
+    owner_bytes = align_up(owner_bytes + ch.plan->total, 4096);
   }
   D.total = D.off_owner + owner_bytes + 4096;
   return DION2_OK;
@@ -272,11 +301,13 @@ int build_tables(DistPlan& D, const dion2_config* c, void* ws) {
     D.t_fls[l] = take(4 * (size_t)n);
   }
   D.t_gprefix = take(4 * (size_t)n);
-  D.t_gidx = take(4 * std::max<size_t>(1, D.owned.size()));
-  D.t_roff = take(8 * std::max<size_t>(1, D.owned.size()) * P);
-  D.t_inpl = take(4 * std::max<size_t>(1, D.owned.size()));
-  const size_t n_owner_groups = D.owner ? D.owner->groups.size() : 0;
-  D.t_pmaps = take(sizeof(CUtensorMap) * std::max<size_t>(1, n_owner_groups * 3 * (size_t)P));
+  for (auto& ch : D.oc) {
+    ch.t_gidx = take(4 * std::max<size_t>(1, ch.owned.size()));
+    ch.t_roff = take(8 * std::max<size_t>(1, ch.owned.size()) * P);
+    ch.t_inpl = take(4 * std::max<size_t>(1, ch.owned.size()));
+    const size_t ng = ch.plan ? ch.plan->groups.size() : 0;
+    ch.t_pmaps = take(sizeof(CUtensorMap) * std::max<size_t>(1, ng * 3 * (size_t)P));
+  }
   D.htab.assign(off, 0);
   if (!D.dtab && cudaMalloc(&D.dtab, off) != cudaSuccess) return DION2_ECUDA;
   auto H = [&](size_t o) { return D.htab.data() + o; };
@@ -398,46 +429,48 @@ int build_tables(DistPlan& D, const dion2_config* c, void* ws) {
       memcpy(H(D.t_fls[l]), fls[l].data(), 4 * fls[l].size());
     }
   }
-  // owner plan + piece table
-  D.max_p_pad = D.max_k_owned = 0;
-  if (!D.owned.empty()) {
-    std::vector<dion2_matrix> om(D.owned.size());
-    for (size_t i = 0; i < D.owned.size(); ++i) {
+  // owner chunk plans + piece tables
+  for (auto& ch : D.oc) {
+    ch.max_p_pad = ch.max_k = 0;
+    if (ch.owned.empty()) continue;
+    Plan& OP = *ch.plan;
+    std::vector<dion2_matrix> om(ch.owned.size());
+    for (size_t i = 0; i < ch.owned.size(); ++i) {
       memset(&om[i], 0, sizeof(om[i]));
-      om[i].rows = D.dm[D.owned[i]].m;
-      om[i].cols = D.dm[D.owned[i]].n;
-      om[i].ld = D.dm[D.owned[i]].n;
+      om[i].rows = D.dm[ch.owned[i]].m;
+      om[i].cols = D.dm[ch.owned[i]].n;
+      om[i].ld = D.dm[ch.owned[i]].n;
     }
-    int rc = build_device_plan(*D.owner, om.data(), c, at(ws, D.off_owner));
+    int rc = build_device_plan(OP, om.data(), c, at(ws, ch.off));
     if (rc) return rc;
-    std::vector<int32_t> gidx(D.owned.size());
-    std::vector<int64_t> roff(D.owned.size() * P);
-    for (size_t i = 0; i < D.owned.size(); ++i) {
-      const DistMat& q = D.dm[D.owned[i]];
-      gidx[i] = D.owned[i];
+    std::vector<int32_t> gidx(ch.owned.size());
+    std::vector<int64_t> roff(ch.owned.size() * P);
+    for (size_t i = 0; i < ch.owned.size(); ++i) {
+      const DistMat& q = D.dm[ch.owned[i]];
+      gidx[i] = ch.owned[i];
       for (int r = 0; r < P; ++r) roff[i * P + r] = q.soff;
-      D.max_p_pad = std::max(D.max_p_pad, D.owner->mp[i].p_pad);
-      D.max_k_owned = std::max(D.max_k_owned, q.k);
+      ch.max_p_pad = std::max(ch.max_p_pad, OP.mp[i].p_pad);
+      ch.max_k = std::max(ch.max_k, q.k);
       // the owner's NS runs on the global orientation: X = k x o (k <= o)
-      if (D.owner->mp[i].p != q.k || D.owner->mp[i].q != q.o) return DION2_EUNSUPPORTED;
+      if (OP.mp[i].p != q.k || OP.mp[i].q != q.o) return DION2_EUNSUPPORTED;
     }
-    memcpy(H(D.t_gidx), gidx.data(), 4 * gidx.size());
-    memcpy(H(D.t_roff), roff.data(), 8 * roff.size());
+    memcpy(H(ch.t_gidx), gidx.data(), 4 * gidx.size());
+    memcpy(H(ch.t_roff), roff.data(), 8 * roff.size());
     // In-place pieces: a Gram-space owner group whose q is a whole number of 256-column tiles
     // and of 64-column k-blocks per rank piece (q_pad == q, qo % 64 == 0, P <= 8) has its gram
     // and apply read X0 straight from the received pieces and its apply write X_T straight into
     // the outgoing pieces (no assemble / disassemble copies); other groups are copied.
-    std::vector<int32_t> inpl(D.owned.size(), 0);
+    std::vector<int32_t> inpl(ch.owned.size(), 0);
     const bool inplace_on = P <= kMaxPieceRanks;
-    CUtensorMap* hmaps = reinterpret_cast<CUtensorMap*>(H(D.t_pmaps));
-    std::vector<int> g_ok(D.owner->groups.size(), 0);
-    for (size_t gi = 0; gi < D.owner->groups.size() && inplace_on; ++gi) {
-      const Group& g = D.owner->groups[gi];
+    CUtensorMap* hmaps = reinterpret_cast<CUtensorMap*>(H(ch.t_pmaps));
+    std::vector<int> g_ok(OP.groups.size(), 0);
+    for (size_t gi = 0; gi < OP.groups.size() && inplace_on; ++gi) {
+      const Group& g = OP.groups[gi];
       if (!g.gs) continue;
-      const DistMat& q0 = D.dm[D.owned[g.mats[0]]];
+      const DistMat& q0 = D.dm[ch.owned[g.mats[0]]];
       bool ok = true;
       for (size_t zi = 0; zi < g.mats.size() && ok; ++zi) {
-        const DistMat& q = D.dm[D.owned[g.mats[zi]]];
+        const DistMat& q = D.dm[ch.owned[g.mats[zi]]];
         ok = q.o == g.q_pad && q.qo % 64 == 0 && q.k == q0.k && q.qo == q0.qo && q.piece == q0.piece &&
              q.soff == q0.soff + (int64_t)zi * q0.piece;
       }
@@ -458,23 +491,23 @@ int build_tables(DistPlan& D, const dion2_config* c, void* ws) {
     // B = X0) at the received pieces, and the last apply (D = X_T) at the outgoing pieces
     // (the last segment's apply reads X0 after an odd number of restart segments, else X1)
     const bool last_reads_x0 = ns_segments(c, c->ns_steps).size() & 1;
-    for (int li = 0; li < (int)D.owner->ns_launches.size(); ++li) {
-      Launch& ln = D.owner->ns_launches[li];
+    for (int li = 0; li < (int)OP.ns_launches.size(); ++li) {
+      Launch& ln = OP.ns_launches[li];
       if (ln.phase != PH_GRAM && ln.phase != PH_APPLY) continue;
       for (int j = 0; j < ln.tc.p.ngroups; ++j) {
         NsGroup& G = ln.tc.p.g[j];
-        for (size_t gi = 0; gi < D.owner->groups.size(); ++gi) {
+        for (size_t gi = 0; gi < OP.groups.size(); ++gi) {
           if (!g_ok[gi]) continue;
-          const Group& og = D.owner->groups[gi];
-          const void* x0 = at(at(ws, D.off_owner), og.off_X0);
-          const void* x1 = at(at(ws, D.off_owner), og.off_X1);
+          const Group& og = OP.groups[gi];
+          const void* x0 = at(at(ws, ch.off), og.off_X0);
+          const void* x1 = at(at(ws, ch.off), og.off_X1);
           // this entry belongs to group gi iff it reads or writes one of gi's X buffers
           const bool mine = ln.phase == PH_GRAM ? (G.a == x0 || G.a == x1) : (G.b == x0 || G.b == x1);
           if (!mine) continue;
           const bool load = ln.phase == PH_GRAM ? G.a == x0 : G.b == x0;
           const bool store = ln.phase == PH_APPLY && G.b == (last_reads_x0 ? x0 : x1);
           if (!load && !store) continue;
-          const DistMat& q0 = D.dm[D.owned[og.mats[0]]];
+          const DistMat& q0 = D.dm[ch.owned[og.mats[0]]];
           G.pieces_qo = q0.qo;
           G.pieces_P = P;
           G.pieces_map = (int)(gi * 3 * P);
@@ -484,14 +517,14 @@ int build_tables(DistPlan& D, const dion2_config* c, void* ws) {
         }
       }
     }
-    memcpy(H(D.t_inpl), inpl.data(), 4 * inpl.size());
-    D.all_inplace = std::all_of(inpl.begin(), inpl.end(), [](int32_t v) { return v == 1; });
-    D.all_inplace_in = std::all_of(inpl.begin(), inpl.end(), [](int32_t v) { return v != 0; });
-    D.ptab.inplace = (const int32_t*)dt(D, D.t_inpl);
-    D.ptab.gidx = (const int32_t*)dt(D, D.t_gidx);
-    D.ptab.roff = (const int64_t*)dt(D, D.t_roff);
-    D.ptab.rstride = D.R;
-    D.ptab.world = P;
+    memcpy(H(ch.t_inpl), inpl.data(), 4 * inpl.size());
+    ch.all_inplace = std::all_of(inpl.begin(), inpl.end(), [](int32_t v) { return v == 1; });
+    ch.all_inplace_in = std::all_of(inpl.begin(), inpl.end(), [](int32_t v) { return v != 0; });
+    ch.ptab.inplace = (const int32_t*)dt(D, ch.t_inpl);
+    ch.ptab.gidx = (const int32_t*)dt(D, ch.t_gidx);
+    ch.ptab.roff = (const int64_t*)dt(D, ch.t_roff);
+    ch.ptab.rstride = D.R;
+    ch.ptab.world = P;
   }
   return DION2_OK;
 }
@@ -575,9 +608,10 @@ int refresh(DistPlan& D, const dion2_shard* sh, const dion2_config* c, cudaStrea
   if (up) {
     if (cudaMemcpyAsync(D.dtab, D.htab.data(), D.htab.size(), cudaMemcpyHostToDevice, s) != cudaSuccess)
       return DION2_ECUDA;
-    if (D.owner && cudaMemcpyAsync(D.owner->dtab, D.owner->host_tables.data(), D.owner->host_tables.size(),
-                                   cudaMemcpyHostToDevice, s) != cudaSuccess)
-      return DION2_ECUDA;
+    for (auto& ch : D.oc)
+      if (ch.plan && cudaMemcpyAsync(ch.plan->dtab, ch.plan->host_tables.data(), ch.plan->host_tables.size(),
+                                     cudaMemcpyHostToDevice, s) != cudaSuccess)
+        return DION2_ECUDA;
     D.uploaded = true;
   }
   return DION2_OK;
@@ -663,19 +697,21 @@ void phase_gather(DistPlan& D, void* ws, const dion2_config* c, Launcher& L, cud
   L.end();
 }
 
-void phase_owner_ns(DistPlan& D, void* ws, const dion2_config* c, Launcher& L, cudaStream_t s) {
-  if (D.owned.empty()) return;
-  Plan& P = *D.owner;
+void phase_owner_ns(DistPlan& D, int chunk, void* ws, const dion2_config* c, Launcher& L, cudaStream_t s) {
+  auto& ch = D.oc[chunk];
+  if (ch.owned.empty()) return;
+  Plan& P = *ch.plan;
   const MatDesc* om = (const MatDesc*)tab(P, P.off_desc);
   L.begin(PH_NORM);
   // all owned matrices in place: one block per matrix computes the norm scale only
-  launch_assemble(s, om, (int)D.owned.size(), D.all_inplace_in ? 1 : D.max_p_pad, D.ptab, (const uint8_t*)at(ws, D.off_recv),
-                  (const float*)at(ws, D.off_sumsq_all), (const float*)at(ws, D.off_nsscale), D.n, c->ns_eps);
+  launch_assemble(s, om, (int)ch.owned.size(), ch.all_inplace_in ? 1 : ch.max_p_pad, ch.ptab,
+                  (const uint8_t*)at(ws, D.off_recv), (const float*)at(ws, D.off_sumsq_all),
+                  (const float*)at(ws, D.off_nsscale), D.n, c->ns_eps);
   L.end();
   run_ns(P, c, L, s, false);
-  if (!D.all_inplace) {
+  if (!ch.all_inplace) {
     L.begin(PH_SCATTER);
-    launch_disassemble(s, om, (int)D.owned.size(), D.max_k_owned, D.ptab, (uint8_t*)at(ws, D.off_osend));
+    launch_disassemble(s, om, (int)ch.owned.size(), ch.max_k, ch.ptab, (uint8_t*)at(ws, D.off_osend));
     L.end();
   }
 }
@@ -710,10 +746,11 @@ void phase_scatter(DistPlan& D, void* ws, const dion2_config* c, Launcher& L, cu
 // ------------------------------------------------------------------ exchanges
 struct Transport {
   virtual ~Transport() = default;
-  virtual int allgather_scores() = 0;
-  virtual int allgather_sumsq() = 0;
-  virtual int to_owners() = 0;
-  virtual int from_owners() = 0;
+  virtual int allgather_scores(cudaStream_t s) = 0;
+  virtual int allgather_sumsq(cudaStream_t s) = 0;
+  // owner chunk `chunk` of every owner: pieces to the owners (C2) / results back (C3)
+  virtual int to_owners(int chunk, cudaStream_t s) = 0;
+  virtual int from_owners(int chunk, cudaStream_t s) = 0;
   uint64_t bytes = 0;
 };
 
@@ -721,116 +758,155 @@ struct NcclTransport : Transport {
   DistPlan& D;
   void* ws;
   ncclComm_t comm;
-  cudaStream_t s;
-  NcclTransport(DistPlan& d, void* w, void* cm, cudaStream_t st) : D(d), ws(w), comm(cm), s(st) {}
-  int allgather_scores() override {
+  NcclTransport(DistPlan& d, void* w, void* cm) : D(d), ws(w), comm(cm) {}
+  int allgather_scores(cudaStream_t s) override {
     bytes += (uint64_t)D.total_d * 4 * (D.world - 1);
     return nccl_api().allgather(at(ws, D.off_scores), at(ws, D.off_scores_all), (size_t)D.total_d, kNcclFloat32, comm,
                                 s)
                ? DION2_ENCCL
                : DION2_OK;
   }
-  int allgather_sumsq() override {
+  int allgather_sumsq(cudaStream_t s) override {
     bytes += (uint64_t)D.n * 4 * (D.world - 1);
     return nccl_api().allgather(at(ws, D.off_sumsq_local), at(ws, D.off_sumsq_all), (size_t)D.n, kNcclFloat32, comm, s)
                ? DION2_ENCCL
                : DION2_OK;
   }
-  int exchange(bool forward) {
+  int exchange(bool forward, int ch, cudaStream_t s) {
     auto& api = nccl_api();
     int rc = 0;
     rc |= api.group_start();
     for (int peer = 0; peer < D.world; ++peer) {
-      // forward: my send section for owner `peer` -> peer's recv section `rank`
-      //          and peer's send section for me -> my recv section `peer`
-      uint8_t* mine = (uint8_t*)at(ws, (forward ? D.off_send : D.off_orecv) + D.sdispl[peer]);
-      uint8_t* owner_side = (uint8_t*)at(ws, (forward ? D.off_recv : D.off_osend) + (size_t)peer * D.R);
-      const size_t nmine = (size_t)D.scount[peer], nown = (size_t)D.R;
+      // forward: my pieces for owner `peer`'s chunk ch -> peer's recv section `rank`, and peer's
+      //          pieces for my chunk ch -> my recv section `peer`; backward mirrors it
+      const int64_t mo = D.cdispl[peer][ch], mn = D.cdispl[peer][ch + 1] - mo;            // in my section for peer
+      const int64_t oo = D.cdispl[D.rank][ch], on = D.cdispl[D.rank][ch + 1] - oo;          // in my owner sections
+      uint8_t* mine = (uint8_t*)at(ws, (forward ? D.off_send : D.off_orecv) + D.sdispl[peer] + mo);
+      uint8_t* owner_side = (uint8_t*)at(ws, (forward ? D.off_recv : D.off_osend) + (size_t)peer * D.R + oo);
       if (forward) {
-        if (nmine) rc |= api.send(mine, nmine, kNcclChar, peer, comm, s);
-        if (nown) rc |= api.recv(owner_side, nown, kNcclChar, peer, comm, s);
+        if (mn) rc |= api.send(mine, (size_t)mn, kNcclChar, peer, comm, s);
+        if (on) rc |= api.recv(owner_side, (size_t)on, kNcclChar, peer, comm, s);
       } else {
-        if (nown) rc |= api.send(owner_side, nown, kNcclChar, peer, comm, s);
-        if (nmine) rc |= api.recv(mine, nmine, kNcclChar, peer, comm, s);
+        if (on) rc |= api.send(owner_side, (size_t)on, kNcclChar, peer, comm, s);
+        if (mn) rc |= api.recv(mine, (size_t)mn, kNcclChar, peer, comm, s);
       }
-      if (peer != D.rank) bytes += forward ? nmine : nown;
+      if (peer != D.rank) bytes += forward ? mn : on;
     }
     rc |= api.group_end();
     return rc ? DION2_ENCCL : DION2_OK;
   }
-  int to_owners() override { return exchange(true); }
-  int from_owners() override { return exchange(false); }
+  int to_owners(int ch, cudaStream_t s) override { return exchange(true, ch, s); }
+  int from_owners(int ch, cudaStream_t s) override { return exchange(false, ch, s); }
 };
 
 // all ranks in one process: every exchange is a set of device-to-device copies
 struct LoopbackTransport : Transport {
   std::vector<DistPlan*> D;
   std::vector<void*> ws;
-  cudaStream_t s;
-  LoopbackTransport(std::vector<DistPlan*> d, std::vector<void*> w, cudaStream_t st) : D(d), ws(w), s(st) {}
-  int cp(void* dst, const void* src, size_t n) {
+  LoopbackTransport(std::vector<DistPlan*> d, std::vector<void*> w) : D(d), ws(w) {}
+  int cp(void* dst, const void* src, size_t n, cudaStream_t s) {
     if (!n) return DION2_OK;
     return cudaMemcpyAsync(dst, src, n, cudaMemcpyDeviceToDevice, s) == cudaSuccess ? DION2_OK : DION2_ECUDA;
   }
-  int allgather_scores() override {
+  int allgather_scores(cudaStream_t s) override {
     const int P = (int)D.size();
     int rc = 0;
     for (int r = 0; r < P; ++r)
       for (int r2 = 0; r2 < P; ++r2)
         rc |= cp(at(ws[r], D[r]->off_scores_all + (size_t)r2 * D[r]->total_d * 4), at(ws[r2], D[r2]->off_scores),
-                 (size_t)D[r]->total_d * 4);
+                 (size_t)D[r]->total_d * 4, s);
     bytes += (uint64_t)D[0]->total_d * 4 * (P - 1);
     return rc ? DION2_ECUDA : DION2_OK;
   }
-  int allgather_sumsq() override {
+  int allgather_sumsq(cudaStream_t s) override {
     const int P = (int)D.size();
     int rc = 0;
     for (int r = 0; r < P; ++r)
       for (int r2 = 0; r2 < P; ++r2)
         rc |= cp(at(ws[r], D[r]->off_sumsq_all + (size_t)r2 * D[r]->n * 4), at(ws[r2], D[r2]->off_sumsq_local),
-                 (size_t)D[r]->n * 4);
+                 (size_t)D[r]->n * 4, s);
     bytes += (uint64_t)D[0]->n * 4 * (P - 1);
     return rc ? DION2_ECUDA : DION2_OK;
   }
-  int to_owners() override {
+  int to_owners(int ch, cudaStream_t s) override {
     const int P = (int)D.size();
     int rc = 0;
     for (int r = 0; r < P; ++r)
       for (int o = 0; o < P; ++o) {
-        rc |= cp(at(ws[o], D[o]->off_recv + (size_t)r * D[o]->R), at(ws[r], D[r]->off_send + D[r]->sdispl[o]),
-                 (size_t)D[r]->scount[o]);
-        if (o != 0 && r == 0) bytes += (uint64_t)D[0]->scount[o];
+        const int64_t off = D[o]->cdispl[o][ch], len = D[o]->cdispl[o][ch + 1] - off;
+        rc |= cp(at(ws[o], D[o]->off_recv + (size_t)r * D[o]->R + off), at(ws[r], D[r]->off_send + D[r]->sdispl[o] + off),
+                 (size_t)len, s);
+        if (o != 0 && r == 0) bytes += (uint64_t)len;
       }
     return rc ? DION2_ECUDA : DION2_OK;
   }
-  int from_owners() override {
+  int from_owners(int ch, cudaStream_t s) override {
     const int P = (int)D.size();
     int rc = 0;
     for (int o = 0; o < P; ++o)
       for (int r = 0; r < P; ++r) {
-        rc |= cp(at(ws[r], D[r]->off_orecv + D[r]->sdispl[o]), at(ws[o], D[o]->off_osend + (size_t)r * D[o]->R),
-                 (size_t)D[r]->scount[o]);
-        if (o == 0 && r != 0) bytes += (uint64_t)D[0]->R;
+        const int64_t off = D[o]->cdispl[o][ch], len = D[o]->cdispl[o][ch + 1] - off;
+        rc |= cp(at(ws[r], D[r]->off_orecv + D[r]->sdispl[o] + off), at(ws[o], D[o]->off_osend + (size_t)r * D[o]->R + off),
+                 (size_t)len, s);
+        if (o == 0 && r != 0) bytes += (uint64_t)len;
       }
     return rc ? DION2_ECUDA : DION2_OK;
   }
 };
 
+// library-owned side stream for the chunked exchanges (non-blocking, default priority)
+cudaStream_t comm_stream() {
+  static cudaStream_t st = nullptr;
+  if (!st) cudaStreamCreateWithFlags(&st, cudaStreamNonBlocking);
+  return st;
+}
+
+// One distributed step.  With one owner chunk everything runs on `s` in order
+// K1 -> C1 -> K2 -> K3 -> C2 -> NS -> C3 -> K7.  With C chunks the exchanges run on a side
+// stream: C2(0..C-1) back to back, the owner NS of chunk c on `s` once C2(c) has landed, and
+// C3(c) once NS(c) is done, so C2(c + 1) and C3(c - 1) overlap NS(c); `s` waits for the last
+// C3 before the sparse update.  All sizes are host-known (no host synchronisation).
 int run_dist(std::vector<DistPlan*>& plans, std::vector<void*>& wss, const std::vector<const dion2_shard*>& shards,
              const dion2_config* c, Transport& T, cudaStream_t s, uint64_t* bytes_out) {
   Launcher L{s};
   int rc = 0;
   const size_t R = plans.size();
+  const int C = plans[0]->nchunks;
   for (size_t i = 0; i < R; ++i)
     if ((rc = refresh(*plans[i], shards[i], c, s))) return rc;
   for (size_t i = 0; i < R; ++i) phase_local_k1(*plans[i], wss[i], L, s);
-  if ((rc = T.allgather_scores())) return rc;                       // C1
+  if ((rc = T.allgather_scores(s))) return rc;                      // C1
   for (size_t i = 0; i < R; ++i) phase_select(*plans[i], wss[i], c, L, s);
   for (size_t i = 0; i < R; ++i) phase_gather(*plans[i], wss[i], c, L, s);
-  if ((rc = T.allgather_sumsq())) return rc;
-  if ((rc = T.to_owners())) return rc;                              // C2
-  for (size_t i = 0; i < R; ++i) phase_owner_ns(*plans[i], wss[i], c, L, s);
-  if ((rc = T.from_owners())) return rc;                            // C3
+  if ((rc = T.allgather_sumsq(s))) return rc;
+  if (C == 1) {
+    if ((rc = T.to_owners(0, s))) return rc;                        // C2
+    for (size_t i = 0; i < R; ++i) phase_owner_ns(*plans[i], 0, wss[i], c, L, s);
+    if ((rc = T.from_owners(0, s))) return rc;                      // C3
+  } else {
+    static std::vector<cudaEvent_t> ev;  // [0] fork, [1 + c] C2(c) landed, [1 + C + c] NS(c) done, last: join
+    while ((int)ev.size() < 2 * C + 2) {
+      cudaEvent_t e;
+      cudaEventCreateWithFlags(&e, cudaEventDisableTiming);
+      ev.push_back(e);
+    }
+    cudaStream_t sc = comm_stream();
+    cudaEventRecord(ev[0], s);
+    cudaStreamWaitEvent(sc, ev[0], 0);
+    for (int ch = 0; ch < C; ++ch) {
+      if ((rc = T.to_owners(ch, sc))) return rc;                    // C2(ch)
+      cudaEventRecord(ev[1 + ch], sc);
+    }
+    for (int ch = 0; ch < C; ++ch) {
+      cudaStreamWaitEvent(s, ev[1 + ch], 0);
+      for (size_t i = 0; i < R; ++i) phase_owner_ns(*plans[i], ch, wss[i], c, L, s);
+      cudaEventRecord(ev[1 + C + ch], s);
+      cudaStreamWaitEvent(sc, ev[1 + C + ch], 0);
+      if ((rc = T.from_owners(ch, sc))) return rc;                  // C3(ch)
+    }
+    cudaEventRecord(ev[2 * C + 1], sc);
+    cudaStreamWaitEvent(s, ev[2 * C + 1], 0);
+  }
   for (size_t i = 0; i < R; ++i) phase_scatter(*plans[i], wss[i], c, L, s);
   g_last_launches = L.count;
   if (bytes_out) *bytes_out = T.bytes;
@@ -1036,7 +1112,7 @@ int dion2_step_batched_dist(const dion2_shard* shards, int32_t n, const dion2_co
   if ((rc = get_plan(&D, shards, n, cfg, world, rank, workspace, ws_bytes))) return rc;
   void* ws = reinterpret_cast<void*>(align_up(reinterpret_cast<uintptr_t>(workspace), 4096));
   cudaStream_t s = reinterpret_cast<cudaStream_t>(stream);
-  NcclTransport T(*D, ws, nccl_comm, s);
+  NcclTransport T(*D, ws, nccl_comm);
   std::vector<DistPlan*> plans{D};
   std::vector<void*> wss{ws};
   std::vector<const dion2_shard*> sh{shards};
@@ -1063,7 +1139,7 @@ int dion2_step_batched_loopback(const dion2_shard* shards, int32_t n, const dion
     sh[r] = shards + (size_t)r * n;
   }
   cudaStream_t s = reinterpret_cast<cudaStream_t>(stream);
-  LoopbackTransport T(plans, wss, s);
+  LoopbackTransport T(plans, wss);
   return run_dist(plans, wss, sh, cfg, T, s, comm_bytes_out);
 }
 
