@@ -180,7 +180,7 @@ std::string plan_key(const dion2_matrix* mats, int n, const dion2_config* c, voi
 std::string env_key() {
   std::string k;
   for (const char* v : {"DION2_NS_PAIR", "DION2_NS_SYM", "DION2_NS_SERPENTINE", "DION2_NS_UPPER",
-                        "DION2_GRAM_SPLITK", "DION2_GRAM_PF"}) {
+                        "DION2_GRAM_SPLITK", "DION2_GRAM_PF", "DION2_DIST_CHUNKS"}) {
     const char* e = getenv(v);
     k.append(e ? e : "-");
     k.push_back('|');

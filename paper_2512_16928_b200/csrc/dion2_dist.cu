@@ -178,10 +178,14 @@ int resolve(DistPlan& D, const dion2_shard* sh, int n, const dion2_config* c, in
     D.dm[j].owner = best;
     load[best] += D.dm[j].flops;
   }
-  // owner chunks (DION2_DIST_CHUNKS, default 2 when there is an exchange): each owner's matrices
-  // in descending NS FLOPs (ties -> lower index) dealt round-robin to the chunks
+  // owner chunks (DION2_DIST_CHUNKS, default 1): each owner's matrices in descending NS FLOPs
+  // (ties -> lower index) dealt round-robin to the chunks.  Measured in loopback on the 1B set
+  // (scripts/ab_dist_chunks.sh): 1 / 2 / 3 chunks -> 3.14 / 3.37 / 3.48 ms per rank at P = 2,
+  // 1.26 / 1.48 / 1.64 at P = 8 -- half-size NS batches (9 matrices per chunk at P = 8, under
+  // one wave) lose more than the overlapped exchange can win (~0.15 ms of NVLink per rank at
+  // P = 8), so the overlap is opt-in.
   const char* ce = getenv("DION2_DIST_CHUNKS");
-  D.nchunks = world > 1 ? std::max(1, ce ? atoi(ce) : 2) : 1;
+  D.nchunks = world > 1 ? std::max(1, ce ? atoi(ce) : 1) : 1;
   for (int o = 0; o < world; ++o) {
     int t = 0;
     for (int j : order)
