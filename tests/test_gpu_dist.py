@@ -91,3 +91,12 @@ def test_nccl_transport_single_rank():
         _assert(run_parity_dist(SHAPES + [(1024, 256)], 0.25, 1, steps=2, mode="nccl", m_transposed=True))
     finally:
         dist.destroy_process_group()
+
+
+@pytest.mark.parametrize("chunks,world", [("2", 2), ("3", 4)])
+def test_loopback_owner_chunks(chunks, world, monkeypatch):
+    """DION2_DIST_CHUNKS: owner chunks whose exchanges (C2 / C3) run on a side stream and overlap
+    the NS of the neighbouring chunk; sections ordered by chunk, in-place pieces per chunk."""
+    monkeypatch.setenv("DION2_DIST_CHUNKS", chunks)
+    _assert(run_parity_dist(SHAPES + [(1024, 256), (4096, 1024)], 0.25, world, steps=3, m_transposed=True))
+    _assert(run_parity_dist(layer_set_1b(1), 0.25, world, steps=2))
