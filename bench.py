@@ -291,7 +291,7 @@ def e2e_run(opt, Ws, Ms, Gs, G_flat, steps, ks):
     """End to end through the public API: pinned host G -> device, the step, and the
     selected index sets + status word read back, every step, inside the timed region."""
     import torch
-    host_G = torch.empty(G_flat.numel(), dtype=torch.float32, pin_memory=True)
+    host_G = torch.empty(G_flat.numel(), dtype=G_flat.dtype, pin_memory=True)
     host_G.copy_(G_flat.cpu())
     sel_dev = torch.empty(sum(ks), dtype=torch.int32, device=G_flat.device)
     sel_views, off = [], 0
@@ -324,7 +324,7 @@ def e2e_run(opt, Ws, Ms, Gs, G_flat, steps, ks):
     e1.record(s)
     torch.cuda.synchronize()
     rc, _ = opt.status()
-    return e0.elapsed_time(e1) / steps, G_flat.numel() * 4, sum(ks) * 4, rc
+    return e0.elapsed_time(e1) / steps, G_flat.numel() * G_flat.element_size(), sum(ks) * 4, rc
 
 
 def run_ours(args):
@@ -510,9 +510,22 @@ def run_ours(args):
 
     # end to end through the public API (host G)
     e2e_ms, h2d, d2h = None, None, None
+    e2e_bf16 = None
     if not args.no_e2e:
         e2e_ms, h2d, d2h, _ = e2e_run(opt, Ws, Ms, Gs, bufs[2], max(2, min(args.steps, 5)),
                                       select_counts(shapes, args.alpha))
+        if not use_dist:
+            # the same with bf16 gradients (mixed-precision training): half the PCIe bytes
+            Gb = bufs[2].to(torch.bfloat16)
+            Gbs, off = [], 0
+            for (m, n) in shapes:
+                Gbs.append(Gb[off:off + m * n].view(m, n))
+                off += m * n
+            ms_b, h2d_b, _, _ = e2e_run(opt, Ws, Ms, Gbs, Gb, max(2, min(args.steps, 5)),
+                                        select_counts(shapes, args.alpha))
+            e2e_bf16 = {"value": ms_b, "unit": "ms/step", "h2d_bytes_per_step": h2d_b}
+            del Gb, Gbs
+            torch.cuda.empty_cache()
     comm = None
     if use_dist:
         opt.step(Ws, Ms, Gs)
@@ -545,6 +558,7 @@ def run_ours(args):
             "ns_standard_equiv_tflops": ns_std_tflops,
             "ns_standard_equiv_frac_bf16_burst": ns_std_frac,
             "ns_ms_per_step": ns_ms,
+            "e2e_bf16_grad": e2e_bf16,
             "ms_per_step_eager": ms_eager,
             "ms_per_step_with_phase_events": ms_timed,
             "phases_note": "per-kernel times (CUDA events around every launch) from a separate K-step pass",
