@@ -105,3 +105,18 @@ def test_mma_flops_credit_only_the_computed_tiles():
     want = sum(0.75 * 2 * p * p * q + 2 * p * p * q + 0.75 * (ts + 3 * ts - 3) * 2 * p ** 3 for ts in (3, 2))
     assert f == want
     assert abs(bench.mma_flops(layer_set_1b(24), 0.25) / 1e12 - 1.488) < 0.001
+
+
+def test_gpus_flag_relaunches_under_torchrun(monkeypatch):
+    """`bench.py --gpus N` without WORLD_SIZE re-runs itself under torch.distributed.run with N
+    ranks on 127.0.0.1 (the driver's multi-GPU launch, done by the script itself)."""
+    calls = []
+    monkeypatch.setattr(bench.subprocess, "call", lambda cmd: calls.append(cmd) or 0)
+    monkeypatch.delenv("WORLD_SIZE", raising=False)
+    monkeypatch.setattr(sys, "argv", ["bench.py", "--gpus", "4", "--steps", "3"])
+    with pytest.raises(SystemExit) as e:
+        bench.main()
+    assert e.value.code == 0
+    cmd = calls[0]
+    assert cmd[1:3] == ["-m", "torch.distributed.run"] and "--nproc-per-node=4" in cmd
+    assert "--master-addr=127.0.0.1" in cmd and cmd[-4:] == ["--gpus", "4", "--steps", "3"]
