@@ -75,16 +75,24 @@ typedef enum {
 
 typedef enum { DION2_AXIS_ROWS = 0, DION2_AXIS_COLS = 1, DION2_AXIS_AUTO = 2 } dion2_axis;  /* P:181, P:273 */
 typedef enum { DION2_SELECT_L1 = 0, DION2_SELECT_RANDOM = 1 } dion2_select;                /* P:198-199 */
+/* Newton-Schulz arithmetic.  DION2_NS_BF16 (= DION2_NS_TC16, the name kept from ABI v1-v5) is the
+   tcgen05 tensor-core path: since ABI v6 its operands are fp16 (10-bit mantissa) with fp32
+   accumulation, X stored as fp16(2^e X) with a power-of-two prescale chosen from the matrix's
+   largest l1 score so no entry can overflow (reading R24); FP32 is the SIMT fp32 validation path. */
 typedef enum { DION2_NS_BF16 = 0, DION2_NS_FP32 = 1 } dion2_precision;
+#define DION2_NS_TC16 DION2_NS_BF16
 typedef enum { DION2_DT_F32 = 0, DION2_DT_BF16 = 1 } dion2_dtype;
-/* How the BF16 Newton-Schulz map is evaluated (reading R23).  Both forms compute the same
-   polynomial map X_T = p_T(... p_1(X_0)) of Alg. 1 l.4; they differ only in rounding.
-   DIRECT: T iterations on X (p x q): A = X X^T, C = a I + b A + c A^2, X <- C X (bf16).
-   GRAM:   the iteration carried out on p x p matrices: A_0 = X_0 X_0^T once, then
-           C_t = a I + b A_t + c A_t^2, Q_{t+1} = C_t Q_t, A_{t+1} = C_t (C_t A_t) in fp16
-           with fp32 accumulation, and X_T = Q_T X_0 once (bf16).  Fewer FLOPs when q >= 2p.
+/* How the tensor-core Newton-Schulz map is evaluated (readings R23, R24).  Both forms compute
+   the same polynomial map X_T = p_T(... p_1(X_0)) of Alg. 1 l.4; they differ only in rounding.
+   DIRECT: T iterations on X (p x q): A = X X^T, C = a I + b A + c A^2, X <- C X (fp16).
+   GRAM:   the iteration carried out on p x p matrices, in restart segments of consecutive
+           iterations whose growth prod |a_t| stays <= 64 ([0,3) + [3,5) for the default quintic):
+           per segment A = X_in X_in^T once, then C_t = a I + b A_t + c A_t^2,
+           Q_{t+1} = C_t Q_t, A_{t+1} = C_t (C_t A_t) (fp16, fp32 accumulation), and
+           X_out = Q X_in once.  Fewer FLOPs when q >= 2p (1.85x at p = 512, q in {2048, 8192}).
    AUTO:   GRAM for a shape group whose padded X has q_pad >= 2 p_pad or whose every member has
-           q >= 2p, DIRECT otherwise. */
+           q >= 2p, DIRECT otherwise.  Both forms meet the 2e-2 parity gate on Gaussian and on
+           ill-conditioned (spiked / power-law) momenta (tests/test_gpu_conditioning.py). */
 typedef enum { DION2_NS_FORM_AUTO = 0, DION2_NS_FORM_DIRECT = 1, DION2_NS_FORM_GRAM = 2 } dion2_ns_form;
 
 /* One weight matrix and its optimizer state. */
@@ -125,7 +133,8 @@ typedef struct {
   int32_t select;     /* dion2_select, default L1 (largest l1 norm).  RANDOM: the k indices
                          with the smallest keys Philox4x32-10(ctr = (index, step_lo, step_hi, matrix id in
                          the batch), key = (seed_lo, seed_hi)) word 0, lower index on ties (reading R22) */
-  int32_t precision;  /* dion2_precision: BF16 = tcgen05 tensor-core NS (hot path); FP32 = SIMT fp32 NS (validation) */
+  int32_t precision;  /* dion2_precision: BF16 (= TC16) = tcgen05 tensor-core NS on fp16 operands (hot path);
+                         FP32 = SIMT fp32 NS (validation) */
   int32_t grad_dtype; /* dion2_dtype of G, default F32 */
   int32_t decay_mode; /* 0 = selective decay Eq. (error-feedback) (paper); 1 = full decay M <- mu*M (ablation) */
   int32_t scale_mode; /* 0 = eta*sqrt(rows/cols) of the full W (Alg. 1 l.6); 1 = sqrt of the submatrix dims (SPEC S:360 flag) */
@@ -193,14 +202,14 @@ const char* dion2_phase_name(int32_t i);
  *   1. M <- M + G and partial l1 scores on the local shard            (K1, local)
  *   2. all-gather of the partial scores, summed in rank order         (NCCL; identical on all ranks)
  *   3. top-k on every rank (identical K everywhere; no index traffic)  (K2)
- *   4. X-piece = wide(M[K])[:, this rank's block] (k x o/P, bf16), local selective decay
+ *   4. X-piece = wide(M[K])[:, this rank's block] (k x o/P, fp16 with the prescale of R24), local selective decay
  *   5. pieces -> owner of the matrix (grouped ncclSend/ncclRecv)      (bytes ~ alpha)
  *   6. owner: assemble X, Newton-Schulz, split O into pieces           (tcgen05 NS)
  *   7. O pieces -> back to every rank; local W[K] update              (K7, local)
  * Owners are assigned by LPT on NS FLOPs, identically on every rank.  All sizes are known on the
  * host, so nothing synchronises the host inside a step.  Requirements: the sharded dimension
  * divisible by P; rows mode n/P % 8 == 0; cols mode m/P % 32 == 0 and k <= 1024; k <= the other
- * dimension (always true in auto mode); bf16 NS.  Otherwise DION2_EUNSUPPORTED.
+ * dimension (always true in auto mode); tensor-core NS.  Otherwise DION2_EUNSUPPORTED.
  * ------------------------------------------------------------------------------------------ */
 typedef struct {
   int64_t rows;        /* GLOBAL m = fan-out */
