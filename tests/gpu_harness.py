@@ -165,7 +165,8 @@ def _finish(res, shapes, Wg, Mg, Wr, Mr, W0):
 
 
 def run_parity_dist(shapes, alpha, world, steps=3, seed=0, mode="loopback", axis="auto", mu=0.95, lr=0.02,
-                    row_scaled=True, device="cuda", select="l1", sel_seed=0, m_transposed=False):
+                    row_scaled=True, device="cuda", select="l1", sel_seed=0, m_transposed=False,
+                    structure: Optional[dict] = None):
     """Distributed step (owner-compute, shards along the non-selection axis) against the
     fp64 oracle on the FULL matrices.  mode = "loopback" (all ranks in this process) or
     "nccl" (world must equal the initialised torch.distributed world; this process is
@@ -211,7 +212,10 @@ def run_parity_dist(shapes, alpha, world, steps=3, seed=0, mode="loopback", axis
         return torch.cat(blocks, dim=1 if axes[i] == 0 else 0)
 
     for t in range(steps):
-        G = [gen_grad(m, n, seed, i, t, row_scaled=row_scaled) for i, (m, n) in enumerate(shapes)]
+        if structure:
+            G = [gen_grad_structured(m, n, seed, i, t, **structure) for i, (m, n) in enumerate(shapes)]
+        else:
+            G = [gen_grad(m, n, seed, i, t, row_scaled=row_scaled) for i, (m, n) in enumerate(shapes)]
         Gg = {r: [D.shard_of(full(G[i], i), axes[i], world, r).to(device) for i in range(len(shapes))] for r in ranks}
         sel = {r: [torch.empty(k, dtype=torch.int32, device=device) for k in ks] for r in ranks}
         if mode == "loopback":

@@ -79,3 +79,24 @@ def test_tiny_and_huge_momenta(mag):
         _check(run_parity([(1024, 2048), (2048, 1024)], 0.25, "auto", "bf16", steps=2))
     finally:
         gpu_harness.gen_grad = orig
+
+
+@pytest.mark.parametrize("world", [2, 8])
+def test_distributed_step_on_spiked_momenta(world):
+    """The owner-compute step (loopback ranks): pieces carry the fp16 prescale of every rank's
+    identical select, the owner folds it into its norm (R24), in-place pieces with the restart."""
+    from gpu_harness import run_parity_dist
+    res = run_parity_dist([(2048, 2048), (2048, 8192), (8192, 2048)], 0.25, world, steps=2,
+                          structure=dict(kind="spike", rank=4, ratio=100))
+    assert res.index_mismatch == 0 and max(res.dW_rel) <= GATE and max(res.M_rel) <= 1e-5, res
+
+
+def test_random_selection_on_power_law_momenta():
+    _check(run_parity([(2048, 2048), (8192, 2048)], 0.25, "auto", "bf16", steps=2, select="random", sel_seed=7,
+                      structure=dict(kind="power", gamma=1.0)))
+
+
+@pytest.mark.parametrize("kw", [dict(grad_bf16=True), dict(storage_transposed=True), dict(m_transposed=True)])
+def test_layout_variants_on_spiked_momenta(kw):
+    _check(run_parity([(1024, 4096), (4096, 1024)], 0.25, "auto", "bf16", steps=2,
+                      structure=dict(kind="spike", rank=16, ratio=100), **kw))
