@@ -100,3 +100,9 @@ def test_random_selection_on_power_law_momenta():
 def test_layout_variants_on_spiked_momenta(kw):
     _check(run_parity([(1024, 4096), (4096, 1024)], 0.25, "auto", "bf16", steps=2,
                       structure=dict(kind="spike", rank=16, ratio=100), **kw))
+
+
+def test_p1024_on_spiked_momenta():
+    """The 8B set's p = 1024 shapes (Wq / Wo 4096 x 4096 at alpha = 1/4: Gram form with the
+    restart, the 1-SM apply since p_pad > 512) on a rank-4 spike."""
+    _check(run_parity([(4096, 4096)], 0.25, "auto", "bf16", steps=2, structure=dict(kind="spike", rank=4, ratio=100)))
