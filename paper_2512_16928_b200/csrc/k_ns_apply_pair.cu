@@ -26,7 +26,11 @@ namespace dion2 {
 namespace {
 
 constexpr int kBK = 64;
-constexpr int kStages = 4;
+// 5 B stages (80 KB of X in flight per CTA) and one 2 KB epilogue staging buffer per warp: the
+// resident A takes 128 KB, and X streams from DRAM at a rate set by the bytes in flight
+// (profiles/r02_tma_box_microbench.txt: 64 KB per SM -> 3.2 TB/s, 128 KB -> 6 TB/s)
+constexpr int kStages = 5;
+constexpr int kStgBufs = 1;
 constexpr int kEpiWarps = 8;
 constexpr int kThreads = 64 + 32 * kEpiWarps;
 constexpr uint32_t kABlk = 128 * kBK * 2;    // one resident A k-block per CTA (128 rows x 64 k)
@@ -38,7 +42,7 @@ constexpr int kAOff = 0;
 constexpr int kBOff = kMaxResidentKB * (int)kABlk;
 constexpr int kBarOff = kBOff + kStages * (int)kBB;
 constexpr int kStageOff = kBarOff + 1024;
-constexpr int kSmem = 1024 + kStageOff + kEpiWarps * 2 * 2048;
+constexpr int kSmem = 1024 + kStageOff + kEpiWarps * kStgBufs * 2048;
 
 struct Chunk {
   int group, z, tm, tn0, len;
@@ -231,8 +235,8 @@ __global__ void __cluster_dims__(2, 1, 1) __launch_bounds__(kThreads, 1)
       for (int cc32 = c0; cc32 < c0 + 4; ++cc32) {
         float v[32];
         tmem_ld_32x32b_x32(tmem_base + acc * 256 + cc32 * 32 + ((uint32_t)(lg * 32) << 16), v);
-        uint8_t* buf = stage_base + (ew * 2 + sbuf) * 2048;
-        if (lane == 0) bulk_wait_read<1>();  // the store issued from this buffer two chunks ago has read it
+        uint8_t* buf = stage_base + (ew * kStgBufs + sbuf) * 2048;
+        if (lane == 0) bulk_wait_read<kStgBufs - 1>();  // the store that last used this buffer has read it
         __syncwarp();
         uint32_t pk[16];
 #pragma unroll
@@ -254,7 +258,7 @@ __global__ void __cluster_dims__(2, 1, 1) __launch_bounds__(kThreads, 1)
           }
           bulk_commit();
         }
-        sbuf ^= 1;
+        sbuf = (sbuf + 1) % kStgBufs;
       }
       tc_fence_before();
       __syncwarp();
