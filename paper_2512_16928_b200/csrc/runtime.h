@@ -74,7 +74,8 @@ struct Group {
 struct Launch {
   int phase;
   int bn;
-  int kind;  // 0 = tc BN128, 1 = tc BN256, 2 = simt, 3 = 2-SM pair, 5 = 2-SM apply with resident A
+  int kind;  // 0 = tc BN128, 1 = tc BN256, 2 = simt, 3 = 2-SM pair, 5 = 2-SM apply with A in smem,
+             // 6 = 2-SM apply with A in TMEM
   NsTcParams tc;
   int simt_group;
 };
