@@ -354,14 +354,14 @@ static int gram_prefetch_ahead() {
 
 // Kind-5 launches (resident-A pair apply) count work in chunks of up to L consecutive 256-column
 // blocks of one 256-row block: L = 8, halved while the launch has fewer than two chunks per CTA pair.
-static void apply_chunks(NsParams& np, int L0 = 8) {
+static void apply_chunks(NsParams& np) {
   const int pairs = sm_count() / 2;
   auto count = [&](int L) {
     int n = 0;
     for (int j = 0; j < np.ngroups; ++j) n += np.g[j].count * ((np.g[j].n_tiles + L - 1) / L) * np.g[j].m_tiles;
     return n;
   };
-  int L = L0;
+  int L = 8;
   while (L > 1 && count(L) < 2 * pairs) L /= 2;
   np.chunk_len = L;
   int base = 0;
@@ -431,14 +431,14 @@ static int append_gram_space_launches(Plan& P, const dion2_config* c, void* ws, 
     const bool apply = phase == PH_APPLY;
     for (size_t s0 = 0; s0 < es.size(); s0 += kMaxGroups) {
       const size_t s1 = std::min(es.size(), s0 + kMaxGroups);
-      bool res_ok = apply && (pair_mode == 1 || pair_mode == 4);
+      bool res_ok = apply && pair_mode == 1;
       for (size_t e = s0; e < s1; ++e) res_ok = res_ok && P.groups[es[e].gi].p_pad <= 64 * kMaxResidentKB;
       const bool pair = !apply || pair_mode == 2 || res_ok;
       const int MT = pair ? 256 : 128, BN = 256;
       Launch L{};
       L.phase = phase;
       L.bn = BN;
-      L.kind = res_ok ? (pair_mode == 4 ? 6 : 5) : (pair ? 3 : 1);
+      L.kind = res_ok ? 5 : (pair ? 3 : 1);
       NsParams& np = L.tc.p;
       np.ngroups = (int)std::min<size_t>(kMaxGroups, es.size() - s0);
       np.ns_scale_all = scale_all;
@@ -465,7 +465,7 @@ static int append_gram_space_launches(Plan& P, const dion2_config* c, void* ws, 
         G.count = g.count;
         G.gmats = (const int32_t*)tab(P, g.off_gmats);
         G.m_tiles = g.p_pad / MT;
-        G.n_tiles = apply ? g.q_pad / (L.kind == 6 ? 128 : BN) : g.p_pad / BN;
+        G.n_tiles = apply ? g.q_pad / BN : g.p_pad / BN;
         G.k_blocks = K / 64;
         G.a = e.a; G.a_mstride = phase == PH_GRAM ? xs : as; G.lda = K;
         G.b = e.b; G.b_mstride = (phase == PH_GRAM || apply) ? xs : as; G.ldb = apply ? g.q_pad : K;
@@ -490,7 +490,6 @@ static int append_gram_space_launches(Plan& P, const dion2_config* c, void* ws, 
       np.b_is_a = np.b_kmajor ? 1 : 0;
       for (int j = 0; j < np.ngroups; ++j) np.b_is_a &= np.g[j].a == np.g[j].b ? 1 : 0;
       if (L.kind == 5) apply_chunks(np);
-      if (L.kind == 6) apply_chunks(np, 16);
       if (phase == PH_GRAM) np.pf_ahead = gram_prefetch_ahead();
       P.ns_launches.push_back(L);
     }
@@ -699,17 +698,15 @@ int build_device_plan(Plan& P, const dion2_matrix* mats, const dion2_config* c, 
   const int pair_mode = !pair_env ? 1
                                   : (strcmp(pair_env, "all") == 0 ? 2
                                                                   : (strcmp(pair_env, "none") == 0 ? 0
-                                                                                                   : (strcmp(pair_env, "1sm_apply") == 0 ? 3
-                                                                                                      : (strcmp(pair_env, "tmem_apply") == 0 ? 4 : 1))));
+                                                                                                   : (strcmp(pair_env, "1sm_apply") == 0 ? 3 : 1)));
   for (int t = 0; t < P.ns_steps; ++t) {
     const float a = c->ns_coeffs[t][0], b = c->ns_coeffs[t][1], cc = c->ns_coeffs[t][2];
     for (int ph = PH_GRAM; ph <= PH_APPLY; ++ph) {
       // apply: the 2-SM kernel with A resident for p_pad <= 512 (k_ns_apply_pair.cu)
-      bool res_all = P.bf16_ns && ph == PH_APPLY && (pair_mode == 1 || pair_mode == 4);  // (3: the 1-SM apply)
+      bool res_all = P.bf16_ns && ph == PH_APPLY && pair_mode == 1;  // (3: the 1-SM apply)
       for (const Group& g : P.groups)
         if (!g.gs) res_all = res_all && g.p_pad <= 64 * kMaxResidentKB;
-      const bool pair = P.bf16_ns && (pair_mode == 2 || ((pair_mode == 1 || pair_mode == 3 || pair_mode == 4) &&
-                                                         (ph != PH_APPLY || res_all)));
+      const bool pair = P.bf16_ns && (pair_mode == 2 || ((pair_mode == 1 || pair_mode == 3) && (ph != PH_APPLY || res_all)));
       // gram and poly outputs are symmetric: the pair kernel computes upper-triangle tiles
       // only and mirrors them (DION2_NS_SYM=0 disables)
       const bool sym = pair && ph != PH_APPLY && !(getenv("DION2_NS_SYM") && atoi(getenv("DION2_NS_SYM")) == 0);
@@ -729,7 +726,7 @@ int build_device_plan(Plan& P, const dion2_matrix* mats, const dion2_config* c, 
           Launch L{};
           L.phase = ph;
           L.bn = BN;
-          L.kind = P.bf16_ns ? (res_all ? (pair_mode == 4 ? 6 : 5) : (pair ? 3 : cls)) : 2;
+          L.kind = P.bf16_ns ? (res_all ? 5 : (pair ? 3 : cls)) : 2;
           NsParams& np = L.tc.p;
           np.ngroups = (int)std::min<size_t>(kMaxGroups, gl.size() - s0);
           np.ns_scale_all = scale_all;
@@ -800,7 +797,6 @@ int build_device_plan(Plan& P, const dion2_matrix* mats, const dion2_config* c, 
           np.b_is_a = np.b_kmajor ? 1 : 0;
           for (int j = 0; j < np.ngroups; ++j) np.b_is_a &= np.g[j].a == np.g[j].b ? 1 : 0;
           if (L.kind == 5) apply_chunks(np);
-          if (L.kind == 6) apply_chunks(np, 16);
           if (ph == PH_GRAM) np.pf_ahead = gram_prefetch_ahead();
           if (P.bf16_ns) {
             P.ns_launches.push_back(L);
@@ -828,7 +824,6 @@ void ensure_device_attrs() {
   launch_fast_paths_attrs();
   ns_pair_set_attrs();
   ns_apply_pair_set_attrs();
-  ns_apply_tmem_set_attrs();
   cudaFuncSetAttribute(k_topk_select, cudaFuncAttributeMaxDynamicSharedMemorySize, 4 * DION2_MAX_SELECT_DIM);
   cudaFuncSetAttribute(k_full_decay, cudaFuncAttributeMaxDynamicSharedMemorySize, DION2_MAX_SELECT_DIM);
   g_attr_done = true;
@@ -848,8 +843,6 @@ int run_ns(Plan& P, const dion2_config* c, Launcher& L, cudaStream_t s, bool do_
     L.begin(ln.phase);
     if (ln.kind == 5) {
       launch_ns_apply_pair(std::min(2 * ln.tc.p.total_tiles, sms & ~1), s, ln.tc);
-    } else if (ln.kind == 6) {
-      launch_ns_apply_tmem(std::min(2 * ln.tc.p.total_tiles, sms & ~1), s, ln.tc);
     } else if (ln.kind == 3) {
       const int sk = ln.tc.p.splitk > 1 ? ln.tc.p.splitk : 1;
       launch_ns_pair(std::min(2 * ln.tc.p.total_tiles * sk, sms & ~1), s, ln.tc);

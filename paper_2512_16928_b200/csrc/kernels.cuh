@@ -175,10 +175,6 @@ void launch_splitk_reduce(cudaStream_t s, const NsParams& p);  // after a split-
 constexpr int kMaxResidentKB = 8;
 void ns_apply_pair_set_attrs();
 void launch_ns_apply_pair(int grid, cudaStream_t s, const NsTcParams& P);
-// apply with A resident in TMEM (k_ns_apply_tmem.cu): p_pad <= 512, m_tiles = p_pad / 256,
-// n_tiles = q_pad / 128, chunks as kind 5
-void ns_apply_tmem_set_attrs();
-void launch_ns_apply_tmem(int grid, cudaStream_t s, const NsTcParams& P);
 
 template <int BN>
 constexpr int ns_tc_stages() { return BN == 256 ? 4 : 6; }

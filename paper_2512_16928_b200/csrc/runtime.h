@@ -74,8 +74,7 @@ struct Group {
 struct Launch {
   int phase;
   int bn;
-  int kind;  // 0 = tc BN128, 1 = tc BN256, 2 = simt, 3 = 2-SM pair, 5 = 2-SM apply with A in smem,
-             // 6 = 2-SM apply with A in TMEM
+  int kind;  // 0 = tc BN128, 1 = tc BN256, 2 = simt, 3 = 2-SM pair, 5 = 2-SM apply with resident A
   NsTcParams tc;
   int simt_group;
 };
