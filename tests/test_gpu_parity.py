@@ -603,3 +603,13 @@ def test_bf16_weights(form):
             else:
                 assert np.array_equal(wg[:, unsel], W_before[i][:, unsel])
             assert np.abs(Ms[i].double().cpu().numpy() - Mr).max() <= 1e-6 * np.abs(Mr).max()
+
+
+@pytest.mark.parametrize("variant", ["1sm_apply", "all"])
+def test_apply_kernel_variants(variant, monkeypatch):
+    """The apply kernels selectable for A/B (DION2_NS_PAIR): the 1-SM kernel and the streaming
+    pair kernel instead of the resident-A pair apply; both NS forms, p_pad 256 and 512, ragged q."""
+    monkeypatch.setenv("DION2_NS_PAIR", variant)
+    shapes = [(512, 2048), (2048, 512), (1024, 4096), (300, 1200), (1024, 1024)]
+    _assert(run_parity(shapes, 0.25, "auto", "bf16", steps=2, row_scaled=True), BF16_TOL)
+    _assert(run_parity(shapes[:3], 0.25, "auto", "bf16", steps=2, ns_form="direct"), BF16_TOL)
