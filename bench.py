@@ -436,7 +436,9 @@ def run_ours(args):
     roof["peak_source"] = f"MEASURED_PEAKS.json ({peak_src}, burst)"
     roof["timing"] = "CUDA events around each launch on the launching stream, separate K-step pass"
     trafp = os.path.join(ROOT, "profiles", "traffic.json")
-    if os.path.exists(trafp):
+    # the committed ncu traffic is per launch of the single-GPU 1B step (one launch per phase)
+    if os.path.exists(trafp) and not use_dist and args.config == "1b" and not args.layers \
+            and de["launches_per_step"] == 1:
         with open(trafp) as f:
             tr = json.load(f)
         if dom in tr:
