@@ -6,14 +6,17 @@
 Workload (N = 1): BASELINE configs[1], the 1B-class transformer matrix set
 (24 layers of Wq, Wk, Wv, Wo 2048x2048, W_up 8192x2048, W_down 2048x8192;
 144 matrices, 1.208 B parameters), fp32 W / M / G, alpha = 0.25, auto axis,
-5 Newton-Schulz steps on the bf16 tcgen05 path.  One "step" = one Dion2
+5 Newton-Schulz steps on the tcgen05 path (fp16 operands, fp32 accumulation;
+DESIGN.md R24).  One "step" = one Dion2
 update of every matrix (Alg. 1 over the whole model).  Synthetic data:
 W0 ~ N(0, 1/n), G ~ N(0, 1) from a seeded generator, M0 = 0.  The inputs
 (14.5 GB touched per step) are far larger than L2 (126 MB), so no flush is
 needed between steps.  The same library at alpha = 1 (full Muon) is timed
 beside it, as is the fp64 oracle on the host cores (cpu_baseline).
 
-Prints ONE JSON line (rank 0).
+Prints ONE JSON line (rank 0); per-phase times and the sweeps go to the sidecar
+gpurun_out/bench_details_<config>_n<N>.json.  `--gpus N` without torchrun re-launches
+this script under torch.distributed.run (one rank per GPU, owner-compute step).
 """
 from __future__ import annotations
 
