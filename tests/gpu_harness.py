@@ -247,3 +247,47 @@ def run_parity_dist(shapes, alpha, world, steps=3, seed=0, mode="loopback", axis
     _finish(res, shapes, Wfull, Mfull, Wr, Mr, W0)
     res.comm_bytes = opt.last_comm_bytes
     return res
+
+
+def run_parity_fsdp(shapes, alpha, steps=3, seed=0, mu=0.95, lr=0.02, m_transposed=True, select="l1"):
+    """The FSDP2 integration (paper_2512_16928_b200.fsdp): one bias-free Linear per (out, in)
+    shape, `fully_shard` with `dion2_placement()` on the initialised torch.distributed world,
+    gradients set as DTensors in the parameters' placements, `Dion2FSDP.step`, against the
+    fp64 oracle on the full matrices (p.full_tensor()).  Index sets are not exposed by the
+    optimizer: a near-tie would show as a dW mismatch (gen_grad is row-scaled: none occur)."""
+    import torch.distributed as dist
+    from torch.distributed.device_mesh import init_device_mesh
+    from torch.distributed.fsdp import fully_shard
+    from torch.distributed.tensor import distribute_tensor
+    from paper_2512_16928_b200.fsdp import Dion2FSDP, dion2_placement
+    res = ParityResult()
+    cfg_o = oracle_cfg(alpha, "auto", mu, lr)
+    cfg_o.select = select
+    mesh = init_device_mesh("cuda", (dist.get_world_size(),))
+    model = torch.nn.Sequential(*[torch.nn.Linear(n, m, bias=False) for (m, n) in shapes]).cuda()  # never called
+    W0 = [gen_w0(m, n, seed, i) for i, (m, n) in enumerate(shapes)]
+    with torch.no_grad():
+        for lin, w in zip(model, W0):
+            lin.weight.copy_(torch.from_numpy(w))
+    fully_shard(model, mesh=mesh, shard_placement_fn=dion2_placement(alpha=alpha))
+    params = [lin.weight for lin in model]
+    opt = Dion2FSDP(params, lr=lr, mu=mu, alpha=alpha, m_transposed=m_transposed, select=select)
+    Wr = [w.astype(np.float64) for w in W0]
+    Mr = [np.zeros((m, n)) for (m, n) in shapes]
+    for t in range(steps):
+        G = [gen_grad(m, n, seed, i, t, row_scaled=True) for i, (m, n) in enumerate(shapes)]
+        for p, g in zip(params, G):
+            p.grad = distribute_tensor(torch.from_numpy(g).cuda(), mesh, p.placements)
+        opt.step()
+        cfg_o.step = t
+        for i in range(len(shapes)):
+            O.dion2_step(Wr[i], Mr[i], G[i].astype(np.float64), cfg_o, matrix_id=i)
+    torch.cuda.synchronize()
+    Wfull = [p.full_tensor().detach() for p in params]
+    for i in range(len(shapes)):
+        wg = Wfull[i].cpu().numpy().astype(np.float64)
+        dref = Wr[i] - W0[i].astype(np.float64)
+        res.dW_rel.append(float(np.linalg.norm(wg - W0[i] - dref) / max(np.linalg.norm(dref), 1e-300)))
+        res.W_rel.append(float(np.linalg.norm(wg - Wr[i]) / np.linalg.norm(Wr[i])))
+    res.comm_bytes = opt.comm_bytes()
+    return res

@@ -4,6 +4,7 @@ One process per GPU (torch.multiprocessing, spawn), NCCL over NVLink, 127.0.0.1 
   * the owner-compute step (dion2_step_batched_dist): each rank holds only its shards, the
     pieces travel through grouped ncclSend / ncclRecv, and the full matrices re-assembled on
     rank 0 match the fp64 oracle (gpu_harness.run_parity_dist, mode "nccl");
+  * the FSDP2 integration (fully_shard with dion2_placement + Dion2FSDP) against the oracle;
   * compressed DP-sync (dion2_step_batched_dpsync): replicas with different local gradients
     stay bit-identical and match the oracle's replica model.
 The single-GPU suite covers the same code in loopback (test_gpu_dist.py, test_gpu_dpsync.py).
@@ -43,6 +44,10 @@ def _worker(rank, world, port, which, errq):
                     res = run_parity_dist(shapes, 0.25, world, steps=3, mode="nccl", m_transposed=mt)
                     assert res.index_mismatch == 0 and max(res.dW_rel) <= 2e-2 and max(res.M_rel) <= 1e-5, res
                     assert res.comm_bytes > 0
+            elif which == "fsdp":
+                from gpu_harness import run_parity_fsdp
+                res = run_parity_fsdp([(256, 512), (512, 256), (1024, 1024), (2048, 512), (512, 2048)], 0.25)
+                assert max(res.dW_rel) <= 2e-2 and res.comm_bytes > 0, res
             else:
                 import test_gpu_dpsync as T
                 T._run(world, "bf16", 2e-2, mode="nccl")
@@ -55,7 +60,7 @@ def _worker(rank, world, port, which, errq):
         raise
 
 
-@pytest.mark.parametrize("which", ["dist", "dpsync"])
+@pytest.mark.parametrize("which", ["dist", "dpsync", "fsdp"])
 def test_world2_nccl(which):
     import torch.multiprocessing as mp
     ctx = mp.get_context("spawn")
