@@ -360,8 +360,12 @@ def run_ours(args):
         info = D.dist_info(shapes, world, rank, alpha=args.alpha, m_transposed=mts)
         bufs, Ws, Ms, Gs = build_state(info["shard"], dev, seed=rank, fan_in=[n for (_, n) in shapes],
                                        m_transposed=mts)
+        # pieces by direct peer stores / loads over NCCL symmetric memory (DION2_FLAG_DIST_DIRECT:
+        # K3 pushes into the owner's window, K7 pulls O; the library falls back to NCCL send /
+        # recv where that is unavailable); DION2_BENCH_DIRECT=0 forces send / recv
+        direct = os.environ.get("DION2_BENCH_DIRECT", "1") == "1"
         make_opt = lambda a: D.Dion2Dist(shapes, alpha=a, axis="auto", precision="bf16",  # noqa: E731
-                                          ns_form=args.ns_form, m_transposed=mts)
+                                          ns_form=args.ns_form, m_transposed=mts, dist_direct=direct)
     else:
         info = None
         # optimizer-state layout: momentum of column-mode matrices stored transposed (the
@@ -376,6 +380,8 @@ def run_ours(args):
         ms = time_steps(opt, Ws, Ms, Gs, args.steps, args.warmup, barrier)
     launches = last_launch_count() * args.steps
     rc, bad = opt.status()
+    # the exchange the distributed plan actually uses (direct peer memory, or NCCL send / recv)
+    xmode = ("direct peer-memory" if opt.exchange_mode() == "direct" else "NCCL send/recv") if use_dist else None
     if rc != 0:
         raise RuntimeError(f"status {rc} (matrix {bad})")
 
@@ -594,7 +600,7 @@ def run_ours(args):
                        "ns_form": args.ns_form,
                        "l2_flush": f"not needed: {12 * n_params / 1e9:.1f} GB touched per step >> 126 MB L2",
                        "parallelism": "single GPU" if not use_dist else
-                       f"owner-compute over {world} GPUs (NCCL; shards along the non-selection axis)",
+                       f"owner-compute over {world} GPUs ({xmode} exchange; shards along the non-selection axis)",
                        "step_mode": "CUDA graph" if (not use_dist and not args.no_graph) else "eager"},
             "roofline": roof,
             "cpu_baseline": cpu,

@@ -50,7 +50,7 @@
 extern "C" {
 #endif
 
-#define DION2_ABI_VERSION 6
+#define DION2_ABI_VERSION 7
 #define DION2_MAX_NS_STEPS 16
 /* dion2_config.reserved0 flag: the sparse update reads eta on the device from the fp32 word at
    byte offset 8 of the workspace's 4096-byte-aligned base (the first multiple of 4096 at or
@@ -58,6 +58,16 @@ extern "C" {
    instead of cfg.lr, so a CUDA graph of the step follows a learning-rate schedule without being
    re-captured.  cfg.lr must still be a valid eta (it is validated, then ignored by the kernels). */
 #define DION2_FLAG_LR_DEVICE 1
+/* dion2_config.reserved0 flag (ABI v7), read by dion2_step_batched_dist / _loopback only:
+   the exchange pieces travel by direct peer stores and loads instead of NCCL send / recv
+   (the fused gather + send).  K3 stores each piece of X straight into its
+   owner's receive buffer and K7 loads its piece of O straight from the owner's outgoing buffer;
+   with NCCL these are symmetric-memory windows (ncclMemAlloc + ncclCommWindowRegister, NCCL
+   >= 2.28 device API) separated by LSA barriers, allocated collectively on the first step of a
+   plan and kept for the process lifetime; in loopback they are the other ranks' workspaces.
+   Requires every rank in one load/store (NVLink) domain, else DION2_EUNSUPPORTED; forces one
+   owner chunk.  Results are bitwise those of the NCCL exchange (same kernels, same bytes). */
+#define DION2_FLAG_DIST_DIRECT 2
 
 typedef enum {
   DION2_OK = 0,
@@ -141,7 +151,7 @@ typedef struct {
   uint64_t seed;      /* random selection key (unused for L1) */
   uint64_t step;      /* random selection counter: the caller's step index (unused for L1) */
   int32_t ns_form;    /* dion2_ns_form, default AUTO (BF16 precision only; FP32 is always DIRECT) */
-  int32_t reserved0;  /* flags: 0, or DION2_FLAG_LR_DEVICE (other bits must be 0) */
+  int32_t reserved0;  /* flags: 0, DION2_FLAG_LR_DEVICE, DION2_FLAG_DIST_DIRECT (other bits must be 0) */
   int32_t w_dtype;    /* dion2_dtype of W (ABI v6): F32 (default) or BF16 -- bf16 weights; the update
                          is computed in fp32 and rounded to nearest once (w <- bf16(float(w) - s o)).
                          M stays fp32 (its l1 scores decide the selection) */
@@ -244,6 +254,13 @@ int dion2_dist_info(const dion2_shard* shards, int32_t n, const dion2_config* cf
 int dion2_step_batched_dist(const dion2_shard* shards, int32_t n, const dion2_config* cfg, void* workspace,
                             size_t ws_bytes, void* nccl_comm, int32_t world, int32_t rank, void* stream,
                             uint64_t* comm_bytes_out);
+
+/* Exchange mode of the distributed plan last built on `workspace` (the same pointer passed to
+ * dion2_step_batched_dist): 1 = direct peer stores / loads over symmetric memory
+ * (DION2_FLAG_DIST_DIRECT honoured), 0 = NCCL send / recv (flag unset, or the fallback when the
+ * NCCL device API or a single NVLink domain is unavailable -- decided identically on every
+ * rank), -1 = no distributed plan on that workspace.  Host-only. */
+int dion2_dist_exchange_mode(const void* workspace);
 
 /* Loopback: all `world` ranks in this process on ONE device, exchanges done with device copies
  * on `stream` (tests the distributed layout and kernels without NCCL or several GPUs).

@@ -23,6 +23,21 @@ FLAGS = ["-O3", "-std=c++17", "-lineinfo", "-Xcompiler", "-fPIC", "--expt-relaxe
          "-I" + os.path.join(ROOT, "include"), "-Xptxas", "-warn-spills"]
 
 
+def _nccl_include():
+    """NCCL 2.28 headers (nccl.h + the device API) of the nvidia-nccl wheel torch links, for
+    k_symm.cu only; without them that file builds its EUNSUPPORTED stub."""
+    try:
+        import importlib.util
+        spec = importlib.util.find_spec("nvidia.nccl")
+        for loc in (spec.submodule_search_locations or []) if spec else []:
+            inc = os.path.join(loc, "include")
+            if os.path.exists(os.path.join(inc, "nccl_device.h")):
+                return inc
+    except (ImportError, ValueError):
+        pass
+    return None
+
+
 def _sources():
     return sorted(os.path.join(CSRC, f) for f in os.listdir(CSRC) if f.endswith(".cu"))
 
@@ -39,6 +54,8 @@ def _compile(src: str, force: bool, verbose: bool) -> str:
     if not force and os.path.exists(obj) and os.path.getmtime(obj) >= newest_dep:
         return obj
     cmd = [NVCC] + ARCH + FLAGS + ["-c", src, "-o", obj]
+    if os.path.basename(src) == "k_symm.cu" and _nccl_include():
+        cmd.insert(len(cmd) - 4, "-I" + _nccl_include())
     if verbose:
         cmd += ["-Xptxas", "-v"]
     r = subprocess.run(cmd, capture_output=True, text=True)

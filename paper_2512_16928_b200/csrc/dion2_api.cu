@@ -128,7 +128,7 @@ int validate_config(const dion2_config* c) {
   if (c->w_dtype != DION2_DT_F32 && c->w_dtype != DION2_DT_BF16) return DION2_EINVAL_CONFIG;
   if (c->decay_mode < 0 || c->decay_mode > 1) return DION2_EINVAL_CONFIG;
   if (c->scale_mode < 0 || c->scale_mode > 1) return DION2_EINVAL_CONFIG;
-  if (c->ns_form < DION2_NS_FORM_AUTO || c->ns_form > DION2_NS_FORM_GRAM || (c->reserved0 & ~DION2_FLAG_LR_DEVICE) != 0)
+  if (c->ns_form < DION2_NS_FORM_AUTO || c->ns_form > DION2_NS_FORM_GRAM || (c->reserved0 & ~(DION2_FLAG_LR_DEVICE | DION2_FLAG_DIST_DIRECT)) != 0)
     return DION2_EINVAL_CONFIG;
   return DION2_OK;
 }

@@ -21,6 +21,7 @@
 #include <numeric>
 
 #include "runtime.h"
+#include "symm.h"
 
 using namespace dion2;
 
@@ -119,6 +120,17 @@ struct DistPlan {
     bool all_inplace_in = false;   // ... reads them in place
   };
   std::vector<OwnerChunk> oc;
+  // Direct peer exchange (DION2_FLAG_DIST_DIRECT, k_symm.cu): K3 pushes each piece straight into
+  // its owner's receive buffer and K7 pulls its piece of O straight from the owner's outgoing
+  // buffer (peer_recv / peer_osend: every rank's buffers as addressable here -- NCCL symmetric
+  // windows, or the other loopback ranks' workspaces); recv_base / osend_base are this rank's
+  // own (owner-side) buffers in either mode.
+  int direct = 0;
+  int64_t win_bytes = 0;  // max over owners of scount * world (same on every rank)
+  uint8_t* recv_base = nullptr;
+  uint8_t* osend_base = nullptr;
+  std::vector<uint8_t*> peer_recv, peer_osend;
+  SymmState* symm = nullptr;  // NCCL windows; kept for the process lifetime (collective teardown)
 };
 
 void* dt(DistPlan& D, size_t off) { return static_cast<uint8_t*>(D.dtab) + off; }
@@ -185,7 +197,8 @@ int resolve(DistPlan& D, const dion2_shard* sh, int n, const dion2_config* c, in
   // one wave) lose more than the overlapped exchange can win (~0.15 ms of NVLink per rank at
   // P = 8), so the overlap is opt-in.
   const char* ce = getenv("DION2_DIST_CHUNKS");
-  D.nchunks = world > 1 ? std::max(1, ce ? atoi(ce) : 1) : 1;
+  D.direct = (c->reserved0 & DION2_FLAG_DIST_DIRECT) ? 1 : 0;
+  D.nchunks = (world > 1 && !D.direct) ? std::max(1, ce ? atoi(ce) : 1) : 1;
   for (int o = 0; o < world; ++o) {
     int t = 0;
     for (int j : order)
@@ -229,6 +242,8 @@ int resolve(DistPlan& D, const dion2_shard* sh, int n, const dion2_config* c, in
     D.scount[o] = run - D.sdispl[o];
   }
   D.R = D.scount[rank];
+  D.win_bytes = 0;
+  for (int o = 0; o < world; ++o) D.win_bytes = std::max<int64_t>(D.win_bytes, D.scount[o] * world);
   D.oc.clear();
   D.oc.resize(D.nchunks);
   for (int j = 0; j < n; ++j)
@@ -480,8 +495,8 @@ int build_tables(DistPlan& D, const dion2_config* c, void* ws) {
       }
       if (!ok) continue;
       for (int r = 0; r < P; ++r) {
-        uint8_t* rb = static_cast<uint8_t*>(at(ws, D.off_recv)) + (int64_t)r * D.R + q0.soff;
-        uint8_t* sb = static_cast<uint8_t*>(at(ws, D.off_osend)) + (int64_t)r * D.R + q0.soff;
+        uint8_t* rb = D.recv_base + (int64_t)r * D.R + q0.soff;
+        uint8_t* sb = D.osend_base + (int64_t)r * D.R + q0.soff;
         CUtensorMap* m = hmaps + gi * 3 * P;
         if (!make_map_strided(&m[r], rb, q0.qo, q0.k, g.count, q0.piece, 64, 128, CU_TENSOR_MAP_SWIZZLE_128B) ||
             !make_map_strided(&m[P + r], rb, q0.qo, q0.k, g.count, q0.piece, 64, 64, CU_TENSOR_MAP_SWIZZLE_128B) ||
@@ -534,8 +549,28 @@ int build_tables(DistPlan& D, const dion2_config* c, void* ws) {
 }
 
 std::map<std::string, std::unique_ptr<DistPlan>> g_dist_plans;
+std::map<const void*, int> g_last_mode;  // aligned workspace -> exchange mode of its last step
 
-std::string dist_key(const dion2_shard* sh, int n, const dion2_config* c, int world, int rank, void* ws) {
+// Direct mode: point K3's piece destination (X0) at the owner's receive buffer and K7's piece
+// source (X1) at the owner's outgoing buffer, section `rank` (the owner's layout:
+// rank * scount[owner] + soff, the offsets the NCCL exchange would copy between).
+void apply_direct(DistPlan& D) {
+  MatDesc* md = reinterpret_cast<MatDesc*>(D.htab.data() + D.t_desc);
+  for (int j = 0; j < D.n; ++j) {
+    const DistMat& q = D.dm[j];
+    const int64_t off = (int64_t)D.rank * D.scount[q.owner] + q.soff;
+    void* x0 = D.peer_recv[q.owner] + off;
+    void* x1 = D.peer_osend[q.owner] + off;
+    if (md[j].X0 != x0 || md[j].X1 != x1) {
+      md[j].X0 = x0;
+      md[j].X1 = x1;
+      D.uploaded = false;
+    }
+  }
+}
+
+std::string dist_key(const dion2_shard* sh, int n, const dion2_config* c, int world, int rank, void* ws,
+                     void* comm = nullptr) {
   std::string k;
   auto put = [&](const void* p, size_t s) { k.append(reinterpret_cast<const char*>(p), s); };
   put(&n, 4);
@@ -558,23 +593,42 @@ std::string dist_key(const dion2_shard* sh, int n, const dion2_config* c, int wo
   put(&c->decay_mode, 4);
   put(&c->scale_mode, 4);
   put(&c->ns_form, 4);  // shapes the owner's NS plan
+  const int direct = (c->reserved0 & DION2_FLAG_DIST_DIRECT) ? 1 : 0;
+  put(&direct, 4);
+  if (direct) put(&comm, sizeof comm);  // the symmetric windows belong to one communicator
   k += env_key();
   return k;
 }
 
 int get_plan(DistPlan** out, const dion2_shard* sh, int n, const dion2_config* c, int world, int rank, void* workspace,
-             size_t ws_bytes) {
+             size_t ws_bytes, void* comm = nullptr, cudaStream_t s = nullptr) {
   void* ws = reinterpret_cast<void*>(align_up(reinterpret_cast<uintptr_t>(workspace), 4096));
   const size_t slack = (uintptr_t)ws - (uintptr_t)workspace;
-  std::string key = dist_key(sh, n, c, world, rank, ws);
+  std::string key = dist_key(sh, n, c, world, rank, ws, comm);
   auto it = g_dist_plans.find(key);
   if (it == g_dist_plans.end()) {
     auto D = std::make_unique<DistPlan>();
     int rc = resolve(*D, sh, n, c, world, rank);
     if (rc) return rc;
     if (D->total - 4096 + slack > ws_bytes) return DION2_EWORKSPACE;
+    D->recv_base = static_cast<uint8_t*>(at(ws, D->off_recv));
+    D->osend_base = static_cast<uint8_t*>(at(ws, D->off_osend));
+    if (D->direct && comm) {  // NCCL: the owner-side buffers are the symmetric windows
+      rc = symm_create(comm, world, (size_t)D->win_bytes, s, &D->symm, &D->recv_base, &D->osend_base, D->peer_recv,
+                       D->peer_osend);
+      // EUNSUPPORTED is decided before any collective call, identically on every rank (no
+      // device API in this NCCL, or ranks outside one NVLink domain): fall back to send / recv
+      if (rc == DION2_EUNSUPPORTED) {
+        D->direct = 0;
+        D->recv_base = static_cast<uint8_t*>(at(ws, D->off_recv));
+        D->osend_base = static_cast<uint8_t*>(at(ws, D->off_osend));
+      } else if (rc) {
+        return rc;
+      }
+    }
     rc = build_tables(*D, c, ws);
     if (rc) return rc;
+    if (D->direct && comm) apply_direct(*D);
     D->ws = ws;
     it = g_dist_plans.emplace(key, std::move(D)).first;
   }
@@ -709,13 +763,13 @@ void phase_owner_ns(DistPlan& D, int chunk, void* ws, const dion2_config* c, Lau
   L.begin(PH_NORM);
   // all owned matrices in place: one block per matrix computes the norm scale only
   launch_assemble(s, om, (int)ch.owned.size(), ch.all_inplace_in ? 1 : ch.max_p_pad, ch.ptab,
-                  (const uint8_t*)at(ws, D.off_recv), (const float*)at(ws, D.off_sumsq_all),
+                  D.recv_base, (const float*)at(ws, D.off_sumsq_all),
                   (const float*)at(ws, D.off_nsscale), D.n, c->ns_eps);
   L.end();
   run_ns(P, c, L, s, false);
   if (!ch.all_inplace) {
     L.begin(PH_SCATTER);
-    launch_disassemble(s, om, (int)ch.owned.size(), ch.max_k, ch.ptab, (uint8_t*)at(ws, D.off_osend));
+    launch_disassemble(s, om, (int)ch.owned.size(), ch.max_k, ch.ptab, D.osend_base);
     L.end();
   }
 }
@@ -799,8 +853,14 @@ struct NcclTransport : Transport {
     rc |= api.group_end();
     return rc ? DION2_ENCCL : DION2_OK;
   }
-  int to_owners(int ch, cudaStream_t s) override { return exchange(true, ch, s); }
-  int from_owners(int ch, cudaStream_t s) override { return exchange(false, ch, s); }
+  // direct mode: K3 already pushed the pieces (K7 will pull O): one LSA barrier each way
+  int direct_sync(bool forward, cudaStream_t s) {
+    for (int peer = 0; peer < D.world; ++peer)
+      if (peer != D.rank) bytes += forward ? D.scount[peer] : D.R;
+    return symm_barrier(D.symm, s);
+  }
+  int to_owners(int ch, cudaStream_t s) override { return D.direct ? direct_sync(true, s) : exchange(true, ch, s); }
+  int from_owners(int ch, cudaStream_t s) override { return D.direct ? direct_sync(false, s) : exchange(false, ch, s); }
 };
 
 // all ranks in one process: every exchange is a set of device-to-device copies
@@ -838,6 +898,10 @@ struct LoopbackTransport : Transport {
     for (int r = 0; r < P; ++r)
       for (int o = 0; o < P; ++o) {
         const int64_t off = D[o]->cdispl[o][ch], len = D[o]->cdispl[o][ch + 1] - off;
+        if (D[0]->direct) {  // pushed by K3 (stream order stands in for the barrier)
+          if (o != 0 && r == 0) bytes += (uint64_t)len;
+          continue;
+        }
         rc |= cp(at(ws[o], D[o]->off_recv + (size_t)r * D[o]->R + off), at(ws[r], D[r]->off_send + D[r]->sdispl[o] + off),
                  (size_t)len, s);
         if (o != 0 && r == 0) bytes += (uint64_t)len;
@@ -850,6 +914,10 @@ struct LoopbackTransport : Transport {
     for (int o = 0; o < P; ++o)
       for (int r = 0; r < P; ++r) {
         const int64_t off = D[o]->cdispl[o][ch], len = D[o]->cdispl[o][ch + 1] - off;
+        if (D[0]->direct) {  // pulled by K7
+          if (o == 0 && r != 0) bytes += (uint64_t)len;
+          continue;
+        }
         rc |= cp(at(ws[r], D[r]->off_orecv + D[r]->sdispl[o] + off), at(ws[o], D[o]->off_osend + (size_t)r * D[o]->R + off),
                  (size_t)len, s);
         if (o == 0 && r != 0) bytes += (uint64_t)len;
@@ -1065,6 +1133,10 @@ int release_dist_plans(uintptr_t lo, uintptr_t hi) {
     const uintptr_t w = reinterpret_cast<uintptr_t>(it->second->ws);
     if (w >= lo && w < hi) { it = g_dist_plans.erase(it); ++dropped; } else { ++it; }
   }
+  for (auto it = g_last_mode.begin(); it != g_last_mode.end();) {
+    const uintptr_t w = reinterpret_cast<uintptr_t>(it->first);
+    if (w >= lo && w < hi) it = g_last_mode.erase(it); else ++it;
+  }
   for (auto it = g_dp_plans.begin(); it != g_dp_plans.end();) {
     const uintptr_t w = reinterpret_cast<uintptr_t>(it->second->P.ws);
     if (w >= lo && w < hi) { it = g_dp_plans.erase(it); ++dropped; } else { ++it; }
@@ -1113,14 +1185,22 @@ int dion2_step_batched_dist(const dion2_shard* shards, int32_t n, const dion2_co
   std::lock_guard<std::mutex> lock(g_mu);
   ensure_device_attrs();
   DistPlan* D = nullptr;
-  if ((rc = get_plan(&D, shards, n, cfg, world, rank, workspace, ws_bytes))) return rc;
-  void* ws = reinterpret_cast<void*>(align_up(reinterpret_cast<uintptr_t>(workspace), 4096));
   cudaStream_t s = reinterpret_cast<cudaStream_t>(stream);
+  if ((rc = get_plan(&D, shards, n, cfg, world, rank, workspace, ws_bytes, nccl_comm, s))) return rc;
+  void* ws = reinterpret_cast<void*>(align_up(reinterpret_cast<uintptr_t>(workspace), 4096));
+  g_last_mode[ws] = D->direct;
   NcclTransport T(*D, ws, nccl_comm);
   std::vector<DistPlan*> plans{D};
   std::vector<void*> wss{ws};
   std::vector<const dion2_shard*> sh{shards};
   return run_dist(plans, wss, sh, cfg, T, s, comm_bytes_out);
+}
+
+int dion2_dist_exchange_mode(const void* workspace) {
+  std::lock_guard<std::mutex> lock(g_mu);
+  const void* ws = reinterpret_cast<const void*>(align_up(reinterpret_cast<uintptr_t>(workspace), 4096));
+  auto it = g_last_mode.find(ws);
+  return it == g_last_mode.end() ? -1 : it->second;
 }
 
 int dion2_step_batched_loopback(const dion2_shard* shards, int32_t n, const dion2_config* cfg,
@@ -1141,6 +1221,17 @@ int dion2_step_batched_loopback(const dion2_shard* shards, int32_t n, const dion
     if ((rc = get_plan(&plans[r], shards + (size_t)r * n, n, cfg, world, r, workspaces[r], ws_bytes))) return rc;
     wss[r] = reinterpret_cast<void*>(align_up(reinterpret_cast<uintptr_t>(workspaces[r]), 4096));
     sh[r] = shards + (size_t)r * n;
+  }
+  if (plans[0]->direct) {  // every loopback rank's buffers are addressable: push / pull directly
+    for (int r = 0; r < world; ++r) {
+      plans[r]->peer_recv.resize(world);
+      plans[r]->peer_osend.resize(world);
+      for (int o = 0; o < world; ++o) {
+        plans[r]->peer_recv[o] = plans[o]->recv_base;
+        plans[r]->peer_osend[o] = plans[o]->osend_base;
+      }
+      apply_direct(*plans[r]);
+    }
   }
   cudaStream_t s = reinterpret_cast<cudaStream_t>(stream);
   LoopbackTransport T(plans, wss);

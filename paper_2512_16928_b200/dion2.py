@@ -22,14 +22,14 @@ AXIS = {"rows": 0, "cols": 1, "auto": 2}
 PRECISION = {"bf16": 0, "fp32": 1}
 SELECT = {"l1": 0, "random": 1}
 NS_FORM = {"auto": 0, "direct": 1, "gram": 2}
-ABI_VERSION = 6  # include/dion2.h DION2_ABI_VERSION
+ABI_VERSION = 7  # include/dion2.h DION2_ABI_VERSION
 STATUS = {0: "OK", 1: "EINVAL_CONFIG", 2: "EINVAL_SHAPE", 3: "EWORKSPACE", 4: "EUNSUPPORTED",
           5: "ECUDA", 6: "ENCCL", 7: "ENONFINITE"}
 EXPORTED = ["dion2_config_init", "dion2_workspace_size", "dion2_step", "dion2_step_batched", "dion2_get_status",
             "dion2_strerror", "dion2_set_phase_timing", "dion2_get_phase_times", "dion2_phase_name",
             "dion2_last_launch_count", "dion2_abi_version", "dion2_dist_info", "dion2_step_batched_dist",
             "dion2_step_batched_loopback", "dion2_dpsync_workspace_size", "dion2_step_batched_dpsync",
-            "dion2_step_batched_dpsync_loopback", "dion2_release_workspace"]
+            "dion2_step_batched_dpsync_loopback", "dion2_release_workspace", "dion2_dist_exchange_mode"]
 
 
 class Dion2Matrix(ctypes.Structure):
@@ -102,6 +102,7 @@ def _lib():
         lib.dion2_step_batched_dpsync.argtypes = [P(Dion2Matrix), ctypes.c_int32, P(Dion2Config), ctypes.c_void_p,
                                                   ctypes.c_size_t, ctypes.c_void_p, ctypes.c_int32, ctypes.c_int32,
                                                   ctypes.c_void_p, P(ctypes.c_uint64)]
+        lib.dion2_dist_exchange_mode.argtypes = [ctypes.c_void_p]
         lib.dion2_step_batched_dpsync_loopback.argtypes = [P(Dion2Matrix), ctypes.c_int32, P(Dion2Config),
                                                            P(ctypes.c_void_p), ctypes.c_size_t, ctypes.c_int32,
                                                            ctypes.c_void_p, P(ctypes.c_uint64)]
@@ -114,10 +115,13 @@ def make_config(alpha: float = 0.25, mu: float = 0.95, lr: float = 0.02, ns_step
                 axis: str = "auto", precision: str = "bf16", grad_dtype: Optional[torch.dtype] = None,
                 decay_mode: int = 0, scale_mode: int = 0, select: str = "l1", seed: int = 0,
                 step: int = 0, ns_form: str = "auto", lr_device: bool = False,
-                w_dtype: Optional[torch.dtype] = None) -> Dion2Config:
+                w_dtype: Optional[torch.dtype] = None, dist_direct: bool = False) -> Dion2Config:
     """ns_form: "auto" | "direct" | "gram" -- how the tensor-core Newton-Schulz map is evaluated
     (include/dion2.h dion2_ns_form, readings R23, R24).  w_dtype: torch.bfloat16 for
-    bf16 weights (the update is computed in fp32 and rounded once), else fp32."""
+    bf16 weights (the update is computed in fp32 and rounded once), else fp32.  dist_direct:
+    the distributed step's pieces travel by direct peer stores / loads (K3 pushes into the
+    owner's receive window, K7 pulls from its outgoing window; NCCL symmetric memory) instead
+    of NCCL send / recv (DION2_FLAG_DIST_DIRECT)."""
     cfg = Dion2Config()
     _lib().dion2_config_init(ctypes.byref(cfg))
     cfg.alpha, cfg.mu, cfg.lr, cfg.ns_steps, cfg.ns_eps = alpha, mu, lr, ns_steps, ns_eps
@@ -134,7 +138,7 @@ def make_config(alpha: float = 0.25, mu: float = 0.95, lr: float = 0.02, ns_step
     cfg.select = SELECT[select]
     cfg.seed, cfg.step = seed, step
     cfg.ns_form = NS_FORM[ns_form]
-    cfg.reserved0 = 1 if lr_device else 0  # DION2_FLAG_LR_DEVICE: eta read from the workspace word
+    cfg.reserved0 = (1 if lr_device else 0) | (2 if dist_direct else 0)  # DION2_FLAG_LR_DEVICE | _DIST_DIRECT
     return cfg
 
 
@@ -541,6 +545,26 @@ class Dion2Dist:
         bad = ctypes.c_int32(-1)
         rc = _lib().dion2_get_status(self._ws.data_ptr(), torch.cuda.current_stream().cuda_stream, ctypes.byref(bad))
         return rc, bad.value
+
+    def release(self) -> None:
+        """Drop the library's plans keyed on this object's workspace (the symmetric windows of a
+        direct-exchange plan are tied to its communicator: release before destroying the group)."""
+        if self._ws is not None:
+            _lib().dion2_release_workspace(self._ws.data_ptr(), self._ws.numel())
+            self._ws = None
+
+    def __del__(self):
+        try:
+            self.release()
+        except Exception:  # interpreter shutdown: the library may already be gone
+            pass
+
+    def exchange_mode(self) -> str:
+        """"direct" (peer stores / loads over symmetric memory), "nccl" (send / recv), or
+        "none" before the first step."""
+        if self._ws is None:
+            return "none"
+        return {1: "direct", 0: "nccl"}.get(_lib().dion2_dist_exchange_mode(self._ws.data_ptr()), "none")
 
 
 class Dion2Loopback:

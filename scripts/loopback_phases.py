@@ -26,6 +26,7 @@ def main():
     ap.add_argument("--world", type=int, nargs="+", default=[2, 4, 8])
     ap.add_argument("--steps", type=int, default=3)
     ap.add_argument("--alpha", type=float, default=0.25)
+    ap.add_argument("--direct", action="store_true", help="direct peer exchange (DION2_FLAG_DIST_DIRECT)")
     args = ap.parse_args()
     shapes = layer_set_1b(24)
     out = {}
@@ -41,7 +42,7 @@ def main():
                 m.append(torch.zeros((sc, sr) if mt else (sr, sc), device="cuda"))
                 g.append(torch.randn(sr, sc, device="cuda"))
             Ws.append(w), Ms.append(m), Gs.append(g)
-        opt = D.Dion2Loopback(shapes, P, alpha=args.alpha, m_transposed=mts)
+        opt = D.Dion2Loopback(shapes, P, alpha=args.alpha, m_transposed=mts, dist_direct=args.direct)
         opt.step(Ws, Ms, Gs)
         torch.cuda.synchronize()
         e0, e1 = torch.cuda.Event(enable_timing=True), torch.cuda.Event(enable_timing=True)

@@ -166,12 +166,13 @@ def _finish(res, shapes, Wg, Mg, Wr, Mr, W0):
 
 def run_parity_dist(shapes, alpha, world, steps=3, seed=0, mode="loopback", axis="auto", mu=0.95, lr=0.02,
                     row_scaled=True, device="cuda", select="l1", sel_seed=0, m_transposed=False,
-                    structure: Optional[dict] = None):
+                    structure: Optional[dict] = None, direct: bool = False):
     """Distributed step (owner-compute, shards along the non-selection axis) against the
     fp64 oracle on the FULL matrices.  mode = "loopback" (all ranks in this process) or
     "nccl" (world must equal the initialised torch.distributed world; this process is
     one rank and holds only its shards; the full matrices are re-assembled with
-    all_gather for the comparison)."""
+    all_gather for the comparison).  direct: pieces pushed / pulled through peer memory
+    (DION2_FLAG_DIST_DIRECT) instead of copied / sent."""
     from paper_2512_16928_b200 import dion2 as D
     res = ParityResult()
     cfg_o = oracle_cfg(alpha, axis, mu, lr)
@@ -190,12 +191,12 @@ def run_parity_dist(shapes, alpha, world, steps=3, seed=0, mode="loopback", axis
     if mode == "loopback":
         ranks = list(range(world))
         opt = D.Dion2Loopback(shapes, world, alpha=alpha, axis=axis, mu=mu, lr=lr, select=select, seed=sel_seed,
-                              m_transposed=mts)
+                              m_transposed=mts, dist_direct=direct)
     else:
         import torch.distributed as dist
         ranks = [dist.get_rank()]
         opt = D.Dion2Dist(shapes, alpha=alpha, axis=axis, mu=mu, lr=lr, select=select, seed=sel_seed,
-                          m_transposed=mts)
+                          m_transposed=mts, dist_direct=direct)
     full = lambda a, i: torch.from_numpy(a)  # noqa: E731
     Wg = {r: [D.shard_of(full(W0[i], i), axes[i], world, r).to(device) for i in range(len(shapes))] for r in ranks}
     Mg = {r: [torch.zeros((w.shape[1], w.shape[0]), device=device) if mts[i] else torch.zeros_like(w)
@@ -246,6 +247,7 @@ def run_parity_dist(shapes, alpha, world, steps=3, seed=0, mode="loopback", axis
     Mfull = [assemble(Mv, i) for i in range(len(shapes))]
     _finish(res, shapes, Wfull, Mfull, Wr, Mr, W0)
     res.comm_bytes = opt.last_comm_bytes
+    res.exchange = opt.exchange_mode() if mode != "loopback" else ("direct" if direct else "copies")
     return res
 
 

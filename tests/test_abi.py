@@ -37,7 +37,7 @@ def test_exports_every_declared_symbol(lib):
 
 
 def test_abi_version(lib):
-    assert lib.dion2_abi_version() == 6
+    assert lib.dion2_abi_version() == 7
 
 
 def test_config_defaults(lib):
@@ -50,7 +50,7 @@ def test_config_defaults(lib):
     assert cfg.ns_form == 0 and cfg.reserved0 == 0
 
 
-@pytest.mark.parametrize("form,reserved", [(3, 0), (-1, 0), (0, 2), (0, 3)])
+@pytest.mark.parametrize("form,reserved", [(3, 0), (-1, 0), (0, 4), (0, 5), (0, 8)])
 def test_ns_form_validation(lib, form, reserved):
     cfg = D.make_config()
     cfg.ns_form, cfg.reserved0 = form, reserved

@@ -100,3 +100,60 @@ def test_loopback_owner_chunks(chunks, world, monkeypatch):
     monkeypatch.setenv("DION2_DIST_CHUNKS", chunks)
     _assert(run_parity_dist(SHAPES + [(1024, 256), (4096, 1024)], 0.25, world, steps=3, m_transposed=True))
     _assert(run_parity_dist(layer_set_1b(1), 0.25, world, steps=2))
+
+
+# ------------------------------------------------------------- direct peer exchange
+@pytest.mark.parametrize("world", [2, 4, 8])
+def test_loopback_direct_exchange(world):
+    """DION2_FLAG_DIST_DIRECT in loopback: K3 pushes the pieces into the owners' receive
+    buffers and K7 pulls O from the owners' outgoing buffers (no exchange copies)."""
+    _assert(run_parity_dist(SHAPES + [(1024, 256), (4096, 1024)], 0.25, world, steps=3, direct=True,
+                            m_transposed=True))
+    _assert(run_parity_dist(layer_set_1b(1), 0.25, world, steps=2, direct=True))
+
+
+@pytest.mark.parametrize("world", [2, 8])
+def test_loopback_direct_is_bitwise_the_copy_exchange(world):
+    """Same kernels, same bytes, other addresses: W, M and the index sets after 3 steps are
+    bit-identical with and without the direct exchange."""
+    from paper_2512_16928_b200 import dion2 as D
+    from synth import gen_grad, gen_w0
+    shapes = SHAPES + layer_set_1b(1)
+    infos = D.dist_info(shapes, world, 0)
+    axes = infos["axis"]
+    out = {}
+    for direct in (False, True):
+        opt = D.Dion2Loopback(shapes, world, alpha=0.25, dist_direct=direct)
+        W = [[D.shard_of(torch.from_numpy(gen_w0(m, n, 0, i)), axes[i], world, r).cuda()
+              for i, (m, n) in enumerate(shapes)] for r in range(world)]
+        M = [[torch.zeros_like(w) for w in W[r]] for r in range(world)]
+        for t in range(3):
+            G = [[D.shard_of(torch.from_numpy(gen_grad(m, n, 0, i, t, row_scaled=True)), axes[i], world, r).cuda()
+                  for i, (m, n) in enumerate(shapes)] for r in range(world)]
+            opt.step(W, M, G, step=t)
+        torch.cuda.synchronize()
+        out[direct] = (W, M, opt.last_comm_bytes)
+    for r in range(world):
+        for i in range(len(shapes)):
+            assert torch.equal(out[False][0][r][i], out[True][0][r][i]), (r, i)
+            assert torch.equal(out[False][1][r][i], out[True][1][r][i]), (r, i)
+    assert out[False][2] == out[True][2]
+
+
+def test_nccl_direct_single_rank():
+    """The NCCL symmetric-memory path with one rank: ncclMemAlloc'd windows registered
+    symmetrically, a device communicator with an LSA barrier, peer pointers read on the device,
+    K3 storing into / K7 loading from the (own) window through them, barriers between phases."""
+    import torch.distributed as dist
+    os.environ.setdefault("MASTER_ADDR", "127.0.0.1")
+    os.environ["MASTER_PORT"] = str(_free_port())
+    torch.cuda.set_device(0)
+    dist.init_process_group("nccl", rank=0, world_size=1, device_id=torch.device("cuda", 0))
+    try:
+        res = run_parity_dist(SHAPES, 0.25, 1, steps=3, mode="nccl", direct=True)
+        _assert(res)
+        assert res.exchange == "direct", res.exchange  # the symmetric windows were set up, no fallback
+        _assert(run_parity_dist(SHAPES + [(1024, 256)], 0.25, 1, steps=2, mode="nccl", m_transposed=True,
+                                direct=True))
+    finally:
+        dist.destroy_process_group()

@@ -3,7 +3,8 @@
 One process per GPU (torch.multiprocessing, spawn), NCCL over NVLink, 127.0.0.1 rendezvous:
   * the owner-compute step (dion2_step_batched_dist): each rank holds only its shards, the
     pieces travel through grouped ncclSend / ncclRecv, and the full matrices re-assembled on
-    rank 0 match the fp64 oracle (gpu_harness.run_parity_dist, mode "nccl");
+    rank 0 match the fp64 oracle (gpu_harness.run_parity_dist, mode "nccl"), with the NCCL
+    exchange and with the direct peer exchange over symmetric memory (DION2_FLAG_DIST_DIRECT);
   * the FSDP2 integration (fully_shard with dion2_placement + Dion2FSDP) against the oracle;
   * compressed DP-sync (dion2_step_batched_dpsync): replicas with different local gradients
     stay bit-identical and match the oracle's replica model.
@@ -40,8 +41,9 @@ def _worker(rank, world, port, which, errq):
             if which == "dist":
                 from gpu_harness import run_parity_dist
                 shapes = [(256, 512), (512, 256), (1024, 1024), (2048, 512), (512, 2048), (4096, 1024)]
-                for mt in (False, True):
-                    res = run_parity_dist(shapes, 0.25, world, steps=3, mode="nccl", m_transposed=mt)
+                for mt, direct in ((False, False), (True, False), (False, True), (True, True)):
+                    res = run_parity_dist(shapes, 0.25, world, steps=3, mode="nccl", m_transposed=mt, direct=direct)
+                    assert res.exchange == ("direct" if direct else "nccl"), res.exchange
                     assert res.index_mismatch == 0 and max(res.dW_rel) <= 2e-2 and max(res.M_rel) <= 1e-5, res
                     assert res.comm_bytes > 0
             elif which == "fsdp":
