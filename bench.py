@@ -504,6 +504,9 @@ def run_ours(args):
             off += m * n
         o_ = Dion2(alpha=args.alpha, axis="auto", precision="bf16", ns_form=args.ns_form, storage_transposed=sts)
         sweep["row_selection_layout_ms_per_step"] = time_steps(o_, Wt, Mt, Gt, 3, 1, None)
+        if not args.no_e2e:  # its end-to-end time (host G upload: PCIe-bound like the default layout's)
+            sweep["row_selection_layout_e2e_ms_per_step"] = e2e_run(o_, Wt, Mt, Gt, bufs[2], 2,
+                                                                    select_counts(shapes, args.alpha))[0]
         del o_
         torch.cuda.empty_cache()
         # the same step with bf16 gradients (mixed-precision training): K1 reads 10 B/param
