@@ -66,7 +66,14 @@ extern "C" {
    >= 2.28 device API) separated by LSA barriers, allocated collectively on the first step of a
    plan and kept for the process lifetime; in loopback they are the other ranks' workspaces.
    Requires every rank in one load/store (NVLink) domain, else DION2_EUNSUPPORTED; forces one
-   owner chunk.  Results are bitwise those of the NCCL exchange (same kernels, same bytes). */
+   owner chunk.  Results are bitwise those of the NCCL exchange (same kernels, same bytes).
+   dion2_step_batched_dpsync (P <= 8) reads it too: each replica packs M[K] into its input
+   window, and after an LSA barrier sums its 1/P slice over all replicas' windows in rank order
+   and stores the sum into every replica's output window (a reduce-scatter + all-gather by
+   peer loads / stores, 2 (P-1)/P of the buffer per rank like a ring all-reduce), a second
+   barrier, then unpacks: the same rank-order sums as the loopback emulation, bit-identical on
+   every replica by construction.  Where the windows are unavailable both entry points fall
+   back to NCCL (dion2_dist_exchange_mode reports which ran). */
 #define DION2_FLAG_DIST_DIRECT 2
 
 typedef enum {
@@ -255,8 +262,8 @@ int dion2_step_batched_dist(const dion2_shard* shards, int32_t n, const dion2_co
                             size_t ws_bytes, void* nccl_comm, int32_t world, int32_t rank, void* stream,
                             uint64_t* comm_bytes_out);
 
-/* Exchange mode of the distributed plan last built on `workspace` (the same pointer passed to
- * dion2_step_batched_dist): 1 = direct peer stores / loads over symmetric memory
+/* Exchange mode of the last distributed or DP-sync step on `workspace` (the same pointer passed
+ * to dion2_step_batched_dist / _dpsync): 1 = direct peer stores / loads over symmetric memory
  * (DION2_FLAG_DIST_DIRECT honoured), 0 = NCCL send / recv (flag unset, or the fallback when the
  * NCCL device API or a single NVLink domain is unavailable -- decided identically on every
  * rank), -1 = no distributed plan on that workspace.  Host-only. */

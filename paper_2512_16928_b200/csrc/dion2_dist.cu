@@ -1002,6 +1002,15 @@ struct DpPlan {
   int64_t buf_floats = 0;   // selected rows of every matrix, then the 2 n tail floats (k_dp_tail)
   int64_t data_floats = 0;
   int total_rows = 0;
+  // direct exchange (DION2_FLAG_DIST_DIRECT): phase 1 packs into pack_buf, the reduce-scatter /
+  // all-gather kernel writes the sum into every replica's red_buf (NCCL symmetric windows, or
+  // the loopback replicas' own buffers); otherwise both are the workspace buffer (in-place
+  // ncclAllReduce)
+  int direct = 0;
+  float* pack_buf = nullptr;
+  float* red_buf = nullptr;
+  std::vector<uint8_t*> peer_in, peer_out;
+  SymmState* symm = nullptr;  // kept for the process lifetime (collective teardown)
   void* dtab = nullptr;  // [n] int32 row prefix, then [n] int64 buffer offsets
   size_t t_prefix = 0, t_off = 0;
   bool uploaded = false;
@@ -1030,7 +1039,7 @@ int dp_layout(DpPlan& D, const dion2_matrix* mats, int n, const dion2_config* c,
 }
 
 int dp_get_plan(DpPlan** out, const dion2_matrix* mats, int n, const dion2_config* c, int world, void* workspace,
-                size_t ws_bytes, void** ws_out) {
+                size_t ws_bytes, void** ws_out, void* comm = nullptr, cudaStream_t s = nullptr) {
   void* ws = reinterpret_cast<void*>(align_up(reinterpret_cast<uintptr_t>(workspace), 4096));
   const size_t slack = (uintptr_t)ws - (uintptr_t)workspace;
   std::string key;
@@ -1055,6 +1064,9 @@ int dp_get_plan(DpPlan** out, const dion2_matrix* mats, int n, const dion2_confi
   put(&c->decay_mode, 4);
   put(&c->scale_mode, 4);
   put(&c->ns_form, 4);
+  const int direct = (c->reserved0 & DION2_FLAG_DIST_DIRECT) && world <= kMaxPieceRanks ? 1 : 0;
+  put(&direct, 4);
+  if (direct) put(&comm, sizeof comm);
   key += env_key();
   auto it = g_dp_plans.find(key);
   if (it == g_dp_plans.end()) {
@@ -1077,6 +1089,20 @@ int dp_get_plan(DpPlan** out, const dion2_matrix* mats, int n, const dion2_confi
       fo += (int64_t)D->P.mp[i].sr * D->P.mp[i].sc;
     }
     if (cudaMalloc(&D->dtab, D->htab.size()) != cudaSuccess) return DION2_ECUDA;
+    D->pack_buf = D->red_buf = (float*)at(ws, D->off_buf);
+    D->direct = direct;
+    if (direct && comm) {  // NCCL: pack into / reduce into symmetric windows
+      uint8_t *in = nullptr, *outb = nullptr;
+      rc = symm_create(comm, world, 4 * (size_t)D->buf_floats, s, &D->symm, &in, &outb, D->peer_in, D->peer_out);
+      if (rc == DION2_EUNSUPPORTED) {  // decided identically on every rank before any collective call
+        D->direct = 0;
+      } else if (rc) {
+        return rc;
+      } else {
+        D->pack_buf = reinterpret_cast<float*>(in);
+        D->red_buf = reinterpret_cast<float*>(outb);
+      }
+    }
     it = g_dp_plans.emplace(key, std::move(D)).first;
   }
   DpPlan& D = *it->second;
@@ -1090,7 +1116,7 @@ void dp_pack(DpPlan& D, void* ws, bool unpack, float scale, cudaStream_t s, Laun
   L.begin(unpack ? PH_GATHER : PH_SELECT);
   launch_dp_pack(unpack, s, (const MatDesc*)tab(D.P, D.P.off_desc),
                  (const int32_t*)((uint8_t*)D.dtab + D.t_prefix), (const int64_t*)((uint8_t*)D.dtab + D.t_off),
-                 D.P.n, D.total_rows, (float*)at(ws, D.off_buf), scale, (const int32_t*)at(ws, D.P.off_bad));
+                 D.P.n, D.total_rows, unpack ? D.red_buf : D.pack_buf, scale, (const int32_t*)at(ws, D.P.off_bad));
   L.end();
 }
 
@@ -1108,7 +1134,7 @@ int dp_phase1(DpPlan& D, const dion2_matrix* mats, const dion2_config* c, void* 
   stage_k1_select(D.P, c, ws, status, L, s, true);
   dp_pack(D, ws, false, 1.f, s, L);
   L.begin(PH_SELECT);
-  launch_dp_tail(s, (const MatDesc*)tab(D.P, D.P.off_desc), D.P.n, (float*)at(ws, D.off_buf) + D.data_floats,
+  launch_dp_tail(s, (const MatDesc*)tab(D.P, D.P.off_desc), D.P.n, D.pack_buf + D.data_floats,
                  (int32_t*)at(ws, D.P.off_bad), status, false);
   L.end();
   return DION2_OK;
@@ -1116,7 +1142,7 @@ int dp_phase1(DpPlan& D, const dion2_matrix* mats, const dion2_config* c, void* 
 
 void dp_phase2(DpPlan& D, const dion2_matrix* mats, const dion2_config* c, void* ws, cudaStream_t s, Launcher& L) {
   L.begin(PH_SELECT);  // global non-finite flags and the common fp16 prescale
-  launch_dp_tail(s, (const MatDesc*)tab(D.P, D.P.off_desc), D.P.n, (float*)at(ws, D.off_buf) + D.data_floats,
+  launch_dp_tail(s, (const MatDesc*)tab(D.P, D.P.off_desc), D.P.n, D.red_buf + D.data_floats,
                  (int32_t*)at(ws, D.P.off_bad), (int32_t*)at(ws, D.P.off_status), true);
   L.end();
   dp_pack(D, ws, true, 1.f / (float)D.world, s, L);  // M[K] <- mean over replicas (skips bad matrices)
@@ -1276,13 +1302,30 @@ int dion2_step_batched_dpsync(const dion2_matrix* user_mats, int32_t n, const di
   ensure_device_attrs();
   DpPlan* D = nullptr;
   void* ws = nullptr;
-  if ((rc = dp_get_plan(&D, mats, n, cfg, world, workspace, ws_bytes, &ws))) return rc;
   cudaStream_t s = reinterpret_cast<cudaStream_t>(stream);
+  if ((rc = dp_get_plan(&D, mats, n, cfg, world, workspace, ws_bytes, &ws, nccl_comm, s))) return rc;
+  g_last_mode[ws] = D->direct;
   Launcher L{s};
   if ((rc = dp_phase1(*D, mats, cfg, ws, s, L))) return rc;
-  float* buf = (float*)at(ws, D->off_buf);
-  if (nccl_api().allreduce(buf, buf, (size_t)D->buf_floats, kNcclFloat32, /*ncclSum*/ 0, nccl_comm, s))
-    return DION2_ENCCL;
+  if (D->direct) {
+    // every replica's pack is in its window -> reduce this rank's slice into every window -> all
+    // slices landed (the second barrier also keeps the next step's pack off the windows until
+    // every replica is done reading)
+    if ((rc = symm_barrier(D->symm, s))) return rc;
+    DpPeerBufs B{};
+    for (int r = 0; r < world; ++r) {
+      B.in[r] = reinterpret_cast<const float*>(D->peer_in[r]);
+      B.out[r] = reinterpret_cast<float*>(D->peer_out[r]);
+    }
+    L.begin(PH_SELECT);
+    launch_dp_reduce_direct(s, B, world, rank, D->buf_floats, g_sm_count > 0 ? g_sm_count : 148);
+    L.end();
+    if ((rc = symm_barrier(D->symm, s))) return rc;
+  } else {
+    float* buf = (float*)at(ws, D->off_buf);
+    if (nccl_api().allreduce(buf, buf, (size_t)D->buf_floats, kNcclFloat32, /*ncclSum*/ 0, nccl_comm, s))
+      return DION2_ENCCL;
+  }
   dp_phase2(*D, mats, cfg, ws, s, L);
   g_last_launches = L.count;
   if (comm_bytes_out) *comm_bytes_out = (uint64_t)(2.0 * (world - 1) / world * 4.0 * (double)D->buf_floats);
@@ -1309,15 +1352,27 @@ int dion2_step_batched_dpsync_loopback(const dion2_matrix* user_mats, int32_t n,
   Launcher L{s};
   for (int r = 0; r < world; ++r)
     if ((rc = dp_phase1(*D[r], mats + (size_t)r * n, cfg, ws[r], s, L))) return rc;
-  // all-reduce (sum) emulated: gather every replica's buffer at replica 0, sum in rank order, broadcast
   const size_t bytes = 4 * (size_t)D[0]->buf_floats;
-  for (int r = 0; r < world; ++r)
-    cudaMemcpyAsync(at(ws[0], D[0]->off_gather + r * bytes), at(ws[r], D[r]->off_buf), bytes,
-                    cudaMemcpyDeviceToDevice, s);
-  launch_sum_rank_scores(s, (const float*)at(ws[0], D[0]->off_gather), (float*)at(ws[0], D[0]->off_buf),
-                         D[0]->buf_floats, world);
-  for (int r = 1; r < world; ++r)
-    cudaMemcpyAsync(at(ws[r], D[r]->off_buf), at(ws[0], D[0]->off_buf), bytes, cudaMemcpyDeviceToDevice, s);
+  if (D[0]->direct) {
+    // direct exchange: each replica's slice summed over every replica's buffer (rank order) and
+    // written back into every buffer (in place; the slices are disjoint)
+    DpPeerBufs B{};
+    for (int r = 0; r < world; ++r) B.in[r] = B.out[r] = D[r]->pack_buf;
+    for (int r = 0; r < world; ++r) {
+      L.begin(PH_SELECT);
+      launch_dp_reduce_direct(s, B, world, r, D[0]->buf_floats, g_sm_count > 0 ? g_sm_count : 148);
+      L.end();
+    }
+  } else {
+    // all-reduce (sum) emulated: gather every replica's buffer at replica 0, sum in rank order, broadcast
+    for (int r = 0; r < world; ++r)
+      cudaMemcpyAsync(at(ws[0], D[0]->off_gather + r * bytes), at(ws[r], D[r]->off_buf), bytes,
+                      cudaMemcpyDeviceToDevice, s);
+    launch_sum_rank_scores(s, (const float*)at(ws[0], D[0]->off_gather), (float*)at(ws[0], D[0]->off_buf),
+                           D[0]->buf_floats, world);
+    for (int r = 1; r < world; ++r)
+      cudaMemcpyAsync(at(ws[r], D[r]->off_buf), at(ws[0], D[0]->off_buf), bytes, cudaMemcpyDeviceToDevice, s);
+  }
   for (int r = 0; r < world; ++r) dp_phase2(*D[r], mats + (size_t)r * n, cfg, ws[r], s, L);
   g_last_launches = L.count;
   if (comm_bytes_out) *comm_bytes_out = (uint64_t)(2.0 * (world - 1) / world * (double)bytes);

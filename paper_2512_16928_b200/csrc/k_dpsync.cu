@@ -4,6 +4,8 @@
 // mode streams contiguous rows of M, cols mode gathers the selected columns, and cols
 // mode with transposed M packs the contiguous rows of S^T (every replica must use the
 // same layout).
+#include <algorithm>
+
 #include "kernels.cuh"
 
 namespace dion2 {
@@ -79,6 +81,34 @@ __global__ void k_dp_tail(const MatDesc* __restrict__ mats, int n_mats, float* _
     set_status_bad(status, md.mid);
   }
   md.ns_scale[2] = (md.x16 && !any_bad) ? x16_prescale(tail[2 * mi]) : 1.f;
+}
+
+// Direct (peer-memory) reduce-scatter + all-gather of the packed buffers (DION2_FLAG_DIST_DIRECT):
+// this rank owns floats [rank * per, (rank + 1) * per) of the buffer; it sums them over the P
+// replicas' input buffers in rank order (as k_sum_rank_scores: the same bits on every replica)
+// and stores the sum into every replica's output buffer.  in / out may alias (loopback).
+__global__ void __launch_bounds__(256) k_dp_reduce_direct(DpPeerBufs B, int P, int rank, int64_t total) {
+  const int64_t per = (total + 4 * (int64_t)P - 1) / (4 * (int64_t)P) * 4;
+  const int64_t lo = (int64_t)rank * per, hi = lo + per < total ? lo + per : total;
+  for (int64_t x = lo + (int64_t)blockIdx.x * blockDim.x + threadIdx.x; x < hi; x += (int64_t)gridDim.x * blockDim.x) {
+    float v[kMaxPieceRanks];
+#pragma unroll
+    for (int r = 0; r < kMaxPieceRanks; ++r)
+      if (r < P) v[r] = __ldcg(B.in[r] + x);
+    float s = 0.f;
+#pragma unroll
+    for (int r = 0; r < kMaxPieceRanks; ++r)
+      if (r < P) s += v[r];
+#pragma unroll
+    for (int r = 0; r < kMaxPieceRanks; ++r)
+      if (r < P) B.out[r][x] = s;
+  }
+}
+
+void launch_dp_reduce_direct(cudaStream_t s, const DpPeerBufs& B, int P, int rank, int64_t total, int sms) {
+  const int64_t per = (total + 4 * (int64_t)P - 1) / (4 * (int64_t)P) * 4;
+  const int64_t blocks = std::max<int64_t>(1, std::min<int64_t>((per + 255) / 256, (int64_t)sms * 8));
+  k_dp_reduce_direct<<<(unsigned)blocks, 256, 0, s>>>(B, P, rank, total);
 }
 
 void launch_dp_tail(cudaStream_t s, const MatDesc* mats, int n_mats, float* tail, int32_t* bad, int32_t* status,

@@ -98,6 +98,12 @@ void launch_dp_tail(cudaStream_t s, const MatDesc* mats, int n_mats, float* tail
                     bool combine);
 void launch_dp_pack(bool unpack, cudaStream_t s, const MatDesc* mats, const int32_t* row_prefix, const int64_t* buf_off,
                     int n_mats, int total_rows, float* buf, float scale, const int32_t* bad);
+// direct DP-sync exchange (peer memory): every replica's packed input and reduced output buffer
+struct DpPeerBufs {
+  const float* in[kMaxPieceRanks];
+  float* out[kMaxPieceRanks];
+};
+void launch_dp_reduce_direct(cudaStream_t s, const DpPeerBufs& B, int P, int rank, int64_t total, int sms);
 
 // ---------------- K4-K6 Newton-Schulz GEMMs
 // D = oscale * (cacc * Aop . Bop + cC * C), written as OutT.

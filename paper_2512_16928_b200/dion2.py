@@ -683,6 +683,15 @@ class Dion2DpSync:
             raise Dion2Error(rc, "dion2_step_batched_dpsync")
         self.last_comm_bytes = nbytes.value
 
+    def exchange_mode(self) -> str:
+        """"direct" (peer-memory reduce-scatter / all-gather into symmetric windows) or "nccl"
+        (ncclAllReduce), "none" before the first step; loopback reports the mode it emulates."""
+        if not self._ws:
+            return "none"
+        return {1: "direct", 0: "nccl"}.get(_lib().dion2_dist_exchange_mode(self._ws[0].data_ptr()),
+                                            "direct" if self.loopback and self.cfg_kw.get("dist_direct") else
+                                            ("nccl" if self.loopback else "none"))
+
     def status(self, replica: int = 0) -> Tuple[int, int]:
         """(code, first bad matrix) of this rank's replica (loopback: of replica `replica`); a
         matrix non-finite on any replica is reported (and skipped) on every replica."""

@@ -18,8 +18,9 @@ pytestmark = pytest.mark.gpu
 SHAPES = [(256, 512), (512, 256), (384, 640), (1024, 512)]
 
 
-def _run(world, precision, tol, steps=3, mode="loopback", m_transposed=False):
-    """m_transposed: column-mode matrices keep M transposed (cols, rows) on every replica."""
+def _run(world, precision, tol, steps=3, mode="loopback", m_transposed=False, direct=False, keep=None):
+    """m_transposed: column-mode matrices keep M transposed (cols, rows) on every replica.
+    direct: the peer-memory reduce (DION2_FLAG_DIST_DIRECT).  keep: a dict receiving W and M."""
     seed, alpha = 21, 0.25
     W0 = [gen_w0(m, n, 0, i) for i, (m, n) in enumerate(SHAPES)]
     reps = world if mode == "loopback" else 1
@@ -30,7 +31,7 @@ def _run(world, precision, tol, steps=3, mode="loopback", m_transposed=False):
     Wr = [[w.astype(np.float64) for w in W0] for _ in range(world)]
     Mr = [[np.zeros((m, n)) for (m, n) in SHAPES] for _ in range(world)]
     opt = D.Dion2DpSync(loopback_world=world if mode == "loopback" else 0, alpha=alpha, precision=precision,
-                        seed=seed, m_transposed=mts)
+                        seed=seed, m_transposed=mts, dist_direct=direct)
     for t in range(steps):
         G = [[gen_grad(m, n, 100 + r, i, t) for i, (m, n) in enumerate(SHAPES)] for r in range(world)]
         if mode == "loopback":
@@ -54,6 +55,8 @@ def _run(world, precision, tol, steps=3, mode="loopback", m_transposed=False):
             rr = r if mode == "loopback" else __import__("torch.distributed").distributed.get_rank()
             mg = (Mg[r][i].T if mts[i] else Mg[r][i]).cpu().double().numpy()
             assert np.abs(mg - Mr[rr][i]).max() <= 1e-5 * np.abs(Mr[rr][i]).max()
+    if keep is not None:
+        keep["W"], keep["M"] = Wg, Mg
     return opt
 
 
@@ -114,3 +117,38 @@ def test_dpsync_nonfinite_on_one_replica_skips_the_matrix_everywhere():
         assert torch.isfinite(Mg[0][2]).all()
         for i in (0, 1, 3):
             assert torch.equal(Wg[r][i], Wg[0][i]) and not torch.equal(Wg[r][i].cpu(), torch.from_numpy(W0[i]))
+
+
+# ------------------------------------------------------------- direct peer-memory reduce
+@pytest.mark.parametrize("world", [2, 3, 8])
+def test_dpsync_loopback_direct_is_bitwise_the_allreduce(world):
+    """DION2_FLAG_DIST_DIRECT: every replica reduces its slice of the packed buffer over all
+    replicas' buffers (rank order) and writes it into every buffer -- the same sums, so W and M
+    are bit-identical to the all-reduce emulation's, with the same byte count."""
+    a, b = {}, {}
+    o1 = _run(world, "bf16", 2e-2, keep=a)
+    o2 = _run(world, "bf16", 2e-2, direct=True, keep=b)
+    assert o1.last_comm_bytes == o2.last_comm_bytes
+    for r in range(world):
+        for i in range(len(SHAPES)):
+            assert torch.equal(a["W"][r][i], b["W"][r][i]) and torch.equal(a["M"][r][i], b["M"][r][i]), (r, i)
+
+
+def test_dpsync_nccl_single_rank_direct():
+    """The symmetric-window path with a one-rank group: pack into the window, LSA barrier, the
+    reduce kernel through the peer pointers, barrier, unpack from the output window."""
+    import torch.distributed as dist
+    s = socket.socket()
+    s.bind(("127.0.0.1", 0))
+    os.environ["MASTER_ADDR"] = "127.0.0.1"
+    os.environ["MASTER_PORT"] = str(s.getsockname()[1])
+    s.close()
+    dist.init_process_group("nccl", rank=0, world_size=1, device_id=torch.device("cuda", 0))
+    try:
+        opt = _run(1, "bf16", 2e-2, mode="nccl", direct=True)
+        assert opt.exchange_mode() == "direct"
+        del opt
+        _run(1, "fp32", 1e-5, mode="nccl", direct=True)
+        _run(1, "bf16", 2e-2, mode="nccl", direct=True, m_transposed=True)
+    finally:
+        dist.destroy_process_group()

@@ -7,7 +7,8 @@ One process per GPU (torch.multiprocessing, spawn), NCCL over NVLink, 127.0.0.1 
     exchange and with the direct peer exchange over symmetric memory (DION2_FLAG_DIST_DIRECT);
   * the FSDP2 integration (fully_shard with dion2_placement + Dion2FSDP) against the oracle;
   * compressed DP-sync (dion2_step_batched_dpsync): replicas with different local gradients
-    stay bit-identical and match the oracle's replica model.
+    stay bit-identical and match the oracle's replica model, with ncclAllReduce and with the
+    direct peer-memory reduce.
 The single-GPU suite covers the same code in loopback (test_gpu_dist.py, test_gpu_dpsync.py).
 """
 import os
@@ -54,6 +55,9 @@ def _worker(rank, world, port, which, errq):
                 import test_gpu_dpsync as T
                 T._run(world, "bf16", 2e-2, mode="nccl")
                 T._run(world, "fp32", 1e-5, mode="nccl")
+                opt = T._run(world, "bf16", 2e-2, mode="nccl", direct=True)
+                assert opt.exchange_mode() == "direct"
+                del opt
         finally:
             dist.destroy_process_group()
     except BaseException as e:  # noqa: BLE001  (reported to the parent)
