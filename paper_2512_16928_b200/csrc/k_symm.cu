@@ -50,6 +50,9 @@ struct SymmApi {
   ncclResult_t (*win_register)(ncclComm_t, void*, size_t, ncclWindow_t*, int) = nullptr;
   ncclResult_t (*devcomm_create)(ncclComm_t, const ncclDevCommRequirements_t*, ncclDevComm_t*) = nullptr;
   ncclTeam_t (*team_lsa)(ncclComm_t) = nullptr;
+  ncclResult_t (*mem_free)(void*) = nullptr;
+  ncclResult_t (*allreduce)(const void*, void*, size_t, ncclDataType_t, ncclRedOp_t, ncclComm_t, cudaStream_t) =
+      nullptr;
   bool ok = false;
 };
 
@@ -63,7 +66,9 @@ SymmApi& symm_api() {
     a.win_register = reinterpret_cast<decltype(a.win_register)>(dlsym(h, "ncclCommWindowRegister"));
     a.devcomm_create = reinterpret_cast<decltype(a.devcomm_create)>(dlsym(h, "ncclDevCommCreate"));
     a.team_lsa = reinterpret_cast<decltype(a.team_lsa)>(dlsym(h, "ncclTeamLsa"));
-    a.ok = a.mem_alloc && a.win_register && a.devcomm_create && a.team_lsa;
+    a.mem_free = reinterpret_cast<decltype(a.mem_free)>(dlsym(h, "ncclMemFree"));
+    a.allreduce = reinterpret_cast<decltype(a.allreduce)>(dlsym(h, "ncclAllReduce"));
+    a.ok = a.mem_alloc && a.win_register && a.devcomm_create && a.team_lsa && a.mem_free && a.allreduce;
     return a;
   }();
   return api;
@@ -97,10 +102,34 @@ int symm_create(void* comm, int world, size_t bytes, cudaStream_t s, SymmState**
   auto* st = new SymmState();
   st->comm = cm;
   const size_t sz = (bytes + NCCL_WIN_REQUIRED_ALIGNMENT - 1) / NCCL_WIN_REQUIRED_ALIGNMENT * NCCL_WIN_REQUIRED_ALIGNMENT;
-  for (int b = 0; b < 2; ++b) {
-    if (api.mem_alloc(&st->buf[b], sz) != ncclSuccess) return DION2_ENCCL;
-    if (api.win_register(cm, st->buf[b], sz, &st->win[b], NCCL_WIN_COLL_SYMMETRIC) != ncclSuccess) return DION2_ENCCL;
+  // the (local) allocations first, then agree on them over the communicator: every rank falls
+  // back to send / recv together if any rank could not allocate, before the collective
+  // registrations
+  int ok = 1;
+  for (int b = 0; b < 2; ++b)
+    if (api.mem_alloc(&st->buf[b], sz) != ncclSuccess) {
+      st->buf[b] = nullptr;
+      ok = 0;
+    }
+  int* dok = nullptr;
+  int all_ok = 0;
+  if (cudaMalloc(&dok, sizeof(int)) != cudaSuccess) return DION2_ECUDA;
+  if (cudaMemcpyAsync(dok, &ok, sizeof(int), cudaMemcpyHostToDevice, s) != cudaSuccess ||
+      api.allreduce(dok, dok, 1, ncclInt32, ncclMin, cm, s) != ncclSuccess ||
+      cudaMemcpyAsync(&all_ok, dok, sizeof(int), cudaMemcpyDeviceToHost, s) != cudaSuccess ||
+      cudaStreamSynchronize(s) != cudaSuccess) {
+    cudaFree(dok);
+    return DION2_ENCCL;
   }
+  cudaFree(dok);
+  if (!all_ok) {
+    for (int b = 0; b < 2; ++b)
+      if (st->buf[b]) api.mem_free(st->buf[b]);
+    delete st;
+    return DION2_EUNSUPPORTED;
+  }
+  for (int b = 0; b < 2; ++b)
+    if (api.win_register(cm, st->buf[b], sz, &st->win[b], NCCL_WIN_COLL_SYMMETRIC) != ncclSuccess) return DION2_ENCCL;
   ncclDevCommRequirements_t req{};
   req.lsaBarrierCount = 1;
   if (api.devcomm_create(cm, &req, &st->dev) != ncclSuccess) return DION2_ENCCL;
@@ -108,10 +137,10 @@ int symm_create(void* comm, int world, size_t bytes, cudaStream_t s, SymmState**
   if (cudaMalloc(&dptr, 2 * sizeof(void*) * world) != cudaSuccess) return DION2_ECUDA;
   k_symm_peers<<<1, 32, 0, s>>>(st->win[0], st->win[1], world, dptr);
   std::vector<void*> h(2 * world);
-  const bool ok = cudaMemcpyAsync(h.data(), dptr, 2 * sizeof(void*) * world, cudaMemcpyDeviceToHost, s) == cudaSuccess &&
-                  cudaStreamSynchronize(s) == cudaSuccess;
+  const bool got = cudaMemcpyAsync(h.data(), dptr, 2 * sizeof(void*) * world, cudaMemcpyDeviceToHost, s) == cudaSuccess &&
+                   cudaStreamSynchronize(s) == cudaSuccess;
   cudaFree(dptr);
-  if (!ok) return DION2_ECUDA;
+  if (!got) return DION2_ECUDA;
   peer_recv.resize(world);
   peer_osend.resize(world);
   for (int p = 0; p < world; ++p) {

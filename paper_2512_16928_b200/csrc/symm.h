@@ -15,7 +15,9 @@ struct SymmState;
 // receive and outgoing windows (`bytes` each, ncclMemAlloc + symmetric registration), a device
 // communicator with one LSA barrier, and returns this rank's window bases and every rank's
 // window bases as mapped into this process.  DION2_EUNSUPPORTED when NCCL lacks the device API
-// or not every rank is load/store reachable (one NVLink domain).  Synchronises `s` once.
+// or not every rank is load/store reachable (one NVLink domain), or any rank could not allocate
+// its windows (agreed with one all-reduce before the collective registration, so every rank
+// returns the same code).  Synchronises `s`.
 int symm_create(void* comm, int world, size_t bytes, cudaStream_t s, SymmState** out, uint8_t** local_recv,
                 uint8_t** local_osend, std::vector<uint8_t*>& peer_recv, std::vector<uint8_t*>& peer_osend);
 
