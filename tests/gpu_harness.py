@@ -251,7 +251,8 @@ def run_parity_dist(shapes, alpha, world, steps=3, seed=0, mode="loopback", axis
     return res
 
 
-def run_parity_fsdp(shapes, alpha, steps=3, seed=0, mu=0.95, lr=0.02, m_transposed=True, select="l1"):
+def run_parity_fsdp(shapes, alpha, steps=3, seed=0, mu=0.95, lr=0.02, m_transposed=True, select="l1",
+                    direct=False):
     """The FSDP2 integration (paper_2512_16928_b200.fsdp): one bias-free Linear per (out, in)
     shape, `fully_shard` with `dion2_placement()` on the initialised torch.distributed world,
     gradients set as DTensors in the parameters' placements, `Dion2FSDP.step`, against the
@@ -273,7 +274,7 @@ def run_parity_fsdp(shapes, alpha, steps=3, seed=0, mu=0.95, lr=0.02, m_transpos
             lin.weight.copy_(torch.from_numpy(w))
     fully_shard(model, mesh=mesh, shard_placement_fn=dion2_placement(alpha=alpha))
     params = [lin.weight for lin in model]
-    opt = Dion2FSDP(params, lr=lr, mu=mu, alpha=alpha, m_transposed=m_transposed, select=select)
+    opt = Dion2FSDP(params, lr=lr, mu=mu, alpha=alpha, m_transposed=m_transposed, select=select, dist_direct=direct)
     Wr = [w.astype(np.float64) for w in W0]
     Mr = [np.zeros((m, n)) for (m, n) in shapes]
     for t in range(steps):
@@ -292,4 +293,5 @@ def run_parity_fsdp(shapes, alpha, steps=3, seed=0, mu=0.95, lr=0.02, m_transpos
         res.dW_rel.append(float(np.linalg.norm(wg - W0[i] - dref) / max(np.linalg.norm(dref), 1e-300)))
         res.W_rel.append(float(np.linalg.norm(wg - Wr[i]) / np.linalg.norm(Wr[i])))
     res.comm_bytes = opt.comm_bytes()
+    res.exchange = [e.exchange_mode() for e in opt._engines]
     return res

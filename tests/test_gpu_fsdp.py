@@ -32,11 +32,12 @@ def nccl_world1():
     dist.destroy_process_group()
 
 
-@pytest.mark.parametrize("mt", [True, False])
-def test_fsdp_one_rank(nccl_world1, mt):
+@pytest.mark.parametrize("mt,direct", [(True, False), (False, False), (True, True)])
+def test_fsdp_one_rank(nccl_world1, mt, direct):
     res = run_parity_fsdp([(256, 512), (512, 256), (1024, 1024), (2048, 512), (512, 2048)], 0.25, steps=3,
-                          m_transposed=mt)
+                          m_transposed=mt, direct=direct)
     assert max(res.dW_rel) <= 2e-2, res
+    assert res.exchange == ["direct" if direct else "nccl"], res.exchange
 
 
 def test_fsdp_training_loop(nccl_world1):
