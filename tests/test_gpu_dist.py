@@ -112,6 +112,12 @@ def test_loopback_direct_exchange(world):
     _assert(run_parity_dist(layer_set_1b(1), 0.25, world, steps=2, direct=True))
 
 
+def test_loopback_direct_three_ranks():
+    """A rank count that is not a power of two (o / P a multiple of 8 but not of 64: the owner's
+    pieces are assembled by copies, pushed and pulled directly)."""
+    _assert(run_parity_dist([(384, 768), (768, 384), (1536, 1536), (480, 1920)], 0.25, 3, steps=3, direct=True))
+
+
 @pytest.mark.parametrize("world", [2, 8])
 def test_loopback_direct_is_bitwise_the_copy_exchange(world):
     """Same kernels, same bytes, other addresses: W, M and the index sets after 3 steps are
