@@ -9,5 +9,5 @@ for spec in ${VARIANTS:-default}; do
   envs=""
   [ "$spec" != "$name" ] && envs=$(echo "${spec#*:}" | tr ',' ' ')
   env $envs timeout 600 $B > gpurun_out/abns_$name.log 2>&1
-  cp gpurun_out/bench_details_1b_n1.json gpurun_out/abns_details_$name.json 2>/dev/null
+  cp gpurun_out/bench_details_${AB_CFG:-1b}_n1.json gpurun_out/abns_details_$name.json 2>/dev/null
 done
