@@ -610,6 +610,18 @@ class Dion2Loopback:
             raise Dion2Error(rc, "dion2_step_batched_loopback")
         self.last_comm_bytes = nbytes.value
 
+    def release(self) -> None:
+        """Drop the library's plans keyed on this object's workspaces."""
+        for w in self._ws:
+            _lib().dion2_release_workspace(w.data_ptr(), w.numel())
+        self._ws = []
+
+    def __del__(self):
+        try:
+            self.release()
+        except Exception:  # interpreter shutdown: the library may already be gone
+            pass
+
 
 class Dion2DpSync:
     """Compressed DP-sync (paper 3.2): each rank is a data-parallel replica with full W, M
@@ -682,6 +694,19 @@ class Dion2DpSync:
         if rc:
             raise Dion2Error(rc, "dion2_step_batched_dpsync")
         self.last_comm_bytes = nbytes.value
+
+    def release(self) -> None:
+        """Drop the library's plans keyed on this object's workspaces (the symmetric windows of a
+        direct-exchange plan are tied to its communicator: release before destroying the group)."""
+        for w in self._ws:
+            _lib().dion2_release_workspace(w.data_ptr(), w.numel())
+        self._ws = []
+
+    def __del__(self):
+        try:
+            self.release()
+        except Exception:  # interpreter shutdown: the library may already be gone
+            pass
 
     def exchange_mode(self) -> str:
         """"direct" (peer-memory reduce-scatter / all-gather into symmetric windows) or "nccl"
