@@ -163,3 +163,46 @@ def test_nccl_direct_single_rank():
                                 direct=True))
     finally:
         dist.destroy_process_group()
+
+
+@pytest.mark.parametrize("world", [2, 4])
+def test_loopback_bf16_state_direct_and_copy(world):
+    """bf16 W and bf16 G through the distributed step (the sparse update rounds W once, the
+    K1 reads bf16 gradients): the direct and the copy exchange give bit-identical W and M,
+    and the cumulative update matches the single-GPU step on the same bf16 inputs within the
+    NS tolerance."""
+    from paper_2512_16928_b200 import Dion2
+    from paper_2512_16928_b200 import dion2 as D
+    from synth import gen_grad, gen_w0
+    shapes = [(512, 1024), (1024, 512), (1024, 1024), (2048, 512)]
+    axes = D.dist_info(shapes, world, 0)["axis"]
+    W0 = [torch.from_numpy(gen_w0(m, n, 3, i)).to(torch.bfloat16) for i, (m, n) in enumerate(shapes)]
+    Gs = [[torch.from_numpy(gen_grad(m, n, 3, i, t, row_scaled=True)).to(torch.bfloat16)
+           for i, (m, n) in enumerate(shapes)] for t in range(3)]
+    out = {}
+    for direct in (False, True):
+        opt = D.Dion2Loopback(shapes, world, alpha=0.25, dist_direct=direct)
+        W = [[D.shard_of(W0[i], axes[i], world, r).cuda() for i in range(len(shapes))] for r in range(world)]
+        M = [[torch.zeros(w.shape, device="cuda") for w in W[r]] for r in range(world)]
+        for t in range(3):
+            G = [[D.shard_of(Gs[t][i], axes[i], world, r).cuda() for i in range(len(shapes))] for r in range(world)]
+            opt.step(W, M, G, step=t)
+        torch.cuda.synchronize()
+        out[direct] = (W, M)
+    for r in range(world):
+        for i in range(len(shapes)):
+            assert torch.equal(out[False][0][r][i], out[True][0][r][i]), (r, i)
+            assert torch.equal(out[False][1][r][i], out[True][1][r][i]), (r, i)
+    # single-GPU reference on the same bf16 inputs
+    single = Dion2(alpha=0.25)
+    Ws = [w.clone().cuda() for w in W0]
+    Ms = [torch.zeros(w.shape, device="cuda") for w in W0]
+    for t in range(3):
+        single.step(Ws, Ms, [g.cuda() for g in Gs[t]])
+    torch.cuda.synchronize()
+    for i in range(len(shapes)):
+        Wd = torch.cat([out[True][0][r][i] for r in range(world)], dim=1 if axes[i] == 0 else 0).float()
+        d_dist = (Wd - W0[i].cuda().float())
+        d_single = (Ws[i].float() - W0[i].cuda().float())
+        rel = (torch.linalg.norm(d_dist - d_single) / torch.linalg.norm(d_single)).item()
+        assert rel <= 2e-2, (i, rel)
