@@ -364,16 +364,17 @@ def run_ours(args):
         # K3 pushes into the owner's window, K7 pulls O; the library falls back to NCCL send /
         # recv where that is unavailable); DION2_BENCH_DIRECT=0 forces send / recv
         direct = os.environ.get("DION2_BENCH_DIRECT", "1") == "1"
-        make_opt = lambda a: D.Dion2Dist(shapes, alpha=a, axis="auto", precision="bf16",  # noqa: E731
-                                          ns_form=args.ns_form, m_transposed=mts, dist_direct=direct)
+        make_opt = lambda a, graph=True: D.Dion2Dist(shapes, alpha=a, axis="auto", precision="bf16",  # noqa: E731
+                                                      ns_form=args.ns_form, m_transposed=mts, dist_direct=direct,
+                                                      cuda_graph=graph and not args.no_graph)
     else:
         info = None
         # optimizer-state layout: momentum of column-mode matrices stored transposed (the
         # column gather of M[:, K] becomes a contiguous row gather of M^T); --no-mt disables
         mts = [(not args.no_mt) and m > n for (m, n) in shapes]
         bufs, Ws, Ms, Gs = build_state(shapes, dev, seed=rank, m_transposed=mts)
-        make_opt = lambda a: Dion2(alpha=a, axis="auto", precision="bf16", m_transposed=mts,  # noqa: E731
-                                   ns_form=args.ns_form, cuda_graph=not args.no_graph)
+        make_opt = lambda a, graph=True: Dion2(alpha=a, axis="auto", precision="bf16", m_transposed=mts,  # noqa: E731
+                                               ns_form=args.ns_form, cuda_graph=graph and not args.no_graph)
     opt = make_opt(args.alpha)
 
     with ClockSampler(local) as clk:
@@ -387,14 +388,13 @@ def run_ours(args):
 
     # the same step without the CUDA graph (every step's launches enqueued by the host)
     ms_eager = None
-    if not use_dist and not args.no_graph:
-        opt_e = Dion2(alpha=args.alpha, axis="auto", precision="bf16", m_transposed=mts, ns_form=args.ns_form)
-        ms_eager = time_steps(opt_e, Ws, Ms, Gs, args.steps, args.warmup, None)
+    if not args.no_graph:
+        opt_e = make_opt(args.alpha, graph=False)
+        ms_eager = time_steps(opt_e, Ws, Ms, Gs, args.steps, args.warmup, barrier)
         del opt_e
 
     # per-phase device time (CUDA events on the launching stream around every launch)
-    opt_iso = Dion2(alpha=args.alpha, axis="auto", precision="bf16", m_transposed=mts, ns_form=args.ns_form) \
-        if not use_dist else make_opt(args.alpha)  # eager: the phase events are recorded per host launch
+    opt_iso = make_opt(args.alpha, graph=False)  # eager: the phase events are recorded per host launch
     opt_iso.step(Ws, Ms, Gs)  # build the plan outside the timed pass
     set_phase_timing(True)
     ms_timed = time_steps(opt_iso, Ws, Ms, Gs, args.steps, 0, None)
@@ -604,7 +604,7 @@ def run_ours(args):
                        "l2_flush": f"not needed: {12 * n_params / 1e9:.1f} GB touched per step >> 126 MB L2",
                        "parallelism": "single GPU" if not use_dist else
                        f"owner-compute over {world} GPUs ({xmode} exchange; shards along the non-selection axis)",
-                       "step_mode": "CUDA graph" if (not use_dist and not args.no_graph) else "eager"},
+                       "step_mode": "CUDA graph" if not args.no_graph else "eager"},
             "roofline": roof,
             "cpu_baseline": cpu,
             "e2e": {"value": e2e_ms, "unit": "ms/step", "h2d_bytes_per_step": h2d, "d2h_bytes_per_step": d2h},

@@ -206,3 +206,39 @@ def test_loopback_bf16_state_direct_and_copy(world):
         d_single = (Ws[i].float() - W0[i].cuda().float())
         rel = (torch.linalg.norm(d_dist - d_single) / torch.linalg.norm(d_single)).item()
         assert rel <= 2e-2, (i, rel)
+
+
+@pytest.mark.parametrize("direct", [False, True])
+def test_nccl_graph_replay_is_bitwise_eager(direct):
+    """Dion2Dist(cuda_graph=True): the step captured on its second identical call (NCCL calls or
+    the direct-exchange barriers inside the graph) and replayed gives bit-identical W and M to
+    the eager step, also when eta changes between replays (read on the device)."""
+    import torch.distributed as dist
+    from paper_2512_16928_b200 import dion2 as D
+    from synth import gen_grad, gen_w0
+    os.environ.setdefault("MASTER_ADDR", "127.0.0.1")
+    os.environ["MASTER_PORT"] = str(_free_port())
+    torch.cuda.set_device(0)
+    dist.init_process_group("nccl", rank=0, world_size=1, device_id=torch.device("cuda", 0))
+    try:
+        shapes = SHAPES + [(1024, 256)]
+        out = []
+        for graph in (False, True):
+            opt = D.Dion2Dist(shapes, alpha=0.25, dist_direct=direct, cuda_graph=graph)
+            W = [torch.from_numpy(gen_w0(m, n, 4, i)).cuda() for i, (m, n) in enumerate(shapes)]
+            M = [torch.zeros(m, n, device="cuda") for (m, n) in shapes]
+            G = [torch.empty(m, n, device="cuda") for (m, n) in shapes]
+            for t in range(5):
+                for i, (m, n) in enumerate(shapes):
+                    G[i].copy_(torch.from_numpy(gen_grad(m, n, 4, i, t, row_scaled=True)))
+                opt.step(W, M, G, lr=0.02 * (1.0 - 0.1 * t))
+            torch.cuda.synchronize()
+            if graph:
+                assert opt._graph is not None  # steps 3..5 replayed
+            out.append((W, M))
+            opt.release()
+        for i in range(len(shapes)):
+            assert torch.equal(out[0][0][i], out[1][0][i]), i
+            assert torch.equal(out[0][1][i], out[1][1][i]), i
+    finally:
+        dist.destroy_process_group()
