@@ -545,7 +545,8 @@ class Dion2Dist:
             if repeat:  # the second identical call: capture it (this call's step ran above)
                 ws_before = self._ws
                 g = torch.cuda.CUDAGraph()
-                with torch.cuda.graph(g):
+                # thread-local capture: the process group's watchdog thread may query its events
+                with torch.cuda.graph(g, capture_error_mode="thread_local"):
                     self._step(Ws, Ms, Gs, sel_out, None, lr_device=True, **override)
                 if self._ws is ws_before:
                     self._graph, self._gkey = g, key
