@@ -619,17 +619,43 @@ class Dion2Loopback:
     exchanges are device copies (dion2_step_batched_loopback).  For testing the
     distributed layout and kernels without several GPUs."""
 
-    def __init__(self, shapes, world, m_transposed=None, **cfg_kw):
+    def __init__(self, shapes, world, m_transposed=None, cuda_graph: bool = False, **cfg_kw):
+        """cuda_graph: as Dion2Dist (capture on the second identical call, replay after)."""
         self.shapes = [tuple(s) for s in shapes]
         self.world = world
         self.cfg_kw = dict(cfg_kw)
         self.m_transposed = m_transposed
+        self.cuda_graph = cuda_graph
+        self._graph = None
+        self._gkey = None
+        self._prev_key = None
         self.infos = [dist_info(self.shapes, world, r, m_transposed=m_transposed, **cfg_kw) for r in range(world)]
         self._ws: List[torch.Tensor] = []
         self.last_comm_bytes = 0
 
     def step(self, Ws, Ms, Gs, sel_out=None, stream=None, **override):
         """Ws, Ms, Gs: [world][n] local shards; sel_out: optional [world][n] int32 tensors."""
+        if self.cuda_graph and stream is None:
+            flat = lambda tss: tuple((t.data_ptr(), tuple(t.shape), t.dtype) for ts in tss for t in ts)  # noqa: E731
+            key = (flat(Ws), flat(Ms), flat(Gs), flat(sel_out or ()),
+                   tuple(sorted((k, repr(v)) for k, v in {**self.cfg_kw, **override}.items())))
+            if self._graph is not None and key == self._gkey:
+                self._graph.replay()
+                return
+            repeat = key == self._prev_key
+            self._prev_key = key
+            self._step(Ws, Ms, Gs, sel_out, None, **override)
+            if repeat:
+                ws_before = list(self._ws)
+                g = torch.cuda.CUDAGraph()
+                with torch.cuda.graph(g, capture_error_mode="thread_local"):
+                    self._step(Ws, Ms, Gs, sel_out, None, **override)
+                if self._ws == ws_before:
+                    self._graph, self._gkey = g, key
+            return
+        self._step(Ws, Ms, Gs, sel_out, stream, **override)
+
+    def _step(self, Ws, Ms, Gs, sel_out, stream, **override):
         kw = dict(self.cfg_kw)
         kw.update(override)
         kw.setdefault("grad_dtype", Gs[0][0].dtype)
@@ -642,6 +668,7 @@ class Dion2Loopback:
             for w in self._ws:
                 _lib().dion2_release_workspace(w.data_ptr(), w.numel())
             self._ws = [torch.empty(need, dtype=torch.uint8, device=dev) for _ in range(P)]
+            self._graph = None
         arr = (Dion2Shard * (n * P))()
         for r in range(P):
             part = _shards(self.shapes, Ws[r], Ms[r], Gs[r], sel_out[r] if sel_out is not None else None,
@@ -659,6 +686,7 @@ class Dion2Loopback:
 
     def release(self) -> None:
         """Drop the library's plans keyed on this object's workspaces."""
+        self._graph = None
         for w in self._ws:
             _lib().dion2_release_workspace(w.data_ptr(), w.numel())
         self._ws = []

@@ -27,6 +27,7 @@ def main():
     ap.add_argument("--steps", type=int, default=3)
     ap.add_argument("--alpha", type=float, default=0.25)
     ap.add_argument("--direct", action="store_true", help="direct peer exchange (DION2_FLAG_DIST_DIRECT)")
+    ap.add_argument("--graph", action="store_true", help="time CUDA-graph replays (Dion2Loopback(cuda_graph=True))")
     args = ap.parse_args()
     shapes = layer_set_1b(24)
     out = {}
@@ -42,8 +43,10 @@ def main():
                 m.append(torch.zeros((sc, sr) if mt else (sr, sc), device="cuda"))
                 g.append(torch.randn(sr, sc, device="cuda"))
             Ws.append(w), Ms.append(m), Gs.append(g)
-        opt = D.Dion2Loopback(shapes, P, alpha=args.alpha, m_transposed=mts, dist_direct=args.direct)
-        opt.step(Ws, Ms, Gs)
+        opt = D.Dion2Loopback(shapes, P, alpha=args.alpha, m_transposed=mts, dist_direct=args.direct,
+                              cuda_graph=args.graph)
+        for _ in range(3 if args.graph else 1):  # graph mode captures on the second call
+            opt.step(Ws, Ms, Gs)
         torch.cuda.synchronize()
         e0, e1 = torch.cuda.Event(enable_timing=True), torch.cuda.Event(enable_timing=True)
         e0.record()
@@ -53,13 +56,17 @@ def main():
         torch.cuda.synchronize()
         total = e0.elapsed_time(e1) / args.steps
         set_phase_timing(True)
+        opt_e = D.Dion2Loopback(shapes, P, alpha=args.alpha, m_transposed=mts, dist_direct=args.direct)
+        opt_e.step(Ws, Ms, Gs)
+        get_phase_times()  # drop the plan-building step's events
         for _ in range(args.steps):
-            opt.step(Ws, Ms, Gs)
+            opt_e.step(Ws, Ms, Gs)
         ph = get_phase_times()
         set_phase_timing(False)
         out[P] = {"ms_all_ranks": total, "ms_per_rank_est": total / P,
                   "phases_ms_per_rank": {k: v[0] / args.steps / P for k, v in ph.items() if v[1]},
-                  "exchange_bytes_per_rank": opt.last_comm_bytes / P}
+                  # rank 0's bytes sent (the loopback transport counts rank 0's side)
+                  "exchange_bytes_rank0": opt.last_comm_bytes}
         del Ws, Ms, Gs, opt
         torch.cuda.empty_cache()
     print(json.dumps(out, indent=1))
