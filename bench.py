@@ -545,7 +545,11 @@ def run_ours(args):
         opt.step(Ws, Ms, Gs)
         comm = {"sent_bytes_per_step_rank": opt.last_comm_bytes,
                 "analytic_piece_bytes_per_step_rank": 2 * sum(info["send_bytes"][o] for o in range(world) if o != rank),
-                "note": "gather-to-owner + scatter-back of k x (o/P) bf16 pieces, plus the score all-gather"}
+                # the NVLink floor of those bytes (each exchange sends and receives concurrently at
+                # 900 GB/s per direction; C2 and C3 follow each other)
+                "nvlink_floor_ms": opt.last_comm_bytes / 900e9 * 1e3,
+                "exchange": xmode,
+                "note": "gather-to-owner + scatter-back of k x (o/P) fp16 pieces, plus the score all-gather"}
 
     # max over ranks
     if world > 1:
