@@ -180,7 +180,7 @@ std::string plan_key(const dion2_matrix* mats, int n, const dion2_config* c, voi
 std::string env_key() {
   std::string k;
   for (const char* v : {"DION2_NS_PAIR", "DION2_NS_SYM", "DION2_NS_SERPENTINE", "DION2_NS_UPPER",
-                        "DION2_GRAM_SPLITK", "DION2_GRAM_PF", "DION2_DIST_CHUNKS"}) {
+                        "DION2_GRAM_SPLITK", "DION2_DIST_CHUNKS"}) {
     const char* e = getenv(v);
     k.append(e ? e : "-");
     k.push_back('|');
@@ -345,12 +345,6 @@ int build_layout(Plan& P, const dion2_matrix* mats, int n, const dion2_config* c
 }
 
 
-// L2 prefetch distance (k-blocks) of the gram launches (DION2_GRAM_PF, A/B only; default 0 = off:
-// 8 k-blocks ahead measured slower, gram 0.351 -> 0.383 ms per step on the 1B set)
-static int gram_prefetch_ahead() {
-  const char* e = getenv("DION2_GRAM_PF");
-  return e ? std::max(0, atoi(e)) : 0;
-}
 
 // Kind-5 launches (resident-A pair apply) count work in chunks of up to L consecutive 256-column
 // blocks of one 256-row block: L = 8, halved while the launch has fewer than two chunks per CTA pair.
@@ -490,7 +484,6 @@ static int append_gram_space_launches(Plan& P, const dion2_config* c, void* ws, 
       np.b_is_a = np.b_kmajor ? 1 : 0;
       for (int j = 0; j < np.ngroups; ++j) np.b_is_a &= np.g[j].a == np.g[j].b ? 1 : 0;
       if (L.kind == 5) apply_chunks(np);
-      if (phase == PH_GRAM) np.pf_ahead = gram_prefetch_ahead();
       P.ns_launches.push_back(L);
     }
     return DION2_OK;
@@ -797,7 +790,6 @@ int build_device_plan(Plan& P, const dion2_matrix* mats, const dion2_config* c, 
           np.b_is_a = np.b_kmajor ? 1 : 0;
           for (int j = 0; j < np.ngroups; ++j) np.b_is_a &= np.g[j].a == np.g[j].b ? 1 : 0;
           if (L.kind == 5) apply_chunks(np);
-          if (ph == PH_GRAM) np.pf_ahead = gram_prefetch_ahead();
           if (P.bf16_ns) {
             P.ns_launches.push_back(L);
           } else {

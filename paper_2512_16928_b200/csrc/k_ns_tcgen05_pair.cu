@@ -164,11 +164,6 @@ __global__ void __cluster_dims__(2, 1, 1) __launch_bounds__(kPairThreads, 1)
           const int pr = G.pieces_load ? (kb * kBK) / G.pieces_qo : 0;
           const int pc = G.pieces_load ? kb * kBK - pr * G.pieces_qo : kb * kBK;
           const CUtensorMap* pmap = G.pieces_load ? &P.mapP[c.group][pr] : nullptr;
-          if (p.pf_ahead && kb + p.pf_ahead < kb1 && !G.pieces_load) {
-            const int kp = (kb + p.pf_ahead) * kBK;
-            tma_prefetch_3d(&P.mapA[c.group], kp, c.tm * 256 + (int)rank * 128, c.z);
-            if (!same) tma_prefetch_3d(&P.mapB[c.group], kp, c.tn * 256 + (int)rank * 128, c.z);
-          }
           if (!at) {
             tma_load_3d_pair(sa, pmap ? pmap : &P.mapA[c.group], leader_full, pc, c.tm * 256 + (int)rank * 128, c.z);
           } else {

@@ -155,9 +155,6 @@ struct NsParams {
   // resident-A apply (k_ns_apply_pair.cu): total_tiles counts chunks of up to chunk_len column
   // blocks of one 256-row block, NsGroup::tile_base the group's first chunk
   int chunk_len;
-  // pair kernel: L2-prefetch the operand boxes of k-block kb + pf_ahead while loading kb
-  // (long-K gram launches streaming X from DRAM); 0: off
-  int pf_ahead;
 };
 
 // tcgen05 path (k_ns_tcgen05.cu): tensor maps for the TMA operand loads.
