@@ -298,14 +298,20 @@ int build_layout(Plan& P, const dion2_matrix* mats, int n, const dion2_config* c
     g.off_X1 = off; off = align_up(off + xb, 4096);
     g.off_A = off;  off = align_up(off + ab, 4096);
     g.off_B = off;  off = align_up(off + ab, 4096);
-    // Gram-space form (reading R23): bf16 hot path, wide X with q >= 2p (AUTO) or forced
-    // AUTO: fewer FLOPs on the padded shapes (q_pad >= 2 p_pad), or every member has q >= 2p:
-    // small p padded up to 256 (e.g. 32 x 256) costs nothing either way and the Gram form
-    // rounds X once (error 0.4% instead of the direct form's 2%, R21 / R23)
-    bool all_wide = true;
-    for (int i : g.mats) all_wide = all_wide && P.mp[i].q >= 2 * P.mp[i].p;
+    // Gram-space form (reading R23): 16-bit hot path, wide X with q >= 2p (AUTO) or forced.
+    // AUTO: fewer FLOPs on the padded shapes (q_pad >= 2 p_pad), or every member has q >= 2p;
+    // and every member has p >= kGramMinP (R25: with fp16 X the direct form is the accurate one
+    // for short X, 0.2-0.9% against up to 3.5% emulated at p <= 32)
+    bool all_wide = true, all_tall_enough = true;
+    for (int i : g.mats) {
+      all_wide = all_wide && P.mp[i].q >= 2 * P.mp[i].p;
+      // reading R25: the fp16 Gram matrix of a short X (p < 64 rows) carries too much of each
+      // eigenvalue per entry -- AUTO keeps the direct form there
+      all_tall_enough = all_tall_enough && P.mp[i].p >= kGramMinP;
+    }
     g.gs = P.bf16_ns && (c->ns_form == DION2_NS_FORM_GRAM ||
-                         (c->ns_form == DION2_NS_FORM_AUTO && (g.q_pad >= 2 * g.p_pad || all_wide)));
+                         (c->ns_form == DION2_NS_FORM_AUTO && all_tall_enough &&
+                          (g.q_pad >= 2 * g.p_pad || all_wide)));
     g.off_C = g.off_Q0 = g.off_Q1 = 0;
     if (g.gs) {
       g.off_C = off;  off = align_up(off + ab, 4096);

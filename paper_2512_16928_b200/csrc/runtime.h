@@ -55,6 +55,9 @@ std::vector<dion2_matrix> storage_view(const dion2_matrix* mats, int n);
 std::string env_key();
 int validate_shape(const dion2_matrix& m, bool need_ptrs);
 
+// AUTO evaluates NS in Gram space only for X with at least this many rows (reading R25)
+constexpr int kGramMinP = 64;
+
 struct MatPlan {
   int mt;  // M stored transposed (cols mode): gather = rows path on M^T, scatter = path (cols / generic)
   int axis, d, o, k, sr, sc, transposed, p, q, p_pad, q_pad, group, zi, rowblocks, ga, gb, sa_pad, sb_pad, path,

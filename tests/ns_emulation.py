@@ -13,6 +13,7 @@ Recipes:
   * ``gram_f16``     -- current Gram-space form: the same prescaled fp16 X0, fp16 recursion,
                         restarted from an explicit X_t whenever prod |a_t| of a segment would
                         exceed 64 (reading R24): [0, 3) + [3, 5) for the default quintic.
+  * ``auto_f16``     -- the AUTO choice between the two (readings R23, R25).
 """
 from __future__ import annotations
 
@@ -119,6 +120,18 @@ def gram_f16(X, coeffs=O.DEFAULT_NS_COEFFS, eps=O.DEFAULT_NS_EPS, growth=RESTART
         Xh = f16(f32(sc * (Q @ Xh)))
         sc = 1.0
     return Xh
+
+
+GRAM_MIN_P = 64  # reading R25 (csrc/runtime.h kGramMinP)
+
+
+def auto_f16(X, coeffs=O.DEFAULT_NS_COEFFS, eps=O.DEFAULT_NS_EPS):
+    """ns_form AUTO for one matrix: the Gram form for wide X (q >= 2p) with p >= 64 rows, else
+    the direct form (readings R23, R25)."""
+    p, q = X.shape
+    if q >= 2 * p and p >= GRAM_MIN_P:
+        return gram_f16(X, coeffs, eps)
+    return direct_f16(X, coeffs, eps)
 
 
 def rel(got, want):
