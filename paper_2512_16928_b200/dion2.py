@@ -142,14 +142,20 @@ def make_config(alpha: float = 0.25, mu: float = 0.95, lr: float = 0.02, ns_step
     return cfg
 
 
+def _ld(t: torch.Tensor) -> int:
+    """Row stride in elements; a one-row tensor's stride(0) is arbitrary in torch (size-1 dims),
+    its leading dimension is its width."""
+    return t.stride(0) if t.shape[0] > 1 else t.shape[1]
+
+
 def _check_tensor(t: torch.Tensor, name: str, dtype: torch.dtype, like: Optional[torch.Tensor] = None):
     if not t.is_cuda:
         raise ValueError(f"{name} must be a CUDA tensor (no CPU path exists)")
     if t.dtype != dtype:
         raise ValueError(f"{name} must be {dtype}, got {t.dtype}")
-    if t.dim() != 2 or t.stride(1) != 1:
+    if t.dim() != 2 or (t.stride(1) != 1 and t.shape[1] > 1):
         raise ValueError(f"{name} must be 2-D with unit column stride")
-    if like is not None and (t.shape != like.shape or t.stride(0) != like.stride(0)):
+    if like is not None and (t.shape != like.shape or _ld(t) != _ld(like)):
         raise ValueError(f"{name} must match W's shape and row stride")
 
 
@@ -178,13 +184,13 @@ def describe(Ws: Sequence[torch.Tensor], Ms: Sequence[torch.Tensor], Gs: Sequenc
             _check_tensor(M, "M (transposed)", torch.float32)
             if tuple(M.shape) != (W.shape[1], W.shape[0]):
                 raise ValueError("a transposed M must have shape (cols, rows)")
-            arr[i].m_transposed, arr[i].ldm = 1, M.stride(0)
+            arr[i].m_transposed, arr[i].ldm = 1, _ld(M)
         else:
             _check_tensor(M, "M", torch.float32, W)
         _check_tensor(G, "G", gdt, W)
         # rows / cols are the LOGICAL fan-out / fan-in (the tensor is (n, m) under storage_transposed)
         arr[i].rows, arr[i].cols = (W.shape[1], W.shape[0]) if stt else (W.shape[0], W.shape[1])
-        arr[i].ld = W.stride(0)
+        arr[i].ld = _ld(W)
         arr[i].W, arr[i].M, arr[i].G = W.data_ptr(), M.data_ptr(), G.data_ptr()
         s = sel_out[i] if sel_out is not None else None
         o = O_out[i] if O_out is not None else None
@@ -451,11 +457,11 @@ def _shards(shapes, Ws=None, Ms=None, Gs=None, sels=None, m_transposed=None):
                 _check_tensor(Ms[i], "M shard (transposed)", torch.float32)
                 if tuple(Ms[i].shape) != (W.shape[1], W.shape[0]):
                     raise ValueError("a transposed M shard must have shape (shard cols, shard rows)")
-                arr[i].ldm = Ms[i].stride(0)
+                arr[i].ldm = _ld(Ms[i])
             else:
                 _check_tensor(Ms[i], "M shard", torch.float32, W)
             _check_tensor(Gs[i], "G shard", Gs[0].dtype, W)
-            arr[i].ld = W.stride(0)
+            arr[i].ld = _ld(W)
             arr[i].W, arr[i].M, arr[i].G = W.data_ptr(), Ms[i].data_ptr(), Gs[i].data_ptr()
             s = sels[i] if sels is not None else None
             arr[i].sel_out = s.data_ptr() if s is not None else None

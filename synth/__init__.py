@@ -64,6 +64,7 @@ def gen_grad_structured(m: int, n: int, seed: int = 0, mid: int = 0, step: int =
     z = r.standard_normal((m, n), dtype=np.float32)
     big = float(np.sqrt(max(m, n)))
     if kind == "spike":
+        rank = min(rank, m, n)
         u, v = _orthonormal(fixed, m, rank), _orthonormal(fixed, n, rank)
         g = z.astype(np.float64) + ratio * big * (u @ v.T)
     elif kind == "power":
