@@ -197,3 +197,48 @@ def test_binding_refuses_cpu_tensors():
     W = torch.zeros(4, 4)
     with pytest.raises(ValueError, match="CUDA"):
         D.describe([W], [W.clone()], [W.clone()])
+
+
+def _randomise(cfg, rng):
+    """Random, mostly invalid, config fields."""
+    cfg.alpha = float(rng.choice([0.0, -0.5, 1e-9, 0.0625, 0.25, 1.0, 1.5, float("nan")]))
+    cfg.mu = float(rng.choice([0.0, 0.95, 1.0, -1.0, 2.0]))
+    cfg.ns_steps = int(rng.choice([0, 1, 5, 16, 17, -3]))
+    cfg.axis = int(rng.integers(-1, 4))
+    cfg.precision = int(rng.integers(-1, 3))
+    cfg.select = int(rng.integers(-1, 3))
+    cfg.decay_mode = int(rng.integers(-1, 3))
+    cfg.scale_mode = int(rng.integers(-1, 3))
+    cfg.grad_dtype = int(rng.integers(-1, 3))
+    cfg.w_dtype = int(rng.integers(-1, 3))
+    cfg.ns_form = int(rng.integers(-1, 4))
+
+
+def test_host_validation_fuzz(lib):
+    """Random configs and shapes through the host-only size query (dion2_workspace_size): every
+    call returns a documented status code (0-4) and never crashes; a successful query is
+    positive.  Even iterations randomise the config on valid shapes, odd ones randomise the
+    shapes (zero, negative, over-long, short or huge row strides) under a valid config."""
+    import numpy as np
+    rng = np.random.default_rng(7)
+    codes = set()
+    for it in range(2000):
+        cfg = D.make_config()
+        if it % 2:
+            cfg.alpha = float(rng.choice([0.0625, 0.25, 1.0]))
+            shapes = [(int(rng.choice([0, 1, 7, 64, 300, 40000, -5])), int(rng.choice([0, 1, 9, 128, 2048, -1])))
+                      for _ in range(int(rng.integers(1, 4)))]
+        else:
+            _randomise(cfg, rng)
+            shapes = [(int(rng.choice([64, 300, 2048])), int(rng.choice([128, 512]))) for _ in range(2)]
+        arr = (D.Dion2Matrix * len(shapes))()
+        for i, (m, n) in enumerate(shapes):
+            arr[i].rows, arr[i].cols = m, n
+            arr[i].ld = int(rng.choice([n, n + 3, max(n - 1, 0), 1 << 40])) if it % 4 == 1 else n
+        out = ctypes.c_size_t(0)
+        rc = lib.dion2_workspace_size(arr, len(shapes), ctypes.byref(cfg), ctypes.byref(out))
+        assert rc in (0, 1, 2, 3, 4), rc
+        if rc == 0:
+            assert out.value > 0
+        codes.add(rc)
+    assert {0, 1, 2} <= codes
