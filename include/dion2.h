@@ -21,9 +21,11 @@
  *    fan-out, cols = fan-in (y = W x).
  *  - The caller owns every buffer (W, M, G, workspace, optional outputs); size
  *    the workspace with dion2_workspace_size() and pass it to every step.  The
- *    library's only device allocation is a small plan-owned table (matrix
+ *    library's device allocations are a small plan-owned table (matrix
  *    descriptors and work lists, a few hundred bytes per matrix), made once per (shapes,
- *    config, workspace) plan on its first step and reused by every later step.
+ *    config, workspace) plan on its first step, reused by every later step and freed by
+ *    dion2_release_workspace(); and, for the distributed entry points with
+ *    DION2_FLAG_DIST_DIRECT, the plan's two NCCL symmetric-memory windows.
  *  - All work is enqueued asynchronously on `stream` (a cudaStream_t passed
  *    as void*; NULL = legacy default stream).  No host synchronisation
  *    happens inside a step.  Calls that touch the same matrices must not
@@ -108,8 +110,11 @@ typedef enum { DION2_DT_F32 = 0, DION2_DT_BF16 = 1 } dion2_dtype;
            Q_{t+1} = C_t Q_t, A_{t+1} = C_t (C_t A_t) (fp16, fp32 accumulation), and
            X_out = Q X_in once.  Fewer FLOPs when q >= 2p (1.85x at p = 512, q in {2048, 8192}).
    AUTO:   GRAM for a shape group whose padded X has q_pad >= 2 p_pad or whose every member has
-           q >= 2p, DIRECT otherwise.  Both forms meet the 2e-2 parity gate on Gaussian and on
-           ill-conditioned (spiked / power-law) momenta (tests/test_gpu_conditioning.py). */
+           q >= 2p, provided every member has p >= 64 rows (reading R25: the fp16 Gram matrix of
+           a short X rounds away too much of its small eigenvalues); DIRECT otherwise.  AUTO meets
+           the 2e-2 parity gate on Gaussian and on ill-conditioned (spiked / power-law) momenta
+           (tests/test_gpu_conditioning.py, tests/test_gpu_fuzz.py); GRAM forced on X with
+           fewer than 64 rows can miss it (emulated up to 3.5% at p = 16). */
 typedef enum { DION2_NS_FORM_AUTO = 0, DION2_NS_FORM_DIRECT = 1, DION2_NS_FORM_GRAM = 2 } dion2_ns_form;
 
 /* One weight matrix and its optimizer state. */
