@@ -10,6 +10,7 @@
 #include <cstdlib>
 #include <cstring>
 #include <map>
+#include <tuple>
 #include <memory>
 #include <mutex>
 #include <string>
@@ -195,7 +196,7 @@ int build_layout(Plan& P, const dion2_matrix* mats, int n, const dion2_config* c
   P.ns_steps = c->ns_steps;
   P.mp.resize(n);
   const size_t xel = P.bf16_ns ? 2 : 4;
-  std::map<std::pair<int, int>, int> gidx;
+  std::map<std::tuple<int, int, int>, int> gidx;
   for (int i = 0; i < n; ++i) {
     const dion2_matrix& m = mats[i];
     MatPlan& q = P.mp[i];
@@ -239,12 +240,15 @@ int build_layout(Plan& P, const dion2_matrix* mats, int n, const dion2_config* c
     q.ga = generic ? (int)ceil_div(q.sa_pad, kTileA) : 0;
     q.gb = generic ? (int)ceil_div(q.sb_pad, kTileB) : 0;
     q.n_sumsq = (q.path == 1 || q.mt) ? q.p_pad : (q.path == 0 ? q.ga * q.gb : q.q_pad / 32);
-    auto key = std::make_pair(q.p_pad, q.q_pad);
+    // reading R25 / k_ns_small.cu: a short X (p <= kTinyP rows) under AUTO is evaluated in fp64
+    q.tiny = (!P.no_tiny && P.bf16_ns && c->ns_form == DION2_NS_FORM_AUTO && q.p <= kTinyP) ? 1 : 0;
+    auto key = std::make_tuple(q.p_pad, q.q_pad, q.tiny);
     auto it = gidx.find(key);
     if (it == gidx.end()) {
       Group g{};
       g.p_pad = q.p_pad;
       g.q_pad = q.q_pad;
+      g.tiny = q.tiny;
       g.count = 0;
       gidx[key] = (int)P.groups.size();
       P.groups.push_back(g);
@@ -281,6 +285,7 @@ int build_layout(Plan& P, const dion2_matrix* mats, int n, const dion2_config* c
   for (auto& g : P.groups) g.off_gmats = take(4 * (size_t)g.count);
   P.off_cf_mats = take(4 * (size_t)n);
   P.off_cf_prefix = take(8 * (size_t)n);
+  P.off_tiny_list = take(4 * (size_t)n);
   P.off_nsscale = take(16 * (size_t)n);
   for (int i = 0; i < n; ++i) {
     MatPlan& q = P.mp[i];
@@ -309,7 +314,7 @@ int build_layout(Plan& P, const dion2_matrix* mats, int n, const dion2_config* c
       // eigenvalue per entry -- AUTO keeps the direct form there
       all_tall_enough = all_tall_enough && P.mp[i].p >= kGramMinP;
     }
-    g.gs = P.bf16_ns && (c->ns_form == DION2_NS_FORM_GRAM ||
+    g.gs = P.bf16_ns && !g.tiny && (c->ns_form == DION2_NS_FORM_GRAM ||
                          (c->ns_form == DION2_NS_FORM_AUTO && all_tall_enough &&
                           (g.q_pad >= 2 * g.p_pad || all_wide)));
     g.off_C = g.off_Q0 = g.off_Q1 = 0;
@@ -584,7 +589,7 @@ int build_device_plan(Plan& P, const dion2_matrix* mats, const dion2_config* c, 
     d.X0 = at(ws, g.off_X0 + (size_t)q.zi * g.p_pad * g.q_pad * xel);
     d.X1 = at(ws, g.off_X1 + (size_t)q.zi * g.p_pad * g.q_pad * xel);
     // X_T lands in X1 after an odd number of applies (direct: T; Gram space: one per segment)
-    d.final_in_x1 = g.gs ? (int)(ns_segments(c, P.ns_steps).size() & 1) : (P.ns_steps & 1);
+    d.final_in_x1 = g.tiny ? 1 : (g.gs ? (int)(ns_segments(c, P.ns_steps).size() & 1) : (P.ns_steps & 1));
     d.gather_tile_base = gt_acc;
     d.gather_tiles_a = q.ga;
     d.gather_tiles_b = q.gb;
@@ -682,6 +687,13 @@ int build_device_plan(Plan& P, const dion2_matrix* mats, const dion2_config* c, 
     memcpy(H(P.off_cf_prefix), cf_prefix.data(), 8 * cf_prefix.size());
   }
   for (auto& g : P.groups) memcpy(H(g.off_gmats), g.mats.data(), 4 * g.mats.size());
+  {
+    std::vector<int32_t> tiny;
+    for (int i = 0; i < n; ++i)
+      if (P.mp[i].tiny) tiny.push_back(i);
+    P.n_tiny = (int)tiny.size();
+    if (P.n_tiny) memcpy(H(P.off_tiny_list), tiny.data(), 4 * tiny.size());
+  }
 
   // ---- Newton-Schulz launch list: per iteration t: gram, poly, apply; per phase the
   // groups are batched (<= kMaxGroups per launch, one BN class per launch).
@@ -714,7 +726,7 @@ int build_device_plan(Plan& P, const dion2_matrix* mats, const dion2_config* c, 
       std::vector<int> by_bn[2];
       for (int gi = 0; gi < (int)P.groups.size(); ++gi) {
         const Group& g = P.groups[gi];
-        if (g.gs) continue;  // Gram-space groups: append_gram_space_launches
+        if (g.gs || g.tiny) continue;  // Gram-space groups: append_gram_space_launches; tiny: k_ns_small
         int bn256 = ph == PH_APPLY ? 1 : (g.p_pad % 256 == 0);
         by_bn[bn256].push_back(gi);
       }
@@ -989,11 +1001,22 @@ void stage_k1_select(Plan& P, const dion2_config* c, void* ws, int32_t* status, 
   }
 }
 
-// K3 gather + selective decay (Alg. 1 l.4-5)
+// K3 gather + selective decay (Alg. 1 l.4-5); first the fp64 NS of short X (k_ns_small.cu), which
+// reads the pre-decay M[K]
 void stage_gather(Plan& P, const dion2_config* c, void* ws, Launcher& L, cudaStream_t s, bool persistent) {
   const int n = P.n;
   const MatDesc* dmats = (const MatDesc*)tab(P, P.off_desc);
   int32_t* bad = (int32_t*)at(ws, P.off_bad);
+  if (P.n_tiny) {
+    NsSmallCoeffs cs{};
+    for (int t = 0; t < c->ns_steps && t < 16; ++t)
+      for (int e = 0; e < 3; ++e) cs.c[t][e] = c->ns_coeffs[t][e];
+    cs.T = c->ns_steps;
+    cs.eps = c->ns_eps;
+    L.begin(PH_NSMUL);
+    launch_ns_small(s, dmats, (const int32_t*)tab(P, P.off_tiny_list), P.n_tiny, bad, cs);
+    L.end();
+  }
   if (P.total_gather_tiles > 0 && P.generic_gather_mats > 0) {
     L.begin(PH_GATHER);
     launch_gather_decay(P.bf16_ns, stream_grid(P.total_gather_tiles, 8, persistent), s, dmats,

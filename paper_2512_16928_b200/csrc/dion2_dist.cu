@@ -288,6 +288,7 @@ int resolve(DistPlan& D, const dion2_shard* sh, int n, const dion2_config* c, in
       om[i].ld = D.dm[ch.owned[i]].n;
     }
     ch.plan = std::make_unique<Plan>();
+    ch.plan->no_tiny = true;  // the owner's X arrives as fp16 pieces: the tensor-core NS handles every group
     int rc = build_layout(*ch.plan, om.data(), (int)om.size(), c);
     if (rc) return rc;
     owner_bytes = align_up(owner_bytes + ch.plan->total, 4096);

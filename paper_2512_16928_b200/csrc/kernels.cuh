@@ -187,6 +187,17 @@ constexpr int ns_tc_smem_bytes() {
          4 * 2 * 2048 /*epilogue staging: 4 warps x 2 buffers x (32 x 32 bf16)*/;
 }
 
+// Short X (p <= kTinyP rows) under ns_form AUTO (k_ns_small.cu): NS in fp64 Gram space straight
+// from the pre-decay momentum, X_T stored as fp16 into X1; one CTA per matrix of `list`.
+constexpr int kTinyP = 32;
+struct NsSmallCoeffs {
+  float c[16][3];
+  int T;
+  float eps;
+};
+void launch_ns_small(cudaStream_t s, const MatDesc* mats, const int32_t* list, int n_list, const int32_t* bad,
+                     const NsSmallCoeffs& C);
+
 // fp32 SIMT validation path (k_ns_simt.cu): grid (n_tiles, m_tiles, count) per group.
 __global__ void k_ns_gemm_simt_f32(const NsParams P, int group);
 

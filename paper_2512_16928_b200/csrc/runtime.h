@@ -62,6 +62,7 @@ struct MatPlan {
   int mt;  // M stored transposed (cols mode): gather = rows path on M^T, scatter = path (cols / generic)
   int axis, d, o, k, sr, sc, transposed, p, q, p_pad, q_pad, group, zi, rowblocks, ga, gb, sa_pad, sb_pad, path,
       n_sumsq, spath;  // spath: scatter path (the cols streaming scatter takes k up to kMaxColKScatter)
+  int tiny = 0;        // short X under AUTO: NS by k_ns_small (fp64 Gram space), not the tensor cores
   float fan_sqrt;
   size_t off_scores, off_partials, off_sel, off_sumsq;
 };
@@ -71,6 +72,7 @@ struct Group {
   std::vector<int> mats;  // global matrix indices
   size_t off_X0, off_X1, off_A, off_B, off_gmats;
   int gs;                           // Newton-Schulz in Gram space (reading R23)
+  int tiny = 0;                     // members take k_ns_small (no tensor-core NS launches)
   size_t off_C, off_Q0, off_Q1;     // Gram-space p x p buffers (gs only)
 };
 
@@ -118,6 +120,10 @@ struct Plan {
   // split-K of the long-K gram launches when their tiles cannot fill the GPU (bf16 pair path)
   int gram_splitk = 1;
   size_t off_splitk = 0;
+  bool no_tiny = false;  // set before build_layout: short X stays on the tensor cores (owner plans of
+                         // the distributed step, whose X arrives as fp16 pieces)
+  size_t off_tiny_list = 0;
+  int n_tiny = 0;
   std::vector<uint8_t> host_tables;  // [off_desc, off_ns_begin) image (descriptors + aux)
   std::vector<Launch> ns_launches;
   void* ws = nullptr;

@@ -123,12 +123,16 @@ def gram_f16(X, coeffs=O.DEFAULT_NS_COEFFS, eps=O.DEFAULT_NS_EPS, growth=RESTART
 
 
 GRAM_MIN_P = 64  # reading R25 (csrc/runtime.h kGramMinP)
+TINY_P = 32      # reading R25 (csrc/kernels.cuh kTinyP): fp64 Gram-space NS, fp16 store of X_T
 
 
 def auto_f16(X, coeffs=O.DEFAULT_NS_COEFFS, eps=O.DEFAULT_NS_EPS):
-    """ns_form AUTO for one matrix: the Gram form for wide X (q >= 2p) with p >= 64 rows, else
-    the direct form (readings R23, R25)."""
+    """ns_form AUTO for one matrix (readings R23, R25): an X of at most 32 rows is evaluated in
+    fp64 and stored once as fp16 (k_ns_small); else the Gram form for wide X (q >= 2p) with
+    p >= 64 rows, else the direct form."""
     p, q = X.shape
+    if p <= TINY_P:
+        return f16(O.newton_schulz(np.asarray(X, np.float64), coeffs, eps))
     if q >= 2 * p and p >= GRAM_MIN_P:
         return gram_f16(X, coeffs, eps)
     return direct_f16(X, coeffs, eps)

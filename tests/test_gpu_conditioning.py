@@ -106,3 +106,24 @@ def test_p1024_on_spiked_momenta():
     """The 8B set's p = 1024 shapes (Wq / Wo 4096 x 4096 at alpha = 1/4: Gram form with the
     restart, the 1-SM apply since p_pad > 512) on a rank-4 spike."""
     _check(run_parity([(4096, 4096)], 0.25, "auto", "bf16", steps=2, structure=dict(kind="spike", rank=4, ratio=100)))
+
+
+@pytest.mark.parametrize("shape,alpha,rank", [((7, 1618), 0.25, 1), ((824, 30), 1.0, 16), ((128, 1678), 0.25, 1),
+                                              ((253, 1280), 0.0625, 4), ((1, 1), 1.0, 1), ((40, 4000), 0.5, 16)])
+def test_short_x_on_extreme_spikes(shape, alpha, rank):
+    """X with at most 32 rows under AUTO runs the fp64 Gram-space NS straight from the momentum
+    (k_ns_small.cu): on spikes at sigma_1 / median ~ 250, where the 16-bit path reached 2.0-3.6%,
+    the update is within the final fp16 store's rounding (a few 1e-4) of the oracle's."""
+    res = run_parity([shape], alpha, "auto", "bf16", steps=2, structure=dict(kind="spike", rank=rank, ratio=250))
+    assert res.index_mismatch == 0 and res.unselected_w_bitwise and res.unselected_m_bitwise, res
+    assert max(res.dW_rel) <= 2e-3, res
+    assert max(res.M_rel) <= 1e-5, res
+
+
+def test_short_x_mixed_with_tensor_core_groups():
+    """Short X next to tensor-core groups (Gram and direct) in one batched call, both layouts of M."""
+    shapes = [(7, 1618), (2357, 2386), (128, 1678), (1920, 615), (30, 900), (1, 1)]
+    for mt in (False, True):
+        res = run_parity(shapes, 0.25, "auto", "bf16", steps=2, m_transposed=mt,
+                         structure=dict(kind="spike", rank=1, ratio=100))
+        _check(res)
