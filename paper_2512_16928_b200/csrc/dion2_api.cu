@@ -240,7 +240,7 @@ int build_layout(Plan& P, const dion2_matrix* mats, int n, const dion2_config* c
     q.ga = generic ? (int)ceil_div(q.sa_pad, kTileA) : 0;
     q.gb = generic ? (int)ceil_div(q.sb_pad, kTileB) : 0;
     q.n_sumsq = (q.path == 1 || q.mt) ? q.p_pad : (q.path == 0 ? q.ga * q.gb : q.q_pad / 32);
-    // reading R25 / k_ns_small.cu: a short X (p <= kTinyP rows) under AUTO is evaluated in fp64
+    // reading R25 / k_ns_small.cu: a short X (p <= kTinyP = 64 rows) under AUTO is evaluated in fp64
     q.tiny = (!P.no_tiny && P.bf16_ns && c->ns_form == DION2_NS_FORM_AUTO && q.p <= kTinyP) ? 1 : 0;
     auto key = std::make_tuple(q.p_pad, q.q_pad, q.tiny);
     auto it = gidx.find(key);

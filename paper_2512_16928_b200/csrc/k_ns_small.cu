@@ -1,10 +1,10 @@
-// Newton-Schulz of short X (p <= kTinyP rows) in fp64 Gram space, straight from the momentum.
+// Newton-Schulz of short X (p <= kTinyP = 64 rows) in fp64 Gram space, straight from the momentum.
 //
 // The 16-bit tensor-core path rounds X once per entry (fp16, 2^-11 relative).  On an X of a few
 // rows whose spectrum is dominated by one or a few directions (a selected submatrix of a spiked
 // momentum), that rounding is a large fraction of the weak directions, and a short X has few
 // directions to average it over: emulated and measured up to 2-3.6% on the cumulative update at
-// p <= 30 for sigma_1 / median ~ 250 (reading R25).  Such matrices are cheap, so
+// p <= 30 and 1.7-1.9% at p = 33..63 for sigma_1 / median ~ 250 (reading R25).  Such matrices are cheap, so
 // AUTO evaluates them exactly instead: one CTA per matrix reads X = wide(M[K]) (pre-decay, fp32;
 // launched after K2 and before K3's decay), accumulates A = X X^T in fp64, runs the whole
 // polynomial recursion of Alg. 1 l.4 (readings R1-R5, R23's Gram-space algebra)
@@ -41,10 +41,16 @@ __device__ __forceinline__ void mm(double* C, const double* A, const double* B, 
 
 }  // namespace
 
+constexpr size_t kSmem = 4 * sizeof(double) * kP * kLd + sizeof(float) * kP * (kChunk + 1);
+
 __global__ void __launch_bounds__(kThreads) k_ns_small(const MatDesc* __restrict__ mats, const int32_t* __restrict__ list,
                                                        int n_list, const int32_t* __restrict__ bad, NsSmallCoeffs C) {
-  __shared__ double A[kP * kLd], B[kP * kLd], Cm[kP * kLd], Q[kP * kLd];
-  __shared__ float xs[kP][kChunk + 1];
+  extern __shared__ __align__(16) uint8_t smem_raw[];
+  double* A = reinterpret_cast<double*>(smem_raw);
+  double* B = A + kP * kLd;
+  double* Cm = B + kP * kLd;
+  double* Q = Cm + kP * kLd;
+  float (*xs)[kChunk + 1] = reinterpret_cast<float (*)[kChunk + 1]>(Q + kP * kLd);
   __shared__ double red;
   const int mi = list[blockIdx.x];
   const MatDesc& md = mats[mi];
@@ -69,9 +75,11 @@ __global__ void __launch_bounds__(kThreads) k_ns_small(const MatDesc* __restrict
         int i = 0, r = pr;
         while (r >= p - i) { r -= p - i; ++i; }
         const int k = i + r;
-        double a = 0.0;
-        for (int jj = 0; jj < w; ++jj) a += (double)xs[i][jj] * (double)xs[k][jj];
-        acc[s] += a;
+        // fp32 products within a 64-column chunk, fp64 across chunks: ~2^-24 relative, far below
+        // the final fp16 store
+        float a = 0.f;
+        for (int jj = 0; jj < w; ++jj) a = fmaf(xs[i][jj], xs[k][jj], a);
+        acc[s] += (double)a;
       }
     }
     __syncthreads();
@@ -144,7 +152,10 @@ __global__ void __launch_bounds__(kThreads) k_ns_small(const MatDesc* __restrict
 
 void launch_ns_small(cudaStream_t s, const MatDesc* mats, const int32_t* list, int n_list, const int32_t* bad,
                      const NsSmallCoeffs& C) {
-  if (n_list > 0) k_ns_small<<<n_list, kThreads, 0, s>>>(mats, list, n_list, bad, C);
+  static const bool attr = cudaFuncSetAttribute(k_ns_small, cudaFuncAttributeMaxDynamicSharedMemorySize,
+                                                (int)kSmem) == cudaSuccess;
+  (void)attr;
+  if (n_list > 0) k_ns_small<<<n_list, kThreads, kSmem, s>>>(mats, list, n_list, bad, C);
 }
 
 }  // namespace dion2

@@ -189,7 +189,7 @@ constexpr int ns_tc_smem_bytes() {
 
 // Short X (p <= kTinyP rows) under ns_form AUTO (k_ns_small.cu): NS in fp64 Gram space straight
 // from the pre-decay momentum, X_T stored as fp16 into X1; one CTA per matrix of `list`.
-constexpr int kTinyP = 32;
+constexpr int kTinyP = 64;
 struct NsSmallCoeffs {
   float c[16][3];
   int T;

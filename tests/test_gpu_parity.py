@@ -473,18 +473,20 @@ def test_bf16_gradient_input():
 
 
 def test_phase_timing_and_launch_count():
-    Ws = [torch.from_numpy(gen_w0(256, 512)).cuda()]
-    Ms = [torch.zeros_like(Ws[0])]
-    set_phase_timing(True)
-    try:
-        Dion2(alpha=0.25).step(Ws, Ms, [torch.ones_like(Ws[0])])
-        times = get_phase_times()
-    finally:
-        set_phase_timing(False)
-    pre = ("momentum_score", "select", "gather_rows")
-    assert last_launch_count() >= 5 + len(pre)
-    for ph in pre + ("ns_gram", "ns_poly", "ns_apply", "scatter_rows"):
-        assert times[ph][1] >= 1 and times[ph][0] > 0
+    # X of 128 rows: the tensor-core Gram-space form; a 32-row X: the fp64 short-X NS (ns_mul phase)
+    for (m, n), ns_phases in (((512, 1024), ("ns_gram", "ns_poly", "ns_apply")), ((128, 512), ("ns_mul",))):
+        Ws = [torch.from_numpy(gen_w0(m, n)).cuda()]
+        Ms = [torch.zeros_like(Ws[0])]
+        set_phase_timing(True)
+        try:
+            Dion2(alpha=0.25).step(Ws, Ms, [torch.ones_like(Ws[0])])
+            times = get_phase_times()
+        finally:
+            set_phase_timing(False)
+        pre = ("momentum_score", "select", "gather_rows")
+        assert last_launch_count() >= len(ns_phases) + 2 + len(pre)
+        for ph in pre + ns_phases + ("scatter_rows",):
+            assert times[ph][1] >= 1 and times[ph][0] > 0, (m, n, ph, times)
 
 
 def test_stream_calls_do_not_disturb_captured_graphs():
