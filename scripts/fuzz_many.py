@@ -68,10 +68,15 @@ def main():
                 alpha = float(rng.choice([0.125, 0.25, 0.5]))
                 direct = bool(rng.random() < 0.5)
                 mt = bool(rng.random() < 0.5)
-                res = run_parity_dist(shapes, alpha, world, steps=2, direct=direct, m_transposed=mt)
+                structure = None
+                if rng.random() < 0.3:
+                    structure = dict(kind="spike", rank=int(rng.choice([1, 4, 16])),
+                                     ratio=float(rng.choice([20, 100, 250])))
+                res = run_parity_dist(shapes, alpha, world, steps=2, direct=direct, m_transposed=mt,
+                                      structure=structure)
                 ok = res.index_mismatch == 0 and max(res.dW_rel) <= 2e-2 and max(res.M_rel) <= 1e-5
                 rec = dict(i=i, kind="dist", world=world, shapes=shapes, alpha=alpha, direct=direct, mt=mt,
-                           dW=max(res.dW_rel), idx=res.index_mismatch, ok=ok)
+                           structure=str(structure), dW=max(res.dW_rel), idx=res.index_mismatch, ok=ok)
         except Exception as e:  # noqa: BLE001
             msg = repr(e)
             # unsupported configurations are reported by the library, not failures of the step
