@@ -148,24 +148,27 @@ def run_parity(shapes: Sequence[Tuple[int, int]], alpha: float, axis: str = "aut
                     else:
                         res.unselected_w_bitwise &= bool(np.array_equal(wb[:, unsel], wa[:, unsel]))
                         res.unselected_m_bitwise &= bool(np.array_equal(expect_m[:, unsel], ma[:, unsel]))
-    _finish(res, shapes, [Wv(i) for i in range(len(shapes))], [Mv(i) for i in range(len(shapes))], Wr, Mr, W0)
+    _finish(res, shapes, [Wv(i) for i in range(len(shapes))], [Mv(i) for i in range(len(shapes))], Wr, Mr, W0,
+            lr, ks)
     return res
 
 
-def _dw_floor(dref, w0):
+def _dw_floor(dref, w0, lr=0.02, k=1):
     """Denominator of the cumulative-update error: ||dW_ref||, floored at 1e-6 ||W_0|| (~16 fp32
-    ulps of W): the updates of steps with opposite signs can cancel (e.g. a 1 x 1 matrix whose
-    Newton-Schulz output is +-0.697 each step), and below that floor the fp32 storage of W, not
-    the step, decides the difference."""
-    return max(float(np.linalg.norm(dref)), 1e-6 * float(np.linalg.norm(np.asarray(w0, np.float64))), 1e-300)
+    ulps of W) and at 1e-3 lr sqrt(k) (a thousandth of one step's nominal update: O has ~unit
+    singular values): the updates of steps with opposite signs can cancel (e.g. a 1 x 1 matrix
+    whose Newton-Schulz output is +-0.697 each step), and below those floors the fp32 storage of W
+    and the fp16 store of O, not the step, decide the difference."""
+    return max(float(np.linalg.norm(dref)), 1e-6 * float(np.linalg.norm(np.asarray(w0, np.float64))),
+               1e-3 * abs(lr) * float(np.sqrt(max(k, 1))), 1e-300)
 
 
-def _finish(res, shapes, Wg, Mg, Wr, Mr, W0):
+def _finish(res, shapes, Wg, Mg, Wr, Mr, W0, lr=0.02, ks=None):
     for i in range(len(shapes)):
         wg = Wg[i].cpu().numpy().astype(np.float64)
         dref = Wr[i] - W0[i].astype(np.float64)
         dgpu = wg - W0[i].astype(np.float64)
-        res.dW_rel.append(float(np.linalg.norm(dgpu - dref) / _dw_floor(dref, W0[i])))
+        res.dW_rel.append(float(np.linalg.norm(dgpu - dref) / _dw_floor(dref, W0[i], lr, ks[i] if ks else 1)))
         res.W_rel.append(float(np.linalg.norm(wg - Wr[i]) / np.linalg.norm(Wr[i])))
         mg = Mg[i].cpu().numpy().astype(np.float64)
         res.M_rel.append(float(np.abs(mg - Mr[i]).max() / max(np.abs(Mr[i]).max(), 1e-300)))
@@ -253,7 +256,7 @@ def run_parity_dist(shapes, alpha, world, steps=3, seed=0, mode="loopback", axis
                     res.index_mismatch += 1
     Wfull = [assemble(Wg, i) for i in range(len(shapes))]
     Mfull = [assemble(Mv, i) for i in range(len(shapes))]
-    _finish(res, shapes, Wfull, Mfull, Wr, Mr, W0)
+    _finish(res, shapes, Wfull, Mfull, Wr, Mr, W0, lr, ks)
     res.comm_bytes = opt.last_comm_bytes
     res.exchange = opt.exchange_mode() if mode != "loopback" else ("direct" if direct else "copies")
     return res
@@ -298,7 +301,7 @@ def run_parity_fsdp(shapes, alpha, steps=3, seed=0, mu=0.95, lr=0.02, m_transpos
     for i in range(len(shapes)):
         wg = Wfull[i].cpu().numpy().astype(np.float64)
         dref = Wr[i] - W0[i].astype(np.float64)
-        res.dW_rel.append(float(np.linalg.norm(wg - W0[i] - dref) / _dw_floor(dref, W0[i])))
+        res.dW_rel.append(float(np.linalg.norm(wg - W0[i] - dref) / _dw_floor(dref, W0[i], lr)))
         res.W_rel.append(float(np.linalg.norm(wg - Wr[i]) / np.linalg.norm(Wr[i])))
     res.comm_bytes = opt.comm_bytes()
     res.exchange = [e.exchange_mode() for e in opt._engines]
