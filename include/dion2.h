@@ -109,8 +109,9 @@ typedef enum { DION2_DT_F32 = 0, DION2_DT_BF16 = 1 } dion2_dtype;
            per segment A = X_in X_in^T once, then C_t = a I + b A_t + c A_t^2,
            Q_{t+1} = C_t Q_t, A_{t+1} = C_t (C_t A_t) (fp16, fp32 accumulation), and
            X_out = Q X_in once.  Fewer FLOPs when q >= 2p (1.85x at p = 512, q in {2048, 8192}).
-   AUTO:   an X of at most 64 rows is evaluated exactly (fp64 Gram space straight from the
-           pre-decay momentum, X_T stored once as fp16; reading R25); otherwise GRAM for a shape
+   AUTO:   an X of at most 128 rows is evaluated in high precision (Gram space straight from the
+           pre-decay momentum, fp64 / fp32 recursion, X_T stored once as fp16; reading R25);
+           otherwise GRAM for a shape
            group whose padded X has q_pad >= 2 p_pad or whose every member has q >= 2p, provided
            every member has p >= 64 rows (R25: the fp16 Gram matrix of a short X rounds away too
            much of its small eigenvalues); DIRECT otherwise.  AUTO meets the 2e-2 parity gate on

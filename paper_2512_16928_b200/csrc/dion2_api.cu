@@ -240,7 +240,7 @@ int build_layout(Plan& P, const dion2_matrix* mats, int n, const dion2_config* c
     q.ga = generic ? (int)ceil_div(q.sa_pad, kTileA) : 0;
     q.gb = generic ? (int)ceil_div(q.sb_pad, kTileB) : 0;
     q.n_sumsq = (q.path == 1 || q.mt) ? q.p_pad : (q.path == 0 ? q.ga * q.gb : q.q_pad / 32);
-    // reading R25 / k_ns_small.cu: a short X (p <= kTinyP = 64 rows) under AUTO is evaluated in fp64
+    // reading R25 / k_ns_small.cu: a short X (p <= kTinyP = 128 rows) under AUTO is evaluated in high precision
     q.tiny = (!P.no_tiny && P.bf16_ns && c->ns_form == DION2_NS_FORM_AUTO && q.p <= kTinyP) ? 1 : 0;
     auto key = std::make_tuple(q.p_pad, q.q_pad, q.tiny);
     auto it = gidx.find(key);
@@ -690,7 +690,10 @@ int build_device_plan(Plan& P, const dion2_matrix* mats, const dion2_config* c, 
   {
     std::vector<int32_t> tiny;
     for (int i = 0; i < n; ++i)
-      if (P.mp[i].tiny) tiny.push_back(i);
+      if (P.mp[i].tiny && P.mp[i].p <= 64) tiny.push_back(i);
+    P.n_tiny64 = (int)tiny.size();
+    for (int i = 0; i < n; ++i)
+      if (P.mp[i].tiny && P.mp[i].p > 64) tiny.push_back(i);
     P.n_tiny = (int)tiny.size();
     if (P.n_tiny) memcpy(H(P.off_tiny_list), tiny.data(), 4 * tiny.size());
   }
@@ -1014,7 +1017,9 @@ void stage_gather(Plan& P, const dion2_config* c, void* ws, Launcher& L, cudaStr
     cs.T = c->ns_steps;
     cs.eps = c->ns_eps;
     L.begin(PH_NSMUL);
-    launch_ns_small(s, dmats, (const int32_t*)tab(P, P.off_tiny_list), P.n_tiny, bad, cs);
+    const int32_t* tl = (const int32_t*)tab(P, P.off_tiny_list);
+    launch_ns_small(s, dmats, tl, P.n_tiny64, bad, cs, false);
+    launch_ns_small(s, dmats, tl + P.n_tiny64, P.n_tiny - P.n_tiny64, bad, cs, true);
     L.end();
   }
   if (P.total_gather_tiles > 0 && P.generic_gather_mats > 0) {

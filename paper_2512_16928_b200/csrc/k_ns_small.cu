@@ -1,24 +1,24 @@
-// Newton-Schulz of short X (p <= kTinyP = 64 rows) in fp64 Gram space, straight from the momentum.
+// Newton-Schulz of short X (p <= kTinyP = 128 rows) in Gram space, straight from the momentum.
 //
-// The 16-bit tensor-core path rounds X once per entry (fp16, 2^-11 relative).  On an X of a few
+// The 16-bit tensor-core path rounds X once per entry (fp16, 2^-11 relative).  On an X of few
 // rows whose spectrum is dominated by one or a few directions (a selected submatrix of a spiked
 // momentum), that rounding is a large fraction of the weak directions, and a short X has few
 // directions to average it over: emulated and measured up to 2-3.6% on the cumulative update at
-// p <= 30 and 1.7-1.9% at p = 33..63 for sigma_1 / median ~ 250 (reading R25).  Such matrices are cheap, so
-// AUTO evaluates them exactly instead: one CTA per matrix reads X = wide(M[K]) (pre-decay, fp32;
-// launched after K2 and before K3's decay), accumulates A = X X^T in fp64, runs the whole
-// polynomial recursion of Alg. 1 l.4 (readings R1-R5, R23's Gram-space algebra)
-// on p x p fp64 matrices, and writes X_T = s Q X as fp16 into X1, where K7 reads it
-// (MatDesc::final_in_x1 = 1).  The only rounding left is that final fp16 store.
+// p <= 30, 1.7-1.9% at p = 33..63 and ~1.5% up to p = 128 for sigma_1 / median ~ 250
+// (reading R25).  Such matrices are cheap, so AUTO evaluates them in high
+// precision instead: one CTA per matrix reads X = wide(M[K]) (pre-decay, fp32; launched after
+// K2 and before K3's decay), accumulates A = X X^T (fp32 products per 32/64-column chunk, fp64
+// across chunks), runs the whole polynomial recursion of Alg. 1 l.4 (readings
+// R1-R5, R23's Gram-space algebra) on p x p matrices -- in fp64 for p <= 64, in fp32 for
+// p <= 128 (shared memory) -- and writes X_T = s Q X as fp16 into X1, where K7 reads it
+// (MatDesc::final_in_x1 = 1).  Products are staged through registers, so three p x p buffers
+// (A, C, Q) suffice.
 #include "kernels.cuh"
 
 namespace dion2 {
 
 namespace {
 
-constexpr int kP = kTinyP;      // max rows
-constexpr int kLd = kP + 1;     // padded smem row of the p x p matrices
-constexpr int kChunk = 64;      // X columns per pass chunk
 constexpr int kThreads = 256;
 
 // element (i, j) of the wide X = S (rows mode) or S^T (cols mode; M transposed or not)
@@ -29,28 +29,50 @@ __device__ __forceinline__ float x_at(const MatDesc& md, int i, int64_t j) {
   return md.M[j * md.ld + r];
 }
 
-// C = A B for p x p row-major smem matrices (ld kLd), all threads
-__device__ __forceinline__ void mm(double* C, const double* A, const double* B, int p) {
-  for (int e = threadIdx.x; e < p * p; e += blockDim.x) {
-    const int i = e / p, k = e % p;
-    double acc = 0.0;
-    for (int l = 0; l < p; ++l) acc += A[i * kLd + l] * B[l * kLd + k];
-    C[i * kLd + k] = acc;
+template <int P, typename R>
+struct Small {
+  static constexpr int kLd = P + 1;
+  static constexpr int kChunk = P <= 64 ? 64 : 32;
+  static constexpr int kOut = (P * P + kThreads - 1) / kThreads;  // outputs per thread of a p x p product
+  static constexpr size_t kSmem = 3 * sizeof(R) * P * kLd + sizeof(float) * P * (kChunk + 1);
+};
+
+// D = X Y (p x p, row-major smem, ld P + 1), staged through registers: D may alias X or Y
+template <int P, typename R>
+__device__ __forceinline__ void mm_inplace(R* D, const R* X, const R* Y, int p) {
+  constexpr int kLd = Small<P, R>::kLd;
+  R v[Small<P, R>::kOut];
+#pragma unroll
+  for (int s = 0; s < Small<P, R>::kOut; ++s) {
+    const int e = threadIdx.x + s * kThreads;
+    R acc = 0;
+    if (e < p * p) {
+      const int i = e / p, k = e % p;
+      for (int l = 0; l < p; ++l) acc += X[i * kLd + l] * Y[l * kLd + k];
+    }
+    v[s] = acc;
   }
+  __syncthreads();
+#pragma unroll
+  for (int s = 0; s < Small<P, R>::kOut; ++s) {
+    const int e = threadIdx.x + s * kThreads;
+    if (e < p * p) D[(e / p) * kLd + e % p] = v[s];
+  }
+  __syncthreads();
 }
 
 }  // namespace
 
-constexpr size_t kSmem = 4 * sizeof(double) * kP * kLd + sizeof(float) * kP * (kChunk + 1);
-
+template <int P, typename R>
 __global__ void __launch_bounds__(kThreads) k_ns_small(const MatDesc* __restrict__ mats, const int32_t* __restrict__ list,
                                                        int n_list, const int32_t* __restrict__ bad, NsSmallCoeffs C) {
+  using S = Small<P, R>;
+  constexpr int kLd = S::kLd, kChunk = S::kChunk;
   extern __shared__ __align__(16) uint8_t smem_raw[];
-  double* A = reinterpret_cast<double*>(smem_raw);
-  double* B = A + kP * kLd;
-  double* Cm = B + kP * kLd;
-  double* Q = Cm + kP * kLd;
-  float (*xs)[kChunk + 1] = reinterpret_cast<float (*)[kChunk + 1]>(Q + kP * kLd);
+  R* A = reinterpret_cast<R*>(smem_raw);
+  R* Cm = A + P * kLd;
+  R* Q = Cm + P * kLd;
+  float (*xs)[kChunk + 1] = reinterpret_cast<float (*)[kChunk + 1]>(Q + P * kLd);
   __shared__ double red;
   const int mi = list[blockIdx.x];
   const MatDesc& md = mats[mi];
@@ -58,8 +80,11 @@ __global__ void __launch_bounds__(kThreads) k_ns_small(const MatDesc* __restrict
   const int p = md.p;
   const int64_t q = md.q;
   // ---- A = X X^T (upper triangle accumulated per thread over all column chunks)
-  constexpr int kMaxPairs = kP * (kP + 1) / 2;
-  double acc[(kMaxPairs + kThreads - 1) / kThreads] = {};
+  constexpr int kMaxPairs = P * (P + 1) / 2;
+  constexpr int kPairsPer = (kMaxPairs + kThreads - 1) / kThreads;
+  double acc[kPairsPer];
+#pragma unroll
+  for (int s = 0; s < kPairsPer; ++s) acc[s] = 0.0;
   const int npairs = p * (p + 1) / 2;
   for (int64_t j0 = 0; j0 < q; j0 += kChunk) {
     const int w = (int)(q - j0 < kChunk ? q - j0 : kChunk);
@@ -69,14 +94,14 @@ __global__ void __launch_bounds__(kThreads) k_ns_small(const MatDesc* __restrict
     }
     __syncthreads();
 #pragma unroll
-    for (int s = 0; s < (kMaxPairs + kThreads - 1) / kThreads; ++s) {
+    for (int s = 0; s < kPairsPer; ++s) {
       const int pr = threadIdx.x + s * kThreads;
       if (pr < npairs) {
         int i = 0, r = pr;
         while (r >= p - i) { r -= p - i; ++i; }
         const int k = i + r;
-        // fp32 products within a 64-column chunk, fp64 across chunks: ~2^-24 relative, far below
-        // the final fp16 store
+        // fp32 products within a chunk, fp64 across chunks (~2^-24 relative, far below the
+        // final fp16 store)
         float a = 0.f;
         for (int jj = 0; jj < w; ++jj) a = fmaf(xs[i][jj], xs[k][jj], a);
         acc[s] += (double)a;
@@ -84,51 +109,47 @@ __global__ void __launch_bounds__(kThreads) k_ns_small(const MatDesc* __restrict
     }
     __syncthreads();
   }
+  // ---- s = 1 / (||X||_F + eps) (reading R3) from the fp64 trace; A <- s^2 A; Q <- I
+  if (threadIdx.x == 0) red = 0.0;
+  __syncthreads();
 #pragma unroll
-  for (int s = 0; s < (kMaxPairs + kThreads - 1) / kThreads; ++s) {
+  for (int s = 0; s < kPairsPer; ++s) {
+    const int pr = threadIdx.x + s * kThreads;
+    if (pr < npairs) {
+      int i = 0, r = pr;
+      while (r >= p - i) { r -= p - i; ++i; }
+      if (r == 0) atomicAdd(&red, acc[s]);  // a diagonal entry
+    }
+  }
+  __syncthreads();
+  const double sc = 1.0 / (sqrt(red) + (double)C.eps);
+#pragma unroll
+  for (int s = 0; s < kPairsPer; ++s) {
     const int pr = threadIdx.x + s * kThreads;
     if (pr < npairs) {
       int i = 0, r = pr;
       while (r >= p - i) { r -= p - i; ++i; }
       const int k = i + r;
-      A[i * kLd + k] = acc[s];
-      A[k * kLd + i] = acc[s];
+      const R v = (R)(acc[s] * sc * sc);
+      A[i * kLd + k] = v;
+      A[k * kLd + i] = v;
     }
   }
-  __syncthreads();
-  // ---- s = 1 / (||X||_F + eps) (reading R3), A <- s^2 A, Q <- I
-  if (threadIdx.x == 0) {
-    double tr = 0.0;
-    for (int i = 0; i < p; ++i) tr += A[i * kLd + i];
-    red = 1.0 / (sqrt(tr) + (double)C.eps);
-  }
-  __syncthreads();
-  const double sc = red;
-  for (int e = threadIdx.x; e < p * p; e += blockDim.x) {
-    const int i = e / p, k = e % p;
-    A[i * kLd + k] *= sc * sc;
-    Q[i * kLd + k] = i == k ? 1.0 : 0.0;
-  }
+  for (int e = threadIdx.x; e < p * p; e += blockDim.x) Q[(e / p) * kLd + e % p] = (e / p == e % p) ? R(1) : R(0);
   __syncthreads();
   // ---- per iteration: C = aI + bA + cA^2, Q <- C Q, A <- C (C A)   (X_{t+1} = C_t X_t)
   for (int t = 0; t < C.T; ++t) {
-    const double a = C.c[t][0], b = C.c[t][1], c = C.c[t][2];
-    mm(B, A, A, p);
-    __syncthreads();
+    const R a = C.c[t][0], b = C.c[t][1], c = C.c[t][2];
+    mm_inplace<P, R>(Cm, A, A, p);  // Cm = A^2
     for (int e = threadIdx.x; e < p * p; e += blockDim.x) {
       const int i = e / p, k = e % p;
-      Cm[i * kLd + k] = (i == k ? a : 0.0) + b * A[i * kLd + k] + c * B[i * kLd + k];
+      Cm[i * kLd + k] = (i == k ? a : R(0)) + b * A[i * kLd + k] + c * Cm[i * kLd + k];
     }
     __syncthreads();
-    mm(B, Cm, Q, p);
-    __syncthreads();
-    for (int e = threadIdx.x; e < p * p; e += blockDim.x) Q[(e / p) * kLd + e % p] = B[(e / p) * kLd + e % p];
-    __syncthreads();
+    mm_inplace<P, R>(Q, Cm, Q, p);
     if (t + 1 < C.T) {
-      mm(B, Cm, A, p);
-      __syncthreads();
-      mm(A, Cm, B, p);
-      __syncthreads();
+      mm_inplace<P, R>(A, Cm, A, p);
+      mm_inplace<P, R>(A, Cm, A, p);
     }
   }
   // ---- X_T = s Q X -> fp16 into X1 (row i, column j at i * q_pad + j)
@@ -143,7 +164,7 @@ __global__ void __launch_bounds__(kThreads) k_ns_small(const MatDesc* __restrict
     for (int e = threadIdx.x; e < p * w; e += blockDim.x) {
       const int i = e / w, jj = e % w;
       double o = 0.0;
-      for (int l = 0; l < p; ++l) o += Q[i * kLd + l] * (double)xs[l][jj];
+      for (int l = 0; l < p; ++l) o += (double)Q[i * kLd + l] * (double)xs[l][jj];
       out[(int64_t)i * md.q_pad + j0 + jj] = __float2half_rn((float)(sc * o));
     }
     __syncthreads();
@@ -151,11 +172,21 @@ __global__ void __launch_bounds__(kThreads) k_ns_small(const MatDesc* __restrict
 }
 
 void launch_ns_small(cudaStream_t s, const MatDesc* mats, const int32_t* list, int n_list, const int32_t* bad,
-                     const NsSmallCoeffs& C) {
-  static const bool attr = cudaFuncSetAttribute(k_ns_small, cudaFuncAttributeMaxDynamicSharedMemorySize,
-                                                (int)kSmem) == cudaSuccess;
-  (void)attr;
-  if (n_list > 0) k_ns_small<<<n_list, kThreads, kSmem, s>>>(mats, list, n_list, bad, C);
+                     const NsSmallCoeffs& C, bool wide) {
+  if (n_list <= 0) return;
+  if (!wide) {
+    using S = Small<64, double>;
+    static const bool attr = cudaFuncSetAttribute(k_ns_small<64, double>, cudaFuncAttributeMaxDynamicSharedMemorySize,
+                                                  (int)S::kSmem) == cudaSuccess;
+    (void)attr;
+    k_ns_small<64, double><<<n_list, kThreads, S::kSmem, s>>>(mats, list, n_list, bad, C);
+  } else {
+    using S = Small<128, float>;
+    static const bool attr = cudaFuncSetAttribute(k_ns_small<128, float>, cudaFuncAttributeMaxDynamicSharedMemorySize,
+                                                  (int)S::kSmem) == cudaSuccess;
+    (void)attr;
+    k_ns_small<128, float><<<n_list, kThreads, S::kSmem, s>>>(mats, list, n_list, bad, C);
+  }
 }
 
 }  // namespace dion2

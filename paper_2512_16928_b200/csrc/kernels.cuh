@@ -189,14 +189,15 @@ constexpr int ns_tc_smem_bytes() {
 
 // Short X (p <= kTinyP rows) under ns_form AUTO (k_ns_small.cu): NS in fp64 Gram space straight
 // from the pre-decay momentum, X_T stored as fp16 into X1; one CTA per matrix of `list`.
-constexpr int kTinyP = 64;
+constexpr int kTinyP = 128;
 struct NsSmallCoeffs {
   float c[16][3];
   int T;
   float eps;
 };
+// wide = false: p <= 64 (fp64 recursion); true: 64 < p <= 128 (fp32 recursion)
 void launch_ns_small(cudaStream_t s, const MatDesc* mats, const int32_t* list, int n_list, const int32_t* bad,
-                     const NsSmallCoeffs& C);
+                     const NsSmallCoeffs& C, bool wide);
 
 // fp32 SIMT validation path (k_ns_simt.cu): grid (n_tiles, m_tiles, count) per group.
 __global__ void k_ns_gemm_simt_f32(const NsParams P, int group);

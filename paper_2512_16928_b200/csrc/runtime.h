@@ -123,7 +123,7 @@ struct Plan {
   bool no_tiny = false;  // set before build_layout: short X stays on the tensor cores (owner plans of
                          // the distributed step, whose X arrives as fp16 pieces)
   size_t off_tiny_list = 0;
-  int n_tiny = 0;
+  int n_tiny = 0, n_tiny64 = 0;  // the list holds the p <= 64 matrices first, then 64 < p <= 128
   std::vector<uint8_t> host_tables;  // [off_desc, off_ns_begin) image (descriptors + aux)
   std::vector<Launch> ns_launches;
   void* ws = nullptr;

@@ -123,11 +123,11 @@ def gram_f16(X, coeffs=O.DEFAULT_NS_COEFFS, eps=O.DEFAULT_NS_EPS, growth=RESTART
 
 
 GRAM_MIN_P = 64  # reading R25 (csrc/runtime.h kGramMinP)
-TINY_P = 64      # reading R25 (csrc/kernels.cuh kTinyP): fp64 Gram-space NS, fp16 store of X_T
+TINY_P = 128     # reading R25 (csrc/kernels.cuh kTinyP): high-precision Gram-space NS, fp16 store of X_T
 
 
 def auto_f16(X, coeffs=O.DEFAULT_NS_COEFFS, eps=O.DEFAULT_NS_EPS):
-    """ns_form AUTO for one matrix (readings R23, R25): an X of at most 64 rows is evaluated in
+    """ns_form AUTO for one matrix (readings R23, R25): an X of at most 128 rows is evaluated in
     fp64 and stored once as fp16 (k_ns_small); else the Gram form for wide X (q >= 2p) with
     p >= 64 rows, else the direct form."""
     p, q = X.shape

@@ -111,11 +111,13 @@ def test_p1024_on_spiked_momenta():
 @pytest.mark.parametrize("shape,alpha,rank", [((7, 1618), 0.25, 1), ((824, 30), 1.0, 16), ((128, 1678), 0.25, 1),
                                               ((253, 1280), 0.0625, 4), ((1, 1), 1.0, 1), ((40, 4000), 0.5, 16),
                                               ((768, 3000), 0.0625, 1), ((1000, 600), 0.0625, 16),
-                                              ((256, 9000), 0.25, 4)])
+                                              ((256, 9000), 0.25, 4), ((1536, 4000), 0.0625, 1),
+                                              ((4000, 1600), 0.0625, 16), ((512, 2048), 0.25, 4)])
 def test_short_x_on_extreme_spikes(shape, alpha, rank):
-    """X with at most 64 rows under AUTO runs the fp64 Gram-space NS straight from the momentum
-    (k_ns_small.cu): on spikes at sigma_1 / median ~ 250, where the 16-bit path reached 1.7-3.6%,
-    the update is within the final fp16 store's rounding (a few 1e-4) of the oracle's."""
+    """X with at most 128 rows under AUTO runs the high-precision Gram-space NS straight from the
+    momentum (k_ns_small.cu; fp64 recursion up to 64 rows, fp32 up to 128): on spikes at
+    sigma_1 / median ~ 250, where the 16-bit path reached 1.5-3.6%, the update is within a few
+    1e-4 of the oracle's (the final fp16 store)."""
     res = run_parity([shape], alpha, "auto", "bf16", steps=2, structure=dict(kind="spike", rank=rank, ratio=250))
     assert res.index_mismatch == 0 and res.unselected_w_bitwise and res.unselected_m_bitwise, res
     assert max(res.dW_rel) <= 2e-3, res

@@ -473,8 +473,8 @@ def test_bf16_gradient_input():
 
 
 def test_phase_timing_and_launch_count():
-    # X of 128 rows: the tensor-core Gram-space form; a 32-row X: the fp64 short-X NS (ns_mul phase)
-    for (m, n), ns_phases in (((512, 1024), ("ns_gram", "ns_poly", "ns_apply")), ((128, 512), ("ns_mul",))):
+    # X of 256 rows: the tensor-core Gram-space form; a 32-row X: the short-X NS (ns_mul phase)
+    for (m, n), ns_phases in (((1024, 2048), ("ns_gram", "ns_poly", "ns_apply")), ((128, 512), ("ns_mul",))):
         Ws = [torch.from_numpy(gen_w0(m, n)).cuda()]
         Ms = [torch.zeros_like(Ws[0])]
         set_phase_timing(True)
