@@ -73,6 +73,10 @@ struct DistMat {
   int n_sumsq;
   int mt;                  // local M shard stored transposed (cols mode): K1 transpose-add, row gather
   size_t off_partials, off_sel, off_sumsq;
+  // short X under AUTO (k <= kTinyP, reading R25): no pieces and no owner; every rank sums the
+  // partial Gram matrices of its column block and applies the exact NS to it locally
+  int tiny = 0;
+  size_t off_tx = 0, off_to = 0;  // local scratch for K3's X store and the local X_T
 };
 
 struct DistPlan {
@@ -131,6 +135,10 @@ struct DistPlan {
   uint8_t* osend_base = nullptr;
   std::vector<uint8_t*> peer_recv, peer_osend;
   SymmState* symm = nullptr;  // NCCL windows; kept for the process lifetime (collective teardown)
+  // short X (DistMat::tiny): the p <= 64 matrices first, then 64 < p <= 128
+  std::vector<int32_t> tiny_list;
+  int n_tiny64 = 0;
+  size_t off_tiny_a = 0, t_tiny = 0;
 };
 
 void* dt(DistPlan& D, size_t off) { return static_cast<uint8_t*>(D.dtab) + off; }
@@ -170,6 +178,8 @@ int resolve(DistPlan& D, const dion2_shard* sh, int n, const dion2_config* c, in
     if (q.mt && q.axis != DION2_AXIS_COLS) return DION2_EUNSUPPORTED;
     if (q.mt && sh[j].ldm < q.srows) return DION2_EINVAL_SHAPE;
     q.piece = (int64_t)align_up((size_t)q.k * q.qo * 2, 256);
+    q.tiny = (c->ns_form == DION2_NS_FORM_AUTO && c->precision == DION2_NS_BF16 && q.k <= kTinyP) ? 1 : 0;
+    if (q.tiny) q.piece = 0;
     const double p = q.k, qq = q.o;
     q.flops = c->ns_steps * (4.0 * p * p * qq + 2.0 * p * p * p);
     // gather/scatter path: streaming rows (1), streaming cols (2), generic tiles (0)
@@ -222,7 +232,7 @@ int resolve(DistPlan& D, const dion2_shard* sh, int n, const dion2_config* c, in
       std::vector<std::pair<int64_t, int64_t>> keys;
       std::vector<int> key_of;
       for (int j = 0; j < n; ++j)
-        if (D.dm[j].owner == o && D.dm[j].chunk == ch) {
+        if (D.dm[j].owner == o && D.dm[j].chunk == ch && !D.dm[j].tiny) {
           const std::pair<int64_t, int64_t> key((int64_t)align_up(D.dm[j].k, 256), (int64_t)align_up(D.dm[j].o, 256));
           int ki = (int)(std::find(keys.begin(), keys.end(), key) - keys.begin());
           if (ki == (int)keys.size()) keys.push_back(key);
@@ -247,7 +257,7 @@ int resolve(DistPlan& D, const dion2_shard* sh, int n, const dion2_config* c, in
   D.oc.clear();
   D.oc.resize(D.nchunks);
   for (int j = 0; j < n; ++j)
-    if (D.dm[j].owner == rank) D.oc[D.dm[j].chunk].owned.push_back(j);
+    if (D.dm[j].owner == rank && !D.dm[j].tiny) D.oc[D.dm[j].chunk].owned.push_back(j);
   // workspace
   size_t off = 0;
   auto take = [&](size_t bytes) {
@@ -264,6 +274,18 @@ int resolve(DistPlan& D, const dion2_shard* sh, int n, const dion2_config* c, in
   D.off_sumsq_local = take(4 * (size_t)n);
   D.off_sumsq_all = take(4 * (size_t)n * world);
   D.off_nsscale = take(16 * (size_t)n);  // per matrix: word 2 = the fp16 prescale K2 writes (R24)
+  D.tiny_list.clear();
+  for (int pass = 0; pass < 2; ++pass)
+    for (int j = 0; j < n; ++j)
+      if (D.dm[j].tiny && ((D.dm[j].k <= 64) == (pass == 0))) D.tiny_list.push_back(j);
+  D.n_tiny64 = 0;
+  for (int j : D.tiny_list) D.n_tiny64 += D.dm[j].k <= 64 ? 1 : 0;
+  D.off_tiny_a = take(8 * (size_t)kTinyP * kTinyP * std::max<size_t>(1, D.tiny_list.size()));
+  for (auto& q : D.dm)
+    if (q.tiny) {
+      q.off_tx = take((size_t)q.k * q.qo * 2);
+      q.off_to = take((size_t)q.k * q.qo * 2);
+    }
   for (auto& q : D.dm) {
     q.off_partials = q.axis == DION2_AXIS_COLS ? take(4 * (size_t)ceil_div(q.srows, kColRowBlock) * q.scols) : 0;
     q.off_sel = take(4 * (size_t)q.k);
@@ -321,6 +343,7 @@ int build_tables(DistPlan& D, const dion2_config* c, void* ws) {
     D.t_fls[l] = take(4 * (size_t)n);
   }
   D.t_gprefix = take(4 * (size_t)n);
+  D.t_tiny = take(4 * std::max<size_t>(1, D.tiny_list.size()));
   for (auto& ch : D.oc) {
     ch.t_gidx = take(4 * std::max<size_t>(1, ch.owned.size()));
     ch.t_roff = take(8 * std::max<size_t>(1, ch.owned.size()) * P);
@@ -370,8 +393,8 @@ int build_tables(DistPlan& D, const dion2_config* c, void* ws) {
     d.sumsq_partials = (float*)at(ws, q.off_sumsq);
     d.ns_scale = (float*)at(ws, D.off_nsscale) + 4 * j;
     d.x16 = 1;
-    d.X0 = at(ws, D.off_send + D.sdispl[q.owner] + q.soff);
-    d.X1 = at(ws, D.off_orecv + D.sdispl[q.owner] + q.soff);
+    d.X0 = q.tiny ? at(ws, q.off_tx) : at(ws, D.off_send + D.sdispl[q.owner] + q.soff);
+    d.X1 = q.tiny ? at(ws, q.off_to) : at(ws, D.off_orecv + D.sdispl[q.owner] + q.soff);
     d.final_in_x1 = 1;
     d.rowblocks = (int)ceil_div(q.srows, kColRowBlock);
     d.mid = j;
@@ -420,6 +443,7 @@ int build_tables(DistPlan& D, const dion2_config* c, void* ws) {
     if (lg == 1 || ls == 1) D.fl_maxk = std::max(D.fl_maxk, q.k);
   }
   memcpy(H(D.t_gprefix), gprefix.data(), 4 * (size_t)n);
+  if (!D.tiny_list.empty()) memcpy(H(D.t_tiny), D.tiny_list.data(), 4 * D.tiny_list.size());
   D.n_row_mats = (int)rowmats.size();
   D.n_col_mats = (int)colmats.size();
   D.n_mt_mats = (int)mtmats.size();
@@ -559,6 +583,7 @@ void apply_direct(DistPlan& D) {
   MatDesc* md = reinterpret_cast<MatDesc*>(D.htab.data() + D.t_desc);
   for (int j = 0; j < D.n; ++j) {
     const DistMat& q = D.dm[j];
+    if (q.tiny) continue;  // local, no pieces
     const int64_t off = (int64_t)D.rank * D.scount[q.owner] + q.soff;
     void* x0 = D.peer_recv[q.owner] + off;
     void* x1 = D.peer_osend[q.owner] + off;
@@ -810,6 +835,7 @@ struct Transport {
   // owner chunk `chunk` of every owner: pieces to the owners (C2) / results back (C3)
   virtual int to_owners(int chunk, cudaStream_t s) = 0;
   virtual int from_owners(int chunk, cudaStream_t s) = 0;
+  virtual int allreduce_tiny(cudaStream_t s) = 0;  // sum of the short-X partial Gram matrices
   uint64_t bytes = 0;
 };
 
@@ -860,6 +886,12 @@ struct NcclTransport : Transport {
       if (peer != D.rank) bytes += forward ? D.scount[peer] : D.R;
     return symm_barrier(D.symm, s);
   }
+  int allreduce_tiny(cudaStream_t s) override {
+    const size_t cnt = (size_t)kTinyP * kTinyP * D.tiny_list.size();
+    bytes += (uint64_t)(2.0 * (D.world - 1) / D.world * 8.0 * (double)cnt);
+    double* a = (double*)at(ws, D.off_tiny_a);
+    return nccl_api().allreduce(a, a, cnt, /*ncclFloat64*/ 8, /*ncclSum*/ 0, comm, s) ? DION2_ENCCL : DION2_OK;
+  }
   int to_owners(int ch, cudaStream_t s) override { return D.direct ? direct_sync(true, s) : exchange(true, ch, s); }
   int from_owners(int ch, cudaStream_t s) override { return D.direct ? direct_sync(false, s) : exchange(false, ch, s); }
 };
@@ -909,6 +941,16 @@ struct LoopbackTransport : Transport {
       }
     return rc ? DION2_ECUDA : DION2_OK;
   }
+  int allreduce_tiny(cudaStream_t s) override {
+    const int P = (int)D.size();
+    const int64_t cnt = (int64_t)kTinyP * kTinyP * (int64_t)D[0]->tiny_list.size();
+    double* a0 = (double*)at(ws[0], D[0]->off_tiny_a);
+    for (int r = 1; r < P; ++r) launch_add_f64(s, a0, (const double*)at(ws[r], D[r]->off_tiny_a), cnt);
+    int rc = 0;
+    for (int r = 1; r < P; ++r) rc |= cp(at(ws[r], D[r]->off_tiny_a), a0, (size_t)cnt * 8, s);
+    bytes += (uint64_t)(2.0 * (P - 1) / P * 8.0 * (double)cnt);
+    return rc ? DION2_ECUDA : DION2_OK;
+  }
   int from_owners(int ch, cudaStream_t s) override {
     const int P = (int)D.size();
     int rc = 0;
@@ -950,6 +992,39 @@ int run_dist(std::vector<DistPlan*>& plans, std::vector<void*>& wss, const std::
   for (size_t i = 0; i < R; ++i) phase_local_k1(*plans[i], wss[i], L, s);
   if ((rc = T.allgather_scores(s))) return rc;                      // C1
   for (size_t i = 0; i < R; ++i) phase_select(*plans[i], wss[i], c, L, s);
+  if (!plans[0]->tiny_list.empty()) {
+    // short X (R25): partial Gram matrices of the local blocks, their sum, the exact NS applied
+    // locally -- before K3 decays M[K]
+    NsSmallCoeffs cs{};
+    for (int t = 0; t < c->ns_steps && t < 16; ++t)
+      for (int e = 0; e < 3; ++e) cs.c[t][e] = c->ns_coeffs[t][e];
+    cs.T = c->ns_steps;
+    cs.eps = c->ns_eps;
+    for (size_t i = 0; i < R; ++i) {
+      DistPlan& D = *plans[i];
+      const MatDesc* dm = (const MatDesc*)dt(D, D.t_desc);
+      const int32_t* tl = (const int32_t*)dt(D, D.t_tiny);
+      double* a = (double*)at(wss[i], D.off_tiny_a);
+      const int n64 = D.n_tiny64, n128 = (int)D.tiny_list.size() - D.n_tiny64;
+      L.begin(PH_NSMUL);
+      launch_ns_small_partial(s, dm, tl, n64, a, false);
+      launch_ns_small_partial(s, dm, tl + n64, n128, a + (int64_t)n64 * kTinyP * kTinyP, true);
+      L.end();
+    }
+    if ((rc = T.allreduce_tiny(s))) return rc;
+    for (size_t i = 0; i < R; ++i) {
+      DistPlan& D = *plans[i];
+      const MatDesc* dm = (const MatDesc*)dt(D, D.t_desc);
+      const int32_t* tl = (const int32_t*)dt(D, D.t_tiny);
+      const int32_t* bad = (const int32_t*)at(wss[i], D.off_bad);
+      const double* a = (const double*)at(wss[i], D.off_tiny_a);
+      const int n64 = D.n_tiny64, n128 = (int)D.tiny_list.size() - D.n_tiny64;
+      L.begin(PH_NSMUL);
+      launch_ns_small_finish(s, dm, tl, n64, bad, a, cs, false);
+      launch_ns_small_finish(s, dm, tl + n64, n128, bad, a + (int64_t)n64 * kTinyP * kTinyP, cs, true);
+      L.end();
+    }
+  }
   for (size_t i = 0; i < R; ++i) phase_gather(*plans[i], wss[i], c, L, s);
   if ((rc = T.allgather_sumsq(s))) return rc;
   if (C == 1) {

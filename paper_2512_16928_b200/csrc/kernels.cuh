@@ -198,6 +198,13 @@ struct NsSmallCoeffs {
 // wide = false: p <= 64 (fp64 recursion); true: 64 < p <= 128 (fp32 recursion)
 void launch_ns_small(cudaStream_t s, const MatDesc* mats, const int32_t* list, int n_list, const int32_t* bad,
                      const NsSmallCoeffs& C, bool wide);
+// distributed step: per-rank partial Gram matrices of the local column blocks (fp64, kTinyP^2
+// apart from Abase), then -- after their all-reduce -- the recursion and the local apply
+void launch_ns_small_partial(cudaStream_t s, const MatDesc* mats, const int32_t* list, int n_list, double* Abase,
+                             bool wide);
+void launch_ns_small_finish(cudaStream_t s, const MatDesc* mats, const int32_t* list, int n_list, const int32_t* bad,
+                            const double* Abase, const NsSmallCoeffs& C, bool wide);
+void launch_add_f64(cudaStream_t s, double* dst, const double* src, int64_t n);
 
 // fp32 SIMT validation path (k_ns_simt.cu): grid (n_tiles, m_tiles, count) per group.
 __global__ void k_ns_gemm_simt_f32(const NsParams P, int group);

@@ -242,3 +242,27 @@ def test_nccl_graph_replay_is_bitwise_eager(direct):
             assert torch.equal(out[0][1][i], out[1][1][i]), i
     finally:
         dist.destroy_process_group()
+
+
+@pytest.mark.parametrize("world,direct", [(2, False), (3, False), (4, True), (8, False)])
+def test_short_x_exact_in_the_distributed_step(world, direct):
+    """Short X (k <= 128, reading R25) in the distributed step: no pieces; every rank sums the
+    partial Gram matrices of its column block (all-reduce) and applies the exact NS locally --
+    within the final fp16 store of the oracle on extreme spikes, next to ordinary matrices."""
+    u = 8 * world
+    shapes = [(3 * u, 75 * u), (117 * u, 3 * u), (72 * u, 96 * u), (24 * u, 120 * u)]
+    res = run_parity_dist(shapes, 0.5, world, steps=2, direct=direct,
+                          structure=dict(kind="spike", rank=4, ratio=250))
+    assert res.index_mismatch == 0 and max(res.M_rel) <= 1e-5, res
+    short = [i for i, (m, n) in enumerate(shapes) if round(0.5 * min(m, n)) <= 128]
+    assert short and max(res.dW_rel[i] for i in short) <= 2e-3, res
+    assert max(res.dW_rel) <= BF16_TOL, res
+
+
+@pytest.mark.parametrize("shapes,world", [([(576, 912), (24, 600), (696, 456), (672, 792)], 3),
+                                          ([(120, 792), (936, 816), (936, 720), (936, 24)], 3)])
+def test_fuzz_cases_short_x_distributed(shapes, world):
+    """The two fuzz cases (profiles/r02_fuzz_100000.jsonl) that reached 2.2% before the
+    distributed short-X path."""
+    res = run_parity_dist(shapes, 0.5, world, steps=2, structure=dict(kind="spike", rank=4, ratio=250))
+    assert res.index_mismatch == 0 and max(res.dW_rel) <= BF16_TOL and max(res.M_rel) <= 1e-5, res
