@@ -30,11 +30,14 @@ def _lib():
     _build.build()
 
 
+TINY_K = 128  # short X (k <= 128, reading R25): summed partial Gram matrices, no pieces
+
+
 def _piece_bytes(m, n, alpha, world):
     ax = O.resolve_axis(m, n, O.AXIS_AUTO)
     d, o = (m, n) if ax == O.AXIS_ROWS else (n, m)
     k = O.select_count(np.float32(alpha), d)
-    raw = k * (o // world) * 2
+    raw = 0 if k <= TINY_K else k * (o // world) * 2
     return -(-raw // 256) * 256, k, o
 
 
@@ -146,7 +149,7 @@ def _worker(rank, world, port, q):
         fullX, send = {}, []
         for o in range(world):
             for j, (m, n) in enumerate(SHAPES):
-                if inf["owner"][j] != o:
+                if inf["owner"][j] != o or _piece_bytes(m, n, alpha, world)[0] == 0:
                     continue
                 M = gen_grad(m, n, 7, j, 0).astype(np.float64)
                 ax = O.resolve_axis(m, n, O.AXIS_AUTO)
@@ -167,7 +170,7 @@ def _worker(rank, world, port, q):
         R = inf["recv_bytes"][0]
         off = 0
         for j, (m, n) in enumerate(SHAPES):
-            if inf["owner"][j] != rank:
+            if inf["owner"][j] != rank or j not in fullX:
                 continue
             X = fullX[j]
             k, o = X.shape
