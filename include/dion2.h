@@ -231,6 +231,10 @@ const char* dion2_phase_name(int32_t i);
  *   5. pieces -> owner of the matrix (grouped ncclSend/ncclRecv)      (bytes ~ alpha)
  *   6. owner: assemble X, Newton-Schulz, split O into pieces           (tcgen05 NS)
  *   7. O pieces -> back to every rank; local W[K] update              (K7, local)
+ * Short X under ns_form AUTO (k <= 128, reading R25) skip steps 4-7's exchange: after step 3
+ * every rank writes the fp64 Gram matrix of its column block X_r, one all-reduce sums them
+ * (A = sum_r X_r X_r^T), and every rank runs the recursion and applies X_T,r = s Q X_r to its
+ * own block before the decay -- exact, no pieces, no owner.
  * Owners are assigned by LPT on NS FLOPs, identically on every rank.  All sizes are known on the
  * host, so nothing synchronises the host inside a step.  Requirements: the sharded dimension
  * divisible by P; rows mode n/P % 8 == 0; cols mode m/P % 32 == 0 and k <= 1024; k <= the other
